@@ -1,0 +1,369 @@
+"""Benchmark: candidate schedules scored per second (BASELINE.json metric).
+
+Step = one pass of the hot path over one batch: fused score (features -> 100-tree
+energy model -> prediction + candidate id) of the rank's population shard, then
+"keep the best": top-k by (score, index); for N>1 the per-shard top-k records are
+all-gathered over NCCL and merged identically on every rank.
+
+    python bench.py [--gpus N --steps K --warmup W]            # our B200 path
+    python bench.py --impl reference [--gpus N ...]            # reference CPU path
+    torchrun --nproc-per-node N bench.py --gpus N ...          # N>1
+
+Workload (config.workload): the ResNet-50 3x3 conv layer of BASELINE configs[1]
+(conv:1,56,56,64,64,3,1,1), population 2^20 per GPU (north_star / configs[3] top
+size), bred exactly like SURVEY §8(d): reproduce(sample_random(op,1024,42), 2^20,
+GeneticRates{}, seed 7); model = the reference-trained 100-tree forest on
+sample_random(op,2048,1234) (tests/golden fixture).  L2: 16 distinct population
+buffers (384 MB incl. outputs) are cycled so no step reads another's data from the
+126 MB L2.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+OP_TEXT = "conv:1,56,56,64,64,3,1,1"
+MODEL_KEY = "c2_r50_conv3x3"
+METRIC = "candidate schedules scored/sec"
+UNIT = "candidates/s"
+# algorithmic bytes per candidate in score mode: 8 B genome in + 8 B prediction + 8 B id out
+ALGO_BYTES = 24
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--pop", type=int, default=1 << 20, help="candidates per GPU per step")
+    p.add_argument("--k", type=int, default=1024, help="top-k kept per step")
+    p.add_argument("--bufs", type=int, default=16)
+    p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample duration")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def load_forest():
+    from etune_testlib import FlatForest
+    g = np.load(os.path.join(ROOT, "tests", "golden", "golden_reference.npz"))
+    k = f"{MODEL_KEY}/model/"
+    return FlatForest(g[k + "feature"], g[k + "threshold"], g[k + "left"], g[k + "right"], g[k + "value"],
+                      g[k + "offsets"], float(g[k + "base_score"][0]), float(g[k + "learning_rate"][0]))
+
+
+def make_population(n: int, seed: int = 7):
+    """SURVEY §8(d) population: reproduce(sample_random(op,1024,42), n, {}, seed)."""
+    from etune_testlib import Oracle, parse_op
+    O = Oracle()
+    op = parse_op(OP_TEXT)
+    par, _ = O.sample_random(op, 1024, 42)
+    s, _, _, _ = O.reproduce(op, par, n, seed)
+    return op, s
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def forest_json(f) -> str:
+    """etune-model-v1 JSON (energy_model.cpp:259-284) so the reference loads the same model."""
+    trees = []
+    for t in range(f.num_trees):
+        a, b = int(f.offsets[t]), int(f.offsets[t + 1])
+        trees.append([{"f": int(f.feature[i]), "t": float(f.threshold[i]), "l": int(f.left[i]),
+                       "r": int(f.right[i]), "v": float(f.value[i])} for i in range(a, b)])
+    return json.dumps({"model_version": "etune-model-v1", "feature_schema": "etune-features-v1",
+                       "params": {"num_trees": f.num_trees, "max_depth": 6, "learning_rate": f.learning_rate,
+                                  "min_leaf_weight": 1e-3, "reg_lambda": 1.0},
+                       "base_score": f.base_score, "reference_energy_mj": 1.0, "trees": trees})
+
+
+def cpu_score_runner():
+    """Returns (kind, fn(op, sched) -> preds, threads).  Prefers the unmodified reference
+    (oracle/_ref) over the restatement (oracle/lib)."""
+    from etune_testlib import Oracle, RefLib, have_ref
+    forest = load_forest()
+    threads = cpu_threads()
+    if have_ref():
+        R = RefLib()
+        model = R.model_from_json(forest_json(forest))
+        return "reference", (lambda op, s: model.score_threads(op, s, threads)), threads
+    O = Oracle()
+    return "port", (lambda op, s: O.score_threads(op, s, forest, threads)), threads
+
+
+def time_cpu(op, sched, target_s: float):
+    kind, fn, threads = cpu_score_runner()
+    m = min(len(sched), 20000)
+    t0 = time.perf_counter()
+    fn(op, sched[:m])
+    dt = time.perf_counter() - t0
+    rate = m / max(dt, 1e-9)
+    m2 = int(min(len(sched), max(m, rate * target_s)))
+    t0 = time.perf_counter()
+    fn(op, sched[:m2])
+    dt = time.perf_counter() - t0
+    return {"value": m2 / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"first {m2} candidates of the bench population ({OP_TEXT}); extract_features + "
+                      f"EnergyModel::predict per candidate over {threads} std::threads; {dt:.1f} s"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = max(mx, float(p[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    op, sched = make_population(args.pop)
+    kind, fn, threads = cpu_score_runner()
+    # bounded sample per step so the whole run ends in a few minutes
+    m = min(len(sched), 20000)
+    t0 = time.perf_counter()
+    fn(op, sched[:m])
+    rate = m / max(time.perf_counter() - t0, 1e-9)
+    per_step = int(min(len(sched), max(10000, rate * 8.0 / max(args.steps + args.warmup, 1))))
+    for w in range(args.warmup):
+        fn(op, sched[:per_step])
+    times = []
+    for s in range(args.steps):
+        lo = (s * per_step) % max(1, len(sched) - per_step)
+        t0 = time.perf_counter()
+        preds = fn(op, sched[lo:lo + per_step])
+        order = np.lexsort((np.arange(len(preds)), preds))[: args.k]  # keep the best (score, index)
+        times.append(time.perf_counter() - t0)
+        del order
+    value = per_step * len(times) / sum(times)
+    sample = (f"{per_step} candidates/step of the bench population ({OP_TEXT}): the reference's "
+              f"extract_features + EnergyModel::predict over {threads} threads + top-{args.k}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"score+top-{args.k} of {OP_TEXT} candidates (CPU reference)", "op": OP_TEXT,
+                   "population_per_step": per_step, "k": args.k},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2411_18873_b200 import capi
+
+    forest_flat = load_forest()
+    op, sched = make_population(args.pop, seed=7 + rank)
+    n = len(sched)
+    ctx = capi.Context(local)
+    plan = capi.Plan(ctx, op)
+    forest = capi.Forest.from_flat(ctx, forest_flat)
+    d_sched = torch.from_numpy(sched).cuda()
+    g0 = plan.encode(d_sched)
+    ctx.synchronize()
+    del d_sched
+    nb = args.bufs
+    genomes = [g0.clone() for _ in range(nb)]
+    preds = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nb)]
+    ids = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(nb)]
+    stream = torch.cuda.current_stream()
+    K = min(args.k, n)
+
+    def step(i):
+        b = i % nb
+        pred, _ = forest.score(plan, genomes[b], out=preds[b], ids_out=ids[b])
+        top = capi.topk(ctx, pred, K)
+        if world > 1:
+            rec = torch.stack([pred[top], (top + rank * n).to(torch.float64)], 1)  # (score, global idx)
+            allrec = torch.empty((world * K, 2), dtype=torch.float64, device="cuda")
+            dist.all_gather_into_tensor(allrec, rec)
+            # deterministic merge identical on every rank: (score, global index) order
+            sc = allrec[:, 0].contiguous()
+            gidx = allrec[:, 1].to(torch.int64)
+            # gathered in rank order, each shard sorted by (score, idx): stable selection
+            # over the concatenation == global (score, index) order
+            sel = capi.topk(ctx, sc, K)
+            return gidx[sel]
+        return top
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = capi.lib().etune_cu_launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for i in range(args.steps):
+            b = (args.warmup + i) % nb
+            kev[i][0].record(stream)
+            forest.score(plan, genomes[b], out=preds[b], ids_out=ids[b])
+            kev[i][1].record(stream)
+            top = capi.topk(ctx, preds[b], K)
+            if world > 1:
+                rec = torch.stack([preds[b][top], (top + rank * n).to(torch.float64)], 1)
+                allrec = torch.empty((world * K, 2), dtype=torch.float64, device="cuda")
+                dist.all_gather_into_tensor(allrec, rec)
+                sel = capi.topk(ctx, allrec[:, 0].contiguous(), K)
+                top = allrec[:, 1].to(torch.int64)[sel]
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = capi.lib().etune_cu_launch_count() - launches0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    kernel_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kernel_ms = t.tolist()
+        dist.barrier()
+    value = world * n / (ms / 1e3)
+
+    # ---- e2e through the reference-facing C-ABI call with host buffers
+    e2e = None
+    if not args.no_e2e:
+        h_sched = torch.from_numpy(sched).pin_memory()
+        h_pred = torch.empty(n, dtype=torch.float64).pin_memory()
+        h_ids = torch.empty(n, dtype=torch.int64).pin_memory()
+        hs, hp, hi = h_sched.numpy(), h_pred.numpy(), h_ids.numpy()
+        for _ in range(2):
+            forest.score_host(plan, hs, hp, hi)
+        if world > 1:
+            dist.barrier()
+        reps = max(3, args.steps // 2)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            forest.score_host(plan, hs, hp, hi)
+        dt = (time.perf_counter() - t0) / reps
+        if world > 1:
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = t.item()
+        e2e = {"value": world * n / dt, "unit": UNIT, "h2d_bytes_per_step": int(n * 96),
+               "d2h_bytes_per_step": int(n * 16), "ms_per_step": dt * 1e3,
+               "api": "etune_cu_score_host (host Schedule[] -> H2D -> encode+validate -> score -> D2H)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = n * ALGO_BYTES / (kernel_ms / 1e3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"score (features -> 100-tree GBDT -> prediction + id) + top-{K} of "
+                               f"{n} {OP_TEXT} candidates per GPU", "op": OP_TEXT, "population_per_gpu": n,
+                   "k": K, "model": "reference-trained 100-tree depth-6 GBDT (tests/golden c2 fixture)",
+                   "parallelism": f"dp{world} (population sharded, NCCL all-gather of top-k records)",
+                   "l2": f"{nb} distinct population buffers cycled ({nb * n * 24 / 2**20:.0f} MB > 126 MB L2)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                     "traffic": None, "kernel": "score_kernel", "kernel_ms": kernel_ms,
+                     "algorithmic_bytes_per_candidate": ALGO_BYTES,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = time_cpu(op, sched, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,215 @@
+/*
+ * etune_cuda.h — C ABI of libetune_cuda.so, the B200 (sm_100a) implementation of the
+ * candidate-schedule scoring hot path of arXiv 2411.18873's energy-aware search.
+ *
+ * Drop-in boundary.  Each entry point replaces one reference interface
+ * (/root/reference/proj/include/etune/, one header per module); the citation is on each declaration.
+ * INTEGRATION.md shows the binding a reference maintainer adds (the reference's own
+ * functions forwarding to these), and the repo's C++ host mirror
+ * (paper_2411_18873_b200/host/etune_b200.hpp) keeps the reference's names.
+ *
+ * Conventions
+ *  - Plain C: POD structs, raw pointers, int64 sizes.  No torch / C++ types.
+ *  - Pointers named d_* are DEVICE pointers (caller-owned, on the ctx's device);
+ *    h_* are HOST pointers (pinned memory recommended for the *_host calls).
+ *  - Device work is enqueued on the ctx stream and is asynchronous unless the name
+ *    ends in _host or _sync.  Data-dependent errors raised on the device (an illegal
+ *    schedule in a batch) are reported by etune_cu_synchronize(), which returns the
+ *    status and the lowest offending index — the element the reference, walking the
+ *    batch in order, would have thrown on.
+ *  - Status codes map 1:1 onto the reference exception classes (errors.hpp:15-100).
+ *  - Bit-exactness: ids, counters, feature vectors, genomes, selected indices and
+ *    offspring are bit-identical to the reference; predictions are bit-identical too
+ *    (FP64, the reference's summation order, no FMA contraction).
+ */
+#ifndef ETUNE_CUDA_H
+#define ETUNE_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ETUNE_CUDA_ABI_VERSION 1
+
+typedef enum etune_status {
+    ETUNE_OK = 0,
+    ETUNE_ERR_PARSE = 1,                 /* etune::ParseError          errors.hpp:15 */
+    ETUNE_ERR_VALIDATION = 2,            /* etune::ValidationError     errors.hpp:21 */
+    ETUNE_ERR_SPACE_EXHAUSTED = 3,       /* etune::SpaceExhausted      errors.hpp:27 */
+    ETUNE_ERR_ILLEGAL_SCHEDULE = 4,      /* etune::IllegalSchedule     errors.hpp:33 */
+    ETUNE_ERR_TOO_LARGE = 5,             /* etune::TooLarge            errors.hpp:39 */
+    ETUNE_ERR_NON_POSITIVE_ENERGY = 6,   /* etune::NonPositiveEnergy   errors.hpp:45 */
+    ETUNE_ERR_INSUFFICIENT_DATA = 7,     /* etune::InsufficientData    errors.hpp:51 */
+    ETUNE_ERR_SCHEMA_MISMATCH = 8,       /* etune::SchemaMismatch      errors.hpp:57 */
+    ETUNE_ERR_VERSION_MISMATCH = 9,      /* etune::VersionMismatch     errors.hpp:63 */
+    ETUNE_ERR_LENGTH_MISMATCH = 10,      /* etune::LengthMismatch      errors.hpp:68 */
+    ETUNE_ERR_EMPTY_INPUT = 11,          /* etune::EmptyInput          errors.hpp:73 */
+    ETUNE_ERR_IO = 12,                   /* etune::IoError             errors.hpp:79 */
+    ETUNE_ERR_CONSISTENCY = 13,          /* etune::ConsistencyError    errors.hpp:85 */
+    ETUNE_ERR_BACKEND_UNAVAILABLE = 14,  /* etune::BackendUnavailable  errors.hpp:91 */
+    ETUNE_ERR_TRACE_MISS = 15,           /* etune::TraceMiss           errors.hpp:97 */
+    ETUNE_ERR_INVALID_ARGUMENT = 64,     /* null pointer / bad size (no reference analogue) */
+    ETUNE_ERR_CUDA = 65,                 /* CUDA runtime failure */
+    ETUNE_ERR_NO_DEVICE = 66,            /* no sm_100 device: the library never falls back to CPU */
+    ETUNE_ERR_UNSUPPORTED = 67           /* shape outside this build's table limits */
+} etune_status;
+
+/* OperatorSpec (opspec.hpp:30-47), words in candidate_id order (space.cpp:24-35).
+ * kind: 0 MM, 1 MV, 2 CONV.  Unused fields keep the reference defaults
+ * (m=n=k=1 for conv, stride=1, padding=0 and conv fields 0 for mm/mv). */
+typedef struct etune_op_spec {
+    int64_t kind, batch, m, n, k, height, width, in_channels, out_channels, kernel_size,
+        stride, padding;
+} etune_op_spec;
+
+/* Schedule (schedule.hpp:40-44): spatial[d] = {blocks, threads, per_thread} for
+ * d = batch, m, n; then k_tile, unroll, vectorize.  96 bytes, int64 like the reference. */
+typedef struct etune_schedule {
+    int64_t spatial[3][3];
+    int64_t k_tile, unroll, vectorize;
+} etune_schedule;
+
+/* SpaceLimits (space.hpp:15-19). */
+typedef struct etune_space_limits {
+    int64_t max_block_threads, max_unroll, max_vectorize;
+} etune_space_limits;
+
+/* CounterSet (counters.hpp:13-24), same field order, 80 bytes. */
+typedef struct etune_counters {
+    int64_t grid, block, flops, int_ops, glb_ld, glb_st, shared_ld, shared_st;
+    double sm_efficiency;
+    int64_t active_sms;
+} etune_counters;
+
+/* DeviceConfig (device.hpp:17-45) numeric fields. */
+typedef struct etune_device_config {
+    int32_t num_sms;
+    int32_t reserved;
+    double constant_power_w, static_power_per_sm_w, dynamic_energy_per_flop_nj,
+        dynamic_energy_per_glb_access_nj, dynamic_energy_per_shared_access_nj,
+        base_throughput_flops_per_s_per_sm, mem_bandwidth_elems_per_s, latency_floor_ms,
+        sampler_hz, warmup_s, noise_sigma_rel;
+    uint64_t rng_seed;
+} etune_device_config;
+
+/* GeneticRates (genetic.hpp:14-18). */
+typedef struct etune_genetic_rates {
+    double mutation, crossover, copy;
+} etune_genetic_rates;
+
+/* BoostParams (energy_model.hpp:33-41). */
+typedef struct etune_boost_params {
+    int32_t num_trees, max_depth;
+    double learning_rate, min_leaf_weight, reg_lambda;
+} etune_boost_params;
+
+/* Defaults identical to the reference's: DeviceConfig::a100_like() (device.cpp:40),
+ * SpaceLimits{} , GeneticRates{}, BoostParams{}. */
+void etune_default_device_config(etune_device_config* out);
+void etune_default_space_limits(etune_space_limits* out);
+void etune_default_genetic_rates(etune_genetic_rates* out);
+void etune_default_boost_params(etune_boost_params* out);
+
+const char* etune_cu_last_error(void); /* thread-local message of the last failure */
+int etune_cu_abi_version(void);
+/* Number of kernels this library has launched in the process (diagnostics / bench). */
+uint64_t etune_cu_launch_count(void);
+
+/* ------------------------------------------------------------------ context */
+typedef struct etune_cu_ctx etune_cu_ctx;
+
+/* stream: a cudaStream_t (NULL -> the library creates its own non-blocking stream). */
+etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out);
+etune_status etune_cu_ctx_destroy(etune_cu_ctx* ctx);
+etune_status etune_cu_ctx_set_stream(etune_cu_ctx* ctx, void* stream);
+void* etune_cu_ctx_stream(etune_cu_ctx* ctx);
+/* Waits for the ctx stream; reports a device-detected data error (first bad index). */
+etune_status etune_cu_synchronize(etune_cu_ctx* ctx, int64_t* first_bad_index);
+
+/* ------------------------------------------------------------------- plans */
+/* A plan holds an operator's knob tables on the device: the ordered tilings of each
+ * spatial extent (space.cpp:69-78), divisors of K (57-67), and the per-operator
+ * feature tables (features.cpp:15-46 factored by the knobs each feature depends on;
+ * log1p evaluated once per distinct counter on the host with the platform libm, the
+ * function the reference calls).  Replaces the per-candidate setup inside
+ * extract_features (features.hpp:35) / ScheduleEnumerator (space.hpp:45).
+ * Throws-equivalents: VALIDATION (op invalid, opspec.cpp:65-93), UNSUPPORTED. */
+typedef struct etune_cu_plan etune_cu_plan;
+etune_status etune_cu_plan_create(etune_cu_ctx* ctx, const etune_op_spec* op,
+                                  const etune_device_config* dev /*NULL=a100_like*/,
+                                  const etune_space_limits* limits /*NULL=defaults*/,
+                                  etune_cu_plan** out);
+etune_status etune_cu_plan_destroy(etune_cu_plan* plan);
+/* LoopNest of the op (opspec.cpp:103-117) and legal-space size (space.cpp:152-160). */
+etune_status etune_cu_plan_nest(const etune_cu_plan* plan, int64_t out4[4]);
+etune_status etune_cu_plan_space_size(const etune_cu_plan* plan, int64_t* out);
+
+/* ---------------------------------------------------------- population codec */
+/* Device-resident populations are 8-byte genomes (uint64 per candidate): indices of
+ * the candidate's knobs in the plan's tables.  encode validates exactly like
+ * validate_schedule (schedule.cpp:26-61); an illegal row is reported by
+ * etune_cu_synchronize as ETUNE_ERR_ILLEGAL_SCHEDULE with its index. */
+etune_status etune_cu_encode(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                             const etune_schedule* d_sched, int64_t n, uint64_t* d_genome);
+etune_status etune_cu_decode(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                             const uint64_t* d_genome, int64_t n, etune_schedule* d_sched);
+
+/* candidate_id (space.hpp:32, space.cpp:22-45) */
+etune_status etune_cu_candidate_ids(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                    const uint64_t* d_genome, int64_t n, uint64_t* d_ids);
+/* derive_counters (counters.hpp:35, counters.cpp:9-49) */
+etune_status etune_cu_counters(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                               const uint64_t* d_genome, int64_t n, etune_counters* d_out);
+/* extract_features (features.hpp:35, features.cpp:48-51): d_feat is n x 16 doubles
+ * (FeatureVector layout); d_ids optional (NULL). */
+etune_status etune_cu_features(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                               const uint64_t* d_genome, int64_t n, double* d_feat,
+                               uint64_t* d_ids);
+
+/* ------------------------------------------------------------- cost model */
+/* EnergyModel trees in the reference's flat TreeNode form (energy_model.hpp:45-57):
+ * node arrays concatenated in tree order, tree_offsets[num_trees+1]. */
+typedef struct etune_cu_forest etune_cu_forest;
+etune_status etune_cu_forest_create(etune_cu_ctx* ctx, const int32_t* feature,
+                                    const double* threshold, const int32_t* left,
+                                    const int32_t* right, const double* value,
+                                    const int64_t* tree_offsets, int64_t num_trees,
+                                    double base_score, double learning_rate,
+                                    etune_cu_forest** out);
+etune_status etune_cu_forest_destroy(etune_cu_forest* forest);
+
+/* EnergyModel::predict_many (energy_model.hpp:73, energy_model.cpp:245-257) on
+ * feature vectors already in device memory (n x 16 doubles). */
+etune_status etune_cu_predict(etune_cu_ctx* ctx, etune_cu_forest* forest,
+                              const double* d_feat, int64_t n, double* d_pred);
+
+/* Fused extract_features + predict (the north-star scoring pass): genome in,
+ * prediction (and optionally candidate id) out.  The forest is compiled per plan
+ * (exact partial evaluation + per-feature rank bins) on first use and cached. */
+etune_status etune_cu_score(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                            etune_cu_forest* forest, const uint64_t* d_genome, int64_t n,
+                            double* d_pred, uint64_t* d_ids /*nullable*/);
+
+/* Reference-facing end-to-end call with HOST buffers: schedules in the reference's
+ * Schedule layout -> predictions (+ ids).  Host->device copy, encode (legality check),
+ * fused score and device->host copy, synchronised.  Equivalent to
+ *   for c in population: pred[i] = model.predict(extract_features(op, c.schedule, dev))
+ * and returns ETUNE_ERR_ILLEGAL_SCHEDULE (with *first_bad) where that loop would throw. */
+etune_status etune_cu_score_host(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                 etune_cu_forest* forest, const etune_schedule* h_sched,
+                                 int64_t n, double* h_pred, uint64_t* h_ids /*nullable*/,
+                                 int64_t* first_bad /*nullable*/);
+
+/* ------------------------------------------------------------- selection */
+/* The k smallest of d_score[0..n) under the total order (score asc, index asc)
+ * ("lowest predicted energy"; SURVEY H3 tie rule), written sorted to
+ * d_idx (int64).  Scratch is taken from the ctx. */
+etune_status etune_cu_topk(etune_cu_ctx* ctx, const double* d_score, int64_t n, int64_t k,
+                           int64_t* d_idx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,298 @@
+"""ctypes binding of libetune_cuda.so (include/etune_cuda.h) for Python callers.
+
+PyTorch is used only as the device-memory / stream plumbing: tensors are passed to
+the C ABI as raw device pointers on the current torch stream.  There is no CPU
+fallback: if the shared library or an sm_100 device is missing, every call raises.
+
+uint64 payloads (genomes, ids) live in int64 tensors (same bits); use
+``as_u64(t)`` to view them as numpy uint64 on the host.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+from typing import Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "lib", "libetune_cuda.so")
+HEADER = os.path.join(ROOT, "include", "etune_cuda.h")
+
+STATUS_NAMES = {
+    0: "OK", 1: "ParseError", 2: "ValidationError", 3: "SpaceExhausted", 4: "IllegalSchedule",
+    5: "TooLarge", 6: "NonPositiveEnergy", 7: "InsufficientData", 8: "SchemaMismatch",
+    9: "VersionMismatch", 10: "LengthMismatch", 11: "EmptyInput", 12: "IoError",
+    13: "ConsistencyError", 14: "BackendUnavailable", 15: "TraceMiss", 64: "InvalidArgument",
+    65: "CudaError", 66: "NoDevice", 67: "Unsupported",
+}
+
+
+class EtuneError(RuntimeError):
+    """Mirrors etune::Error (errors.hpp:9-12); .code is the etune_status."""
+
+    def __init__(self, code: int, msg: str, index: int = -1):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+        self.index = index
+
+
+class OpSpec(C.Structure):
+    _fields_ = [(n, C.c_int64) for n in ("kind", "batch", "m", "n", "k", "height", "width", "in_channels",
+                                         "out_channels", "kernel_size", "stride", "padding")]
+
+
+class SpaceLimits(C.Structure):
+    _fields_ = [("max_block_threads", C.c_int64), ("max_unroll", C.c_int64), ("max_vectorize", C.c_int64)]
+
+
+class DeviceConfig(C.Structure):
+    _fields_ = [("num_sms", C.c_int32), ("reserved", C.c_int32)] + [
+        (n, C.c_double) for n in (
+            "constant_power_w", "static_power_per_sm_w", "dynamic_energy_per_flop_nj",
+            "dynamic_energy_per_glb_access_nj", "dynamic_energy_per_shared_access_nj",
+            "base_throughput_flops_per_s_per_sm", "mem_bandwidth_elems_per_s", "latency_floor_ms",
+            "sampler_hz", "warmup_s", "noise_sigma_rel")] + [("rng_seed", C.c_uint64)]
+
+
+_VP = C.c_void_p
+_I64 = C.c_int64
+_PTR = C.c_void_p
+
+_SIGS = {
+    "etune_default_device_config": (None, [C.POINTER(DeviceConfig)]),
+    "etune_default_space_limits": (None, [C.POINTER(SpaceLimits)]),
+    "etune_cu_last_error": (C.c_char_p, []),
+    "etune_cu_abi_version": (C.c_int, []),
+    "etune_cu_launch_count": (C.c_uint64, []),
+    "etune_cu_ctx_create": (C.c_int, [C.c_int, _VP, C.POINTER(_VP)]),
+    "etune_cu_ctx_destroy": (C.c_int, [_VP]),
+    "etune_cu_ctx_set_stream": (C.c_int, [_VP, _VP]),
+    "etune_cu_ctx_stream": (_VP, [_VP]),
+    "etune_cu_synchronize": (C.c_int, [_VP, C.POINTER(_I64)]),
+    "etune_cu_plan_create": (C.c_int, [_VP, C.POINTER(OpSpec), C.POINTER(DeviceConfig),
+                                       C.POINTER(SpaceLimits), C.POINTER(_VP)]),
+    "etune_cu_plan_destroy": (C.c_int, [_VP]),
+    "etune_cu_plan_nest": (C.c_int, [_VP, _PTR]),
+    "etune_cu_plan_space_size": (C.c_int, [_VP, C.POINTER(_I64)]),
+    "etune_cu_encode": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
+    "etune_cu_decode": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
+    "etune_cu_candidate_ids": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
+    "etune_cu_counters": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
+    "etune_cu_features": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR, _PTR]),
+    "etune_cu_forest_create": (C.c_int, [_VP, _PTR, _PTR, _PTR, _PTR, _PTR, _PTR, _I64, C.c_double,
+                                         C.c_double, C.POINTER(_VP)]),
+    "etune_cu_forest_destroy": (C.c_int, [_VP]),
+    "etune_cu_predict": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
+    "etune_cu_score": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR]),
+    "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
+    "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
+}
+
+_lib = None
+
+
+def header_functions() -> list[str]:
+    """Every function the public header declares."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:etune_status|void\*?|const char\*|int|uint64_t)\s+(etune_\w+)\s*\(", txt, re.M)))
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise EtuneError(65, f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(st: int, index: int = -1):
+    if st != 0:
+        raise EtuneError(st, lib().etune_cu_last_error().decode(), index)
+
+
+def op_spec(op) -> OpSpec:
+    w = [int(x) for x in np.asarray(op, dtype=np.int64).reshape(12)]
+    return OpSpec(*w)
+
+
+def default_device_config(num_sms: Optional[int] = None) -> DeviceConfig:
+    d = DeviceConfig()
+    lib().etune_default_device_config(C.byref(d))
+    if num_sms is not None:
+        d.num_sms = int(num_sms)
+    return d
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return None
+    if hasattr(t, "data_ptr"):
+        return t.data_ptr()
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    raise TypeError(type(t))
+
+
+def as_u64(t) -> np.ndarray:
+    a = t.detach().cpu().numpy() if hasattr(t, "detach") else np.asarray(t)
+    return a.view(np.uint64)
+
+
+class Context:
+    """etune_cu_ctx bound to a device and (by default) torch's current stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        import torch
+        self.device = device
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self._torch_stream = stream
+        h = C.c_void_p()
+        _check(lib().etune_cu_ctx_create(device, C.c_void_p(stream.cuda_stream), C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().etune_cu_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        bad = C.c_int64(-1)
+        st = lib().etune_cu_synchronize(self.h, C.byref(bad))
+        _check(st, bad.value)
+
+
+class Plan:
+    def __init__(self, ctx: Context, op, num_sms: int = 108, limits=None, dev: Optional[DeviceConfig] = None):
+        self.ctx = ctx
+        self.op = np.asarray(op, dtype=np.int64).reshape(12).copy()
+        d = dev if dev is not None else default_device_config(num_sms)
+        lim = None
+        if limits is not None:
+            lim = SpaceLimits(*[int(x) for x in limits])
+        h = C.c_void_p()
+        _check(lib().etune_cu_plan_create(ctx.h, C.byref(op_spec(self.op)), C.byref(d),
+                                          C.byref(lim) if lim is not None else None, C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().etune_cu_plan_destroy(self.h)
+        except Exception:
+            pass
+
+    def nest(self):
+        out = np.zeros(4, np.int64)
+        _check(lib().etune_cu_plan_nest(self.h, out.ctypes.data))
+        return out
+
+    def space_size(self) -> int:
+        v = C.c_int64()
+        _check(lib().etune_cu_plan_space_size(self.h, C.byref(v)))
+        return v.value
+
+    # --- codec / features (device tensors in, device tensors out)
+    def encode(self, sched):
+        import torch
+        n = sched.shape[0]
+        g = torch.empty(n, dtype=torch.int64, device=sched.device)
+        _check(lib().etune_cu_encode(self.ctx.h, self.h, _ptr(sched), n, _ptr(g)))
+        return g
+
+    def decode(self, genome):
+        import torch
+        n = genome.shape[0]
+        s = torch.empty((n, 12), dtype=torch.int64, device=genome.device)
+        _check(lib().etune_cu_decode(self.ctx.h, self.h, _ptr(genome), n, _ptr(s)))
+        return s
+
+    def ids(self, genome):
+        import torch
+        out = torch.empty_like(genome)
+        _check(lib().etune_cu_candidate_ids(self.ctx.h, self.h, _ptr(genome), genome.shape[0], _ptr(out)))
+        return out
+
+    def counters(self, genome):
+        import torch
+        out = torch.empty((genome.shape[0], 10), dtype=torch.int64, device=genome.device)
+        _check(lib().etune_cu_counters(self.ctx.h, self.h, _ptr(genome), genome.shape[0], _ptr(out)))
+        return out
+
+    def features(self, genome, with_ids: bool = False):
+        import torch
+        n = genome.shape[0]
+        f = torch.empty((n, 16), dtype=torch.float64, device=genome.device)
+        ids = torch.empty_like(genome) if with_ids else None
+        _check(lib().etune_cu_features(self.ctx.h, self.h, _ptr(genome), n, _ptr(f), _ptr(ids)))
+        return (f, ids) if with_ids else f
+
+
+class Forest:
+    def __init__(self, ctx: Context, feature, threshold, left, right, value, offsets, base_score: float,
+                 learning_rate: float):
+        self.ctx = ctx
+        self._keep = [np.ascontiguousarray(feature, np.int32), np.ascontiguousarray(threshold, np.float64),
+                      np.ascontiguousarray(left, np.int32), np.ascontiguousarray(right, np.int32),
+                      np.ascontiguousarray(value, np.float64), np.ascontiguousarray(offsets, np.int64)]
+        fe, th, le, ri, va, off = self._keep
+        h = C.c_void_p()
+        _check(lib().etune_cu_forest_create(ctx.h, fe.ctypes.data, th.ctypes.data, le.ctypes.data, ri.ctypes.data,
+                                            va.ctypes.data, off.ctypes.data, len(off) - 1, float(base_score),
+                                            float(learning_rate), C.byref(h)))
+        self.h = h
+
+    @staticmethod
+    def from_flat(ctx: Context, f) -> "Forest":
+        return Forest(ctx, f.feature, f.threshold, f.left, f.right, f.value, f.offsets, f.base_score,
+                      f.learning_rate)
+
+    def __del__(self):
+        try:
+            lib().etune_cu_forest_destroy(self.h)
+        except Exception:
+            pass
+
+    def predict(self, feats):
+        import torch
+        n = feats.shape[0]
+        out = torch.empty(n, dtype=torch.float64, device=feats.device)
+        _check(lib().etune_cu_predict(self.ctx.h, self.h, _ptr(feats), n, _ptr(out)))
+        return out
+
+    def score(self, plan: Plan, genome, with_ids: bool = False, out=None, ids_out=None):
+        import torch
+        n = genome.shape[0]
+        pred = out if out is not None else torch.empty(n, dtype=torch.float64, device=genome.device)
+        ids = ids_out if ids_out is not None else (torch.empty_like(genome) if with_ids else None)
+        _check(lib().etune_cu_score(self.ctx.h, plan.h, self.h, _ptr(genome), n, _ptr(pred), _ptr(ids)))
+        return (pred, ids) if (with_ids or ids_out is not None) else pred
+
+    def score_host(self, plan: Plan, sched: np.ndarray, pred: np.ndarray, ids: Optional[np.ndarray] = None):
+        """Reference-facing call on HOST buffers (pinned numpy views recommended)."""
+        n = sched.shape[0]
+        bad = C.c_int64(-1)
+        st = lib().etune_cu_score_host(self.ctx.h, plan.h, self.h, _ptr(sched), n, _ptr(pred), _ptr(ids),
+                                       C.byref(bad))
+        _check(st, bad.value)
+
+
+def topk(ctx: Context, score, k: int):
+    import torch
+    out = torch.empty(k, dtype=torch.int64, device=score.device)
+    _check(lib().etune_cu_topk(ctx.h, _ptr(score), score.shape[0], k, _ptr(out)))
+    return out

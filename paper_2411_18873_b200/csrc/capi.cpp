@@ -1,0 +1,421 @@
+// C ABI (include/etune_cuda.h): handles, argument checking, status mapping and
+// launch orchestration.  No compute happens here: every data-parallel step is a
+// kernel in kernels.cu / sort.cu.  There is deliberately no CPU fallback — without
+// an sm_100 device every entry point returns ETUNE_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "forest.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using namespace etune_b200;
+
+namespace etune_b200 {
+thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+}  // namespace etune_b200
+
+struct etune_cu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 0;
+    unsigned long long* d_err = nullptr;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // staging for the *_host path
+    void* io = nullptr;
+    size_t io_bytes = 0;
+    LaunchCtx lc() const { return LaunchCtx{stream, sm_count, d_err}; }
+};
+
+struct etune_cu_plan {
+    etune_cu_ctx* ctx = nullptr;
+    PlanBuild build;
+    uint8_t* d_blob = nullptr;
+    uint64_t serial = 0;
+};
+
+struct CompiledScore {
+    uint8_t* d_blob = nullptr;
+    uint32_t bytes = 0;
+    ScoreStats stats;
+};
+
+struct etune_cu_forest {
+    etune_cu_ctx* ctx = nullptr;
+    ForestHost host;
+    uint8_t* d_predict = nullptr;
+    uint32_t predict_bytes = 0;
+    std::mutex mu;
+    std::map<uint64_t, CompiledScore> compiled;  // by plan serial
+};
+
+namespace {
+
+std::mutex g_serial_mu;
+uint64_t g_serial = 0;
+
+etune_status fail(etune_status st, const std::string& msg) {
+    set_error(msg);
+    return st;
+}
+
+etune_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(ETUNE_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CU(expr)                                           \
+    do {                                                   \
+        cudaError_t _e = (expr);                           \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+    } while (0)
+
+etune_status ensure_scratch(etune_cu_ctx* c, size_t bytes) {
+    if (c->scratch_bytes >= bytes) return ETUNE_OK;
+    if (c->scratch) {
+        CU(cudaStreamSynchronize(c->stream));
+        CU(cudaFree(c->scratch));
+        c->scratch = nullptr;
+        c->scratch_bytes = 0;
+    }
+    CU(cudaMalloc(&c->scratch, bytes));
+    c->scratch_bytes = bytes;
+    return ETUNE_OK;
+}
+
+etune_status ensure_io(etune_cu_ctx* c, size_t bytes) {
+    if (c->io_bytes >= bytes) return ETUNE_OK;
+    if (c->io) {
+        CU(cudaStreamSynchronize(c->stream));
+        CU(cudaFree(c->io));
+        c->io = nullptr;
+        c->io_bytes = 0;
+    }
+    CU(cudaMalloc(&c->io, bytes));
+    c->io_bytes = bytes;
+    return ETUNE_OK;
+}
+
+etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledScore** out) {
+    std::lock_guard<std::mutex> lock(f->mu);
+    auto it = f->compiled.find(p->serial);
+    if (it != f->compiled.end()) {
+        *out = &it->second;
+        return ETUNE_OK;
+    }
+    std::vector<uint8_t> blob;
+    std::string err;
+    CompiledScore cs;
+    if (etune_status st = build_score_blob(f->host, p->build, &blob, &cs.stats, &err)) return fail(st, err);
+    const int cap = max_dynamic_smem(f->ctx->device);
+    if (blob.size() > size_t(cap)) {
+        return fail(ETUNE_ERR_UNSUPPORTED, "compiled forest (" + std::to_string(blob.size()) +
+                                               " B) exceeds shared memory (" + std::to_string(cap) + " B)");
+    }
+    CU(cudaMalloc(&cs.d_blob, blob.size()));
+    CU(cudaMemcpyAsync(cs.d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
+    CU(cudaStreamSynchronize(f->ctx->stream));
+    cs.bytes = uint32_t(blob.size());
+    auto res = f->compiled.emplace(p->serial, cs);
+    *out = &res.first->second;
+    return ETUNE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void etune_default_device_config(etune_device_config* o) {  // device.hpp:17-45
+    std::memset(o, 0, sizeof(*o));
+    o->num_sms = 108;
+    o->constant_power_w = 60.0;
+    o->static_power_per_sm_w = 0.55;
+    o->dynamic_energy_per_flop_nj = 0.002;
+    o->dynamic_energy_per_glb_access_nj = 0.125;
+    o->dynamic_energy_per_shared_access_nj = 0.0125;
+    o->base_throughput_flops_per_s_per_sm = 1.8e11;
+    o->mem_bandwidth_elems_per_s = 3.3e11;
+    o->latency_floor_ms = 1e-5;
+    o->sampler_hz = 50.0;
+    o->warmup_s = 2.0;
+    o->noise_sigma_rel = 0.05;
+    o->rng_seed = 1234;
+}
+void etune_default_space_limits(etune_space_limits* o) {  // space.hpp:15-19
+    o->max_block_threads = 1024;
+    o->max_unroll = 8;
+    o->max_vectorize = 4;
+}
+void etune_default_genetic_rates(etune_genetic_rates* o) {  // genetic.hpp:14-18
+    o->mutation = 0.85;
+    o->crossover = 0.10;
+    o->copy = 0.05;
+}
+void etune_default_boost_params(etune_boost_params* o) {  // energy_model.hpp:33-41
+    o->num_trees = 100;
+    o->max_depth = 6;
+    o->learning_rate = 0.1;
+    o->min_leaf_weight = 1e-3;
+    o->reg_lambda = 1.0;
+}
+
+const char* etune_cu_last_error(void) { return g_error.c_str(); }
+int etune_cu_abi_version(void) { return ETUNE_CUDA_ABI_VERSION; }
+uint64_t etune_cu_launch_count(void) { return launch_count(); }
+
+etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out) {
+    if (!out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "out is null");
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0)
+        return fail(ETUNE_ERR_NO_DEVICE, "no CUDA device " + std::to_string(device));
+    cudaDeviceProp prop{};
+    CU(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10)
+        return fail(ETUNE_ERR_NO_DEVICE, std::string("device is ") + prop.name + " (sm_" + std::to_string(prop.major) +
+                                             std::to_string(prop.minor) + "); this library is built for sm_100a");
+    CU(cudaSetDevice(device));
+    auto c = std::make_unique<etune_cu_ctx>();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    if (stream) {
+        c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+    }
+    CU(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    *out = c.release();
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_ctx_destroy(etune_cu_ctx* c) {
+    if (!c) return ETUNE_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_err);
+    cudaFree(c->scratch);
+    cudaFree(c->io);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_ctx_set_stream(etune_cu_ctx* c, void* stream) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "ctx is null");
+    CU(cudaStreamSynchronize(c->stream));
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    c->own_stream = false;
+    c->stream = static_cast<cudaStream_t>(stream);
+    return ETUNE_OK;
+}
+
+void* etune_cu_ctx_stream(etune_cu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+etune_status etune_cu_synchronize(etune_cu_ctx* c, int64_t* first_bad) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "ctx is null");
+    unsigned long long v = kNoError;
+    CU(cudaMemcpyAsync(&v, c->d_err, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    if (first_bad) *first_bad = -1;
+    if (v == kNoError) return ETUNE_OK;
+    CU(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    const int64_t idx = int64_t(v >> 8);
+    const etune_status st = etune_status(v & 0xffu);
+    if (first_bad) *first_bad = idx;
+    return fail(st, st == ETUNE_ERR_ILLEGAL_SCHEDULE
+                        ? "schedule " + std::to_string(idx) + " does not fit the operator (validate_schedule)"
+                        : "schedule " + std::to_string(idx) + " cannot be represented by this build");
+}
+
+etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, const etune_device_config* dev,
+                                  const etune_space_limits* limits, etune_cu_plan** out) {
+    if (!c || !op || !out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    etune_device_config d;
+    etune_default_device_config(&d);
+    if (dev) d = *dev;
+    etune_space_limits l;
+    etune_default_space_limits(&l);
+    if (limits) l = *limits;
+    auto p = std::make_unique<etune_cu_plan>();
+    p->ctx = c;
+    std::string err;
+    if (etune_status st = build_plan(*op, d, l, &p->build, &err)) return fail(st, err);
+    CU(cudaSetDevice(c->device));
+    CU(cudaMalloc(&p->d_blob, p->build.blob.size()));
+    CU(cudaMemcpyAsync(p->d_blob, p->build.blob.data(), p->build.blob.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    {
+        std::lock_guard<std::mutex> lock(g_serial_mu);
+        p->serial = ++g_serial;
+    }
+    *out = p.release();
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_plan_destroy(etune_cu_plan* p) {
+    if (!p) return ETUNE_OK;
+    cudaFree(p->d_blob);
+    delete p;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_plan_nest(const etune_cu_plan* p, int64_t out4[4]) {
+    if (!p || !out4) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    op_nest(p->build.op, out4);
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_plan_space_size(const etune_cu_plan* p, int64_t* out) {
+    if (!p || !out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    *out = p->build.space_size;
+    return ETUNE_OK;
+}
+
+#define CHECK_PLAN_ARGS(ptr)                                                   \
+    if (!c || !p) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx/plan");    \
+    if (n < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "negative n");          \
+    if (n > 0 && !(ptr)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer")
+
+etune_status etune_cu_encode(etune_cu_ctx* c, const etune_cu_plan* p, const etune_schedule* d_sched, int64_t n,
+                             uint64_t* d_genome) {
+    CHECK_PLAN_ARGS(d_sched && d_genome);
+    CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, n, d_genome));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_decode(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
+                             etune_schedule* d_sched) {
+    CHECK_PLAN_ARGS(d_sched && d_genome);
+    CU(launch_decode(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_sched));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_candidate_ids(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
+                                    uint64_t* d_ids) {
+    CHECK_PLAN_ARGS(d_ids && d_genome);
+    CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_ids));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_counters(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
+                               etune_counters* d_out) {
+    CHECK_PLAN_ARGS(d_out && d_genome);
+    CU(launch_counters(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_out));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_features(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
+                               double* d_feat, uint64_t* d_ids) {
+    CHECK_PLAN_ARGS(d_feat && d_genome);
+    CU(launch_features(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_feat, d_ids));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, const double* threshold,
+                                    const int32_t* left, const int32_t* right, const double* value,
+                                    const int64_t* tree_offsets, int64_t num_trees, double base_score,
+                                    double learning_rate, etune_cu_forest** out) {
+    if (!c || !out || !tree_offsets || num_trees < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    auto f = std::make_unique<etune_cu_forest>();
+    f->ctx = c;
+    const int64_t nn = tree_offsets[num_trees];
+    if (nn < 0 || (nn > 0 && (!feature || !threshold || !left || !right || !value)))
+        return fail(ETUNE_ERR_INVALID_ARGUMENT, "null node arrays");
+    f->host.feature.assign(feature, feature + nn);
+    f->host.threshold.assign(threshold, threshold + nn);
+    f->host.left.assign(left, left + nn);
+    f->host.right.assign(right, right + nn);
+    f->host.value.assign(value, value + nn);
+    f->host.offsets.assign(tree_offsets, tree_offsets + num_trees + 1);
+    f->host.base = base_score;
+    f->host.lr = learning_rate;
+    std::vector<uint8_t> blob;
+    std::string err;
+    if (etune_status st = build_predict_blob(f->host, &blob, &err)) return fail(st, err);
+    CU(cudaSetDevice(c->device));
+    CU(cudaMalloc(&f->d_predict, blob.size()));
+    CU(cudaMemcpyAsync(f->d_predict, blob.data(), blob.size(), cudaMemcpyHostToDevice, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    f->predict_bytes = uint32_t(blob.size());
+    *out = f.release();
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_forest_destroy(etune_cu_forest* f) {
+    if (!f) return ETUNE_OK;
+    cudaFree(f->d_predict);
+    for (auto& kv : f->compiled) cudaFree(kv.second.d_blob);
+    delete f;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_predict(etune_cu_ctx* c, etune_cu_forest* f, const double* d_feat, int64_t n,
+                              double* d_pred) {
+    if (!c || !f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx/forest");
+    if (n < 0 || (n > 0 && (!d_feat || !d_pred))) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad buffers");
+    CU(launch_predict(c->lc(), f->d_predict, f->predict_bytes, d_feat, n, d_pred));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const uint64_t* d_genome,
+                            int64_t n, double* d_pred, uint64_t* d_ids) {
+    CHECK_PLAN_ARGS(d_genome && d_pred);
+    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+    CompiledScore* cs = nullptr;
+    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
+                                 const etune_schedule* h_sched, int64_t n, double* h_pred, uint64_t* h_ids,
+                                 int64_t* first_bad) {
+    CHECK_PLAN_ARGS(h_sched && h_pred);
+    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+    if (first_bad) *first_bad = -1;
+    if (n == 0) return ETUNE_OK;
+    CompiledScore* cs = nullptr;
+    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    // chunked so the staging buffers stay bounded; one synchronisation at the end
+    const int64_t chunk = int64_t(1) << 18;
+    const size_t per = sizeof(etune_schedule) + 8 + 8 + 8;  // sched, genome, pred, id
+    const int64_t cap = n < chunk ? n : chunk;
+    if (etune_status st = ensure_io(c, size_t(cap) * per)) return st;
+    char* io = static_cast<char*>(c->io);
+    auto* d_sched = reinterpret_cast<etune_schedule*>(io);
+    auto* d_gen = reinterpret_cast<uint64_t*>(io + size_t(cap) * sizeof(etune_schedule));
+    auto* d_pred = reinterpret_cast<double*>(io + size_t(cap) * (sizeof(etune_schedule) + 8));
+    auto* d_ids = reinterpret_cast<uint64_t*>(io + size_t(cap) * (sizeof(etune_schedule) + 16));
+    for (int64_t lo = 0; lo < n; lo += chunk) {
+        const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
+        CU(cudaMemcpyAsync(d_sched, h_sched + lo, size_t(m) * sizeof(etune_schedule), cudaMemcpyHostToDevice,
+                           c->stream));
+        CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, m, d_gen, lo));
+        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_gen, m, d_pred, h_ids ? d_ids : nullptr));
+        CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
+        if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
+    }
+    return etune_cu_synchronize(c, first_bad);
+}
+
+etune_status etune_cu_topk(etune_cu_ctx* c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    if (n < 0 || k < 0 || k > n) return fail(ETUNE_ERR_INVALID_ARGUMENT, "need 0 <= k <= n");
+    if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
+    if (k == 0) return ETUNE_OK;
+    if (!d_score || !d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
+    if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
+    CU(launch_topk(c->lc(), d_score, n, k, d_idx, c->scratch));
+    return ETUNE_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,35 @@
+// Forest compiler: reference TreeNode arrays -> (a) generic predict blob,
+// (b) per-plan score blob (rank bins + partially evaluated perfect trees).
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "etune_internal.hpp"
+#include "plan.hpp"
+
+namespace etune_b200 {
+
+struct ForestHost {
+    std::vector<int32_t> feature, left, right;
+    std::vector<double> threshold, value;
+    std::vector<int64_t> offsets;  // num_trees + 1
+    double base = 0.0, lr = 0.0;
+    int64_t num_trees() const { return int64_t(offsets.size()) - 1; }
+};
+
+etune_status forest_validate(const ForestHost& F, std::string* err);
+etune_status build_predict_blob(const ForestHost& F, std::vector<uint8_t>* blob, std::string* err);
+
+struct ScoreStats {
+    int64_t internal_nodes_in = 0;   // reference interior nodes
+    int64_t tests_folded = 0;        // tests resolved at compile time for this op
+    int64_t perfect_slots = 0;       // emitted test words
+    int max_depth = 0;
+    int sum_depth = 0;
+};
+etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
+                              ScoreStats* stats, std::string* err);
+
+}  // namespace etune_b200

@@ -1,0 +1,495 @@
+// sm_100a kernels for the scoring hot path.
+//
+//   encode / decode      Schedule (96 B, reference layout) <-> 8-byte genome
+//   ids                  candidate_id (space.cpp:22-45), FNV-1a, operator prefix hoisted
+//   counters             derive_counters (counters.cpp:9-49), int64 exact
+//   features             extract_features (features.cpp:15-51) via the plan's tables
+//   score                fused features -> 100-tree forest -> prediction (+ id)
+//   predict              EnergyModel::predict on caller feature vectors
+//
+// All kernels are persistent grid-stride loops sized to the SM count; every kernel
+// first stages its read-only blob (knob tables, bins, compiled forest) into shared
+// memory, so the per-candidate work touches HBM only for its 8-byte genome and its
+// outputs.  Built with -fmad=false: every double op rounds exactly like the
+// reference's; no transcendental is evaluated on the device.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+
+#include "etune_internal.hpp"
+#include "kernels.hpp"
+
+namespace etune_b200 {
+
+namespace {
+
+constexpr uint64_t kFnvPrime = 1099511628211ull;
+constexpr uint64_t mulmod64(uint64_t a, uint64_t b) { return a * b; }
+constexpr uint64_t kFnvPrime4 = mulmod64(mulmod64(kFnvPrime, kFnvPrime), mulmod64(kFnvPrime, kFnvPrime));
+
+constexpr int kThreads = 256;
+
+__device__ __forceinline__ void stage(const uint8_t* __restrict__ g, uint32_t bytes, int4* s) {
+    const int4* src = reinterpret_cast<const int4*>(g);
+    const uint32_t n16 = bytes >> 4;
+    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) s[i] = __ldg(src + i);
+}
+
+__device__ __forceinline__ void report(unsigned long long* err, int64_t index, int code) {
+    atomicMin(err, (static_cast<unsigned long long>(index) << 8) | static_cast<unsigned>(code));
+}
+
+// FNV-1a over one 8-byte little-endian word whose upper 4 bytes are zero (every
+// schedule value is < 2^32): 4 byte steps, then the 4 zero bytes as one multiply.
+__device__ __forceinline__ uint64_t fnv_small(uint64_t h, uint32_t v) {
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        h ^= (v >> (8 * b)) & 0xffu;
+        h *= kFnvPrime;
+    }
+    return h * kFnvPrime4;
+}
+
+template <typename T>
+__device__ __forceinline__ const T* at(const uint8_t* base, uint32_t off) {
+    return reinterpret_cast<const T*>(base + off);
+}
+
+struct Knobs {
+    TilingRec r[3];
+    int64_t k_tile;
+    uint32_t unroll, vec;
+    uint32_t k;
+};
+
+__device__ __forceinline__ uint64_t candidate_hash(uint64_t prefix, const Knobs& c) {
+    uint64_t h = prefix;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        h = fnv_small(h, c.r[d].blocks);
+        h = fnv_small(h, c.r[d].threads);
+        h = fnv_small(h, c.r[d].pt);
+    }
+    h = fnv_small(h, static_cast<uint32_t>(c.k_tile));
+    h = fnv_small(h, c.unroll);
+    h = fnv_small(h, c.vec);
+    return h;
+}
+
+__device__ __forceinline__ Knobs load_knobs(const uint8_t* P, const PlanHdr& H, uint64_t g) {
+    const Genome x = genome_unpack(g);
+    Knobs c;
+    c.r[0] = at<TilingRec>(P, H.off_til[0])[x.t0];
+    c.r[1] = at<TilingRec>(P, H.off_til[1])[x.t1];
+    c.r[2] = at<TilingRec>(P, H.off_til[2])[x.t2];
+    c.k = x.k;
+    c.k_tile = at<int64_t>(P, H.off_divk)[x.k];
+    c.unroll = 1u << x.u;
+    c.vec = 1u << x.v;
+    return c;
+}
+
+// ------------------------------------------------------------------ encode
+__device__ __forceinline__ int find_tiling(const TilingRec* T, int n, int64_t blocks, int64_t threads) {
+    int lo = 0, hi = n;  // first rec >= (blocks, threads)
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        const TilingRec& r = T[mid];
+        const bool less = (int64_t(r.blocks) < blocks) || (int64_t(r.blocks) == blocks && int64_t(r.threads) < threads);
+        if (less) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kThreads) encode_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
+                                                          int use_smem, const etune_schedule* __restrict__ sched,
+                                                          int64_t n, uint64_t* __restrict__ genome,
+                                                          unsigned long long* err, int64_t index_base) {
+    extern __shared__ int4 smem[];
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        stage(gplan, bytes, smem);
+        __syncthreads();
+        P = reinterpret_cast<const uint8_t*>(smem);
+    }
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const int64_t ext[3] = {H.B, H.M, H.N};
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const etune_schedule s = sched[i];
+        // validate_schedule, schedule.cpp:26-61
+        bool ok = true;
+        uint64_t block = 1;
+        for (int d = 0; d < 3; ++d) {
+            const int64_t b = s.spatial[d][0], t = s.spatial[d][1], p = s.spatial[d][2];
+            if (b < 1 || t < 1 || p < 1) ok = false;
+            if (uint64_t(b) * uint64_t(t) * uint64_t(p) != uint64_t(ext[d])) ok = false;
+            block *= uint64_t(t);
+        }
+        if (s.k_tile < 1 || (ok && H.K % s.k_tile != 0)) ok = false;
+        if (int64_t(block) < 1 || int64_t(block) > 1024) ok = false;
+        const int64_t u = s.unroll;
+        if (!(u > 0 && (u & (u - 1)) == 0) || (s.k_tile >= 1 && s.k_tile % u != 0)) ok = false;
+        const int64_t v = s.vectorize;
+        if ((v != 1 && v != 2 && v != 4) || (s.spatial[2][2] >= 1 && s.spatial[2][2] % v != 0)) ok = false;
+        if (!ok) {
+            report(err, index_base + i, ETUNE_ERR_ILLEGAL_SCHEDULE);
+            genome[i] = 0;
+            continue;
+        }
+        uint32_t ti[3];
+        for (int d = 0; d < 3; ++d) {
+            const TilingRec* T = at<TilingRec>(P, H.off_til[d]);
+            const int j = find_tiling(T, H.nt[d], s.spatial[d][0], s.spatial[d][1]);
+            if (j >= H.nt[d] || int64_t(T[j].blocks) != s.spatial[d][0] || int64_t(T[j].threads) != s.spatial[d][1]) {
+                ok = false;  // product wrapped: legal per int64 rules but not a real tiling
+            }
+            ti[d] = uint32_t(j);
+        }
+        const int64_t* DK = at<int64_t>(P, H.off_divk);
+        int lo = 0, hi = H.ndk;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (DK[mid] < s.k_tile) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint32_t ul = uint32_t(__ffsll(u) - 1), vl = uint32_t(__ffsll(v) - 1);
+        if (!ok || lo >= H.ndk || ul > 15) {
+            report(err, index_base + i, ETUNE_ERR_UNSUPPORTED);
+            genome[i] = 0;
+            continue;
+        }
+        genome[i] = genome_pack(ti[0], ti[1], ti[2], uint32_t(lo), ul, vl);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) decode_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
+                                                          int use_smem, const uint64_t* __restrict__ genome,
+                                                          int64_t n, etune_schedule* __restrict__ out) {
+    extern __shared__ int4 smem[];
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        stage(gplan, bytes, smem);
+        __syncthreads();
+        P = reinterpret_cast<const uint8_t*>(smem);
+    }
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const Knobs c = load_knobs(P, H, genome[i]);
+        etune_schedule s;
+        for (int d = 0; d < 3; ++d) {
+            s.spatial[d][0] = c.r[d].blocks;
+            s.spatial[d][1] = c.r[d].threads;
+            s.spatial[d][2] = c.r[d].pt;
+        }
+        s.k_tile = c.k_tile;
+        s.unroll = c.unroll;
+        s.vectorize = c.vec;
+        out[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) ids_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
+                                                       int use_smem, const uint64_t* __restrict__ genome,
+                                                       int64_t n, uint64_t* __restrict__ ids) {
+    extern __shared__ int4 smem[];
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        stage(gplan, bytes, smem);
+        __syncthreads();
+        P = reinterpret_cast<const uint8_t*>(smem);
+    }
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        ids[i] = candidate_hash(H.fnv_prefix, load_knobs(P, H, genome[i]));
+    }
+}
+
+// ---------------------------------------------------------------- counters
+__global__ void __launch_bounds__(kThreads) counters_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
+                                                            int use_smem, const uint64_t* __restrict__ genome,
+                                                            int64_t n, etune_counters* __restrict__ out) {
+    extern __shared__ int4 smem[];
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        stage(gplan, bytes, smem);
+        __syncthreads();
+        P = reinterpret_cast<const uint8_t*>(smem);
+    }
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const Knobs c = load_knobs(P, H, genome[i]);
+        // counters.cpp:14-47, same int64 expressions and evaluation order
+        const int64_t bt_b = int64_t(c.r[0].threads) * c.r[0].pt;
+        const int64_t bt_m = int64_t(c.r[1].threads) * c.r[1].pt;
+        const int64_t bt_n = int64_t(c.r[2].threads) * c.r[2].pt;
+        etune_counters o;
+        o.grid = int64_t(c.r[0].blocks) * c.r[1].blocks * c.r[2].blocks;
+        o.block = int64_t(c.r[0].threads) * c.r[1].threads * c.r[2].threads;
+        const int64_t steps = H.K / c.k_tile;
+        const int64_t outputs = H.B * H.M * H.N;
+        o.flops = 2 * outputs * H.K;
+        const int64_t tile = bt_b * c.k_tile * (bt_m + bt_n);
+        o.glb_ld = o.grid * steps * tile;
+        o.shared_st = o.glb_ld;
+        o.shared_ld = o.grid * o.block * H.K * int64_t(c.r[0].pt) * (int64_t(c.r[1].pt) + int64_t(c.r[2].pt));
+        o.int_ops = o.shared_ld;
+        o.glb_st = outputs;
+        o.active_sms = o.grid < H.num_sms ? o.grid : H.num_sms;
+        const double q = __ddiv_rn(static_cast<double>(o.block), 256.0);
+        o.sm_efficiency = __dmul_rn(__ddiv_rn(static_cast<double>(o.active_sms), static_cast<double>(H.num_sms)),
+                                    q < 1.0 ? q : 1.0);
+        out[i] = o;
+    }
+}
+
+// ---------------------------------------------------------------- features
+__global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
+                                                            int use_smem, const uint64_t* __restrict__ genome,
+                                                            int64_t n, double* __restrict__ feat,
+                                                            uint64_t* __restrict__ ids) {
+    extern __shared__ int4 smem[];
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        stage(gplan, bytes, smem);
+        __syncthreads();
+        P = reinterpret_cast<const uint8_t*>(smem);
+    }
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const int nd1 = H.nd[1], nd2 = H.nd[2];
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const Knobs c = load_knobs(P, H, genome[i]);
+        const uint32_t block = c.r[0].threads * c.r[1].threads * c.r[2].threads;
+        const uint32_t gk = at<uint16_t>(P, H.off_gridkey)[(c.r[0].db * nd1 + c.r[1].db) * nd2 + c.r[2].db];
+        const GridRec gr = at<GridRec>(P, H.off_grid)[gk];
+        const GlbRec gl = at<GlbRec>(P, H.off_glb2)[c.r[1].dbt * nd2 + c.r[2].dbt];
+        const double lint = at<double>(P, H.off_int2)[c.r[1].dpt * nd2 + c.r[2].dpt];
+        const BlockRec br = at<BlockRec>(P, H.off_block)[block <= 1024 ? block : 1024];
+        const int lv = (c.r[0].pt > 1) + (c.r[1].pt > 1) + (c.r[2].pt > 1);
+        double f[16];  // features.cpp:27-45 layout
+        f[0] = H.f0;
+        f[1] = lint;
+        f[2] = gl.lg_glb_ld;
+        f[3] = H.f3;
+        f[4] = lint;
+        f[5] = gl.lg_glb_ld;
+        f[6] = static_cast<double>(c.vec);
+        f[7] = static_cast<double>(c.unroll);
+        f[8] = at<double>(P, H.off_lvl)[lv];
+        f[9] = at<double>(P, H.off_ptn)[c.r[2].dpt];
+        f[10] = at<double>(P, H.off_steps)[c.k];
+        f[11] = gr.lg_grid;
+        f[12] = br.lg_block;
+        f[13] = __dmul_rn(gr.a, br.b);
+        f[14] = gr.lg_active;
+        f[15] = gl.f15;
+        double2* o = reinterpret_cast<double2*>(feat + 16 * i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = make_double2(f[2 * j], f[2 * j + 1]);
+        if (ids) ids[i] = candidate_hash(H.fnv_prefix, c);
+    }
+}
+
+// ------------------------------------------------------------------- score
+// Fused feature bins -> forest -> prediction.  Per thread: one candidate at a time.
+__global__ void __launch_bounds__(kThreads, 2) score_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
+                                                           const uint64_t* __restrict__ genome, int64_t n,
+                                                           double* __restrict__ pred, uint64_t* __restrict__ ids) {
+    extern __shared__ int4 smem[];
+    stage(gblob, bytes, smem);
+    __syncthreads();
+    const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
+    const ScoreHdr& H = *reinterpret_cast<const ScoreHdr*>(S);
+    const TilingRec* T0 = at<TilingRec>(S, H.off_til[0]);
+    const TilingRec* T1 = at<TilingRec>(S, H.off_til[1]);
+    const TilingRec* T2 = at<TilingRec>(S, H.off_til[2]);
+    const uint16_t* gridkey = at<uint16_t>(S, H.off_gridkey);
+    const uint16_t* bgrid = at<uint16_t>(S, H.off_bgrid);
+    const double* grida = at<double>(S, H.off_grida);
+    const uint16_t* bint2 = at<uint16_t>(S, H.off_bint2);
+    const uint32_t* bglb2 = at<uint32_t>(S, H.off_bglb2);
+    const uint8_t* bblock = at<uint8_t>(S, H.off_bblock);
+    const double* blockb = at<double>(S, H.off_blockb);
+    const uint8_t* bptn = at<uint8_t>(S, H.off_bptn);
+    const uint8_t* bsteps = at<uint8_t>(S, H.off_bsteps);
+    const uint8_t* small = at<uint8_t>(S, H.off_small);
+    const double* f13 = at<double>(S, H.off_f13);
+    const int4* meta = at<int4>(S, H.off_meta);
+    const uint32_t* nodes = at<uint32_t>(S, H.off_nodes);
+    const double* leaves = at<double>(S, H.off_leaves);
+    const int nd1 = H.nd[1], nd2 = H.nd[2], n13 = H.n13, ntrees = H.ntrees;
+    const uint32_t c0 = H.bconst[0], c3 = H.bconst[3];
+    const double base = H.base, lr = H.lr;
+    const int64_t* divk = at<int64_t>(S, H.off_divk);
+    const uint64_t prefix = H.fnv_prefix;
+
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const Genome x = genome_unpack(__ldg(genome + i));
+        const TilingRec r0 = T0[x.t0], r1 = T1[x.t1], r2 = T2[x.t2];
+        uint32_t block = r0.threads * r1.threads * r2.threads;
+        block = block <= 1024u ? block : 1024u;
+        const uint32_t gk = gridkey[(r0.db * nd1 + r1.db) * nd2 + r2.db];
+        const uint32_t lv = (r0.pt > 1) + (r1.pt > 1) + (r2.pt > 1);
+        const uint32_t bi = bint2[r1.dpt * nd2 + r2.dpt];
+        const uint32_t bg = bglb2[r1.dbt * nd2 + r2.dbt];
+        const uint32_t bgr = bgrid[gk];
+        const double x13 = __dmul_rn(grida[gk], blockb[block]);
+        int lo = 0, hi = n13;  // #boundaries <= x13
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (f13[mid] <= x13) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint32_t b13 = uint32_t(lo) + 1u;
+        // bytes j of (R0,R1,R2,R3) = bin'(feature j)
+        const uint32_t R0 = c0 | ((bi & 0xffu) << 8) | ((bg & 0xffu) << 16) | (c3 << 24);
+        const uint32_t R1 = (bi >> 8) | (bg & 0xff00u) | (uint32_t(small[20 + x.v]) << 16) |
+                            (uint32_t(small[4 + x.u]) << 24);
+        const uint32_t R2 = uint32_t(small[lv]) | (uint32_t(bptn[r2.dpt]) << 8) | (uint32_t(bsteps[x.k]) << 16) |
+                            ((bgr & 0xffu) << 24);
+        const uint32_t R3 = uint32_t(bblock[block]) | (b13 << 8) | ((bgr & 0xff00u) << 8) | ((bg >> 16) << 24);
+
+        double sum = 0.0;
+        for (int t = 0; t < ntrees; ++t) {
+            const int4 m = meta[t];  // node_base, leaf_base, depth
+            const uint32_t* nd = nodes + m.x;
+            uint32_t s = 0;
+            for (int l = 0; l < m.z; ++l) {
+                const uint32_t w = nd[s];
+                const bool hiPair = (w & 0x10000u) != 0;
+                const uint32_t a = hiPair ? R2 : R0;
+                const uint32_t b = hiPair ? R3 : R1;
+                const uint32_t xb = __byte_perm(a, b, w);
+                s = 2u * s + 1u + (xb >= w ? 1u : 0u);
+            }
+            sum = __dadd_rn(sum, leaves[m.y + int(s) - ((1 << m.z) - 1)]);
+        }
+        const double p = __dadd_rn(base, __dmul_rn(lr, sum));  // energy_model.cpp:248
+        pred[i] = (1e-6 < p) ? p : 1e-6;
+        if (ids) {
+            Knobs c;
+            c.r[0] = r0;
+            c.r[1] = r1;
+            c.r[2] = r2;
+            c.k_tile = divk[x.k];
+            c.unroll = 1u << x.u;
+            c.vec = 1u << x.v;
+            ids[i] = candidate_hash(prefix, c);
+        }
+    }
+}
+
+// ----------------------------------------------------------------- predict
+__global__ void __launch_bounds__(kThreads) predict_kernel(const uint8_t* __restrict__ gblob,
+                                                           const double* __restrict__ feat, int64_t n,
+                                                           double* __restrict__ pred) {
+    const PredictHdr H = *reinterpret_cast<const PredictHdr*>(gblob);
+    const int32_t* roots = at<int32_t>(gblob, H.off_roots);
+    const GNode* nodes = at<GNode>(gblob, H.off_nodes);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        double f[16];
+        const double2* src = reinterpret_cast<const double2*>(feat + 16 * i);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const double2 v = src[j];
+            f[2 * j] = v.x;
+            f[2 * j + 1] = v.y;
+        }
+        double sum = 0.0;
+        for (int t = 0; t < H.ntrees; ++t) {  // energy_model.cpp:36-44, 245-249
+            int node = __ldg(roots + t);
+            int feature = __ldg(&nodes[node].feature);
+            while (feature >= 0) {
+                double v = 0.0;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v = (j == feature) ? f[j] : v;
+                node = v < __ldg(&nodes[node].thr) ? __ldg(&nodes[node].left) : __ldg(&nodes[node].right);
+                feature = __ldg(&nodes[node].feature);
+            }
+            sum = __dadd_rn(sum, __ldg(&nodes[node].value));
+        }
+        const double p = __dadd_rn(H.base, __dmul_rn(H.lr, sum));
+        pred[i] = (1e-6 < p) ? p : 1e-6;
+    }
+}
+
+int grid_for(const LaunchCtx& c, int64_t n, int per_sm) {
+    const int64_t want = (n + kThreads - 1) / kThreads;
+    const int64_t cap = int64_t(c.sm_count) * per_sm;
+    return int(want < cap ? (want > 0 ? want : 1) : cap);
+}
+
+constexpr uint32_t kPlanSmemCap = 96 * 1024;
+
+template <typename K, typename... A>
+cudaError_t launch_plan_kernel(K kernel, const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, int64_t n,
+                               A... args) {
+    if (n <= 0) return cudaSuccess;
+    const int use_smem = bytes <= kPlanSmemCap ? 1 : 0;
+    const size_t sm = use_smem ? bytes : 0;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
+    kernel<<<grid_for(c, n, 8), kThreads, sm, c.stream>>>(d_plan, bytes, use_smem, args...);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launches(int k) { g_launches.fetch_add(uint64_t(k), std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+int max_dynamic_smem(int device) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    return v;
+}
+
+cudaError_t launch_encode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const etune_schedule* d_sched,
+                          int64_t n, uint64_t* d_genome, int64_t index_base) {
+    return launch_plan_kernel(encode_kernel, c, d_plan, bytes, n, d_sched, n, d_genome, c.d_err, index_base);
+}
+cudaError_t launch_decode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
+                          int64_t n, etune_schedule* d_sched) {
+    return launch_plan_kernel(decode_kernel, c, d_plan, bytes, n, d_genome, n, d_sched);
+}
+cudaError_t launch_ids(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
+                       int64_t n, uint64_t* d_ids) {
+    return launch_plan_kernel(ids_kernel, c, d_plan, bytes, n, d_genome, n, d_ids);
+}
+cudaError_t launch_counters(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
+                            int64_t n, etune_counters* d_out) {
+    return launch_plan_kernel(counters_kernel, c, d_plan, bytes, n, d_genome, n, d_out);
+}
+cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
+                            int64_t n, double* d_feat, uint64_t* d_ids) {
+    return launch_plan_kernel(features_kernel, c, d_plan, bytes, n, d_genome, n, d_feat, d_ids);
+}
+
+cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
+                         int64_t n, double* d_pred, uint64_t* d_ids) {
+    if (n <= 0) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kThreads, bytes);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    score_kernel<<<grid_for(c, n, per_sm), kThreads, bytes, c.stream>>>(d_score, bytes, d_genome, n, d_pred, d_ids);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_blob, uint32_t /*bytes*/, const double* d_feat,
+                           int64_t n, double* d_pred) {
+    if (n <= 0) return cudaSuccess;
+    predict_kernel<<<grid_for(c, n, 8), kThreads, 0, c.stream>>>(d_blob, d_feat, n, d_pred);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace etune_b200

@@ -1,0 +1,49 @@
+// Host-side launchers for the sm_100a kernels (kernels.cu, sort.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "etune_internal.hpp"
+
+namespace etune_b200 {
+
+struct LaunchCtx {
+    cudaStream_t stream;
+    int sm_count;                 // physical SMs of the GPU (148 on B200)
+    unsigned long long* d_err;    // packed (index << 8 | status), min wins
+};
+
+// d_err sentinel: no error
+constexpr unsigned long long kNoError = ~0ull;
+
+cudaError_t launch_encode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                          const etune_schedule* d_sched, int64_t n, uint64_t* d_genome,
+                          int64_t index_base = 0);
+cudaError_t launch_decode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                          const uint64_t* d_genome, int64_t n, etune_schedule* d_sched);
+cudaError_t launch_ids(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                       const uint64_t* d_genome, int64_t n, uint64_t* d_ids);
+cudaError_t launch_counters(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                            const uint64_t* d_genome, int64_t n, etune_counters* d_out);
+cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                            const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
+cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
+                         const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids);
+cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_pred_blob, uint32_t bytes,
+                           const double* d_feat, int64_t n, double* d_pred);
+
+// (score asc, index asc) top-k; scratch sized by topk_scratch_bytes(n).
+size_t topk_scratch_bytes(int64_t n);
+cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, int64_t k,
+                        int64_t* d_idx, void* d_scratch);
+
+// process-wide count of kernel launches (incremented by every launcher)
+void note_launches(int k);
+uint64_t launch_count();
+
+// Largest dynamic smem the score kernel may use on this device.
+int max_dynamic_smem(int device);
+
+}  // namespace etune_b200
