@@ -45,7 +45,7 @@ ALGO_BYTES = 24
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=200)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--pop", type=int, default=1 << 20, help="candidates per GPU per step")
@@ -110,73 +110,76 @@ def cpu_score_runner():
 
 
 def time_cpu(op, sched, target_s: float):
+    """Bounded CPU sample: whole passes over (a prefix of) the population until
+    ~target_s of work has been timed."""
     kind, fn, threads = cpu_score_runner()
     m = min(len(sched), 20000)
     t0 = time.perf_counter()
     fn(op, sched[:m])
-    dt = time.perf_counter() - t0
-    rate = m / max(dt, 1e-9)
-    m2 = int(min(len(sched), max(m, rate * target_s)))
-    t0 = time.perf_counter()
-    fn(op, sched[:m2])
-    dt = time.perf_counter() - t0
-    return {"value": m2 / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"first {m2} candidates of the bench population ({OP_TEXT}); extract_features + "
-                      f"EnergyModel::predict per candidate over {threads} std::threads; {dt:.1f} s"}
+    rate = m / max(time.perf_counter() - t0, 1e-9)
+    total = int(max(m, rate * target_s))
+    done, dt = 0, 0.0
+    while done < total:
+        chunk = sched[: min(len(sched), total - done)]
+        t0 = time.perf_counter()
+        fn(op, chunk)
+        dt += time.perf_counter() - t0
+        done += len(chunk)
+    return {"value": done / dt, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{done} candidates (passes over the bench population, {OP_TEXT}); the reference's "
+                      f"extract_features + EnergyModel::predict per candidate over {threads} std::threads; "
+                      f"{dt:.1f} s"}
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled through NVML during the timed region
+    (a background thread every 5 ms, plus explicit samples at its start and end)."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.proc = None
-        self.lines = []
+        self.sm, self.max_sm, self.reasons = [], 0.0, set()
+        self.stop = threading.Event()
+        self.nv = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu)
+            self.max_sm = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+
+    def sample(self):
+        if not self.nv:
+            return
+        try:
+            self.sm.append(float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)))
+            r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            for nm, bit in self.REASONS.items():
+                if r & bit:
+                    self.reasons.add(nm)
+        except Exception:
+            pass
+
+    def _loop(self):
+        while not self.stop.wait(0.005):
+            self.sample()
 
     def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except FileNotFoundError:
-            self.proc = None
+        self.t = threading.Thread(target=self._loop, daemon=True)
+        self.t.start()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.stop.set()
+        self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            p = [x.strip() for x in ln.split(",")]
-            if len(p) < 9:
-                continue
-            try:
-                sm.append(float(p[1]))
-                mx = max(mx, float(p[2]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, p[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.max_sm or None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
 
 
 def run_reference(args):
@@ -223,6 +226,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    stream = torch.cuda.Stream(local)
+    torch.cuda.set_stream(stream)  # the ctx, events and collectives all run on this stream
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2411_18873_b200 import capi
@@ -241,7 +246,6 @@ def run_ours(args):
     genomes = [g0.clone() for _ in range(nb)]
     preds = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nb)]
     ids = [torch.empty(n, dtype=torch.int64, device="cuda") for _ in range(nb)]
-    stream = torch.cuda.current_stream()
     K = min(args.k, n)
 
     def step(i):
@@ -273,6 +277,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
+        clk.sample()
         for i in range(args.steps):
             b = (args.warmup + i) % nb
             kev[i][0].record(stream)
@@ -286,6 +291,7 @@ def run_ours(args):
                 sel = capi.topk(ctx, allrec[:, 0].contiguous(), K)
                 top = allrec[:, 1].to(torch.int64)[sel]
         ev1.record(stream)
+        clk.sample()
         torch.cuda.synchronize()
     launches = capi.lib().etune_cu_launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps

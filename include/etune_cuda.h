@@ -120,7 +120,7 @@ uint64_t etune_cu_launch_count(void);
 /* ------------------------------------------------------------------ context */
 typedef struct etune_cu_ctx etune_cu_ctx;
 
-/* stream: a cudaStream_t (NULL -> the library creates its own non-blocking stream). */
+/* stream: the cudaStream_t every call of this ctx is ordered on (NULL = default stream). */
 etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out);
 etune_status etune_cu_ctx_destroy(etune_cu_ctx* ctx);
 etune_status etune_cu_ctx_set_stream(etune_cu_ctx* ctx, void* stream);
@@ -201,6 +201,12 @@ etune_status etune_cu_score_host(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                  etune_cu_forest* forest, const etune_schedule* h_sched,
                                  int64_t n, double* h_pred, uint64_t* h_ids /*nullable*/,
                                  int64_t* first_bad /*nullable*/);
+
+/* Diagnostics of the per-plan forest compilation: {reference interior nodes, tests
+ * folded for this operator, class->mask table entries, max leaves per tree, total
+ * leaves, blob bytes, bitmask of feature channels still tested, trees}. */
+etune_status etune_cu_forest_compile_stats(etune_cu_forest* forest, const etune_cu_plan* plan,
+                                           int64_t out[8]);
 
 /* ------------------------------------------------------------- selection */
 /* The k smallest of d_score[0..n) under the total order (score asc, index asc)

@@ -46,6 +46,7 @@ struct etune_cu_plan {
 struct CompiledScore {
     uint8_t* d_blob = nullptr;
     uint32_t bytes = 0;
+    int mask_bits = 32;
     ScoreStats stats;
 };
 
@@ -124,6 +125,7 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     CU(cudaMemcpyAsync(cs.d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaStreamSynchronize(f->ctx->stream));
     cs.bytes = uint32_t(blob.size());
+    cs.mask_bits = reinterpret_cast<const ScoreHdr*>(blob.data())->mask_bits;
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;
@@ -185,12 +187,7 @@ etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out) {
     auto c = std::make_unique<etune_cu_ctx>();
     c->device = device;
     c->sm_count = prop.multiProcessorCount;
-    if (stream) {
-        c->stream = static_cast<cudaStream_t>(stream);
-    } else {
-        CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-        c->own_stream = true;
-    }
+    c->stream = static_cast<cudaStream_t>(stream);  // NULL = the default stream
     CU(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
     CU(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
     *out = c.release();
@@ -372,7 +369,7 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
-    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids));
+    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits));
     return ETUNE_OK;
 }
 
@@ -400,7 +397,7 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         CU(cudaMemcpyAsync(d_sched, h_sched + lo, size_t(m) * sizeof(etune_schedule), cudaMemcpyHostToDevice,
                            c->stream));
         CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, m, d_gen, lo));
-        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_gen, m, d_pred, h_ids ? d_ids : nullptr));
+        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_gen, m, d_pred, h_ids ? d_ids : nullptr, cs->mask_bits));
         CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
         if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
     }
@@ -419,3 +416,18 @@ etune_status etune_cu_topk(etune_cu_ctx* c, const double* d_score, int64_t n, in
 }
 
 }  // extern "C"
+
+extern "C" etune_status etune_cu_forest_compile_stats(etune_cu_forest* f, const etune_cu_plan* p, int64_t out[8]) {
+    if (!f || !p || !out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    CompiledScore* cs = nullptr;
+    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    out[0] = cs->stats.internal_nodes_in;
+    out[1] = cs->stats.tests_folded;
+    out[2] = cs->stats.lut_entries;
+    out[3] = cs->stats.max_leaves;
+    out[4] = cs->stats.total_leaves;
+    out[5] = cs->bytes;
+    out[6] = cs->stats.channels_used;
+    out[7] = f->host.num_trees();
+    return ETUNE_OK;
+}

@@ -104,43 +104,46 @@ struct PlanHdr {
 };
 
 // ------------------------------------------------------------ score blob
-// Per (plan, forest): rank bins + the forest partially evaluated for the op and
-// laid out as perfect binary trees of 32-bit test words.
-//
-// Bins: every feature j gets a byte b' = 1 + #(effective thresholds on j <= x);
-// a node test "f[j] < thr" becomes "b'_j < r'" and is evaluated branch-free as
-//   x = prmt(pairlo, pairhi, w) (byte j replicated x4);  go_right = (x >= w)
-// with w = r' << 24 | pair << 16 | (j & 7) * 0x1111  (see forest.cpp).
-struct TreeMeta {
-    int32_t node_base;  // index into nodes[] (uint32)
-    int32_t leaf_base;  // index into leaves[] (double)
-    int32_t depth;      // perfect depth after partial evaluation (0 = single leaf)
-    int32_t pad;
+// Per (plan, forest).  Each feature is a function of one "channel key" of the
+// candidate (e.g. glb_ld, f2/f5/f15, is keyed by the (block-tile m, block-tile n)
+// divisor pair).  The host partitions every channel's key domain into classes of
+// identical test outcomes over the whole forest, then stores per (tree, channel) a
+// lookup table  class -> bitmask of the tree's leaves that stay reachable
+// (QuickScorer: a node whose test goes right removes its left subtree's leaves).
+// Device: mask = AND_c LUT[t][c][class_c]; exit leaf = lowest set bit; leaf values
+// are the reference's doubles, summed in tree order (energy_model.cpp:247).
+enum Channel : int {
+    kChInt = 0,   // (dpt_m, dpt_n)          -> f1, f4 (int_ops = shared_ld)
+    kChGlb = 1,   // (dbt_m, dbt_n)          -> f2, f5, f15 (glb_ld = shared_st)
+    kChGrid = 2,  // grid index              -> f11, f14
+    kChBlk = 3,   // block size 0..1024      -> f12
+    kChEff = 4,   // f13 rank bin            -> f13 (sm_efficiency = a(grid) * b(block))
+    kChKuv = 5,   // (k idx, log2 u, log2 v) -> f10, f7, f6
+    kChLvp = 6,   // (levels, dpt_n)         -> f8, f9
+    kNumChannels = 7
+};
+
+struct TreeRec {          // 32 bytes, read warp-uniformly
+    uint32_t lut[7];      // mask-word index of this tree's LUT per channel (shared all-ones
+                          // table when the tree does not test the channel)
+    uint32_t leaf_base;   // index into leaves[]
 };
 
 struct ScoreHdr {
     int64_t K;
     uint64_t fnv_prefix;
     double base, lr;
-    int32_t ntrees, max_depth;
-    int32_t nt[3], nd[3], ndk, ngrid;
-    int32_t n13;             // effective f13 boundaries (device binary search)
-    uint8_t bconst[16];      // bins of features constant over the op (f0, f3, ...)
+    int32_t ntrees, mask_bits;   // 32 or 64
+    int32_t nt[3], nd[3], ndk, ngrid, n13, pad;
     uint32_t off_til[3];     // TilingRec
     uint32_t off_divk;       // int64 k values (ids)
-    uint32_t off_gridkey;    // uint16
-    uint32_t off_bgrid;      // uint16 per grid: f11 | f14 << 8
-    uint32_t off_grida;      // double per grid
-    uint32_t off_bint2;      // uint16 per (dpt1, dpt2): f1 | f4 << 8
-    uint32_t off_bglb2;      // uint32 per (dbt1, dbt2): f2 | f5 << 8 | f15 << 16
-    uint32_t off_bblock;     // uint8 per block 0..1024: f12
-    uint32_t off_blockb;     // double per block 0..1024
-    uint32_t off_bptn;       // uint8 per dpt2: f9
-    uint32_t off_bsteps;     // uint8 per k: f10
-    uint32_t off_small;      // uint8[32]: lvl[4] (f8), u[16] (f7), v[4] (f6), pad
-    uint32_t off_f13;        // double[n13] boundaries
-    uint32_t off_meta;       // TreeMeta[ntrees]
-    uint32_t off_nodes;      // uint32
+    uint32_t off_gridkey;    // uint16 [nd0][nd1][nd2]
+    uint32_t off_grida;      // double per grid: active/sms
+    uint32_t off_blockb;     // double per block 0..1024: min(1, block/256)
+    uint32_t off_f13;        // double[n13] effective f13 boundaries
+    uint32_t off_cls[7];     // uint8 class tables per channel key (kChEff: none)
+    uint32_t off_trees;      // TreeRec[ntrees]
+    uint32_t off_lut;        // mask words (uint32 or uint64)
     uint32_t off_leaves;     // double
     uint32_t total;
 };

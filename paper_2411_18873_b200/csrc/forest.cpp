@@ -1,23 +1,26 @@
 // Forest compiler.
 //
 // The reference evaluates every tree by walking `f[feature] < threshold ? left : right`
-// on FP64 features (energy_model.cpp:36-44).  For one operator every feature takes
-// values from a small known set V_j (the plan's tables), so a test only matters
-// through rho = #{v in V_j : v < thr}: for attainable x, x < thr <=> idx_j(x) < rho.
-//   * rho == 0 or rho == |V_j|  -> the test is constant for this op: folded away.
-//   * otherwise the distinct rho of feature j become its "effective thresholds" R_j,
-//     bin_j(x) = #{rho in R_j : rho <= idx_j(x)} (fits a byte when |R_j| <= 254),
-//     and the test becomes  bin_j(x) < r  with r = 1 + position of rho in R_j.
-// Tests that a path already decides (same feature, nested ranks) are folded too.
-// What remains is emitted as a perfect binary tree per reference tree (shallow
-// leaves padded with always-right dummy tests, leaf value replicated) so the device
-// walk is branch-free with a uniform trip count.  Leaf values are the reference's
-// doubles, summed on device in the reference's tree order (energy_model.cpp:247).
+// on FP64 features (energy_model.cpp:36-44).  For one operator each feature is a
+// function of one small "channel key" of the candidate (etune_internal.hpp, Channel),
+// whose value set is known exactly from the plan's tables.  So, per operator:
+//   1. every key value of a channel is evaluated against every test of the forest on
+//      that channel's features, with the exact doubles the reference would compare;
+//      keys with identical outcome vectors form one class (u8);
+//   2. per (tree, channel) a table class -> mask of the tree's leaves that remain
+//      reachable (a node whose test goes right removes its left subtree's leaves);
+//      tests whose outcome is the same for every attainable candidate (e.g. on the
+//      constant features f0/f3) are folded into the tree's base mask;
+//   3. on the device the exit leaf is the lowest set bit of the AND of the tree's
+//      channel masks (QuickScorer's argument: the exit leaf survives every AND and
+//      every leaf left of it lies in the left subtree of a node that went right).
+// Leaf values are the reference's doubles, summed in tree order.
 #include "forest.hpp"
 
 #include <algorithm>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 
 namespace etune_b200 {
@@ -30,20 +33,6 @@ uint32_t put(std::vector<uint8_t>& blob, const T* data, size_t count) {
     blob.resize(off + sizeof(T) * count);
     if (count) std::memcpy(blob.data() + off, data, sizeof(T) * count);
     return off;
-}
-
-struct CNode {
-    bool leaf = true;
-    double value = 0.0;
-    int feat = 0;
-    int rprime = 0;  // test word rank (bin+1 domain)
-    std::unique_ptr<CNode> kid[2];
-    int depth() const { return leaf ? 0 : 1 + std::max(kid[0]->depth(), kid[1]->depth()); }
-};
-
-void sort_unique(std::vector<double>& v) {
-    std::sort(v.begin(), v.end());
-    v.erase(std::unique(v.begin(), v.end()), v.end());
 }
 
 }  // namespace
@@ -110,226 +99,269 @@ etune_status build_predict_blob(const ForestHost& F, std::vector<uint8_t>* blob,
     return ETUNE_OK;
 }
 
+namespace {
+
+// value of feature j for key `key` of its channel (only for j with a table-backed channel)
+struct ChannelKeys {
+    int nkeys[kNumChannels] = {0, 0, 0, 0, 0, 0, 0};
+};
+
+int channel_of(int j) {
+    switch (j) {
+    case 1: case 4: return kChInt;
+    case 2: case 5: case 15: return kChGlb;
+    case 11: case 14: return kChGrid;
+    case 12: return kChBlk;
+    case 13: return kChEff;
+    case 6: case 7: case 10: return kChKuv;
+    case 8: case 9: return kChLvp;
+    default: return -1;  // f0, f3: constant over the operator
+    }
+}
+
+}  // namespace
+
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
                               ScoreStats* stats, std::string* err) {
     if (etune_status st = forest_validate(F, err)) return st;
     const PlanHdr& PH = P.hdr;
+    const int nd1 = PH.nd[1], nd2 = PH.nd[2], ndk = PH.ndk;
+    ScoreStats S;
 
-    // ---- attainable value sets V_j (supersets are fine: they only refine bins)
-    std::vector<double> V[16];
-    V[0] = {PH.f0};
-    V[3] = {PH.f3};
-    for (double x : P.int2) {
-        V[1].push_back(x);
-        V[4].push_back(x);
-    }
-    for (const GlbRec& g : P.glb2) {
-        V[2].push_back(g.lg_glb_ld);
-        V[5].push_back(g.lg_glb_ld);
-        V[15].push_back(g.f15);
-    }
-    V[6] = {1.0, 2.0, 4.0};
-    for (int u = 0; u < 16; ++u) V[7].push_back(double(int64_t(1) << u));
-    for (double x : P.lvl) V[8].push_back(x);
-    for (double x : P.ptn) V[9].push_back(x);
-    for (double x : P.steps) V[10].push_back(x);
-    for (const GridRec& g : P.grid) {
-        V[11].push_back(g.lg_grid);
-        V[14].push_back(g.lg_active);
-    }
-    for (int b = 0; b <= 1024; ++b) V[12].push_back(P.block[b].lg_block);
+    // ---- f13 (a(grid) * b(block)): the only feature computed on device; its class is
+    // the number of effective f13 boundaries <= x (binary search in smem).
+    std::vector<double> V13;
     for (const GridRec& g : P.grid)
-        for (int b = 1; b <= 1024; ++b) V[13].push_back(g.a * P.block[b].b);
-    for (auto& v : V) sort_unique(v);
+        for (int b = 1; b <= 1024; ++b) V13.push_back(g.a * P.block[b].b);
+    std::sort(V13.begin(), V13.end());
+    V13.erase(std::unique(V13.begin(), V13.end()), V13.end());
+    std::vector<double> f13b;  // boundaries V13[rho], rho in (0, |V13|)
+    for (size_t i = 0; i < F.feature.size(); ++i) {
+        if (F.feature[i] != 13) continue;
+        const size_t rho = size_t(std::lower_bound(V13.begin(), V13.end(), F.threshold[i]) - V13.begin());
+        if (rho > 0 && rho < V13.size()) f13b.push_back(V13[rho]);
+    }
+    std::sort(f13b.begin(), f13b.end());
+    f13b.erase(std::unique(f13b.begin(), f13b.end()), f13b.end());
 
-    auto rho_of = [&](int j, double thr) {
-        return int(std::lower_bound(V[j].begin(), V[j].end(), thr) - V[j].begin());
+    // ---- feature value of (channel, key) for feature j
+    const int nkeys[kNumChannels] = {nd1 * nd2, nd1 * nd2, PH.ngrid, 1025, int(f13b.size()) + 1, ndk * 64,
+                                     4 * nd2};
+    auto value = [&](int j, int key) -> double {
+        switch (j) {
+        case 1: case 4: return P.int2[size_t(key)];
+        case 2: case 5: return P.glb2[size_t(key)].lg_glb_ld;
+        case 15: return P.glb2[size_t(key)].f15;
+        case 11: return P.grid[size_t(key)].lg_grid;
+        case 14: return P.grid[size_t(key)].lg_active;
+        case 12: return P.block[size_t(key)].lg_block;
+        case 13: return key == 0 ? V13.front() : f13b[size_t(key - 1)];  // class representative
+        case 10: return P.steps[size_t(key / 64)];
+        case 7: return double(int64_t(1) << ((key / 4) % 16));
+        case 6: return double(1 << (key % 4));
+        case 8: return P.lvl[key / nd2];
+        case 9: return P.ptn[size_t(key % nd2)];
+        default: return 0.0;
+        }
     };
-    // ---- effective thresholds R_j
-    std::vector<int> R[16];
+    auto key_valid = [&](int c, int key) {  // kuv keys with v == 3 or k beyond K: unreachable
+        if (c == kChKuv) return (key % 4) < 3;
+        return true;
+    };
+
+    // ---- distinct tests per channel, then classes of keys by outcome signature
+    std::vector<std::pair<int, double>> tests[kNumChannels];
     for (size_t i = 0; i < F.feature.size(); ++i) {
         const int j = F.feature[i];
         if (j < 0) continue;
-        const int rho = rho_of(j, F.threshold[i]);
-        if (rho > 0 && rho < int(V[j].size())) R[j].push_back(rho);
+        const int c = channel_of(j);
+        if (c >= 0) tests[c].push_back({j, F.threshold[i]});
     }
-    for (auto& r : R) {
-        std::sort(r.begin(), r.end());
-        r.erase(std::unique(r.begin(), r.end()), r.end());
-        if (r.size() > 254) {
-            *err = "a feature has more than 254 effective split points for this operator "
-                   "(byte bins); not supported by this build";
-            return ETUNE_ERR_UNSUPPORTED;
+    std::vector<std::vector<uint8_t>> cls(kNumChannels);
+    std::vector<std::vector<int>> rep(kNumChannels);  // representative key per class
+    for (int c = 0; c < kNumChannels; ++c) {
+        auto& T = tests[c];
+        std::sort(T.begin(), T.end());
+        T.erase(std::unique(T.begin(), T.end()), T.end());
+        std::map<std::vector<bool>, int> sig2cls;
+        cls[c].assign(size_t(nkeys[c]), 0);
+        for (int key = 0; key < nkeys[c]; ++key) {
+            if (!key_valid(c, key)) continue;
+            std::vector<bool> sig(T.size());
+            for (size_t q = 0; q < T.size(); ++q) sig[q] = value(T[q].first, key) < T[q].second;
+            auto it = sig2cls.find(sig);
+            int id;
+            if (it == sig2cls.end()) {
+                id = int(sig2cls.size());
+                sig2cls.emplace(std::move(sig), id);
+                rep[c].push_back(key);
+            } else {
+                id = it->second;
+            }
+            if (id > 255) {
+                *err = "more than 256 outcome classes on one feature channel for this operator";
+                return ETUNE_ERR_UNSUPPORTED;
+            }
+            cls[c][size_t(key)] = uint8_t(id);
         }
+        if (rep[c].empty()) rep[c].push_back(0);
     }
-    auto bin_of = [&](int j, double x) -> uint8_t {  // 1 + #(R_j <= idx(x))
-        const int ix = rho_of(j, x);
-        return uint8_t(1 + (std::upper_bound(R[j].begin(), R[j].end(), ix) - R[j].begin()));
-    };
 
-    // ---- compile trees
-    ScoreStats S;
-    int lo[16], hi[16];
-    for (int j = 0; j < 16; ++j) {
-        lo[j] = 1;
-        hi[j] = int(R[j].size()) + 1;
-    }
-    std::function<std::unique_ptr<CNode>(int64_t, int64_t, int)> compile =
-        [&](int64_t base, int64_t i, int guard) -> std::unique_ptr<CNode> {
-        if (guard > 64) return nullptr;  // cycle
-        auto node = std::make_unique<CNode>();
-        const int j = F.feature[base + i];
-        if (j < 0) {
-            node->value = F.value[base + i];
-            return node;
-        }
-        S.internal_nodes_in++;
-        const int rho = rho_of(j, F.threshold[base + i]);
-        if (rho == 0) {  // x < thr never: right
-            S.tests_folded++;
-            return compile(base, F.right[base + i], guard + 1);
-        }
-        if (rho == int(V[j].size())) {  // always left
-            S.tests_folded++;
-            return compile(base, F.left[base + i], guard + 1);
-        }
-        const int pos = int(std::lower_bound(R[j].begin(), R[j].end(), rho) - R[j].begin());
-        const int rp = pos + 2;  // go right iff b'_j >= rp
-        if (lo[j] >= rp) {
-            S.tests_folded++;
-            return compile(base, F.right[base + i], guard + 1);
-        }
-        if (hi[j] < rp) {
-            S.tests_folded++;
-            return compile(base, F.left[base + i], guard + 1);
-        }
-        node->leaf = false;
-        node->feat = j;
-        node->rprime = rp;
-        const int save_lo = lo[j], save_hi = hi[j];
-        hi[j] = rp - 1;
-        node->kid[0] = compile(base, F.left[base + i], guard + 1);
-        hi[j] = save_hi;
-        lo[j] = rp;
-        node->kid[1] = compile(base, F.right[base + i], guard + 1);
-        lo[j] = save_lo;
-        if (!node->kid[0] || !node->kid[1]) return nullptr;
-        return node;
-    };
-
+    // ---- per tree: leaves in order, left-subtree masks, per-channel LUTs
     const int64_t T = F.num_trees();
-    std::vector<TreeMeta> meta(static_cast<size_t>(T));
-    std::vector<uint32_t> nodes;
+    int max_leaves = 1;
+    for (int64_t t = 0; t < T; ++t) {
+        int nl = 0;
+        for (int64_t i = F.offsets[t]; i < F.offsets[t + 1]; ++i) nl += F.feature[i] < 0;
+        max_leaves = std::max(max_leaves, nl);
+    }
+    if (max_leaves > 64) {
+        *err = "a tree has more than 64 leaves (max_depth > 6); not supported by this build";
+        return ETUNE_ERR_UNSUPPORTED;
+    }
+    const int mbits = max_leaves <= 32 ? 32 : 64;
+    const uint64_t full = mbits == 32 ? 0xffffffffull : ~0ull;
+
+    std::vector<uint64_t> lut;  // mask words; word 0.. = shared all-ones table (256 entries)
+    lut.assign(256, full);
+    std::map<std::vector<uint64_t>, uint32_t> dedupe;
+    std::vector<TreeRec> recs(static_cast<size_t>(T));
     std::vector<double> leaves;
     for (int64_t t = 0; t < T; ++t) {
-        auto root = compile(F.offsets[t], 0, 0);
-        if (!root) {
-            *err = "tree contains a cycle";
-            return ETUNE_ERR_IO;
-        }
-        const int D = root->depth();
-        if (D > 12) {
-            *err = "tree deeper than 12 after partial evaluation; not supported by this build";
-            return ETUNE_ERR_UNSUPPORTED;
-        }
-        S.max_depth = std::max(S.max_depth, D);
-        S.sum_depth += D;
-        meta[t].node_base = int32_t(nodes.size());
-        meta[t].leaf_base = int32_t(leaves.size());
-        meta[t].depth = D;
-        meta[t].pad = 0;
-        const size_t ni = (size_t(1) << D) - 1;
-        const size_t nl = size_t(1) << D;
-        const size_t nb = nodes.size(), lb = leaves.size();
-        nodes.resize(nb + ni, 0x01000000u);
-        leaves.resize(lb + nl, 0.0);
-        S.perfect_slots += int64_t(ni);
-        std::function<void(const CNode*, size_t, int)> emit = [&](const CNode* c, size_t slot, int level) {
-            if (level == D) {
-                leaves[lb + (slot - ni)] = c->value;
-                return;
+        const int64_t b = F.offsets[t], e = F.offsets[t + 1];
+        // in-order leaf numbering and left-subtree leaf masks (iterative DFS)
+        std::vector<int> leaf_id(size_t(e - b), -1);
+        std::vector<uint64_t> sub(size_t(e - b), 0);
+        std::vector<double> lv;
+        std::function<uint64_t(int64_t, int)> walk = [&](int64_t i, int guard) -> uint64_t {
+            if (guard > 64) return 0;
+            if (F.feature[b + i] < 0) {
+                leaf_id[size_t(i)] = int(lv.size());
+                lv.push_back(F.value[b + i]);
+                return sub[size_t(i)] = uint64_t(1) << leaf_id[size_t(i)];
             }
-            if (c->leaf) {  // dummy always-right test; replicate the leaf below
-                nodes[nb + slot] = 0x01000000u;
-                emit(c, 2 * slot + 1, level + 1);
-                emit(c, 2 * slot + 2, level + 1);
-                return;
-            }
-            const uint32_t pair = uint32_t(c->feat) >> 3;
-            const uint32_t q = uint32_t(c->feat) & 7u;
-            nodes[nb + slot] = (uint32_t(c->rprime) << 24) | (pair << 16) | (q * 0x1111u);
-            emit(c->kid[0].get(), 2 * slot + 1, level + 1);
-            emit(c->kid[1].get(), 2 * slot + 2, level + 1);
+            const uint64_t l = walk(F.left[b + i], guard + 1);
+            const uint64_t r = walk(F.right[b + i], guard + 1);
+            return sub[size_t(i)] = l | r;
         };
-        emit(root.get(), 0, 0);
+        walk(0, 0);
+        uint64_t base = full;
+        std::vector<std::vector<uint64_t>> tl(kNumChannels);
+        std::vector<bool> used(kNumChannels, false);
+        // visit reachable interior nodes
+        std::vector<int64_t> stack = {0};
+        while (!stack.empty()) {
+            const int64_t i = stack.back();
+            stack.pop_back();
+            const int j = F.feature[b + i];
+            if (j < 0) continue;
+            S.internal_nodes_in++;
+            const uint64_t lmask = sub[size_t(F.left[b + i])];
+            const int c = channel_of(j);
+            const double thr = F.threshold[b + i];
+            if (c < 0) {  // constant feature
+                const double x = (j == 0) ? PH.f0 : PH.f3;
+                if (!(x < thr)) base &= ~lmask;
+                S.tests_folded++;
+            } else {
+                // outcome per class (via representative key)
+                bool all_left = true, all_right = true;
+                std::vector<bool> right(rep[c].size());
+                for (size_t k = 0; k < rep[c].size(); ++k) {
+                    right[k] = !(value(j, rep[c][k]) < thr);
+                    all_left &= !right[k];
+                    all_right &= right[k];
+                }
+                if (all_left || all_right) {
+                    S.tests_folded++;
+                    if (all_right) base &= ~lmask;
+                } else {
+                    if (!used[c]) {
+                        used[c] = true;
+                        tl[c].assign(rep[c].size(), full);
+                        S.channels_used |= 1 << c;
+                    }
+                    for (size_t k = 0; k < rep[c].size(); ++k)
+                        if (right[k]) tl[c][k] &= ~lmask;
+                }
+            }
+            stack.push_back(F.left[b + i]);
+            stack.push_back(F.right[b + i]);
+        }
+        // fold the base mask into one channel table
+        if (base != full) {
+            int host = -1;
+            for (int c = 0; c < kNumChannels; ++c)
+                if (used[c]) {
+                    host = c;
+                    break;
+                }
+            if (host < 0) {  // nothing varies: private constant table on the smallest channel
+                host = kChEff;
+                for (int c = 0; c < kNumChannels; ++c)
+                    if (rep[c].size() < rep[host].size()) host = c;
+                used[host] = true;
+                tl[host].assign(rep[host].size(), full);
+            }
+            for (auto& m : tl[host]) m &= base;
+        }
+        TreeRec& R = recs[size_t(t)];
+        for (int c = 0; c < kNumChannels; ++c) {
+            if (!used[c]) {
+                R.lut[c] = 0;  // all-ones table
+                continue;
+            }
+            auto it = dedupe.find(tl[c]);
+            if (it != dedupe.end()) {
+                R.lut[c] = it->second;
+            } else {
+                const uint32_t off = uint32_t(lut.size());
+                lut.insert(lut.end(), tl[c].begin(), tl[c].end());
+                dedupe.emplace(tl[c], off);
+                R.lut[c] = off;
+            }
+            S.lut_entries += int64_t(tl[c].size());
+        }
+        R.leaf_base = uint32_t(leaves.size());
+        leaves.insert(leaves.end(), lv.begin(), lv.end());
+        S.total_leaves += int(lv.size());
+        S.max_leaves = std::max(S.max_leaves, int(lv.size()));
     }
 
-    // ---- bin tables
+    // ---- blob
     ScoreHdr H{};
     H.K = PH.K;
     H.fnv_prefix = PH.fnv_prefix;
     H.base = F.base;
     H.lr = F.lr;
     H.ntrees = int32_t(T);
-    H.max_depth = S.max_depth;
+    H.mask_bits = mbits;
     for (int d = 0; d < 3; ++d) {
         H.nt[d] = PH.nt[d];
         H.nd[d] = PH.nd[d];
     }
     H.ndk = PH.ndk;
     H.ngrid = PH.ngrid;
-    for (int j = 0; j < 16; ++j) H.bconst[j] = 1;
-    H.bconst[0] = bin_of(0, PH.f0);
-    H.bconst[3] = bin_of(3, PH.f3);
-
-    std::vector<uint16_t> bgrid(P.grid.size());
-    std::vector<double> grida(P.grid.size());
-    for (size_t g = 0; g < P.grid.size(); ++g) {
-        bgrid[g] = uint16_t(bin_of(11, P.grid[g].lg_grid) | (bin_of(14, P.grid[g].lg_active) << 8));
-        grida[g] = P.grid[g].a;
-    }
-    std::vector<uint16_t> bint2(P.int2.size());
-    for (size_t i = 0; i < P.int2.size(); ++i)
-        bint2[i] = uint16_t(bin_of(1, P.int2[i]) | (bin_of(4, P.int2[i]) << 8));
-    std::vector<uint32_t> bglb2(P.glb2.size());
-    for (size_t i = 0; i < P.glb2.size(); ++i)
-        bglb2[i] = uint32_t(bin_of(2, P.glb2[i].lg_glb_ld)) | (uint32_t(bin_of(5, P.glb2[i].lg_glb_ld)) << 8) |
-                   (uint32_t(bin_of(15, P.glb2[i].f15)) << 16);
-    std::vector<uint8_t> bblock(1025 + 15, 1);
-    std::vector<double> blockb(1025);
-    for (int b = 0; b <= 1024; ++b) {
-        bblock[b] = bin_of(12, P.block[b].lg_block);
-        blockb[b] = P.block[b].b;
-    }
-    std::vector<uint8_t> bptn(P.ptn.size());
-    for (size_t i = 0; i < P.ptn.size(); ++i) bptn[i] = bin_of(9, P.ptn[i]);
-    std::vector<uint8_t> bsteps(P.steps.size());
-    for (size_t i = 0; i < P.steps.size(); ++i) bsteps[i] = bin_of(10, P.steps[i]);
-    uint8_t small[32];
-    std::memset(small, 1, sizeof(small));
-    for (int c = 0; c < 4; ++c) small[c] = bin_of(8, P.lvl[c]);
-    for (int u = 0; u < 16; ++u) small[4 + u] = bin_of(7, double(int64_t(1) << u));
-    for (int v = 0; v < 3; ++v) small[20 + v] = bin_of(6, double(1 << v));
-    std::vector<double> f13;
-    for (int rho : R[13]) f13.push_back(V[13][size_t(rho)]);
-    H.n13 = int32_t(f13.size());
+    H.n13 = int32_t(f13b.size());
+    std::vector<double> grida(P.grid.size()), blockb(1025);
+    for (size_t g = 0; g < P.grid.size(); ++g) grida[g] = P.grid[g].a;
+    for (int b2 = 0; b2 <= 1024; ++b2) blockb[size_t(b2)] = P.block[size_t(b2)].b;
 
     blob->assign(align16(sizeof(ScoreHdr)), 0);
     for (int d = 0; d < 3; ++d) H.off_til[d] = put(*blob, P.til[d].data(), P.til[d].size());
     H.off_divk = put(*blob, P.divk.data(), P.divk.size());
     H.off_gridkey = put(*blob, P.gridkey.data(), P.gridkey.size());
-    H.off_bgrid = put(*blob, bgrid.data(), bgrid.size());
     H.off_grida = put(*blob, grida.data(), grida.size());
-    H.off_bint2 = put(*blob, bint2.data(), bint2.size());
-    H.off_bglb2 = put(*blob, bglb2.data(), bglb2.size());
-    H.off_bblock = put(*blob, bblock.data(), bblock.size());
     H.off_blockb = put(*blob, blockb.data(), blockb.size());
-    H.off_bptn = put(*blob, bptn.data(), bptn.size());
-    H.off_bsteps = put(*blob, bsteps.data(), bsteps.size());
-    H.off_small = put(*blob, small, 32);
-    H.off_f13 = put(*blob, f13.data(), f13.size());
-    H.off_meta = put(*blob, meta.data(), meta.size());
-    H.off_nodes = put(*blob, nodes.data(), nodes.size());
+    H.off_f13 = put(*blob, f13b.data(), f13b.size());
+    for (int c = 0; c < kNumChannels; ++c) H.off_cls[c] = put(*blob, cls[c].data(), cls[c].size());
+    H.off_trees = put(*blob, recs.data(), recs.size());
+    if (mbits == 32) {
+        std::vector<uint32_t> l32(lut.begin(), lut.end());
+        H.off_lut = put(*blob, l32.data(), l32.size());
+    } else {
+        H.off_lut = put(*blob, lut.data(), lut.size());
+    }
     H.off_leaves = put(*blob, leaves.data(), leaves.size());
     blob->resize(align16(blob->size()));
     H.total = uint32_t(blob->size());

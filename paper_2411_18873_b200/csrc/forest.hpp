@@ -25,9 +25,10 @@ etune_status build_predict_blob(const ForestHost& F, std::vector<uint8_t>* blob,
 struct ScoreStats {
     int64_t internal_nodes_in = 0;   // reference interior nodes
     int64_t tests_folded = 0;        // tests resolved at compile time for this op
-    int64_t perfect_slots = 0;       // emitted test words
-    int max_depth = 0;
-    int sum_depth = 0;
+    int64_t lut_entries = 0;         // class->mask entries referenced by trees
+    int max_leaves = 0;
+    int total_leaves = 0;
+    int channels_used = 0;           // bitmask of channels still tested after folding
 };
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
                               ScoreStats* stats, std::string* err);

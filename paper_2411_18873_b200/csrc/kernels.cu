@@ -19,6 +19,7 @@
 
 #include "etune_internal.hpp"
 #include "kernels.hpp"
+#include "score_core.hpp"
 
 namespace etune_b200 {
 
@@ -292,89 +293,34 @@ __global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __res
 }
 
 // ------------------------------------------------------------------- score
-// Fused feature bins -> forest -> prediction.  Per thread: one candidate at a time.
-__global__ void __launch_bounds__(kThreads, 2) score_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
-                                                           const uint64_t* __restrict__ genome, int64_t n,
-                                                           double* __restrict__ pred, uint64_t* __restrict__ ids) {
+// Fused feature classes -> forest (per-tree leaf-mask tables) -> prediction (+ id).
+// One candidate per thread per iteration; the whole compiled forest lives in smem.
+constexpr int kScoreThreads = 512;
+
+template <typename M>
+__global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
+                                                                const uint64_t* __restrict__ genome, int64_t n,
+                                                                double* __restrict__ pred,
+                                                                uint64_t* __restrict__ ids) {
     extern __shared__ int4 smem[];
     stage(gblob, bytes, smem);
     __syncthreads();
     const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
     const ScoreHdr& H = *reinterpret_cast<const ScoreHdr*>(S);
-    const TilingRec* T0 = at<TilingRec>(S, H.off_til[0]);
-    const TilingRec* T1 = at<TilingRec>(S, H.off_til[1]);
-    const TilingRec* T2 = at<TilingRec>(S, H.off_til[2]);
-    const uint16_t* gridkey = at<uint16_t>(S, H.off_gridkey);
-    const uint16_t* bgrid = at<uint16_t>(S, H.off_bgrid);
-    const double* grida = at<double>(S, H.off_grida);
-    const uint16_t* bint2 = at<uint16_t>(S, H.off_bint2);
-    const uint32_t* bglb2 = at<uint32_t>(S, H.off_bglb2);
-    const uint8_t* bblock = at<uint8_t>(S, H.off_bblock);
-    const double* blockb = at<double>(S, H.off_blockb);
-    const uint8_t* bptn = at<uint8_t>(S, H.off_bptn);
-    const uint8_t* bsteps = at<uint8_t>(S, H.off_bsteps);
-    const uint8_t* small = at<uint8_t>(S, H.off_small);
-    const double* f13 = at<double>(S, H.off_f13);
-    const int4* meta = at<int4>(S, H.off_meta);
-    const uint32_t* nodes = at<uint32_t>(S, H.off_nodes);
-    const double* leaves = at<double>(S, H.off_leaves);
-    const int nd1 = H.nd[1], nd2 = H.nd[2], n13 = H.n13, ntrees = H.ntrees;
-    const uint32_t c0 = H.bconst[0], c3 = H.bconst[3];
-    const double base = H.base, lr = H.lr;
     const int64_t* divk = at<int64_t>(S, H.off_divk);
     const uint64_t prefix = H.fnv_prefix;
-
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const Genome x = genome_unpack(__ldg(genome + i));
-        const TilingRec r0 = T0[x.t0], r1 = T1[x.t1], r2 = T2[x.t2];
-        uint32_t block = r0.threads * r1.threads * r2.threads;
-        block = block <= 1024u ? block : 1024u;
-        const uint32_t gk = gridkey[(r0.db * nd1 + r1.db) * nd2 + r2.db];
-        const uint32_t lv = (r0.pt > 1) + (r1.pt > 1) + (r2.pt > 1);
-        const uint32_t bi = bint2[r1.dpt * nd2 + r2.dpt];
-        const uint32_t bg = bglb2[r1.dbt * nd2 + r2.dbt];
-        const uint32_t bgr = bgrid[gk];
-        const double x13 = __dmul_rn(grida[gk], blockb[block]);
-        int lo = 0, hi = n13;  // #boundaries <= x13
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (f13[mid] <= x13) lo = mid + 1;
-            else hi = mid;
-        }
-        const uint32_t b13 = uint32_t(lo) + 1u;
-        // bytes j of (R0,R1,R2,R3) = bin'(feature j)
-        const uint32_t R0 = c0 | ((bi & 0xffu) << 8) | ((bg & 0xffu) << 16) | (c3 << 24);
-        const uint32_t R1 = (bi >> 8) | (bg & 0xff00u) | (uint32_t(small[20 + x.v]) << 16) |
-                            (uint32_t(small[4 + x.u]) << 24);
-        const uint32_t R2 = uint32_t(small[lv]) | (uint32_t(bptn[r2.dpt]) << 8) | (uint32_t(bsteps[x.k]) << 16) |
-                            ((bgr & 0xffu) << 24);
-        const uint32_t R3 = uint32_t(bblock[block]) | (b13 << 8) | ((bgr & 0xff00u) << 8) | ((bg >> 16) << 24);
-
-        double sum = 0.0;
-        for (int t = 0; t < ntrees; ++t) {
-            const int4 m = meta[t];  // node_base, leaf_base, depth
-            const uint32_t* nd = nodes + m.x;
-            uint32_t s = 0;
-            for (int l = 0; l < m.z; ++l) {
-                const uint32_t w = nd[s];
-                const bool hiPair = (w & 0x10000u) != 0;
-                const uint32_t a = hiPair ? R2 : R0;
-                const uint32_t b = hiPair ? R3 : R1;
-                const uint32_t xb = __byte_perm(a, b, w);
-                s = 2u * s + 1u + (xb >= w ? 1u : 0u);
-            }
-            sum = __dadd_rn(sum, leaves[m.y + int(s) - ((1 << m.z) - 1)]);
-        }
-        const double p = __dadd_rn(base, __dmul_rn(lr, sum));  // energy_model.cpp:248
-        pred[i] = (1e-6 < p) ? p : 1e-6;
+        const CandClasses cc = candidate_classes(S, H, __ldg(genome + i));
+        const double sum = forest_sum<M>(S, H, cc.c);
+        pred[i] = finish_prediction(H, sum);
         if (ids) {
             Knobs c;
-            c.r[0] = r0;
-            c.r[1] = r1;
-            c.r[2] = r2;
-            c.k_tile = divk[x.k];
-            c.unroll = 1u << x.u;
-            c.vec = 1u << x.v;
+            c.r[0] = cc.r[0];
+            c.r[1] = cc.r[1];
+            c.r[2] = cc.r[2];
+            c.k_tile = divk[cc.x.k];
+            c.unroll = 1u << cc.x.u;
+            c.vec = 1u << cc.x.v;
             ids[i] = candidate_hash(prefix, c);
         }
     }
@@ -470,18 +416,28 @@ cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
     return launch_plan_kernel(features_kernel, c, d_plan, bytes, n, d_genome, n, d_feat, d_ids);
 }
 
-cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
-                         int64_t n, double* d_pred, uint64_t* d_ids) {
-    if (n <= 0) return cudaSuccess;
-    cudaError_t e = cudaFuncSetAttribute(score_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
+template <typename M>
+cudaError_t launch_score_t(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
+                           int64_t n, double* d_pred, uint64_t* d_ids) {
+    cudaError_t e = cudaFuncSetAttribute(score_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel, kThreads, bytes);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<M>, kScoreThreads, bytes);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    score_kernel<<<grid_for(c, n, per_sm), kThreads, bytes, c.stream>>>(d_score, bytes, d_genome, n, d_pred, d_ids);
+    const int64_t want = (n + kScoreThreads - 1) / kScoreThreads;
+    const int64_t cap = int64_t(c.sm_count) * per_sm;
+    const int grid = int(want < cap ? want : cap);
+    score_kernel<M><<<grid, kScoreThreads, bytes, c.stream>>>(d_score, bytes, d_genome, n, d_pred, d_ids);
     note_launches(1);
     return cudaGetLastError();
+}
+
+cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
+                         int64_t n, double* d_pred, uint64_t* d_ids, int mask_bits) {
+    if (n <= 0) return cudaSuccess;
+    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids)
+                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids);
 }
 
 cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_blob, uint32_t /*bytes*/, const double* d_feat,

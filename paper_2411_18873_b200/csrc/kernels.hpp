@@ -30,7 +30,8 @@ cudaError_t launch_counters(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                             const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
-                         const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids);
+                         const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
+                         int mask_bits);
 cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_pred_blob, uint32_t bytes,
                            const double* d_feat, int64_t n, double* d_pred);
 

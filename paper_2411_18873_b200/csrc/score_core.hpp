@@ -1,0 +1,108 @@
+// Per-candidate scoring core shared by score_kernel (kernels.cu).  Written as a
+// __host__ __device__ template only so that tests/cpp/score_core_test.cpp can check
+// the forest compiler's tables on a CPU without a GPU; the product never calls it on
+// the host (libetune_cuda.so has no host scoring path).
+#pragma once
+
+#include <cstdint>
+
+#include "etune_internal.hpp"
+
+#if !defined(__CUDACC__) && !defined(__forceinline__)
+#define __forceinline__ inline
+#endif
+
+#if defined(__CUDA_ARCH__)
+#define ETUNE_DMUL(a, b) __dmul_rn(a, b)
+#define ETUNE_DADD(a, b) __dadd_rn(a, b)
+#define ETUNE_FFS32(x) (__ffs(int(x)) - 1)
+#define ETUNE_FFS64(x) (__ffsll((long long)(x)) - 1)
+#else
+#define ETUNE_DMUL(a, b) ((a) * (b))
+#define ETUNE_DADD(a, b) ((a) + (b))
+#define ETUNE_FFS32(x) (__builtin_ffs(int(x)) - 1)
+#define ETUNE_FFS64(x) (__builtin_ffsll((long long)(x)) - 1)
+#endif
+
+namespace etune_b200 {
+
+template <typename T>
+__host__ __device__ __forceinline__ const T* blob_at(const uint8_t* base, uint32_t off) {
+    return reinterpret_cast<const T*>(base + off);
+}
+
+// Class of every channel for one genome (see Channel in etune_internal.hpp), plus the
+// tiling records the candidate id needs.
+struct CandClasses {
+    uint32_t c[kNumChannels];
+    TilingRec r[3];
+    Genome x;
+};
+
+__host__ __device__ __forceinline__ CandClasses candidate_classes(const uint8_t* S, const ScoreHdr& H, uint64_t g) {
+    CandClasses o;
+    o.x = genome_unpack(g);
+    o.r[0] = blob_at<TilingRec>(S, H.off_til[0])[o.x.t0];
+    o.r[1] = blob_at<TilingRec>(S, H.off_til[1])[o.x.t1];
+    o.r[2] = blob_at<TilingRec>(S, H.off_til[2])[o.x.t2];
+    const int nd1 = H.nd[1], nd2 = H.nd[2];
+    uint32_t block = o.r[0].threads * o.r[1].threads * o.r[2].threads;
+    block = block <= 1024u ? block : 1024u;
+    const uint32_t gk = blob_at<uint16_t>(S, H.off_gridkey)[(o.r[0].db * nd1 + o.r[1].db) * nd2 + o.r[2].db];
+    const uint32_t lv = (o.r[0].pt > 1) + (o.r[1].pt > 1) + (o.r[2].pt > 1);
+    o.c[kChInt] = blob_at<uint8_t>(S, H.off_cls[kChInt])[o.r[1].dpt * nd2 + o.r[2].dpt];
+    o.c[kChGlb] = blob_at<uint8_t>(S, H.off_cls[kChGlb])[o.r[1].dbt * nd2 + o.r[2].dbt];
+    o.c[kChGrid] = blob_at<uint8_t>(S, H.off_cls[kChGrid])[gk];
+    o.c[kChBlk] = blob_at<uint8_t>(S, H.off_cls[kChBlk])[block];
+    // f13 = (active/sms) * min(1, block/256) (counters.cpp:44-47), exact IEEE product
+    const double x13 = ETUNE_DMUL(blob_at<double>(S, H.off_grida)[gk], blob_at<double>(S, H.off_blockb)[block]);
+    const double* f13 = blob_at<double>(S, H.off_f13);
+    int lo = 0, hi = H.n13;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (f13[mid] <= x13) lo = mid + 1;
+        else hi = mid;
+    }
+    o.c[kChEff] = uint32_t(lo);
+    o.c[kChKuv] = blob_at<uint8_t>(S, H.off_cls[kChKuv])[(o.x.k * 16u + o.x.u) * 4u + o.x.v];
+    o.c[kChLvp] = blob_at<uint8_t>(S, H.off_cls[kChLvp])[lv * nd2 + o.r[2].dpt];
+    return o;
+}
+
+// Sum of leaf values over trees [0, ntrees) in tree order (energy_model.cpp:247).
+template <typename M>
+__host__ __device__ __forceinline__ double forest_sum(const uint8_t* S, const ScoreHdr& H, const uint32_t* c) {
+    const TreeRec* trees = blob_at<TreeRec>(S, H.off_trees);
+    const M* lut = blob_at<M>(S, H.off_lut);
+    const double* leaves = blob_at<double>(S, H.off_leaves);
+    double sum = 0.0;
+    int t = 0;
+    // two trees per iteration: 14 independent table reads in flight per thread
+    for (; t + 1 < H.ntrees; t += 2) {
+        const TreeRec a = trees[t];
+        const TreeRec b = trees[t + 1];
+        const M ma = lut[a.lut[0] + c[0]] & lut[a.lut[1] + c[1]] & lut[a.lut[2] + c[2]] & lut[a.lut[3] + c[3]] &
+                     lut[a.lut[4] + c[4]] & lut[a.lut[5] + c[5]] & lut[a.lut[6] + c[6]];
+        const M mb = lut[b.lut[0] + c[0]] & lut[b.lut[1] + c[1]] & lut[b.lut[2] + c[2]] & lut[b.lut[3] + c[3]] &
+                     lut[b.lut[4] + c[4]] & lut[b.lut[5] + c[5]] & lut[b.lut[6] + c[6]];
+        const int la = sizeof(M) == 4 ? ETUNE_FFS32(ma) : ETUNE_FFS64(ma);
+        const int lb = sizeof(M) == 4 ? ETUNE_FFS32(mb) : ETUNE_FFS64(mb);
+        sum = ETUNE_DADD(sum, leaves[a.leaf_base + la]);
+        sum = ETUNE_DADD(sum, leaves[b.leaf_base + lb]);
+    }
+    for (; t < H.ntrees; ++t) {
+        const TreeRec a = trees[t];
+        const M ma = lut[a.lut[0] + c[0]] & lut[a.lut[1] + c[1]] & lut[a.lut[2] + c[2]] & lut[a.lut[3] + c[3]] &
+                     lut[a.lut[4] + c[4]] & lut[a.lut[5] + c[5]] & lut[a.lut[6] + c[6]];
+        const int la = sizeof(M) == 4 ? ETUNE_FFS32(ma) : ETUNE_FFS64(ma);
+        sum = ETUNE_DADD(sum, leaves[a.leaf_base + la]);
+    }
+    return sum;
+}
+
+__host__ __device__ __forceinline__ double finish_prediction(const ScoreHdr& H, double sum) {
+    const double p = ETUNE_DADD(H.base, ETUNE_DMUL(H.lr, sum));  // energy_model.cpp:248
+    return (1e-6 < p) ? p : 1e-6;                                // std::max(kPredictionFloor, p)
+}
+
+}  // namespace etune_b200

@@ -81,7 +81,7 @@ def test_full_space_vs_oracle(oracle, ctx, capi, text):
                                   "mm:8,384,384,64"])
 def test_large_samples_vs_oracle(oracle, ctx, capi, text):
     op = parse_op(text)
-    s, ids = oracle.sample_random(op, 20000, 42)
+    s, ids = oracle.sample_random(op, min(20000, oracle.count(op)), 42)
     plan = capi.Plan(ctx, op, num_sms=148)
     g = plan.encode(dev(s))
     f, dids = plan.features(g, with_ids=True)
