@@ -136,12 +136,13 @@ def test_score_other_operator_forest(golden, oracle, ctx, capi):
 
 
 def test_trained_here_forest(oracle, ctx, capi):
-    """A deeper forest (depth 8) trained by the oracle on fresh data."""
+    """Full depth-6 trees (up to 64 leaves: the 64-bit leaf-mask path), trained by the
+    oracle on fresh data with min_leaf_weight 0."""
     op = parse_op("mm:1,256,512,384")
     s, _ = oracle.sample_random(op, 1500, 3)
     f = oracle.features(op, s)
     e = 1.0 + (f[:, 2] * 0.3 + f[:, 12] * 0.1 + f[:, 6]) % 2.7
-    fl, _, _ = oracle.train(f, e, num_trees=40, max_depth=8)
+    fl, _, _ = oracle.train(f, e, num_trees=40, max_depth=6, min_leaf_weight=0.0)
     pop, _ = oracle.sample_random(op, 30000, 4)
     ref = oracle.predict(fl, oracle.features(op, pop))
     plan = capi.Plan(ctx, op)
