@@ -47,6 +47,7 @@ struct CompiledScore {
     uint8_t* d_blob = nullptr;
     uint32_t bytes = 0;
     int mask_bits = 32;
+    std::shared_ptr<ForestParams> params;  // tree records, passed by value to the kernel
     ScoreStats stats;
 };
 
@@ -125,7 +126,11 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     CU(cudaMemcpyAsync(cs.d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaStreamSynchronize(f->ctx->stream));
     cs.bytes = uint32_t(blob.size());
-    cs.mask_bits = reinterpret_cast<const ScoreHdr*>(blob.data())->mask_bits;
+    const ScoreHdr* hdr = reinterpret_cast<const ScoreHdr*>(blob.data());
+    cs.mask_bits = hdr->mask_bits;
+    cs.params = std::make_shared<ForestParams>();
+    std::memset(cs.params.get(), 0, sizeof(ForestParams));
+    std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;
@@ -369,7 +374,7 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
-    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits));
+    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params));
     return ETUNE_OK;
 }
 
@@ -397,7 +402,7 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         CU(cudaMemcpyAsync(d_sched, h_sched + lo, size_t(m) * sizeof(etune_schedule), cudaMemcpyHostToDevice,
                            c->stream));
         CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, m, d_gen, lo));
-        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_gen, m, d_pred, h_ids ? d_ids : nullptr, cs->mask_bits));
+        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_gen, m, d_pred, h_ids ? d_ids : nullptr, cs->mask_bits, *cs->params));
         CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
         if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
     }

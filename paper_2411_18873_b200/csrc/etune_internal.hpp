@@ -123,10 +123,14 @@ enum Channel : int {
     kNumChannels = 7
 };
 
-struct TreeRec {          // 32 bytes, read warp-uniformly
+struct TreeRec {          // 32 bytes, read warp-uniformly (kernel-parameter constant bank)
     uint32_t lut[7];      // mask-word index of this tree's LUT per channel (shared all-ones
                           // table when the tree does not test the channel)
-    uint32_t leaf_base;   // index into leaves[]
+    uint32_t meta;        // leaf_base (index into leaves[], bits 0-23) | used-channel mask << 24
+};
+constexpr int kMaxParamTrees = 1000;  // 32000 B of kernel parameters (CUDA 12.1+: 32764 max)
+struct ForestParams {
+    TreeRec rec[kMaxParamTrees];
 };
 
 struct ScoreHdr {

@@ -209,6 +209,10 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
 
     // ---- per tree: leaves in order, left-subtree masks, per-channel LUTs
     const int64_t T = F.num_trees();
+    if (T > kMaxParamTrees) {
+        *err = "more than 1000 trees; not supported by this build";
+        return ETUNE_ERR_UNSUPPORTED;
+    }
     int max_leaves = 1;
     for (int64_t t = 0; t < T; ++t) {
         int nl = 0;
@@ -322,7 +326,13 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
             }
             S.lut_entries += int64_t(tl[c].size());
         }
-        R.leaf_base = uint32_t(leaves.size());
+        uint32_t used_mask = 0;
+        for (int c = 0; c < kNumChannels; ++c) used_mask |= uint32_t(used[c]) << c;
+        if (leaves.size() >= (1u << 24)) {
+            *err = "forest has more than 2^24 leaves";
+            return ETUNE_ERR_UNSUPPORTED;
+        }
+        R.meta = uint32_t(leaves.size()) | (used_mask << 24);
         leaves.insert(leaves.end(), lv.begin(), lv.end());
         S.total_leaves += int(lv.size());
         S.max_leaves = std::max(S.max_leaves, int(lv.size()));

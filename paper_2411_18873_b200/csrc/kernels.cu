@@ -301,7 +301,8 @@ template <typename M>
 __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
                                                                 const uint64_t* __restrict__ genome, int64_t n,
                                                                 double* __restrict__ pred,
-                                                                uint64_t* __restrict__ ids) {
+                                                                uint64_t* __restrict__ ids,
+                                                                const __grid_constant__ ForestParams fp) {
     extern __shared__ int4 smem[];
     stage(gblob, bytes, smem);
     __syncthreads();
@@ -311,7 +312,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
     const uint64_t prefix = H.fnv_prefix;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const CandClasses cc = candidate_classes(S, H, __ldg(genome + i));
-        const double sum = forest_sum<M>(S, H, cc.c);
+        const double sum = forest_sum<M>(S, H, fp.rec, cc.c);
         pred[i] = finish_prediction(H, sum);
         if (ids) {
             Knobs c;
@@ -418,7 +419,7 @@ cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
 
 template <typename M>
 cudaError_t launch_score_t(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
-                           int64_t n, double* d_pred, uint64_t* d_ids) {
+                           int64_t n, double* d_pred, uint64_t* d_ids, const ForestParams& fp) {
     cudaError_t e = cudaFuncSetAttribute(score_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
@@ -428,16 +429,16 @@ cudaError_t launch_score_t(const LaunchCtx& c, const uint8_t* d_score, uint32_t 
     const int64_t want = (n + kScoreThreads - 1) / kScoreThreads;
     const int64_t cap = int64_t(c.sm_count) * per_sm;
     const int grid = int(want < cap ? want : cap);
-    score_kernel<M><<<grid, kScoreThreads, bytes, c.stream>>>(d_score, bytes, d_genome, n, d_pred, d_ids);
+    score_kernel<M><<<grid, kScoreThreads, bytes, c.stream>>>(d_score, bytes, d_genome, n, d_pred, d_ids, fp);
     note_launches(1);
     return cudaGetLastError();
 }
 
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
-                         int64_t n, double* d_pred, uint64_t* d_ids, int mask_bits) {
+                         int64_t n, double* d_pred, uint64_t* d_ids, int mask_bits, const ForestParams& fp) {
     if (n <= 0) return cudaSuccess;
-    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids)
-                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids);
+    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp)
+                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp);
 }
 
 cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_blob, uint32_t /*bytes*/, const double* d_feat,

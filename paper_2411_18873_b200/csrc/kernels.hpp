@@ -31,7 +31,7 @@ cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
                             const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
                          const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
-                         int mask_bits);
+                         int mask_bits, const ForestParams& fp);
 cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_pred_blob, uint32_t bytes,
                            const double* d_feat, int64_t n, double* d_pred);
 

@@ -70,32 +70,42 @@ __host__ __device__ __forceinline__ CandClasses candidate_classes(const uint8_t*
 }
 
 // Sum of leaf values over trees [0, ntrees) in tree order (energy_model.cpp:247).
+// `trees` is warp-uniform (on the device: the kernel-parameter constant bank);
+// channels a tree does not test are skipped by predication (no smem traffic).
 template <typename M>
-__host__ __device__ __forceinline__ double forest_sum(const uint8_t* S, const ScoreHdr& H, const uint32_t* c) {
-    const TreeRec* trees = blob_at<TreeRec>(S, H.off_trees);
+__host__ __device__ __forceinline__ M tree_mask(const TreeRec& r, const M* lut, const uint32_t* c) {
+    M m = ~M(0);
+#pragma unroll
+    for (int ch = 0; ch < kNumChannels; ++ch)
+        if ((r.meta >> (24 + ch)) & 1u) m &= lut[r.lut[ch] + c[ch]];
+    return m;
+}
+
+template <typename M>
+__host__ __device__ __forceinline__ double forest_sum(const uint8_t* S, const ScoreHdr& H, const TreeRec* trees,
+                                                      const uint32_t* c) {
     const M* lut = blob_at<M>(S, H.off_lut);
     const double* leaves = blob_at<double>(S, H.off_leaves);
     double sum = 0.0;
     int t = 0;
-    // two trees per iteration: 14 independent table reads in flight per thread
+    // two trees per iteration: their table reads are independent (ILP)
     for (; t + 1 < H.ntrees; t += 2) {
         const TreeRec a = trees[t];
         const TreeRec b = trees[t + 1];
-        const M ma = lut[a.lut[0] + c[0]] & lut[a.lut[1] + c[1]] & lut[a.lut[2] + c[2]] & lut[a.lut[3] + c[3]] &
-                     lut[a.lut[4] + c[4]] & lut[a.lut[5] + c[5]] & lut[a.lut[6] + c[6]];
-        const M mb = lut[b.lut[0] + c[0]] & lut[b.lut[1] + c[1]] & lut[b.lut[2] + c[2]] & lut[b.lut[3] + c[3]] &
-                     lut[b.lut[4] + c[4]] & lut[b.lut[5] + c[5]] & lut[b.lut[6] + c[6]];
+        const M ma = tree_mask<M>(a, lut, c);
+        const M mb = tree_mask<M>(b, lut, c);
         const int la = sizeof(M) == 4 ? ETUNE_FFS32(ma) : ETUNE_FFS64(ma);
         const int lb = sizeof(M) == 4 ? ETUNE_FFS32(mb) : ETUNE_FFS64(mb);
-        sum = ETUNE_DADD(sum, leaves[a.leaf_base + la]);
-        sum = ETUNE_DADD(sum, leaves[b.leaf_base + lb]);
+        const double va = leaves[(a.meta & 0xffffffu) + la];
+        const double vb = leaves[(b.meta & 0xffffffu) + lb];
+        sum = ETUNE_DADD(sum, va);
+        sum = ETUNE_DADD(sum, vb);
     }
     for (; t < H.ntrees; ++t) {
         const TreeRec a = trees[t];
-        const M ma = lut[a.lut[0] + c[0]] & lut[a.lut[1] + c[1]] & lut[a.lut[2] + c[2]] & lut[a.lut[3] + c[3]] &
-                     lut[a.lut[4] + c[4]] & lut[a.lut[5] + c[5]] & lut[a.lut[6] + c[6]];
+        const M ma = tree_mask<M>(a, lut, c);
         const int la = sizeof(M) == 4 ? ETUNE_FFS32(ma) : ETUNE_FFS64(ma);
-        sum = ETUNE_DADD(sum, leaves[a.leaf_base + la]);
+        sum = ETUNE_DADD(sum, leaves[(a.meta & 0xffffffu) + la]);
     }
     return sum;
 }

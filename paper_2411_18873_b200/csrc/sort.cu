@@ -1,19 +1,19 @@
 // Selection: the k lowest predictions under the total order (score asc, index asc).
 //
-// topk (no host synchronisation, everything decided on the device):
-//   1. prep      order-preserving 64-bit keys + AND/OR of all keys (which bits vary)
-//   2. hist      2048-bin histogram of the top 11 varying bits
-//   3. pick      one CTA: bucket d1 that holds the k-th key
-//   4. gather    keys of bucket d1 -> small buffer
-//   5. refine    one CTA: radix-select the exact k-th key T inside the bucket;
-//                need = k - #(key < T)   (ties at T are taken by ascending index)
-//   6. count     per tile: #(key < T), #(key == T)
-//   7. offsets   one CTA: exclusive scans over tiles
-//   8. scatter   stable compaction -> exactly k (key, index) pairs in index order
-//   9. order     sort the k pairs by (key, index): one-CTA bitonic for k <= 4096,
-//                else the stable LSD radix sort below (k is known on the host)
-// Warp-aggregated shared-memory atomics (__match_any_sync) keep heavily tied
-// predictions (thousands tie at the k-th value) from serialising.
+// topk = ONE cooperative kernel (grid-wide barriers between phases, no host sync):
+//   A. order-preserving 64-bit keys (cached in shared memory per CTA) + AND/OR of
+//      all keys, i.e. which bits vary at all
+//   B. MSB-first radix select of the exact k-th key T over the varying bits, 11-bit
+//      digits: per-CTA shared histograms (warp-aggregated atomics, so thousands of
+//      tied predictions - SURVEY H3 - do not serialise) -> global histogram -> every
+//      CTA derives the same digit
+//   C. per-CTA counts of key < T and key == T
+//   D. stable compaction in index order: all keys < T plus the `need` lowest-index
+//      keys == T -> exactly k (key, index) pairs
+//   E. CTA 0 bitonic-sorts the k pairs by (key, index)  [k <= 4096]
+// For k > 4096 the host follows with the stable LSD radix sort below (k is known on
+// the host, so no synchronisation is needed to decide).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -34,17 +34,14 @@ __device__ __forceinline__ uint64_t order_key(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-struct TopkState {
+constexpr int kCoopT = 1024;
+constexpr int kMaxPasses = 6;             // 11-bit digits over <= 64 varying bits
+constexpr int kSmemKeys = 24 * 1024;      // keys cached per CTA (192 KB)
+
+struct TopkWork {
     unsigned long long andor[2];
-    unsigned long long T;        // exact k-th key
-    unsigned int hist[kBins];
-    unsigned int d1;             // bucket of the k-th key
-    unsigned int below1;         // #keys in buckets < d1
-    unsigned int bucket_n;       // gathered keys
-    unsigned int below;          // #(key < T)
-    unsigned int need;           // #(key == T) to take, lowest indices first
-    int shift;                   // digit = (key >> shift) & 2047
-    unsigned int pad[2];
+    unsigned int hist[kMaxPasses][kBins];
+    unsigned int cnt[2][1024];            // per-CTA (lt, eq) counts
 };
 
 // warp-aggregated shared atomic add of 1 to bin[d]
@@ -55,305 +52,205 @@ __device__ __forceinline__ void agg_inc(unsigned int* bin, unsigned d, bool vali
     if ((__ffs(peers) - 1) == int(threadIdx.x & 31)) atomicAdd(&bin[d], unsigned(__popc(peers)));
 }
 
-__global__ void __launch_bounds__(kT) prep_kernel(const double* __restrict__ score, int64_t n,
-                                                  uint64_t* __restrict__ keys, TopkState* st) {
+__device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* red) {
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    unsigned t = 0;
+    for (int w = 0; w < int(blockDim.x >> 5); ++w) t += red[w];
+    return t;
+}
+
+// Whole top-k in one cooperative launch (grid-wide barriers between phases).  Each CTA
+// owns one contiguous chunk of the scores, caches its keys in shared memory (when they
+// fit) and all CTAs derive identical radix decisions from the global histograms.
+__global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __restrict__ score, int64_t n, int64_t k,
+                                                              TopkWork* __restrict__ w, uint64_t* __restrict__ sel_key,
+                                                              uint32_t* __restrict__ sel_idx, int64_t* __restrict__ out,
+                                                              int cache_keys, int final_sort) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ unsigned long long skeys[];
+    __shared__ unsigned int h[kBins];
+    __shared__ unsigned int red[32];
+    __shared__ unsigned int s_pick[2];
+    const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
+    const int64_t chunk = (n + G - 1) / G;
+    const int64_t lo = int64_t(b) * chunk;
+    const int64_t hi = lo + chunk < n ? lo + chunk : n;
+    const int64_t m = hi > lo ? hi - lo : 0;
+    auto key_at = [&](int64_t j) -> uint64_t {  // j in [0, m)
+        return cache_keys ? skeys[j] : order_key(score[lo + j]);
+    };
+
+    // ---- phase A: keys (+ cache) and which bits vary
     uint64_t a = ~0ull, o = 0ull;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint64_t k = order_key(score[i]);
-        keys[i] = k;
-        a &= k;
-        o |= k;
+    for (int64_t j = tid; j < m; j += blockDim.x) {
+        const uint64_t key = order_key(score[lo + j]);
+        if (cache_keys) skeys[j] = key;
+        a &= key;
+        o |= key;
     }
     for (int s = 16; s > 0; s >>= 1) {
         a &= __shfl_xor_sync(0xffffffffu, a, s);
         o |= __shfl_xor_sync(0xffffffffu, o, s);
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAnd(&st->andor[0], a);
-        atomicOr(&st->andor[1], o);
-    }
-}
-
-__device__ __forceinline__ int top_shift(const TopkState* st) {
-    const uint64_t v = st->andor[0] ^ st->andor[1];
-    if (v == 0) return 64;  // all keys equal
-    const int hb = 63 - __clzll(static_cast<long long>(v));
-    return hb >= 10 ? hb - 10 : 0;
-}
-
-__global__ void __launch_bounds__(kT) hist_kernel(const uint64_t* __restrict__ keys, int64_t n, TopkState* st) {
-    __shared__ unsigned int h[kBins];
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x) h[i] = 0;
-    __syncthreads();
-    const int shift = top_shift(st);
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t nr = (n + stride - 1) / stride * stride;  // uniform trip count for the warp collectives
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < nr; i += stride) {
-        const bool v = i < n;
-        const unsigned d = (v && shift < 64) ? unsigned(keys[i] >> shift) & (kBins - 1) : 0u;
-        agg_inc(h, d, v);
+    __shared__ unsigned long long ra[32], ro[32];
+    if ((tid & 31) == 0) {
+        ra[tid >> 5] = a;
+        ro[tid >> 5] = o;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < kBins; i += blockDim.x)
-        if (h[i]) atomicAdd(&st->hist[i], h[i]);
-}
-
-// one CTA of 1024: find the bucket holding the k-th smallest key
-__global__ void __launch_bounds__(1024) pick_kernel(int64_t k, TopkState* st) {
-    __shared__ unsigned int part[1024];
-    const int t = threadIdx.x;
-    const unsigned a = st->hist[2 * t], b = st->hist[2 * t + 1];
-    part[t] = a + b;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        const unsigned v = t >= off ? part[t - off] : 0u;
-        __syncthreads();
-        part[t] += v;
-        __syncthreads();
-    }
-    const unsigned before = part[t] - a - b;  // exclusive
-    const unsigned kk = unsigned(k);
-    if (before < kk && before + a >= kk) {
-        st->d1 = 2 * t;
-        st->below1 = before;
-    } else if (before + a < kk && before + a + b >= kk) {
-        st->d1 = 2 * t + 1;
-        st->below1 = before + a;
-    }
-    if (t == 0) {
-        st->shift = top_shift(st);
-        st->bucket_n = 0;
-    }
-}
-
-__global__ void __launch_bounds__(kT) gather_kernel(const uint64_t* __restrict__ keys, int64_t n, TopkState* st,
-                                                    uint64_t* __restrict__ bucket) {
-    const int shift = st->shift;
-    const unsigned d1 = st->d1;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const uint64_t key = keys[i];
-        const unsigned d = shift < 64 ? unsigned(key >> shift) & (kBins - 1) : 0u;
-        if (d == d1) bucket[atomicAdd(&st->bucket_n, 1u)] = key;
-    }
-}
-
-// one CTA: exact k-th key inside the bucket by 8-bit MSB radix select on the bits
-// below the first digit.
-__global__ void __launch_bounds__(1024) refine_kernel(const uint64_t* __restrict__ bucket, int64_t k, TopkState* st) {
-    __shared__ unsigned int h[256];
-    __shared__ unsigned long long s_prefix;
-    __shared__ unsigned int s_rem, s_dig;
-    const int t = threadIdx.x;
-    const int shift0 = st->shift;
-    const unsigned m = st->bucket_n;
-    unsigned long long prefix = 0;  // bits below shift0 fixed so far
-    unsigned rem = unsigned(k) - st->below1;  // rank (1-based) of the target within the bucket
-    int bit = shift0;                         // next digit covers [bit-8, bit)
-    if (shift0 >= 64) {  // all keys identical
-        if (t == 0) {
-            st->T = st->andor[0];
-            st->below = 0;
-            st->need = unsigned(k);
+    if (tid == 0) {
+        for (int i = 1; i < int(blockDim.x >> 5); ++i) {
+            a &= ra[i];
+            o |= ro[i];
         }
-        return;
+        atomicAnd(&w->andor[0], ra[0] & a);
+        atomicOr(&w->andor[1], ro[0] | o);
     }
-    const unsigned long long high = (st->andor[0] >> shift0 << shift0) |  // constant top bits ...
-                                    (static_cast<unsigned long long>(st->d1) << shift0);  // ... + bucket digit
-    // note: bits above shift0+11 are constant, so (andor[0] >> shift0 << shift0) keeps them
-    unsigned long long fixed_mask = ~0ull << shift0;
-    while (bit > 0) {
-        const int w = bit >= 8 ? 8 : bit;
-        const int lo = bit - w;
-        for (int i = t; i < 256; i += blockDim.x) h[i] = 0;
+    grid.sync();
+
+    // ---- phase B: radix select of the exact k-th key T (MSB first, 11-bit digits)
+    const uint64_t andv = w->andor[0], varying = andv ^ w->andor[1];
+    uint64_t prefix = andv;  // bits above `bit` fixed so far
+    unsigned rem = unsigned(k);  // 1-based rank of T inside the current prefix group
+    int bit = varying ? 64 - __clzll(static_cast<long long>(varying)) : 0;  // bits [0, bit) still open
+    for (int pass = 0; bit > 0; ++pass) {
+        const int width = bit >= 11 ? 11 : bit;
+        const int sh = bit - width;
+        const uint64_t himask = (bit >= 64) ? 0ull : (~0ull << bit);
+        for (int i = tid; i < kBins; i += blockDim.x) h[i] = 0;
         __syncthreads();
-        const unsigned mr = (m + 1023u) / 1024u * 1024u;
-        for (unsigned i = t; i < mr; i += blockDim.x) {
+        const int64_t mr = (m + blockDim.x - 1) / blockDim.x * blockDim.x;
+        for (int64_t j = tid; j < mr; j += blockDim.x) {
             bool v = false;
             unsigned d = 0;
-            if (i < m) {
-                const uint64_t key = bucket[i];
-                v = ((key & fixed_mask) & ~(~0ull << shift0)) == prefix;
-                d = unsigned(key >> lo) & ((1u << w) - 1u);
+            if (j < m) {
+                const uint64_t key = key_at(j);
+                v = (key & himask) == (prefix & himask);
+                d = unsigned(key >> sh) & ((1u << width) - 1u);
             }
             agg_inc(h, d, v);
         }
         __syncthreads();
-        if (t == 0) {
-            unsigned c = 0, dsel = 0;
-            for (unsigned d = 0; d < (1u << w); ++d) {
-                if (c + h[d] >= rem) {
-                    dsel = d;
-                    break;
+        for (int i = tid; i < (1 << width); i += blockDim.x)
+            if (h[i]) atomicAdd(&w->hist[pass][i], h[i]);
+        grid.sync();
+        // every CTA: pick the digit holding rank `rem` (identical result everywhere)
+        const int nb = 1 << width;
+        const int per = (nb + blockDim.x - 1) / blockDim.x;  // 1 or 2 bins per thread
+        unsigned mine = 0;
+        for (int q = 0; q < per; ++q) {
+            const int i = tid * per + q;
+            if (i < nb) mine += w->hist[pass][i];
+        }
+        // inclusive scan of `mine` over the block
+        unsigned x = mine;
+        for (int s = 1; s < 32; s <<= 1) {
+            const unsigned y = __shfl_up_sync(0xffffffffu, x, s);
+            if ((tid & 31) >= s) x += y;
+        }
+        if ((tid & 31) == 31) red[tid >> 5] = x;
+        __syncthreads();
+        unsigned wbase = 0;
+        for (int i = 0; i < (tid >> 5); ++i) wbase += red[i];
+        unsigned run = wbase + x - mine;  // exclusive
+        for (int q = 0; q < per; ++q) {
+            const int i = tid * per + q;
+            if (i < nb) {
+                const unsigned c = w->hist[pass][i];
+                if (run < rem && run + c >= rem) {
+                    s_pick[0] = unsigned(i);
+                    s_pick[1] = rem - run;
                 }
-                c += h[d];
+                run += c;
             }
-            s_rem = rem - c;
-            s_dig = dsel;
         }
         __syncthreads();
-        rem = s_rem;
-        prefix |= static_cast<unsigned long long>(s_dig) << lo;
-        fixed_mask |= ((1ull << w) - 1ull) << lo;
-        bit = lo;
+        prefix = (prefix & himask) | (uint64_t(s_pick[0]) << sh);  // bits below sh: still open
+        rem = s_pick[1];
+        bit = sh;
         __syncthreads();
     }
-    if (t == 0) {
-        const unsigned long long T = (high & (~0ull << shift0)) | prefix;
-        st->T = T;
-        (void)s_prefix;
-    }
-    __syncthreads();
-    // #bucket keys < T -> below = below1 + that
-    __shared__ unsigned int s_lt;
-    if (t == 0) s_lt = 0;
-    __syncthreads();
-    const unsigned long long T = st->T;
-    unsigned lt = 0;
-    for (unsigned i = t; i < m; i += blockDim.x) lt += bucket[i] < T;
-    for (int s = 16; s > 0; s >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, s);
-    if ((t & 31) == 0) atomicAdd(&s_lt, lt);
-    __syncthreads();
-    if (t == 0) {
-        st->below = st->below1 + s_lt;
-        st->need = unsigned(k) - st->below;
-    }
-}
-
-__global__ void __launch_bounds__(kT) count_kernel(const uint64_t* __restrict__ keys, int64_t n, const TopkState* st,
-                                                   unsigned int* __restrict__ lt_cnt, unsigned int* __restrict__ eq_cnt) {
-    const unsigned long long T = st->T;
+    const uint64_t T = prefix;
+    const unsigned need = rem;                // ties at T taken by ascending index
+    // ---- phase C: per-CTA counts
     unsigned lt = 0, eq = 0;
-    const int64_t base = int64_t(blockIdx.x) * kTile;
-    for (int r = 0; r < kTile / kT; ++r) {
-        const int64_t i = base + r * kT + threadIdx.x;
-        if (i < n) {
-            const uint64_t key = keys[i];
-            lt += key < T;
-            eq += key == T;
-        }
+    for (int64_t j = tid; j < m; j += blockDim.x) {
+        const uint64_t key = key_at(j);
+        lt += key < T;
+        eq += key == T;
     }
-    for (int s = 16; s > 0; s >>= 1) {
-        lt += __shfl_xor_sync(0xffffffffu, lt, s);
-        eq += __shfl_xor_sync(0xffffffffu, eq, s);
+    lt = block_sum(lt, red);
+    eq = block_sum(eq, red);
+    if (tid == 0) {
+        w->cnt[0][b] = lt;
+        w->cnt[1][b] = eq;
     }
-    __shared__ unsigned int sl[kT / 32], se[kT / 32];
-    if ((threadIdx.x & 31) == 0) {
-        sl[threadIdx.x >> 5] = lt;
-        se[threadIdx.x >> 5] = eq;
+    grid.sync();
+    // ---- phase D: stable compaction in index order
+    unsigned pl = 0, pe = 0;
+    for (int i = tid; i < b; i += blockDim.x) {
+        pl += w->cnt[0][i];
+        pe += w->cnt[1][i];
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned a = 0, b = 0;
-        for (int w = 0; w < kT / 32; ++w) {
-            a += sl[w];
-            b += se[w];
-        }
-        lt_cnt[blockIdx.x] = a;
-        eq_cnt[blockIdx.x] = b;
-    }
-}
-
-// exclusive scan of two u32 arrays of length m (one CTA of 1024, m arbitrary)
-__global__ void __launch_bounds__(1024) scan2_kernel(unsigned int* __restrict__ a, unsigned int* __restrict__ b, int m) {
-    __shared__ unsigned int pa[1024], pb[1024];
-    __shared__ unsigned int carry_a, carry_b;
-    const int t = threadIdx.x;
-    if (t == 0) carry_a = carry_b = 0;
-    __syncthreads();
-    for (int base = 0; base < m; base += 1024) {
-        const int i = base + t;
-        const unsigned va = i < m ? a[i] : 0u, vb = i < m ? b[i] : 0u;
-        pa[t] = va;
-        pb[t] = vb;
-        __syncthreads();
-        for (int off = 1; off < 1024; off <<= 1) {
-            const unsigned xa = t >= off ? pa[t - off] : 0u, xb = t >= off ? pb[t - off] : 0u;
-            __syncthreads();
-            pa[t] += xa;
-            pb[t] += xb;
-            __syncthreads();
-        }
-        if (i < m) {
-            a[i] = carry_a + pa[t] - va;
-            b[i] = carry_b + pb[t] - vb;
-        }
-        __syncthreads();
-        if (t == 1023) {
-            carry_a += pa[1023];
-            carry_b += pb[1023];
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void __launch_bounds__(kT) scatter_sel_kernel(const uint64_t* __restrict__ keys, int64_t n,
-                                                         const TopkState* st, const unsigned int* __restrict__ lt_off,
-                                                         const unsigned int* __restrict__ eq_off,
-                                                         uint64_t* __restrict__ out_key, uint32_t* __restrict__ out_idx) {
-    const unsigned long long T = st->T;
-    const unsigned need = st->need;
-    __shared__ unsigned int wl[kT / 32], we[kT / 32];
-    __shared__ unsigned int run_l, run_e;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) {
-        run_l = lt_off[blockIdx.x];
-        run_e = eq_off[blockIdx.x];
-    }
-    const int64_t base = int64_t(blockIdx.x) * kTile;
-    const unsigned ltmask = (1u << lane) - 1u;
-    for (int r = 0; r < kTile / kT; ++r) {
-        const int64_t i = base + r * kT + threadIdx.x;
+    pl = block_sum(pl, red);
+    pe = block_sum(pe, red);
+    __shared__ unsigned wl[32], we[32];
+    const int lane = tid & 31, warp = tid >> 5;
+    const unsigned ltm = (1u << lane) - 1u;
+    const int64_t mr = (m + blockDim.x - 1) / blockDim.x * blockDim.x;
+    for (int64_t j0 = 0; j0 < mr; j0 += blockDim.x) {
+        const int64_t j = j0 + tid;
         uint64_t key = 0;
-        bool islt = false, iseq = false;
-        if (i < n) {
-            key = keys[i];
-            islt = key < T;
-            iseq = key == T;
+        bool isl = false, ise = false;
+        if (j < m) {
+            key = key_at(j);
+            isl = key < T;
+            ise = key == T;
         }
-        const unsigned bl = __ballot_sync(0xffffffffu, islt), be = __ballot_sync(0xffffffffu, iseq);
+        const unsigned bl = __ballot_sync(0xffffffffu, isl), be = __ballot_sync(0xffffffffu, ise);
         if (lane == 0) {
             wl[warp] = __popc(bl);
             we[warp] = __popc(be);
         }
         __syncthreads();
-        unsigned pl = run_l, pe = run_e;
-        for (int w = 0; w < warp; ++w) {
-            pl += wl[w];
-            pe += we[w];
+        unsigned xl = pl, xe = pe;
+        for (int i = 0; i < warp; ++i) {
+            xl += wl[i];
+            xe += we[i];
         }
-        pl += __popc(bl & ltmask);
-        pe += __popc(be & ltmask);
-        if (islt || (iseq && pe < need)) {
-            const unsigned pos = pl + (pe < need ? pe : need);
-            out_key[pos] = key;
-            out_idx[pos] = uint32_t(i);
+        xl += __popc(bl & ltm);
+        xe += __popc(be & ltm);
+        if (isl || (ise && xe < need)) {
+            const unsigned pos = xl + (xe < need ? xe : need);
+            sel_key[pos] = key;
+            sel_idx[pos] = uint32_t(lo + j);
         }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            for (int w = 0; w < kT / 32; ++w) {
-                run_l += wl[w];
-                run_e += we[w];
-            }
+        for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+            pl += wl[i];
+            pe += we[i];
         }
         __syncthreads();
     }
-}
-
-// one CTA: bitonic sort of m <= kSmallSort (key, idx) pairs, write idx as int64
-__global__ void __launch_bounds__(1024) small_sort_kernel(const uint64_t* __restrict__ key, const uint32_t* __restrict__ idx,
-                                                         int m, int64_t* __restrict__ out) {
-    __shared__ unsigned long long sk[kSmallSort];
-    __shared__ unsigned int si[kSmallSort];
+    if (!final_sort) return;
+    grid.sync();
+    // ---- phase E: CTA 0 sorts the k pairs by (key, index) (bitonic, k <= kSmallSort)
+    if (b != 0) return;
+    unsigned long long* sk = skeys;
+    unsigned int* si = reinterpret_cast<unsigned int*>(skeys + kSmallSort);
     int P = 1;
-    while (P < m) P <<= 1;
-    for (int i = threadIdx.x; i < P; i += blockDim.x) {
-        sk[i] = i < m ? key[i] : ~0ull;
-        si[i] = i < m ? idx[i] : 0xffffffffu;
+    while (P < int(k)) P <<= 1;
+    for (int i = tid; i < P; i += blockDim.x) {
+        sk[i] = i < int(k) ? sel_key[i] : ~0ull;
+        si[i] = i < int(k) ? sel_idx[i] : 0xffffffffu;
     }
     __syncthreads();
     for (int size = 2; size <= P; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
+            for (int i = tid; i < P; i += blockDim.x) {
                 const int j = i ^ stride;
                 if (j > i) {
                     const bool up = (i & size) == 0;
@@ -371,7 +268,7 @@ __global__ void __launch_bounds__(1024) small_sort_kernel(const uint64_t* __rest
             __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < m; i += blockDim.x) out[i] = si[i];
+    for (int i = tid; i < int(k); i += blockDim.x) out[i] = si[i];
 }
 
 // ------------------------------------------------------- stable LSD radix sort
@@ -490,88 +387,70 @@ __global__ void widen_kernel(const uint32_t* __restrict__ vals, int64_t k, int64
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
-struct Scratch {
-    TopkState* st;
-    uint64_t* keys;
-    uint64_t* bucket;
-    unsigned int* lt;
-    unsigned int* eq;
-    uint64_t* sel_key[2];
-    uint32_t* sel_idx[2];
-    uint32_t* lsd_hist;
-};
-
-Scratch carve(void* p, int64_t n, int64_t k) {
-    const int64_t ntiles = (n + kTile - 1) / kTile;
-    const int64_t ktiles = (k + kTile - 1) / kTile;
-    char* c = static_cast<char*>(p);
-    Scratch s;
-    s.st = reinterpret_cast<TopkState*>(c);
-    c += al256(sizeof(TopkState));
-    s.keys = reinterpret_cast<uint64_t*>(c);
-    c += al256(8 * size_t(n));
-    s.bucket = reinterpret_cast<uint64_t*>(c);
-    c += al256(8 * size_t(n));
-    s.lt = reinterpret_cast<unsigned int*>(c);
-    c += al256(4 * size_t(ntiles));
-    s.eq = reinterpret_cast<unsigned int*>(c);
-    c += al256(4 * size_t(ntiles));
-    for (int b = 0; b < 2; ++b) {
-        s.sel_key[b] = reinterpret_cast<uint64_t*>(c);
-        c += al256(8 * size_t(k));
-        s.sel_idx[b] = reinterpret_cast<uint32_t*>(c);
-        c += al256(4 * size_t(k));
-    }
-    s.lsd_hist = reinterpret_cast<uint32_t*>(c);
-    (void)ktiles;
-    return s;
-}
-
 }  // namespace
 
 size_t topk_scratch_bytes(int64_t n) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
-    return al256(sizeof(TopkState)) + 2 * al256(8 * size_t(n)) + 2 * al256(4 * size_t(ntiles)) +
-           2 * (al256(8 * size_t(n)) + al256(4 * size_t(n))) + al256(4 * 256 * size_t(ntiles));
+    return al256(sizeof(TopkWork)) + 2 * (al256(8 * size_t(n)) + al256(4 * size_t(n))) +
+           al256(4 * 256 * size_t(ntiles));
 }
 
 cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx,
                         void* d_scratch) {
     if (n <= 0 || k <= 0) return cudaSuccess;
-    Scratch s = carve(d_scratch, n, k);
-    const int ntiles = int((n + kTile - 1) / kTile);
-    cudaError_t e = cudaMemsetAsync(s.st, 0, sizeof(TopkState), c.stream);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(&s.st->andor[0], 0xff, 8, c.stream);
-    if (e != cudaSuccess) return e;
-    const int grid = int((n + kT - 1) / kT < int64_t(c.sm_count) * 4 ? (n + kT - 1) / kT : int64_t(c.sm_count) * 4);
-    prep_kernel<<<grid, kT, 0, c.stream>>>(d_score, n, s.keys, s.st);
-    hist_kernel<<<grid, kT, 0, c.stream>>>(s.keys, n, s.st);
-    pick_kernel<<<1, 1024, 0, c.stream>>>(k, s.st);
-    gather_kernel<<<grid, kT, 0, c.stream>>>(s.keys, n, s.st, s.bucket);
-    refine_kernel<<<1, 1024, 0, c.stream>>>(s.bucket, k, s.st);
-    count_kernel<<<ntiles, kT, 0, c.stream>>>(s.keys, n, s.st, s.lt, s.eq);
-    scan2_kernel<<<1, 1024, 0, c.stream>>>(s.lt, s.eq, ntiles);
-    scatter_sel_kernel<<<ntiles, kT, 0, c.stream>>>(s.keys, n, s.st, s.lt, s.eq, s.sel_key[0], s.sel_idx[0]);
-    note_launches(8);
-    if (k <= kSmallSort) {
-        small_sort_kernel<<<1, 1024, 0, c.stream>>>(s.sel_key[0], s.sel_idx[0], int(k), d_idx);
-        note_launches(1);
-        return cudaGetLastError();
+    char* p = static_cast<char*>(d_scratch);
+    TopkWork* w = reinterpret_cast<TopkWork*>(p);
+    p += al256(sizeof(TopkWork));
+    uint64_t* sk[2];
+    uint32_t* sv[2];
+    for (int i = 0; i < 2; ++i) {
+        sk[i] = reinterpret_cast<uint64_t*>(p);
+        p += al256(8 * size_t(n));
+        sv[i] = reinterpret_cast<uint32_t*>(p);
+        p += al256(4 * size_t(n));
     }
-    // stable LSD sort of the k selected pairs (already in index order) by key
+    uint32_t* lsd_hist = reinterpret_cast<uint32_t*>(p);
+
+    // one CTA per SM; cache keys in smem when the per-CTA chunk fits
+    int G = c.sm_count;
+    const int64_t chunk = (n + G - 1) / G;
+    const int cache = chunk <= kSmemKeys ? 1 : 0;
+    const int final_sort = k <= kSmallSort ? 1 : 0;
+    size_t smem = cache ? size_t(chunk) * 8 : 0;
+    if (final_sort) {
+        const size_t need = size_t(kSmallSort) * 12;
+        if (smem < need) smem = need;
+    }
+    cudaError_t e = cudaFuncSetAttribute(topk_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_coop_kernel, kCoopT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    if (G > 1024) G = 1024;
+    e = cudaMemsetAsync(w, 0, sizeof(TopkWork), c.stream);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(&w->andor[0], 0xff, 8, c.stream);
+    if (e != cudaSuccess) return e;
+    void* args[] = {(void*)&d_score, (void*)&n, (void*)&k, (void*)&w, (void*)&sk[0], (void*)&sv[0], (void*)&d_idx,
+                    (void*)&cache, (void*)&final_sort};
+    e = cudaLaunchCooperativeKernel((const void*)topk_coop_kernel, dim3(G), dim3(kCoopT), args, smem, c.stream);
+    if (e != cudaSuccess) return e;
+    note_launches(1);
+    if (final_sort) return cudaSuccess;
+    // stable LSD sort of the k selected pairs (in index order) by key
     const int kt = int((k + kTile - 1) / kTile);
     int cur = 0;
     for (int shift = 0; shift < 64; shift += 8) {
-        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(s.sel_key[cur], k, shift, s.lsd_hist, kt);
-        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(s.lsd_hist, kt);
-        lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(s.sel_key[cur], s.sel_idx[cur], k, shift, s.lsd_hist, kt,
-                                                        s.sel_key[cur ^ 1], s.sel_idx[cur ^ 1]);
+        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(sk[cur], k, shift, lsd_hist, kt);
+        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(lsd_hist, kt);
+        lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(sk[cur], sv[cur], k, shift, lsd_hist, kt, sk[cur ^ 1],
+                                                        sv[cur ^ 1]);
         cur ^= 1;
         note_launches(3);
     }
     const int tg = int((k + 255) / 256 < 1024 ? (k + 255) / 256 : 1024);
-    widen_kernel<<<tg, 256, 0, c.stream>>>(s.sel_idx[cur], k, d_idx);
+    widen_kernel<<<tg, 256, 0, c.stream>>>(sv[cur], k, d_idx);
     note_launches(1);
     return cudaGetLastError();
 }
