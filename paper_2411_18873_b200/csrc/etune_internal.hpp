@@ -124,9 +124,9 @@ enum Channel : int {
 };
 
 struct TreeRec {          // 32 bytes, read warp-uniformly (kernel-parameter constant bank)
-    uint32_t lut[7];      // mask-word index of this tree's LUT per channel (shared all-ones
-                          // table when the tree does not test the channel)
-    uint32_t meta;        // leaf_base (index into leaves[], bits 0-23) | used-channel mask << 24
+    uint32_t lut[7];      // byte offset (from the blob start) of this tree's class->mask
+                          // table per channel; only meaningful when the channel is used
+    uint32_t meta;        // byte offset of the tree's leaf values (bits 0-23) | used-channel mask << 24
 };
 constexpr int kMaxParamTrees = 1000;  // 32000 B of kernel parameters (CUDA 12.1+: 32764 max)
 struct ForestParams {

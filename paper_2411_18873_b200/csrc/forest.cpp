@@ -365,6 +365,7 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
     H.off_blockb = put(*blob, blockb.data(), blockb.size());
     H.off_f13 = put(*blob, f13b.data(), f13b.size());
     for (int c = 0; c < kNumChannels; ++c) H.off_cls[c] = put(*blob, cls[c].data(), cls[c].size());
+    // tree records hold byte offsets from the blob start: reserve, then fill
     H.off_trees = put(*blob, recs.data(), recs.size());
     if (mbits == 32) {
         std::vector<uint32_t> l32(lut.begin(), lut.end());
@@ -373,6 +374,18 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
         H.off_lut = put(*blob, lut.data(), lut.size());
     }
     H.off_leaves = put(*blob, leaves.data(), leaves.size());
+    const uint32_t mbytes = uint32_t(mbits / 8);
+    for (TreeRec& R : recs) {
+        const uint32_t used_mask = R.meta >> 24;
+        for (int c = 0; c < kNumChannels; ++c) R.lut[c] = H.off_lut + R.lut[c] * mbytes;
+        const uint32_t lb = H.off_leaves + (R.meta & 0xffffffu) * 8u;
+        if (lb >= (1u << 24)) {
+            *err = "compiled forest too large";
+            return ETUNE_ERR_UNSUPPORTED;
+        }
+        R.meta = lb | (used_mask << 24);
+    }
+    std::memcpy(blob->data() + H.off_trees, recs.data(), recs.size() * sizeof(TreeRec));
     blob->resize(align16(blob->size()));
     H.total = uint32_t(blob->size());
     std::memcpy(blob->data(), &H, sizeof(H));

@@ -72,40 +72,85 @@ __host__ __device__ __forceinline__ CandClasses candidate_classes(const uint8_t*
 // Sum of leaf values over trees [0, ntrees) in tree order (energy_model.cpp:247).
 // `trees` is warp-uniform (on the device: the kernel-parameter constant bank);
 // channels a tree does not test are skipped by predication (no smem traffic).
+// `cb` are the candidate's channel classes pre-scaled to byte offsets
+// (class * sizeof(M)); table and leaf offsets in the records are byte offsets from
+// the blob start, so each lookup is one add + one shared load.
+// Shared-memory loads by 32-bit shared-window address on the device (one IADD per
+// table lookup: record offset + pre-scaled class + blob base); host: plain pointers.
+#if defined(__CUDA_ARCH__)
+using SAddr = uint32_t;
+__device__ __forceinline__ uint32_t lds32(SAddr a) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint64_t lds64(SAddr a) {
+    uint64_t v;
+    asm("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double ldsf64(SAddr a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ SAddr blob_saddr(const uint8_t* S) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(S));
+}
+#else
+using SAddr = const uint8_t*;
+inline uint32_t lds32(SAddr a) { return *reinterpret_cast<const uint32_t*>(a); }
+inline uint64_t lds64(SAddr a) { return *reinterpret_cast<const uint64_t*>(a); }
+inline double ldsf64(SAddr a) { return *reinterpret_cast<const double*>(a); }
+inline SAddr blob_saddr(const uint8_t* S) { return S; }
+#endif
+
 template <typename M>
-__host__ __device__ __forceinline__ M tree_mask(const TreeRec& r, const M* lut, const uint32_t* c) {
+__host__ __device__ __forceinline__ M lds_mask(SAddr a) {
+    if constexpr (sizeof(M) == 4) return lds32(a);
+    else return lds64(a);
+}
+
+// `cb[ch]` = blob base + class * sizeof(M): each lookup is one add + one shared load.
+template <typename M>
+__host__ __device__ __forceinline__ M tree_mask(const TreeRec& r, const SAddr* cb) {
     M m = ~M(0);
 #pragma unroll
     for (int ch = 0; ch < kNumChannels; ++ch)
-        if ((r.meta >> (24 + ch)) & 1u) m &= lut[r.lut[ch] + c[ch]];
+        if ((r.meta >> (24 + ch)) & 1u) m &= lds_mask<M>(cb[ch] + r.lut[ch]);
     return m;
+}
+
+template <typename M>
+__host__ __device__ __forceinline__ double leaf_value(SAddr base, const TreeRec& r, M m) {
+    const int l = sizeof(M) == 4 ? ETUNE_FFS32(m) : ETUNE_FFS64(m);
+    return ldsf64(base + ((r.meta & 0xffffffu) + uint32_t(l) * 8u));
 }
 
 template <typename M>
 __host__ __device__ __forceinline__ double forest_sum(const uint8_t* S, const ScoreHdr& H, const TreeRec* trees,
                                                       const uint32_t* c) {
-    const M* lut = blob_at<M>(S, H.off_lut);
-    const double* leaves = blob_at<double>(S, H.off_leaves);
+    const SAddr base = blob_saddr(S);
+    SAddr cb[kNumChannels];
+#pragma unroll
+    for (int ch = 0; ch < kNumChannels; ++ch) cb[ch] = base + c[ch] * uint32_t(sizeof(M));
     double sum = 0.0;
     int t = 0;
+    const int nt = H.ntrees;
     // two trees per iteration: their table reads are independent (ILP)
-    for (; t + 1 < H.ntrees; t += 2) {
+    for (; t + 1 < nt; t += 2) {
         const TreeRec a = trees[t];
         const TreeRec b = trees[t + 1];
-        const M ma = tree_mask<M>(a, lut, c);
-        const M mb = tree_mask<M>(b, lut, c);
-        const int la = sizeof(M) == 4 ? ETUNE_FFS32(ma) : ETUNE_FFS64(ma);
-        const int lb = sizeof(M) == 4 ? ETUNE_FFS32(mb) : ETUNE_FFS64(mb);
-        const double va = leaves[(a.meta & 0xffffffu) + la];
-        const double vb = leaves[(b.meta & 0xffffffu) + lb];
+        const M ma = tree_mask<M>(a, cb);
+        const M mb = tree_mask<M>(b, cb);
+        const double va = leaf_value<M>(base, a, ma);
+        const double vb = leaf_value<M>(base, b, mb);
         sum = ETUNE_DADD(sum, va);
         sum = ETUNE_DADD(sum, vb);
     }
-    for (; t < H.ntrees; ++t) {
+    for (; t < nt; ++t) {
         const TreeRec a = trees[t];
-        const M ma = tree_mask<M>(a, lut, c);
-        const int la = sizeof(M) == 4 ? ETUNE_FFS32(ma) : ETUNE_FFS64(ma);
-        sum = ETUNE_DADD(sum, leaves[(a.meta & 0xffffffu) + la]);
+        sum = ETUNE_DADD(sum, leaf_value<M>(base, a, tree_mask<M>(a, cb)));
     }
     return sum;
 }

@@ -35,7 +35,7 @@ __device__ __forceinline__ uint64_t order_key(double x) {
 }
 
 constexpr int kCoopT = 1024;
-constexpr int kMaxPasses = 6;             // 11-bit digits over <= 64 varying bits
+constexpr int kMaxPasses = 7;             // 8 + 11-bit digits over <= 64 varying bits
 constexpr int kSmemKeys = 24 * 1024;      // keys cached per CTA (192 KB)
 
 struct TopkWork {
@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
     unsigned rem = unsigned(k);  // 1-based rank of T inside the current prefix group
     int bit = varying ? 64 - __clzll(static_cast<long long>(varying)) : 0;  // bits [0, bit) still open
     for (int pass = 0; bit > 0; ++pass) {
-        const int width = bit >= 11 ? 11 : bit;
+        const int dw = pass == 0 ? 8 : 11;  // narrow first digit: fewer global atomics
+        const int width = bit >= dw ? dw : bit;
         const int sh = bit - width;
         const uint64_t himask = (bit >= 64) ? 0ull : (~0ull << bit);
         for (int i = tid; i < kBins; i += blockDim.x) h[i] = 0;
