@@ -42,6 +42,7 @@ def pytest_sessionstart(session):
     if _stale(os.path.join(orc, "lib", "liboracle.so"),
               [os.path.join(orc, "etune_oracle.cpp"), os.path.join(orc, "etune_oracle.h")]):
         subprocess.run(["make", "-s", "-C", orc, "oracle"], check=True)
+    subprocess.run(["make", "-s", "-C", os.path.join(HERE, "cpp")], check=True)
     try:
         import __graft_entry__ as ge
         ge.build_product(quiet=True)
