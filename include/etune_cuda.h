@@ -208,6 +208,24 @@ etune_status etune_cu_score_host(etune_cu_ctx* ctx, const etune_cu_plan* plan,
 etune_status etune_cu_forest_compile_stats(etune_cu_forest* forest, const etune_cu_plan* plan,
                                            int64_t out[8]);
 
+/* ---------------------------------------------------------- reproduction */
+/* reproduce (genetic.hpp:48-51, genetic.cpp:137-187) on device genomes, bit-exact with
+ * the reference's ONE sequential std::mt19937_64(seed) stream: offspring i starts from
+ * parents[i % num_parents] and is a mutation / crossover / copy drawn exactly as the
+ * reference draws it (the stream is generated on the device; the data-dependent word
+ * offsets are resolved there by speculation).  rates NULL = GeneticRates{}.
+ * d_partner[i] (nullable) = crossover partner's parent index, -1 for mutation/copy, so
+ * lineage = {id(parents[i % P])} or {id(base), id(parents[d_partner[i]])}.
+ * d_ids (nullable) = candidate_id of every offspring.
+ * Errors: VALIDATION (num_parents < 1, rates summing to <= 0 — genetic.cpp:140-152);
+ * ILLEGAL_SCHEDULE at the first offspring whose repair fails (reported by
+ * etune_cu_synchronize with its index, like the reference's throw from repair). */
+etune_status etune_cu_reproduce(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                const uint64_t* d_parents, int64_t num_parents, int64_t n,
+                                const etune_genetic_rates* rates, uint64_t seed,
+                                uint64_t* d_offspring, int32_t* d_partner /*nullable*/,
+                                uint64_t* d_ids /*nullable*/);
+
 /* ------------------------------------------------------------- selection */
 /* The k smallest of d_score[0..n) under the total order (score asc, index asc)
  * ("lowest predicted energy"; SURVEY H3 tie rule), written sorted to

@@ -57,6 +57,10 @@ class DeviceConfig(C.Structure):
             "sampler_hz", "warmup_s", "noise_sigma_rel")] + [("rng_seed", C.c_uint64)]
 
 
+class GeneticRates(C.Structure):
+    _fields_ = [("mutation", C.c_double), ("crossover", C.c_double), ("copy", C.c_double)]
+
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _PTR = C.c_void_p
@@ -89,6 +93,8 @@ _SIGS = {
     "etune_cu_score": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
+    "etune_cu_reproduce": (C.c_int, [_VP, _VP, _PTR, _I64, _I64, C.POINTER(GeneticRates), C.c_uint64, _PTR, _PTR,
+                                     _PTR]),
 }
 
 _lib = None
@@ -240,6 +246,20 @@ class Plan:
         ids = torch.empty_like(genome) if with_ids else None
         _check(lib().etune_cu_features(self.ctx.h, self.h, _ptr(genome), n, _ptr(f), _ptr(ids)))
         return (f, ids) if with_ids else f
+
+
+def reproduce(plan: "Plan", parents, n: int, seed: int, rates=(0.85, 0.10, 0.05)):
+    """reproduce (genetic.cpp:137-187) on device genomes -> (offspring genomes, partner idx, ids).
+    Offspring i's base parent is i % len(parents); partner[i] = -1 unless a crossover."""
+    import torch
+    dev = parents.device
+    out = torch.empty(n, dtype=torch.int64, device=dev)
+    partner = torch.empty(n, dtype=torch.int32, device=dev)
+    ids = torch.empty(n, dtype=torch.int64, device=dev)
+    r = GeneticRates(*[float(x) for x in rates])
+    _check(lib().etune_cu_reproduce(plan.ctx.h, plan.h, _ptr(parents), parents.shape[0], n, C.byref(r),
+                                    C.c_uint64(seed), _ptr(out), _ptr(partner), _ptr(ids)))
+    return out, partner, ids
 
 
 class Forest:

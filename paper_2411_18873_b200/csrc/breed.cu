@@ -1,0 +1,446 @@
+// reproduce() on the device, bit-exact with the reference's single sequential
+// std::mt19937_64 stream (genetic.cpp:137-187).
+//
+// The obstacle: offspring i consumes a data-dependent number of RNG words
+// (1 for a copy, 2-5 for a mutation, >=3 for a crossover, plus rejection and repair
+// draws), so offspring i's first word index o_i is a sequential prefix over
+// everything before it.  breed_kernel resolves that chain on one CTA per call by
+// speculation:
+//
+//   1. The CTA owns the MT19937-64 state and generates the reference's word stream
+//      itself, 312 words per cooperative twist, into a shared-memory ring
+//      (the stream never goes to HBM).
+//   2. Each round lays out a window of candidate start offsets for the next J
+//      offspring (level j centred on j*mean words, +-~4 sd*sqrt(j)), and the 1024
+//      threads evaluate breed_one() at every (level, offset) cell in parallel:
+//      words consumed, the child genome and the crossover partner.
+//   3. One thread walks the chain through the cells (o_{i+1} = o_i + words(i, o_i)),
+//      stopping at the first level whose true offset fell outside its window; the
+//      resolved children are written out and the next round starts there.
+//
+// Every resolved child is therefore the exact evaluation at its true offset: the
+// speculation only affects speed (how many levels a round resolves), never results.
+// The per-offspring work uses the plan's knob tables (tilings in
+// enumerate_dim_tilings order, divisors of K), so mutate_knob / pick_different /
+// repair_schedule reduce to index arithmetic on the 8-byte genome.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "etune_internal.hpp"
+#include "kernels.hpp"
+
+namespace etune_b200 {
+
+namespace {
+
+constexpr int kBreedThreads = 1024;
+constexpr int kRing = 4096;           // words of the MT stream kept in shared memory
+constexpr int kCells = 2048;          // speculative (offspring, offset) evaluations per round
+constexpr int kMaxLevels = 96;        // offspring resolved per round at most
+constexpr uint16_t kUnknown = 0;      // cell needs words beyond the generated horizon
+constexpr uint16_t kIllegal = 0xffff; // repair produced an illegal schedule (reference throws)
+
+constexpr uint64_t kMtA = 0xb5026f5aa96619e9ull;
+constexpr uint64_t kUpper = 0xffffffff80000000ull;
+constexpr uint64_t kLower = 0x7fffffffull;
+
+__device__ __forceinline__ uint64_t temper(uint64_t y) {  // std::mt19937_64 output function
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71d67fffeda60000ull;
+    y ^= (y << 37) & 0xfff7eee000000000ull;
+    y ^= y >> 43;
+    return y;
+}
+
+__device__ __forceinline__ uint64_t twist1(uint64_t cur, uint64_t next, uint64_t far) {
+    const uint64_t x = (cur & kUpper) | (next & kLower);
+    return far ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
+}
+
+template <typename T>
+__device__ __forceinline__ const T* at(const uint8_t* base, uint32_t off) {
+    return reinterpret_cast<const T*>(base + off);
+}
+
+// Sequential reader of the word stream held in the ring; positions at or beyond
+// `hi` are not generated yet, which makes the evaluation "unknown".
+struct Cursor {
+    const uint64_t* ring;
+    uint64_t p, hi;
+    bool ok;
+    __device__ __forceinline__ uint64_t next() {
+        if (p >= hi) {
+            ok = false;
+            return 0;
+        }
+        return ring[(p++) & (kRing - 1)];
+    }
+};
+
+// uniform_int_distribution<size_t>(0, r-1)(rng) of libstdc++ (GCC 13) on a 64-bit
+// engine: Lemire's multiply-shift with the (-r % r) rejection threshold.
+__device__ __forceinline__ uint64_t lemire(Cursor& c, uint64_t r) {
+    uint64_t x = c.next();
+    uint64_t lo = x * r;
+    uint64_t hi = __umul64hi(x, r);
+    if (lo < r) {
+        const uint64_t thr = (0ull - r) % r;
+        while (lo < thr && c.ok) {
+            x = c.next();
+            lo = x * r;
+            hi = __umul64hi(x, r);
+        }
+    }
+    return hi;
+}
+
+__device__ __forceinline__ int ctz64(int64_t v) { return __ffsll(static_cast<long long>(v)) - 1; }
+
+struct BreedConst {
+    const uint8_t* P;   // plan blob (shared memory when it fits)
+    const uint64_t* par;
+    const uint64_t* pid;
+    int64_t np;
+    double mut, mutcro, total;
+    int has_other;
+};
+
+struct Child {
+    uint64_t g;
+    int32_t partner;
+    uint16_t words;  // kUnknown / kIllegal / consumed count
+};
+
+// pick_different over options {0..m-1} (index space) avoiding index `a` that is one
+// of them: alternatives are all options but `a`, in order (genetic.cpp:32-44).
+__device__ __forceinline__ uint32_t pick_other(Cursor& c, uint32_t m, uint32_t a) {
+    if (m <= 1) return a;
+    const uint32_t j = uint32_t(lemire(c, m - 1));
+    return j < a ? j : j + 1;
+}
+
+// pick_different over the power-of-two list {2^0..2^cap} avoiding 2^a (a may lie
+// outside the list: then every option is an alternative) — legal_unrolls /
+// legal_vectors in log2 form (genetic.cpp:11-29).
+__device__ __forceinline__ uint32_t pick_pow2(Cursor& c, uint32_t cap, uint32_t a) {
+    const uint32_t m = cap + 1;
+    if (m <= 1) return 0;  // options.front() == 1
+    if (a <= cap) {
+        const uint32_t j = uint32_t(lemire(c, m - 1));
+        return j < a ? j : j + 1;
+    }
+    return uint32_t(lemire(c, m));
+}
+
+// One offspring evaluated at word offset `start` (genetic.cpp:160-185).
+__device__ Child breed_one(const BreedConst& K, const PlanHdr& H, int64_t i, const uint64_t* ring, uint64_t start,
+                           uint64_t hi) {
+    Cursor c{ring, start, hi, true};
+    Child out{0, -1, kUnknown};
+    const int64_t base = i % K.np;
+    Genome x = genome_unpack(__ldg(K.par + base));
+    const TilingRec* til[3] = {at<TilingRec>(K.P, H.off_til[0]), at<TilingRec>(K.P, H.off_til[1]),
+                               at<TilingRec>(K.P, H.off_til[2])};
+    const int64_t* divk = at<int64_t>(K.P, H.off_divk);
+    // uniform_real_distribution<double>(0,1) = generate_canonical<double,53>: double(w) / 2^64,
+    // clamped to nextafter(1, 0); then * total (genetic.cpp:162)
+    const double coin = __dmul_rn(__ull2double_rn(c.next()), 0x1p-64);
+    const double u = __dmul_rn(coin < 1.0 ? coin : 0x1.fffffffffffffp-1, K.total);
+    bool repair = true;
+    if (u < K.mut) {
+        const uint32_t knob = uint32_t(lemire(c, 6));  // uniform_int_distribution<int>(0, 5)
+        switch (knob) {
+        case 0: x.t0 = pick_other(c, uint32_t(H.nt[0]), x.t0); break;
+        case 1: x.t1 = pick_other(c, uint32_t(H.nt[1]), x.t1); break;
+        case 2: x.t2 = pick_other(c, uint32_t(H.nt[2]), x.t2); break;
+        case 3: x.k = pick_other(c, uint32_t(H.ndk), x.k); break;
+        case 4: {
+            const int cu = min(H.max_unroll_log2, ctz64(divk[x.k]));
+            x.u = pick_pow2(c, uint32_t(cu), x.u);
+            break;
+        }
+        default: {
+            const int cv = min(H.max_vec_log2, ctz64(int64_t(til[2][x.t2].pt)));
+            x.v = pick_pow2(c, uint32_t(cv), x.v);
+            break;
+        }
+        }
+    } else if (u < K.mutcro) {
+        const uint64_t bid = __ldg(K.pid + base);
+        int64_t pi = int64_t(lemire(c, uint64_t(K.np)));
+        while (K.has_other && c.ok && __ldg(K.pid + pi) == bid) pi = int64_t(lemire(c, uint64_t(K.np)));
+        const uint32_t mask = uint32_t(c.next() & 63u);
+        const Genome y = genome_unpack(__ldg(K.par + pi));  // crossover_with_mask, genetic.cpp:48-58
+        if (mask & 1u) x.t0 = y.t0;
+        if (mask & 2u) x.t1 = y.t1;
+        if (mask & 4u) x.t2 = y.t2;
+        if (mask & 8u) x.k = y.k;
+        if (mask & 16u) x.u = y.u;
+        if (mask & 32u) x.v = y.v;
+        out.partner = int32_t(pi);
+    } else {
+        repair = false;  // copy
+    }
+    if (repair && c.ok) {  // repair_schedule, genetic.cpp:89-135
+        const int64_t cap = H.block_cap;
+        uint32_t t[3] = {x.t0, x.t1, x.t2};
+        for (int attempt = 0; attempt < 64 && c.ok; ++attempt) {
+            const uint64_t th[3] = {til[0][t[0]].threads, til[1][t[1]].threads, til[2][t[2]].threads};
+            const int64_t block = int64_t(th[0] * th[1] * th[2]);
+            if (!(block > cap)) break;
+            int dim = 0;
+            if (th[1] > th[dim]) dim = 1;
+            if (th[2] > th[dim]) dim = 2;
+            const int64_t other = block / int64_t(th[dim]);
+            const TilingRec* T = til[dim];
+            const int nt = H.nt[dim];
+            uint32_t fit = 0;
+            for (int j = 0; j < nt; ++j) fit += int64_t(uint64_t(T[j].threads) * uint64_t(other)) <= cap;
+            if (fit == 0) {
+                t[dim] = uint32_t(nt - 1);  // {extent, 1, 1}: the last tiling in enumeration order
+            } else {
+                uint32_t r = uint32_t(lemire(c, fit));
+                for (int j = 0; j < nt; ++j) {
+                    if (int64_t(uint64_t(T[j].threads) * uint64_t(other)) <= cap) {
+                        if (r == 0) {
+                            t[dim] = uint32_t(j);
+                            break;
+                        }
+                        --r;
+                    }
+                }
+            }
+        }
+        x.t0 = t[0];
+        x.t1 = t[1];
+        x.t2 = t[2];
+        // k_tile is a divisor of K by construction (genome index), so the k_tile branch never fires
+        const uint32_t cu = uint32_t(min(H.max_unroll_log2, ctz64(divk[x.k])));
+        if (x.u > cu) x.u = uint32_t(lemire(c, cu + 1));
+        const uint32_t cv = uint32_t(min(H.max_vec_log2, ctz64(int64_t(til[2][x.t2].pt))));
+        if (x.v > cv) x.v = uint32_t(lemire(c, cv + 1));
+        const int64_t block =
+            int64_t(uint64_t(til[0][x.t0].threads) * til[1][x.t1].threads * uint64_t(til[2][x.t2].threads));
+        if (c.ok && (block < 1 || block > 1024)) {  // validate_schedule (schedule.cpp:26-61)
+            out.words = kIllegal;
+            return out;
+        }
+    }
+    if (!c.ok) return out;
+    out.g = genome_pack(x.t0, x.t1, x.t2, x.k, x.u, x.v);
+    const uint64_t used = c.p - start;
+    out.words = used < 0xfffeull ? uint16_t(used) : uint16_t(0xfffe);
+    return out;
+}
+
+struct BreedState {
+    int64_t resolved;       // offspring written
+    uint64_t words;         // RNG words consumed by them
+    int32_t status;         // 0 ok, else etune_status
+    int32_t pad;
+};
+
+__global__ void __launch_bounds__(kBreedThreads, 1)
+    breed_kernel(const uint8_t* __restrict__ gplan, uint32_t plan_bytes, int use_smem,
+                 const uint64_t* __restrict__ par, const uint64_t* __restrict__ pid, int64_t np, int64_t n,
+                 double mut, double mutcro, double total, uint64_t seed, uint64_t* __restrict__ out,
+                 int32_t* __restrict__ partner, unsigned long long* err, BreedState* st) {
+    // dynamic shared memory: [ring | cell genomes | cell partners | cell words | mt | plan]
+    extern __shared__ int4 smem[];
+    uint64_t* ring = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* cg = ring + kRing;
+    int32_t* cp = reinterpret_cast<int32_t*>(cg + kCells);
+    uint16_t* cw = reinterpret_cast<uint16_t*>(cp + kCells);
+    uint64_t* mt = reinterpret_cast<uint64_t*>(cw + kCells);
+    __shared__ int32_t lstart[kMaxLevels + 1], llo[kMaxLevels], lhi[kMaxLevels];
+    __shared__ int16_t sel[kMaxLevels];
+    __shared__ int s_levels, s_resolved, s_status, s_other;
+    __shared__ uint64_t s_step;
+    const int tid = threadIdx.x;
+
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        int4* dst = reinterpret_cast<int4*>(mt + 312);
+        const int4* src = reinterpret_cast<const int4*>(gplan);
+        for (uint32_t i = tid; i < (plan_bytes >> 4); i += blockDim.x) dst[i] = __ldg(src + i);
+        P = reinterpret_cast<const uint8_t*>(dst);
+    }
+    // has_other: some parent id differs from another (genetic.cpp:172-174)
+    if (tid == 0) s_other = 0;
+    __syncthreads();
+    {
+        const uint64_t id0 = __ldg(pid);
+        int diff = 0;
+        for (int64_t j = tid; j < np; j += blockDim.x) diff |= __ldg(pid + j) != id0;
+        if (__syncthreads_or(diff) && tid == 0) s_other = 1;
+    }
+    // std::mt19937_64(seed) (libstdc++ seeding: f = 6364136223846793005)
+    if (tid == 0) {
+        uint64_t v = seed;
+        mt[0] = v;
+        for (int i = 1; i < 312; ++i) {
+            v = 6364136223846793005ull * (v ^ (v >> 62)) + uint64_t(i);
+            mt[i] = v;
+        }
+    }
+    __syncthreads();
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    BreedConst K{P, par, pid, np, mut, mutcro, total, s_other};
+
+    uint64_t hi = 0;          // words generated so far (ring holds [hi - kRing, hi) at most)
+    uint64_t o0 = 0;          // first word of offspring i0
+    int64_t i0 = 0;
+    double mean = 2.8, var = 0.6;  // running word-count statistics (window placement only)
+    double s1 = 0.0, s2 = 0.0;
+    int64_t cnt = 0;
+    int status = 0;
+    while (i0 < n) {
+        // ---- extend the stream: cooperative twists while the ring has room
+        while (hi + 312 <= o0 + kRing) {
+            uint64_t cur = 0, nxt = 0;
+            if (tid < 312) {
+                cur = mt[tid];
+                nxt = tid < 311 ? mt[tid + 1] : 0;
+            }
+            __syncthreads();
+            if (tid < 156) mt[tid] = twist1(cur, nxt, mt[tid + 156]);
+            __syncthreads();
+            if (tid >= 156 && tid < 311) mt[tid] = twist1(cur, nxt, mt[tid - 156]);
+            if (tid == 311) {
+                const uint64_t m0 = mt[0], m155 = mt[155];
+                mt[311] = twist1(cur, m0, m155);
+            }
+            __syncthreads();
+            if (tid < 312) ring[(hi + uint64_t(tid)) & (kRing - 1)] = temper(mt[tid]);
+            hi += 312;
+        }
+        // ---- level windows
+        if (tid == 0) {
+            const double sd = sqrt(var > 0.05 ? var : 0.05);
+            int cells = 0, j = 0;
+            for (; j < kMaxLevels && i0 + j < n; ++j) {
+                int lo, hi_j;
+                if (j == 0) {
+                    lo = 0;
+                    hi_j = 0;
+                } else {
+                    const double c = mean * j;
+                    const int h = 2 + int(ceil(4.0 * sd * sqrt(double(j))));
+                    lo = max(j, int(floor(c)) - h);
+                    hi_j = int(ceil(c)) + h;
+                }
+                const int w = hi_j - lo + 1;
+                if (cells + w > kCells) break;
+                lstart[j] = cells;
+                llo[j] = lo;
+                lhi[j] = hi_j;
+                cells += w;
+            }
+            lstart[j] = cells;
+            s_levels = j;
+        }
+        __syncthreads();
+        const int J = s_levels, ncell = lstart[J];
+        // ---- speculative evaluation of every (level, offset) cell
+        for (int cell = tid; cell < ncell; cell += blockDim.x) {
+            int lo = 0, hi2 = J;  // level of this cell: last j with lstart[j] <= cell
+            while (hi2 - lo > 1) {
+                const int mid = (lo + hi2) >> 1;
+                if (lstart[mid] <= cell) lo = mid;
+                else hi2 = mid;
+            }
+            const int j = lo;
+            const uint64_t off = o0 + uint64_t(llo[j] + (cell - lstart[j]));
+            const Child ch = breed_one(K, H, i0 + j, ring, off, hi);
+            cg[cell] = ch.g;
+            cp[cell] = ch.partner;
+            cw[cell] = ch.words;
+        }
+        __syncthreads();
+        // ---- walk the true chain through the cells
+        if (tid == 0) {
+            int x = 0, r = 0, stt = 0;
+            for (int j = 0; j < J; ++j) {
+                if (x < llo[j] || x > lhi[j]) break;
+                const int cell = lstart[j] + (x - llo[j]);
+                const uint16_t w = cw[cell];
+                if (w == kUnknown) break;
+                if (w == kIllegal) {
+                    stt = ETUNE_ERR_ILLEGAL_SCHEDULE;
+                    atomicMin(err, (static_cast<unsigned long long>(i0 + j) << 8) | unsigned(stt));
+                    break;
+                }
+                sel[j] = int16_t(cell);
+                x += w;
+                ++r;
+            }
+            if (r == 0 && stt == 0 && hi + 312 > o0 + kRing) {
+                // offspring i0 alone needs more than the ring's words (a crossover whose
+                // partner search runs for thousands of draws): beyond this build's window
+                stt = ETUNE_ERR_UNSUPPORTED;
+                atomicMin(err, (static_cast<unsigned long long>(i0) << 8) | unsigned(stt));
+            }
+            s_resolved = r;
+            s_status = stt;
+            s_step = uint64_t(x);
+        }
+        __syncthreads();
+        const int R = s_resolved;
+        if (tid < R) {
+            const int cell = sel[tid];
+            out[i0 + tid] = cg[cell];
+            if (partner) partner[i0 + tid] = cp[cell];
+        }
+        // running statistics of words per offspring, from the resolved levels
+        if (R > 0) {
+            for (int j = 0; j < R; ++j) {  // uniform loop: every thread keeps the same stats
+                const double w = double(cw[sel[j]]);
+                s1 += w;
+                s2 += w * w;
+            }
+            cnt += R;
+            mean = s1 / double(cnt);
+            var = s2 / double(cnt) - mean * mean;
+        }
+        o0 += s_step;
+        i0 += R;
+        status = s_status;
+        __syncthreads();
+        if (status) break;
+    }
+    if (tid == 0) {
+        st->resolved = i0;
+        st->words = o0;
+        st->status = status;
+    }
+}
+
+}  // namespace
+
+size_t breed_state_bytes() { return sizeof(BreedState); }
+
+cudaError_t launch_breed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
+                         const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
+                         uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_state) {
+    if (n <= 0) return cudaSuccess;
+    const double mutcro = mut + cro;     // genetic.cpp:169, evaluated like the reference
+    const double total = mutcro + cpy;   // genetic.cpp:150: mutation + crossover + copy
+    // ~64 KB of working arrays; the plan blob joins them in shared memory when it fits
+    constexpr size_t kFixed = size_t(kRing) * 8 + size_t(kCells) * (8 + 4 + 2) + 312 * 8;
+    static_assert(kFixed % 16 == 0, "plan section must stay 16-byte aligned");
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int use_smem = (kFixed + plan_bytes + 2048 <= size_t(optin)) ? 1 : 0;
+    const size_t dyn = kFixed + (use_smem ? plan_bytes : 0);
+    cudaError_t e = cudaFuncSetAttribute(breed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+    if (e != cudaSuccess) return e;
+    breed_kernel<<<1, kBreedThreads, dyn, c.stream>>>(d_plan, plan_bytes, use_smem, d_par, d_pid, np, n, mut, mutcro,
+                                                      total, seed, d_out, d_partner, c.d_err,
+                                                      static_cast<BreedState*>(d_state));
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace etune_b200

@@ -33,6 +33,8 @@ struct etune_cu_ctx {
     // staging for the *_host path
     void* io = nullptr;
     size_t io_bytes = 0;
+    void* breed = nullptr;  // BreedState + parent ids
+    size_t breed_bytes = 0;
     LaunchCtx lc() const { return LaunchCtx{stream, sm_count, d_err}; }
 };
 
@@ -206,6 +208,7 @@ etune_status etune_cu_ctx_destroy(etune_cu_ctx* c) {
     cudaFree(c->d_err);
     cudaFree(c->scratch);
     cudaFree(c->io);
+    cudaFree(c->breed);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return ETUNE_OK;
@@ -407,6 +410,39 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
     }
     return etune_cu_synchronize(c, first_bad);
+}
+
+etune_status etune_cu_reproduce(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np,
+                                int64_t n, const etune_genetic_rates* rates, uint64_t seed, uint64_t* d_out,
+                                int32_t* d_partner, uint64_t* d_ids) {
+    if (!c || !p) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx/plan");
+    if (n < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "negative n");
+    if (np < 1 || !d_par) return fail(ETUNE_ERR_VALIDATION, "reproduce requires at least one parent");
+    etune_genetic_rates r;
+    etune_default_genetic_rates(&r);
+    if (rates) r = *rates;
+    if (!(r.mutation + r.crossover + r.copy > 0.0))
+        return fail(ETUNE_ERR_VALIDATION, "genetic rates must not all be zero");
+    if (n == 0) return ETUNE_OK;
+    if (!d_out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null offspring buffer");
+    if (np >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "more than 2^31 parents");
+    const size_t need = 256 + size_t(np) * 8;
+    if (c->breed_bytes < need) {
+        if (c->breed) {
+            CU(cudaStreamSynchronize(c->stream));
+            CU(cudaFree(c->breed));
+            c->breed = nullptr;
+            c->breed_bytes = 0;
+        }
+        CU(cudaMalloc(&c->breed, need));
+        c->breed_bytes = need;
+    }
+    uint64_t* d_pid = reinterpret_cast<uint64_t*>(static_cast<char*>(c->breed) + 256);
+    CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_par, np, d_pid));
+    CU(launch_breed(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover, r.copy,
+                    seed, d_out, d_partner, c->breed));
+    if (d_ids) CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_out, n, d_ids));
+    return ETUNE_OK;
 }
 
 etune_status etune_cu_topk(etune_cu_ctx* c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx) {

@@ -40,6 +40,13 @@ size_t topk_scratch_bytes(int64_t n);
 cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, int64_t k,
                         int64_t* d_idx, void* d_scratch);
 
+// reproduce (genetic.cpp:137-187): one CTA resolves the RNG-offset chain by speculation
+// and writes offspring genomes (+ crossover partner index, -1 otherwise).
+size_t breed_state_bytes();
+cudaError_t launch_breed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
+                         const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
+                         uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_state);
+
 // process-wide count of kernel launches (incremented by every launcher)
 void note_launches(int k);
 uint64_t launch_count();

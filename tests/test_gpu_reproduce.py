@@ -1,0 +1,124 @@
+"""GPU parity of etune_cu_reproduce (device reproduce, genetic.cpp:137-187) against the
+reference's golden offspring and the oracle: offspring schedules, ids and lineage are
+bit-exact (the device consumes the reference's single mt19937_64 stream)."""
+import numpy as np
+import pytest
+
+from etune_testlib import parse_op
+from golden.make_golden import OPS
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+NAMES = [n for n, _, _ in OPS]
+
+
+@pytest.fixture(scope="module")
+def capi():
+    from paper_2411_18873_b200 import capi as c
+    return c
+
+
+@pytest.fixture(scope="module")
+def ctx(capi):
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return capi.Context(0)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run(capi, ctx, op, parents, n, seed, rates=(0.85, 0.10, 0.05), limits=None):
+    plan = capi.Plan(ctx, op, limits=limits)
+    g = plan.encode(dev(parents))
+    out, partner, ids = capi.reproduce(plan, g, n, seed, rates)
+    sched = plan.decode(out)
+    ctx.synchronize()
+    return sched.cpu().numpy(), partner.cpu().numpy(), capi.as_u64(ids)
+
+
+def check(oracle, capi, op, parents, n, got, seed, rates=(0.85, 0.10, 0.05), limits=None):
+    s, ids, lin, ll = oracle.reproduce(op, parents, n, seed, rates, limits)
+    gs, gp, gid = got
+    assert (gs == s).all()
+    assert (gid == ids).all()
+    pid = oracle.ids(op, parents)
+    base = np.arange(n) % len(parents)
+    assert (lin[:, 0] == pid[base]).all()
+    cro = gp >= 0
+    assert (ll == np.where(cro, 2, 1)).all()
+    assert (lin[cro, 1] == pid[gp[cro]]).all()
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_reproduce_golden(golden, ctx, capi, name):
+    op = golden[f"{name}/op"]
+    par = golden[f"{name}/repro_parents"]
+    gs, gp, gid = run(capi, ctx, op, par, 512, 7)
+    assert (gs == golden[f"{name}/repro_sched"]).all()
+    assert (gid == golden[f"{name}/repro_ids"]).all()
+    lin, ll = golden[f"{name}/repro_lineage"], golden[f"{name}/repro_lineage_len"]
+    assert (ll == np.where(gp >= 0, 2, 1)).all()
+
+
+@pytest.mark.parametrize("text,npar,n,seed", [
+    ("conv:1,56,56,64,64,3,1,1", 1024, 1 << 16, 7),
+    ("mm:1,1024,1024,1024", 512, 20000, 11),
+    ("mm:1,512,3072,768", 2048, 50000, 3),
+    ("mm:4,96,200,50", 300, 30000, 5),      # batch > 1: batch-tiling mutations draw
+    ("mm:3,12,18,10", 17, 9999, 1),
+    ("mv:1,1,1000,2048", 64, 4097, 99),
+    ("conv:2,4,4,2,2,1,1,0", 40, 3000, 8),
+])
+def test_reproduce_vs_oracle(oracle, ctx, capi, text, npar, n, seed):
+    op = parse_op(text)
+    par, _ = oracle.sample_random(op, min(npar, oracle.count(op)), 42)
+    check(oracle, capi, op, par, n, run(capi, ctx, op, par, n, seed), seed)
+
+
+@pytest.mark.parametrize("rates", [(1.0, 0.0, 0.0), (0.0, 1.0, 0.0), (0.0, 0.0, 1.0), (0.3, 0.3, 0.4),
+                                   (2.0, 7.0, 1.0)])
+def test_reproduce_rates(oracle, ctx, capi, rates):
+    op = parse_op("conv:1,28,28,128,512,1,1,0")
+    par, _ = oracle.sample_random(op, 200, 4)
+    check(oracle, capi, op, par, 20000, run(capi, ctx, op, par, 20000, 12, rates), 12, rates)
+
+
+def test_reproduce_duplicate_parents(oracle, ctx, capi):
+    """Duplicated parent ids: the crossover partner loop (genetic.cpp:172-177) must skip
+    equal ids; with ALL parents identical has_other is false and no redraw happens."""
+    op = parse_op("mm:1,64,64,64")
+    par, _ = oracle.sample_random(op, 8, 3)
+    dup = np.concatenate([np.repeat(par[:1], 30, 0), par[1:3]])  # 30 copies + 2 others
+    for p in (dup, np.repeat(par[:1], 5, 0), par[:1]):
+        check(oracle, capi, op, p, 5000, run(capi, ctx, op, p, 5000, 21, (0.2, 0.8, 0.0)), 21, (0.2, 0.8, 0.0))
+
+
+@pytest.mark.parametrize("limits", [(128, 8, 4), (1024, 2, 1), (64, 1, 2), (1024, 32, 4)])
+def test_reproduce_limits(oracle, ctx, capi, limits):
+    """SpaceLimits change legal unroll/vector lists and the repair block cap."""
+    op = parse_op("mm:1,256,512,384")
+    lim = np.array(limits, np.int64)
+    par, _ = oracle.sample_random(op, 100, 6, lim)
+    check(oracle, capi, op, par, 20000, run(capi, ctx, op, par, 20000, 5, limits=lim), 5, limits=lim)
+
+
+def test_reproduce_edge_sizes(oracle, ctx, capi):
+    op = parse_op("mm:1,8,8,8")
+    par, _ = oracle.sample_random(op, 3, 1)
+    for n in (1, 2, 95, 96, 97, 313):
+        check(oracle, capi, op, par, n, run(capi, ctx, op, par, n, 77), 77)
+
+
+def test_reproduce_errors(ctx, capi):
+    op = parse_op("mm:1,8,8,8")
+    plan = capi.Plan(ctx, op)
+    g = torch.zeros(0, dtype=torch.int64, device="cuda")
+    with pytest.raises(capi.EtuneError) as e:
+        capi.reproduce(plan, g, 10, 1)
+    assert e.value.code == 2
+    g = torch.zeros(1, dtype=torch.int64, device="cuda")
+    with pytest.raises(capi.EtuneError) as e:
+        capi.reproduce(plan, g, 10, 1, (0.0, 0.0, 0.0))
+    assert e.value.code == 2
