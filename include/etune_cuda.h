@@ -208,6 +208,33 @@ etune_status etune_cu_score_host(etune_cu_ctx* ctx, const etune_cu_plan* plan,
 etune_status etune_cu_forest_compile_stats(etune_cu_forest* forest, const etune_cu_plan* plan,
                                            int64_t out[8]);
 
+/* ------------------------------------------------------ cost-model update */
+/* EnergyModel::train (energy_model.hpp:69-70, energy_model.cpp:173-243) on device
+ * samples: d_feat n x 16 doubles, d_energy n measured energies (mJ).  Bit-exact with
+ * the reference: every node (feature, threshold, left, right, value), the base score,
+ * the reference energy and the per-round training loss.  params NULL = BoostParams{};
+ * max_depth <= 10 in this build.
+ * Outputs (device, caller-owned): node arrays with capacity
+ * num_trees * (2^(max_depth+1) - 1), tree_offsets[num_trees + 1] (node ranges, tree
+ * order, node indices local to their tree like RegressionTree::nodes),
+ * d_scalars[2] = {base_score, reference_energy_mj}, d_training_loss[num_trees + 1]
+ * (nullable: training_loss_per_round, energy_model.hpp:81-85).
+ * Errors: INSUFFICIENT_DATA (n < 2, host-side); NON_POSITIVE_ENERGY reported by
+ * etune_cu_synchronize with the first offending index; UNSUPPORTED (max_depth > 10). */
+etune_status etune_cu_train(etune_cu_ctx* ctx, const double* d_feat, const double* d_energy, int64_t n,
+                            const etune_boost_params* params, int32_t* d_feature, double* d_threshold,
+                            int32_t* d_left, int32_t* d_right, double* d_value, int64_t* d_tree_offsets,
+                            double* d_scalars, double* d_training_loss /*nullable*/);
+
+/* A forest built from device-resident trained arrays (as written by etune_cu_train);
+ * synchronises the ctx stream, then behaves like etune_cu_forest_create. */
+etune_status etune_cu_forest_from_device(etune_cu_ctx* ctx, const int32_t* d_feature,
+                                         const double* d_threshold, const int32_t* d_left,
+                                         const int32_t* d_right, const double* d_value,
+                                         const int64_t* d_tree_offsets, int64_t num_trees,
+                                         const double* d_scalars, double learning_rate,
+                                         etune_cu_forest** out);
+
 /* ---------------------------------------------------------- reproduction */
 /* reproduce (genetic.hpp:48-51, genetic.cpp:137-187) on device genomes, bit-exact with
  * the reference's ONE sequential std::mt19937_64(seed) stream: offspring i starts from

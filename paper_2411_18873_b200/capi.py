@@ -61,6 +61,11 @@ class GeneticRates(C.Structure):
     _fields_ = [("mutation", C.c_double), ("crossover", C.c_double), ("copy", C.c_double)]
 
 
+class BoostParams(C.Structure):
+    _fields_ = [("num_trees", C.c_int32), ("max_depth", C.c_int32), ("learning_rate", C.c_double),
+                ("min_leaf_weight", C.c_double), ("reg_lambda", C.c_double)]
+
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _PTR = C.c_void_p
@@ -93,6 +98,10 @@ _SIGS = {
     "etune_cu_score": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
+    "etune_cu_train": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(BoostParams), _PTR, _PTR, _PTR, _PTR, _PTR, _PTR,
+                                 _PTR, _PTR]),
+    "etune_cu_forest_from_device": (C.c_int, [_VP, _PTR, _PTR, _PTR, _PTR, _PTR, _PTR, _I64, _PTR, C.c_double,
+                                              C.POINTER(_VP)]),
     "etune_cu_reproduce": (C.c_int, [_VP, _VP, _PTR, _I64, _I64, C.POINTER(GeneticRates), C.c_uint64, _PTR, _PTR,
                                      _PTR]),
 }
@@ -262,6 +271,50 @@ def reproduce(plan: "Plan", parents, n: int, seed: int, rates=(0.85, 0.10, 0.05)
     return out, partner, ids
 
 
+class TrainedModel:
+    """Device-resident output of etune_cu_train (EnergyModel::train, energy_model.cpp:173-243)."""
+
+    def __init__(self, ctx, nodes, offsets, scalars, loss, num_trees, learning_rate, params):
+        self.ctx, self.nodes, self.offsets, self.scalars, self.loss = ctx, nodes, offsets, scalars, loss
+        self.num_trees, self.learning_rate, self.params = num_trees, learning_rate, params
+
+    def host(self):
+        """(feature, threshold, left, right, value, offsets, base_score, reference_energy, loss) on the host."""
+        self.ctx.synchronize()
+        off = self.offsets.cpu().numpy()
+        nn = int(off[-1])
+        fe, th, le, ri, va = (t[:nn].cpu().numpy() for t in self.nodes)
+        sc = self.scalars.cpu().numpy()
+        loss = self.loss.cpu().numpy() if self.loss is not None else None
+        return fe, th, le, ri, va, off, float(sc[0]), float(sc[1]), loss
+
+    def forest(self) -> "Forest":
+        fe, th, le, ri, va = self.nodes
+        h = C.c_void_p()
+        _check(lib().etune_cu_forest_from_device(self.ctx.h, _ptr(fe), _ptr(th), _ptr(le), _ptr(ri), _ptr(va),
+                                                 _ptr(self.offsets), self.num_trees, _ptr(self.scalars),
+                                                 float(self.learning_rate), C.byref(h)))
+        return Forest._wrap(self.ctx, h)
+
+
+def train(ctx: "Context", feats, energy, num_trees: int = 100, max_depth: int = 6, learning_rate: float = 0.1,
+          min_leaf_weight: float = 1e-3, reg_lambda: float = 1.0, with_loss: bool = True) -> TrainedModel:
+    import torch
+    dev = feats.device
+    n = feats.shape[0]
+    cap = max(1, num_trees * ((1 << (max_depth + 1)) - 1))
+    nodes = (torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(cap, dtype=torch.float64, device=dev),
+             torch.empty(cap, dtype=torch.int32, device=dev), torch.empty(cap, dtype=torch.int32, device=dev),
+             torch.empty(cap, dtype=torch.float64, device=dev))
+    off = torch.zeros(num_trees + 1, dtype=torch.int64, device=dev)
+    sc = torch.zeros(2, dtype=torch.float64, device=dev)
+    loss = torch.zeros(num_trees + 1, dtype=torch.float64, device=dev) if with_loss else None
+    p = BoostParams(int(num_trees), int(max_depth), float(learning_rate), float(min_leaf_weight), float(reg_lambda))
+    _check(lib().etune_cu_train(ctx.h, _ptr(feats), _ptr(energy), n, C.byref(p), *[_ptr(t) for t in nodes], _ptr(off),
+                                _ptr(sc), _ptr(loss)))
+    return TrainedModel(ctx, nodes, off, sc, loss, num_trees, learning_rate, p)
+
+
 class Forest:
     def __init__(self, ctx: Context, feature, threshold, left, right, value, offsets, base_score: float,
                  learning_rate: float):
@@ -275,6 +328,12 @@ class Forest:
                                             va.ctypes.data, off.ctypes.data, len(off) - 1, float(base_score),
                                             float(learning_rate), C.byref(h)))
         self.h = h
+
+    @staticmethod
+    def _wrap(ctx: Context, h) -> "Forest":
+        f = Forest.__new__(Forest)
+        f.ctx, f.h, f._keep = ctx, h, []
+        return f
 
     @staticmethod
     def from_flat(ctx: Context, f) -> "Forest":

@@ -46,6 +46,7 @@ struct etune_cu_plan {
 };
 
 struct CompiledScore {
+    bool walk = false;        // compiled form unsupported / too large: general tree-walk kernel
     uint8_t* d_blob = nullptr;
     uint32_t bytes = 0;
     int mask_bits = 32;
@@ -118,11 +119,16 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     std::vector<uint8_t> blob;
     std::string err;
     CompiledScore cs;
-    if (etune_status st = build_score_blob(f->host, p->build, &blob, &cs.stats, &err)) return fail(st, err);
+    const etune_status bst = build_score_blob(f->host, p->build, &blob, &cs.stats, &err);
+    if (bst != ETUNE_OK && bst != ETUNE_ERR_UNSUPPORTED) return fail(bst, err);
     const int cap = max_dynamic_smem(f->ctx->device);
-    if (blob.size() > size_t(cap)) {
-        return fail(ETUNE_ERR_UNSUPPORTED, "compiled forest (" + std::to_string(blob.size()) +
-                                               " B) exceeds shared memory (" + std::to_string(cap) + " B)");
+    if (bst == ETUNE_ERR_UNSUPPORTED || blob.size() > size_t(cap)) {
+        // the general path: features + the reference tree walk (any forest)
+        if (p->build.hdr.total > uint32_t(cap)) return fail(ETUNE_ERR_UNSUPPORTED, "plan tables exceed shared memory");
+        cs.walk = true;
+        auto res = f->compiled.emplace(p->serial, cs);
+        *out = &res.first->second;
+        return ETUNE_OK;
     }
     CU(cudaMalloc(&cs.d_blob, blob.size()));
     CU(cudaMemcpyAsync(cs.d_blob, blob.data(), blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
@@ -136,6 +142,14 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;
+}
+
+cudaError_t run_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
+                      const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids) {
+    if (cs->walk)
+        return launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
+                                 d_pred, d_ids);
+    return launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params);
 }
 
 }  // namespace
@@ -377,7 +391,7 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
-    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params));
+    CU(run_score(c, p, f, cs, d_genome, n, d_pred, d_ids));
     return ETUNE_OK;
 }
 
@@ -405,11 +419,60 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         CU(cudaMemcpyAsync(d_sched, h_sched + lo, size_t(m) * sizeof(etune_schedule), cudaMemcpyHostToDevice,
                            c->stream));
         CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, m, d_gen, lo));
-        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_gen, m, d_pred, h_ids ? d_ids : nullptr, cs->mask_bits, *cs->params));
+        CU(run_score(c, p, f, cs, d_gen, m, d_pred, h_ids ? d_ids : nullptr));
         CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
         if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
     }
     return etune_cu_synchronize(c, first_bad);
+}
+
+etune_status etune_cu_train(etune_cu_ctx* c, const double* d_feat, const double* d_energy, int64_t n,
+                            const etune_boost_params* params, int32_t* d_feature, double* d_threshold,
+                            int32_t* d_left, int32_t* d_right, double* d_value, int64_t* d_off, double* d_scalars,
+                            double* d_loss) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    if (n < 2) return fail(ETUNE_ERR_INSUFFICIENT_DATA, "training needs at least 2 samples, got " + std::to_string(n));
+    if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "more than 2^31 samples");
+    etune_boost_params bp;
+    etune_default_boost_params(&bp);
+    if (params) bp = *params;
+    if (bp.num_trees < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "num_trees < 0");
+    if (bp.max_depth < 0 || bp.max_depth > train_max_depth())
+        return fail(ETUNE_ERR_UNSUPPORTED, "max_depth outside [0, " + std::to_string(train_max_depth()) + "]");
+    if (!d_feat || !d_energy || !d_feature || !d_threshold || !d_left || !d_right || !d_value || !d_off ||
+        !d_scalars)
+        return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
+    if (etune_status st = ensure_scratch(c, train_scratch_bytes(n))) return st;
+    CU(launch_train(c->lc(), d_feat, d_energy, n, bp.num_trees, bp.max_depth, bp.learning_rate, bp.min_leaf_weight,
+                    bp.reg_lambda, d_feature, d_threshold, d_left, d_right, d_value, d_off, d_scalars, d_loss,
+                    c->scratch));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_forest_from_device(etune_cu_ctx* c, const int32_t* d_feature, const double* d_threshold,
+                                         const int32_t* d_left, const int32_t* d_right, const double* d_value,
+                                         const int64_t* d_off, int64_t num_trees, const double* d_scalars,
+                                         double learning_rate, etune_cu_forest** out) {
+    if (!c || !out || !d_off || !d_scalars || num_trees < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    if (etune_status st = etune_cu_synchronize(c, nullptr)) return st;
+    std::vector<int64_t> off(size_t(num_trees) + 1, 0);
+    double sc[2] = {0, 0};
+    CU(cudaMemcpy(off.data(), d_off, off.size() * 8, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(sc, d_scalars, sizeof(sc), cudaMemcpyDeviceToHost));
+    const int64_t nn = off[size_t(num_trees)];
+    if (nn < 0) return fail(ETUNE_ERR_CONSISTENCY, "negative node count");
+    const size_t m = static_cast<size_t>(nn);
+    std::vector<int32_t> fe(m), le(m), ri(m);
+    std::vector<double> th(m), va(m);
+    if (nn > 0) {
+        CU(cudaMemcpy(fe.data(), d_feature, size_t(nn) * 4, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(le.data(), d_left, size_t(nn) * 4, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(ri.data(), d_right, size_t(nn) * 4, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(th.data(), d_threshold, size_t(nn) * 8, cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(va.data(), d_value, size_t(nn) * 8, cudaMemcpyDeviceToHost));
+    }
+    return etune_cu_forest_create(c, fe.data(), th.data(), le.data(), ri.data(), va.data(), off.data(), num_trees,
+                                  sc[0], learning_rate, out);
 }
 
 etune_status etune_cu_reproduce(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np,

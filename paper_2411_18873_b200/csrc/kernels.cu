@@ -246,6 +246,34 @@ __global__ void __launch_bounds__(kThreads) counters_kernel(const uint8_t* __res
 }
 
 // ---------------------------------------------------------------- features
+// features_from_counters (features.cpp:15-46) through the plan's tables.
+__device__ __forceinline__ void plan_features(const uint8_t* P, const PlanHdr& H, const Knobs& c, double f[16]) {
+    const int nd1 = H.nd[1], nd2 = H.nd[2];
+    const uint32_t block = c.r[0].threads * c.r[1].threads * c.r[2].threads;
+    const uint32_t gk = at<uint16_t>(P, H.off_gridkey)[(c.r[0].db * nd1 + c.r[1].db) * nd2 + c.r[2].db];
+    const GridRec gr = at<GridRec>(P, H.off_grid)[gk];
+    const GlbRec gl = at<GlbRec>(P, H.off_glb2)[c.r[1].dbt * nd2 + c.r[2].dbt];
+    const double lint = at<double>(P, H.off_int2)[c.r[1].dpt * nd2 + c.r[2].dpt];
+    const BlockRec br = at<BlockRec>(P, H.off_block)[block <= 1024 ? block : 1024];
+    const int lv = (c.r[0].pt > 1) + (c.r[1].pt > 1) + (c.r[2].pt > 1);
+    f[0] = H.f0;
+    f[1] = lint;
+    f[2] = gl.lg_glb_ld;
+    f[3] = H.f3;
+    f[4] = lint;
+    f[5] = gl.lg_glb_ld;
+    f[6] = static_cast<double>(c.vec);
+    f[7] = static_cast<double>(c.unroll);
+    f[8] = at<double>(P, H.off_lvl)[lv];
+    f[9] = at<double>(P, H.off_ptn)[c.r[2].dpt];
+    f[10] = at<double>(P, H.off_steps)[c.k];
+    f[11] = gr.lg_grid;
+    f[12] = br.lg_block;
+    f[13] = __dmul_rn(gr.a, br.b);
+    f[14] = gr.lg_active;
+    f[15] = gl.f15;
+}
+
 __global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
                                                             int use_smem, const uint64_t* __restrict__ genome,
                                                             int64_t n, double* __restrict__ feat,
@@ -258,36 +286,65 @@ __global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __res
         P = reinterpret_cast<const uint8_t*>(smem);
     }
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
-    const int nd1 = H.nd[1], nd2 = H.nd[2];
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const Knobs c = load_knobs(P, H, genome[i]);
-        const uint32_t block = c.r[0].threads * c.r[1].threads * c.r[2].threads;
-        const uint32_t gk = at<uint16_t>(P, H.off_gridkey)[(c.r[0].db * nd1 + c.r[1].db) * nd2 + c.r[2].db];
-        const GridRec gr = at<GridRec>(P, H.off_grid)[gk];
-        const GlbRec gl = at<GlbRec>(P, H.off_glb2)[c.r[1].dbt * nd2 + c.r[2].dbt];
-        const double lint = at<double>(P, H.off_int2)[c.r[1].dpt * nd2 + c.r[2].dpt];
-        const BlockRec br = at<BlockRec>(P, H.off_block)[block <= 1024 ? block : 1024];
-        const int lv = (c.r[0].pt > 1) + (c.r[1].pt > 1) + (c.r[2].pt > 1);
         double f[16];  // features.cpp:27-45 layout
-        f[0] = H.f0;
-        f[1] = lint;
-        f[2] = gl.lg_glb_ld;
-        f[3] = H.f3;
-        f[4] = lint;
-        f[5] = gl.lg_glb_ld;
-        f[6] = static_cast<double>(c.vec);
-        f[7] = static_cast<double>(c.unroll);
-        f[8] = at<double>(P, H.off_lvl)[lv];
-        f[9] = at<double>(P, H.off_ptn)[c.r[2].dpt];
-        f[10] = at<double>(P, H.off_steps)[c.k];
-        f[11] = gr.lg_grid;
-        f[12] = br.lg_block;
-        f[13] = __dmul_rn(gr.a, br.b);
-        f[14] = gr.lg_active;
-        f[15] = gl.f15;
+        plan_features(P, H, c, f);
         double2* o = reinterpret_cast<double2*>(feat + 16 * i);
 #pragma unroll
         for (int j = 0; j < 8; ++j) o[j] = make_double2(f[2 * j], f[2 * j + 1]);
+        if (ids) ids[i] = candidate_hash(H.fnv_prefix, c);
+    }
+}
+
+// RegressionTree::eval summed in tree order (energy_model.cpp:36-44, 245-249)
+__device__ __forceinline__ double walk_forest(const PredictHdr& H, const int32_t* roots, const GNode* nodes,
+                                              const double f[16]) {
+    double sum = 0.0;
+    for (int t = 0; t < H.ntrees; ++t) {
+        int node = roots[t];
+        int feature = nodes[node].feature;
+        while (feature >= 0) {
+            double v = 0.0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v = (j == feature) ? f[j] : v;
+            node = v < nodes[node].thr ? nodes[node].left : nodes[node].right;
+            feature = nodes[node].feature;
+        }
+        sum = __dadd_rn(sum, nodes[node].value);
+    }
+    const double p = __dadd_rn(H.base, __dmul_rn(H.lr, sum));
+    return (1e-6 < p) ? p : 1e-6;
+}
+
+// General scoring path for forests whose compiled form does not fit shared memory
+// (many outcome classes, > 64 leaves per tree, > 1000 trees): features from the plan
+// tables, then the reference's tree walk over the node array (shared memory when it
+// fits, else L1/L2-cached global).
+__global__ void __launch_bounds__(kThreads) score_walk_kernel(const uint8_t* __restrict__ gplan, uint32_t plan_bytes,
+                                                              const uint8_t* __restrict__ gpred, uint32_t pred_bytes,
+                                                              int pred_in_smem, const uint64_t* __restrict__ genome,
+                                                              int64_t n, double* __restrict__ pred,
+                                                              uint64_t* __restrict__ ids) {
+    extern __shared__ int4 smem[];
+    stage(gplan, plan_bytes, smem);
+    const uint8_t* P = reinterpret_cast<const uint8_t*>(smem);
+    const uint8_t* Q = gpred;
+    if (pred_in_smem) {
+        int4* dst = smem + (plan_bytes >> 4);
+        stage(gpred, pred_bytes, dst);
+        Q = reinterpret_cast<const uint8_t*>(dst);
+    }
+    __syncthreads();
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const PredictHdr& QH = *reinterpret_cast<const PredictHdr*>(Q);
+    const int32_t* roots = at<int32_t>(Q, QH.off_roots);
+    const GNode* nodes = at<GNode>(Q, QH.off_nodes);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const Knobs c = load_knobs(P, H, __ldg(genome + i));
+        double f[16];
+        plan_features(P, H, c, f);
+        pred[i] = walk_forest(QH, roots, nodes, f);
         if (ids) ids[i] = candidate_hash(H.fnv_prefix, c);
     }
 }
@@ -343,21 +400,7 @@ __global__ void __launch_bounds__(kThreads) predict_kernel(const uint8_t* __rest
             f[2 * j] = v.x;
             f[2 * j + 1] = v.y;
         }
-        double sum = 0.0;
-        for (int t = 0; t < H.ntrees; ++t) {  // energy_model.cpp:36-44, 245-249
-            int node = __ldg(roots + t);
-            int feature = __ldg(&nodes[node].feature);
-            while (feature >= 0) {
-                double v = 0.0;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v = (j == feature) ? f[j] : v;
-                node = v < __ldg(&nodes[node].thr) ? __ldg(&nodes[node].left) : __ldg(&nodes[node].right);
-                feature = __ldg(&nodes[node].feature);
-            }
-            sum = __dadd_rn(sum, __ldg(&nodes[node].value));
-        }
-        const double p = __dadd_rn(H.base, __dmul_rn(H.lr, sum));
-        pred[i] = (1e-6 < p) ? p : 1e-6;
+        pred[i] = walk_forest(H, roots, nodes, f);
     }
 }
 
@@ -439,6 +482,28 @@ cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t by
     if (n <= 0) return cudaSuccess;
     return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp)
                            : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp);
+}
+
+cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,
+                              uint32_t pred_bytes, const uint64_t* d_genome, int64_t n, double* d_out,
+                              uint64_t* d_ids) {
+    if (n <= 0) return cudaSuccess;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (plan_bytes > uint32_t(optin)) return cudaErrorInvalidValue;
+    const int pred_in_smem = size_t(plan_bytes) + pred_bytes <= size_t(optin) ? 1 : 0;
+    const size_t sm = plan_bytes + (pred_in_smem ? pred_bytes : 0);
+    cudaError_t e = cudaFuncSetAttribute(score_walk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_walk_kernel, kThreads, sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    score_walk_kernel<<<grid_for(c, n, per_sm), kThreads, sm, c.stream>>>(d_plan, plan_bytes, d_pred, pred_bytes,
+                                                                          pred_in_smem, d_genome, n, d_out, d_ids);
+    note_launches(1);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_blob, uint32_t /*bytes*/, const double* d_feat,

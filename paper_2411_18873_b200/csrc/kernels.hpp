@@ -32,6 +32,10 @@ cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
                          const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
                          int mask_bits, const ForestParams& fp);
+// General path: features + reference tree walk (any forest the reference can train).
+cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,
+                              uint32_t pred_bytes, const uint64_t* d_genome, int64_t n, double* d_out,
+                              uint64_t* d_ids);
 cudaError_t launch_predict(const LaunchCtx& c, const uint8_t* d_pred_blob, uint32_t bytes,
                            const double* d_feat, int64_t n, double* d_pred);
 
@@ -46,6 +50,14 @@ size_t breed_state_bytes();
 cudaError_t launch_breed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
                          const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
                          uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_state);
+
+// EnergyModel::train (energy_model.cpp:173-243), bit-exact; scratch from train_scratch_bytes(n).
+size_t train_scratch_bytes(int64_t n);
+int train_max_depth();
+cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double* d_energy, int64_t n, int num_trees,
+                         int max_depth, double lr, double mlw, double lambda, int32_t* o_feature, double* o_thr,
+                         int32_t* o_left, int32_t* o_right, double* o_value, int64_t* o_off, double* o_scalars,
+                         double* o_loss, void* scratch);
 
 // process-wide count of kernel launches (incremented by every launcher)
 void note_launches(int k);

@@ -198,3 +198,26 @@ def test_score_host_e2e(golden, oracle, ctx, capi):
     with pytest.raises(capi.EtuneError) as e:
         fo.score_host(plan, s, pred, hid)
     assert e.value.code == 4 and e.value.index == 299999
+
+
+@pytest.mark.parametrize("depth,smooth", [(8, False), (6, True)])
+def test_score_general_walk_path(oracle, ctx, capi, depth, smooth):
+    """Forests whose compiled form is unsupported (> 64 leaves per tree) or does not fit
+    shared memory (hundreds of outcome classes) take the general features + tree-walk
+    kernel; results stay bit-exact."""
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    s, _ = oracle.sample_random(op, 3000, 77)
+    f = oracle.features(op, s)
+    if smooth:
+        e = 1.0 + (f[:, 2] * 0.2 + f[:, 13] + f[:, 10] * 0.1) % 1.9
+    else:
+        e = 1.0 + (f[:, 1] * 0.37 + f[:, 9] * 0.11 + f[:, 13]) % 2.3
+    fl, _, _ = oracle.train(f, e, num_trees=60, max_depth=depth, min_leaf_weight=0.0)
+    pop, ids = oracle.sample_random(op, 40000, 5)
+    ref = oracle.predict(fl, oracle.features(op, pop))
+    plan = capi.Plan(ctx, op)
+    fo = capi.Forest.from_flat(ctx, fl)
+    pred, dids = fo.score(plan, plan.encode(dev(pop)), with_ids=True)
+    ctx.synchronize()
+    assert (bits(pred) == ref.view(np.uint64)).all()
+    assert (capi.as_u64(dids) == ids).all()
