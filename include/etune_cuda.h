@@ -226,6 +226,19 @@ etune_status etune_cu_train(etune_cu_ctx* ctx, const double* d_feat, const doubl
                             int32_t* d_left, int32_t* d_right, double* d_value, int64_t* d_tree_offsets,
                             double* d_scalars, double* d_training_loss /*nullable*/);
 
+/* energy_loss (Eq. 1; energy_model.hpp:19-24, energy_model.cpp:23-34) for n samples:
+ * d_out[3i..3i+2] = {value, gradient, hessian}.  NON_POSITIVE_ENERGY (first index) at
+ * etune_cu_synchronize. */
+etune_status etune_cu_energy_loss(etune_cu_ctx* ctx, const double* d_pred, const double* d_meas, int64_t n,
+                                  double* d_out);
+
+/* snr_db (energy_model.hpp:108-109, energy_model.cpp:352-370): the two sums are formed
+ * on the device in the reference's order; the final scalar 10*log10(signal/error),
+ * capped at 100 dB, is taken with the platform libm like the reference.  Synchronous.
+ * Errors: EMPTY_INPUT (n == 0), NON_POSITIVE_ENERGY (with *first_bad). */
+etune_status etune_cu_snr_db(etune_cu_ctx* ctx, const double* d_pred, const double* d_meas, int64_t n,
+                             double* h_out, int64_t* first_bad /*nullable*/);
+
 /* A forest built from device-resident trained arrays (as written by etune_cu_train);
  * synchronises the ctx stream, then behaves like etune_cu_forest_create. */
 etune_status etune_cu_forest_from_device(etune_cu_ctx* ctx, const int32_t* d_feature,
@@ -259,6 +272,28 @@ etune_status etune_cu_reproduce(etune_cu_ctx* ctx, const etune_cu_plan* plan,
  * d_idx (int64).  Scratch is taken from the ctx. */
 etune_status etune_cu_topk(etune_cu_ctx* ctx, const double* d_score, int64_t n, int64_t k,
                            int64_t* d_idx);
+
+/* ------------------------------------------------------- multi-GPU (NCCL) */
+/* One rank per GPU over NVLink/NVSwitch.  The population shards by index: rank r owns
+ * the contiguous global range [global_offset, global_offset + n) with offsets
+ * increasing with rank.  NCCL carries only the per-shard top-k records and the
+ * broadcast of trained model arrays (north_star); everything else is shard-local. */
+#define ETUNE_NCCL_UNIQUE_ID_BYTES 128
+etune_status etune_cu_nccl_unique_id(void* out_id /* ETUNE_NCCL_UNIQUE_ID_BYTES */);
+/* Collective over all ranks: binds an NCCL communicator to the ctx (its device/stream). */
+etune_status etune_cu_ctx_attach_nccl(etune_cu_ctx* ctx, const void* unique_id, int nranks, int rank);
+
+/* Population-sharded selection: every rank passes its shard's scores; on return every
+ * rank holds the SAME k global indices (and scores, nullable), sorted by
+ * (score asc, global index asc) — identical to etune_cu_topk over the concatenated
+ * population.  Local top-k -> ncclAllGather of (score, index) records -> on-device
+ * merge.  Without an attached communicator it is the single-rank case. */
+etune_status etune_cu_topk_sharded(etune_cu_ctx* ctx, const double* d_score, int64_t n,
+                                   int64_t global_offset, int64_t k, int64_t* d_idx_global,
+                                   double* d_score_out /*nullable*/);
+
+/* ncclBroadcast of `bytes` device bytes from `root` (trained forest arrays). */
+etune_status etune_cu_broadcast(etune_cu_ctx* ctx, void* d_buf, int64_t bytes, int root);
 
 #ifdef __cplusplus
 }

@@ -102,6 +102,12 @@ _SIGS = {
                                  _PTR, _PTR]),
     "etune_cu_forest_from_device": (C.c_int, [_VP, _PTR, _PTR, _PTR, _PTR, _PTR, _PTR, _I64, _PTR, C.c_double,
                                               C.POINTER(_VP)]),
+    "etune_cu_energy_loss": (C.c_int, [_VP, _PTR, _PTR, _I64, _PTR]),
+    "etune_cu_snr_db": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(C.c_double), C.POINTER(_I64)]),
+    "etune_cu_nccl_unique_id": (C.c_int, [_PTR]),
+    "etune_cu_ctx_attach_nccl": (C.c_int, [_VP, _PTR, C.c_int, C.c_int]),
+    "etune_cu_topk_sharded": (C.c_int, [_VP, _PTR, _I64, _I64, _I64, _PTR, _PTR]),
+    "etune_cu_broadcast": (C.c_int, [_VP, _PTR, _I64, C.c_int]),
     "etune_cu_reproduce": (C.c_int, [_VP, _VP, _PTR, _I64, _I64, C.POINTER(GeneticRates), C.c_uint64, _PTR, _PTR,
                                      _PTR]),
 }
@@ -368,6 +374,48 @@ class Forest:
         st = lib().etune_cu_score_host(self.ctx.h, plan.h, self.h, _ptr(sched), n, _ptr(pred), _ptr(ids),
                                        C.byref(bad))
         _check(st, bad.value)
+
+
+def energy_loss(ctx: Context, pred, meas):
+    """energy_loss (Eq. 1) per sample -> (n, 3) {value, gradient, hessian}."""
+    import torch
+    out = torch.empty((pred.shape[0], 3), dtype=torch.float64, device=pred.device)
+    _check(lib().etune_cu_energy_loss(ctx.h, _ptr(pred), _ptr(meas), pred.shape[0], _ptr(out)))
+    return out
+
+
+def snr_db(ctx: Context, pred, meas) -> float:
+    out = C.c_double()
+    bad = C.c_int64(-1)
+    st = lib().etune_cu_snr_db(ctx.h, _ptr(pred), _ptr(meas), pred.shape[0], C.byref(out), C.byref(bad))
+    _check(st, bad.value)
+    return out.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().etune_cu_nccl_unique_id(buf))
+    return buf.raw
+
+
+def attach_nccl(ctx: Context, unique_id: bytes, nranks: int, rank: int):
+    buf = C.create_string_buffer(bytes(unique_id), 128)
+    _check(lib().etune_cu_ctx_attach_nccl(ctx.h, buf, int(nranks), int(rank)))
+
+
+def topk_sharded(ctx: Context, score, global_offset: int, k: int):
+    """Population-sharded keep-the-best: identical (global idx, score) on every rank."""
+    import torch
+    idx = torch.empty(k, dtype=torch.int64, device=score.device)
+    sc = torch.empty(k, dtype=torch.float64, device=score.device)
+    _check(lib().etune_cu_topk_sharded(ctx.h, _ptr(score), score.shape[0], int(global_offset), int(k), _ptr(idx),
+                                       _ptr(sc)))
+    return idx, sc
+
+
+def broadcast(ctx: Context, t, root: int = 0):
+    _check(lib().etune_cu_broadcast(ctx.h, _ptr(t), t.numel() * t.element_size(), int(root)))
+    return t
 
 
 def topk(ctx: Context, score, k: int):

@@ -3,7 +3,10 @@
 // kernel in kernels.cu / sort.cu.  There is deliberately no CPU fallback — without
 // an sm_100 device every entry point returns ETUNE_ERR_NO_DEVICE.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -35,6 +38,10 @@ struct etune_cu_ctx {
     size_t io_bytes = 0;
     void* breed = nullptr;  // BreedState + parent ids
     size_t breed_bytes = 0;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    void* shard = nullptr;  // sharded-selection records
+    size_t shard_bytes = 0;
     LaunchCtx lc() const { return LaunchCtx{stream, sm_count, d_err}; }
 };
 
@@ -223,6 +230,8 @@ etune_status etune_cu_ctx_destroy(etune_cu_ctx* c) {
     cudaFree(c->scratch);
     cudaFree(c->io);
     cudaFree(c->breed);
+    cudaFree(c->shard);
+    if (c->comm) ncclCommDestroy(c->comm);
     if (c->own_stream) cudaStreamDestroy(c->stream);
     delete c;
     return ETUNE_OK;
@@ -449,6 +458,31 @@ etune_status etune_cu_train(etune_cu_ctx* c, const double* d_feat, const double*
     return ETUNE_OK;
 }
 
+etune_status etune_cu_energy_loss(etune_cu_ctx* c, const double* d_pred, const double* d_meas, int64_t n,
+                                  double* d_out) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    if (n < 0 || (n > 0 && (!d_pred || !d_meas || !d_out))) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad buffers");
+    CU(launch_energy_loss(c->lc(), d_pred, d_meas, n, d_out));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_snr_db(etune_cu_ctx* c, const double* d_pred, const double* d_meas, int64_t n, double* h_out,
+                             int64_t* first_bad) {
+    if (!c || !h_out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    if (first_bad) *first_bad = -1;
+    if (n == 0) return fail(ETUNE_ERR_EMPTY_INPUT, "snr_db requires non-empty input");
+    if (n < 0 || !d_pred || !d_meas) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad buffers");
+    if (etune_status st = ensure_scratch(c, 256)) return st;
+    double* d2 = static_cast<double*>(c->scratch);
+    CU(launch_snr_sums(c->lc(), d_pred, d_meas, n, d2));
+    double sums[2] = {0, 0};
+    CU(cudaMemcpyAsync(sums, d2, sizeof(sums), cudaMemcpyDeviceToHost, c->stream));
+    if (etune_status st = etune_cu_synchronize(c, first_bad)) return st;
+    // energy_model.cpp:368-369
+    *h_out = sums[1] <= 0.0 ? 100.0 : std::min(100.0, 10.0 * std::log10(sums[0] / sums[1]));
+    return ETUNE_OK;
+}
+
 etune_status etune_cu_forest_from_device(etune_cu_ctx* c, const int32_t* d_feature, const double* d_threshold,
                                          const int32_t* d_left, const int32_t* d_right, const double* d_value,
                                          const int64_t* d_off, int64_t num_trees, const double* d_scalars,
@@ -516,6 +550,97 @@ etune_status etune_cu_topk(etune_cu_ctx* c, const double* d_score, int64_t n, in
     if (!d_score || !d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
     if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
     CU(launch_topk(c->lc(), d_score, n, k, d_idx, c->scratch));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_nccl_unique_id(void* out_id) {
+    if (!out_id) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null id");
+    static_assert(sizeof(ncclUniqueId) == ETUNE_NCCL_UNIQUE_ID_BYTES, "NCCL id size");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(ETUNE_ERR_CUDA, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out_id, &id, sizeof(id));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_ctx_attach_nccl(etune_cu_ctx* c, const void* unique_id, int nranks, int rank) {
+    if (!c || !unique_id || nranks < 1 || rank < 0 || rank >= nranks)
+        return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+    CU(cudaSetDevice(c->device));
+    if (c->comm) {
+        ncclCommDestroy(c->comm);
+        c->comm = nullptr;
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id, sizeof(id));
+    const ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        c->comm = nullptr;
+        return fail(ETUNE_ERR_CUDA, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    c->nranks = nranks;
+    c->rank = rank;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_topk_sharded(etune_cu_ctx* c, const double* d_score, int64_t n, int64_t goff, int64_t k,
+                                   int64_t* d_idx, double* d_sc) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    if (n < 0 || k < 0 || goff < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "negative size");
+    if (k == 0) return ETUNE_OK;
+    if (!d_idx || (n > 0 && !d_score)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
+    const int W = c->comm ? c->nranks : 1;
+    const int64_t kl = std::min(k, n);
+    // records: [k local scores | k local gidx | W*k gathered scores | W*k gathered gidx | k positions]
+    const size_t need = size_t(k) * 16 * (1 + size_t(W)) + size_t(k) * 8 + 1024;
+    if (c->shard_bytes < need) {
+        if (c->shard) {
+            CU(cudaStreamSynchronize(c->stream));
+            CU(cudaFree(c->shard));
+            c->shard = nullptr;
+            c->shard_bytes = 0;
+        }
+        CU(cudaMalloc(&c->shard, need));
+        c->shard_bytes = need;
+    }
+    double* ls = static_cast<double*>(c->shard);
+    int64_t* lg = reinterpret_cast<int64_t*>(ls + k);
+    double* gs = reinterpret_cast<double*>(lg + k);
+    int64_t* gg = reinterpret_cast<int64_t*>(gs + size_t(W) * k);
+    int64_t* pos = gg + size_t(W) * k;
+    int64_t* lidx = pos;  // local selection reuses the position buffer
+    if (kl > 0) {
+        if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "shard >= 2^31");
+        if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
+        CU(launch_topk(c->lc(), d_score, n, kl, lidx, c->scratch));
+    }
+    CU(launch_pack_records(c->lc(), d_score, lidx, kl, k, goff, ls, lg));
+    if (W > 1) {
+        ncclResult_t r = ncclGroupStart();
+        if (r == ncclSuccess) r = ncclAllGather(ls, gs, size_t(k), ncclFloat64, c->comm, c->stream);
+        if (r == ncclSuccess) r = ncclAllGather(lg, gg, size_t(k), ncclInt64, c->comm, c->stream);
+        const ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(ETUNE_ERR_CUDA, std::string("ncclAllGather: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+    } else {
+        gs = ls;
+        gg = lg;
+    }
+    // shards are contiguous and ascending by rank, each list sorted by (score, gidx):
+    // (score, position) order over the rank-major concatenation == (score, gidx) order
+    const int64_t tot = int64_t(W) * k;
+    if (etune_status st = ensure_scratch(c, topk_scratch_bytes(tot))) return st;
+    CU(launch_topk(c->lc(), gs, tot, k, pos, c->scratch));
+    CU(launch_gather_records(c->lc(), gs, gg, pos, k, d_idx, d_sc));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_broadcast(etune_cu_ctx* c, void* d_buf, int64_t bytes, int root) {
+    if (!c || bytes < 0 || (bytes > 0 && !d_buf)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (!c->comm || c->nranks == 1 || bytes == 0) return ETUNE_OK;
+    if (root < 0 || root >= c->nranks) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad root");
+    const ncclResult_t r = ncclBroadcast(d_buf, d_buf, size_t(bytes), ncclUint8, root, c->comm, c->stream);
+    if (r != ncclSuccess) return fail(ETUNE_ERR_CUDA, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
     return ETUNE_OK;
 }
 

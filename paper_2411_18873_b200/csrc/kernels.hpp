@@ -59,6 +59,20 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
                          int32_t* o_left, int32_t* o_right, double* o_value, int64_t* o_off, double* o_scalars,
                          double* o_loss, void* scratch);
 
+// energy_loss (Eq. 1) per sample -> out[3*i..] = {value, gradient, hessian}
+cudaError_t launch_energy_loss(const LaunchCtx& c, const double* d_pred, const double* d_meas, int64_t n,
+                               double* d_out3);
+// snr_db's sequential sums {signal, error}
+cudaError_t launch_snr_sums(const LaunchCtx& c, const double* d_pred, const double* d_meas, int64_t n,
+                            double* d_out2);
+
+// sharded selection helpers (model.cu): records of the local top-k (padded to k with
+// +inf / INT64_MAX), and the final gather of (gidx, score) by merged positions
+cudaError_t launch_pack_records(const LaunchCtx& c, const double* d_score, const int64_t* d_lidx, int64_t kl,
+                                int64_t k, int64_t goff, double* d_rs, int64_t* d_rg);
+cudaError_t launch_gather_records(const LaunchCtx& c, const double* d_gs, const int64_t* d_gg, const int64_t* d_pos,
+                                  int64_t k, int64_t* d_idx, double* d_sc);
+
 // process-wide count of kernel launches (incremented by every launcher)
 void note_launches(int k);
 uint64_t launch_count();
