@@ -156,6 +156,14 @@ etune_status etune_cu_encode(etune_cu_ctx* ctx, const etune_cu_plan* plan,
 etune_status etune_cu_decode(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                              const uint64_t* d_genome, int64_t n, etune_schedule* d_sched);
 
+/* sample_random (space.hpp:80-82, space.cpp:170-251) on the device, bit-exact with
+ * the reference's std::mt19937_64(seed) stream: n distinct legal genomes in the
+ * reference's order (d_ids nullable).  Synchronous (the attempt count is data
+ * dependent).  Errors: VALIDATION (n < 1), SPACE_EXHAUSTED (fewer than n legal
+ * schedules, or the reference's attempt budget 10000 + 1000 n exceeded). */
+etune_status etune_cu_sample_random(etune_cu_ctx* ctx, const etune_cu_plan* plan, int64_t n,
+                                    uint64_t seed, uint64_t* d_genome, uint64_t* d_ids /*nullable*/);
+
 /* candidate_id (space.hpp:32, space.cpp:22-45) */
 etune_status etune_cu_candidate_ids(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                     const uint64_t* d_genome, int64_t n, uint64_t* d_ids);
@@ -167,6 +175,19 @@ etune_status etune_cu_counters(etune_cu_ctx* ctx, const etune_cu_plan* plan,
 etune_status etune_cu_features(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                const uint64_t* d_genome, int64_t n, double* d_feat,
                                uint64_t* d_ids);
+
+/* ------------------------------------------------------------ measurement */
+/* SimBackend (measure.hpp:102-114) on device genomes, with the plan's DeviceConfig:
+ * sim_true_power_and_latency (measure.hpp:29-41) and nvml_sim_measure's
+ * sampler average (measure.hpp:43-60).  d_latency_ms is required
+ * (measure_latency_ms); d_power_w / d_energy_mj / d_iterations are nullable — all
+ * three NULL is the cheap latency-only evaluation used by the latency filter.
+ * The reference ships no implementation of these; parity is against the repo's CPU
+ * restatement (oracle/), whose operation order and noise generator (Irwin-Hall over
+ * splitmix64, no libm) this kernel follows bit for bit. */
+etune_status etune_cu_sim_measure(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                  const uint64_t* d_genome, int64_t n, double* d_latency_ms,
+                                  double* d_power_w, double* d_energy_mj, int64_t* d_iterations);
 
 /* ------------------------------------------------------------- cost model */
 /* EnergyModel trees in the reference's flat TreeNode form (energy_model.hpp:45-57):

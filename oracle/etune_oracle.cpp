@@ -531,6 +531,80 @@ int orc_enumerate(const int64_t* op, const int64_t* limits, int64_t cap, int64_t
     return OK;
 }
 
+// ------------------------------------------------------- measurement (sim)
+// The reference declares SimBackend / sim_true_power_and_latency / nvml_sim_measure
+// (measure.hpp:29-60, 102-114) but ships no implementation; SPEC:314-322 fixes the
+// formula: latency = max(compute, memory, floor), power = constant + static*active +
+// dynamic_energy / latency.  This restatement (parity unpinned by the reference) fixes
+// the operation order, and the sampler noise is made bit-reproducible on any IEEE
+// machine: z = (sum of 12 uniforms from splitmix64) - 6 (Irwin-Hall), no libm.  The
+// device kernel (paper_2411_18873_b200/csrc/measure.cu) follows it operation by
+// operation.  Constants: 1000 iterations / 2 s sample window, samples
+// capped at 4096 per measurement.
+namespace {
+uint64_t splitmix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+struct SimDev {
+    double num_sms, constant, static_sm, e_flop, e_glb, e_shared, tput, bw, floor_ms, hz, warmup, sigma;
+    uint64_t seed;
+};
+void sim_measure(const Counters& c, const SimDev& d, uint64_t id, double* out4) {
+    const double active = static_cast<double>(c.active);
+    const double compute_s = static_cast<double>(c.flops) / ((active * d.tput) * c.sm_eff);
+    const double memory_s = static_cast<double>(c.glb_ld + c.glb_st) / d.bw;
+    double lat_ms = (compute_s > memory_s ? compute_s : memory_s) * 1000.0;
+    if (lat_ms < d.floor_ms) lat_ms = d.floor_ms;
+    const double dyn_mj = ((static_cast<double>(c.flops) * d.e_flop + static_cast<double>(c.glb_ld + c.glb_st) * d.e_glb) +
+                           static_cast<double>(c.shared_ld + c.shared_st) * d.e_shared) * 1e-6;
+    const double power = (d.constant + d.static_sm * active) + dyn_mj / lat_ms;
+    const double lat_s = lat_ms / 1000.0;
+    const double want = std::ceil(2.0 / lat_s);
+    const int64_t iters = want > 1000.0 ? static_cast<int64_t>(want) : 1000;
+    double sf = std::floor(static_cast<double>(iters) * lat_s * d.hz);
+    if (sf < 1.0) sf = 1.0;
+    if (sf > 4096.0) sf = 4096.0;
+    const int64_t S = static_cast<int64_t>(sf);
+    double avg = power;
+    if (d.sigma != 0.0) {
+        const uint64_t key = splitmix(d.seed ^ id);
+        double sum = 0.0;
+        for (int64_t j = 0; j < S; ++j) {
+            double z = -6.0;
+            for (int q = 0; q < 12; ++q)
+                z += static_cast<double>(splitmix(key + static_cast<uint64_t>(j * 12 + q)) >> 11) * 0x1p-53;
+            sum += power * (1.0 + d.sigma * z);
+        }
+        avg = sum / static_cast<double>(S);
+    }
+    out4[0] = lat_ms;
+    out4[1] = avg;
+    out4[2] = avg * lat_ms;
+    out4[3] = static_cast<double>(iters);
+}
+}  // namespace
+
+/* dev13: num_sms, constant_w, static_per_sm_w, e_flop_nj, e_glb_nj, e_shared_nj,
+ * throughput_flops_per_s_per_sm, bandwidth_elems_per_s, latency_floor_ms, sampler_hz,
+ * warmup_s, noise_sigma_rel (doubles) ; seed separately.  out: n x {latency_ms,
+ * avg_power_w, energy_mj, iterations}. */
+int orc_sim_measure(const int64_t* op, const int64_t* sched, int64_t n, const double* dev12, uint64_t seed,
+                    double* out) {
+    const Op o = op_of(op);
+    const SimDev d{dev12[0], dev12[1], dev12[2], dev12[3], dev12[4], dev12[5], dev12[6],
+                   dev12[7], dev12[8], dev12[9], dev12[10], dev12[11], seed};
+    const int sms = static_cast<int>(dev12[0]);
+    for (int64_t i = 0; i < n; ++i) {
+        const Sched s = sched_of(sched + 12 * i);
+        if (int st = validate_schedule(o, s)) return st;
+        sim_measure(derive(o, s, sms), d, cand_id(o, s), out + 4 * i);
+    }
+    return OK;
+}
+
 int orc_counters(const int64_t* op, const int64_t* sched, int64_t n, int num_sms, int64_t* out) {
     const Op o = op_of(op);
     for (int64_t i = 0; i < n; ++i) {

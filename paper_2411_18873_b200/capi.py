@@ -102,6 +102,8 @@ _SIGS = {
                                  _PTR, _PTR]),
     "etune_cu_forest_from_device": (C.c_int, [_VP, _PTR, _PTR, _PTR, _PTR, _PTR, _PTR, _I64, _PTR, C.c_double,
                                               C.POINTER(_VP)]),
+    "etune_cu_sample_random": (C.c_int, [_VP, _VP, _I64, C.c_uint64, _PTR, _PTR]),
+    "etune_cu_sim_measure": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR, _PTR, _PTR, _PTR]),
     "etune_cu_energy_loss": (C.c_int, [_VP, _PTR, _PTR, _I64, _PTR]),
     "etune_cu_snr_db": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(C.c_double), C.POINTER(_I64)]),
     "etune_cu_nccl_unique_id": (C.c_int, [_PTR]),
@@ -145,11 +147,14 @@ def op_spec(op) -> OpSpec:
     return OpSpec(*w)
 
 
-def default_device_config(num_sms: Optional[int] = None) -> DeviceConfig:
+def default_device_config(num_sms: Optional[int] = None, **fields) -> DeviceConfig:
+    """DeviceConfig::a100_like() (device.hpp:17-45) with optional field overrides."""
     d = DeviceConfig()
     lib().etune_default_device_config(C.byref(d))
     if num_sms is not None:
         d.num_sms = int(num_sms)
+    for k, v in fields.items():
+        setattr(d, k, type(getattr(d, k))(v))
     return d
 
 
@@ -253,6 +258,29 @@ class Plan:
         out = torch.empty((genome.shape[0], 10), dtype=torch.int64, device=genome.device)
         _check(lib().etune_cu_counters(self.ctx.h, self.h, _ptr(genome), genome.shape[0], _ptr(out)))
         return out
+
+    def sample_random(self, n: int, seed: int, with_ids: bool = False):
+        """sample_random (space.cpp:170-251) on the device -> genomes (+ ids)."""
+        import torch
+        g = torch.empty(n, dtype=torch.int64, device=torch.device("cuda", self.ctx.device))
+        ids = torch.empty_like(g) if with_ids else None
+        _check(lib().etune_cu_sample_random(self.ctx.h, self.h, int(n), C.c_uint64(seed), _ptr(g), _ptr(ids)))
+        return (g, ids) if with_ids else g
+
+    def sim_measure(self, genome, latency_only: bool = False):
+        """SimBackend on device genomes -> (latency_ms, power_w, energy_mj, iterations)."""
+        import torch
+        n = genome.shape[0]
+        lat = torch.empty(n, dtype=torch.float64, device=genome.device)
+        if latency_only:
+            _check(lib().etune_cu_sim_measure(self.ctx.h, self.h, _ptr(genome), n, _ptr(lat), None, None, None))
+            return lat
+        pw = torch.empty_like(lat)
+        en = torch.empty_like(lat)
+        it = torch.empty(n, dtype=torch.int64, device=genome.device)
+        _check(lib().etune_cu_sim_measure(self.ctx.h, self.h, _ptr(genome), n, _ptr(lat), _ptr(pw), _ptr(en),
+                                          _ptr(it)))
+        return lat, pw, en, it
 
     def features(self, genome, with_ids: bool = False):
         import torch

@@ -29,6 +29,7 @@
 
 #include "etune_internal.hpp"
 #include "kernels.hpp"
+#include "mt64.cuh"
 
 namespace etune_b200 {
 
@@ -40,23 +41,6 @@ constexpr int kCells = 2048;          // speculative (offspring, offset) evaluat
 constexpr int kMaxLevels = 96;        // offspring resolved per round at most
 constexpr uint16_t kUnknown = 0;      // cell needs words beyond the generated horizon
 constexpr uint16_t kIllegal = 0xffff; // repair produced an illegal schedule (reference throws)
-
-constexpr uint64_t kMtA = 0xb5026f5aa96619e9ull;
-constexpr uint64_t kUpper = 0xffffffff80000000ull;
-constexpr uint64_t kLower = 0x7fffffffull;
-
-__device__ __forceinline__ uint64_t temper(uint64_t y) {  // std::mt19937_64 output function
-    y ^= (y >> 29) & 0x5555555555555555ull;
-    y ^= (y << 17) & 0x71d67fffeda60000ull;
-    y ^= (y << 37) & 0xfff7eee000000000ull;
-    y ^= y >> 43;
-    return y;
-}
-
-__device__ __forceinline__ uint64_t twist1(uint64_t cur, uint64_t next, uint64_t far) {
-    const uint64_t x = (cur & kUpper) | (next & kLower);
-    return far ^ (x >> 1) ^ ((x & 1ull) ? kMtA : 0ull);
-}
 
 template <typename T>
 __device__ __forceinline__ const T* at(const uint8_t* base, uint32_t off) {
@@ -275,15 +259,7 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
         for (int64_t j = tid; j < np; j += blockDim.x) diff |= __ldg(pid + j) != id0;
         if (__syncthreads_or(diff) && tid == 0) s_other = 1;
     }
-    // std::mt19937_64(seed) (libstdc++ seeding: f = 6364136223846793005)
-    if (tid == 0) {
-        uint64_t v = seed;
-        mt[0] = v;
-        for (int i = 1; i < 312; ++i) {
-            v = 6364136223846793005ull * (v ^ (v >> 62)) + uint64_t(i);
-            mt[i] = v;
-        }
-    }
+    if (tid == 0) mt64::seed_state(mt, seed);  // std::mt19937_64(seed)
     __syncthreads();
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
     BreedConst K{P, par, pid, np, mut, mutcro, total, s_other};
@@ -298,21 +274,8 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
     while (i0 < n) {
         // ---- extend the stream: cooperative twists while the ring has room
         while (hi + 312 <= o0 + kRing) {
-            uint64_t cur = 0, nxt = 0;
-            if (tid < 312) {
-                cur = mt[tid];
-                nxt = tid < 311 ? mt[tid + 1] : 0;
-            }
-            __syncthreads();
-            if (tid < 156) mt[tid] = twist1(cur, nxt, mt[tid + 156]);
-            __syncthreads();
-            if (tid >= 156 && tid < 311) mt[tid] = twist1(cur, nxt, mt[tid - 156]);
-            if (tid == 311) {
-                const uint64_t m0 = mt[0], m155 = mt[155];
-                mt[311] = twist1(cur, m0, m155);
-            }
-            __syncthreads();
-            if (tid < 312) ring[(hi + uint64_t(tid)) & (kRing - 1)] = temper(mt[tid]);
+            mt64::twist_block(mt);
+            if (tid < 312) ring[(hi + uint64_t(tid)) & (kRing - 1)] = mt64::temper(mt[tid]);
             hi += 312;
         }
         // ---- level windows

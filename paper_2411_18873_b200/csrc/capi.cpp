@@ -327,6 +327,62 @@ etune_status etune_cu_decode(etune_cu_ctx* c, const etune_cu_plan* p, const uint
     return ETUNE_OK;
 }
 
+etune_status etune_cu_sample_random(etune_cu_ctx* c, const etune_cu_plan* p, int64_t n, uint64_t seed,
+                                    uint64_t* d_out, uint64_t* d_ids) {
+    if (!c || !p) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx/plan");
+    if (n < 1) return fail(ETUNE_ERR_VALIDATION, "sample_random requires n >= 1");
+    if (!d_out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null output");
+    const PlanBuild& B = p->build;
+    const int64_t cap = std::max<int64_t>(2 * n, 4096);  // space.cpp:175
+    const int64_t counted = std::min<int64_t>(B.space_size, cap + 1);
+    if (counted < n)
+        return fail(ETUNE_ERR_SPACE_EXHAUSTED, "requested " + std::to_string(n) + " candidates but only " +
+                                                   std::to_string(counted) + " legal schedules exist");
+    if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
+    int64_t* d_found = nullptr;
+    int* d_flags = nullptr;
+    if (etune_status st = ensure_scratch(c, 0)) return st;  // no-op; keeps the scratch policy uniform
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&d_found), 64, c->stream));
+    d_flags = reinterpret_cast<int*>(d_found + 4);
+    int64_t found = 0, flags = 0;
+    if (counted <= cap) {
+        const int64_t dims[6] = {B.hdr.nt[0], B.hdr.nt[1], B.hdr.nt[2], B.hdr.ndk, int64_t(B.unroll_opts.size()),
+                                 int64_t(B.vec_opts.size())};
+        int64_t q = 1;
+        for (int i = 0; i < 6; ++i) q *= dims[i];
+        if (etune_status st = ensure_scratch(c, sample_scratch_bytes(n, q, true))) return st;
+        CU(launch_sample_small(c->lc(), p->d_blob, dims, seed, n, d_out, d_found, d_flags, c->scratch));
+        CU(cudaMemcpyAsync(&found, d_found, 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaStreamSynchronize(c->stream));
+        if (found != B.space_size) {
+            cudaFree(d_found);
+            return fail(ETUNE_ERR_CONSISTENCY, "device enumeration disagrees with the plan's space size");
+        }
+    } else {
+        const int64_t max_attempts = 10000 + n * 1000;  // space.cpp:214
+        int64_t A = std::min<int64_t>(max_attempts, n + n / 2 + 4096);
+        for (;;) {
+            if (etune_status st = ensure_scratch(c, sample_scratch_bytes(A, 0, false))) return st;
+            CU(launch_sample_large(c->lc(), p->d_blob, seed, n, A, d_out, d_found, d_flags, c->scratch));
+            int h_flags = 0;
+            CU(cudaMemcpyAsync(&found, d_found, 8, cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaMemcpyAsync(&h_flags, d_flags, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            CU(cudaStreamSynchronize(c->stream));
+            flags = h_flags;
+            if (found >= n) break;
+            if (A >= max_attempts || A >= (int64_t(1) << 30)) {
+                cudaFree(d_found);
+                return fail(ETUNE_ERR_SPACE_EXHAUSTED, "random sampling failed to find enough distinct candidates");
+            }
+            A = std::min<int64_t>(max_attempts, 2 * A);
+        }
+    }
+    (void)flags;
+    CU(cudaFreeAsync(d_found, c->stream));
+    if (d_ids) CU(launch_ids(c->lc(), p->d_blob, B.hdr.total, d_out, n, d_ids));
+    return ETUNE_OK;
+}
+
 etune_status etune_cu_candidate_ids(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
                                     uint64_t* d_ids) {
     CHECK_PLAN_ARGS(d_ids && d_genome);
@@ -345,6 +401,25 @@ etune_status etune_cu_features(etune_cu_ctx* c, const etune_cu_plan* p, const ui
                                double* d_feat, uint64_t* d_ids) {
     CHECK_PLAN_ARGS(d_feat && d_genome);
     CU(launch_features(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_feat, d_ids));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_sim_measure(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
+                                  double* d_lat, double* d_pow, double* d_en, int64_t* d_iters) {
+    CHECK_PLAN_ARGS(d_genome && d_lat);
+    const etune_device_config& D = p->build.dev;
+    SimDevice d{D.base_throughput_flops_per_s_per_sm,
+                D.mem_bandwidth_elems_per_s,
+                D.latency_floor_ms,
+                D.dynamic_energy_per_flop_nj,
+                D.dynamic_energy_per_glb_access_nj,
+                D.dynamic_energy_per_shared_access_nj,
+                D.constant_power_w,
+                D.static_power_per_sm_w,
+                D.sampler_hz,
+                D.noise_sigma_rel,
+                D.rng_seed};
+    CU(launch_sim_measure(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d, d_lat, d_pow, d_en, d_iters));
     return ETUNE_OK;
 }
 

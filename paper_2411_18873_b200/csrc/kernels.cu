@@ -208,6 +208,30 @@ __global__ void __launch_bounds__(kThreads) ids_kernel(const uint8_t* __restrict
 }
 
 // ---------------------------------------------------------------- counters
+// derive_counters (counters.cpp:14-47), same int64 expressions and evaluation order
+__device__ __forceinline__ etune_counters plan_counters(const PlanHdr& H, const Knobs& c) {
+    const int64_t bt_b = int64_t(c.r[0].threads) * c.r[0].pt;
+    const int64_t bt_m = int64_t(c.r[1].threads) * c.r[1].pt;
+    const int64_t bt_n = int64_t(c.r[2].threads) * c.r[2].pt;
+    etune_counters o;
+    o.grid = int64_t(c.r[0].blocks) * c.r[1].blocks * c.r[2].blocks;
+    o.block = int64_t(c.r[0].threads) * c.r[1].threads * c.r[2].threads;
+    const int64_t steps = H.K / c.k_tile;
+    const int64_t outputs = H.B * H.M * H.N;
+    o.flops = 2 * outputs * H.K;
+    const int64_t tile = bt_b * c.k_tile * (bt_m + bt_n);
+    o.glb_ld = o.grid * steps * tile;
+    o.shared_st = o.glb_ld;
+    o.shared_ld = o.grid * o.block * H.K * int64_t(c.r[0].pt) * (int64_t(c.r[1].pt) + int64_t(c.r[2].pt));
+    o.int_ops = o.shared_ld;
+    o.glb_st = outputs;
+    o.active_sms = o.grid < H.num_sms ? o.grid : H.num_sms;
+    const double q = __ddiv_rn(static_cast<double>(o.block), 256.0);
+    o.sm_efficiency = __dmul_rn(__ddiv_rn(static_cast<double>(o.active_sms), static_cast<double>(H.num_sms)),
+                                q < 1.0 ? q : 1.0);
+    return o;
+}
+
 __global__ void __launch_bounds__(kThreads) counters_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
                                                             int use_smem, const uint64_t* __restrict__ genome,
                                                             int64_t n, etune_counters* __restrict__ out) {
@@ -219,29 +243,73 @@ __global__ void __launch_bounds__(kThreads) counters_kernel(const uint8_t* __res
         P = reinterpret_cast<const uint8_t*>(smem);
     }
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        out[i] = plan_counters(H, load_knobs(P, H, genome[i]));
+}
+
+// ------------------------------------------------------ SimBackend measure
+// sim_true_power_and_latency + nvml_sim_measure (measure.hpp:29-60; formula SPEC:314-322).
+// No reference implementation exists: this follows the oracle restatement
+// (oracle/etune_oracle.cpp, sim_measure) operation by operation; the sampler noise is
+// Irwin-Hall over splitmix64 words, so it is bit-reproducible without libm.
+__device__ __forceinline__ uint64_t splitmix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+__global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
+                                                               int use_smem, const uint64_t* __restrict__ genome,
+                                                               int64_t n, SimDevice d, double* __restrict__ lat,
+                                                               double* __restrict__ pow, double* __restrict__ en,
+                                                               int64_t* __restrict__ iters) {
+    extern __shared__ int4 smem[];
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        stage(gplan, bytes, smem);
+        __syncthreads();
+        P = reinterpret_cast<const uint8_t*>(smem);
+    }
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const Knobs c = load_knobs(P, H, genome[i]);
-        // counters.cpp:14-47, same int64 expressions and evaluation order
-        const int64_t bt_b = int64_t(c.r[0].threads) * c.r[0].pt;
-        const int64_t bt_m = int64_t(c.r[1].threads) * c.r[1].pt;
-        const int64_t bt_n = int64_t(c.r[2].threads) * c.r[2].pt;
-        etune_counters o;
-        o.grid = int64_t(c.r[0].blocks) * c.r[1].blocks * c.r[2].blocks;
-        o.block = int64_t(c.r[0].threads) * c.r[1].threads * c.r[2].threads;
-        const int64_t steps = H.K / c.k_tile;
-        const int64_t outputs = H.B * H.M * H.N;
-        o.flops = 2 * outputs * H.K;
-        const int64_t tile = bt_b * c.k_tile * (bt_m + bt_n);
-        o.glb_ld = o.grid * steps * tile;
-        o.shared_st = o.glb_ld;
-        o.shared_ld = o.grid * o.block * H.K * int64_t(c.r[0].pt) * (int64_t(c.r[1].pt) + int64_t(c.r[2].pt));
-        o.int_ops = o.shared_ld;
-        o.glb_st = outputs;
-        o.active_sms = o.grid < H.num_sms ? o.grid : H.num_sms;
-        const double q = __ddiv_rn(static_cast<double>(o.block), 256.0);
-        o.sm_efficiency = __dmul_rn(__ddiv_rn(static_cast<double>(o.active_sms), static_cast<double>(H.num_sms)),
-                                    q < 1.0 ? q : 1.0);
-        out[i] = o;
+        const Knobs kn = load_knobs(P, H, genome[i]);
+        const etune_counters c = plan_counters(H, kn);
+        const double active = static_cast<double>(c.active_sms);
+        const double compute_s =
+            __ddiv_rn(static_cast<double>(c.flops), __dmul_rn(__dmul_rn(active, d.tput), c.sm_efficiency));
+        const double memory_s = __ddiv_rn(static_cast<double>(c.glb_ld + c.glb_st), d.bw);
+        double lat_ms = __dmul_rn(compute_s > memory_s ? compute_s : memory_s, 1000.0);
+        if (lat_ms < d.floor_ms) lat_ms = d.floor_ms;
+        lat[i] = lat_ms;
+        if (!pow && !en && !iters) continue;  // measure_latency_ms only
+        const double dyn_mj = __dmul_rn(
+            __dadd_rn(__dadd_rn(__dmul_rn(static_cast<double>(c.flops), d.e_flop),
+                                __dmul_rn(static_cast<double>(c.glb_ld + c.glb_st), d.e_glb)),
+                      __dmul_rn(static_cast<double>(c.shared_ld + c.shared_st), d.e_shared)),
+            1e-6);
+        const double power = __dadd_rn(__dadd_rn(d.constant, __dmul_rn(d.static_sm, active)), __ddiv_rn(dyn_mj, lat_ms));
+        const double lat_s = __ddiv_rn(lat_ms, 1000.0);
+        const double want = ceil(__ddiv_rn(2.0, lat_s));
+        const int64_t it = want > 1000.0 ? static_cast<int64_t>(want) : 1000;
+        double sf = floor(__dmul_rn(__dmul_rn(static_cast<double>(it), lat_s), d.hz));
+        sf = sf < 1.0 ? 1.0 : (sf > 4096.0 ? 4096.0 : sf);
+        const int64_t S = static_cast<int64_t>(sf);
+        double avg = power;
+        if (d.sigma != 0.0) {
+            const uint64_t key = splitmix(d.seed ^ candidate_hash(H.fnv_prefix, kn));
+            double sum = 0.0;
+            for (int64_t j = 0; j < S; ++j) {
+                double z = -6.0;
+                for (int q = 0; q < 12; ++q)
+                    z = __dadd_rn(z, __dmul_rn(static_cast<double>(splitmix(key + uint64_t(j * 12 + q)) >> 11), 0x1p-53));
+                sum = __dadd_rn(sum, __dmul_rn(power, __dadd_rn(1.0, __dmul_rn(d.sigma, z))));
+            }
+            avg = __ddiv_rn(sum, static_cast<double>(S));
+        }
+        if (pow) pow[i] = avg;
+        if (en) en[i] = __dmul_rn(avg, lat_ms);
+        if (iters) iters[i] = it;
     }
 }
 
@@ -454,6 +522,11 @@ cudaError_t launch_ids(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes
 cudaError_t launch_counters(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
                             int64_t n, etune_counters* d_out) {
     return launch_plan_kernel(counters_kernel, c, d_plan, bytes, n, d_genome, n, d_out);
+}
+cudaError_t launch_sim_measure(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
+                               int64_t n, const SimDevice& d, double* d_lat, double* d_pow, double* d_en,
+                               int64_t* d_iters) {
+    return launch_plan_kernel(sim_measure_kernel, c, d_plan, bytes, n, d_genome, n, d, d_lat, d_pow, d_en, d_iters);
 }
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
                             int64_t n, double* d_feat, uint64_t* d_ids) {

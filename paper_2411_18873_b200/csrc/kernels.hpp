@@ -27,6 +27,14 @@ cudaError_t launch_ids(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_
                        const uint64_t* d_genome, int64_t n, uint64_t* d_ids);
 cudaError_t launch_counters(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                             const uint64_t* d_genome, int64_t n, etune_counters* d_out);
+// SimBackend (measure.hpp:29-60, 102-114): latency only when pow/en/iters are null.
+struct SimDevice {
+    double tput, bw, floor_ms, e_flop, e_glb, e_shared, constant, static_sm, hz, sigma;
+    uint64_t seed;
+};
+cudaError_t launch_sim_measure(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
+                               int64_t n, const SimDevice& d, double* d_lat, double* d_pow, double* d_en,
+                               int64_t* d_iters);
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                             const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
@@ -72,6 +80,19 @@ cudaError_t launch_pack_records(const LaunchCtx& c, const double* d_score, const
                                 int64_t k, int64_t goff, double* d_rs, int64_t* d_rg);
 cudaError_t launch_gather_records(const LaunchCtx& c, const double* d_gs, const int64_t* d_gg, const int64_t* d_pos,
                                   int64_t k, int64_t* d_idx, double* d_sc);
+
+// stable LSD radix sort of (u64 key, u32 value) pairs by the low `bits` bits, in place
+size_t sort_pairs_scratch_bytes(int64_t n);
+cudaError_t launch_sort_pairs(const LaunchCtx& c, uint64_t* keys, uint32_t* vals, int64_t n, int bits,
+                              void* scratch);
+
+// sample_random (space.cpp:170-251): large-space attempts / small-space enumerate + Fisher-Yates.
+// Scratch: sample_scratch_bytes(attempts, 0, false) / (n, odometer product, true).
+size_t sample_scratch_bytes(int64_t n, int64_t space_or_product, bool small);
+cudaError_t launch_sample_large(const LaunchCtx& c, const uint8_t* d_plan, uint64_t seed, int64_t n, int64_t A,
+                                uint64_t* d_out, int64_t* d_found, int* d_flags, void* scratch);
+cudaError_t launch_sample_small(const LaunchCtx& c, const uint8_t* d_plan, const int64_t dims[6], uint64_t seed,
+                                int64_t n, uint64_t* d_out, int64_t* d_found, int* d_flags, void* scratch);
 
 // process-wide count of kernel launches (incremented by every launcher)
 void note_launches(int k);

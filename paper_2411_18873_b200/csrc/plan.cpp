@@ -107,6 +107,7 @@ etune_status build_plan(const etune_op_spec& op, const etune_device_config& dev,
     P->op = op;
     P->limits = limits;
     P->num_sms = dev.num_sms;
+    P->dev = dev;
     int64_t nest[4];
     op_nest(op, nest);
     const int64_t B = nest[0], M = nest[1], N = nest[2], K = nest[3];

@@ -13,6 +13,7 @@ struct PlanBuild {
     etune_op_spec op{};
     etune_space_limits limits{};
     int num_sms = 108;
+    etune_device_config dev{};        // the simulated device (SimBackend)
     PlanHdr hdr{};
     std::vector<uint8_t> blob;  // hdr + tables, 16-byte aligned sections
 

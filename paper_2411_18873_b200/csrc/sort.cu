@@ -390,6 +390,40 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 }  // namespace
 
+size_t sort_pairs_scratch_bytes(int64_t n) {
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    return al256(8 * size_t(n)) + al256(4 * size_t(n)) + al256(4 * 256 * size_t(ntiles));
+}
+
+// Stable LSD radix sort of (u64 key, u32 value) pairs by the low `bits` key bits
+// (8-bit digits); result in place.
+cudaError_t launch_sort_pairs(const LaunchCtx& c, uint64_t* keys, uint32_t* vals, int64_t n, int bits,
+                              void* scratch) {
+    if (n <= 1) return cudaSuccess;
+    char* p = static_cast<char*>(scratch);
+    uint64_t* k2 = reinterpret_cast<uint64_t*>(p);
+    p += al256(8 * size_t(n));
+    uint32_t* v2 = reinterpret_cast<uint32_t*>(p);
+    p += al256(4 * size_t(n));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+    const int kt = int((n + kTile - 1) / kTile);
+    uint64_t* kk[2] = {keys, k2};
+    uint32_t* vv[2] = {vals, v2};
+    int cur = 0;
+    for (int shift = 0; shift < bits; shift += 8) {
+        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], n, shift, hist, kt);
+        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(hist, kt);
+        lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], vv[cur], n, shift, hist, kt, kk[cur ^ 1], vv[cur ^ 1]);
+        cur ^= 1;
+        note_launches(3);
+    }
+    if (cur) {
+        cudaMemcpyAsync(keys, k2, 8 * size_t(n), cudaMemcpyDeviceToDevice, c.stream);
+        cudaMemcpyAsync(vals, v2, 4 * size_t(n), cudaMemcpyDeviceToDevice, c.stream);
+    }
+    return cudaGetLastError();
+}
+
 size_t topk_scratch_bytes(int64_t n) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
     return al256(sizeof(TopkWork)) + 2 * (al256(8 * size_t(n)) + al256(4 * size_t(n))) +

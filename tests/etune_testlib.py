@@ -54,6 +54,18 @@ def default_limits() -> np.ndarray:
     return np.array([1024, 8, 4], dtype=np.int64)
 
 
+# DeviceConfig::a100_like() numeric fields (device.hpp:17-45), etune_device_config order
+DEVICE_FIELDS = ("num_sms", "constant_power_w", "static_power_per_sm_w", "dynamic_energy_per_flop_nj",
+                 "dynamic_energy_per_glb_access_nj", "dynamic_energy_per_shared_access_nj",
+                 "base_throughput_flops_per_s_per_sm", "mem_bandwidth_elems_per_s", "latency_floor_ms",
+                 "sampler_hz", "warmup_s", "noise_sigma_rel")
+DEFAULT_DEVICE = dict(num_sms=108, constant_power_w=60.0, static_power_per_sm_w=0.55,
+                      dynamic_energy_per_flop_nj=0.002, dynamic_energy_per_glb_access_nj=0.125,
+                      dynamic_energy_per_shared_access_nj=0.0125, base_throughput_flops_per_s_per_sm=1.8e11,
+                      mem_bandwidth_elems_per_s=3.3e11, latency_floor_ms=1e-5, sampler_hz=50.0, warmup_s=2.0,
+                      noise_sigma_rel=0.05, rng_seed=1234)
+
+
 class EtuneError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"status {code}: {msg}")
@@ -106,6 +118,7 @@ class Oracle(_Lib):
         L.orc_enumerate.argtypes = [I64P, I64P, C.c_int64, I64P, C.POINTER(C.c_int64)]
         L.orc_counters.argtypes = [I64P, I64P, C.c_int64, C.c_int, I64P]
         L.orc_features.argtypes = [I64P, I64P, C.c_int64, C.c_int, F64P]
+        L.orc_sim_measure.argtypes = [I64P, I64P, C.c_int64, F64P, C.c_uint64, F64P]
         for nm in ("orc_mt64_words", "orc_std_mt64_words"):
             getattr(L, nm).argtypes = [C.c_uint64, C.c_int64, U64P]
         for nm in ("orc_lemire", "orc_std_uniform"):
@@ -167,6 +180,17 @@ class Oracle(_Lib):
         sched = np.ascontiguousarray(sched, np.int64).reshape(-1, 12)
         out = np.zeros((len(sched), 16), np.float64)
         self._check(self.L.orc_features(op, sched, len(sched), num_sms, out))
+        return out
+
+    def sim_measure(self, op, sched, dev=None):
+        """SimBackend restatement: n x {latency_ms, avg_power_w, energy_mj, iterations}.
+        dev: dict of DeviceConfig numeric fields (defaults: a100_like, device.hpp:17-45)."""
+        d = dict(DEFAULT_DEVICE)
+        d.update(dev or {})
+        dev12 = np.array([d[k] for k in DEVICE_FIELDS], np.float64)
+        sched = np.ascontiguousarray(sched, np.int64).reshape(-1, 12)
+        out = np.zeros((len(sched), 4), np.float64)
+        self._check(self.L.orc_sim_measure(op, sched, len(sched), dev12, int(d["rng_seed"]), out))
         return out
 
     # --- search primitives

@@ -95,3 +95,30 @@ def test_topk_sharded_nccl_one_rank(oracle, ctx, capi):
     capi.broadcast(c2, buf, 0)
     c2.synchronize()
     assert (buf.cpu().numpy() == np.arange(10)).all()
+
+
+@pytest.mark.parametrize("text,dev", [
+    ("mm:1,512,512,512", {}), ("conv:1,56,56,64,64,3,1,1", {"noise_sigma_rel": 0.0}),
+    ("mm:1,512,3072,768", {"num_sms": 148, "rng_seed": 99, "noise_sigma_rel": 0.2}),
+    ("mm:1,1,1,1", {}), ("mv:1,1,1000,2048", {"sampler_hz": 30.0, "latency_floor_ms": 0.5})])
+def test_sim_measure_vs_oracle(oracle, ctx, capi, text, dev):
+    from etune_testlib import parse_op
+    op = parse_op(text)
+    s, _ = oracle.sample_random(op, min(20000, oracle.count(op)), 3)
+    ref = oracle.sim_measure(op, s, dev)
+    d = capi.default_device_config(**dev)
+    plan = capi.Plan(ctx, op, dev=d)
+    g = plan.encode(dev_t(s))
+    lat, pw, en, it = plan.sim_measure(g)
+    lat_only = plan.sim_measure(g, latency_only=True)
+    ctx.synchronize()
+    for j, t in enumerate((lat, pw, en)):
+        assert (t.cpu().numpy().view(np.uint64) == ref[:, j].view(np.uint64)).all()
+    assert (it.cpu().numpy() == ref[:, 3].astype(np.int64)).all()
+    assert (lat_only.cpu().numpy().view(np.uint64) == ref[:, 0].view(np.uint64)).all()
+    if dev.get("noise_sigma_rel", 0.05) == 0.0:  # SPEC:336 noiseless -> true power exactly
+        assert np.allclose(en.cpu().numpy(), pw.cpu().numpy() * lat.cpu().numpy(), rtol=1e-15)
+
+
+def dev_t(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
