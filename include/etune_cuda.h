@@ -294,6 +294,57 @@ etune_status etune_cu_reproduce(etune_cu_ctx* ctx, const etune_cu_plan* plan,
 etune_status etune_cu_topk(etune_cu_ctx* ctx, const double* d_score, int64_t n, int64_t k,
                            int64_t* d_idx);
 
+/* ------------------------------------------------------ search (Algorithm 1) */
+/* The energy-aware genetic search of PAPER:223-254 / SPEC:372-457 (the reference ships
+ * it only as a spec; there is no reference code).  Every data-parallel step runs on the
+ * device through this library; the host keeps the per-round scalars (k, SNR, best).
+ * Choices where the spec is silent: initial parents = the M
+ * fastest of the initial sample; round r reproduces with seed rng_seed + r; k is kept
+ * in integer fifths; SNR compares step-3 predictions with the measured energies
+ * normalised by the model's reference energy; selections break ties by index. */
+typedef struct etune_search_config {
+    int64_t M;                 /* kept per round after the latency filter */
+    int64_t generation_size;   /* > M */
+    int32_t k_init_fifths;     /* 5 == k 1.0 */
+    int32_t max_rounds;
+    int32_t patience;          /* rounds without > improve_rel best-energy gain (5) */
+    int32_t inverted_semantics;/* 1: the paper's literal prose reading of the k rule */
+    double mu_db;              /* SNR threshold (20 dB) */
+    double improve_rel;        /* 0.001 */
+    uint64_t rng_seed;
+    etune_genetic_rates rates;
+    etune_boost_params boost;
+} etune_search_config;
+
+typedef struct etune_round_report {   /* RoundReport */
+    int64_t round;                    /* 0 = initial_round */
+    int32_t k_before_fifths, k_after_fifths;
+    double snr_db;                    /* NaN for round 0 */
+    int64_t measured;                 /* energy measurements this round */
+    int64_t cumulative_measured;
+    uint64_t best_id;
+    double best_latency_ms, best_energy_mj, best_power_w;
+    double wall_ms;                   /* host wall time of the round, device synchronised */
+} etune_round_report;
+
+typedef struct etune_cu_search etune_cu_search;
+void etune_default_search_config(etune_search_config* out);
+/* Backend: the plan's SimBackend (etune_cu_sim_measure). */
+etune_status etune_cu_search_create(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                    const etune_search_config* cfg, etune_cu_search** out);
+etune_status etune_cu_search_destroy(etune_cu_search* s);
+etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* out);  /* initial_round */
+etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* out);    /* round */
+/* run_search: initial round (if not yet run) then rounds until max_rounds or patience;
+ * writes up to cap reports, *n_reports = rounds run. */
+etune_status etune_cu_search_run(etune_cu_search* s, etune_round_report* reports, int64_t cap,
+                                 int64_t* n_reports);
+/* best measured candidate: energy, then latency, then id */
+etune_status etune_cu_search_best(etune_cu_search* s, etune_schedule* h_sched, uint64_t* h_id,
+                                  double* h_latency_ms, double* h_energy_mj);
+/* current parents (device genomes; *n = count, at most cap written) */
+etune_status etune_cu_search_parents(etune_cu_search* s, uint64_t* d_out, int64_t cap, int64_t* n);
+
 /* ------------------------------------------------------- multi-GPU (NCCL) */
 /* One rank per GPU over NVLink/NVSwitch.  The population shards by index: rank r owns
  * the contiguous global range [global_offset, global_offset + n) with offsets

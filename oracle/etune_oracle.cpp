@@ -6,6 +6,7 @@
 #include "etune_oracle.h"
 
 #include <algorithm>
+#include <limits>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -1018,3 +1019,154 @@ int orc_score_threads(const int64_t* op, const int64_t* sched, int64_t n, int nu
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------- Algorithm 1 (search)
+// CPU restatement of the search loop (the reference has no
+// code) built from the restated primitives above, step for step what
+// paper_2411_18873_b200/csrc/search.cpp does on the device.  cfg_i: M, generation_size,
+// k_init_fifths, max_rounds, patience, inverted, num_trees, max_depth; cfg_d: mu_db,
+// improve_rel, mutation, crossover, copy, learning_rate, min_leaf_weight, reg_lambda.
+// Reports: rep_i n x {round, k_before, k_after, measured, cumulative, best_id},
+// rep_d n x {snr_db, best_latency_ms, best_energy_mj, best_power_w}.
+extern "C" int orc_run_search(const int64_t* op, const int64_t* limits, const double* dev12, uint64_t dev_seed,
+                              const int64_t* cfg_i, const double* cfg_d, uint64_t seed, int64_t max_reports,
+                              int64_t* rep_i, double* rep_d, int64_t* n_reports, int64_t* out_parents,
+                              int64_t* n_parents) {
+    const int64_t M = cfg_i[0], G = cfg_i[1];
+    int k5 = int(cfg_i[2]);
+    const int64_t max_rounds = cfg_i[3], patience = cfg_i[4], inverted = cfg_i[5];
+    const int trees = int(cfg_i[6]), depth = int(cfg_i[7]);
+    const double mu = cfg_d[0], improve = cfg_d[1], rates[3] = {cfg_d[2], cfg_d[3], cfg_d[4]};
+    const double lr = cfg_d[5], mlw = cfg_d[6], lam = cfg_d[7];
+    const int sms = int(dev12[0]);
+    using VI = std::vector<int64_t>;
+    using VD = std::vector<double>;
+    auto sched_rows = [](const VI& all, const VI& idx) {
+        VI out(idx.size() * 12);
+        for (size_t j = 0; j < idx.size(); ++j)
+            std::copy(all.begin() + 12 * idx[j], all.begin() + 12 * idx[j] + 12, out.begin() + 12 * j);
+        return out;
+    };
+    VD feats, energy;  // accumulated samples
+    const size_t cap_nodes = size_t(std::max(trees, 1)) * ((size_t(1) << (depth + 1)) - 1);
+    std::vector<int32_t> fe(cap_nodes), le(cap_nodes), ri(cap_nodes);
+    VD th(cap_nodes), va(cap_nodes), loss(size_t(trees) + 1);
+    std::vector<int64_t> off(size_t(trees) + 1);
+    double base = 0, ref = 0;
+    auto retrain = [&]() {
+        return orc_train(feats.data(), energy.data(), int64_t(energy.size()), trees, depth, lr, mlw, lam, fe.data(),
+                         th.data(), le.data(), ri.data(), va.data(), off.data(), &base, &ref, loss.data());
+    };
+    bool have_best = false;
+    uint64_t best_id = 0;
+    double best_lat = 0, best_en = 0, best_pow = 0;
+    int64_t cumulative = 0, stall = 0, nrep = 0;
+    auto update_best = [&](const VI& s, const VD& m4) -> bool {
+        const int64_t n = int64_t(s.size() / 12);
+        std::vector<uint64_t> ids(static_cast<size_t>(n));
+        orc_candidate_ids(op, s.data(), n, ids.data());
+        const double before = have_best ? best_en : std::numeric_limits<double>::infinity();
+        for (int64_t i = 0; i < n; ++i) {
+            const double l = m4[4 * i], p = m4[4 * i + 1], e = m4[4 * i + 2];
+            const bool better = !have_best || e < best_en ||
+                                (e == best_en && (l < best_lat || (l == best_lat && ids[i] < best_id)));
+            if (better) {
+                have_best = true;
+                best_en = e;
+                best_lat = l;
+                best_id = ids[i];
+                best_pow = p;
+            }
+        }
+        return best_en < before * (1.0 - improve);
+    };
+    auto report = [&](int64_t round, int kb, double snr, int64_t measured) {
+        if (nrep < max_reports) {
+            int64_t* ri = rep_i + 6 * nrep;
+            double* rd = rep_d + 4 * nrep;
+            ri[0] = round;
+            ri[1] = kb;
+            ri[2] = k5;
+            ri[3] = measured;
+            ri[4] = cumulative;
+            std::memcpy(&ri[5], &best_id, 8);
+            rd[0] = snr;
+            rd[1] = best_lat;
+            rd[2] = best_en;
+            rd[3] = best_pow;
+        }
+        ++nrep;
+    };
+    // initial round
+    VI pop(size_t(G) * 12);
+    std::vector<uint64_t> pid(static_cast<size_t>(G));
+    if (int st = orc_sample_random(op, G, seed, limits, pop.data(), pid.data())) return st;
+    VD m4(size_t(G) * 4);
+    if (int st = orc_sim_measure(op, pop.data(), G, dev12, dev_seed, m4.data())) return st;
+    VD lat(static_cast<size_t>(G));
+    for (int64_t i = 0; i < G; ++i) lat[i] = m4[4 * i];
+    VI idx(static_cast<size_t>(M));
+    orc_topk(lat.data(), G, M, idx.data());
+    VI mg = sched_rows(pop, idx);
+    VD mm(size_t(M) * 4);
+    orc_sim_measure(op, mg.data(), M, dev12, dev_seed, mm.data());
+    feats.resize(size_t(M) * 16);
+    orc_features(op, mg.data(), M, sms, feats.data());
+    for (int64_t i = 0; i < M; ++i) energy.push_back(mm[4 * i + 2]);
+    if (int st = retrain()) return st;
+    VI par = mg;
+    cumulative = M;
+    update_best(mg, mm);
+    report(0, k5, std::numeric_limits<double>::quiet_NaN(), M);
+    for (int64_t r = 1; r <= max_rounds && stall < patience; ++r) {
+        const int64_t np = int64_t(par.size() / 12);
+        VI off_s(size_t(G) * 12);
+        std::vector<uint64_t> oid(static_cast<size_t>(G)), lin(size_t(G) * 2);
+        std::vector<int8_t> ll(static_cast<size_t>(G));
+        if (int st = orc_reproduce(op, par.data(), np, G, rates, seed + uint64_t(r), limits, off_s.data(), oid.data(),
+                                   lin.data(), ll.data()))
+            return st;
+        orc_sim_measure(op, off_s.data(), G, dev12, dev_seed, m4.data());
+        for (int64_t i = 0; i < G; ++i) lat[i] = m4[4 * i];
+        orc_topk(lat.data(), G, M, idx.data());
+        mg = sched_rows(off_s, idx);
+        VD f(size_t(M) * 16), pred(static_cast<size_t>(M));
+        orc_features(op, mg.data(), M, sms, f.data());
+        orc_predict(fe.data(), th.data(), le.data(), ri.data(), va.data(), off.data(), trees, base, lr, f.data(), M,
+                    pred.data());
+        int64_t km = (int64_t(k5) * M + 4) / 5;
+        if (km < 1) km = 1;
+        VI sel(static_cast<size_t>(km));
+        orc_topk(pred.data(), M, km, sel.data());
+        VI sg = sched_rows(mg, sel);
+        VD sm(size_t(km) * 4), psel(static_cast<size_t>(km)), mnorm(static_cast<size_t>(km));
+        orc_sim_measure(op, sg.data(), km, dev12, dev_seed, sm.data());
+        for (int64_t i = 0; i < km; ++i) {
+            psel[i] = pred[sel[i]];
+            mnorm[i] = sm[4 * i + 2] / ref;
+        }
+        double snr = 0.0;
+        if (int st = orc_snr_db(psel.data(), mnorm.data(), km, &snr)) return st;
+        const int64_t npar = (M + 1) / 2;
+        VI pidx(static_cast<size_t>(npar));
+        orc_topk(pred.data(), M, npar, pidx.data());
+        par = sched_rows(mg, pidx);
+        const size_t old = feats.size();
+        feats.resize(old + size_t(km) * 16);
+        orc_features(op, sg.data(), km, sms, feats.data() + old);
+        for (int64_t i = 0; i < km; ++i) energy.push_back(sm[4 * i + 2]);
+        if (int st = retrain()) return st;
+        const int kb = k5;
+        const bool poor = inverted ? !(snr < mu) : (snr < mu);
+        k5 = poor ? std::min(5, k5 + 1) : std::max(0, k5 - 1);
+        cumulative += km;
+        const bool improved = update_best(sg, sm);
+        stall = improved ? 0 : stall + 1;
+        report(r, kb, snr, km);
+    }
+    *n_reports = nrep;
+    const int64_t np = int64_t(par.size() / 12);
+    *n_parents = np;
+    if (out_parents) std::copy(par.begin(), par.end(), out_parents);
+    return OK;
+}

@@ -66,6 +66,23 @@ class BoostParams(C.Structure):
                 ("min_leaf_weight", C.c_double), ("reg_lambda", C.c_double)]
 
 
+class SearchConfig(C.Structure):
+    _fields_ = [("M", C.c_int64), ("generation_size", C.c_int64), ("k_init_fifths", C.c_int32),
+                ("max_rounds", C.c_int32), ("patience", C.c_int32), ("inverted_semantics", C.c_int32),
+                ("mu_db", C.c_double), ("improve_rel", C.c_double), ("rng_seed", C.c_uint64),
+                ("rates", GeneticRates), ("boost", BoostParams)]
+
+
+class RoundReport(C.Structure):
+    _fields_ = [("round", C.c_int64), ("k_before_fifths", C.c_int32), ("k_after_fifths", C.c_int32),
+                ("snr_db", C.c_double), ("measured", C.c_int64), ("cumulative_measured", C.c_int64),
+                ("best_id", C.c_uint64), ("best_latency_ms", C.c_double), ("best_energy_mj", C.c_double),
+                ("best_power_w", C.c_double), ("wall_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _PTR = C.c_void_p
@@ -110,6 +127,15 @@ _SIGS = {
     "etune_cu_ctx_attach_nccl": (C.c_int, [_VP, _PTR, C.c_int, C.c_int]),
     "etune_cu_topk_sharded": (C.c_int, [_VP, _PTR, _I64, _I64, _I64, _PTR, _PTR]),
     "etune_cu_broadcast": (C.c_int, [_VP, _PTR, _I64, C.c_int]),
+    "etune_default_search_config": (None, [C.POINTER(SearchConfig)]),
+    "etune_cu_search_create": (C.c_int, [_VP, _VP, C.POINTER(SearchConfig), C.POINTER(_VP)]),
+    "etune_cu_search_destroy": (C.c_int, [_VP]),
+    "etune_cu_search_initial": (C.c_int, [_VP, C.POINTER(RoundReport)]),
+    "etune_cu_search_round": (C.c_int, [_VP, C.POINTER(RoundReport)]),
+    "etune_cu_search_run": (C.c_int, [_VP, _PTR, _I64, C.POINTER(_I64)]),
+    "etune_cu_search_best": (C.c_int, [_VP, _PTR, C.POINTER(C.c_uint64), C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]),
+    "etune_cu_search_parents": (C.c_int, [_VP, _PTR, _I64, C.POINTER(_I64)]),
     "etune_cu_reproduce": (C.c_int, [_VP, _VP, _PTR, _I64, _I64, C.POINTER(GeneticRates), C.c_uint64, _PTR, _PTR,
                                      _PTR]),
 }
@@ -444,6 +470,67 @@ def topk_sharded(ctx: Context, score, global_offset: int, k: int):
 def broadcast(ctx: Context, t, root: int = 0):
     _check(lib().etune_cu_broadcast(ctx.h, _ptr(t), t.numel() * t.element_size(), int(root)))
     return t
+
+
+def search_config(**kw) -> SearchConfig:
+    """etune_default_search_config with overrides; rates/boost fields by name."""
+    cfg = SearchConfig()
+    lib().etune_default_search_config(C.byref(cfg))
+    for k, v in kw.items():
+        if hasattr(cfg.rates, k):
+            setattr(cfg.rates, k, float(v))
+        elif hasattr(cfg.boost, k):
+            setattr(cfg.boost, k, type(getattr(cfg.boost, k))(v))
+        else:
+            setattr(cfg, k, type(getattr(cfg, k))(v))
+    return cfg
+
+
+class Search:
+    """Algorithm 1 on the device (etune_cu_search_*), SimBackend measurements."""
+
+    def __init__(self, plan: "Plan", cfg: SearchConfig):
+        self.plan, self.cfg = plan, cfg
+        h = C.c_void_p()
+        _check(lib().etune_cu_search_create(plan.ctx.h, plan.h, C.byref(cfg), C.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        try:
+            lib().etune_cu_search_destroy(self.h)
+        except Exception:
+            pass
+
+    def initial(self) -> RoundReport:
+        r = RoundReport()
+        _check(lib().etune_cu_search_initial(self.h, C.byref(r)))
+        return r
+
+    def round(self) -> RoundReport:
+        r = RoundReport()
+        _check(lib().etune_cu_search_round(self.h, C.byref(r)))
+        return r
+
+    def run(self):
+        cap = int(self.cfg.max_rounds) + 2
+        arr = (RoundReport * cap)()
+        n = C.c_int64()
+        _check(lib().etune_cu_search_run(self.h, C.cast(arr, C.c_void_p), cap, C.byref(n)))
+        return [arr[i] for i in range(min(n.value, cap))]
+
+    def best(self):
+        s = np.zeros(12, np.int64)
+        i, lat, en = C.c_uint64(), C.c_double(), C.c_double()
+        _check(lib().etune_cu_search_best(self.h, s.ctypes.data, C.byref(i), C.byref(lat), C.byref(en)))
+        return s, i.value, lat.value, en.value
+
+    def parents(self):
+        import torch
+        n = C.c_int64()
+        _check(lib().etune_cu_search_parents(self.h, None, 0, C.byref(n)))
+        out = torch.empty(n.value, dtype=torch.int64, device=torch.device("cuda", self.plan.ctx.device))
+        _check(lib().etune_cu_search_parents(self.h, _ptr(out), n.value, C.byref(n)))
+        return out
 
 
 def topk(ctx: Context, score, k: int):

@@ -25,50 +25,7 @@ thread_local std::string g_error;
 void set_error(const std::string& msg) { g_error = msg; }
 }  // namespace etune_b200
 
-struct etune_cu_ctx {
-    int device = 0;
-    cudaStream_t stream = nullptr;
-    bool own_stream = false;
-    int sm_count = 0;
-    unsigned long long* d_err = nullptr;
-    void* scratch = nullptr;
-    size_t scratch_bytes = 0;
-    // staging for the *_host path
-    void* io = nullptr;
-    size_t io_bytes = 0;
-    void* breed = nullptr;  // BreedState + parent ids
-    size_t breed_bytes = 0;
-    ncclComm_t comm = nullptr;
-    int nranks = 1, rank = 0;
-    void* shard = nullptr;  // sharded-selection records
-    size_t shard_bytes = 0;
-    LaunchCtx lc() const { return LaunchCtx{stream, sm_count, d_err}; }
-};
-
-struct etune_cu_plan {
-    etune_cu_ctx* ctx = nullptr;
-    PlanBuild build;
-    uint8_t* d_blob = nullptr;
-    uint64_t serial = 0;
-};
-
-struct CompiledScore {
-    bool walk = false;        // compiled form unsupported / too large: general tree-walk kernel
-    uint8_t* d_blob = nullptr;
-    uint32_t bytes = 0;
-    int mask_bits = 32;
-    std::shared_ptr<ForestParams> params;  // tree records, passed by value to the kernel
-    ScoreStats stats;
-};
-
-struct etune_cu_forest {
-    etune_cu_ctx* ctx = nullptr;
-    ForestHost host;
-    uint8_t* d_predict = nullptr;
-    uint32_t predict_bytes = 0;
-    std::mutex mu;
-    std::map<uint64_t, CompiledScore> compiled;  // by plan serial
-};
+#include "handles.hpp"
 
 namespace {
 

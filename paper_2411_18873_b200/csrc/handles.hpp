@@ -1,0 +1,60 @@
+// Handle definitions shared by the C ABI (capi.cpp) and the host search driver
+// (search.cpp).  Not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "forest.hpp"
+#include "kernels.hpp"
+#include "plan.hpp"
+
+struct etune_cu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int sm_count = 0;
+    unsigned long long* d_err = nullptr;
+    void* scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // staging for the *_host path
+    void* io = nullptr;
+    size_t io_bytes = 0;
+    void* breed = nullptr;  // BreedState + parent ids
+    size_t breed_bytes = 0;
+    ncclComm_t comm = nullptr;
+    int nranks = 1, rank = 0;
+    void* shard = nullptr;  // sharded-selection records
+    size_t shard_bytes = 0;
+    etune_b200::LaunchCtx lc() const { return etune_b200::LaunchCtx{stream, sm_count, d_err}; }
+};
+
+struct etune_cu_plan {
+    etune_cu_ctx* ctx = nullptr;
+    etune_b200::PlanBuild build;
+    uint8_t* d_blob = nullptr;
+    uint64_t serial = 0;
+};
+
+struct CompiledScore {
+    bool walk = false;        // compiled form unsupported / too large: general tree-walk kernel
+    uint8_t* d_blob = nullptr;
+    uint32_t bytes = 0;
+    int mask_bits = 32;
+    std::shared_ptr<etune_b200::ForestParams> params;  // tree records, passed by value to the kernel
+    etune_b200::ScoreStats stats;
+};
+
+struct etune_cu_forest {
+    etune_cu_ctx* ctx = nullptr;
+    etune_b200::ForestHost host;
+    uint8_t* d_predict = nullptr;
+    uint32_t predict_bytes = 0;
+    std::mutex mu;
+    std::map<uint64_t, CompiledScore> compiled;  // by plan serial
+};
+

@@ -94,6 +94,10 @@ cudaError_t launch_sample_large(const LaunchCtx& c, const uint8_t* d_plan, uint6
 cudaError_t launch_sample_small(const LaunchCtx& c, const uint8_t* d_plan, const int64_t dims[6], uint64_t seed,
                                 int64_t n, uint64_t* d_out, int64_t* d_found, int* d_flags, void* scratch);
 
+// dst[j] = src[idx[j]] for 8-byte elements (genomes, doubles); y = x / *divisor
+cudaError_t launch_gather_u64(const LaunchCtx& c, const void* d_src, const int64_t* d_idx, int64_t n, void* d_dst);
+cudaError_t launch_div_scalar(const LaunchCtx& c, const double* d_x, int64_t n, const double* d_divisor, double* d_y);
+
 // process-wide count of kernel launches (incremented by every launcher)
 void note_launches(int k);
 uint64_t launch_count();

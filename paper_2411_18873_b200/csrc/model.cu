@@ -78,7 +78,37 @@ __global__ void gather_records_kernel(const double* __restrict__ gs, const int64
     }
 }
 
+__global__ void gather_u64_kernel(const uint64_t* __restrict__ src, const int64_t* __restrict__ idx, int64_t n,
+                                  uint64_t* __restrict__ dst) {
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+        dst[j] = src[idx[j]];
+}
+
+__global__ void div_scalar_kernel(const double* __restrict__ x, int64_t n, const double* __restrict__ d,
+                                  double* __restrict__ y) {
+    const double v = *d;
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < n; j += int64_t(gridDim.x) * blockDim.x)
+        y[j] = __ddiv_rn(x[j], v);
+}
+
 }  // namespace
+
+cudaError_t launch_gather_u64(const LaunchCtx& c, const void* d_src, const int64_t* d_idx, int64_t n, void* d_dst) {
+    if (n <= 0) return cudaSuccess;
+    const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(c.sm_count) * 8));
+    gather_u64_kernel<<<grid, 256, 0, c.stream>>>(static_cast<const uint64_t*>(d_src), d_idx, n,
+                                                  static_cast<uint64_t*>(d_dst));
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_div_scalar(const LaunchCtx& c, const double* d_x, int64_t n, const double* d_divisor, double* d_y) {
+    if (n <= 0) return cudaSuccess;
+    const int grid = int(std::min<int64_t>((n + 255) / 256, int64_t(c.sm_count) * 8));
+    div_scalar_kernel<<<grid, 256, 0, c.stream>>>(d_x, n, d_divisor, d_y);
+    note_launches(1);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pack_records(const LaunchCtx& c, const double* d_score, const int64_t* d_lidx, int64_t kl,
                                 int64_t k, int64_t goff, double* d_rs, int64_t* d_rg) {

@@ -1,0 +1,365 @@
+// Algorithm 1: the energy-aware genetic search loop.
+// The reference has no code for it, so this is the repo's restatement; the CPU oracle
+// (oracle/etune_oracle.cpp, orc_run_search) runs the same loop step for step and the
+// GPU tests compare their round reports bit for bit.
+//
+// Host C++ orchestrates; every population-sized step is a kernel of this library,
+// called through its own C ABI:
+//   round r:  reproduce -> SimBackend latency -> top-M -> score with the model ->
+//             top-ceil(k M) -> SimBackend energy -> SNR -> append samples -> retrain ->
+//             parents = top-ceil(M/2) by prediction.
+// Only the per-round scalars (k, SNR, the measured records for the best-so-far) cross
+// to the host.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "handles.hpp"
+
+using namespace etune_b200;
+
+struct etune_cu_search {
+    etune_cu_ctx* ctx = nullptr;
+    const etune_cu_plan* plan = nullptr;
+    etune_search_config cfg{};
+    int k5 = 5;
+    int64_t round = -1;  // -1: initial round not run yet
+    int64_t cumulative = 0;
+    int stall = 0;
+    // best measured (energy, latency, id)
+    bool have_best = false;
+    uint64_t best_id = 0, best_genome = 0;
+    double best_lat = 0, best_en = 0, best_pow = 0;
+    // device buffers
+    uint64_t *pop = nullptr, *mgen = nullptr, *selgen = nullptr, *par = nullptr, *ids = nullptr;
+    double *lat = nullptr, *mpred = nullptr, *psel = nullptr, *mlat = nullptr, *mpow = nullptr, *men = nullptr,
+           *mnorm = nullptr;
+    int64_t *idx = nullptr, *sel = nullptr;
+    int64_t np = 0;
+    // training samples (grow by doubling)
+    double *feat = nullptr, *energy = nullptr;
+    int64_t nsamples = 0, cap = 0;
+    // model arrays
+    int32_t *m_feature = nullptr, *m_left = nullptr, *m_right = nullptr;
+    double *m_thr = nullptr, *m_value = nullptr, *m_sc = nullptr;
+    int64_t* m_off = nullptr;
+    etune_cu_forest* model = nullptr;
+    std::vector<void*> allocs;
+};
+
+namespace {
+
+etune_status sfail(etune_status st, const std::string& msg) {
+    set_error(msg);
+    return st;
+}
+
+#define SCU(expr)                                                                                   \
+    do {                                                                                            \
+        cudaError_t _e = (expr);                                                                    \
+        if (_e != cudaSuccess) return sfail(ETUNE_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+#define SOK(expr)                            \
+    do {                                     \
+        etune_status _s = (expr);            \
+        if (_s != ETUNE_OK) return _s;       \
+    } while (0)
+
+template <typename T>
+etune_status dalloc(etune_cu_search* s, T** p, int64_t n) {
+    void* v = nullptr;
+    SCU(cudaMalloc(&v, size_t(std::max<int64_t>(n, 1)) * sizeof(T)));
+    s->allocs.push_back(v);
+    *p = static_cast<T*>(v);
+    return ETUNE_OK;
+}
+
+int64_t ceil_fifths(int k5, int64_t M) {  // ceil(k * M) with k = k5 / 5, minimum 1
+    const int64_t v = (int64_t(k5) * M + 4) / 5;
+    return v < 1 ? 1 : v;
+}
+
+// append n measured candidates (features of `gen`, energies) to the training set
+etune_status append_samples(etune_cu_search* s, const uint64_t* gen, const double* en, int64_t n) {
+    etune_cu_ctx* c = s->ctx;
+    if (s->nsamples + n > s->cap) {
+        int64_t nc = std::max<int64_t>(s->cap * 2, s->nsamples + n);
+        double *f2 = nullptr, *e2 = nullptr;
+        SCU(cudaMalloc(&f2, size_t(nc) * 16 * 8));
+        SCU(cudaMalloc(&e2, size_t(nc) * 8));
+        if (s->nsamples) {
+            SCU(cudaMemcpyAsync(f2, s->feat, size_t(s->nsamples) * 16 * 8, cudaMemcpyDeviceToDevice, c->stream));
+            SCU(cudaMemcpyAsync(e2, s->energy, size_t(s->nsamples) * 8, cudaMemcpyDeviceToDevice, c->stream));
+        }
+        SCU(cudaStreamSynchronize(c->stream));
+        cudaFree(s->feat);
+        cudaFree(s->energy);
+        s->feat = f2;
+        s->energy = e2;
+        s->cap = nc;
+    }
+    SOK(etune_cu_features(c, s->plan, gen, n, s->feat + s->nsamples * 16, nullptr));
+    SCU(cudaMemcpyAsync(s->energy + s->nsamples, en, size_t(n) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    s->nsamples += n;
+    return ETUNE_OK;
+}
+
+etune_status retrain(etune_cu_search* s) {
+    etune_cu_ctx* c = s->ctx;
+    SOK(etune_cu_train(c, s->feat, s->energy, s->nsamples, &s->cfg.boost, s->m_feature, s->m_thr, s->m_left,
+                       s->m_right, s->m_value, s->m_off, s->m_sc, nullptr));
+    etune_cu_forest* f = nullptr;
+    SOK(etune_cu_forest_from_device(c, s->m_feature, s->m_thr, s->m_left, s->m_right, s->m_value, s->m_off,
+                                    s->cfg.boost.num_trees, s->m_sc, s->cfg.boost.learning_rate, &f));
+    if (s->model) etune_cu_forest_destroy(s->model);
+    s->model = f;
+    return ETUNE_OK;
+}
+
+// best-so-far over the n measured records of this round
+etune_status update_best(etune_cu_search* s, const uint64_t* gen, int64_t n, bool* improved) {
+    etune_cu_ctx* c = s->ctx;
+    SOK(etune_cu_candidate_ids(c, s->plan, gen, n, s->ids));
+    const size_t m = static_cast<size_t>(n);
+    std::vector<uint64_t> ids(m), g(m);
+    std::vector<double> lat(m), en(m), pw(m);
+    SCU(cudaMemcpyAsync(ids.data(), s->ids, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(g.data(), gen, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(lat.data(), s->mlat, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(en.data(), s->men, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(pw.data(), s->mpow, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    SOK(etune_cu_synchronize(c, nullptr));
+    const double before = s->have_best ? s->best_en : std::numeric_limits<double>::infinity();
+    for (int64_t i = 0; i < n; ++i) {
+        const bool better = !s->have_best || en[i] < s->best_en ||
+                            (en[i] == s->best_en && (lat[i] < s->best_lat ||
+                                                     (lat[i] == s->best_lat && ids[i] < s->best_id)));
+        if (better) {
+            s->have_best = true;
+            s->best_en = en[i];
+            s->best_lat = lat[i];
+            s->best_id = ids[i];
+            s->best_pow = pw[i];
+            s->best_genome = g[i];
+        }
+    }
+    // "improvement > 0.1 %" of the best measured energy
+    *improved = s->best_en < before * (1.0 - s->cfg.improve_rel);
+    return ETUNE_OK;
+}
+
+void fill_report(const etune_cu_search* s, int kb, double snr, int64_t measured, double ms, etune_round_report* r) {
+    if (!r) return;
+    r->round = s->round;
+    r->k_before_fifths = kb;
+    r->k_after_fifths = s->k5;
+    r->snr_db = snr;
+    r->measured = measured;
+    r->cumulative_measured = s->cumulative;
+    r->best_id = s->best_id;
+    r->best_latency_ms = s->best_lat;
+    r->best_energy_mj = s->best_en;
+    r->best_power_w = s->best_pow;
+    r->wall_ms = ms;
+}
+
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+}  // namespace
+
+extern "C" {
+
+void etune_default_search_config(etune_search_config* o) {
+    std::memset(o, 0, sizeof(*o));
+    o->M = 512;
+    o->generation_size = 2048;
+    o->k_init_fifths = 5;
+    o->max_rounds = 10;
+    o->patience = 5;
+    o->inverted_semantics = 0;
+    o->mu_db = 20.0;
+    o->improve_rel = 0.001;
+    o->rng_seed = 42;
+    etune_default_genetic_rates(&o->rates);
+    etune_default_boost_params(&o->boost);
+}
+
+etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, const etune_search_config* cfg,
+                                    etune_cu_search** out) {
+    if (!c || !p || !out) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    etune_search_config C;
+    etune_default_search_config(&C);
+    if (cfg) C = *cfg;
+    if (!(C.M > 0 && C.M <= C.generation_size))
+        return sfail(ETUNE_ERR_VALIDATION, "SearchConfig needs 0 < M <= generation_size");
+    if (C.k_init_fifths < 0 || C.k_init_fifths > 5) return sfail(ETUNE_ERR_VALIDATION, "k must lie in [0, 1]");
+    if (!std::isfinite(C.mu_db)) return sfail(ETUNE_ERR_VALIDATION, "mu_db must be finite");
+    if (C.boost.max_depth < 0 || C.boost.max_depth > train_max_depth() || C.boost.num_trees < 0)
+        return sfail(ETUNE_ERR_UNSUPPORTED, "boost parameters outside this build's range");
+    auto s = std::make_unique<etune_cu_search>();
+    s->ctx = c;
+    s->plan = p;
+    s->cfg = C;
+    s->k5 = C.k_init_fifths;
+    const int64_t G = C.generation_size, M = C.M;
+    SOK(dalloc(s.get(), &s->pop, G));
+    SOK(dalloc(s.get(), &s->lat, G));
+    SOK(dalloc(s.get(), &s->idx, M));
+    SOK(dalloc(s.get(), &s->mgen, M));
+    SOK(dalloc(s.get(), &s->mpred, M));
+    SOK(dalloc(s.get(), &s->sel, M));
+    SOK(dalloc(s.get(), &s->selgen, M));
+    SOK(dalloc(s.get(), &s->psel, M));
+    SOK(dalloc(s.get(), &s->mlat, M));
+    SOK(dalloc(s.get(), &s->mpow, M));
+    SOK(dalloc(s.get(), &s->men, M));
+    SOK(dalloc(s.get(), &s->mnorm, M));
+    SOK(dalloc(s.get(), &s->par, M));
+    SOK(dalloc(s.get(), &s->ids, M));
+    const int64_t nodes = int64_t(C.boost.num_trees) * ((int64_t(1) << (C.boost.max_depth + 1)) - 1);
+    SOK(dalloc(s.get(), &s->m_feature, nodes));
+    SOK(dalloc(s.get(), &s->m_left, nodes));
+    SOK(dalloc(s.get(), &s->m_right, nodes));
+    SOK(dalloc(s.get(), &s->m_thr, nodes));
+    SOK(dalloc(s.get(), &s->m_value, nodes));
+    SOK(dalloc(s.get(), &s->m_off, C.boost.num_trees + 1));
+    SOK(dalloc(s.get(), &s->m_sc, 2));
+    *out = s.release();
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_search_destroy(etune_cu_search* s) {
+    if (!s) return ETUNE_OK;
+    cudaStreamSynchronize(s->ctx->stream);
+    if (s->model) etune_cu_forest_destroy(s->model);
+    for (void* p : s->allocs) cudaFree(p);
+    cudaFree(s->feat);
+    cudaFree(s->energy);
+    delete s;
+    return ETUNE_OK;
+}
+
+// initial_round: sample, latency-filter to M, measure all M, first model.
+etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* rep) {
+    if (!s) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "null search");
+    etune_cu_ctx* c = s->ctx;
+    const double t0 = now_ms();
+    const int64_t G = s->cfg.generation_size, M = s->cfg.M;
+    SOK(etune_cu_sample_random(c, s->plan, G, s->cfg.rng_seed, s->pop, nullptr));
+    SOK(etune_cu_sim_measure(c, s->plan, s->pop, G, s->lat, nullptr, nullptr, nullptr));
+    SOK(etune_cu_topk(c, s->lat, G, M, s->idx));  // LatencyEvaAndPick(Kernel_generation, M)
+    SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
+    SOK(etune_cu_sim_measure(c, s->plan, s->mgen, M, s->mlat, s->mpow, s->men, nullptr));
+    SOK(append_samples(s, s->mgen, s->men, M));
+    SOK(retrain(s));
+    SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(M) * 8, cudaMemcpyDeviceToDevice, c->stream));
+    s->np = M;
+    s->round = 0;
+    s->cumulative = M;
+    bool improved = false;
+    SOK(update_best(s, s->mgen, M, &improved));
+    fill_report(s, s->k5, std::numeric_limits<double>::quiet_NaN(), M, now_ms() - t0, rep);
+    return ETUNE_OK;
+}
+
+// round
+etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) {
+    if (!s) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "null search");
+    if (s->round < 0) return sfail(ETUNE_ERR_VALIDATION, "initial round has not run");
+    etune_cu_ctx* c = s->ctx;
+    const double t0 = now_ms();
+    const int64_t G = s->cfg.generation_size, M = s->cfg.M;
+    const int64_t r = s->round + 1;
+    // 1. GeneticReproduction(Kernel_parents)
+    SOK(etune_cu_reproduce(c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
+                           nullptr, nullptr));
+    // 2. LatencyEvaAndPick(Kernel_generation, M)
+    SOK(etune_cu_sim_measure(c, s->plan, s->pop, G, s->lat, nullptr, nullptr, nullptr));
+    SOK(etune_cu_topk(c, s->lat, G, M, s->idx));
+    SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
+    // 3. EnergyModelEvaAndPick(Kernel_M, EnergyModel, k*M)
+    SOK(etune_cu_score(c, s->plan, s->model, s->mgen, M, s->mpred, nullptr));
+    const int64_t km = ceil_fifths(s->k5, M);
+    SOK(etune_cu_topk(c, s->mpred, M, km, s->sel));
+    SCU(launch_gather_u64(c->lc(), s->mgen, s->sel, km, s->selgen));
+    SCU(launch_gather_u64(c->lc(), s->mpred, s->sel, km, s->psel));
+    // 4. NVMLMeasurement(Kernel_kM)  (SimBackend)
+    SOK(etune_cu_sim_measure(c, s->plan, s->selgen, km, s->mlat, s->mpow, s->men, nullptr));
+    // 6. SNR of step-3 predictions vs the measurements in the model's normalised units
+    SCU(launch_div_scalar(c->lc(), s->men, km, s->m_sc + 1, s->mnorm));
+    double snr = 0.0;
+    SOK(etune_cu_snr_db(c, s->psel, s->mnorm, km, &snr, nullptr));
+    // 8. parents <- ceil(0.5 M) lowest model-scored of the M
+    const int64_t np = (M + 1) / 2;
+    SOK(etune_cu_topk(c, s->mpred, M, np, s->idx));
+    SCU(launch_gather_u64(c->lc(), s->mgen, s->idx, np, s->par));
+    s->np = np;
+    // 5. ModelUpdate on all accumulated samples
+    SOK(append_samples(s, s->selgen, s->men, km));
+    SOK(retrain(s));
+    // 7. k controller, k in integer fifths
+    const int kb = s->k5;
+    const bool poor = s->cfg.inverted_semantics ? !(snr < s->cfg.mu_db) : (snr < s->cfg.mu_db);
+    s->k5 = poor ? std::min(5, s->k5 + 1) : std::max(0, s->k5 - 1);
+    s->round = r;
+    s->cumulative += km;
+    bool improved = false;
+    SOK(update_best(s, s->selgen, km, &improved));
+    s->stall = improved ? 0 : s->stall + 1;
+    fill_report(s, kb, snr, km, now_ms() - t0, rep);
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_search_run(etune_cu_search* s, etune_round_report* reports, int64_t cap, int64_t* n_reports) {
+    if (!s) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "null search");
+    int64_t n = 0;
+    etune_round_report r{};
+    if (s->round < 0) {
+        SOK(etune_cu_search_initial(s, &r));
+        if (reports && n < cap) reports[n] = r;
+        ++n;
+    }
+    while (s->round < s->cfg.max_rounds && s->stall < s->cfg.patience) {
+        SOK(etune_cu_search_round(s, &r));
+        if (reports && n < cap) reports[n] = r;
+        ++n;
+    }
+    if (n_reports) *n_reports = n;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_search_best(etune_cu_search* s, etune_schedule* h_sched, uint64_t* h_id, double* h_lat,
+                                  double* h_en) {
+    if (!s || !s->have_best) return sfail(ETUNE_ERR_VALIDATION, "no measured candidate yet");
+    if (h_id) *h_id = s->best_id;
+    if (h_lat) *h_lat = s->best_lat;
+    if (h_en) *h_en = s->best_en;
+    if (h_sched) {
+        etune_cu_ctx* c = s->ctx;
+        SCU(cudaMemcpyAsync(s->ids, &s->best_genome, 8, cudaMemcpyHostToDevice, c->stream));
+        etune_schedule* d = nullptr;
+        SCU(cudaMalloc(&d, sizeof(etune_schedule)));
+        SOK(etune_cu_decode(c, s->plan, s->ids, 1, d));
+        SCU(cudaMemcpyAsync(h_sched, d, sizeof(etune_schedule), cudaMemcpyDeviceToHost, c->stream));
+        SCU(cudaStreamSynchronize(c->stream));
+        cudaFree(d);
+    }
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_search_parents(etune_cu_search* s, uint64_t* d_out, int64_t cap, int64_t* n) {
+    if (!s || !n) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    *n = s->np;
+    const int64_t m = std::min(cap, s->np);
+    if (m > 0 && d_out)
+        SCU(cudaMemcpyAsync(d_out, s->par, size_t(m) * 8, cudaMemcpyDeviceToDevice, s->ctx->stream));
+    return ETUNE_OK;
+}
+
+}  // extern "C"

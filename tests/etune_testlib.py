@@ -119,6 +119,8 @@ class Oracle(_Lib):
         L.orc_counters.argtypes = [I64P, I64P, C.c_int64, C.c_int, I64P]
         L.orc_features.argtypes = [I64P, I64P, C.c_int64, C.c_int, F64P]
         L.orc_sim_measure.argtypes = [I64P, I64P, C.c_int64, F64P, C.c_uint64, F64P]
+        L.orc_run_search.argtypes = [I64P, I64P, F64P, C.c_uint64, I64P, F64P, C.c_uint64, C.c_int64, I64P, F64P,
+                                     C.POINTER(C.c_int64), I64P, C.POINTER(C.c_int64)]
         for nm in ("orc_mt64_words", "orc_std_mt64_words"):
             getattr(L, nm).argtypes = [C.c_uint64, C.c_int64, U64P]
         for nm in ("orc_lemire", "orc_std_uniform"):
@@ -192,6 +194,26 @@ class Oracle(_Lib):
         out = np.zeros((len(sched), 4), np.float64)
         self._check(self.L.orc_sim_measure(op, sched, len(sched), dev12, int(d["rng_seed"]), out))
         return out
+
+    def run_search(self, op, M, G, seed, max_rounds=10, patience=5, k_init_fifths=5, inverted=0, num_trees=100,
+                   max_depth=6, mu_db=20.0, improve_rel=0.001, rates=(0.85, 0.10, 0.05), lr=0.1,
+                   min_leaf_weight=1e-3, reg_lambda=1.0, dev=None, limits=None):
+        """Algorithm 1 restatement -> (reports_int n x 6, reports_f64 n x 4, parent schedules)."""
+        d = dict(DEFAULT_DEVICE)
+        d.update(dev or {})
+        dev12 = np.array([d[k] for k in DEVICE_FIELDS], np.float64)
+        cfg_i = np.array([M, G, k_init_fifths, max_rounds, patience, inverted, num_trees, max_depth], np.int64)
+        cfg_d = np.array([mu_db, improve_rel, *rates, lr, min_leaf_weight, reg_lambda], np.float64)
+        cap = max_rounds + 1
+        ri = np.zeros((cap, 6), np.int64)
+        rd = np.zeros((cap, 4), np.float64)
+        par = np.zeros(((M + 1) // 2 if max_rounds > 0 else M, 12), np.int64)
+        par = np.zeros((M, 12), np.int64)
+        nr, npar = C.c_int64(), C.c_int64()
+        self._check(self.L.orc_run_search(op, default_limits() if limits is None else limits, dev12,
+                                          int(d["rng_seed"]), cfg_i, cfg_d, seed, cap, ri, rd, C.byref(nr), par,
+                                          C.byref(npar)))
+        return ri[:nr.value], rd[:nr.value], par[:npar.value]
 
     # --- search primitives
     def sample_random(self, op, n, seed, limits=None):
