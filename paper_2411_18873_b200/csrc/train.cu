@@ -16,8 +16,14 @@
 // exactly the order in which the reference's per-node scans and sample-order
 // routing visit the children's samples.  Leaves keep their (dead) ranges.
 //
-// Every kernel reads the data-dependent frontier size from device memory, so a whole
-// training is one launch sequence with no host synchronisation.
+// Every kernel reads the data-dependent frontier size from device memory, so one
+// tree is a fixed launch sequence: it is captured once as a CUDA graph and replayed
+// num_trees times, with no host synchronisation inside a training.
+//
+// Per level: gather (grad/hess/feature values into list order) -> chains (one warp per
+// (list, node): the sequential prefix sums, staged through shared memory) -> gains at
+// every position (parallel; per-(node, feature) argmax by two atomic passes) -> decide
+// -> left flags -> stable partition (global scan of the left flags + scatter).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,6 +31,7 @@
 
 #include "etune_internal.hpp"
 #include "kernels.hpp"
+#include "scan.cuh"
 
 namespace etune_b200 {
 
@@ -43,13 +50,14 @@ struct TrainCtl {
     int32_t seg_start[2][kMaxSeg], seg_end[2][kMaxSeg], seg_node[2][kMaxSeg];
     int32_t split[kMaxSeg];   // child rank r (children 2r, 2r+1 of the next frontier) or -1
     int32_t nnodes;
-    int32_t pad;
+    int32_t tree;             // trees finished
     int64_t out_nodes;        // nodes written to the output forest so far
     // current tree
     int32_t feature[kMaxNodes], left[kMaxNodes], right[kMaxNodes];
     double thr[kMaxNodes], value[kMaxNodes], sg[kMaxNodes], sh[kMaxNodes];
-    // per (segment, feature) best split candidate
-    double bgain[kMaxSeg][kF], bthr[kMaxSeg][kF];
+    // per (segment, feature) best split: max gain bits (gains are > 0), then min position
+    unsigned long long gbits[kMaxSeg][kF];
+    int32_t gpos[kMaxSeg][kF];
     double base, reference;
 };
 
@@ -64,14 +72,39 @@ __device__ __forceinline__ double obj(double g, double h, double lambda) {  // l
 }
 
 // ---------------------------------------------------------------- init
+// Sequential sum of x[0..n) in index order by one thread, reading 256-element chunks the
+// whole CTA staged into shared memory (the reference's loops are one dependent chain).
+__device__ double cta_sequential_sum(const double* __restrict__ x, int64_t n, double* stage) {
+    double acc = 0.0;
+    for (int64_t base = 0; base < n; base += 1024) {
+        const int cnt = int(n - base < 1024 ? n - base : 1024);
+        __syncthreads();
+        for (int j = threadIdx.x; j < cnt; j += blockDim.x) stage[j] = x[base + j];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int j = 0; j < cnt; j += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = stage[j + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j + u < cnt) acc = __dadd_rn(acc, v[u]);
+            }
+        }
+    }
+    return acc;  // meaningful in thread 0
+}
+
 // reference energy (min), NonPositiveEnergy check, targets, harmonic-mean base score
-// (one sequential chain, energy_model.cpp:199-202), pred = base.
+// (one sequential chain, energy_model.cpp:199-202), pred = base; `tmp` is n doubles.
 __global__ void __launch_bounds__(1024) init_kernel(const double* __restrict__ energy, int64_t n,
                                                    double* __restrict__ target, double* __restrict__ pred,
                                                    TrainCtl* ctl, unsigned long long* err,
-                                                   double* __restrict__ loss0) {
+                                                   double* __restrict__ loss0, double* __restrict__ tmp) {
     __shared__ double red[32];
+    __shared__ double stage[1024 + 8];
     __shared__ int bad;
+    __shared__ double s_base;
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
     double m = __longlong_as_double(0x7ff0000000000000ll);
@@ -92,43 +125,51 @@ __global__ void __launch_bounds__(1024) init_kernel(const double* __restrict__ e
     if (bad) return;
     double ref = red[0];
     for (int w = 1; w < int(blockDim.x >> 5); ++w) ref = red[w] < ref ? red[w] : ref;
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) target[i] = __ddiv_rn(energy[i], ref);
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const double t = __ddiv_rn(energy[i], ref);
+        target[i] = t;
+        tmp[i] = __ddiv_rn(1.0, t);
+    }
     __syncthreads();
-    __shared__ double s_base;
+    const double inv = cta_sequential_sum(tmp, n, stage);
     if (threadIdx.x == 0) {
-        double inv = 0.0;
-        for (int64_t i = 0; i < n; ++i) inv = __dadd_rn(inv, __ddiv_rn(1.0, target[i]));
         s_base = __ddiv_rn(static_cast<double>(n), inv);
         ctl->base = s_base;
         ctl->reference = ref;
         ctl->out_nodes = 0;
+        ctl->tree = 0;
     }
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) pred[i] = s_base;
-    if (loss0 && threadIdx.x == 0) {  // mean_loss() before any tree (cpp 221-227)
-        double tot = 0.0;
-        for (int64_t i = 0; i < n; ++i) {
-            const double d = __dsub_rn(s_base, target[i]);
-            tot = __dadd_rn(tot, __ddiv_rn(__dmul_rn(d, d), target[i]));
+    const double base = s_base;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) pred[i] = base;
+    if (loss0) {  // mean_loss() before any tree (cpp 221-227)
+        __syncthreads();
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const double d = __dsub_rn(base, target[i]);
+            tmp[i] = __ddiv_rn(__dmul_rn(d, d), target[i]);
         }
-        loss0[0] = __ddiv_rn(tot, static_cast<double>(n));
+        __syncthreads();
+        const double tot = cta_sequential_sum(tmp, n, stage);
+        if (threadIdx.x == 0) loss0[0] = __ddiv_rn(tot, static_cast<double>(n));
     }
 }
 
 // ----------------------------------------------------------------- sort
-// One CTA per feature: bitonic sort of (order_key(value), index) pairs in global
-// memory == std::stable_sort by value (energy_model.cpp:204-213); list 16 = identity.
+// One CTA per feature: bitonic sort of (order_key(value), index) pairs == std::stable_sort
+// by value (energy_model.cpp:204-213); list 16 = identity.  In shared memory when the
+// padded column fits (n <= 16384), else in global memory.
 __global__ void __launch_bounds__(1024) sort_kernel(const double* __restrict__ feats, int64_t n, int64_t n2,
-                                                   uint64_t* __restrict__ kbuf, uint32_t* __restrict__ ibuf,
-                                                   int32_t* __restrict__ lists) {
+                                                   int in_smem, uint64_t* __restrict__ kbuf,
+                                                   uint32_t* __restrict__ ibuf, int32_t* __restrict__ lists) {
+    extern __shared__ uint64_t sortmem[];
     const int f = blockIdx.x;
     int32_t* out = lists + int64_t(f) * n;
     if (f == kSampleList) {
         for (int64_t i = threadIdx.x; i < n; i += blockDim.x) out[i] = int32_t(i);
         return;
     }
-    uint64_t* K = kbuf + int64_t(f) * n2;
-    uint32_t* I = ibuf + int64_t(f) * n2;
+    uint64_t* K = in_smem ? sortmem : kbuf + int64_t(f) * n2;
+    uint32_t* I = in_smem ? reinterpret_cast<uint32_t*>(sortmem + n2) : ibuf + int64_t(f) * n2;
     for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) {
         K[i] = i < n ? order_key(feats[i * kF + f]) : ~0ull;
         I[i] = i < n ? uint32_t(i) : 0xffffffffu;
@@ -181,113 +222,180 @@ __global__ void grad_kernel(const double* __restrict__ pred, const double* __res
     }
 }
 
-// gl/hl[l][pos] = grad/hess[list[l][pos]]: the chains below then stream contiguously
-__global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int nl, const double* __restrict__ grad,
-                              const double* __restrict__ hess, double* __restrict__ gl, double* __restrict__ hl) {
-    const int64_t tot = int64_t(nl) * n;
-    const int64_t off = int64_t(kLists - nl) * n;  // nl == 1: sample list only
-    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
-        const int32_t idx = lists[off + q];
-        gl[off + q] = grad[idx];
-        hl[off + q] = hess[idx];
+// segment (frontier index) of every position, -1 for dead ranges; identical for all lists
+__global__ void segmap_kernel(int64_t n, int lvl, const TrainCtl* __restrict__ ctl, int32_t* __restrict__ segmap) {
+    const int b = lvl & 1;
+    const int nseg = ctl->nseg[b];
+    const int32_t* ss = ctl->seg_start[b];
+    const int32_t* se = ctl->seg_end[b];
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
+        int lo = 0, hi = nseg;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ss[mid] <= p) lo = mid + 1;
+            else hi = mid;
+        }
+        const int k = lo - 1;
+        segmap[p] = (k >= 0 && p < se[k]) ? k : -1;
     }
 }
 
-// One thread per (list, frontier segment): the sequential running sums.
+// gl/hl[l][p] = grad/hess[list[l][p]], fv[l][p] = feature l of that sample: everything the
+// chains and gains read afterwards is contiguous in list order
+__global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int nl, const double* __restrict__ grad,
+                              const double* __restrict__ hess, const double* __restrict__ feats,
+                              double* __restrict__ gl, double* __restrict__ hl, double* __restrict__ fv) {
+    const int64_t tot = int64_t(nl) * n;
+    const int64_t off = int64_t(kLists - nl) * n;  // nl == 1: sample list only
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t g = off + q;
+        const int32_t idx = lists[g];
+        gl[g] = grad[idx];
+        hl[g] = hess[idx];
+        if (g < int64_t(kF) * n) fv[g] = feats[int64_t(idx) * kF + g / n];
+    }
+}
+
+// One warp per (list, frontier segment): the sequential running sums, 256 elements at
+// a time staged through shared memory (coalesced in, one lane chains, coalesced out).
 //   lists 0..15: exclusive prefix at every position (the `run` of cpp 95-121)
 //   list 16:     the node's (grad, hess) totals in sample order (cpp 73-76, 150-155)
-__global__ void chain_kernel(int64_t n, int lvl, int only_totals, const double* __restrict__ gl,
-                             const double* __restrict__ hl, double* __restrict__ pg, double* __restrict__ ph,
-                             TrainCtl* ctl) {
+constexpr int kChainWarps = 4;
+constexpr int kChunk = 256;
+__global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int lvl, int only_totals,
+                                                                 const double* __restrict__ gl,
+                                                                 const double* __restrict__ hl,
+                                                                 double* __restrict__ pg, double* __restrict__ ph,
+                                                                 TrainCtl* ctl) {
+    __shared__ double ig[kChainWarps][kChunk + 8], ih[kChainWarps][kChunk + 8];
+    __shared__ double og[kChainWarps][kChunk], oh[kChainWarps][kChunk];
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     if (nseg <= 0) return;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x * kChainWarps + w;
     const int l = only_totals ? kSampleList : t / nseg;
     const int k = only_totals ? t : t % nseg;
     if (k >= nseg || l >= kLists) return;
     const int s = ctl->seg_start[b][k], e = ctl->seg_end[b][k];
     const double* G = gl + int64_t(l) * n;
     const double* Hh = hl + int64_t(l) * n;
-    double rg = 0.0, rh = 0.0;
-    if (l == kSampleList) {
-        for (int p = s; p < e; ++p) {
-            rg = __dadd_rn(rg, G[p]);
-            rh = __dadd_rn(rh, Hh[p]);
-        }
-        const int node = ctl->seg_node[b][k];
-        ctl->sg[node] = rg;
-        ctl->sh[node] = rh;
-        return;
-    }
     double* PG = pg + int64_t(l) * n;
     double* PH = ph + int64_t(l) * n;
-    for (int p = s; p < e; ++p) {
-        PG[p] = rg;
-        PH[p] = rh;
-        rg = __dadd_rn(rg, G[p]);
-        rh = __dadd_rn(rh, Hh[p]);
+    const bool prefixes = l != kSampleList;
+    double rg = 0.0, rh = 0.0;
+    for (int base = s; base < e; base += kChunk) {
+        const int cnt = min(kChunk, e - base);
+        for (int j = lane; j < cnt; j += 32) {
+            ig[w][j] = G[base + j];
+            ih[w][j] = Hh[base + j];
+        }
+        __syncwarp();
+        if (lane == 0) {
+            // full batches of 8: the chain only; each prefix lives in its own register until
+            // the batch is stored, so no store waits on (or blocks) the next add
+            const int full = cnt & ~7;
+            for (int j = 0; j < full; j += 8) {
+                double g[8], h[8], pgv[8], phv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    g[u] = ig[w][j + u];
+                    h[u] = ih[w][j + u];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    pgv[u] = rg;
+                    phv[u] = rh;
+                    rg = __dadd_rn(rg, g[u]);
+                    rh = __dadd_rn(rh, h[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    og[w][j + u] = pgv[u];
+                    oh[w][j + u] = phv[u];
+                }
+            }
+            for (int j = full; j < cnt; ++j) {
+                const double g = ig[w][j], h = ih[w][j];
+                og[w][j] = rg;
+                oh[w][j] = rh;
+                rg = __dadd_rn(rg, g);
+                rh = __dadd_rn(rh, h);
+            }
+        }
+        __syncwarp();
+        if (prefixes) {
+            for (int j = lane; j < cnt; j += 32) {
+                PG[base + j] = og[w][j];
+                PH[base + j] = oh[w][j];
+            }
+        }
+        __syncwarp();
+    }
+    if (lane == 0) {
+        if (!prefixes) {
+            const int node = ctl->seg_node[b][k];
+            ctl->sg[node] = rg;
+            ctl->sh[node] = rh;
+        } else {
+            ctl->gbits[k][l] = 0ull;
+            ctl->gpos[k][l] = 0x7fffffff;
+        }
     }
 }
 
-// One CTA per (segment, feature): best split of this node on this feature.
-__global__ void __launch_bounds__(256) gain_kernel(const double* __restrict__ feats, const int32_t* __restrict__ lists,
-                                                   int64_t n, int lvl, const double* __restrict__ pg,
-                                                   const double* __restrict__ ph, double mlw, double lambda,
-                                                   TrainCtl* ctl) {
+// split gain at every (feature list, position) (cpp 97-118); per-(node, feature) max
+// gain by atomicMax on the (positive) gain's bits
+__global__ void gain_kernel(int64_t n, int lvl, const int32_t* __restrict__ segmap, const double* __restrict__ fv,
+                            const double* __restrict__ pg, const double* __restrict__ ph, double mlw, double lambda,
+                            double* __restrict__ gains, TrainCtl* ctl) {
     const int b = lvl & 1;
-    const int k = blockIdx.x, f = blockIdx.y;
-    if (k >= ctl->nseg[b]) return;
-    const int s = ctl->seg_start[b][k], e = ctl->seg_end[b][k];
-    const int node = ctl->seg_node[b][k];
-    const double tg = ctl->sg[node], th = ctl->sh[node];
-    const double tobj = obj(tg, th, lambda);
-    const int32_t* L = lists + int64_t(f) * n;
-    const double* PG = pg + int64_t(f) * n;
-    const double* PH = ph + int64_t(f) * n;
-    double best = 0.0, bthr = 0.0;
-    int bpos = 0x7fffffff;
-    for (int p = s + 1 + int(threadIdx.x); p < e; p += blockDim.x) {
-        const double v = feats[int64_t(L[p]) * kF + f];
-        const double pv = feats[int64_t(L[p - 1]) * kF + f];
-        if (!(v > pv)) continue;
-        const double rg = PG[p], rh = PH[p];
-        const double qg = __dsub_rn(tg, rg), qh = __dsub_rn(th, rh);
-        if (!(rh >= mlw && qh >= mlw)) continue;
-        const double gain = __dmul_rn(0.5, __dsub_rn(__dadd_rn(obj(rg, rh, lambda), obj(qg, qh, lambda)), tobj));
-        if (gain > kMinSplitGain && (gain > best || (gain == best && p < bpos))) {
-            best = gain;
-            bpos = p;
-            bthr = __dmul_rn(0.5, __dadd_rn(pv, v));
-        }
-    }
-    // block argmax: larger gain, then smaller position
-    __shared__ double sgain[256], sthr[256];
-    __shared__ int spos[256];
-    sgain[threadIdx.x] = best;
-    spos[threadIdx.x] = bpos;
-    sthr[threadIdx.x] = bthr;
-    __syncthreads();
-    for (int st = blockDim.x >> 1; st > 0; st >>= 1) {
-        if (int(threadIdx.x) < st) {
-            const int o = threadIdx.x + st;
-            if (sgain[o] > sgain[threadIdx.x] || (sgain[o] == sgain[threadIdx.x] && spos[o] < spos[threadIdx.x])) {
-                sgain[threadIdx.x] = sgain[o];
-                spos[threadIdx.x] = spos[o];
-                sthr[threadIdx.x] = sthr[o];
+    const int64_t tot = int64_t(kF) * n;
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t p = q % n;
+        const int l = int(q / n);
+        const int k = segmap[p];
+        double gain = -1.0;
+        if (k >= 0 && p > ctl->seg_start[b][k]) {
+            const double v = fv[q], pv = fv[q - 1];
+            if (v > pv) {
+                const int node = ctl->seg_node[b][k];
+                const double tg = ctl->sg[node], th = ctl->sh[node];
+                const double rg = pg[q], rh = ph[q];
+                const double qg = __dsub_rn(tg, rg), qh = __dsub_rn(th, rh);
+                if (rh >= mlw && qh >= mlw) {
+                    const double g = __dmul_rn(
+                        0.5, __dsub_rn(__dadd_rn(obj(rg, rh, lambda), obj(qg, qh, lambda)), obj(tg, th, lambda)));
+                    if (g > kMinSplitGain) {
+                        gain = g;
+                        atomicMax(&ctl->gbits[k][l], static_cast<unsigned long long>(__double_as_longlong(g)));
+                    }
+                }
             }
         }
-        __syncthreads();
+        gains[q] = gain;
     }
-    if (threadIdx.x == 0) {
-        ctl->bgain[k][f] = spos[0] == 0x7fffffff ? 0.0 : sgain[0];
-        ctl->bthr[k][f] = sthr[0];
+}
+
+// earliest position attaining the max (ties: the reference's strict > keeps the first)
+__global__ void gainpos_kernel(int64_t n, const int32_t* __restrict__ segmap, const double* __restrict__ gains,
+                               TrainCtl* ctl) {
+    const int64_t tot = int64_t(kF) * n;
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
+        const double g = gains[q];
+        if (!(g > 0.0)) continue;
+        const int64_t p = q % n;
+        const int l = int(q / n);
+        const int k = segmap[p];
+        if (static_cast<unsigned long long>(__double_as_longlong(g)) == ctl->gbits[k][l])
+            atomicMin(&ctl->gpos[k][l], int32_t(p));
     }
 }
 
 // One CTA: choose each node's split (features in order, strictly larger gain wins,
 // cpp 111-117), allocate children in frontier order (cpp 130-143).
-__global__ void __launch_bounds__(1024) decide_kernel(int lvl, TrainCtl* ctl) {
+__global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const double* __restrict__ fv,
+                                                      TrainCtl* ctl) {
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     __shared__ int wsum[32];
@@ -300,16 +408,19 @@ __global__ void __launch_bounds__(1024) decide_kernel(int lvl, TrainCtl* ctl) {
         double bg = 0.0, bt = 0.0;
         if (k < nseg) {
             for (int f = 0; f < kF; ++f) {
-                const double g = ctl->bgain[k][f];
+                const unsigned long long bits = ctl->gbits[k][f];
+                if (bits == 0ull) continue;
+                const double g = __longlong_as_double(static_cast<long long>(bits));
                 if (g > kMinSplitGain && g > bg) {
                     bg = g;
                     bf = f;
-                    bt = ctl->bthr[k][f];
+                    const int64_t pos = ctl->gpos[k][f];
+                    const double* F = fv + int64_t(f) * n;
+                    bt = __dmul_rn(0.5, __dadd_rn(F[pos - 1], F[pos]));  // cpp 115-116
                 }
             }
         }
         const int flag = bf >= 0;
-        // exclusive scan of flags over the block
         const unsigned bal = __ballot_sync(0xffffffffu, flag);
         const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
         if (lane == 0) wsum[w] = __popc(bal);
@@ -350,96 +461,75 @@ __global__ void __launch_bounds__(1024) decide_kernel(int lvl, TrainCtl* ctl) {
     }
 }
 
-// One CTA per list: stable partition of every split segment into [left | right]
-// (value < threshold goes left, cpp 146-148).  List 16 also writes the children's
-// segment bounds.
-__global__ void __launch_bounds__(1024) partition_kernel(const double* __restrict__ feats,
-                                                        const int32_t* __restrict__ src, int32_t* __restrict__ dst,
-                                                        int32_t* __restrict__ pre, int64_t n, int lvl,
-                                                        TrainCtl* ctl) {
+// routing decision per sample of a split node: value < threshold goes left (cpp 146-148)
+__global__ void leftflag_kernel(const double* __restrict__ feats, const int32_t* __restrict__ lists, int64_t n,
+                                int lvl, const int32_t* __restrict__ segmap, const TrainCtl* __restrict__ ctl,
+                                uint8_t* __restrict__ lf) {
     const int b = lvl & 1;
-    const int l = blockIdx.x;
-    const int nseg = ctl->nseg[b];
-    const int32_t* S = src + int64_t(l) * n;
-    int32_t* D = dst + int64_t(l) * n;
-    int32_t* P = pre + int64_t(l) * (n + 1);
-    __shared__ int wsum[32];
-    __shared__ int carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    const int* ss = ctl->seg_start[b];
-    const int* se = ctl->seg_end[b];
-    auto seg_of = [&](int64_t p) -> int {  // active segment containing p, or -1
-        int lo = 0, hi = nseg;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (ss[mid] <= p) lo = mid + 1;
-            else hi = mid;
-        }
-        const int k = lo - 1;
-        return (k >= 0 && p < se[k]) ? k : -1;
-    };
-    auto goes_left = [&](int64_t p, int k) -> int {
-        if (k < 0 || ctl->split[k] < 0) return 0;
+    const int32_t* S = lists + int64_t(kSampleList) * n;
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
+        const int k = segmap[p];
+        if (k < 0 || ctl->split[k] < 0) continue;
         const int node = ctl->seg_node[b][k];
-        return feats[int64_t(S[p]) * kF + ctl->feature[node]] < ctl->thr[node] ? 1 : 0;
-    };
-    // pass 1: exclusive prefix of left flags over the whole list
-    const int64_t nr = (n + blockDim.x - 1) / blockDim.x * blockDim.x;
-    for (int64_t p0 = 0; p0 < nr; p0 += blockDim.x) {
-        const int64_t p = p0 + threadIdx.x;
-        const int fl = p < n ? goes_left(p, seg_of(p)) : 0;
-        const unsigned bal = __ballot_sync(0xffffffffu, fl);
-        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-        if (lane == 0) wsum[w] = __popc(bal);
-        __syncthreads();
-        int before = carry + __popc(bal & ((1u << lane) - 1u));
-        int total = 0;
-        for (int i = 0; i < int(blockDim.x >> 5); ++i) {
-            if (i < w) before += wsum[i];
-            total += wsum[i];
-        }
-        if (p < n) P[p] = before;
-        __syncthreads();
-        if (threadIdx.x == 0) carry += total;
-        __syncthreads();
+        const int32_t idx = S[p];
+        lf[idx] = feats[int64_t(idx) * kF + ctl->feature[node]] < ctl->thr[node] ? 1 : 0;
     }
-    if (threadIdx.x == 0) P[n] = carry;
-    __syncthreads();
-    // pass 2: scatter
-    for (int64_t p = threadIdx.x; p < n; p += blockDim.x) {
-        const int k = seg_of(p);
+}
+
+struct LeftFlagFn {  // flag of list position q (0 outside split segments)
+    const int32_t* lists;
+    const int32_t* segmap;
+    const int32_t* split;
+    const uint8_t* lf;
+    int64_t n;
+    __device__ int64_t operator()(int64_t q) const {
+        const int k = segmap[q % n];
+        return (k >= 0 && split[k] >= 0) ? int64_t(lf[lists[q]]) : 0;
+    }
+};
+struct PrefixWrite {
+    int64_t* pfx;
+    __device__ void operator()(int64_t q, int64_t ex) const { pfx[q] = ex; }
+};
+
+// stable partition of every split segment into [left | right] in every list; list 16
+// also writes the children's segment bounds
+__global__ void scatter_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                               const int64_t* __restrict__ pfx, const int32_t* __restrict__ segmap, int64_t n,
+                               int lvl, TrainCtl* ctl) {
+    const int b = lvl & 1;
+    const int64_t tot = int64_t(kLists) * n;
+    for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t l = q / n, p = q % n;
+        const int k = segmap[p];
         int64_t d = p;
         if (k >= 0 && ctl->split[k] >= 0) {
-            const int s = ss[k], e = se[k];
-            const int pl = P[p] - P[s];
-            const int L = P[e] - P[s];
-            const int left = P[p + 1] - P[p];
+            const int64_t s = ctl->seg_start[b][k], e = ctl->seg_end[b][k];
+            const int64_t* P = pfx + l * n;
+            const int64_t pl = P[p] - P[s];
+            const int64_t L = P[e] - P[s];
+            const int64_t left = P[p + 1] - P[p];
             d = left ? s + pl : s + L + (p - s - pl);
+            if (l == kSampleList && p == s) {
+                const int r = ctl->split[k];
+                ctl->seg_start[b ^ 1][2 * r] = int32_t(s);
+                ctl->seg_end[b ^ 1][2 * r] = int32_t(s + L);
+                ctl->seg_start[b ^ 1][2 * r + 1] = int32_t(s + L);
+                ctl->seg_end[b ^ 1][2 * r + 1] = int32_t(e);
+            }
         }
-        D[d] = S[p];
-    }
-    if (l == kSampleList) {
-        for (int k = threadIdx.x; k < nseg; k += blockDim.x) {
-            const int r = ctl->split[k];
-            if (r < 0) continue;
-            const int s = ss[k], e = se[k];
-            const int L = P[e] - P[s];
-            ctl->seg_start[b ^ 1][2 * r] = s;
-            ctl->seg_end[b ^ 1][2 * r] = s + L;
-            ctl->seg_start[b ^ 1][2 * r + 1] = s + L;
-            ctl->seg_end[b ^ 1][2 * r + 1] = e;
-        }
+        dst[l * n + d] = src[q];
     }
 }
 
 // Leaf Newton weights (cpp 161-166) and the tree appended to the output forest.
-__global__ void __launch_bounds__(1024) finalize_kernel(int tree, double lambda, TrainCtl* ctl,
+__global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl* ctl,
                                                        int32_t* __restrict__ o_feature, double* __restrict__ o_thr,
                                                        int32_t* __restrict__ o_left, int32_t* __restrict__ o_right,
                                                        double* __restrict__ o_value, int64_t* __restrict__ o_off) {
     const int nn = ctl->nnodes;
     const int64_t base = ctl->out_nodes;
+    const int tree = ctl->tree;
     for (int i = threadIdx.x; i < nn; i += blockDim.x) {
         if (ctl->feature[i] < 0) ctl->value[i] = __ddiv_rn(-ctl->sg[i], __dadd_rn(ctl->sh[i], lambda));
         o_feature[base + i] = ctl->feature[i];
@@ -453,6 +543,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(int tree, double lambda,
         if (tree == 0) o_off[0] = 0;
         o_off[tree + 1] = base + nn;
         ctl->out_nodes = base + nn;
+        ctl->tree = tree + 1;
     }
 }
 
@@ -470,14 +561,18 @@ __global__ void update_kernel(const double* __restrict__ feats, int64_t n, doubl
     }
 }
 
-__global__ void loss_kernel(const double* __restrict__ pred, const double* __restrict__ target, int64_t n,
-                            double* __restrict__ out) {
-    double tot = 0.0;
-    for (int64_t i = 0; i < n; ++i) {
+__global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ pred,
+                                                   const double* __restrict__ target, int64_t n,
+                                                   const TrainCtl* __restrict__ ctl, double* __restrict__ loss,
+                                                   double* __restrict__ tmp) {
+    __shared__ double stage[1024 + 8];
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = __dsub_rn(pred[i], target[i]);
-        tot = __dadd_rn(tot, __ddiv_rn(__dmul_rn(d, d), target[i]));
+        tmp[i] = __ddiv_rn(__dmul_rn(d, d), target[i]);
     }
-    *out = __ddiv_rn(tot, static_cast<double>(n));
+    __syncthreads();
+    const double tot = cta_sequential_sum(tmp, n, stage);
+    if (threadIdx.x == 0) loss[ctl->tree] = __ddiv_rn(tot, static_cast<double>(n));  // after finalize: round t+1
 }
 
 int64_t pow2_at_least(int64_t v) {
@@ -492,12 +587,16 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 size_t train_scratch_bytes(int64_t n) {
     const int64_t n2 = pow2_at_least(n);
-    return al256(sizeof(TrainCtl)) + 3 * al256(8 * size_t(n))         // target, pred, grad
-           + al256(8 * size_t(n))                                       // hess
-           + 4 * al256(8 * size_t(kLists) * n)                          // gl, hl, pg, ph
-           + 3 * al256(4 * size_t(kLists) * n)                          // base lists + 2 work buffers
-           + al256(4 * size_t(kLists) * (n + 1))                        // partition prefixes
-           + al256(size_t(kF) * n2 * 12);                               // sort keys + indices
+    const size_t L = size_t(kLists) * size_t(n);
+    const size_t F = size_t(kF) * size_t(n);
+    return al256(sizeof(TrainCtl)) + 4 * al256(8 * size_t(n))     // target, pred, grad, hess
+           + 2 * al256(8 * L)                                     // gl, hl
+           + 4 * al256(8 * F)                                     // fv, pg, ph, gains
+           + 3 * al256(4 * L)                                     // base lists + 2 work buffers
+           + al256(8 * (L + 1))                                   // partition prefix
+           + al256(4 * size_t(n)) + al256(size_t(n))              // segmap, left flags
+           + al256(8 * ((L + 1023) / 1024 + 2))                   // scan tile sums
+           + al256(size_t(kF) * n2 * 12);                         // sort keys + indices
 }
 
 int train_max_depth() { return kMaxDepth; }
@@ -513,64 +612,107 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
         return r;
     };
     const int64_t n2 = pow2_at_least(n);
+    const size_t L = size_t(kLists) * size_t(n);
+    const size_t F = size_t(kF) * size_t(n);
     TrainCtl* ctl = reinterpret_cast<TrainCtl*>(take(sizeof(TrainCtl)));
     double* target = reinterpret_cast<double*>(take(8 * size_t(n)));
     double* pred = reinterpret_cast<double*>(take(8 * size_t(n)));
     double* grad = reinterpret_cast<double*>(take(8 * size_t(n)));
     double* hess = reinterpret_cast<double*>(take(8 * size_t(n)));
-    double* gl = reinterpret_cast<double*>(take(8 * size_t(kLists) * n));
-    double* hl = reinterpret_cast<double*>(take(8 * size_t(kLists) * n));
-    double* pg = reinterpret_cast<double*>(take(8 * size_t(kLists) * n));
-    double* ph = reinterpret_cast<double*>(take(8 * size_t(kLists) * n));
-    int32_t* base_lists = reinterpret_cast<int32_t*>(take(4 * size_t(kLists) * n));
-    int32_t* work[2] = {reinterpret_cast<int32_t*>(take(4 * size_t(kLists) * n)),
-                        reinterpret_cast<int32_t*>(take(4 * size_t(kLists) * n))};
-    int32_t* pre = reinterpret_cast<int32_t*>(take(4 * size_t(kLists) * (n + 1)));
+    double* gl = reinterpret_cast<double*>(take(8 * L));
+    double* hl = reinterpret_cast<double*>(take(8 * L));
+    double* fv = reinterpret_cast<double*>(take(8 * F));
+    double* pg = reinterpret_cast<double*>(take(8 * F));
+    double* ph = reinterpret_cast<double*>(take(8 * F));
+    double* gains = reinterpret_cast<double*>(take(8 * F));
+    int32_t* base_lists = reinterpret_cast<int32_t*>(take(4 * L));
+    int32_t* work[2] = {reinterpret_cast<int32_t*>(take(4 * L)), reinterpret_cast<int32_t*>(take(4 * L))};
+    int64_t* pfx = reinterpret_cast<int64_t*>(take(8 * (L + 1)));
+    int32_t* segmap = reinterpret_cast<int32_t*>(take(4 * size_t(n)));
+    uint8_t* lf = reinterpret_cast<uint8_t*>(take(size_t(n)));
+    int64_t* sums = reinterpret_cast<int64_t*>(take(8 * ((L + 1023) / 1024 + 2)));
     uint64_t* kbuf = reinterpret_cast<uint64_t*>(take(size_t(kF) * n2 * 12));
     uint32_t* ibuf = reinterpret_cast<uint32_t*>(kbuf + size_t(kF) * n2);
 
-    const int ew = int(std::min<int64_t>((n + 255) / 256, int64_t(c.sm_count) * 8));
-    init_kernel<<<1, 1024, 0, c.stream>>>(d_energy, n, target, pred, ctl, c.d_err, o_loss);
-    sort_kernel<<<kLists, 1024, 0, c.stream>>>(d_feat, n, n2, kbuf, ibuf, base_lists);
-    int launches = 2;
-    for (int t = 0; t < num_trees; ++t) {
-        grad_kernel<<<ew, 256, 0, c.stream>>>(pred, target, n, grad, hess, ctl);
-        const int32_t* cur = base_lists;
-        int wb = 0;
-        int lvl = 0;
-        for (int depth = 0; depth < max_depth; ++depth, ++lvl) {
-            const int segs = 1 << depth;  // frontier bound at this depth
-            gather_kernel<<<int(std::min<int64_t>((kLists * n + 255) / 256, int64_t(c.sm_count) * 16)), 256, 0,
-                            c.stream>>>(cur, n, kLists, grad, hess, gl, hl);
-            const int chains = kLists * segs;
-            chain_kernel<<<(chains + 63) / 64, 64, 0, c.stream>>>(n, lvl, 0, gl, hl, pg, ph, ctl);
-            gain_kernel<<<dim3(segs, kF), 256, 0, c.stream>>>(d_feat, cur, n, lvl, pg, ph, mlw, lambda, ctl);
-            decide_kernel<<<1, 1024, 0, c.stream>>>(lvl, ctl);
-            partition_kernel<<<kLists, 1024, 0, c.stream>>>(d_feat, cur, work[wb], pre, n, lvl, ctl);
-            cur = work[wb];
-            wb ^= 1;
-            launches += 5;
-        }
-        // totals of the last frontier (children created at the deepest level)
-        gather_kernel<<<int(std::min<int64_t>((n + 255) / 256, int64_t(c.sm_count) * 16)), 256, 0, c.stream>>>(
-            cur, n, 1, grad, hess, gl, hl);
-        const int segs = 1 << max_depth;
-        chain_kernel<<<(segs + 63) / 64, 64, 0, c.stream>>>(n, lvl, 1, gl, hl, pg, ph, ctl);
-        finalize_kernel<<<1, 1024, 0, c.stream>>>(t, lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
-        update_kernel<<<ew, 256, 0, c.stream>>>(d_feat, n, lr, ctl, pred);
-        launches += 4;
-        if (o_loss) {
-            loss_kernel<<<1, 1, 0, c.stream>>>(pred, target, n, o_loss + t + 1);
-            launches += 1;
-        }
+    init_kernel<<<1, 1024, 0, c.stream>>>(d_energy, n, target, pred, ctl, c.d_err, o_loss, grad);
+    const size_t sort_smem = size_t(n2) * 12;
+    const int sort_in_smem = sort_smem <= 200 * 1024 ? 1 : 0;
+    if (sort_in_smem) {
+        cudaError_t ea = cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sort_smem));
+        if (ea != cudaSuccess) return ea;
     }
+    sort_kernel<<<kLists, 1024, sort_in_smem ? sort_smem : 0, c.stream>>>(d_feat, n, n2, sort_in_smem, kbuf, ibuf,
+                                                                          base_lists);
+    note_launches(2);
     if (num_trees == 0) {
         cudaMemsetAsync(o_off, 0, sizeof(int64_t), c.stream);
+        cudaMemcpyAsync(o_scalars, &ctl->base, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
+        return cudaGetLastError();
     }
+
+    // one tree as a fixed launch sequence, captured once and replayed num_trees times
+    cudaStream_t cap = nullptr;
+    cudaError_t e = cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return e;
+    e = cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(cap);
+        return e;
+    }
+    auto grid = [&](int64_t items) {
+        return int(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(c.sm_count) * 16)));
+    };
+    int launches = 0;
+    grad_kernel<<<grid(n), 256, 0, cap>>>(pred, target, n, grad, hess, ctl);
+    ++launches;
+    const int32_t* cur = base_lists;
+    int wb = 0;
+    int lvl = 0;
+    for (int depth = 0; depth < max_depth; ++depth, ++lvl) {
+        const int segs = 1 << depth;  // frontier bound at this depth
+        segmap_kernel<<<grid(n), 256, 0, cap>>>(n, lvl, ctl, segmap);
+        gather_kernel<<<grid(int64_t(L)), 256, 0, cap>>>(cur, n, kLists, grad, hess, d_feat, gl, hl, fv);
+        const int warps = kLists * segs;
+        chain_kernel<<<(warps + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap>>>(n, lvl, 0, gl, hl, pg,
+                                                                                              ph, ctl);
+        gain_kernel<<<grid(int64_t(F)), 256, 0, cap>>>(n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
+        gainpos_kernel<<<grid(int64_t(F)), 256, 0, cap>>>(n, segmap, gains, ctl);
+        decide_kernel<<<1, 1024, 0, cap>>>(n, lvl, fv, ctl);
+        leftflag_kernel<<<grid(n), 256, 0, cap>>>(d_feat, cur, n, lvl, segmap, ctl, lf);
+        e = scan_apply(cap, int64_t(L), LeftFlagFn{cur, segmap, ctl->split, lf, n}, PrefixWrite{pfx}, sums,
+                       pfx + L);
+        if (e != cudaSuccess) break;
+        scatter_kernel<<<grid(int64_t(L)), 256, 0, cap>>>(cur, work[wb], pfx, segmap, n, lvl, ctl);
+        cur = work[wb];
+        wb ^= 1;
+        launches += 11;
+    }
+    // totals of the last frontier (children created at the deepest level)
+    gather_kernel<<<grid(n), 256, 0, cap>>>(cur, n, 1, grad, hess, d_feat, gl, hl, fv);
+    const int segs = 1 << max_depth;
+    chain_kernel<<<(segs + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap>>>(n, lvl, 1, gl, hl, pg, ph,
+                                                                                       ctl);
+    finalize_kernel<<<1, 1024, 0, cap>>>(lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
+    update_kernel<<<grid(n), 256, 0, cap>>>(d_feat, n, lr, ctl, pred);
+    launches += 4;
+    if (o_loss) {
+        loss_kernel<<<1, 1024, 0, cap>>>(pred, target, n, ctl, o_loss, gains);
+        launches += 1;
+    }
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ec = cudaStreamEndCapture(cap, &graph);
+    if (e == cudaSuccess) e = ec;
+    cudaGraphExec_t exec = nullptr;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+    for (int t = 0; t < num_trees && e == cudaSuccess; ++t) e = cudaGraphLaunch(exec, c.stream);
+    note_launches(launches * num_trees);
     // base score + reference energy
-    cudaMemcpyAsync(o_scalars, &ctl->base, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
-    note_launches(launches);
-    return cudaGetLastError();
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(o_scalars, &ctl->base, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
+    if (exec) cudaGraphExecDestroy(exec);  // deferred by the driver until the launches complete
+    if (graph) cudaGraphDestroy(graph);
+    cudaStreamDestroy(cap);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace etune_b200
