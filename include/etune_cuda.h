@@ -213,6 +213,13 @@ etune_status etune_cu_score(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                             etune_cu_forest* forest, const uint64_t* d_genome, int64_t n,
                             double* d_pred, uint64_t* d_ids /*nullable*/);
 
+/* One step of the hot path: fused score of a device population, then its k best by
+ * (prediction asc, index asc) into d_idx (sorted).  d_ids nullable. */
+etune_status etune_cu_score_select(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                   etune_cu_forest* forest, const uint64_t* d_genome, int64_t n,
+                                   int64_t k, double* d_pred, uint64_t* d_ids /*nullable*/,
+                                   int64_t* d_idx);
+
 /* Reference-facing end-to-end call with HOST buffers: schedules in the reference's
  * Schedule layout -> predictions (+ ids).  Host->device copy, encode (legality check),
  * fused score and device->host copy, synchronised.  Equivalent to

@@ -113,6 +113,7 @@ _SIGS = {
     "etune_cu_forest_destroy": (C.c_int, [_VP]),
     "etune_cu_predict": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
     "etune_cu_score": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR]),
+    "etune_cu_score_select": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _I64, _PTR, _PTR, _PTR]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
     "etune_cu_train": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(BoostParams), _PTR, _PTR, _PTR, _PTR, _PTR, _PTR,
@@ -421,6 +422,12 @@ class Forest:
         _check(lib().etune_cu_score(self.ctx.h, plan.h, self.h, _ptr(genome), n, _ptr(pred), _ptr(ids)))
         return (pred, ids) if (with_ids or ids_out is not None) else pred
 
+    def score_select(self, plan: Plan, genome, k: int, pred, idx, ids=None):
+        """Fused score + keep-the-best (etune_cu_score_select) into preallocated tensors."""
+        _check(lib().etune_cu_score_select(self.ctx.h, plan.h, self.h, _ptr(genome), genome.shape[0], int(k),
+                                           _ptr(pred), _ptr(ids), _ptr(idx)))
+        return pred, idx
+
     def score_host(self, plan: Plan, sched: np.ndarray, pred: np.ndarray, ids: Optional[np.ndarray] = None):
         """Reference-facing call on HOST buffers (pinned numpy views recommended)."""
         n = sched.shape[0]
@@ -457,11 +464,11 @@ def attach_nccl(ctx: Context, unique_id: bytes, nranks: int, rank: int):
     _check(lib().etune_cu_ctx_attach_nccl(ctx.h, buf, int(nranks), int(rank)))
 
 
-def topk_sharded(ctx: Context, score, global_offset: int, k: int):
+def topk_sharded(ctx: Context, score, global_offset: int, k: int, idx=None, sc=None):
     """Population-sharded keep-the-best: identical (global idx, score) on every rank."""
     import torch
-    idx = torch.empty(k, dtype=torch.int64, device=score.device)
-    sc = torch.empty(k, dtype=torch.float64, device=score.device)
+    idx = idx if idx is not None else torch.empty(k, dtype=torch.int64, device=score.device)
+    sc = sc if sc is not None else torch.empty(k, dtype=torch.float64, device=score.device)
     _check(lib().etune_cu_topk_sharded(ctx.h, _ptr(score), score.shape[0], int(global_offset), int(k), _ptr(idx),
                                        _ptr(sc)))
     return idx, sc
@@ -533,8 +540,8 @@ class Search:
         return out
 
 
-def topk(ctx: Context, score, k: int):
+def topk(ctx: Context, score, k: int, out=None):
     import torch
-    out = torch.empty(k, dtype=torch.int64, device=score.device)
+    out = out if out is not None else torch.empty(k, dtype=torch.int64, device=score.device)
     _check(lib().etune_cu_topk(ctx.h, _ptr(score), score.shape[0], k, _ptr(out)))
     return out

@@ -17,15 +17,44 @@
 #include "forest.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "handles.hpp"
 
 using namespace etune_b200;
 
 namespace etune_b200 {
 thread_local std::string g_error;
+void ctx_free_now(etune_cu_ctx* c) {
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_err);
+    cudaFree(c->scratch);
+    cudaFree(c->io);
+    cudaFree(c->breed);
+    cudaFree(c->shard);
+    if (c->h2d) {
+        cudaStreamDestroy(c->h2d);
+        cudaStreamDestroy(c->d2h);
+        for (int b = 0; b < 2; ++b) {
+            cudaEventDestroy(c->ev_in[b]);
+            cudaEventDestroy(c->ev_done[b]);
+            cudaEventDestroy(c->ev_out[b]);
+        }
+    }
+    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->own_stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+
+// Handles hold a reference on their ctx: destroying the ctx before its plans, forests
+// or searches (any order a garbage collector picks) defers the release until the last
+// of them is gone.
+void ctx_retain(etune_cu_ctx* c) { c->refs.fetch_add(1); }
+void ctx_release(etune_cu_ctx* c) {
+    if (c->refs.fetch_sub(1) == 1 && c->closing.load()) ctx_free_now(c);
+}
 void set_error(const std::string& msg) { g_error = msg; }
 }  // namespace etune_b200
-
-#include "handles.hpp"
 
 namespace {
 
@@ -100,6 +129,7 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     cs.bytes = uint32_t(blob.size());
     const ScoreHdr* hdr = reinterpret_cast<const ScoreHdr*>(blob.data());
     cs.mask_bits = hdr->mask_bits;
+    CU(score_occupancy(cs.mask_bits, cs.bytes, &cs.per_sm));
     cs.params = std::make_shared<ForestParams>();
     std::memset(cs.params.get(), 0, sizeof(ForestParams));
     std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
@@ -113,7 +143,8 @@ cudaError_t run_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* 
     if (cs->walk)
         return launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
                                  d_pred, d_ids);
-    return launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params);
+    return launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
+                        cs->per_sm);
 }
 
 }  // namespace
@@ -181,16 +212,9 @@ etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out) {
 
 etune_status etune_cu_ctx_destroy(etune_cu_ctx* c) {
     if (!c) return ETUNE_OK;
-    cudaSetDevice(c->device);
-    cudaStreamSynchronize(c->stream);
-    cudaFree(c->d_err);
-    cudaFree(c->scratch);
-    cudaFree(c->io);
-    cudaFree(c->breed);
-    cudaFree(c->shard);
-    if (c->comm) ncclCommDestroy(c->comm);
-    if (c->own_stream) cudaStreamDestroy(c->stream);
-    delete c;
+    c->closing.store(true);
+    ctx_retain(c);
+    ctx_release(c);  // frees now unless plans / forests / searches still hold it
     return ETUNE_OK;
 }
 
@@ -242,14 +266,17 @@ etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, cons
         std::lock_guard<std::mutex> lock(g_serial_mu);
         p->serial = ++g_serial;
     }
+    ctx_retain(c);
     *out = p.release();
     return ETUNE_OK;
 }
 
 etune_status etune_cu_plan_destroy(etune_cu_plan* p) {
     if (!p) return ETUNE_OK;
+    etune_cu_ctx* c = p->ctx;
     cudaFree(p->d_blob);
     delete p;
+    ctx_release(c);
     return ETUNE_OK;
 }
 
@@ -406,6 +433,7 @@ etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, con
     CU(cudaMemcpyAsync(f->d_predict, blob.data(), blob.size(), cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     f->predict_bytes = uint32_t(blob.size());
+    ctx_retain(c);
     *out = f.release();
     return ETUNE_OK;
 }
@@ -414,7 +442,9 @@ etune_status etune_cu_forest_destroy(etune_cu_forest* f) {
     if (!f) return ETUNE_OK;
     cudaFree(f->d_predict);
     for (auto& kv : f->compiled) cudaFree(kv.second.d_blob);
+    etune_cu_ctx* c = f->ctx;
     delete f;
+    ctx_release(c);
     return ETUNE_OK;
 }
 
@@ -436,6 +466,13 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     return ETUNE_OK;
 }
 
+etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
+                                   const uint64_t* d_genome, int64_t n, int64_t k, double* d_pred, uint64_t* d_ids,
+                                   int64_t* d_idx) {
+    if (etune_status st = etune_cu_score(c, p, f, d_genome, n, d_pred, d_ids)) return st;
+    return etune_cu_topk(c, d_pred, n, k, d_idx);
+}
+
 etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
                                  const etune_schedule* h_sched, int64_t n, double* h_pred, uint64_t* h_ids,
                                  int64_t* first_bad) {
@@ -445,25 +482,50 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
     if (n == 0) return ETUNE_OK;
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
-    // chunked so the staging buffers stay bounded; one synchronisation at the end
-    const int64_t chunk = int64_t(1) << 18;
+    // Chunked three-stage pipeline over two staging buffers: H2D of chunk i+1 (copy-in
+    // stream) overlaps encode+score of chunk i (ctx stream) and D2H of chunk i-1
+    // (copy-out stream); PCIe is full duplex.  One synchronisation at the end.
+    const int64_t chunk = int64_t(1) << 17;
     const size_t per = sizeof(etune_schedule) + 8 + 8 + 8;  // sched, genome, pred, id
     const int64_t cap = n < chunk ? n : chunk;
-    if (etune_status st = ensure_io(c, size_t(cap) * per)) return st;
+    if (etune_status st = ensure_io(c, 2 * size_t(cap) * per)) return st;
+    if (!c->h2d) {
+        CU(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+        CU(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CU(cudaEventCreateWithFlags(&c->ev_in[b], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->ev_done[b], cudaEventDisableTiming));
+            CU(cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming));
+        }
+    }
+    // the caller's earlier work on the ctx stream happens-before this call's copies
+    CU(cudaEventRecord(c->ev_done[0], c->stream));
+    CU(cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
+    CU(cudaStreamWaitEvent(c->d2h, c->ev_done[0], 0));
     char* io = static_cast<char*>(c->io);
-    auto* d_sched = reinterpret_cast<etune_schedule*>(io);
-    auto* d_gen = reinterpret_cast<uint64_t*>(io + size_t(cap) * sizeof(etune_schedule));
-    auto* d_pred = reinterpret_cast<double*>(io + size_t(cap) * (sizeof(etune_schedule) + 8));
-    auto* d_ids = reinterpret_cast<uint64_t*>(io + size_t(cap) * (sizeof(etune_schedule) + 16));
-    for (int64_t lo = 0; lo < n; lo += chunk) {
+    for (int64_t lo = 0, i = 0; lo < n; lo += chunk, ++i) {
+        const int b = int(i & 1);
+        char* base = io + size_t(b) * size_t(cap) * per;
+        auto* d_sched = reinterpret_cast<etune_schedule*>(base);
+        auto* d_gen = reinterpret_cast<uint64_t*>(base + size_t(cap) * sizeof(etune_schedule));
+        auto* d_pred = reinterpret_cast<double*>(base + size_t(cap) * (sizeof(etune_schedule) + 8));
+        auto* d_ids = reinterpret_cast<uint64_t*>(base + size_t(cap) * (sizeof(etune_schedule) + 16));
         const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
+        if (i >= 2) CU(cudaStreamWaitEvent(c->h2d, c->ev_out[b], 0));  // buffer b drained by chunk i-2's D2H
         CU(cudaMemcpyAsync(d_sched, h_sched + lo, size_t(m) * sizeof(etune_schedule), cudaMemcpyHostToDevice,
-                           c->stream));
+                           c->h2d));
+        CU(cudaEventRecord(c->ev_in[b], c->h2d));
+        CU(cudaStreamWaitEvent(c->stream, c->ev_in[b], 0));
         CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, m, d_gen, lo));
         CU(run_score(c, p, f, cs, d_gen, m, d_pred, h_ids ? d_ids : nullptr));
-        CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
-        if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->stream));
+        CU(cudaEventRecord(c->ev_done[b], c->stream));
+        CU(cudaStreamWaitEvent(c->d2h, c->ev_done[b], 0));
+        CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+        if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+        CU(cudaEventRecord(c->ev_out[b], c->d2h));
     }
+    CU(cudaEventRecord(c->ev_out[0], c->d2h));
+    CU(cudaStreamWaitEvent(c->stream, c->ev_out[0], 0));
     return etune_cu_synchronize(c, first_bad);
 }
 

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -14,6 +15,8 @@
 #include "plan.hpp"
 
 struct etune_cu_ctx {
+    std::atomic<int> refs{0};        // live plans / forests / searches
+    std::atomic<bool> closing{false};
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -30,8 +33,16 @@ struct etune_cu_ctx {
     int nranks = 1, rank = 0;
     void* shard = nullptr;  // sharded-selection records
     size_t shard_bytes = 0;
+    // *_host pipelines: copy-in / copy-out streams and per-buffer events
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
     etune_b200::LaunchCtx lc() const { return etune_b200::LaunchCtx{stream, sm_count, d_err}; }
 };
+
+namespace etune_b200 {
+void ctx_retain(etune_cu_ctx* c);
+void ctx_release(etune_cu_ctx* c);
+}  // namespace etune_b200
 
 struct etune_cu_plan {
     etune_cu_ctx* ctx = nullptr;
@@ -45,6 +56,7 @@ struct CompiledScore {
     uint8_t* d_blob = nullptr;
     uint32_t bytes = 0;
     int mask_bits = 32;
+    int per_sm = 1;           // resident CTAs per SM (queried once at compile time)
     std::shared_ptr<etune_b200::ForestParams> params;  // tree records, passed by value to the kernel
     etune_b200::ScoreStats stats;
 };

@@ -534,14 +534,25 @@ cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
 }
 
 template <typename M>
+cudaError_t score_occupancy_t(uint32_t bytes, int* per_sm) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, score_kernel<M>);
+    if (e != cudaSuccess) return e;
+    // the attribute is a per-function ceiling: the opt-in maximum minus static smem
+    e = cudaFuncSetAttribute(score_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - int(fa.sharedSizeBytes));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, score_kernel<M>, kScoreThreads, bytes);
+    if (e != cudaSuccess) return e;
+    return *per_sm < 1 ? cudaErrorInvalidConfiguration : cudaSuccess;
+}
+
+template <typename M>
 cudaError_t launch_score_t(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
-                           int64_t n, double* d_pred, uint64_t* d_ids, const ForestParams& fp) {
-    cudaError_t e = cudaFuncSetAttribute(score_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_kernel<M>, kScoreThreads, bytes);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+                           int64_t n, double* d_pred, uint64_t* d_ids, const ForestParams& fp, int per_sm) {
     const int64_t want = (n + kScoreThreads - 1) / kScoreThreads;
     const int64_t cap = int64_t(c.sm_count) * per_sm;
     const int grid = int(want < cap ? want : cap);
@@ -550,11 +561,16 @@ cudaError_t launch_score_t(const LaunchCtx& c, const uint8_t* d_score, uint32_t 
     return cudaGetLastError();
 }
 
+cudaError_t score_occupancy(int mask_bits, uint32_t bytes, int* per_sm) {
+    return mask_bits == 32 ? score_occupancy_t<uint32_t>(bytes, per_sm) : score_occupancy_t<uint64_t>(bytes, per_sm);
+}
+
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
-                         int64_t n, double* d_pred, uint64_t* d_ids, int mask_bits, const ForestParams& fp) {
+                         int64_t n, double* d_pred, uint64_t* d_ids, int mask_bits, const ForestParams& fp,
+                         int per_sm) {
     if (n <= 0) return cudaSuccess;
-    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp)
-                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp);
+    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm)
+                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm);
 }
 
 cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,

@@ -37,9 +37,11 @@ cudaError_t launch_sim_measure(const LaunchCtx& c, const uint8_t* d_plan, uint32
                                int64_t* d_iters);
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                             const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
+// resident CTAs per SM of the compiled score kernel for a blob size (sets the smem ceiling)
+cudaError_t score_occupancy(int mask_bits, uint32_t bytes, int* per_sm);
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
                          const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
-                         int mask_bits, const ForestParams& fp);
+                         int mask_bits, const ForestParams& fp, int per_sm);
 // General path: features + reference tree walk (any forest the reference can train).
 cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,
                               uint32_t pred_bytes, const uint64_t* d_genome, int64_t n, double* d_out,

@@ -230,6 +230,7 @@ etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, con
     SOK(dalloc(s.get(), &s->m_value, nodes));
     SOK(dalloc(s.get(), &s->m_off, C.boost.num_trees + 1));
     SOK(dalloc(s.get(), &s->m_sc, 2));
+    ctx_retain(c);
     *out = s.release();
     return ETUNE_OK;
 }
@@ -241,7 +242,9 @@ etune_status etune_cu_search_destroy(etune_cu_search* s) {
     for (void* p : s->allocs) cudaFree(p);
     cudaFree(s->feat);
     cudaFree(s->energy);
+    etune_cu_ctx* c = s->ctx;
     delete s;
+    ctx_release(c);
     return ETUNE_OK;
 }
 

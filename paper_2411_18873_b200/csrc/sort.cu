@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "kernels.hpp"
 
@@ -456,12 +457,24 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
         const size_t need = size_t(kSmallSort) * 12;
         if (smem < need) smem = need;
     }
-    cudaError_t e = cudaFuncSetAttribute(topk_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    if (e != cudaSuccess) return e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, topk_coop_kernel, kCoopT, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+    // one 1024-thread CTA per SM; the smem ceiling is set once to the device maximum and
+    // co-residency holds as long as the request fits it
+    static std::once_flag once;
+    static int optin = 0;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaFuncAttributes fa{};
+        attr_err = cudaFuncGetAttributes(&fa, topk_coop_kernel);
+        optin -= int(fa.sharedSizeBytes);  // dynamic ceiling = opt-in maximum minus static smem
+        if (attr_err == cudaSuccess)
+            attr_err = cudaFuncSetAttribute(topk_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    if (smem > size_t(optin)) return cudaErrorCooperativeLaunchTooLarge;
+    cudaError_t e = cudaSuccess;
     if (G > 1024) G = 1024;
     e = cudaMemsetAsync(w, 0, sizeof(TopkWork), c.stream);
     if (e != cudaSuccess) return e;
