@@ -25,7 +25,6 @@ namespace etune_b200 {
 
 namespace {
 
-constexpr int kT = 512;            // threads per CTA for streaming kernels
 constexpr int kTile = 4096;        // items per tile (count/scatter, LSD sort)
 constexpr int kBins = 2048;        // 11-bit digits
 constexpr int kSmallSort = 4096;   // one-CTA bitonic bound
@@ -40,7 +39,7 @@ constexpr int kMaxPasses = 7;             // 8 + 11-bit digits over <= 64 varyin
 constexpr int kSmemKeys = 24 * 1024;      // keys cached per CTA (192 KB)
 
 struct TopkWork {
-    unsigned long long andor[2];
+    unsigned long long cta_and[1024], cta_or[1024];         // phase A, one slot per CTA (no init)
     unsigned int hist[kMaxPasses][kBins];
     unsigned int cnt[2][1024];            // per-CTA (lt, eq) counts
 };
@@ -108,13 +107,36 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
             a &= ra[i];
             o |= ro[i];
         }
-        atomicAnd(&w->andor[0], ra[0] & a);
-        atomicOr(&w->andor[1], ro[0] | o);
+        w->cta_and[b] = ra[0] & a;
+        w->cta_or[b] = ro[0] | o;
+    }
+    if (b == 0) {  // the rest of the work area is initialised here: no memsets before the launch
+        unsigned int* hz = &w->hist[0][0];
+        for (int i = tid; i < kMaxPasses * kBins; i += blockDim.x) hz[i] = 0u;
     }
     grid.sync();
 
     // ---- phase B: radix select of the exact k-th key T (MSB first, 11-bit digits)
-    const uint64_t andv = w->andor[0], varying = andv ^ w->andor[1];
+    uint64_t andv = ~0ull, orv = 0ull;
+    for (int i = tid; i < G; i += blockDim.x) {  // block-wide reduction of the per-CTA slots
+        andv &= w->cta_and[i];
+        orv |= w->cta_or[i];
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        andv &= __shfl_xor_sync(0xffffffffu, andv, s);
+        orv |= __shfl_xor_sync(0xffffffffu, orv, s);
+    }
+    __syncthreads();  // ra/ro reuse
+    if ((tid & 31) == 0) {
+        ra[tid >> 5] = andv;
+        ro[tid >> 5] = orv;
+    }
+    __syncthreads();
+    for (int i = 0; i < int(blockDim.x >> 5); ++i) {
+        andv &= ra[i];
+        orv |= ro[i];
+    }
+    const uint64_t varying = andv ^ orv;
     uint64_t prefix = andv;  // bits above `bit` fixed so far
     unsigned rem = unsigned(k);  // 1-based rank of T inside the current prefix group
     int bit = varying ? 64 - __clzll(static_cast<long long>(varying)) : 0;  // bits [0, bit) still open
@@ -446,7 +468,6 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
         p += al256(4 * size_t(n));
     }
     uint32_t* lsd_hist = reinterpret_cast<uint32_t*>(p);
-
     // one CTA per SM; cache keys in smem when the per-CTA chunk fits
     int G = c.sm_count;
     const int64_t chunk = (n + G - 1) / G;
@@ -476,12 +497,8 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
     if (smem > size_t(optin)) return cudaErrorCooperativeLaunchTooLarge;
     cudaError_t e = cudaSuccess;
     if (G > 1024) G = 1024;
-    e = cudaMemsetAsync(w, 0, sizeof(TopkWork), c.stream);
-    if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(&w->andor[0], 0xff, 8, c.stream);
-    if (e != cudaSuccess) return e;
-    void* args[] = {(void*)&d_score, (void*)&n, (void*)&k, (void*)&w, (void*)&sk[0], (void*)&sv[0], (void*)&d_idx,
-                    (void*)&cache, (void*)&final_sort};
+    void* args[] = {(void*)&d_score, (void*)&n,           (void*)&k,        (void*)&w,          (void*)&sk[0],
+                    (void*)&sv[0],   (void*)&d_idx,       (void*)&cache,    (void*)&final_sort};
     e = cudaLaunchCooperativeKernel((const void*)topk_coop_kernel, dim3(G), dim3(kCoopT), args, smem, c.stream);
     if (e != cudaSuccess) return e;
     note_launches(1);

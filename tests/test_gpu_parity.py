@@ -221,3 +221,33 @@ def test_score_general_walk_path(oracle, ctx, capi, depth, smooth):
     ctx.synchronize()
     assert (bits(pred) == ref.view(np.uint64)).all()
     assert (capi.as_u64(dids) == ids).all()
+
+
+def _topk_case(kind, n):
+    rng = np.random.default_rng(n)
+    if kind == "all_equal":
+        return np.full(n, 1.25)
+    if kind == "hidden_small":  # small values where the stride-n/8192 sample never looks: overflow fallback
+        v = rng.uniform(2.0, 3.0, n)
+        stride = n // 8192
+        mask = (np.arange(n) % stride) != 0
+        idx = np.nonzero(mask)[0][:40000]
+        v[idx] = rng.uniform(0.5, 0.6, len(idx))
+        return v
+    if kind == "hidden_large":  # sample sees only the smallest values: too few keys <= T -> fallback
+        stride = n // 8192
+        v = rng.uniform(5.0, 6.0, n)
+        v[::stride] = rng.uniform(0.1, 0.2, len(v[::stride]))
+        return v
+    if kind == "two_values":
+        return rng.choice([0.75, 1.5], n, p=[0.001, 0.999])
+    return rng.normal(1.0, 0.1, n)
+
+
+@pytest.mark.parametrize("kind", ["all_equal", "hidden_small", "hidden_large", "two_values", "normal"])
+@pytest.mark.parametrize("n,k", [(1 << 20, 1024), (300000, 4096), (40000, 1)])
+def test_topk_fast_path_and_fallback(oracle, ctx, capi, kind, n, k):
+    vals = _topk_case(kind, n)
+    idx = capi.topk(ctx, dev(vals), k)
+    ctx.synchronize()
+    assert (idx.cpu().numpy() == oracle.topk(vals, k)).all()
