@@ -121,6 +121,11 @@ int channel_of(int j) {
 
 }  // namespace
 
+size_t debruijn_slot(int leaf, int mbits) {
+    if (mbits == 32) return size_t((uint32_t(1u << leaf) * 0x077CB531u) >> 27);
+    return size_t((uint64_t(1) << leaf) * 0x03f79d71b4ca8b09ull >> 58);
+}
+
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
                               ScoreStats* stats, std::string* err) {
     if (etune_status st = forest_validate(F, err)) return st;
@@ -333,7 +338,22 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
             return ETUNE_ERR_UNSUPPORTED;
         }
         R.meta = uint32_t(leaves.size()) | (used_mask << 24);
-        leaves.insert(leaves.end(), lv.begin(), lv.end());
+        // leaf l lives at its de Bruijn slot of (1 << l): the device turns the exit mask's
+        // lowest set bit into the slot with AND/NEG/IMAD/SHF (no XU bit-scan)
+        // and the block is split into the high words of all slots, then the low words:
+        // 32-bit loads of distinct slots never share a bank (a 64-bit load of 32 slots spans
+        // 256 B and conflicts), so each leaf value costs exactly two conflict-free wavefronts
+        std::vector<uint32_t> words(size_t(2 * mbits), 0u);
+        for (size_t l = 0; l < lv.size(); ++l) {
+            uint64_t bits = 0;
+            std::memcpy(&bits, &lv[l], 8);
+            const size_t slot = debruijn_slot(int(l), mbits);
+            words[slot] = uint32_t(bits >> 32);
+            words[size_t(mbits) + slot] = uint32_t(bits);
+        }
+        std::vector<double> block(static_cast<size_t>(mbits));
+        std::memcpy(block.data(), words.data(), words.size() * 4);
+        leaves.insert(leaves.end(), block.begin(), block.end());
         S.total_leaves += int(lv.size());
         S.max_leaves = std::max(S.max_leaves, int(lv.size()));
     }

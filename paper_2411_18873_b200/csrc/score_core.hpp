@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 
 #include "etune_internal.hpp"
 
@@ -105,6 +106,17 @@ inline double ldsf64(SAddr a) { return *reinterpret_cast<const double*>(a); }
 inline SAddr blob_saddr(const uint8_t* S) { return S; }
 #endif
 
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ double join_f64(uint32_t hi, uint32_t lo) { return __hiloint2double(int(hi), int(lo)); }
+#else
+inline double join_f64(uint32_t hi, uint32_t lo) {
+    const uint64_t b = (uint64_t(hi) << 32) | lo;
+    double d;
+    std::memcpy(&d, &b, 8);
+    return d;
+}
+#endif
+
 template <typename M>
 __host__ __device__ __forceinline__ M lds_mask(SAddr a) {
     if constexpr (sizeof(M) == 4) return lds32(a);
@@ -121,10 +133,21 @@ __host__ __device__ __forceinline__ M tree_mask(const TreeRec& r, const SAddr* c
     return m;
 }
 
+// Exit leaf = lowest set bit of the mask; leaves are stored at the de Bruijn slot of
+// their bit (forest.cpp), so the slot is (m & -m) * B >> (bits - log2 bits): integer
+// ALU/FMA-pipe work instead of a BREV + FLO pair on the saturated XU pipe.
 template <typename M>
 __host__ __device__ __forceinline__ double leaf_value(SAddr base, const TreeRec& r, M m) {
-    const int l = sizeof(M) == 4 ? ETUNE_FFS32(m) : ETUNE_FFS64(m);
-    return ldsf64(base + ((r.meta & 0xffffffu) + uint32_t(l) * 8u));
+    uint32_t slot;
+    if constexpr (sizeof(M) == 4) {
+        slot = (uint32_t(m & (0u - m)) * 0x077CB531u) >> 27;
+    } else {
+        slot = uint32_t((uint64_t(m & (0ull - m)) * 0x03f79d71b4ca8b09ull) >> 58);
+    }
+    const SAddr blk = base + ((r.meta & 0xffffffu) + slot * 4u);
+    const uint32_t hi = lds32(blk);
+    const uint32_t lo = lds32(blk + uint32_t(sizeof(M)) * 32u);  // low words follow the mbits high words
+    return join_f64(hi, lo);
 }
 
 template <typename M>
