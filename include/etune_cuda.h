@@ -189,6 +189,40 @@ etune_status etune_cu_sim_measure(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                   const uint64_t* d_genome, int64_t n, double* d_latency_ms,
                                   double* d_power_w, double* d_energy_mj, int64_t* d_iterations);
 
+/* NVML measurement harness (north_star (5); the reference's NvmlBackend, measure.hpp:
+ * 130-140, is a stub that always throws BackendUnavailable).  Each schedule runs as a
+ * runtime-tiled fp32 GEMM / implicit-GEMM conv kernel honouring its tiling, k_tile,
+ * unroll and vectorize; after warmup_ms of repeats, iterations = clamp(window_ms /
+ * latency, min_iterations, max_iterations) runs are timed with CUDA events and the
+ * NVML cumulative energy counter (nvmlDeviceGetTotalEnergyConsumption) is read around
+ * them: avg_power_w = energy delta / wall time, energy_mj = avg_power_w x latency_ms
+ * (PAPER:164-165).  Schedules the kernel cannot run (per-thread tile
+ * above 8x8 in (m, n), shared tiles beyond the device limit, too many registers for the
+ * block) get feasible = 0 and infinite latency/energy. */
+typedef struct etune_nvml_params {
+    double warmup_ms, window_ms;
+    int64_t min_iterations, max_iterations;
+} etune_nvml_params;
+typedef struct etune_measurement {   /* MeasurementRecord (measure.hpp:17-25) */
+    uint64_t candidate_id;
+    double latency_ms, avg_power_w, energy_mj;
+    int64_t iterations;
+    int32_t feasible, reserved;
+} etune_measurement;
+void etune_default_nvml_params(etune_nvml_params* out);  /* 50 ms, 200 ms, 10, 1e6 */
+/* *out = 1 when NVML energy counters are readable for the ctx's GPU */
+etune_status etune_cu_nvml_available(etune_cu_ctx* ctx, int* out);
+/* one run of a schedule's candidate kernel on caller buffers (mm: A[B][M][K], B[B][K][N],
+ * C[B][M][N]; conv: input NCHW, weights [Cout][Cin*ks*ks], output [B][Cout][OH*OW]);
+ * UNSUPPORTED when the schedule is infeasible for the kernel */
+etune_status etune_cu_candidate_run(etune_cu_ctx* ctx, const etune_cu_plan* plan, const etune_schedule* h_sched,
+                                    const float* d_a, const float* d_b, float* d_c);
+/* measure n host schedules (synchronous); ILLEGAL_SCHEDULE with *first_bad like the
+ * reference; BACKEND_UNAVAILABLE without NVML */
+etune_status etune_cu_nvml_measure(etune_cu_ctx* ctx, const etune_cu_plan* plan, const etune_schedule* h_sched,
+                                   int64_t n, const etune_nvml_params* params, etune_measurement* h_out,
+                                   int64_t* first_bad /*nullable*/);
+
 /* ------------------------------------------------------------- cost model */
 /* EnergyModel trees in the reference's flat TreeNode form (energy_model.hpp:45-57):
  * node arrays concatenated in tree order, tree_offsets[num_trees+1]. */

@@ -83,6 +83,17 @@ class RoundReport(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class NvmlParams(C.Structure):
+    _fields_ = [("warmup_ms", C.c_double), ("window_ms", C.c_double), ("min_iterations", C.c_int64),
+                ("max_iterations", C.c_int64)]
+
+
+class Measurement(C.Structure):
+    _fields_ = [("candidate_id", C.c_uint64), ("latency_ms", C.c_double), ("avg_power_w", C.c_double),
+                ("energy_mj", C.c_double), ("iterations", C.c_int64), ("feasible", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _PTR = C.c_void_p
@@ -122,6 +133,10 @@ _SIGS = {
                                               C.POINTER(_VP)]),
     "etune_cu_sample_random": (C.c_int, [_VP, _VP, _I64, C.c_uint64, _PTR, _PTR]),
     "etune_cu_sim_measure": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR, _PTR, _PTR, _PTR]),
+    "etune_default_nvml_params": (None, [C.POINTER(NvmlParams)]),
+    "etune_cu_nvml_available": (C.c_int, [_VP, C.POINTER(C.c_int)]),
+    "etune_cu_candidate_run": (C.c_int, [_VP, _VP, _PTR, _PTR, _PTR, _PTR]),
+    "etune_cu_nvml_measure": (C.c_int, [_VP, _VP, _PTR, _I64, C.POINTER(NvmlParams), _PTR, C.POINTER(_I64)]),
     "etune_cu_energy_loss": (C.c_int, [_VP, _PTR, _PTR, _I64, _PTR]),
     "etune_cu_snr_db": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(C.c_double), C.POINTER(_I64)]),
     "etune_cu_nccl_unique_id": (C.c_int, [_PTR]),
@@ -435,6 +450,32 @@ class Forest:
         st = lib().etune_cu_score_host(self.ctx.h, plan.h, self.h, _ptr(sched), n, _ptr(pred), _ptr(ids),
                                        C.byref(bad))
         _check(st, bad.value)
+
+
+def nvml_available(ctx: Context) -> bool:
+    v = C.c_int()
+    _check(lib().etune_cu_nvml_available(ctx.h, C.byref(v)))
+    return bool(v.value)
+
+
+def candidate_run(plan: "Plan", sched_row: np.ndarray, a, b, c):
+    """One run of a schedule's candidate kernel on caller device buffers (fp32)."""
+    s = np.ascontiguousarray(sched_row, np.int64).reshape(12)
+    _check(lib().etune_cu_candidate_run(plan.ctx.h, plan.h, s.ctypes.data, _ptr(a), _ptr(b), _ptr(c)))
+
+
+def nvml_measure(plan: "Plan", sched: np.ndarray, warmup_ms=50.0, window_ms=200.0, min_iterations=10,
+                 max_iterations=1000000):
+    """Measure host schedules with the NVML harness -> structured numpy records."""
+    s = np.ascontiguousarray(sched, np.int64).reshape(-1, 12)
+    n = len(s)
+    out = (Measurement * max(n, 1))()
+    p = NvmlParams(float(warmup_ms), float(window_ms), int(min_iterations), int(max_iterations))
+    bad = C.c_int64(-1)
+    st = lib().etune_cu_nvml_measure(plan.ctx.h, plan.h, s.ctypes.data, n, C.byref(p), C.cast(out, C.c_void_p),
+                                     C.byref(bad))
+    _check(st, bad.value)
+    return [{k: getattr(out[i], k) for k, _ in Measurement._fields_} for i in range(n)]
 
 
 def energy_loss(ctx: Context, pred, meas):

@@ -6,7 +6,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <limits>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -405,6 +407,182 @@ etune_status etune_cu_sim_measure(etune_cu_ctx* c, const etune_cu_plan* p, const
                 D.rng_seed};
     CU(launch_sim_measure(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d, d_lat, d_pow, d_en, d_iters));
     return ETUNE_OK;
+}
+
+void etune_default_nvml_params(etune_nvml_params* o) {
+    o->warmup_ms = 50.0;
+    o->window_ms = 200.0;
+    o->min_iterations = 10;
+    o->max_iterations = 1000000;
+}
+
+etune_status etune_cu_nvml_available(etune_cu_ctx* c, int* out) {
+    if (!c || !out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    std::string why;
+    *out = nvml_device_handle(c->device, &why) != nullptr ? 1 : 0;
+    return ETUNE_OK;
+}
+
+namespace {
+
+struct CandOperands {
+    float *a = nullptr, *b = nullptr, *c = nullptr;
+    ~CandOperands() {
+        cudaFree(a);
+        cudaFree(b);
+        cudaFree(c);
+    }
+};
+
+// operand element counts of the op (A, B, C)
+void operand_sizes(const etune_op_spec& op, const int64_t nest[4], int64_t* na, int64_t* nb, int64_t* nc) {
+    if (op.kind == 2) {
+        *na = op.batch * op.in_channels * op.height * op.width;
+        *nb = op.out_channels * nest[3];
+    } else {
+        *na = nest[0] * nest[1] * nest[3];
+        *nb = nest[0] * nest[3] * nest[2];
+    }
+    *nc = nest[0] * nest[1] * nest[2];
+}
+
+etune_status prepare_candidate(etune_cu_ctx* c, const etune_cu_plan* p, const etune_schedule& s,
+                               std::vector<uint8_t>* geom, size_t* smem, int* grid, int* block, bool* feasible) {
+    int64_t nest[4];
+    op_nest(p->build.op, nest);
+    geom->assign(candidate_geom_bytes(), 0);
+    const int cap = max_dynamic_smem(c->device);
+    *feasible = candidate_geometry(p->build.op, nest, s, cap, geom->data(), smem, grid, block);
+    if (*feasible) *feasible = candidate_fits(geom->data(), *block);
+    return ETUNE_OK;
+}
+
+}  // namespace
+
+etune_status etune_cu_candidate_run(etune_cu_ctx* c, const etune_cu_plan* p, const etune_schedule* h_sched,
+                                    const float* d_a, const float* d_b, float* d_c) {
+    if (!c || !p || !h_sched || !d_a || !d_b || !d_c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    std::vector<uint8_t> geom;
+    size_t smem = 0;
+    int grid = 0, block = 0;
+    bool ok = false;
+    if (etune_status st = prepare_candidate(c, p, *h_sched, &geom, &smem, &grid, &block, &ok)) return st;
+    if (!ok) return fail(ETUNE_ERR_UNSUPPORTED, "schedule infeasible for the candidate kernel");
+    CU(launch_candidate(c->stream, geom.data(), smem, grid, block, d_a, d_b, d_c));
+    note_launches(1);
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_nvml_measure(etune_cu_ctx* c, const etune_cu_plan* p, const etune_schedule* h_sched, int64_t n,
+                                   const etune_nvml_params* params, etune_measurement* h_out, int64_t* first_bad) {
+    if (!c || !p || (n > 0 && (!h_sched || !h_out)) || n < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (first_bad) *first_bad = -1;
+    if (n == 0) return ETUNE_OK;
+    std::string why;
+    void* nv = nvml_device_handle(c->device, &why);
+    if (!nv) return fail(ETUNE_ERR_BACKEND_UNAVAILABLE, "NVML energy counters unavailable: " + why);
+    etune_nvml_params P;
+    etune_default_nvml_params(&P);
+    if (params) P = *params;
+    // legality + ids on the device (validate_schedule, candidate_id)
+    etune_schedule* d_s = nullptr;
+    uint64_t *d_g = nullptr, *d_id = nullptr;
+    CU(cudaMalloc(&d_s, size_t(n) * sizeof(etune_schedule)));
+    CU(cudaMalloc(&d_g, size_t(n) * 8));
+    CU(cudaMalloc(&d_id, size_t(n) * 8));
+    CU(cudaMemcpyAsync(d_s, h_sched, size_t(n) * sizeof(etune_schedule), cudaMemcpyHostToDevice, c->stream));
+    CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_s, n, d_g));
+    CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_g, n, d_id));
+    std::vector<uint64_t> ids(static_cast<size_t>(n));
+    CU(cudaMemcpyAsync(ids.data(), d_id, size_t(n) * 8, cudaMemcpyDeviceToHost, c->stream));
+    const etune_status vst = etune_cu_synchronize(c, first_bad);
+    cudaFree(d_s);
+    cudaFree(d_g);
+    cudaFree(d_id);
+    if (vst != ETUNE_OK) return vst;
+    int64_t nest[4];
+    op_nest(p->build.op, nest);
+    int64_t na = 0, nb = 0, nc = 0;
+    operand_sizes(p->build.op, nest, &na, &nb, &nc);
+    CandOperands ops;
+    CU(cudaMalloc(&ops.a, size_t(na) * 4));
+    CU(cudaMalloc(&ops.b, size_t(nb) * 4));
+    CU(cudaMalloc(&ops.c, size_t(nc) * 4));
+    CU(launch_fill(c->stream, ops.a, na, 1u));
+    CU(launch_fill(c->stream, ops.b, nb, 2u));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    auto now_ms = [] {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    };
+    etune_status result = ETUNE_OK;
+    for (int64_t i = 0; i < n && result == ETUNE_OK; ++i) {
+        etune_measurement& r = h_out[i];
+        std::memset(&r, 0, sizeof(r));
+        r.candidate_id = ids[size_t(i)];
+        std::vector<uint8_t> geom;
+        size_t smem = 0;
+        int grid = 0, block = 0;
+        bool ok = false;
+        prepare_candidate(c, p, h_sched[i], &geom, &smem, &grid, &block, &ok);
+        if (!ok) {
+            r.feasible = 0;
+            r.latency_ms = r.energy_mj = std::numeric_limits<double>::infinity();
+            continue;
+        }
+        r.feasible = 1;
+        auto run = [&](int64_t reps) -> cudaError_t {
+            for (int64_t q = 0; q < reps; ++q) {
+                const cudaError_t e = launch_candidate(c->stream, geom.data(), smem, grid, block, ops.a, ops.b, ops.c);
+                if (e != cudaSuccess) return e;
+            }
+            return cudaSuccess;
+        };
+        // warm-up (pre-heat) and a latency estimate for the window
+        int64_t reps = 1;
+        double est = 0.0, spent = 0.0;
+        while (true) {
+            cudaEventRecord(e0, c->stream);
+            if (cudaError_t e = run(reps)) {
+                result = cuda_fail(e, "candidate kernel");
+                break;
+            }
+            cudaEventRecord(e1, c->stream);
+            cudaEventSynchronize(e1);
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            est = double(ms) / double(reps);
+            spent += ms;
+            if (spent >= P.warmup_ms) break;
+            reps = std::min<int64_t>(reps * 4, std::max<int64_t>(1, int64_t((P.warmup_ms - spent) / std::max(est, 1e-4))));
+        }
+        if (result != ETUNE_OK) break;
+        int64_t iters = int64_t(std::ceil(P.window_ms / std::max(est, 1e-6)));
+        iters = std::max<int64_t>(P.min_iterations, std::min<int64_t>(P.max_iterations, iters));
+        unsigned long long mj0 = 0, mj1 = 0;
+        const double w0 = now_ms();
+        nvml_energy_mj(nv, &mj0);
+        cudaEventRecord(e0, c->stream);
+        if (cudaError_t e = run(iters)) {
+            result = cuda_fail(e, "candidate kernel");
+            break;
+        }
+        cudaEventRecord(e1, c->stream);
+        cudaEventSynchronize(e1);
+        nvml_energy_mj(nv, &mj1);
+        const double wall = now_ms() - w0;
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        note_launches(int(std::min<int64_t>(iters, 1 << 30)));
+        r.iterations = iters;
+        r.latency_ms = double(ms) / double(iters);
+        r.avg_power_w = double(mj1 - mj0) / wall;           // mJ / ms = W
+        r.energy_mj = r.avg_power_w * r.latency_ms;          // SPEC:302 identity (W x ms = mJ)
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return result;
 }
 
 etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, const double* threshold,

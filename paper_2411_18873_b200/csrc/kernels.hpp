@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
 
 #include "etune_internal.hpp"
 
@@ -99,6 +100,18 @@ cudaError_t launch_sample_small(const LaunchCtx& c, const uint8_t* d_plan, const
 // dst[j] = src[idx[j]] for 8-byte elements (genomes, doubles); y = x / *divisor
 cudaError_t launch_gather_u64(const LaunchCtx& c, const void* d_src, const int64_t* d_idx, int64_t n, void* d_dst);
 cudaError_t launch_div_scalar(const LaunchCtx& c, const double* d_x, int64_t n, const double* d_divisor, double* d_y);
+
+// measurement harness (harness.cu): candidate GEMM/conv kernel per Schedule + NVML energy
+bool nvml_available(std::string* why);
+void* nvml_device_handle(int cuda_device, std::string* why);
+bool nvml_energy_mj(void* handle, unsigned long long* mj);
+size_t candidate_geom_bytes();
+bool candidate_geometry(const etune_op_spec& op, const int64_t nest[4], const etune_schedule& s, int smem_cap,
+                        void* out_geom, size_t* smem, int* grid, int* block);
+bool candidate_fits(const void* geom, int block);
+cudaError_t launch_candidate(cudaStream_t st, const void* geom, size_t smem, int grid, int block, const float* A,
+                             const float* B, float* C);
+cudaError_t launch_fill(cudaStream_t st, float* x, int64_t n, uint32_t seed);
 
 // process-wide count of kernel launches (incremented by every launcher)
 void note_launches(int k);
