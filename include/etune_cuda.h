@@ -217,6 +217,11 @@ etune_status etune_cu_nvml_available(etune_cu_ctx* ctx, int* out);
  * UNSUPPORTED when the schedule is infeasible for the kernel */
 etune_status etune_cu_candidate_run(etune_cu_ctx* ctx, const etune_cu_plan* plan, const etune_schedule* h_sched,
                                     const float* d_a, const float* d_b, float* d_c);
+/* measured latency only (the LatencyEvaAndPick step on hardware): one warm run, then
+ * `reps` timed runs per schedule; infinity for infeasible schedules */
+etune_status etune_cu_candidate_latency(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                        const etune_schedule* h_sched, int64_t n, int32_t reps,
+                                        double* h_latency_ms);
 /* measure n host schedules (synchronous); ILLEGAL_SCHEDULE with *first_bad like the
  * reference; BACKEND_UNAVAILABLE without NVML */
 etune_status etune_cu_nvml_measure(etune_cu_ctx* ctx, const etune_cu_plan* plan, const etune_schedule* h_sched,
@@ -355,6 +360,10 @@ typedef struct etune_search_config {
     uint64_t rng_seed;
     etune_genetic_rates rates;
     etune_boost_params boost;
+    int32_t backend;           /* 0: SimBackend (device formula), 1: the GPU itself (candidate kernels:
+                                  CUDA-event latency filter, NVML energy of the selected) */
+    int32_t latency_reps;      /* backend 1: timed runs per candidate in the latency filter */
+    etune_nvml_params nvml;    /* backend 1: energy measurement protocol */
 } etune_search_config;
 
 typedef struct etune_round_report {   /* RoundReport */
@@ -370,7 +379,8 @@ typedef struct etune_round_report {   /* RoundReport */
 
 typedef struct etune_cu_search etune_cu_search;
 void etune_default_search_config(etune_search_config* out);
-/* Backend: the plan's SimBackend (etune_cu_sim_measure). */
+/* Backend 0: the plan's SimBackend (etune_cu_sim_measure); backend 1: measurements on
+ * this GPU (etune_cu_candidate_latency + etune_cu_nvml_measure). */
 etune_status etune_cu_search_create(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                     const etune_search_config* cfg, etune_cu_search** out);
 etune_status etune_cu_search_destroy(etune_cu_search* s);

@@ -66,11 +66,23 @@ class BoostParams(C.Structure):
                 ("min_leaf_weight", C.c_double), ("reg_lambda", C.c_double)]
 
 
+class NvmlParams(C.Structure):
+    _fields_ = [("warmup_ms", C.c_double), ("window_ms", C.c_double), ("min_iterations", C.c_int64),
+                ("max_iterations", C.c_int64)]
+
+
+class Measurement(C.Structure):
+    _fields_ = [("candidate_id", C.c_uint64), ("latency_ms", C.c_double), ("avg_power_w", C.c_double),
+                ("energy_mj", C.c_double), ("iterations", C.c_int64), ("feasible", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
 class SearchConfig(C.Structure):
     _fields_ = [("M", C.c_int64), ("generation_size", C.c_int64), ("k_init_fifths", C.c_int32),
                 ("max_rounds", C.c_int32), ("patience", C.c_int32), ("inverted_semantics", C.c_int32),
                 ("mu_db", C.c_double), ("improve_rel", C.c_double), ("rng_seed", C.c_uint64),
-                ("rates", GeneticRates), ("boost", BoostParams)]
+                ("rates", GeneticRates), ("boost", BoostParams), ("backend", C.c_int32),
+                ("latency_reps", C.c_int32), ("nvml", NvmlParams)]
 
 
 class RoundReport(C.Structure):
@@ -81,17 +93,6 @@ class RoundReport(C.Structure):
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
-
-
-class NvmlParams(C.Structure):
-    _fields_ = [("warmup_ms", C.c_double), ("window_ms", C.c_double), ("min_iterations", C.c_int64),
-                ("max_iterations", C.c_int64)]
-
-
-class Measurement(C.Structure):
-    _fields_ = [("candidate_id", C.c_uint64), ("latency_ms", C.c_double), ("avg_power_w", C.c_double),
-                ("energy_mj", C.c_double), ("iterations", C.c_int64), ("feasible", C.c_int32),
-                ("reserved", C.c_int32)]
 
 
 _VP = C.c_void_p
@@ -525,7 +526,9 @@ def search_config(**kw) -> SearchConfig:
     cfg = SearchConfig()
     lib().etune_default_search_config(C.byref(cfg))
     for k, v in kw.items():
-        if hasattr(cfg.rates, k):
+        if k in ("warmup_ms", "window_ms", "min_iterations", "max_iterations"):
+            setattr(cfg.nvml, k, type(getattr(cfg.nvml, k))(v))
+        elif hasattr(cfg.rates, k):
             setattr(cfg.rates, k, float(v))
         elif hasattr(cfg.boost, k):
             setattr(cfg.boost, k, type(getattr(cfg.boost, k))(v))

@@ -242,9 +242,21 @@ etune_status etune_cu_synchronize(etune_cu_ctx* c, int64_t* first_bad) {
     const int64_t idx = int64_t(v >> 8);
     const etune_status st = etune_status(v & 0xffu);
     if (first_bad) *first_bad = idx;
-    return fail(st, st == ETUNE_ERR_ILLEGAL_SCHEDULE
-                        ? "schedule " + std::to_string(idx) + " does not fit the operator (validate_schedule)"
-                        : "schedule " + std::to_string(idx) + " cannot be represented by this build");
+    std::string what;
+    switch (st) {
+    case ETUNE_ERR_ILLEGAL_SCHEDULE:
+        what = "schedule " + std::to_string(idx) + " does not fit the operator (validate_schedule)";
+        break;
+    case ETUNE_ERR_NON_POSITIVE_ENERGY:
+        what = "measured energy at element " + std::to_string(idx) + " is not positive";
+        break;
+    case ETUNE_ERR_UNSUPPORTED:
+        what = "element " + std::to_string(idx) + " cannot be represented by this build";
+        break;
+    default:
+        what = "device-side error " + std::to_string(int(st)) + " at element " + std::to_string(idx);
+    }
+    return fail(st, what);
 }
 
 etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, const etune_device_config* dev,
@@ -473,6 +485,55 @@ etune_status etune_cu_candidate_run(etune_cu_ctx* c, const etune_cu_plan* p, con
     return ETUNE_OK;
 }
 
+etune_status etune_cu_candidate_latency(etune_cu_ctx* c, const etune_cu_plan* p, const etune_schedule* h_sched,
+                                        int64_t n, int32_t reps, double* h_ms) {
+    if (!c || !p || n < 0 || (n > 0 && (!h_sched || !h_ms)) || reps < 1)
+        return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (n == 0) return ETUNE_OK;
+    int64_t nest[4];
+    op_nest(p->build.op, nest);
+    int64_t na = 0, nb = 0, nc = 0;
+    operand_sizes(p->build.op, nest, &na, &nb, &nc);
+    CandOperands ops;
+    CU(cudaMalloc(&ops.a, size_t(na) * 4));
+    CU(cudaMalloc(&ops.b, size_t(nb) * 4));
+    CU(cudaMalloc(&ops.c, size_t(nc) * 4));
+    CU(launch_fill(c->stream, ops.a, na, 1u));
+    CU(launch_fill(c->stream, ops.b, nb, 2u));
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    etune_status result = ETUNE_OK;
+    for (int64_t i = 0; i < n; ++i) {
+        std::vector<uint8_t> geom;
+        size_t smem = 0;
+        int grid = 0, block = 0;
+        bool ok = false;
+        prepare_candidate(c, p, h_sched[i], &geom, &smem, &grid, &block, &ok);
+        if (!ok) {
+            h_ms[i] = std::numeric_limits<double>::infinity();
+            continue;
+        }
+        cudaError_t e = launch_candidate(c->stream, geom.data(), smem, grid, block, ops.a, ops.b, ops.c);  // warm
+        cudaEventRecord(e0, c->stream);
+        for (int r = 0; r < reps && e == cudaSuccess; ++r)
+            e = launch_candidate(c->stream, geom.data(), smem, grid, block, ops.a, ops.b, ops.c);
+        cudaEventRecord(e1, c->stream);
+        if (e != cudaSuccess) {
+            result = cuda_fail(e, "candidate kernel");
+            break;
+        }
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        h_ms[i] = double(ms) / reps;
+        note_launches(reps + 1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return result;
+}
+
 etune_status etune_cu_nvml_measure(etune_cu_ctx* c, const etune_cu_plan* p, const etune_schedule* h_sched, int64_t n,
                                    const etune_nvml_params* params, etune_measurement* h_out, int64_t* first_bad) {
     if (!c || !p || (n > 0 && (!h_sched || !h_out)) || n < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
@@ -569,6 +630,20 @@ etune_status etune_cu_nvml_measure(etune_cu_ctx* c, const etune_cu_plan* p, cons
             break;
         }
         cudaEventRecord(e1, c->stream);
+        // while the repeats run: NVML power samples every ~2 ms (the paper's sampler,
+        // PAPER:184-185), used when the energy counter has not ticked over the window
+        double psum = 0.0;
+        int64_t pn = 0;
+        while (cudaEventQuery(e1) == cudaErrorNotReady) {
+            unsigned int mw = 0;
+            if (nvml_power_mw(nv, &mw)) {
+                psum += double(mw);
+                ++pn;
+            }
+            const double t = now_ms();
+            while (now_ms() - t < 2.0) {
+            }
+        }
         cudaEventSynchronize(e1);
         nvml_energy_mj(nv, &mj1);
         const double wall = now_ms() - w0;
@@ -577,8 +652,18 @@ etune_status etune_cu_nvml_measure(etune_cu_ctx* c, const etune_cu_plan* p, cons
         note_launches(int(std::min<int64_t>(iters, 1 << 30)));
         r.iterations = iters;
         r.latency_ms = double(ms) / double(iters);
-        r.avg_power_w = double(mj1 - mj0) / wall;           // mJ / ms = W
-        r.energy_mj = r.avg_power_w * r.latency_ms;          // SPEC:302 identity (W x ms = mJ)
+        if (mj1 > mj0) {
+            r.avg_power_w = double(mj1 - mj0) / wall;  // mJ / ms = W
+        } else {
+            if (pn == 0) {
+                unsigned int mw = 0;
+                nvml_power_mw(nv, &mw);
+                psum = double(mw);
+                pn = 1;
+            }
+            r.avg_power_w = psum / double(pn) / 1000.0;
+        }
+        r.energy_mj = r.avg_power_w * r.latency_ms;  // SPEC:302 identity (W x ms = mJ)
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);

@@ -242,6 +242,7 @@ void* nvml_device_handle(int cuda_device, std::string* why) {
 }
 
 bool nvml_energy_mj(void* h, unsigned long long* mj) { return nvml().energy(h, mj) == 0; }
+bool nvml_power_mw(void* h, unsigned int* mw) { return nvml().power(h, mw) == 0; }
 
 // Feasibility + launch geometry of one schedule; returns false (infeasible) when the
 // per-thread tile or the shared tiles exceed this build's kernel limits.

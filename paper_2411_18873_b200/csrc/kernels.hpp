@@ -105,6 +105,7 @@ cudaError_t launch_div_scalar(const LaunchCtx& c, const double* d_x, int64_t n, 
 bool nvml_available(std::string* why);
 void* nvml_device_handle(int cuda_device, std::string* why);
 bool nvml_energy_mj(void* handle, unsigned long long* mj);
+bool nvml_power_mw(void* handle, unsigned int* mw);
 size_t candidate_geom_bytes();
 bool candidate_geometry(const etune_op_spec& op, const int64_t nest[4], const etune_schedule& s, int smem_cap,
                         void* out_geom, size_t* smem, int* grid, int* block);

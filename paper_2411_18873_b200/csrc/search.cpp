@@ -167,6 +167,58 @@ void fill_report(const etune_cu_search* s, int kb, double snr, int64_t measured,
     r->wall_ms = ms;
 }
 
+// host copies of device genomes as the reference's Schedule records
+etune_status host_schedules(etune_cu_search* s, const uint64_t* gen, int64_t n, std::vector<etune_schedule>* out) {
+    etune_cu_ctx* c = s->ctx;
+    etune_schedule* d = nullptr;
+    SCU(cudaMalloc(&d, size_t(std::max<int64_t>(n, 1)) * sizeof(etune_schedule)));
+    etune_status st = etune_cu_decode(c, s->plan, gen, n, d);
+    out->resize(static_cast<size_t>(n));
+    if (st == ETUNE_OK && n > 0) {
+        const cudaError_t e =
+            cudaMemcpyAsync(out->data(), d, size_t(n) * sizeof(etune_schedule), cudaMemcpyDeviceToHost, c->stream);
+        if (e != cudaSuccess) st = sfail(ETUNE_ERR_CUDA, cudaGetErrorString(e));
+    }
+    if (st == ETUNE_OK) st = etune_cu_synchronize(c, nullptr);
+    cudaFree(d);
+    return st;
+}
+
+// LatencyEvaAndPick's measurement: the backend's latency of n device genomes into d_lat
+etune_status measure_latency(etune_cu_search* s, const uint64_t* gen, int64_t n, double* d_lat) {
+    if (s->cfg.backend == 0) return etune_cu_sim_measure(s->ctx, s->plan, gen, n, d_lat, nullptr, nullptr, nullptr);
+    std::vector<etune_schedule> h;
+    SOK(host_schedules(s, gen, n, &h));
+    std::vector<double> lat(static_cast<size_t>(n));
+    SOK(etune_cu_candidate_latency(s->ctx, s->plan, h.data(), n, s->cfg.latency_reps, lat.data()));
+    SCU(cudaMemcpyAsync(d_lat, lat.data(), size_t(n) * 8, cudaMemcpyHostToDevice, s->ctx->stream));
+    return etune_cu_synchronize(s->ctx, nullptr);
+}
+
+// NVMLMeasurement: latency, power and energy of n device genomes into mlat/mpow/men.
+// A selected schedule the candidate kernel cannot run gets a finite penalty energy
+// (1e30 mJ) so that training stays finite; it is never the best.
+etune_status measure_energy(etune_cu_search* s, const uint64_t* gen, int64_t n) {
+    if (s->cfg.backend == 0)
+        return etune_cu_sim_measure(s->ctx, s->plan, gen, n, s->mlat, s->mpow, s->men, nullptr);
+    std::vector<etune_schedule> h;
+    SOK(host_schedules(s, gen, n, &h));
+    std::vector<etune_measurement> rec(static_cast<size_t>(n));
+    SOK(etune_cu_nvml_measure(s->ctx, s->plan, h.data(), n, &s->cfg.nvml, rec.data(), nullptr));
+    std::vector<double> lat(static_cast<size_t>(n)), pw(static_cast<size_t>(n)), en(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        const etune_measurement& r = rec[size_t(i)];
+        lat[size_t(i)] = r.feasible ? r.latency_ms : 1e30;
+        pw[size_t(i)] = r.feasible ? r.avg_power_w : 0.0;
+        en[size_t(i)] = r.feasible ? r.energy_mj : 1e30;
+    }
+    cudaStream_t st = s->ctx->stream;
+    SCU(cudaMemcpyAsync(s->mlat, lat.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    SCU(cudaMemcpyAsync(s->mpow, pw.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    SCU(cudaMemcpyAsync(s->men, en.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    return etune_cu_synchronize(s->ctx, nullptr);
+}
+
 double now_ms() {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -188,6 +240,9 @@ void etune_default_search_config(etune_search_config* o) {
     o->rng_seed = 42;
     etune_default_genetic_rates(&o->rates);
     etune_default_boost_params(&o->boost);
+    o->backend = 0;
+    o->latency_reps = 3;
+    etune_default_nvml_params(&o->nvml);
 }
 
 etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, const etune_search_config* cfg,
@@ -200,6 +255,12 @@ etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, con
         return sfail(ETUNE_ERR_VALIDATION, "SearchConfig needs 0 < M <= generation_size");
     if (C.k_init_fifths < 0 || C.k_init_fifths > 5) return sfail(ETUNE_ERR_VALIDATION, "k must lie in [0, 1]");
     if (!std::isfinite(C.mu_db)) return sfail(ETUNE_ERR_VALIDATION, "mu_db must be finite");
+    if (C.backend != 0 && C.backend != 1) return sfail(ETUNE_ERR_VALIDATION, "backend must be 0 (sim) or 1 (gpu)");
+    if (C.backend == 1) {
+        std::string why;
+        if (!nvml_device_handle(c->device, &why))
+            return sfail(ETUNE_ERR_BACKEND_UNAVAILABLE, "NVML energy counters unavailable: " + why);
+    }
     if (C.boost.max_depth < 0 || C.boost.max_depth > train_max_depth() || C.boost.num_trees < 0)
         return sfail(ETUNE_ERR_UNSUPPORTED, "boost parameters outside this build's range");
     auto s = std::make_unique<etune_cu_search>();
@@ -255,10 +316,10 @@ etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* rep
     const double t0 = now_ms();
     const int64_t G = s->cfg.generation_size, M = s->cfg.M;
     SOK(etune_cu_sample_random(c, s->plan, G, s->cfg.rng_seed, s->pop, nullptr));
-    SOK(etune_cu_sim_measure(c, s->plan, s->pop, G, s->lat, nullptr, nullptr, nullptr));
+    SOK(measure_latency(s, s->pop, G, s->lat));
     SOK(etune_cu_topk(c, s->lat, G, M, s->idx));  // LatencyEvaAndPick(Kernel_generation, M)
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
-    SOK(etune_cu_sim_measure(c, s->plan, s->mgen, M, s->mlat, s->mpow, s->men, nullptr));
+    SOK(measure_energy(s, s->mgen, M));
     SOK(append_samples(s, s->mgen, s->men, M));
     SOK(retrain(s));
     SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(M) * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -283,7 +344,7 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     SOK(etune_cu_reproduce(c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
                            nullptr, nullptr));
     // 2. LatencyEvaAndPick(Kernel_generation, M)
-    SOK(etune_cu_sim_measure(c, s->plan, s->pop, G, s->lat, nullptr, nullptr, nullptr));
+    SOK(measure_latency(s, s->pop, G, s->lat));
     SOK(etune_cu_topk(c, s->lat, G, M, s->idx));
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
     // 3. EnergyModelEvaAndPick(Kernel_M, EnergyModel, k*M)
@@ -292,8 +353,8 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     SOK(etune_cu_topk(c, s->mpred, M, km, s->sel));
     SCU(launch_gather_u64(c->lc(), s->mgen, s->sel, km, s->selgen));
     SCU(launch_gather_u64(c->lc(), s->mpred, s->sel, km, s->psel));
-    // 4. NVMLMeasurement(Kernel_kM)  (SimBackend)
-    SOK(etune_cu_sim_measure(c, s->plan, s->selgen, km, s->mlat, s->mpow, s->men, nullptr));
+    // 4. NVMLMeasurement(Kernel_kM)
+    SOK(measure_energy(s, s->selgen, km));
     // 6. SNR of step-3 predictions vs the measurements in the model's normalised units
     SCU(launch_div_scalar(c->lc(), s->men, km, s->m_sc + 1, s->mnorm));
     double snr = 0.0;

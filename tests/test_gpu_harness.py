@@ -77,3 +77,23 @@ def test_nvml_measure_records(oracle, ctx, capi):
     with pytest.raises(capi.EtuneError) as e:
         capi.nvml_measure(capi.Plan(ctx, op), bad)
     assert e.value.code == 4 and e.value.index == 2
+
+
+def test_search_on_the_gpu_backend(oracle, ctx, capi):
+    """Algorithm 1 with measurements on this B200 (BASELINE configs[2] shape: BERT FFN
+    GEMM, the cost model updated every round from NVML-measured candidate kernels)."""
+    if not capi.nvml_available(ctx):
+        pytest.skip("NVML energy counters not readable here")
+    op = parse_op("mm:1,512,3072,768")
+    plan = capi.Plan(ctx, op)
+    cfg = capi.search_config(M=32, generation_size=128, rng_seed=5, max_rounds=2, backend=1, latency_reps=2,
+                             warmup_ms=10, window_ms=40, min_iterations=3, num_trees=30)
+    s = capi.Search(plan, cfg)
+    reps = s.run()
+    assert len(reps) == 3
+    assert reps[0].measured == 32 and reps[0].cumulative_measured == 32
+    best = [r.best_energy_mj for r in reps]
+    assert all(b2 <= b1 for b1, b2 in zip(best, best[1:]))
+    assert 0 < best[-1] < 1e30 and reps[-1].best_power_w > 20
+    sched, bid, lat, en = s.best()
+    assert oracle.ids(op, sched[None, :])[0] == bid and lat > 0
