@@ -1,4 +1,4 @@
-"""Benchmark: candidate schedules scored per second (BASELINE.json metric).
+"""Benchmark: candidate schedules scored per second and search-round latency (BASELINE.json metric).
 
 Step = one pass of the hot path over one batch: fused score (features -> 100-tree
 energy model -> prediction + candidate id) of the rank's population shard, then
@@ -16,6 +16,11 @@ GeneticRates{}, seed 7); model = the reference-trained 100-tree forest on
 sample_random(op,2048,1234) (tests/golden fixture).  L2: 16 distinct population
 buffers (384 MB incl. outputs) are cycled so no step reads another's data from the
 126 MB L2.
+
+Also reported: e2e (the same scoring through the reference-facing C-ABI call on HOST
+Schedule[] buffers, H2D/D2H inside the timed region), search_round_latency (Algorithm 1
+rounds of BASELINE configs[1]: generation 16384, M 4096, on the device), roofline of the
+score kernel and the reference CPU path (cpu_baseline).
 """
 from __future__ import annotations
 
