@@ -134,7 +134,10 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     CU(score_occupancy(cs.mask_bits, cs.bytes, &cs.per_sm));
     cs.params = std::make_shared<ForestParams>();
     std::memset(cs.params.get(), 0, sizeof(ForestParams));
-    std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
+    if (hdr->npairs > 0)
+        std::memcpy(cs.params->pair, blob.data() + hdr->off_trees, sizeof(PairRec) * size_t(hdr->npairs));
+    else
+        std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;

@@ -129,8 +129,18 @@ struct TreeRec {          // 32 bytes, read warp-uniformly (kernel-parameter con
     uint32_t meta;        // byte offset of the tree's leaf values (bits 0-23) | used-channel mask << 24
 };
 constexpr int kMaxParamTrees = 1000;  // 32000 B of kernel parameters (CUDA 12.1+: 32764 max)
-struct ForestParams {
+// Pair mode (32-bit leaf masks): trees 2p and 2p+1 share one record and one 64-bit
+// class->(mask_a | mask_b << 32) table per channel, so one 8-byte shared load serves
+// both trees (one wavefront when the channel has <= 16 classes).
+struct PairRec {          // 36 bytes
+    uint32_t lut[7];      // byte offset of the pair's class->mask-pair table per channel
+    uint32_t meta_a;      // leaf block of tree 2p (bits 0-23) | union of used channels << 24
+    uint32_t meta_b;      // leaf block of tree 2p+1 (bits 0-23) | 1 << 31 when tree 2p+1 exists
+};
+static_assert(sizeof(PairRec) == 36, "PairRec layout");
+union ForestParams {
     TreeRec rec[kMaxParamTrees];
+    PairRec pair[kMaxParamTrees / 2];
 };
 
 struct ScoreHdr {
@@ -138,7 +148,7 @@ struct ScoreHdr {
     uint64_t fnv_prefix;
     double base, lr;
     int32_t ntrees, mask_bits;   // 32 or 64
-    int32_t nt[3], nd[3], ndk, ngrid, n13, pad;
+    int32_t nt[3], nd[3], ndk, ngrid, n13, npairs;  // npairs > 0: pair mode (PairRec records)
     uint32_t off_til[3];     // TilingRec
     uint32_t off_divk;       // int64 k values (ids)
     uint32_t off_gridkey;    // uint16 [nd0][nd1][nd2]
@@ -146,8 +156,8 @@ struct ScoreHdr {
     uint32_t off_blockb;     // double per block 0..1024: min(1, block/256)
     uint32_t off_f13;        // double[n13] effective f13 boundaries
     uint32_t off_cls[7];     // uint8 class tables per channel key (kChEff: none)
-    uint32_t off_trees;      // TreeRec[ntrees]
-    uint32_t off_lut;        // mask words (uint32 or uint64)
+    uint32_t off_trees;      // TreeRec[ntrees] or PairRec[npairs]
+    uint32_t off_lut;        // mask words (uint32 or uint64; pair mode: uint64 mask pairs)
     uint32_t off_leaves;     // double
     uint32_t total;
 };

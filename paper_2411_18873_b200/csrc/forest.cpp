@@ -236,6 +236,8 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
     std::map<std::vector<uint64_t>, uint32_t> dedupe;
     std::vector<TreeRec> recs(static_cast<size_t>(T));
     std::vector<double> leaves;
+    std::vector<std::vector<std::vector<uint64_t>>> tree_tl(static_cast<size_t>(T));  // pair mode input
+    std::vector<uint32_t> tree_used(static_cast<size_t>(T), 0u);
     for (int64_t t = 0; t < T; ++t) {
         const int64_t b = F.offsets[t], e = F.offsets[t + 1];
         // in-order leaf numbering and left-subtree leaf masks (iterative DFS)
@@ -333,6 +335,8 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
         }
         uint32_t used_mask = 0;
         for (int c = 0; c < kNumChannels; ++c) used_mask |= uint32_t(used[c]) << c;
+        tree_used[size_t(t)] = used_mask;
+        tree_tl[size_t(t)] = tl;
         if (leaves.size() >= (1u << 24)) {
             *err = "forest has more than 2^24 leaves";
             return ETUNE_ERR_UNSUPPORTED;
@@ -358,6 +362,51 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
         S.max_leaves = std::max(S.max_leaves, int(lv.size()));
     }
 
+    // ---- pair mode (32-bit masks): trees 2p, 2p+1 share one record and 64-bit tables
+    const bool paired = mbits == 32;
+    std::vector<PairRec> precs;
+    std::vector<uint64_t> plut;
+    if (paired) {
+        plut.assign(256, ~0ull);  // shared all-ones pair table
+        std::map<std::vector<uint64_t>, uint32_t> pdedupe;
+        const int64_t np = (T + 1) / 2;
+        precs.resize(static_cast<size_t>(np));
+        for (int64_t p = 0; p < np; ++p) {
+            const size_t a = size_t(2 * p), b = size_t(2 * p + 1);
+            const bool hasb = int64_t(b) < T;
+            const uint32_t ua = tree_used[a], ub = hasb ? tree_used[b] : 0u;
+            const uint32_t used = ua | ub;
+            PairRec& PR = precs[size_t(p)];
+            for (int c = 0; c < kNumChannels; ++c) {
+                if (!((used >> c) & 1u)) {
+                    PR.lut[c] = 0;
+                    continue;
+                }
+                std::vector<uint64_t> tab(rep[c].size());
+                for (size_t x = 0; x < tab.size(); ++x) {
+                    const uint64_t ma = ((ua >> c) & 1u) ? tree_tl[a][size_t(c)][x] : 0xffffffffull;
+                    const uint64_t mb = ((ub >> c) & 1u) ? tree_tl[b][size_t(c)][x] : 0xffffffffull;
+                    tab[x] = (ma & 0xffffffffull) | (mb << 32);
+                }
+                auto it = pdedupe.find(tab);
+                if (it != pdedupe.end()) {
+                    PR.lut[c] = it->second;
+                } else {
+                    // a table that fits one 128-byte bank row is placed inside one, so a
+                    // warp's loads of it are a single conflict-free wavefront
+                    if (tab.size() <= 16 && (plut.size() % 16) + tab.size() > 16)
+                        plut.resize((plut.size() + 15) / 16 * 16, ~0ull);
+                    const uint32_t off = uint32_t(plut.size());
+                    plut.insert(plut.end(), tab.begin(), tab.end());
+                    pdedupe.emplace(tab, off);
+                    PR.lut[c] = off;
+                }
+            }
+            PR.meta_a = (recs[a].meta & 0xffffffu) | (used << 24);
+            PR.meta_b = hasb ? ((recs[b].meta & 0xffffffu) | (1u << 31)) : 0u;
+        }
+    }
+
     // ---- blob
     ScoreHdr H{};
     H.K = PH.K;
@@ -373,6 +422,7 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
     H.ndk = PH.ndk;
     H.ngrid = PH.ngrid;
     H.n13 = int32_t(f13b.size());
+    H.npairs = 0;
     std::vector<double> grida(P.grid.size()), blockb(1025);
     for (size_t g = 0; g < P.grid.size(); ++g) grida[g] = P.grid[g].a;
     for (int b2 = 0; b2 <= 1024; ++b2) blockb[size_t(b2)] = P.block[size_t(b2)].b;
@@ -386,26 +436,49 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
     H.off_f13 = put(*blob, f13b.data(), f13b.size());
     for (int c = 0; c < kNumChannels; ++c) H.off_cls[c] = put(*blob, cls[c].data(), cls[c].size());
     // tree records hold byte offsets from the blob start: reserve, then fill
-    H.off_trees = put(*blob, recs.data(), recs.size());
-    if (mbits == 32) {
-        std::vector<uint32_t> l32(lut.begin(), lut.end());
-        H.off_lut = put(*blob, l32.data(), l32.size());
+    if (paired) {
+        H.npairs = int32_t(precs.size());
+        H.off_trees = put(*blob, precs.data(), precs.size());
+        blob->resize((blob->size() + 127) & ~size_t(127));  // bank-row aligned (see the table placement)
+        H.off_lut = put(*blob, plut.data(), plut.size());
     } else {
-        H.off_lut = put(*blob, lut.data(), lut.size());
+        H.off_trees = put(*blob, recs.data(), recs.size());
     }
+    if (!paired) H.off_lut = put(*blob, lut.data(), lut.size());  // 64-bit masks
     H.off_leaves = put(*blob, leaves.data(), leaves.size());
     const uint32_t mbytes = uint32_t(mbits / 8);
-    for (TreeRec& R : recs) {
-        const uint32_t used_mask = R.meta >> 24;
-        for (int c = 0; c < kNumChannels; ++c) R.lut[c] = H.off_lut + R.lut[c] * mbytes;
-        const uint32_t lb = H.off_leaves + (R.meta & 0xffffffu) * 8u;
-        if (lb >= (1u << 24)) {
-            *err = "compiled forest too large";
-            return ETUNE_ERR_UNSUPPORTED;
+    auto leaf_bytes = [&](uint32_t idx, uint32_t* out) {
+        const uint32_t lb = H.off_leaves + idx * 8u;
+        if (lb >= (1u << 24)) return false;
+        *out = lb;
+        return true;
+    };
+    if (paired) {
+        for (PairRec& PR : precs) {
+            const uint32_t used = PR.meta_a >> 24;
+            for (int c = 0; c < kNumChannels; ++c) PR.lut[c] = H.off_lut + PR.lut[c] * 8u;
+            uint32_t la = 0, lb = 0;
+            if (!leaf_bytes(PR.meta_a & 0xffffffu, &la) || !leaf_bytes(PR.meta_b & 0xffffffu, &lb)) {
+                *err = "compiled forest too large";
+                return ETUNE_ERR_UNSUPPORTED;
+            }
+            PR.meta_a = la | (used << 24);
+            PR.meta_b = (PR.meta_b >> 31) ? (lb | (1u << 31)) : 0u;
         }
-        R.meta = lb | (used_mask << 24);
+        std::memcpy(blob->data() + H.off_trees, precs.data(), precs.size() * sizeof(PairRec));
+    } else {
+        for (TreeRec& R : recs) {
+            const uint32_t used_mask = R.meta >> 24;
+            for (int c = 0; c < kNumChannels; ++c) R.lut[c] = H.off_lut + R.lut[c] * mbytes;
+            uint32_t lb = 0;
+            if (!leaf_bytes(R.meta & 0xffffffu, &lb)) {
+                *err = "compiled forest too large";
+                return ETUNE_ERR_UNSUPPORTED;
+            }
+            R.meta = lb | (used_mask << 24);
+        }
+        std::memcpy(blob->data() + H.off_trees, recs.data(), recs.size() * sizeof(TreeRec));
     }
-    std::memcpy(blob->data() + H.off_trees, recs.data(), recs.size() * sizeof(TreeRec));
     blob->resize(align16(blob->size()));
     H.total = uint32_t(blob->size());
     std::memcpy(blob->data(), &H, sizeof(H));

@@ -437,7 +437,8 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
     const uint64_t prefix = H.fnv_prefix;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const CandClasses cc = candidate_classes(S, H, __ldg(genome + i));
-        const double sum = forest_sum<M>(S, H, fp.rec, cc.c);
+        const double sum = (sizeof(M) == 4 && H.npairs > 0) ? forest_sum_pairs(S, H, fp.pair, cc.c)
+                                                            : forest_sum<M>(S, H, fp.rec, cc.c);
         pred[i] = finish_prediction(H, sum);
         if (ids) {
             Knobs c;

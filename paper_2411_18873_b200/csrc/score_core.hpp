@@ -178,6 +178,38 @@ __host__ __device__ __forceinline__ double forest_sum(const uint8_t* S, const Sc
     return sum;
 }
 
+// Pair mode (32-bit masks): one 8-byte table load per used channel serves trees 2p and
+// 2p+1; `cb8[ch]` = blob base + class * 8.  Sums stay in tree order.
+__host__ __device__ __forceinline__ double leaf_value32(SAddr base, uint32_t off, uint32_t m) {
+    const uint32_t slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
+    const SAddr blk = base + off + slot * 4u;
+    return join_f64(lds32(blk), lds32(blk + 128u));
+}
+
+__host__ __device__ __forceinline__ double forest_sum_pairs(const uint8_t* S, const ScoreHdr& H, const PairRec* pairs,
+                                                            const uint32_t* c) {
+    const SAddr base = blob_saddr(S);
+    SAddr cb[kNumChannels];
+#pragma unroll
+    for (int ch = 0; ch < kNumChannels; ++ch) cb[ch] = base + c[ch] * 8u;
+    double sum = 0.0;
+    const int np = H.npairs;
+    for (int p = 0; p < np; ++p) {
+        const PairRec r = pairs[p];
+        uint64_t m = ~0ull;
+#pragma unroll
+        for (int ch = 0; ch < kNumChannels; ++ch)
+            if ((r.meta_a >> (24 + ch)) & 1u) m &= lds64(cb[ch] + r.lut[ch]);
+        const double va = leaf_value32(base, r.meta_a & 0xffffffu, uint32_t(m));
+        sum = ETUNE_DADD(sum, va);
+        if (r.meta_b >> 31) {
+            const double vb = leaf_value32(base, r.meta_b & 0xffffffu, uint32_t(m >> 32));
+            sum = ETUNE_DADD(sum, vb);
+        }
+    }
+    return sum;
+}
+
 __host__ __device__ __forceinline__ double finish_prediction(const ScoreHdr& H, double sum) {
     const double p = ETUNE_DADD(H.base, ETUNE_DMUL(H.lr, sum));  // energy_model.cpp:248
     return (1e-6 < p) ? p : 1e-6;                                // std::max(kPredictionFloor, p)

@@ -67,7 +67,9 @@ extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* fe
         const uint32_t v = uint32_t(__builtin_ctzll(uint64_t(s[11])));
         const CandClasses cc = candidate_classes(B, H, genome_pack(ti[0], ti[1], ti[2], k, u, v));
         const TreeRec* trees = blob_at<TreeRec>(B, H.off_trees);
-        const double sum = H.mask_bits == 32 ? forest_sum<uint32_t>(B, H, trees, cc.c) : forest_sum<uint64_t>(B, H, trees, cc.c);
+        const double sum = H.npairs > 0 ? forest_sum_pairs(B, H, blob_at<PairRec>(B, H.off_trees), cc.c)
+                           : H.mask_bits == 32 ? forest_sum<uint32_t>(B, H, trees, cc.c)
+                                               : forest_sum<uint64_t>(B, H, trees, cc.c);
         out[i] = finish_prediction(H, sum);
     }
     if (stats_out) {
