@@ -177,23 +177,26 @@ __device__ Child breed_one(const BreedConst& K, const PlanHdr& H, int64_t i, con
             if (th[1] > th[dim]) dim = 1;
             if (th[2] > th[dim]) dim = 2;
             const int64_t other = block / int64_t(th[dim]);
-            const TilingRec* T = til[dim];
-            const int nt = H.nt[dim];
-            uint32_t fit = 0;
-            for (int j = 0; j < nt; ++j) fit += int64_t(uint64_t(T[j].threads) * uint64_t(other)) <= cap;
+            // tilings with threads * other <= cap, in enumeration order: the precomputed
+            // list for the largest distinct thread count <= cap / other
+            const uint8_t* F = K.P + H.off_fit[dim];
+            const int ntv = reinterpret_cast<const FitHeader*>(F)->ntv;
+            const uint32_t* tv = reinterpret_cast<const uint32_t*>(F + sizeof(FitHeader));
+            const uint32_t* start = tv + ntv;
+            const uint16_t* list = reinterpret_cast<const uint16_t*>(start + ntv + 1);
+            const int64_t lim = other > 0 ? cap / other : -1;
+            int lo = 0, hi = ntv;  // number of distinct thread counts <= lim
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (int64_t(tv[mid]) <= lim) lo = mid + 1;
+                else hi = mid;
+            }
+            const uint32_t fit = lo > 0 ? start[lo] - start[lo - 1] : 0u;
             if (fit == 0) {
-                t[dim] = uint32_t(nt - 1);  // {extent, 1, 1}: the last tiling in enumeration order
+                t[dim] = uint32_t(H.nt[dim] - 1);  // {extent, 1, 1}: the last tiling in enumeration order
             } else {
-                uint32_t r = uint32_t(lemire(c, fit));
-                for (int j = 0; j < nt; ++j) {
-                    if (int64_t(uint64_t(T[j].threads) * uint64_t(other)) <= cap) {
-                        if (r == 0) {
-                            t[dim] = uint32_t(j);
-                            break;
-                        }
-                        --r;
-                    }
-                }
+                const uint32_t r = uint32_t(lemire(c, fit));
+                t[dim] = list[start[lo - 1] + r];
             }
         }
         x.t0 = t[0];
@@ -280,7 +283,7 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
         }
         // ---- level windows
         if (tid == 0) {
-            const double sd = sqrt(var > 0.05 ? var : 0.05);
+            const float sd = sqrtf(float(var > 0.05 ? var : 0.05));  // window placement only: fp32 is plenty
             int cells = 0, j = 0;
             for (; j < kMaxLevels && i0 + j < n; ++j) {
                 int lo, hi_j;
@@ -288,10 +291,10 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
                     lo = 0;
                     hi_j = 0;
                 } else {
-                    const double c = mean * j;
-                    const int h = 2 + int(ceil(4.0 * sd * sqrt(double(j))));
-                    lo = max(j, int(floor(c)) - h);
-                    hi_j = int(ceil(c)) + h;
+                    const float c = float(mean) * float(j);
+                    const int h = 2 + int(ceilf(4.0f * sd * sqrtf(float(j))));
+                    lo = max(j, int(floorf(c)) - h);
+                    hi_j = int(ceilf(c)) + h;
                 }
                 const int w = hi_j - lo + 1;
                 if (cells + w > kCells) break;

@@ -100,7 +100,16 @@ struct PlanHdr {
     uint32_t off_ptn;     // double [nd2] log1p(pt_n)
     uint32_t off_steps;   // double [ndk] log1p(K / k_tile)
     uint32_t off_lvl;     // double [4] log1p(8..11)
+    uint32_t off_fit[3];  // repair tables per dim (FitTables below)
     uint32_t total;
+};
+
+// repair_schedule's "tilings whose threads fit" lists (genetic.cpp:101-110), per dim:
+//   int32 ntv; int32 pad; uint32 tv[ntv] (distinct thread counts, ascending);
+//   uint32 start[ntv + 1]; uint16 list[] where list[start[c] .. start[c+1]) are the
+//   tiling indices with threads <= tv[c], in enumeration order.
+struct FitHeader {
+    int32_t ntv, pad;
 };
 
 // ------------------------------------------------------------ score blob

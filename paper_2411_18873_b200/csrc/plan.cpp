@@ -283,6 +283,30 @@ etune_status build_plan(const etune_op_spec& op, const etune_device_config& dev,
     H.off_ptn = put(blob, P->ptn.data(), P->ptn.size());
     H.off_steps = put(blob, P->steps.data(), P->steps.size());
     H.off_lvl = put(blob, P->lvl, 4);
+    for (int d = 0; d < 3; ++d) {  // repair fit tables (breed_kernel)
+        std::vector<uint32_t> tv;
+        for (const TilingRec& r : P->til[d]) tv.push_back(r.threads);
+        std::sort(tv.begin(), tv.end());
+        tv.erase(std::unique(tv.begin(), tv.end()), tv.end());
+        std::vector<uint32_t> start(1, 0u);
+        std::vector<uint16_t> list;
+        for (uint32_t lim : tv) {
+            for (size_t j = 0; j < P->til[d].size(); ++j)
+                if (P->til[d][j].threads <= lim) list.push_back(uint16_t(j));
+            start.push_back(uint32_t(list.size()));
+        }
+        std::vector<uint8_t> blk(sizeof(FitHeader) + 4 * tv.size() + 4 * start.size() + 2 * list.size());
+        FitHeader fh{int32_t(tv.size()), 0};
+        size_t o = 0;
+        std::memcpy(blk.data() + o, &fh, sizeof(fh));
+        o += sizeof(fh);
+        std::memcpy(blk.data() + o, tv.data(), 4 * tv.size());
+        o += 4 * tv.size();
+        std::memcpy(blk.data() + o, start.data(), 4 * start.size());
+        o += 4 * start.size();
+        if (!list.empty()) std::memcpy(blk.data() + o, list.data(), 2 * list.size());
+        H.off_fit[d] = put(blob, blk.data(), blk.size());
+    }
     blob.resize(align16(blob.size()));
     H.total = uint32_t(blob.size());
     std::memcpy(blob.data(), &H, sizeof(H));
