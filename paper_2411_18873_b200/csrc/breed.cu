@@ -38,7 +38,8 @@ namespace {
 constexpr int kBreedThreads = 1024;
 constexpr int kRing = 4096;           // words of the MT stream kept in shared memory
 constexpr int kCells = 2048;          // speculative (offspring, offset) evaluations per round
-constexpr int kMaxLevels = 96;        // offspring resolved per round at most
+constexpr int kMaxLevels = 96;        // offspring resolved per round at most (3 per lane of warp 0)
+constexpr int kJump = 7;              // pointer-doubling tables: 2^7 >= kMaxLevels
 constexpr uint16_t kUnknown = 0;      // cell needs words beyond the generated horizon
 constexpr uint16_t kIllegal = 0xffff; // repair produced an illegal schedule (reference throws)
 
@@ -239,11 +240,14 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
     uint64_t* cg = ring + kRing;
     int32_t* cp = reinterpret_cast<int32_t*>(cg + kCells);
     uint16_t* cw = reinterpret_cast<uint16_t*>(cp + kCells);
-    uint64_t* mt = reinterpret_cast<uint64_t*>(cw + kCells);
+    int16_t* jt = reinterpret_cast<int16_t*>(cw + kCells);     // [kJump][kCells] successor^(2^r)
+    uint8_t* clev = reinterpret_cast<uint8_t*>(jt + kJump * kCells);  // level of each cell
+    uint64_t* mt = reinterpret_cast<uint64_t*>(clev + kCells);
     __shared__ int32_t lstart[kMaxLevels + 1], llo[kMaxLevels], lhi[kMaxLevels];
-    __shared__ int16_t sel[kMaxLevels];
+    __shared__ int16_t path[kMaxLevels];
     __shared__ int s_levels, s_resolved, s_status, s_other;
     __shared__ uint64_t s_step;
+    __shared__ double s_mean, s_var;
     const int tid = threadIdx.x;
 
     const uint8_t* P = gplan;
@@ -270,8 +274,11 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
     uint64_t hi = 0;          // words generated so far (ring holds [hi - kRing, hi) at most)
     uint64_t o0 = 0;          // first word of offspring i0
     int64_t i0 = 0;
-    double mean = 2.8, var = 0.6;  // running word-count statistics (window placement only)
-    double s1 = 0.0, s2 = 0.0;
+    double s1 = 0.0, s2 = 0.0;  // running word-count statistics (warp 0; window placement only)
+    if (tid == 0) {
+        s_mean = 2.8;
+        s_var = 0.6;
+    }
     int64_t cnt = 0;
     int status = 0;
     while (i0 < n) {
@@ -281,30 +288,44 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
             if (tid < 312) ring[(hi + uint64_t(tid)) & (kRing - 1)] = mt64::temper(mt[tid]);
             hi += 312;
         }
-        // ---- level windows
-        if (tid == 0) {
-            const float sd = sqrtf(float(var > 0.05 ? var : 0.05));  // window placement only: fp32 is plenty
-            int cells = 0, j = 0;
-            for (; j < kMaxLevels && i0 + j < n; ++j) {
-                int lo, hi_j;
-                if (j == 0) {
-                    lo = 0;
-                    hi_j = 0;
-                } else {
-                    const float c = float(mean) * float(j);
+        // ---- level windows (warp 0: widths, then a warp scan of the cell counts)
+        if (tid < 32) {
+            const float sd = sqrtf(float(s_var > 0.05 ? s_var : 0.05));  // window placement only
+            const float mean = float(s_mean);
+            int carry = 0, levels = 0;
+            for (int q = 0; q < kMaxLevels / 32; ++q) {
+                const int j = q * 32 + tid;
+                int lo = 0, hi_j = 0;
+                if (j > 0) {
+                    const float c = mean * float(j);
                     const int h = 2 + int(ceilf(4.0f * sd * sqrtf(float(j))));
                     lo = max(j, int(floorf(c)) - h);
                     hi_j = int(ceilf(c)) + h;
                 }
                 const int w = hi_j - lo + 1;
-                if (cells + w > kCells) break;
-                lstart[j] = cells;
-                llo[j] = lo;
-                lhi[j] = hi_j;
-                cells += w;
+                int x = w;  // inclusive scan of widths
+                for (int sft = 1; sft < 32; sft <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, sft);
+                    if (tid >= sft) x += y;
+                }
+                const int start = carry + x - w;
+                const bool fits = start + w <= kCells && i0 + j < n;
+                const unsigned ok = __ballot_sync(0xffffffffu, fits);
+                const int take = (~ok) ? __ffs(~ok) - 1 : 32;  // leading levels that fit
+                if (tid < take) {
+                    lstart[j] = start;
+                    llo[j] = lo;
+                    lhi[j] = hi_j;
+                }
+                levels += take;
+                carry += __shfl_sync(0xffffffffu, x, 31);
+                if (take < 32) {
+                    if (tid == take) lstart[j] = start;  // end sentinel
+                    break;
+                }
+                if (q == kMaxLevels / 32 - 1 && tid == 31) lstart[j + 1] = start + w;
             }
-            lstart[j] = cells;
-            s_levels = j;
+            if (tid == 0) s_levels = levels;
         }
         __syncthreads();
         const int J = s_levels, ncell = lstart[J];
@@ -322,57 +343,89 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
             cg[cell] = ch.g;
             cp[cell] = ch.partner;
             cw[cell] = ch.words;
+            clev[cell] = uint8_t(j);
         }
         __syncthreads();
-        // ---- walk the true chain through the cells
-        if (tid == 0) {
-            int x = 0, r = 0, stt = 0;
-            for (int j = 0; j < J; ++j) {
-                if (x < llo[j] || x > lhi[j]) break;
-                const int cell = lstart[j] + (x - llo[j]);
-                const uint16_t w = cw[cell];
-                if (w == kUnknown) break;
-                if (w == kIllegal) {
-                    stt = ETUNE_ERR_ILLEGAL_SCHEDULE;
-                    atomicMin(err, (static_cast<unsigned long long>(i0 + j) << 8) | unsigned(stt));
-                    break;
-                }
-                sel[j] = int16_t(cell);
-                x += w;
-                ++r;
+        // ---- the true chain through the cells by pointer doubling:
+        // succ(level j, offset x) = (level j+1, x + words) when that offset lies in the window
+        for (int cell = tid; cell < ncell; cell += blockDim.x) {
+            const int j = clev[cell];
+            const uint16_t w = cw[cell];
+            int16_t nx = -1;
+            if (w != kUnknown && w != kIllegal && j + 1 < J) {
+                const int x = llo[j] + (cell - lstart[j]) + int(w);
+                if (x >= llo[j + 1] && x <= lhi[j + 1]) nx = int16_t(lstart[j + 1] + (x - llo[j + 1]));
             }
-            if (r == 0 && stt == 0 && hi + 312 > o0 + kRing) {
+            jt[cell] = nx;
+        }
+        __syncthreads();
+        for (int r = 1; r < kJump; ++r) {
+            const int16_t* prev = jt + (r - 1) * kCells;
+            int16_t* cur = jt + r * kCells;
+            for (int cell = tid; cell < ncell; cell += blockDim.x) {
+                const int16_t m = prev[cell];
+                cur[cell] = m < 0 ? int16_t(-1) : prev[m];
+            }
+            __syncthreads();
+        }
+        if (tid < J) {  // cell of level j on the chain from (level 0, offset 0) = cell 0
+            int c = 0;
+            for (int r = 0; r < kJump && c >= 0; ++r)
+                if ((tid >> r) & 1) c = jt[r * kCells + c];
+            path[tid] = int16_t(c);
+        }
+        if (tid == 0) s_resolved = J;
+        __syncthreads();
+        if (tid < J) {  // resolved = leading levels whose cell exists and evaluated completely
+            const int c = path[tid];
+            if (c < 0 || cw[c] == kUnknown || cw[c] == kIllegal) atomicMin(&s_resolved, tid);
+        }
+        __syncthreads();
+        const int R = s_resolved;
+        if (tid == 0) {
+            int stt = 0;
+            if (R < J && path[R] >= 0 && cw[path[R]] == kIllegal) {
+                stt = ETUNE_ERR_ILLEGAL_SCHEDULE;
+                atomicMin(err, (static_cast<unsigned long long>(i0 + R) << 8) | unsigned(stt));
+            } else if (R == 0 && hi + 312 > o0 + kRing) {
                 // offspring i0 alone needs more than the ring's words (a crossover whose
                 // partner search runs for thousands of draws): beyond this build's window
                 stt = ETUNE_ERR_UNSUPPORTED;
                 atomicMin(err, (static_cast<unsigned long long>(i0) << 8) | unsigned(stt));
             }
-            s_resolved = r;
             s_status = stt;
-            s_step = uint64_t(x);
+            const int last = R > 0 ? path[R - 1] : -1;
+            s_step = R > 0 ? uint64_t(llo[R - 1] + (last - lstart[R - 1]) + int(cw[last])) : 0ull;
         }
-        __syncthreads();
-        const int R = s_resolved;
         if (tid < R) {
-            const int cell = sel[tid];
+            const int cell = path[tid];
             out[i0 + tid] = cg[cell];
             if (partner) partner[i0 + tid] = cp[cell];
         }
-        // running statistics of words per offspring, from the resolved levels
-        if (R > 0) {
-            for (int j = 0; j < R; ++j) {  // uniform loop: every thread keeps the same stats
-                const double w = double(cw[sel[j]]);
-                s1 += w;
-                s2 += w * w;
+        // running statistics of words per offspring (warp 0; window placement only)
+        if (tid < 32 && R > 0) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int j = tid; j < R; j += 32) {
+                const double w = double(cw[path[j]]);
+                a1 += w;
+                a2 += w * w;
             }
+            for (int sft = 16; sft > 0; sft >>= 1) {
+                a1 += __shfl_xor_sync(0xffffffffu, a1, sft);
+                a2 += __shfl_xor_sync(0xffffffffu, a2, sft);
+            }
+            s1 += a1;
+            s2 += a2;
             cnt += R;
-            mean = s1 / double(cnt);
-            var = s2 / double(cnt) - mean * mean;
+            if (tid == 0) {
+                s_mean = s1 / double(cnt);
+                s_var = s2 / double(cnt) - s_mean * s_mean;
+            }
         }
+        __syncthreads();
         o0 += s_step;
         i0 += R;
         status = s_status;
-        __syncthreads();
         if (status) break;
     }
     if (tid == 0) {
@@ -393,7 +446,7 @@ cudaError_t launch_breed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t pla
     const double mutcro = mut + cro;     // genetic.cpp:169, evaluated like the reference
     const double total = mutcro + cpy;   // genetic.cpp:150: mutation + crossover + copy
     // ~64 KB of working arrays; the plan blob joins them in shared memory when it fits
-    constexpr size_t kFixed = size_t(kRing) * 8 + size_t(kCells) * (8 + 4 + 2) + 312 * 8;
+    constexpr size_t kFixed = size_t(kRing) * 8 + size_t(kCells) * (8 + 4 + 2 + 2 * kJump + 1) + 312 * 8;
     static_assert(kFixed % 16 == 0, "plan section must stay 16-byte aligned");
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
