@@ -574,9 +574,14 @@ void sim_measure(const Counters& c, const SimDev& d, uint64_t id, double* out4) 
         const uint64_t key = splitmix(d.seed ^ id);
         double sum = 0.0;
         for (int64_t j = 0; j < S; ++j) {
-            double z = -6.0;
-            for (int q = 0; q < 12; ++q)
-                z += static_cast<double>(splitmix(key + static_cast<uint64_t>(j * 12 + q)) >> 11) * 0x1p-53;
+            // z ~ Irwin-Hall(12) - 6: twelve 16-bit uniforms from three splitmix64 words,
+            // summed as integers (exact), one conversion
+            uint64_t usum = 0;
+            for (int q = 0; q < 3; ++q) {
+                const uint64_t h = splitmix(key + static_cast<uint64_t>(j * 3 + q));
+                for (int b = 0; b < 4; ++b) usum += (h >> (16 * b)) & 0xffffu;
+            }
+            const double z = static_cast<double>(usum) * 0x1p-16 - 6.0;
             sum += power * (1.0 + d.sigma * z);
         }
         avg = sum / static_cast<double>(S);

@@ -259,6 +259,23 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
     return x ^ (x >> 31);
 }
 
+// sample j of the simulated sampler: power * (1 + sigma * z_j), z_j = Irwin-Hall(12) - 6
+// from twelve 16-bit uniforms of three splitmix64 words (integer sum, one conversion)
+__device__ __forceinline__ double sim_sample(double power, double sigma, uint64_t key, int64_t j) {
+    uint64_t usum = 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        const uint64_t h = splitmix(key + uint64_t(j * 3 + q));
+        usum += (h & 0xffffu) + ((h >> 16) & 0xffffu) + ((h >> 32) & 0xffffu) + (h >> 48);
+    }
+    const double z = __dsub_rn(__dmul_rn(static_cast<double>(usum), 0x1p-16), 6.0);
+    return __dmul_rn(power, __dadd_rn(1.0, __dmul_rn(sigma, z)));
+}
+
+// WARP = false: one candidate per thread (no sampler noise to draw); WARP = true: one
+// candidate per warp, the lanes draw 32 samples at a time and every lane forms the same
+// sequential sum from shuffled-in values (sum order j = 0..S-1, like the restatement).
+template <bool WARP>
 __global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
                                                                int use_smem, const uint64_t* __restrict__ genome,
                                                                int64_t n, SimDevice d, double* __restrict__ lat,
@@ -272,7 +289,12 @@ __global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __
         P = reinterpret_cast<const uint8_t*>(smem);
     }
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t unit0 = WARP ? (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5
+                               : blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    const int64_t ustride = WARP ? (int64_t(gridDim.x) * blockDim.x) >> 5 : int64_t(gridDim.x) * blockDim.x;
+    const bool writer = !WARP || lane == 0;
+    for (int64_t i = unit0; i < n; i += ustride) {
         const Knobs kn = load_knobs(P, H, genome[i]);
         const etune_counters c = plan_counters(H, kn);
         const double active = static_cast<double>(c.active_sms);
@@ -281,7 +303,7 @@ __global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __
         const double memory_s = __ddiv_rn(static_cast<double>(c.glb_ld + c.glb_st), d.bw);
         double lat_ms = __dmul_rn(compute_s > memory_s ? compute_s : memory_s, 1000.0);
         if (lat_ms < d.floor_ms) lat_ms = d.floor_ms;
-        lat[i] = lat_ms;
+        if (writer) lat[i] = lat_ms;
         if (!pow && !en && !iters) continue;  // measure_latency_ms only
         const double dyn_mj = __dmul_rn(
             __dadd_rn(__dadd_rn(__dmul_rn(static_cast<double>(c.flops), d.e_flop),
@@ -299,17 +321,22 @@ __global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __
         if (d.sigma != 0.0) {
             const uint64_t key = splitmix(d.seed ^ candidate_hash(H.fnv_prefix, kn));
             double sum = 0.0;
-            for (int64_t j = 0; j < S; ++j) {
-                double z = -6.0;
-                for (int q = 0; q < 12; ++q)
-                    z = __dadd_rn(z, __dmul_rn(static_cast<double>(splitmix(key + uint64_t(j * 12 + q)) >> 11), 0x1p-53));
-                sum = __dadd_rn(sum, __dmul_rn(power, __dadd_rn(1.0, __dmul_rn(d.sigma, z))));
+            if (WARP) {
+                for (int64_t base = 0; base < S; base += 32) {
+                    const double v = base + lane < S ? sim_sample(power, d.sigma, key, base + lane) : 0.0;
+                    const int cnt = int(S - base < 32 ? S - base : 32);
+                    for (int t = 0; t < cnt; ++t) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, v, t));
+                }
+            } else {
+                for (int64_t j = 0; j < S; ++j) sum = __dadd_rn(sum, sim_sample(power, d.sigma, key, j));
             }
             avg = __ddiv_rn(sum, static_cast<double>(S));
         }
-        if (pow) pow[i] = avg;
-        if (en) en[i] = __dmul_rn(avg, lat_ms);
-        if (iters) iters[i] = it;
+        if (writer) {
+            if (pow) pow[i] = avg;
+            if (en) en[i] = __dmul_rn(avg, lat_ms);
+            if (iters) iters[i] = it;
+        }
     }
 }
 
@@ -527,7 +554,13 @@ cudaError_t launch_counters(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
 cudaError_t launch_sim_measure(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
                                int64_t n, const SimDevice& d, double* d_lat, double* d_pow, double* d_en,
                                int64_t* d_iters) {
-    return launch_plan_kernel(sim_measure_kernel, c, d_plan, bytes, n, d_genome, n, d, d_lat, d_pow, d_en, d_iters);
+    const bool noise = d.sigma != 0.0 && (d_pow || d_en || d_iters);
+    if (!noise)
+        return launch_plan_kernel(sim_measure_kernel<false>, c, d_plan, bytes, n, d_genome, n, d, d_lat, d_pow, d_en,
+                                  d_iters);
+    // one warp per candidate: size the grid by warps (launch_plan_kernel sizes by threads)
+    return launch_plan_kernel(sim_measure_kernel<true>, c, d_plan, bytes, n * 32, d_genome, n, d, d_lat, d_pow, d_en,
+                              d_iters);
 }
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
                             int64_t n, double* d_feat, uint64_t* d_ids) {
