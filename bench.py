@@ -363,6 +363,12 @@ def run_ours(args):
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = n * ALGO_BYTES / (kernel_ms / 1e3) / 1e9
+    traffic = None
+    try:  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+        t = json.load(open(os.path.join(ROOT, "profiles", "score_kernel_traffic.json")))
+        traffic = int(t["dram_bytes_read_per_launch"]) + int(t["dram_bytes_write_per_launch"])
+    except Exception:
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -374,7 +380,7 @@ def run_ours(args):
                                   f"inside the C ABI)",
                    "l2": f"{nb} distinct population buffers cycled ({nb * n * 24 / 2**20:.0f} MB > 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": None, "kernel": "score_kernel", "kernel_ms": kernel_ms,
+                     "traffic": traffic, "kernel": "score_kernel", "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_candidate": ALGO_BYTES,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else
                                     "fallback 6650 GB/s (B200_PROFILING.md)",
