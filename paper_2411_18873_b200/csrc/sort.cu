@@ -62,6 +62,38 @@ __device__ __forceinline__ unsigned block_sum(unsigned v, unsigned* red) {
     return t;
 }
 
+// Exclusive scan across the warps of a block of one value per warp (`v` significant in
+// lane 0 of each warp); returns the warp's exclusive prefix to every lane and the block
+// total in *total.  Two barriers.
+__device__ __forceinline__ unsigned warp_prefix(unsigned v, unsigned* buf, unsigned* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) buf[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        const unsigned x = lane < nw ? buf[lane] : 0u;
+        unsigned y = x;
+        for (int s = 1; s < 32; s <<= 1) {
+            const unsigned t = __shfl_up_sync(0xffffffffu, y, s);
+            if (lane >= s) y += t;
+        }
+        if (lane < nw) buf[32 + lane] = y - x;
+        if (lane == 31) buf[64] = y;
+    }
+    __syncthreads();
+    *total = buf[64];
+    return buf[32 + warp];
+}
+
+// (key, index) compare-exchange for the in-register bitonic network
+__device__ __forceinline__ void cmpx(unsigned long long& k, unsigned& i, unsigned long long pk, unsigned pi,
+                                     bool keep_min) {
+    const bool mine_less = k < pk || (k == pk && i < pi);
+    if (mine_less != keep_min) {
+        k = pk;
+        i = pi;
+    }
+}
+
 // Whole top-k in one cooperative launch (grid-wide barriers between phases).  Each CTA
 // owns one contiguous chunk of the scores, caches its keys in shared memory (when they
 // fit) and all CTAs derive identical radix decisions from the global histograms.
@@ -74,6 +106,7 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
     extern __shared__ unsigned long long skeys[];
     __shared__ unsigned int h[kBins];
     __shared__ unsigned int red[32];
+    __shared__ unsigned int scanbuf[72];
     __shared__ unsigned int s_pick[2];
     const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x;
     const int64_t chunk = (n + G - 1) / G;
@@ -170,16 +203,14 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
             const int i = tid * per + q;
             if (i < nb) mine += w->hist[pass][i];
         }
-        // inclusive scan of `mine` over the block
+        // exclusive scan of `mine` over the block
         unsigned x = mine;
         for (int s = 1; s < 32; s <<= 1) {
             const unsigned y = __shfl_up_sync(0xffffffffu, x, s);
             if ((tid & 31) >= s) x += y;
         }
-        if ((tid & 31) == 31) red[tid >> 5] = x;
-        __syncthreads();
-        unsigned wbase = 0;
-        for (int i = 0; i < (tid >> 5); ++i) wbase += red[i];
+        unsigned btot;
+        const unsigned wbase = warp_prefix(__shfl_sync(0xffffffffu, x, 31), scanbuf, &btot);
         unsigned run = wbase + x - mine;  // exclusive
         for (int q = 0; q < per; ++q) {
             const int i = tid * per + q;
@@ -222,8 +253,7 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
     }
     pl = block_sum(pl, red);
     pe = block_sum(pe, red);
-    __shared__ unsigned wl[32], we[32];
-    const int lane = tid & 31, warp = tid >> 5;
+    const int lane = tid & 31;
     const unsigned ltm = (1u << lane) - 1u;
     const int64_t mr = (m + blockDim.x - 1) / blockDim.x * blockDim.x;
     for (int64_t j0 = 0; j0 < mr; j0 += blockDim.x) {
@@ -236,37 +266,59 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
             ise = key == T;
         }
         const unsigned bl = __ballot_sync(0xffffffffu, isl), be = __ballot_sync(0xffffffffu, ise);
-        if (lane == 0) {
-            wl[warp] = __popc(bl);
-            we[warp] = __popc(be);
-        }
-        __syncthreads();
-        unsigned xl = pl, xe = pe;
-        for (int i = 0; i < warp; ++i) {
-            xl += wl[i];
-            xe += we[i];
-        }
-        xl += __popc(bl & ltm);
-        xe += __popc(be & ltm);
+        // one scan of both counts packed in 16-bit halves (a block holds <= 1024 keys)
+        unsigned tot;
+        const unsigned x0 = warp_prefix(unsigned(__popc(bl)) | (unsigned(__popc(be)) << 16), scanbuf, &tot);
+        const unsigned tl = tot & 0xffffu, te = tot >> 16;
+        const unsigned xl = pl + (x0 & 0xffffu) + __popc(bl & ltm);
+        const unsigned xe = pe + (x0 >> 16) + __popc(be & ltm);
         if (isl || (ise && xe < need)) {
             const unsigned pos = xl + (xe < need ? xe : need);
             sel_key[pos] = key;
             sel_idx[pos] = uint32_t(lo + j);
         }
-        for (int i = 0; i < int(blockDim.x >> 5); ++i) {
-            pl += wl[i];
-            pe += we[i];
-        }
-        __syncthreads();
+        pl += tl;
+        pe += te;
+        __syncthreads();  // scan buffers reused by the next chunk
     }
     if (!final_sort) return;
     grid.sync();
     // ---- phase E: CTA 0 sorts the k pairs by (key, index) (bitonic, k <= kSmallSort)
     if (b != 0) return;
-    unsigned long long* sk = skeys;
-    unsigned int* si = reinterpret_cast<unsigned int*>(skeys + kSmallSort);
     int P = 1;
     while (P < int(k)) P <<= 1;
+    if (P <= int(blockDim.x)) {
+        // one pair per thread in registers: strides < 32 by warp shuffles, larger strides
+        // through shared memory (15 exchanges for 1024 pairs instead of 55 smem stages)
+        unsigned long long* xk = skeys;
+        unsigned int* xi = reinterpret_cast<unsigned int*>(skeys + 1024);
+        unsigned long long kk = tid < int(k) ? sel_key[tid] : ~0ull;
+        unsigned ii = tid < int(k) ? sel_idx[tid] : 0xffffffffu;
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const bool up = (tid & size) == 0;
+                const bool low = (tid & stride) == 0;  // the lower index of the pair
+                unsigned long long pk;
+                unsigned pi;
+                if (stride >= 32) {
+                    __syncthreads();
+                    xk[tid] = kk;
+                    xi[tid] = ii;
+                    __syncthreads();
+                    pk = xk[tid ^ stride];
+                    pi = xi[tid ^ stride];
+                } else {
+                    pk = __shfl_xor_sync(0xffffffffu, kk, stride);
+                    pi = __shfl_xor_sync(0xffffffffu, ii, stride);
+                }
+                if (tid < P) cmpx(kk, ii, pk, pi, up == low);
+            }
+        }
+        if (tid < int(k)) out[tid] = ii;
+        return;
+    }
+    unsigned long long* sk = skeys;
+    unsigned int* si = reinterpret_cast<unsigned int*>(skeys + kSmallSort);
     for (int i = tid; i < P; i += blockDim.x) {
         sk[i] = i < int(k) ? sel_key[i] : ~0ull;
         si[i] = i < int(k) ? sel_idx[i] : 0xffffffffu;
