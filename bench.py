@@ -262,8 +262,7 @@ def run_ours(args):
     from paper_2411_18873_b200 import capi
 
     forest_flat = load_forest()
-    op, sched = make_population(args.pop, seed=7 + rank)
-    n = len(sched)
+    op = parse_op_text(OP_TEXT)
     ctx = capi.Context(local)
     if world > 1:  # the library's own NCCL communicator (per-shard top-k all-gather)
         uid = [capi.nccl_unique_id() if rank == 0 else None]
@@ -271,10 +270,13 @@ def run_ours(args):
         capi.attach_nccl(ctx, uid[0], world, rank)
     plan = capi.Plan(ctx, op)
     forest = capi.Forest.from_flat(ctx, forest_flat)
-    d_sched = torch.from_numpy(sched).cuda()
-    g0 = plan.encode(d_sched)
+    # the SURVEY §8(d) population, bred on the device (bit-exact with the reference's
+    # sample_random + reproduce): reproduce(sample_random(op, 1024, 42), n, {}, 7 + rank)
+    parents = plan.sample_random(1024, 42)
+    g0, _, _ = capi.reproduce(plan, parents, args.pop, 7 + rank)
+    sched = plan.decode(g0).cpu().numpy()  # host Schedule[] for the e2e call and the CPU baseline
     ctx.synchronize()
-    del d_sched
+    n = len(sched)
     nb = args.bufs
     genomes = [g0.clone() for _ in range(nb)]
     preds = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nb)]
@@ -283,17 +285,12 @@ def run_ours(args):
     top = torch.empty(K, dtype=torch.int64, device="cuda")
     top_sc = torch.empty(K, dtype=torch.float64, device="cuda")
 
-    def step(i, kev=None):
+    def step(i):
         b = i % nb
-        if kev is not None:
-            kev[0].record(stream)
-        forest.score(plan, genomes[b], out=preds[b], ids_out=ids[b])
-        if kev is not None:
-            kev[1].record(stream)
-        if world > 1:  # local top-k -> ncclAllGather of (score, global idx) -> identical merge
-            capi.topk_sharded(ctx, preds[b], rank * n, K, idx=top, sc=top_sc)
-        else:
-            capi.topk(ctx, preds[b], K, out=top)
+        if world > 1:  # fused score + local top-k -> ncclAllGather of (score, global idx) -> identical merge
+            forest.score_select_sharded(plan, genomes[b], rank * n, K, preds[b], top, sc=top_sc, ids=ids[b])
+        else:  # fused score + top-k (etune_cu_score_select)
+            forest.score_select(plan, genomes[b], K, preds[b], top, ids=ids[b])
 
     for i in range(args.warmup):
         step(i)
@@ -303,19 +300,26 @@ def run_ours(args):
     launches0 = capi.lib().etune_cu_launch_count()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         ev0.record(stream)
         clk.sample()
         for i in range(args.steps):
-            step(args.warmup + i, kev[i])
+            step(args.warmup + i)
         ev1.record(stream)
         clk.sample()
         torch.cuda.synchronize()
     launches = capi.lib().etune_cu_launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
-    kernel_ms = sum(a.elapsed_time(b) for a, b in kev) / args.steps
+    # kernel split: a separate pass with CUDA events around the score kernel and the
+    # selection kernels of each call (events serialise the PDL overlap, so the timed
+    # loop above runs without them)
+    capi.profile_score(ctx, True)
+    for i in range(args.steps):
+        step(args.warmup + args.steps + i)
+    score_ms, select_ms, score_calls = capi.profile_score(ctx, False)
+    kernel_ms = score_ms / max(score_calls, 1)
+    select_ms = select_ms / max(score_calls, 1)
     if world > 1:
         t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -373,8 +377,8 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"score (features -> 100-tree GBDT -> prediction + id) + top-{K} of "
-                               f"{n} {OP_TEXT} candidates per GPU", "op": OP_TEXT, "population_per_gpu": n,
+        "config": {"workload": f"fused score (features -> 100-tree GBDT -> prediction + id, bucketed) + "
+                               f"top-{K} of {n} {OP_TEXT} candidates per GPU", "op": OP_TEXT, "population_per_gpu": n,
                    "k": K, "model": "reference-trained 100-tree depth-6 GBDT (tests/golden c2 fixture)",
                    "parallelism": f"dp{world} (population sharded; NCCL all-gather of per-shard top-k records "
                                   f"inside the C ABI)",
@@ -384,7 +388,8 @@ def run_ours(args):
                      "algorithmic_bytes_per_candidate": ALGO_BYTES,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else
                                     "fallback 6650 GB/s (B200_PROFILING.md)",
-                     "note": "SM-bound by design (shared-memory pipe), see profiles/"},
+                     "note": "SM-bound by design (shared-memory pipe), see profiles/",
+                     "select_ms": select_ms},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -253,11 +253,21 @@ etune_status etune_cu_score(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                             double* d_pred, uint64_t* d_ids /*nullable*/);
 
 /* One step of the hot path: fused score of a device population, then its k best by
- * (prediction asc, index asc) into d_idx (sorted).  d_ids nullable. */
+ * (prediction asc, index asc) into d_idx (sorted).  d_ids nullable.  Same result as
+ * etune_cu_score + etune_cu_topk; for k <= 4096 the score kernel also buckets every
+ * prediction, so the selection reads the predictions once and resolves one bucket.
+ * Replaces the reference's predict_many (energy_model.hpp:72) + partial sort. */
 etune_status etune_cu_score_select(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                    etune_cu_forest* forest, const uint64_t* d_genome, int64_t n,
                                    int64_t k, double* d_pred, uint64_t* d_ids /*nullable*/,
                                    int64_t* d_idx);
+
+/* Device time of the score kernels and of the selection kernels launched by
+ * etune_cu_score_select since the last call (CUDA events on the ctx stream;
+ * synchronises when any were recorded), then switches that timing on (on != 0) or off.
+ * For benchmarks and profiling (the events serialise the launches they separate). */
+etune_status etune_cu_profile_score(etune_cu_ctx* ctx, int on, double* score_ms /*nullable*/,
+                                    double* select_ms /*nullable*/, int64_t* launches /*nullable*/);
 
 /* Reference-facing end-to-end call with HOST buffers: schedules in the reference's
  * Schedule layout -> predictions (+ ids).  Host->device copy, encode (legality check),
@@ -414,6 +424,16 @@ etune_status etune_cu_ctx_attach_nccl(etune_cu_ctx* ctx, const void* unique_id, 
 etune_status etune_cu_topk_sharded(etune_cu_ctx* ctx, const double* d_score, int64_t n,
                                    int64_t global_offset, int64_t k, int64_t* d_idx_global,
                                    double* d_score_out /*nullable*/);
+
+/* etune_cu_score_select on a shard: fused score of the rank's n candidates (global
+ * indices [global_offset, global_offset + n)), its local k best, then the same
+ * all-gather + merge as etune_cu_topk_sharded: every rank returns the same k global
+ * indices (and scores, nullable). */
+etune_status etune_cu_score_select_sharded(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                           etune_cu_forest* forest, const uint64_t* d_genome,
+                                           int64_t n, int64_t global_offset, int64_t k,
+                                           double* d_pred, uint64_t* d_ids /*nullable*/,
+                                           int64_t* d_idx_global, double* d_score_out /*nullable*/);
 
 /* ncclBroadcast of `bytes` device bytes from `root` (trained forest arrays). */
 etune_status etune_cu_broadcast(etune_cu_ctx* ctx, void* d_buf, int64_t bytes, int root);

@@ -126,6 +126,9 @@ _SIGS = {
     "etune_cu_predict": (C.c_int, [_VP, _VP, _PTR, _I64, _PTR]),
     "etune_cu_score": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR]),
     "etune_cu_score_select": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _I64, _PTR, _PTR, _PTR]),
+    "etune_cu_score_select_sharded": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _I64, _I64, _PTR, _PTR, _PTR, _PTR]),
+    "etune_cu_profile_score": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                         C.POINTER(_I64)]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
     "etune_cu_train": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(BoostParams), _PTR, _PTR, _PTR, _PTR, _PTR, _PTR,
@@ -444,6 +447,13 @@ class Forest:
                                            _ptr(pred), _ptr(ids), _ptr(idx)))
         return pred, idx
 
+    def score_select_sharded(self, plan: Plan, genome, global_offset: int, k: int, pred, idx, sc=None, ids=None):
+        """Fused score + per-shard keep-the-best + all-gather merge (etune_cu_score_select_sharded)."""
+        _check(lib().etune_cu_score_select_sharded(self.ctx.h, plan.h, self.h, _ptr(genome), genome.shape[0],
+                                                   int(global_offset), int(k), _ptr(pred), _ptr(ids), _ptr(idx),
+                                                   _ptr(sc)))
+        return idx, sc
+
     def score_host(self, plan: Plan, sched: np.ndarray, pred: np.ndarray, ids: Optional[np.ndarray] = None):
         """Reference-facing call on HOST buffers (pinned numpy views recommended)."""
         n = sched.shape[0]
@@ -582,6 +592,16 @@ class Search:
         out = torch.empty(n.value, dtype=torch.int64, device=torch.device("cuda", self.plan.ctx.device))
         _check(lib().etune_cu_search_parents(self.h, _ptr(out), n.value, C.byref(n)))
         return out
+
+
+def profile_score(ctx: Context, on: bool):
+    """(score-kernel ms, selection ms, calls) recorded inside score_select since the last call;
+    then timing on/off."""
+    ms = C.c_double()
+    sel = C.c_double()
+    cnt = _I64()
+    _check(lib().etune_cu_profile_score(ctx.h, int(bool(on)), C.byref(ms), C.byref(sel), C.byref(cnt)))
+    return ms.value, sel.value, cnt.value
 
 
 def topk(ctx: Context, score, k: int, out=None):

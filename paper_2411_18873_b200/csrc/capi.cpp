@@ -33,6 +33,9 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->io);
     cudaFree(c->breed);
     cudaFree(c->shard);
+    cudaFree(c->sel);
+    for (auto& e : c->prof_ev)
+        for (cudaEvent_t x : e) cudaEventDestroy(x);
     if (c->h2d) {
         cudaStreamDestroy(c->h2d);
         cudaStreamDestroy(c->d2h);
@@ -104,6 +107,44 @@ etune_status ensure_io(etune_cu_ctx* c, size_t bytes) {
     return ETUNE_OK;
 }
 
+uint64_t order_key_host(double x) {
+    uint64_t b;
+    std::memcpy(&b, &x, 8);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Buckets of the fused selection: the prediction range the forest can produce
+// (base + lr * sum of per-tree leaf extremes, floored like EnergyModel::predict,
+// energy_model.cpp:245-249), split into kSelBins equal spans of order keys.  Only the
+// resolution depends on these bounds: the bucket function clamps, so it stays exact.
+void selection_buckets(const ForestHost& F, uint64_t* kmin, uint32_t* shift) {
+    double lo = 0.0, hi = 0.0;
+    for (int64_t t = 0; t < F.num_trees(); ++t) {
+        double tl = 0.0, th = 0.0;
+        bool any = false;
+        for (int64_t i = F.offsets[t]; i < F.offsets[t + 1]; ++i) {
+            if (F.feature[i] >= 0) continue;
+            const double v = F.value[i];
+            tl = any ? std::min(tl, v) : v;
+            th = any ? std::max(th, v) : v;
+            any = true;
+        }
+        lo += tl;
+        hi += th;
+    }
+    double plo = F.base + F.lr * (F.lr >= 0 ? lo : hi);
+    double phi = F.base + F.lr * (F.lr >= 0 ? hi : lo);
+    plo = std::max(1e-6, plo);
+    phi = std::max(1e-6, phi);
+    uint64_t a = order_key_host(plo), b = order_key_host(phi);
+    if (!(b > a)) b = a + 1;  // degenerate or NaN bounds: any bucketing is still exact
+    const uint64_t span = b - a;
+    uint32_t s = 0;
+    while (s < 63 && (span >> s) >= uint64_t(kSelBins)) ++s;
+    *kmin = a;
+    *shift = s;
+}
+
 etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledScore** out) {
     std::lock_guard<std::mutex> lock(f->mu);
     auto it = f->compiled.find(p->serial);
@@ -116,7 +157,7 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     CompiledScore cs;
     const etune_status bst = build_score_blob(f->host, p->build, &blob, &cs.stats, &err);
     if (bst != ETUNE_OK && bst != ETUNE_ERR_UNSUPPORTED) return fail(bst, err);
-    const int cap = max_dynamic_smem(f->ctx->device);
+    const int cap = max_dynamic_smem(f->ctx->device) - score_static_smem();
     if (bst == ETUNE_ERR_UNSUPPORTED || blob.size() > size_t(cap)) {
         // the general path: features + the reference tree walk (any forest)
         if (p->build.hdr.total > uint32_t(cap)) return fail(ETUNE_ERR_UNSUPPORTED, "plan tables exceed shared memory");
@@ -138,6 +179,7 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
         std::memcpy(cs.params->pair, blob.data() + hdr->off_trees, sizeof(PairRec) * size_t(hdr->npairs));
     else
         std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
+    selection_buckets(f->host, &cs.sel_kmin, &cs.sel_shift);
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;
@@ -150,6 +192,109 @@ cudaError_t run_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* 
                                  d_pred, d_ids);
     return launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
                         cs->per_sm);
+}
+
+
+// Fused score + keep-the-best on one shard: the score kernel fills the selection
+// histogram, sel_filter/sel_finish (sort.cu) resolve the k lowest (score, index).
+// Forests on the tree-walk path and k > kSelMaxK use score + the cooperative top-k.
+etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
+                                const uint64_t* d_genome, int64_t n, int64_t k, double* d_pred, uint64_t* d_ids,
+                                int64_t* d_idx) {
+    if (cs->walk || k > kSelMaxK || k == 0) {
+        CU(run_score(c, p, f, cs, d_genome, n, d_pred, d_ids));
+        if (k == 0) return ETUNE_OK;
+        if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
+        CU(launch_topk(c->lc(), d_pred, n, k, d_idx, c->scratch));
+        return ETUNE_OK;
+    }
+    const size_t need = select_scratch_bytes(n, k);
+    if (c->sel_bytes < need) {
+        if (c->sel) {
+            CU(cudaStreamSynchronize(c->stream));
+            CU(cudaFree(c->sel));
+            c->sel = nullptr;
+            c->sel_bytes = 0;
+        }
+        CU(cudaMalloc(&c->sel, need));
+        c->sel_bytes = need;
+        c->sel_dirty = true;
+    }
+    if (c->sel_dirty) CU(cudaMemsetAsync(c->sel, 0, 8192, c->stream));  // histogram + list counters
+    c->sel_dirty = true;
+    const SelHist sh{select_hist(c->sel), cs->sel_kmin, cs->sel_shift};
+    const bool prof = c->prof_on;
+    if (prof) {
+        if (c->prof_used == c->prof_ev.size()) {
+            std::array<cudaEvent_t, 3> e{};
+            for (cudaEvent_t& x : e) CU(cudaEventCreate(&x));
+            c->prof_ev.push_back(e);
+        }
+        CU(cudaEventRecord(c->prof_ev[c->prof_used][0], c->stream));
+    }
+    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
+                    cs->per_sm, sh));
+    if (prof) CU(cudaEventRecord(c->prof_ev[c->prof_used][1], c->stream));
+    CU(launch_select(c->lc(), d_pred, n, k, d_idx, c->sel, sh));
+    if (prof) CU(cudaEventRecord(c->prof_ev[c->prof_used++][2], c->stream));
+    c->sel_dirty = false;
+    return ETUNE_OK;
+}
+
+// records: [k local scores | k local gidx | W*k gathered scores | W*k gathered gidx | k positions]
+struct ShardBufs {
+    double *ls, *gs;
+    int64_t *lg, *gg, *pos, *lidx;
+};
+
+etune_status shard_buffers(etune_cu_ctx* c, int64_t k, ShardBufs* b) {
+    const int W = c->comm ? c->nranks : 1;
+    const size_t need = size_t(k) * 16 * (1 + size_t(W)) + size_t(k) * 8 + 1024;
+    if (c->shard_bytes < need) {
+        if (c->shard) {
+            CU(cudaStreamSynchronize(c->stream));
+            CU(cudaFree(c->shard));
+            c->shard = nullptr;
+            c->shard_bytes = 0;
+        }
+        CU(cudaMalloc(&c->shard, need));
+        c->shard_bytes = need;
+    }
+    b->ls = static_cast<double*>(c->shard);
+    b->lg = reinterpret_cast<int64_t*>(b->ls + k);
+    b->gs = reinterpret_cast<double*>(b->lg + k);
+    b->gg = reinterpret_cast<int64_t*>(b->gs + size_t(W) * k);
+    b->pos = b->gg + size_t(W) * k;
+    b->lidx = b->pos;  // local selection reuses the position buffer
+    return ETUNE_OK;
+}
+
+// Local top-kl indices in b.lidx -> (score, global index) records -> ncclAllGather ->
+// the identical merged top-k on every rank.
+etune_status shard_merge(etune_cu_ctx* c, const double* d_score, int64_t kl, int64_t k, int64_t goff,
+                         const ShardBufs& b, int64_t* d_idx, double* d_sc) {
+    const int W = c->comm ? c->nranks : 1;
+    double* gs = b.gs;
+    int64_t* gg = b.gg;
+    CU(launch_pack_records(c->lc(), d_score, b.lidx, kl, k, goff, b.ls, b.lg));
+    if (W > 1) {
+        ncclResult_t r = ncclGroupStart();
+        if (r == ncclSuccess) r = ncclAllGather(b.ls, gs, size_t(k), ncclFloat64, c->comm, c->stream);
+        if (r == ncclSuccess) r = ncclAllGather(b.lg, gg, size_t(k), ncclInt64, c->comm, c->stream);
+        const ncclResult_t r2 = ncclGroupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(ETUNE_ERR_CUDA, std::string("ncclAllGather: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
+    } else {
+        gs = b.ls;
+        gg = b.lg;
+    }
+    // shards are contiguous and ascending by rank, each list sorted by (score, gidx):
+    // (score, position) order over the rank-major concatenation == (score, gidx) order
+    const int64_t tot = int64_t(W) * k;
+    if (etune_status st = ensure_scratch(c, topk_scratch_bytes(tot))) return st;
+    CU(launch_topk(c->lc(), gs, tot, k, b.pos, c->scratch));
+    CU(launch_gather_records(c->lc(), gs, gg, b.pos, k, d_idx, d_sc));
+    return ETUNE_OK;
 }
 
 }  // namespace
@@ -735,8 +880,54 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
 etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
                                    const uint64_t* d_genome, int64_t n, int64_t k, double* d_pred, uint64_t* d_ids,
                                    int64_t* d_idx) {
-    if (etune_status st = etune_cu_score(c, p, f, d_genome, n, d_pred, d_ids)) return st;
-    return etune_cu_topk(c, d_pred, n, k, d_idx);
+    CHECK_PLAN_ARGS(d_genome && d_pred);
+    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+    if (k < 0 || k > n) return fail(ETUNE_ERR_INVALID_ARGUMENT, "need 0 <= k <= n");
+    if (k > 0 && !d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null index buffer");
+    if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
+    CompiledScore* cs = nullptr;
+    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    return score_select_local(c, p, f, cs, d_genome, n, k, d_pred, d_ids, d_idx);
+}
+
+etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
+                                           const uint64_t* d_genome, int64_t n, int64_t goff, int64_t k,
+                                           double* d_pred, uint64_t* d_ids, int64_t* d_idx, double* d_sc) {
+    CHECK_PLAN_ARGS(d_pred && (n == 0 || d_genome));
+    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+    if (k < 0 || goff < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "negative size");
+    if (k == 0) return ETUNE_OK;
+    if (!d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
+    if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "shard >= 2^31");
+    CompiledScore* cs = nullptr;
+    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    ShardBufs sb;
+    if (etune_status st = shard_buffers(c, k, &sb)) return st;
+    const int64_t kl = std::min(k, n);
+    if (etune_status st = score_select_local(c, p, f, cs, d_genome, n, kl, d_pred, d_ids, sb.lidx)) return st;
+    return shard_merge(c, d_pred, kl, k, goff, sb, d_idx, d_sc);
+}
+
+etune_status etune_cu_profile_score(etune_cu_ctx* c, int on, double* score_ms, double* select_ms,
+                                    int64_t* launches) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    double ms = 0.0, sel = 0.0;
+    if (c->prof_used) {
+        CU(cudaStreamSynchronize(c->stream));
+        for (size_t i = 0; i < c->prof_used; ++i) {
+            float e = 0.f, f = 0.f;
+            CU(cudaEventElapsedTime(&e, c->prof_ev[i][0], c->prof_ev[i][1]));
+            CU(cudaEventElapsedTime(&f, c->prof_ev[i][1], c->prof_ev[i][2]));
+            ms += e;
+            sel += f;
+        }
+    }
+    if (score_ms) *score_ms = ms;
+    if (select_ms) *select_ms = sel;
+    if (launches) *launches = int64_t(c->prof_used);
+    c->prof_used = 0;
+    c->prof_on = on != 0;
+    return ETUNE_OK;
 }
 
 etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
@@ -949,50 +1140,15 @@ etune_status etune_cu_topk_sharded(etune_cu_ctx* c, const double* d_score, int64
     if (n < 0 || k < 0 || goff < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "negative size");
     if (k == 0) return ETUNE_OK;
     if (!d_idx || (n > 0 && !d_score)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
-    const int W = c->comm ? c->nranks : 1;
+    ShardBufs sb;
+    if (etune_status st = shard_buffers(c, k, &sb)) return st;
     const int64_t kl = std::min(k, n);
-    // records: [k local scores | k local gidx | W*k gathered scores | W*k gathered gidx | k positions]
-    const size_t need = size_t(k) * 16 * (1 + size_t(W)) + size_t(k) * 8 + 1024;
-    if (c->shard_bytes < need) {
-        if (c->shard) {
-            CU(cudaStreamSynchronize(c->stream));
-            CU(cudaFree(c->shard));
-            c->shard = nullptr;
-            c->shard_bytes = 0;
-        }
-        CU(cudaMalloc(&c->shard, need));
-        c->shard_bytes = need;
-    }
-    double* ls = static_cast<double*>(c->shard);
-    int64_t* lg = reinterpret_cast<int64_t*>(ls + k);
-    double* gs = reinterpret_cast<double*>(lg + k);
-    int64_t* gg = reinterpret_cast<int64_t*>(gs + size_t(W) * k);
-    int64_t* pos = gg + size_t(W) * k;
-    int64_t* lidx = pos;  // local selection reuses the position buffer
     if (kl > 0) {
         if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "shard >= 2^31");
         if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
-        CU(launch_topk(c->lc(), d_score, n, kl, lidx, c->scratch));
+        CU(launch_topk(c->lc(), d_score, n, kl, sb.lidx, c->scratch));
     }
-    CU(launch_pack_records(c->lc(), d_score, lidx, kl, k, goff, ls, lg));
-    if (W > 1) {
-        ncclResult_t r = ncclGroupStart();
-        if (r == ncclSuccess) r = ncclAllGather(ls, gs, size_t(k), ncclFloat64, c->comm, c->stream);
-        if (r == ncclSuccess) r = ncclAllGather(lg, gg, size_t(k), ncclInt64, c->comm, c->stream);
-        const ncclResult_t r2 = ncclGroupEnd();
-        if (r != ncclSuccess || r2 != ncclSuccess)
-            return fail(ETUNE_ERR_CUDA, std::string("ncclAllGather: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
-    } else {
-        gs = ls;
-        gg = lg;
-    }
-    // shards are contiguous and ascending by rank, each list sorted by (score, gidx):
-    // (score, position) order over the rank-major concatenation == (score, gidx) order
-    const int64_t tot = int64_t(W) * k;
-    if (etune_status st = ensure_scratch(c, topk_scratch_bytes(tot))) return st;
-    CU(launch_topk(c->lc(), gs, tot, k, pos, c->scratch));
-    CU(launch_gather_records(c->lc(), gs, gg, pos, k, d_idx, d_sc));
-    return ETUNE_OK;
+    return shard_merge(c, d_score, kl, k, goff, sb, d_idx, d_sc);
 }
 
 etune_status etune_cu_broadcast(etune_cu_ctx* c, void* d_buf, int64_t bytes, int root) {

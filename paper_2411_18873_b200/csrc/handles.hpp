@@ -5,10 +5,13 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <array>
 #include <atomic>
 #include <map>
 #include <memory>
 #include <mutex>
+#include <utility>
+#include <vector>
 
 #include "forest.hpp"
 #include "kernels.hpp"
@@ -33,6 +36,13 @@ struct etune_cu_ctx {
     int nranks = 1, rank = 0;
     void* shard = nullptr;  // sharded-selection records
     size_t shard_bytes = 0;
+    void* sel = nullptr;    // fused score_select work area (histogram, bucket lists)
+    size_t sel_bytes = 0;
+    bool sel_dirty = false; // a score_select sequence did not complete: re-zero first
+    // optional device timing of the score kernel inside score_select (bench / profiling)
+    bool prof_on = false;
+    std::vector<std::array<cudaEvent_t, 3>> prof_ev;  // before score, after score, after select
+    size_t prof_used = 0;
     // *_host pipelines: copy-in / copy-out streams and per-buffer events
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
@@ -58,6 +68,8 @@ struct CompiledScore {
     int mask_bits = 32;
     int per_sm = 1;           // resident CTAs per SM (queried once at compile time)
     std::shared_ptr<etune_b200::ForestParams> params;  // tree records, passed by value to the kernel
+    uint64_t sel_kmin = 0;    // fused selection buckets: order key of the lowest possible
+    uint32_t sel_shift = 0;   // prediction, and the key bits one bucket spans
     etune_b200::ScoreStats stats;
 };
 

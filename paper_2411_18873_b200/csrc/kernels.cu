@@ -19,6 +19,7 @@
 
 #include "etune_internal.hpp"
 #include "kernels.hpp"
+#include "pdl.cuh"
 #include "score_core.hpp"
 
 namespace etune_b200 {
@@ -449,15 +450,29 @@ __global__ void __launch_bounds__(kThreads) score_walk_kernel(const uint8_t* __r
 // One candidate per thread per iteration; the whole compiled forest lives in smem.
 constexpr int kScoreThreads = 512;
 
+// Bucket of a prediction for the fused selection (SelHist in kernels.hpp): monotone in
+// the (score) order, so every key of a lower bucket is smaller than every key above it.
+__device__ __forceinline__ uint32_t sel_bin(double p, const SelHist& s) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(p));
+    const uint64_t key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+    if (key < s.kmin) return 0u;
+    const uint64_t d = (key - s.kmin) >> s.shift;
+    return d < uint64_t(kSelBins - 1) ? uint32_t(d) : uint32_t(kSelBins - 1);
+}
+
 template <typename M>
 __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
                                                                 const uint64_t* __restrict__ genome, int64_t n,
                                                                 double* __restrict__ pred,
-                                                                uint64_t* __restrict__ ids,
+                                                                uint64_t* __restrict__ ids, const SelHist sel,
                                                                 const __grid_constant__ ForestParams fp) {
     extern __shared__ int4 smem[];
-    stage(gblob, bytes, smem);
+    __shared__ uint32_t shist[kSelBins];
+    if (sel.hist)
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) shist[i] = 0u;
+    stage(gblob, bytes, smem);  // read-only blob: overlaps the previous kernel's tail (PDL)
     __syncthreads();
+    pdl_wait();
     const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
     const ScoreHdr& H = *reinterpret_cast<const ScoreHdr*>(S);
     const int64_t* divk = at<int64_t>(S, H.off_divk);
@@ -466,7 +481,9 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
         const CandClasses cc = candidate_classes(S, H, __ldg(genome + i));
         const double sum = (sizeof(M) == 4 && H.npairs > 0) ? forest_sum_pairs(S, H, fp.pair, cc.c)
                                                             : forest_sum<M>(S, H, fp.rec, cc.c);
-        pred[i] = finish_prediction(H, sum);
+        const double p = finish_prediction(H, sum);
+        pred[i] = p;
+        if (sel.hist) atomicAdd(&shist[sel_bin(p, sel)], 1u);
         if (ids) {
             Knobs c;
             c.r[0] = cc.r[0];
@@ -476,6 +493,13 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
             c.unroll = 1u << cc.x.u;
             c.vec = 1u << cc.x.v;
             ids[i] = candidate_hash(prefix, c);
+        }
+    }
+    if (sel.hist) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) {
+            const uint32_t v = shist[i];
+            if (v) atomicAdd(sel.hist + i, v);
         }
     }
 }
@@ -586,13 +610,15 @@ cudaError_t score_occupancy_t(uint32_t bytes, int* per_sm) {
 
 template <typename M>
 cudaError_t launch_score_t(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
-                           int64_t n, double* d_pred, uint64_t* d_ids, const ForestParams& fp, int per_sm) {
+                           int64_t n, double* d_pred, uint64_t* d_ids, const ForestParams& fp, int per_sm,
+                           const SelHist& sel) {
     const int64_t want = (n + kScoreThreads - 1) / kScoreThreads;
     const int64_t cap = int64_t(c.sm_count) * per_sm;
     const int grid = int(want < cap ? want : cap);
-    score_kernel<M><<<grid, kScoreThreads, bytes, c.stream>>>(d_score, bytes, d_genome, n, d_pred, d_ids, fp);
+    const cudaError_t e = launch_pdl(score_kernel<M>, dim3(grid), dim3(kScoreThreads), bytes, c.stream, d_score,
+                                     bytes, d_genome, n, d_pred, d_ids, sel, fp);
     note_launches(1);
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t score_occupancy(int mask_bits, uint32_t bytes, int* per_sm) {
@@ -601,10 +627,17 @@ cudaError_t score_occupancy(int mask_bits, uint32_t bytes, int* per_sm) {
 
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t bytes, const uint64_t* d_genome,
                          int64_t n, double* d_pred, uint64_t* d_ids, int mask_bits, const ForestParams& fp,
-                         int per_sm) {
+                         int per_sm, const SelHist& sel) {
     if (n <= 0) return cudaSuccess;
-    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm)
-                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm);
+    return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm, sel)
+                           : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm, sel);
+}
+
+int score_static_smem() {
+    cudaFuncAttributes a{}, b{};
+    if (cudaFuncGetAttributes(&a, score_kernel<uint32_t>) != cudaSuccess) return kSelBins * 4;
+    if (cudaFuncGetAttributes(&b, score_kernel<uint64_t>) != cudaSuccess) return kSelBins * 4;
+    return int(a.sharedSizeBytes > b.sharedSizeBytes ? a.sharedSizeBytes : b.sharedSizeBytes);
 }
 
 cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,

@@ -38,11 +38,32 @@ cudaError_t launch_sim_measure(const LaunchCtx& c, const uint8_t* d_plan, uint32
                                int64_t* d_iters);
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                             const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
+// Fused selection (score_select): the score kernel also counts every prediction into
+// kSelBins buckets of its order-preserving key.  The bucket function is monotone
+// (keys below kmin -> 0, above the range -> last bucket), so it is exact for any
+// bounds; the forest's leaf-value bounds only decide how finely the buckets resolve.
+constexpr int kSelBins = 1024;
+constexpr int kSelMaxK = 4096;  // one-CTA final sort bound
+struct SelHist {
+    uint32_t* hist;  // kSelBins global counters (null: no histogram)
+    uint64_t kmin;
+    uint32_t shift;
+};
 // resident CTAs per SM of the compiled score kernel for a blob size (sets the smem ceiling)
 cudaError_t score_occupancy(int mask_bits, uint32_t bytes, int* per_sm);
+// static shared memory the score kernel holds besides the compiled blob
+int score_static_smem();
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
                          const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
-                         int mask_bits, const ForestParams& fp, int per_sm);
+                         int mask_bits, const ForestParams& fp, int per_sm, const SelHist& sel = SelHist{});
+// Selection from the histogram the score kernel filled: filter (keys below the k-th
+// key's bucket + the bucket itself) -> one-CTA radix select inside the bucket and
+// (key, index) sort of the k.  Leaves the histogram zeroed for the next call.
+// Scratch from select_scratch_bytes(n, k); zero it once (cudaMemset) after allocation.
+size_t select_scratch_bytes(int64_t n, int64_t k);
+uint32_t* select_hist(void* d_sel);
+cudaError_t launch_select(const LaunchCtx& c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx,
+                          void* d_sel, const SelHist& sel);
 // General path: features + reference tree walk (any forest the reference can train).
 cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,
                               uint32_t pred_bytes, const uint64_t* d_genome, int64_t n, double* d_out,

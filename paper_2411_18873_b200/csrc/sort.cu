@@ -20,6 +20,7 @@
 #include <mutex>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace etune_b200 {
 
@@ -463,6 +464,416 @@ __global__ void widen_kernel(const uint32_t* __restrict__ vals, int64_t k, int64
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// --------------------------------------------- fused selection (score_select)
+// The score kernel has counted every prediction into kSelBins monotone buckets
+// (kernels.cu sel_bin).  Bucket d* holds the k-th key: every key of a lower bucket
+// is selected, the bucket itself is resolved exactly by one CTA.
+struct SelWork {
+    unsigned int hist[kSelBins];
+    unsigned int nL, nB;  // appended below-bucket / in-bucket pairs
+    unsigned int pad[62];
+};
+constexpr int kSelT = 512;          // filter CTA
+constexpr int kFinT = 1024;         // finish CTA
+constexpr int kSelCacheB = 8192;    // in-bucket pairs cached in the finish CTA's smem
+
+struct SelLayout {
+    SelWork* w;
+    uint64_t* lk;  // [kSelMaxK]
+    uint32_t* li;
+    uint64_t* bk;  // [n]
+    uint32_t* bi;
+};
+
+__host__ __device__ inline size_t sel_al(size_t x) { return (x + 255) & ~size_t(255); }
+
+SelLayout sel_layout(void* base, int64_t n) {
+    char* p = static_cast<char*>(base);
+    SelLayout L;
+    L.w = reinterpret_cast<SelWork*>(p);
+    p += sel_al(sizeof(SelWork));
+    L.lk = reinterpret_cast<uint64_t*>(p);
+    p += sel_al(8 * size_t(kSelMaxK));
+    L.li = reinterpret_cast<uint32_t*>(p);
+    p += sel_al(4 * size_t(kSelMaxK));
+    L.bk = reinterpret_cast<uint64_t*>(p);
+    p += sel_al(8 * size_t(n));
+    L.bi = reinterpret_cast<uint32_t*>(p);
+    return L;
+}
+
+// Warp-aggregated append of (key, index) to list (ck, ci) under counter *cnt.
+__device__ __forceinline__ void warp_append(bool take, uint64_t key, uint32_t idx, unsigned int* cnt,
+                                            uint64_t* ck, uint32_t* ci) {
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(cnt, unsigned(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (take) {
+        const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+        ck[pos] = key;
+        ci[pos] = idx;
+    }
+}
+
+// Every CTA derives the same d* (the bucket holding rank k) from the global histogram,
+// then streams its contiguous chunk of the scores.
+__global__ void __launch_bounds__(kSelT) sel_filter_kernel(const double* __restrict__ score, int64_t n, int64_t k,
+                                                           SelLayout L, const SelHist sel) {
+    __shared__ unsigned int scanbuf[72];
+    __shared__ unsigned int s_d;
+    const int tid = threadIdx.x;
+    pdl_wait();
+    static_assert(kSelBins == 2 * kSelT, "two bins per thread");
+    const unsigned h0 = L.w->hist[2 * tid], h1 = L.w->hist[2 * tid + 1];
+    const unsigned mine = h0 + h1;
+    unsigned x = mine;
+    for (int s = 1; s < 32; s <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, s);
+        if ((tid & 31) >= s) x += y;
+    }
+    unsigned btot;
+    const unsigned run = warp_prefix(__shfl_sync(0xffffffffu, x, 31), scanbuf, &btot) + x - mine;  // exclusive
+    const unsigned kk = unsigned(k);
+    if (run < kk && run + h0 >= kk) s_d = unsigned(2 * tid);
+    else if (run + h0 < kk && run + mine >= kk) s_d = unsigned(2 * tid + 1);
+    __syncthreads();
+    const unsigned d = s_d;
+    const int G = gridDim.x, b = blockIdx.x;
+    const int64_t chunk = ((n + G - 1) / G + 31) & ~int64_t(31);
+    const int64_t lo = int64_t(b) * chunk;
+    const int64_t hi = lo + chunk < n ? lo + chunk : n;
+    for (int64_t j0 = lo; j0 < hi; j0 += blockDim.x) {
+        const int64_t j = j0 + tid;
+        uint64_t key = 0;
+        unsigned bin = kSelBins;
+        if (j < hi) {
+            const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(score[j]));
+            key = (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
+            if (key < sel.kmin) {
+                bin = 0u;
+            } else {
+                const uint64_t q = (key - sel.kmin) >> sel.shift;
+                bin = q < uint64_t(kSelBins - 1) ? unsigned(q) : unsigned(kSelBins - 1);
+            }
+        }
+        warp_append(bin < d, key, uint32_t(j), &L.w->nL, L.lk, L.li);
+        warp_append(bin == d, key, uint32_t(j), &L.w->nB, L.bk, L.bi);
+    }
+}
+
+// Candidate set C = below-bucket list ++ in-bucket list.  When it is small (the usual
+// case) every element's rank in C under (key, index) is counted directly: CTA b owns
+// items [32b, 32b+32) (one per lane), its 8 warps split C, and out[rank] = index for
+// rank < k.  O(|C|^2) compares spread over the whole GPU: |C| = 4096 is 16.7 M compares
+// (~2 us); larger sets (heavy ties spilling the bucket) take sel_finish_kernel.
+constexpr int kRankT = 256;
+constexpr int kRankChunk = 1024;
+constexpr unsigned kRankCap = 8192;
+
+__device__ __forceinline__ ulonglong2 cand_at(const SelLayout& L, unsigned nL, unsigned t) {
+    return t < nL ? make_ulonglong2(L.lk[t], L.li[t]) : make_ulonglong2(L.bk[t - nL], L.bi[t - nL]);
+}
+
+__global__ void __launch_bounds__(kRankT) sel_rank_kernel(int64_t k, SelLayout L, int64_t* __restrict__ out) {
+    __shared__ ulonglong2 rec[kRankChunk];
+    __shared__ unsigned part[kRankT / 32][32];
+    pdl_wait();
+    const unsigned nL = L.w->nL, nC = nL + L.w->nB;
+    if (nC > kRankCap) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kW = kRankT / 32;
+    for (unsigned ib = blockIdx.x; ib * 32u < nC; ib += gridDim.x) {
+        const unsigned i = ib * 32u + lane;
+        const ulonglong2 me = i < nC ? cand_at(L, nL, i) : make_ulonglong2(~0ull, ~0ull);
+        unsigned cnt = 0;
+        for (unsigned j0 = 0; j0 < nC; j0 += kRankChunk) {
+            const unsigned m = nC - j0 < unsigned(kRankChunk) ? nC - j0 : unsigned(kRankChunk);
+            __syncthreads();
+            for (unsigned t = tid; t < m; t += kRankT) rec[t] = cand_at(L, nL, j0 + t);
+            __syncthreads();
+            const unsigned per = (m + kW - 1) / kW;
+            const unsigned a = warp * per, b = a + per < m ? a + per : m;
+#pragma unroll 4
+            for (unsigned j = a; j < b; ++j) {
+                const ulonglong2 r = rec[j];
+                cnt += (r.x < me.x) || (r.x == me.x && r.y < me.y);
+            }
+        }
+        part[warp][lane] = cnt;
+        __syncthreads();
+        if (warp == 0 && i < nC) {
+            unsigned rank = 0;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) rank += part[w][lane];
+            if (rank < unsigned(k)) out[rank] = int64_t(me.y);
+        }
+    }
+}
+
+// Block (1024 threads) pick of the bin holding 1-based rank `rem` among nb <= 2048
+// counters; result in s_pick = {bin, rank inside the bin}.  Ends with a barrier.
+__device__ __forceinline__ void block_pick(const unsigned* h, int nb, unsigned rem, unsigned* scanbuf,
+                                           unsigned* s_pick) {
+    const int tid = threadIdx.x;
+    const int per = (nb + blockDim.x - 1) / blockDim.x;
+    unsigned mine = 0;
+    for (int q = 0; q < per; ++q) {
+        const int i = tid * per + q;
+        if (i < nb) mine += h[i];
+    }
+    unsigned x = mine;
+    for (int s = 1; s < 32; s <<= 1) {
+        const unsigned y = __shfl_up_sync(0xffffffffu, x, s);
+        if ((tid & 31) >= s) x += y;
+    }
+    unsigned btot;
+    unsigned run = warp_prefix(__shfl_sync(0xffffffffu, x, 31), scanbuf, &btot) + x - mine;
+    for (int q = 0; q < per; ++q) {
+        const int i = tid * per + q;
+        if (i < nb) {
+            const unsigned c = h[i];
+            if (run < rem && run + c >= rem) {
+                s_pick[0] = unsigned(i);
+                s_pick[1] = rem - run;
+            }
+            run += c;
+        }
+    }
+    __syncthreads();
+}
+
+// One CTA: exact (key, index) rank-`rem` element inside bucket d*, then the k pairs
+// (all below-bucket pairs + the selected in-bucket ones) sorted by (key, index).
+__global__ void __launch_bounds__(kFinT, 1) sel_finish_kernel(int64_t k, SelLayout L, int64_t* __restrict__ out) {
+    extern __shared__ unsigned long long fsm[];
+    unsigned long long* xk = fsm;                                    // [kSelMaxK]
+    unsigned int* xi = reinterpret_cast<unsigned int*>(xk + kSelMaxK);  // [kSelMaxK]
+    unsigned long long* ck = reinterpret_cast<unsigned long long*>(xi + kSelMaxK);  // [kSelCacheB]
+    unsigned int* ci = reinterpret_cast<unsigned int*>(ck + kSelCacheB);            // [kSelCacheB]
+    __shared__ unsigned int h[kBins];
+    __shared__ unsigned int red[32];
+    __shared__ unsigned int scanbuf[72];
+    __shared__ unsigned int s_pick[2];
+    __shared__ unsigned int s_cnt;
+    __shared__ unsigned long long ra[32], ro[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    pdl_wait();
+    const unsigned nL = L.w->nL, nB = L.w->nB;
+    const unsigned K = unsigned(k);
+    if (nL + nB <= kRankCap) {  // sel_rank_kernel wrote the result: only reset the work area
+        for (int i = tid; i < kSelBins; i += blockDim.x) L.w->hist[i] = 0u;
+        if (tid == 0) {
+            L.w->nL = 0u;
+            L.w->nB = 0u;
+        }
+        return;
+    }
+    const bool cached = nB <= unsigned(kSelCacheB);
+    if (cached)
+        for (unsigned j = tid; j < nB; j += blockDim.x) {
+            ck[j] = L.bk[j];
+            ci[j] = L.bi[j];
+        }
+    const unsigned long long* BK = cached ? ck : reinterpret_cast<const unsigned long long*>(L.bk);
+    const unsigned int* BI = cached ? ci : L.bi;
+    const unsigned nBr = (nB + blockDim.x - 1) / blockDim.x * blockDim.x;
+
+    // ---- exact key T of in-bucket rank rem (MSB-first radix select over the varying bits)
+    uint64_t a = ~0ull, o = 0ull;
+    for (unsigned j = tid; j < nB; j += blockDim.x) {
+        a &= BK[j];
+        o |= BK[j];
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        a &= __shfl_xor_sync(0xffffffffu, a, s);
+        o |= __shfl_xor_sync(0xffffffffu, o, s);
+    }
+    if (lane == 0) {
+        ra[warp] = a;
+        ro[warp] = o;
+    }
+    __syncthreads();
+    for (int i = 0; i < nw; ++i) {
+        a &= ra[i];
+        o |= ro[i];
+    }
+    uint64_t prefix = a;
+    unsigned rem = K - nL;  // >= 1: bucket d* holds rank K
+    int bit = (a ^ o) ? 64 - __clzll(static_cast<long long>(a ^ o)) : 0;
+    while (bit > 0) {
+        const int width = bit >= 11 ? 11 : bit;
+        const int sh = bit - width;
+        const uint64_t himask = bit >= 64 ? 0ull : (~0ull << bit);
+        for (int i = tid; i < kBins; i += blockDim.x) h[i] = 0u;
+        __syncthreads();
+        for (unsigned j = tid; j < nBr; j += blockDim.x) {
+            bool v = false;
+            unsigned dg = 0;
+            if (j < nB) {
+                const uint64_t key = BK[j];
+                v = (key & himask) == (prefix & himask);
+                dg = unsigned(key >> sh) & ((1u << width) - 1u);
+            }
+            agg_inc(h, dg, v);
+        }
+        __syncthreads();
+        block_pick(h, 1 << width, rem, scanbuf, s_pick);
+        prefix = (prefix & himask) | (uint64_t(s_pick[0]) << sh);
+        rem = s_pick[1];
+        bit = sh;
+        __syncthreads();
+    }
+    const uint64_t T = prefix;
+    const unsigned need = rem;  // keys == T to take, lowest index first
+    unsigned eq = 0;
+    for (unsigned j = tid; j < nB; j += blockDim.x) eq += BK[j] == T;
+    eq = block_sum(eq, red);
+    // ---- ties at T: the need-th smallest index among them (indices are unique)
+    unsigned istar = 0xffffffffu;
+    if (eq > need) {
+        unsigned ia = ~0u, io = 0u;
+        for (unsigned j = tid; j < nB; j += blockDim.x)
+            if (BK[j] == T) {
+                ia &= BI[j];
+                io |= BI[j];
+            }
+        for (int s = 16; s > 0; s >>= 1) {
+            ia &= __shfl_xor_sync(0xffffffffu, ia, s);
+            io |= __shfl_xor_sync(0xffffffffu, io, s);
+        }
+        __syncthreads();
+        if (lane == 0) {
+            ra[warp] = ia;
+            ro[warp] = io;
+        }
+        __syncthreads();
+        for (int i = 0; i < nw; ++i) {
+            ia &= unsigned(ra[i]);
+            io |= unsigned(ro[i]);
+        }
+        unsigned ip = ia, irem = need;
+        int ib = (ia ^ io) ? 32 - __clz(int(ia ^ io)) : 0;
+        while (ib > 0) {
+            const int width = ib >= 11 ? 11 : ib;
+            const int sh = ib - width;
+            const unsigned himask = ib >= 32 ? 0u : (~0u << ib);
+            for (int i = tid; i < kBins; i += blockDim.x) h[i] = 0u;
+            __syncthreads();
+            for (unsigned j = tid; j < nBr; j += blockDim.x) {
+                bool v = false;
+                unsigned dg = 0;
+                if (j < nB && BK[j] == T) {
+                    const unsigned id = BI[j];
+                    v = (id & himask) == (ip & himask);
+                    dg = (id >> sh) & ((1u << width) - 1u);
+                }
+                agg_inc(h, dg, v);
+            }
+            __syncthreads();
+            block_pick(h, 1 << width, irem, scanbuf, s_pick);
+            ip = (ip & himask) | (s_pick[0] << sh);
+            irem = s_pick[1];
+            ib = sh;
+            __syncthreads();
+        }
+        istar = ip;
+    }
+    // ---- gather the k pairs: all below-bucket pairs, then the selected in-bucket ones
+    for (unsigned j = tid; j < nL; j += blockDim.x) {
+        xk[j] = L.lk[j];
+        xi[j] = L.li[j];
+    }
+    if (tid == 0) s_cnt = nL;
+    __syncthreads();
+    for (unsigned j = tid; j < nBr; j += blockDim.x) {
+        bool take = false;
+        uint64_t key = 0;
+        unsigned id = 0;
+        if (j < nB) {
+            key = BK[j];
+            id = BI[j];
+            take = key < T || (key == T && id <= istar);
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(&s_cnt, unsigned(__popc(m)));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (take) {
+                const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
+                xk[pos] = key;
+                xi[pos] = id;
+            }
+        }
+    }
+    __syncthreads();
+    // ---- (key, index) sort of the K pairs
+    int P = 1;
+    while (P < int(K)) P <<= 1;
+    if (P <= int(blockDim.x)) {
+        unsigned long long kk = tid < int(K) ? xk[tid] : ~0ull;
+        unsigned ii = tid < int(K) ? xi[tid] : 0xffffffffu;
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                const bool up = (tid & size) == 0;
+                const bool low = (tid & stride) == 0;
+                unsigned long long pk;
+                unsigned pi;
+                if (stride >= 32) {
+                    __syncthreads();
+                    xk[tid] = kk;
+                    xi[tid] = ii;
+                    __syncthreads();
+                    pk = xk[tid ^ stride];
+                    pi = xi[tid ^ stride];
+                } else {
+                    pk = __shfl_xor_sync(0xffffffffu, kk, stride);
+                    pi = __shfl_xor_sync(0xffffffffu, ii, stride);
+                }
+                if (tid < P) cmpx(kk, ii, pk, pi, up == low);
+            }
+        }
+        if (tid < int(K)) out[tid] = ii;
+    } else {
+        for (int i = int(K) + tid; i < P; i += blockDim.x) {
+            xk[i] = ~0ull;
+            xi[i] = 0xffffffffu;
+        }
+        __syncthreads();
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int i = tid; i < P; i += blockDim.x) {
+                    const int j = i ^ stride;
+                    if (j > i) {
+                        const bool up = (i & size) == 0;
+                        const bool gt = (xk[i] > xk[j]) || (xk[i] == xk[j] && xi[i] > xi[j]);
+                        if (gt == up) {
+                            const unsigned long long tk = xk[i];
+                            xk[i] = xk[j];
+                            xk[j] = tk;
+                            const unsigned ti = xi[i];
+                            xi[i] = xi[j];
+                            xi[j] = ti;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int i = tid; i < int(K); i += blockDim.x) out[i] = xi[i];
+    }
+    // ---- leave the work area clean for the next score_select
+    for (int i = tid; i < kSelBins; i += blockDim.x) L.w->hist[i] = 0u;
+    if (tid == 0) {
+        L.w->nL = 0u;
+        L.w->nB = 0u;
+    }
+}
 }  // namespace
 
 size_t sort_pairs_scratch_bytes(int64_t n) {
@@ -570,6 +981,38 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
     widen_kernel<<<tg, 256, 0, c.stream>>>(sv[cur], k, d_idx);
     note_launches(1);
     return cudaGetLastError();
+}
+
+size_t select_scratch_bytes(int64_t n, int64_t k) {
+    (void)k;
+    return sel_al(sizeof(SelWork)) + sel_al(8 * size_t(kSelMaxK)) + sel_al(4 * size_t(kSelMaxK)) +
+           sel_al(8 * size_t(n)) + sel_al(4 * size_t(n));
+}
+
+uint32_t* select_hist(void* d_sel) { return reinterpret_cast<SelWork*>(d_sel)->hist; }
+
+cudaError_t launch_select(const LaunchCtx& c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx,
+                          void* d_sel, const SelHist& sel) {
+    if (n <= 0 || k <= 0) return cudaSuccess;
+    if (k > kSelMaxK || k > n) return cudaErrorInvalidValue;
+    const SelLayout L = sel_layout(d_sel, n);
+    int64_t G = 2 * int64_t(c.sm_count);
+    const int64_t want = (n + kSelT - 1) / kSelT;
+    if (want < G) G = want;
+    cudaError_t e = launch_pdl(sel_filter_kernel, dim3(unsigned(G)), dim3(kSelT), 0, c.stream, d_score, n, k, L, sel);
+    if (e != cudaSuccess) return e;
+    const size_t smem = size_t(kSelMaxK) * 12 + size_t(kSelCacheB) * 12;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [&] {
+        attr = cudaFuncSetAttribute(sel_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    });
+    if (attr != cudaSuccess) return attr;
+    e = launch_pdl(sel_rank_kernel, dim3(2 * c.sm_count), dim3(kRankT), 0, c.stream, k, L, d_idx);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(sel_finish_kernel, dim3(1), dim3(kFinT), smem, c.stream, k, L, d_idx);
+    note_launches(3);
+    return e;
 }
 
 }  // namespace etune_b200

@@ -1,0 +1,144 @@
+"""GPU parity of the fused score + keep-the-best (etune_cu_score_select): the score
+kernel buckets every prediction, the selection resolves the k-th key's bucket.  The
+selected indices must equal the oracle's (prediction asc, index asc) top-k of the
+oracle's predictions, bit for bit, for any population: distinct scores, heavy ties
+(bucket larger than the finish CTA's shared-memory cache), every score equal, k at
+the bucket edges, repeated calls (the work area resets itself)."""
+import numpy as np
+import pytest
+
+from etune_testlib import FlatForest, parse_op
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+OP = "conv:1,56,56,64,64,3,1,1"
+MODEL = "c2_r50_conv3x3"
+
+
+@pytest.fixture(scope="module")
+def capi():
+    from paper_2411_18873_b200 import capi as c
+    return c
+
+
+@pytest.fixture(scope="module")
+def ctx(capi):
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    return capi.Context(0)
+
+
+@pytest.fixture(scope="module")
+def setup(golden, oracle, ctx, capi):
+    k = f"{MODEL}/model/"
+    flat = FlatForest(golden[k + "feature"], golden[k + "threshold"], golden[k + "left"], golden[k + "right"],
+                      golden[k + "value"], golden[k + "offsets"], float(golden[k + "base_score"][0]),
+                      float(golden[k + "learning_rate"][0]))
+    op = parse_op(OP)
+    plan = capi.Plan(ctx, op)
+    forest = capi.Forest.from_flat(ctx, flat)
+    parents, _ = oracle.sample_random(op, 1024, 42)
+    return op, plan, forest, flat, parents
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_select(capi, ctx, plan, forest, sched, k):
+    g = plan.encode(dev(sched))
+    n = len(sched)
+    pred = torch.empty(n, dtype=torch.float64, device="cuda")
+    idx = torch.empty(max(k, 1), dtype=torch.int64, device="cuda")
+    forest.score_select(plan, g, k, pred, idx)
+    ctx.synchronize()
+    return pred.cpu().numpy(), idx.cpu().numpy()[:k]
+
+
+def expect(oracle, op, flat, sched, k):
+    p = oracle.predict(flat, oracle.features(op, sched))
+    return p, oracle.topk(p, k)
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (37, 5), (4096, 4096), (100003, 1024), (1 << 18, 4096), (1 << 18, 1),
+                                 (1 << 18, 1000)])
+def test_score_select_bred_population(oracle, ctx, capi, setup, n, k):
+    op, plan, forest, flat, parents = setup
+    sched = oracle.reproduce(op, parents, n, 7 + n)[0] if n > 1024 else parents[:n]
+    p_ref, want = expect(oracle, op, flat, sched, k)
+    pred, got = run_select(capi, ctx, plan, forest, sched, k)
+    assert (pred.view(np.uint64) == p_ref.view(np.uint64)).all()
+    assert (got == want).all()
+
+
+@pytest.mark.parametrize("distinct,n,k", [(1, 50000, 1024), (3, 30000, 4096), (40, 200000, 3000), (7, 9000, 8)])
+def test_score_select_heavy_ties(oracle, ctx, capi, setup, distinct, n, k):
+    """Few distinct schedules replicated: bucket d* holds whole tie groups (often more
+    pairs than the finish CTA caches), ties resolve by lowest index."""
+    op, plan, forest, flat, parents = setup
+    rng = np.random.default_rng(distinct * 1000 + n)
+    sched = parents[rng.integers(0, distinct, n) if distinct > 1 else np.zeros(n, np.int64)]
+    p_ref, want = expect(oracle, op, flat, sched, k)
+    pred, got = run_select(capi, ctx, plan, forest, sched, k)
+    assert (pred.view(np.uint64) == p_ref.view(np.uint64)).all()
+    assert (got == want).all()
+
+
+def test_score_select_matches_unfused_and_resets(oracle, ctx, capi, setup):
+    """Back-to-back calls on different populations (no host sync between them) equal
+    score + cooperative top-k: the histogram and list counters reset in-kernel."""
+    op, plan, forest, flat, parents = setup
+    pops = [oracle.reproduce(op, parents, 60000, s)[0] for s in (1, 2, 3)]
+    gs = [plan.encode(dev(s)) for s in pops]
+    outs = []
+    for g in gs:
+        pred = torch.empty(len(g), dtype=torch.float64, device="cuda")
+        idx = torch.empty(2048, dtype=torch.int64, device="cuda")
+        forest.score_select(plan, g, 2048, pred, idx)
+        outs.append((pred, idx))
+    ctx.synchronize()
+    for (pred, idx), s in zip(outs, pops):
+        ref = capi.topk(ctx, pred, 2048)
+        ctx.synchronize()
+        assert (idx.cpu().numpy() == ref.cpu().numpy()).all()
+        _, want = expect(oracle, op, flat, s, 2048)
+        assert (idx.cpu().numpy() == want).all()
+
+
+def test_score_select_large_k_falls_back(oracle, ctx, capi, setup):
+    op, plan, forest, flat, parents = setup
+    sched = oracle.reproduce(op, parents, 50000, 11)[0]
+    _, want = expect(oracle, op, flat, sched, 10000)
+    _, got = run_select(capi, ctx, plan, forest, sched, 10000)
+    assert (got == want).all()
+
+
+def test_score_select_sharded_single_rank(oracle, ctx, capi, setup):
+    """Shards scored + selected locally, merged (single-rank communicator semantics):
+    per-shard results equal the oracle's shard top-k with global indices."""
+    op, plan, forest, flat, parents = setup
+    sched = oracle.reproduce(op, parents, 120000, 5)[0]
+    p_ref = oracle.predict(flat, oracle.features(op, sched))
+    lo, hi, k = 40000, 120000, 1024
+    g = plan.encode(dev(sched[lo:hi]))
+    pred = torch.empty(hi - lo, dtype=torch.float64, device="cuda")
+    idx = torch.empty(k, dtype=torch.int64, device="cuda")
+    sc = torch.empty(k, dtype=torch.float64, device="cuda")
+    forest.score_select_sharded(plan, g, lo, k, pred, idx, sc)
+    ctx.synchronize()
+    want = lo + oracle.topk(p_ref[lo:hi], k)
+    assert (idx.cpu().numpy() == want).all()
+    assert (sc.cpu().numpy().view(np.uint64) == p_ref[want].view(np.uint64)).all()
+
+
+def test_profile_score_events(oracle, ctx, capi, setup):
+    op, plan, forest, flat, parents = setup
+    sched = oracle.reproduce(op, parents, 1 << 16, 3)[0]
+    g = plan.encode(dev(sched))
+    pred = torch.empty(len(sched), dtype=torch.float64, device="cuda")
+    idx = torch.empty(64, dtype=torch.int64, device="cuda")
+    capi.profile_score(ctx, True)
+    for _ in range(3):
+        forest.score_select(plan, g, 64, pred, idx)
+    ms, sel_ms, cnt = capi.profile_score(ctx, False)
+    assert cnt == 3 and ms > 0.0 and sel_ms > 0.0
