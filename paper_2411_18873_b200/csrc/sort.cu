@@ -471,7 +471,8 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 struct SelWork {
     unsigned int hist[kSelBins];
     unsigned int nL, nB;  // appended below-bucket / in-bucket pairs
-    unsigned int pad[62];
+    unsigned int ticket;  // sel_rank_kernel: CTAs done
+    unsigned int pad[61];
 };
 constexpr int kSelT = 512;          // filter CTA
 constexpr int kFinT = 1024;         // finish CTA
@@ -481,8 +482,10 @@ struct SelLayout {
     SelWork* w;
     uint64_t* lk;  // [kSelMaxK]
     uint32_t* li;
+    uint32_t* lr;  // rank counters of the below-bucket pairs
     uint64_t* bk;  // [n]
     uint32_t* bi;
+    uint32_t* br;  // rank counters of the in-bucket pairs
 };
 
 __host__ __device__ inline size_t sel_al(size_t x) { return (x + 255) & ~size_t(255); }
@@ -496,38 +499,40 @@ SelLayout sel_layout(void* base, int64_t n) {
     p += sel_al(8 * size_t(kSelMaxK));
     L.li = reinterpret_cast<uint32_t*>(p);
     p += sel_al(4 * size_t(kSelMaxK));
+    L.lr = reinterpret_cast<uint32_t*>(p);
+    p += sel_al(4 * size_t(kSelMaxK));
     L.bk = reinterpret_cast<uint64_t*>(p);
     p += sel_al(8 * size_t(n));
     L.bi = reinterpret_cast<uint32_t*>(p);
+    p += sel_al(4 * size_t(n));
+    L.br = reinterpret_cast<uint32_t*>(p);
     return L;
 }
 
-// Warp-aggregated append of (key, index) to list (ck, ci) under counter *cnt.
-__device__ __forceinline__ void warp_append(bool take, uint64_t key, uint32_t idx, unsigned int* cnt,
-                                            uint64_t* ck, uint32_t* ci) {
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (!m) return;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(m) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(cnt, unsigned(__popc(m)));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (take) {
-        const unsigned pos = base + __popc(m & ((1u << lane) - 1u));
-        ck[pos] = key;
-        ci[pos] = idx;
-    }
-}
-
 // Every CTA derives the same d* (the bucket holding rank k) from the global histogram,
-// then streams its contiguous chunk of the scores.
+// then classifies kFiltPer scores per thread (loads issued before the histogram scan,
+// so their latency overlaps it).
+constexpr int kFiltPer = 8;
+
 __global__ void __launch_bounds__(kSelT) sel_filter_kernel(const double* __restrict__ score, int64_t n, int64_t k,
                                                            SelLayout L, const SelHist sel) {
     __shared__ unsigned int scanbuf[72];
     __shared__ unsigned int s_d;
     const int tid = threadIdx.x;
-    pdl_wait();
     static_assert(kSelBins == 2 * kSelT, "two bins per thread");
+    const int64_t span = int64_t(kSelT) * kFiltPer;
+    int64_t base = int64_t(blockIdx.x) * span;
+    double v[kFiltPer];
+#pragma unroll
+    for (int r = 0; r < kFiltPer; ++r) {  // scores are written by the score kernel: after the wait
+        v[r] = 0.0;
+    }
+    pdl_wait();
+#pragma unroll
+    for (int r = 0; r < kFiltPer; ++r) {
+        const int64_t j = base + r * kSelT + tid;
+        if (j < n) v[r] = __ldcg(score + j);
+    }
     const unsigned h0 = L.w->hist[2 * tid], h1 = L.w->hist[2 * tid + 1];
     const unsigned mine = h0 + h1;
     unsigned x = mine;
@@ -542,76 +547,174 @@ __global__ void __launch_bounds__(kSelT) sel_filter_kernel(const double* __restr
     else if (run + h0 < kk && run + mine >= kk) s_d = unsigned(2 * tid + 1);
     __syncthreads();
     const unsigned d = s_d;
-    const int G = gridDim.x, b = blockIdx.x;
-    const int64_t chunk = ((n + G - 1) / G + 31) & ~int64_t(31);
-    const int64_t lo = int64_t(b) * chunk;
-    const int64_t hi = lo + chunk < n ? lo + chunk : n;
-    for (int64_t j0 = lo; j0 < hi; j0 += blockDim.x) {
-        const int64_t j = j0 + tid;
-        uint64_t key = 0;
-        unsigned bin = kSelBins;
-        if (j < hi) {
-            const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(score[j]));
-            key = (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
-            if (key < sel.kmin) {
-                bin = 0u;
-            } else {
-                const uint64_t q = (key - sel.kmin) >> sel.shift;
-                bin = q < uint64_t(kSelBins - 1) ? unsigned(q) : unsigned(kSelBins - 1);
+    __shared__ unsigned s_base[2];
+    for (;;) {
+        // classify; takes are appended CTA-aggregated (one global atomic per list per
+        // CTA), so thousands of tied predictions do not serialise on one counter
+        uint64_t key[kFiltPer];
+        unsigned tl = 0, tb = 0;
+#pragma unroll
+        for (int r = 0; r < kFiltPer; ++r) {
+            const int64_t j = base + r * kSelT + tid;
+            const uint64_t bits = static_cast<uint64_t>(__double_as_longlong(v[r]));
+            key[r] = (bits >> 63) ? ~bits : (bits | 0x8000000000000000ull);
+            unsigned bin = kSelBins;
+            if (j < n) {
+                if (key[r] < sel.kmin) {
+                    bin = 0u;
+                } else {
+                    const uint64_t q = (key[r] - sel.kmin) >> sel.shift;
+                    bin = q < uint64_t(kSelBins - 1) ? unsigned(q) : unsigned(kSelBins - 1);
+                }
+            }
+            tl |= unsigned(bin < d) << r;
+            tb |= unsigned(bin == d) << r;
+        }
+        if (__syncthreads_or(tl | tb)) {
+            const unsigned c = unsigned(__popc(tl)) | (unsigned(__popc(tb)) << 16);
+            unsigned x = c;
+            for (int s = 1; s < 32; s <<= 1) {
+                const unsigned y = __shfl_up_sync(0xffffffffu, x, s);
+                if ((tid & 31) >= s) x += y;
+            }
+            unsigned tot;
+            const unsigned pre = warp_prefix(__shfl_sync(0xffffffffu, x, 31), scanbuf, &tot) + x - c;
+            if (tid == 0) {
+                s_base[0] = (tot & 0xffffu) ? atomicAdd(&L.w->nL, tot & 0xffffu) : 0u;
+                s_base[1] = (tot >> 16) ? atomicAdd(&L.w->nB, tot >> 16) : 0u;
+            }
+            __syncthreads();
+            unsigned pl = s_base[0] + (pre & 0xffffu), pb = s_base[1] + (pre >> 16);
+#pragma unroll
+            for (int r = 0; r < kFiltPer; ++r) {
+                const uint32_t j = uint32_t(base + r * kSelT + tid);
+                if ((tl >> r) & 1u) {
+                    L.lk[pl] = key[r];
+                    L.li[pl] = j;
+                    L.lr[pl] = 0u;  // sel_rank_kernel accumulates into it
+                    ++pl;
+                }
+                if ((tb >> r) & 1u) {
+                    L.bk[pb] = key[r];
+                    L.bi[pb] = j;
+                    L.br[pb] = 0u;
+                    ++pb;
+                }
             }
         }
-        warp_append(bin < d, key, uint32_t(j), &L.w->nL, L.lk, L.li);
-        warp_append(bin == d, key, uint32_t(j), &L.w->nB, L.bk, L.bi);
+        base += int64_t(gridDim.x) * span;
+        if (base >= n) break;
+#pragma unroll
+        for (int r = 0; r < kFiltPer; ++r) {
+            const int64_t j = base + r * kSelT + tid;
+            v[r] = j < n ? __ldcg(score + j) : 0.0;
+        }
     }
 }
 
 // Candidate set C = below-bucket list ++ in-bucket list.  When it is small (the usual
-// case) every element's rank in C under (key, index) is counted directly: CTA b owns
-// items [32b, 32b+32) (one per lane), its 8 warps split C, and out[rank] = index for
-// rank < k.  O(|C|^2) compares spread over the whole GPU: |C| = 4096 is 16.7 M compares
-// (~2 us); larger sets (heavy ties spilling the bucket) take sel_finish_kernel.
-constexpr int kRankT = 256;
-constexpr int kRankChunk = 1024;
+// case) every element's rank in C under (key, index) is counted directly and
+// out[rank] = index for rank < k.  Work units are tiles of kRankI items x kRankJ
+// candidates spread over the whole GPU (each lane holds 4 items, each staged record
+// is one broadcast shared load compared against all 4 by a 96-bit borrow chain);
+// partial ranks go to the per-pair counters (zeroed by the filter) with atomics and the
+// last CTA scatters.  |C| = 4096: 16.7 M compares.  Larger sets (heavy ties spilling
+// the bucket) take sel_finish_kernel.
+constexpr int kRankT = 512;
+constexpr int kRankR = 4;                     // items per lane
+constexpr unsigned kRankI = 32 * kRankR;      // items per tile
+constexpr unsigned kRankJ = 512;              // candidates per tile
 constexpr unsigned kRankCap = 8192;
 
 __device__ __forceinline__ ulonglong2 cand_at(const SelLayout& L, unsigned nL, unsigned t) {
     return t < nL ? make_ulonglong2(L.lk[t], L.li[t]) : make_ulonglong2(L.bk[t - nL], L.bi[t - nL]);
 }
 
+// 0xffffffff when (rk, ri) < (mk, mi) lexicographically, else 0: the borrow out of the
+// 96-bit subtraction, sign-extended (callers subtract it from a counter)
+__device__ __forceinline__ unsigned less96(unsigned long long rk, unsigned ri, unsigned long long mk, unsigned mi) {
+    unsigned b;
+    asm("{\n\t.reg .u32 t;\n\t"
+        "sub.cc.u32 t, %1, %4;\n\t"
+        "subc.cc.u32 t, %2, %5;\n\t"
+        "subc.cc.u32 t, %3, %6;\n\t"
+        "subc.u32 %0, 0, 0;\n\t}"
+        : "=r"(b)
+        : "r"(ri), "r"(unsigned(rk)), "r"(unsigned(rk >> 32)), "r"(mi), "r"(unsigned(mk)), "r"(unsigned(mk >> 32)));
+    return b;
+}
+
 __global__ void __launch_bounds__(kRankT) sel_rank_kernel(int64_t k, SelLayout L, int64_t* __restrict__ out) {
-    __shared__ ulonglong2 rec[kRankChunk];
-    __shared__ unsigned part[kRankT / 32][32];
+    __shared__ ulonglong2 rec[kRankJ];
+    __shared__ unsigned part[kRankT / 32][kRankI];
+    __shared__ unsigned s_last;
     pdl_wait();
     const unsigned nL = L.w->nL, nC = nL + L.w->nB;
     if (nC > kRankCap) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kW = kRankT / 32;
-    for (unsigned ib = blockIdx.x; ib * 32u < nC; ib += gridDim.x) {
-        const unsigned i = ib * 32u + lane;
-        const ulonglong2 me = i < nC ? cand_at(L, nL, i) : make_ulonglong2(~0ull, ~0ull);
-        unsigned cnt = 0;
-        for (unsigned j0 = 0; j0 < nC; j0 += kRankChunk) {
-            const unsigned m = nC - j0 < unsigned(kRankChunk) ? nC - j0 : unsigned(kRankChunk);
-            __syncthreads();
-            for (unsigned t = tid; t < m; t += kRankT) rec[t] = cand_at(L, nL, j0 + t);
-            __syncthreads();
-            const unsigned per = (m + kW - 1) / kW;
-            const unsigned a = warp * per, b = a + per < m ? a + per : m;
-#pragma unroll 4
-            for (unsigned j = a; j < b; ++j) {
-                const ulonglong2 r = rec[j];
-                cnt += (r.x < me.x) || (r.x == me.x && r.y < me.y);
-            }
-        }
-        part[warp][lane] = cnt;
-        __syncthreads();
-        if (warp == 0 && i < nC) {
-            unsigned rank = 0;
+    const unsigned ni = (nC + kRankI - 1) / kRankI, nj = (nC + kRankJ - 1) / kRankJ;
+    for (unsigned u = blockIdx.x; u < ni * nj; u += gridDim.x) {
+        const unsigned ib = u / nj, jb = u % nj;
+        const unsigned j0 = jb * kRankJ;
+        const unsigned m = nC - j0 < kRankJ ? nC - j0 : kRankJ;
+        __syncthreads();  // rec / part reuse
+        for (unsigned t = tid; t < m; t += kRankT) rec[t] = cand_at(L, nL, j0 + t);
+        unsigned long long mk[kRankR];
+        unsigned mi[kRankR], cnt[kRankR];
 #pragma unroll
-            for (int w = 0; w < kW; ++w) rank += part[w][lane];
-            if (rank < unsigned(k)) out[rank] = int64_t(me.y);
+        for (int r = 0; r < kRankR; ++r) {
+            const unsigned i = ib * kRankI + r * 32 + lane;
+            const ulonglong2 me = i < nC ? cand_at(L, nL, i) : make_ulonglong2(~0ull, ~0ull);
+            mk[r] = me.x;
+            mi[r] = unsigned(me.y);
+            cnt[r] = 0;
+        }
+        __syncthreads();
+        const unsigned per = (m + kW - 1) / kW;
+        const unsigned a = warp * per, b = a + per < m ? a + per : m;
+#pragma unroll 2
+        for (unsigned j = a; j < b; ++j) {
+            const ulonglong2 rj = rec[j];
+#pragma unroll
+            for (int r = 0; r < kRankR; ++r) cnt[r] -= less96(rj.x, unsigned(rj.y), mk[r], mi[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < kRankR; ++r) part[warp][r * 32 + lane] = cnt[r];
+        __syncthreads();
+        if (tid < int(kRankI)) {
+            unsigned c = 0;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) c += part[w][tid];
+            const unsigned i = ib * kRankI + tid;
+            if (i < nC && c) atomicAdd(i < nL ? L.lr + i : L.br + (i - nL), c);
         }
     }
+    // the last CTA to finish scatters out[rank] = index for rank < k
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&L.w->ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    constexpr int kB = 8;  // independent loads in flight per thread
+    for (unsigned i0 = 0; i0 < nC; i0 += kB * kRankT) {
+        unsigned rk[kB], id[kB];
+#pragma unroll
+        for (int r = 0; r < kB; ++r) {
+            const unsigned i = i0 + r * kRankT + tid;
+            rk[r] = 0xffffffffu;
+            id[r] = 0;
+            if (i < nC) {
+                rk[r] = __ldcg(i < nL ? L.lr + i : L.br + (i - nL));
+                id[r] = i < nL ? L.li[i] : L.bi[i - nL];
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kB; ++r)
+            if (rk[r] < unsigned(k)) out[rk[r]] = int64_t(id[r]);
+    }
+    if (tid == 0) L.w->ticket = 0u;
 }
 
 // Block (1024 threads) pick of the bin holding 1-based rank `rem` among nb <= 2048
@@ -985,8 +1088,8 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
 
 size_t select_scratch_bytes(int64_t n, int64_t k) {
     (void)k;
-    return sel_al(sizeof(SelWork)) + sel_al(8 * size_t(kSelMaxK)) + sel_al(4 * size_t(kSelMaxK)) +
-           sel_al(8 * size_t(n)) + sel_al(4 * size_t(n));
+    return sel_al(sizeof(SelWork)) + sel_al(8 * size_t(kSelMaxK)) + 2 * sel_al(4 * size_t(kSelMaxK)) +
+           sel_al(8 * size_t(n)) + 2 * sel_al(4 * size_t(n));
 }
 
 uint32_t* select_hist(void* d_sel) { return reinterpret_cast<SelWork*>(d_sel)->hist; }
@@ -996,8 +1099,8 @@ cudaError_t launch_select(const LaunchCtx& c, const double* d_score, int64_t n, 
     if (n <= 0 || k <= 0) return cudaSuccess;
     if (k > kSelMaxK || k > n) return cudaErrorInvalidValue;
     const SelLayout L = sel_layout(d_sel, n);
-    int64_t G = 2 * int64_t(c.sm_count);
-    const int64_t want = (n + kSelT - 1) / kSelT;
+    int64_t G = 4 * int64_t(c.sm_count);
+    const int64_t want = (n + int64_t(kSelT) * kFiltPer - 1) / (int64_t(kSelT) * kFiltPer);
     if (want < G) G = want;
     cudaError_t e = launch_pdl(sel_filter_kernel, dim3(unsigned(G)), dim3(kSelT), 0, c.stream, d_score, n, k, L, sel);
     if (e != cudaSuccess) return e;
