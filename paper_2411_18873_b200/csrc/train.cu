@@ -256,19 +256,31 @@ __global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int 
     }
 }
 
-// One warp per (list, frontier segment): the sequential running sums, 256 elements at
-// a time staged through shared memory (coalesced in, one lane chains, coalesced out).
+// One warp per (list, frontier segment): the sequential running sums, kChunk elements
+// at a time staged through shared memory.  The next chunk's (grad, hess) is copied
+// with cp.async by all lanes BEFORE lane 0 starts chaining the current one, so the
+// global-load latency hides under the FP64 add chain (double buffer); the chain itself
+// loads its smem operands one batch of 8 ahead.
 //   lists 0..15: exclusive prefix at every position (the `run` of cpp 95-121)
 //   list 16:     the node's (grad, hess) totals in sample order (cpp 73-76, 150-155)
 constexpr int kChainWarps = 4;
 constexpr int kChunk = 256;
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int lvl, int only_totals,
                                                                  const double* __restrict__ gl,
                                                                  const double* __restrict__ hl,
                                                                  double* __restrict__ pg, double* __restrict__ ph,
                                                                  TrainCtl* ctl) {
-    __shared__ double ig[kChainWarps][kChunk + 8], ih[kChainWarps][kChunk + 8];
-    __shared__ double og[kChainWarps][kChunk], oh[kChainWarps][kChunk];
+    // prefixes overwrite their operands in place (each operand is in registers by then)
+    __shared__ double ig[kChainWarps][2][kChunk + 8], ih[kChainWarps][2][kChunk + 8];
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     if (nseg <= 0) return;
@@ -284,23 +296,49 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
     double* PH = ph + int64_t(l) * n;
     const bool prefixes = l != kSampleList;
     double rg = 0.0, rh = 0.0;
-    for (int base = s; base < e; base += kChunk) {
-        const int cnt = min(kChunk, e - base);
-        for (int j = lane; j < cnt; j += 32) {
-            ig[w][j] = G[base + j];
-            ih[w][j] = Hh[base + j];
+    if (s < e) {
+        const int cnt0 = min(kChunk, e - s);
+        for (int j = lane; j < cnt0; j += 32) {
+            cp_async8(&ig[w][0][j], G + s + j);
+            cp_async8(&ih[w][0][j], Hh + s + j);
         }
+    }
+    cp_async_commit();
+    int buf = 0;
+    for (int base = s; base < e; base += kChunk, buf ^= 1) {
+        const int cnt = min(kChunk, e - base);
+        const int nb = base + kChunk;
+        if (nb < e) {  // prefetch the next chunk into the other buffer
+            const int cn = min(kChunk, e - nb);
+            for (int j = lane; j < cn; j += 32) {
+                cp_async8(&ig[w][buf ^ 1][j], G + nb + j);
+                cp_async8(&ih[w][buf ^ 1][j], Hh + nb + j);
+            }
+        }
+        cp_async_commit();
+        cp_async_wait_prev();  // the current chunk has landed (for this lane's copies)
         __syncwarp();
         if (lane == 0) {
-            // full batches of 8: the chain only; each prefix lives in its own register until
-            // the batch is stored, so no store waits on (or blocks) the next add
+            double* cg = ig[w][buf];
+            double* ch = ih[w][buf];
+            // full batches of 8: each prefix lives in its own register until the batch is
+            // stored; the next batch's operands are loaded before this batch's adds
             const int full = cnt & ~7;
-            for (int j = 0; j < full; j += 8) {
-                double g[8], h[8], pgv[8], phv[8];
+            double g[8], h[8];
+            if (full) {
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    g[u] = ig[w][j + u];
-                    h[u] = ih[w][j + u];
+                    g[u] = cg[u];
+                    h[u] = ch[u];
+                }
+            }
+            for (int j = 0; j < full; j += 8) {
+                double pgv[8], phv[8], gn[8], hn[8];
+                const int jn = j + 8 < full ? j + 8 : j;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    gn[u] = cg[jn + u];
+                    hn[u] = ch[jn + u];
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -311,27 +349,30 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    og[w][j + u] = pgv[u];
-                    oh[w][j + u] = phv[u];
+                    cg[j + u] = pgv[u];
+                    ch[j + u] = phv[u];
+                    g[u] = gn[u];
+                    h[u] = hn[u];
                 }
             }
             for (int j = full; j < cnt; ++j) {
-                const double g = ig[w][j], h = ih[w][j];
-                og[w][j] = rg;
-                oh[w][j] = rh;
-                rg = __dadd_rn(rg, g);
-                rh = __dadd_rn(rh, h);
+                const double gg = cg[j], hh = ch[j];
+                cg[j] = rg;
+                ch[j] = rh;
+                rg = __dadd_rn(rg, gg);
+                rh = __dadd_rn(rh, hh);
             }
         }
         __syncwarp();
         if (prefixes) {
             for (int j = lane; j < cnt; j += 32) {
-                PG[base + j] = og[w][j];
-                PH[base + j] = oh[w][j];
+                PG[base + j] = ig[w][buf][j];
+                PH[base + j] = ih[w][buf][j];
             }
         }
         __syncwarp();
     }
+    cp_async_wait_all();
     if (lane == 0) {
         if (!prefixes) {
             const int node = ctl->seg_node[b][k];
