@@ -15,6 +15,9 @@
 #include <mutex>
 #include <string>
 #include <vector>
+#include <thread>
+
+#include <sched.h>
 
 #include "forest.hpp"
 #include "kernels.hpp"
@@ -34,6 +37,8 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->breed);
     cudaFree(c->shard);
     cudaFree(c->sel);
+    if (c->hpin) cudaFreeHost(c->hpin);
+    c->pool.reset();
     for (auto& e : c->prof_ev)
         for (cudaEvent_t x : e) cudaEventDestroy(x);
     if (c->h2d) {
@@ -92,6 +97,55 @@ etune_status ensure_scratch(etune_cu_ctx* c, size_t bytes) {
     CU(cudaMalloc(&c->scratch, bytes));
     c->scratch_bytes = bytes;
     return ETUNE_OK;
+}
+
+// Narrow rows [a, b) of the caller's Schedule[] to W-wide fields; false when a field
+// does not fit (negative or >= 2^(8 sizeof W)), in which case the chunk is re-packed wider.
+template <typename W>
+bool narrow_rows(const etune_schedule* src, W* dst, int64_t a, int64_t b) {
+    const int64_t* s = reinterpret_cast<const int64_t*>(src);
+    uint64_t hi = 0;
+    for (int64_t i = 12 * a; i < 12 * b; ++i) {
+        const uint64_t v = uint64_t(s[i]);
+        hi |= v >> (8 * sizeof(W));
+        dst[i] = W(v);
+    }
+    return hi == 0;
+}
+
+int host_threads() {
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, CPU_COUNT(&set));
+    return std::max(1u, std::thread::hardware_concurrency());
+}
+
+// Packs m rows into pinned `dst` with the narrowest field width that holds them (2, 4 or
+// 8 bytes), split over the host pool.  Returns the field width.
+int pack_rows(etune_cu_ctx* c, const etune_schedule* src, int64_t m, void* dst) {
+    const int tasks = std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m / 2048));
+    auto range = [&](int t, int64_t* a, int64_t* b) {
+        *a = m * t / tasks;
+        *b = m * (t + 1) / tasks;
+    };
+    std::vector<char> ok(size_t(tasks), 1);
+    c->pool->run(tasks, [&](int t) {
+        int64_t a, b;
+        range(t, &a, &b);
+        ok[size_t(t)] = narrow_rows(src, static_cast<uint16_t*>(dst), a, b);
+    });
+    if (std::all_of(ok.begin(), ok.end(), [](char x) { return x != 0; })) return 2;
+    c->pool->run(tasks, [&](int t) {
+        int64_t a, b;
+        range(t, &a, &b);
+        ok[size_t(t)] = narrow_rows(src, static_cast<uint32_t*>(dst), a, b);
+    });
+    if (std::all_of(ok.begin(), ok.end(), [](char x) { return x != 0; })) return 4;
+    c->pool->run(tasks, [&](int t) {
+        int64_t a, b;
+        range(t, &a, &b);
+        std::memcpy(static_cast<etune_schedule*>(dst) + a, src + a, size_t(b - a) * sizeof(etune_schedule));
+    });
+    return 8;
 }
 
 etune_status ensure_io(etune_cu_ctx* c, size_t bytes) {
@@ -939,13 +993,27 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
     if (n == 0) return ETUNE_OK;
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
-    // Chunked three-stage pipeline over two staging buffers: H2D of chunk i+1 (copy-in
-    // stream) overlaps encode+score of chunk i (ctx stream) and D2H of chunk i-1
-    // (copy-out stream); PCIe is full duplex.  One synchronisation at the end.
+    // Chunked pipeline over two staging buffers.  The host pool narrows chunk i's rows
+    // into pinned staging (24 B/row when every field fits 16 bits) while the GPU works
+    // on chunk i-1; then H2D of chunk i (copy-in stream) overlaps encode+score of chunk
+    // i-1 (ctx stream) and D2H of chunk i-2 (copy-out stream).  One synchronisation at
+    // the end.
     const int64_t chunk = int64_t(1) << 17;
-    const size_t per = sizeof(etune_schedule) + 8 + 8 + 8;  // sched, genome, pred, id
+    const size_t per = sizeof(etune_schedule) + 8 + 8 + 8;  // rows (widest), genome, pred, id
     const int64_t cap = n < chunk ? n : chunk;
     if (etune_status st = ensure_io(c, 2 * size_t(cap) * per)) return st;
+    const size_t pin_need = 2 * size_t(cap) * sizeof(etune_schedule);
+    if (c->hpin_bytes < pin_need) {
+        if (c->hpin) {
+            CU(cudaStreamSynchronize(c->stream));
+            CU(cudaFreeHost(c->hpin));
+            c->hpin = nullptr;
+            c->hpin_bytes = 0;
+        }
+        CU(cudaHostAlloc(&c->hpin, pin_need, cudaHostAllocDefault));
+        c->hpin_bytes = pin_need;
+    }
+    if (!c->pool) c->pool.reset(new HostPool(host_threads() - 1));
     if (!c->h2d) {
         CU(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
         CU(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
@@ -960,20 +1028,23 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
     CU(cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
     CU(cudaStreamWaitEvent(c->d2h, c->ev_done[0], 0));
     char* io = static_cast<char*>(c->io);
+    char* pin = static_cast<char*>(c->hpin);
     for (int64_t lo = 0, i = 0; lo < n; lo += chunk, ++i) {
         const int b = int(i & 1);
         char* base = io + size_t(b) * size_t(cap) * per;
-        auto* d_sched = reinterpret_cast<etune_schedule*>(base);
+        void* d_rows = base;
         auto* d_gen = reinterpret_cast<uint64_t*>(base + size_t(cap) * sizeof(etune_schedule));
         auto* d_pred = reinterpret_cast<double*>(base + size_t(cap) * (sizeof(etune_schedule) + 8));
         auto* d_ids = reinterpret_cast<uint64_t*>(base + size_t(cap) * (sizeof(etune_schedule) + 16));
+        void* h_rows = pin + size_t(b) * size_t(cap) * sizeof(etune_schedule);
         const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
+        if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));  // pinned buffer b read by chunk i-2's H2D
+        const int fb = pack_rows(c, h_sched + lo, m, h_rows);
         if (i >= 2) CU(cudaStreamWaitEvent(c->h2d, c->ev_out[b], 0));  // buffer b drained by chunk i-2's D2H
-        CU(cudaMemcpyAsync(d_sched, h_sched + lo, size_t(m) * sizeof(etune_schedule), cudaMemcpyHostToDevice,
-                           c->h2d));
+        CU(cudaMemcpyAsync(d_rows, h_rows, size_t(m) * 12 * size_t(fb), cudaMemcpyHostToDevice, c->h2d));
         CU(cudaEventRecord(c->ev_in[b], c->h2d));
         CU(cudaStreamWaitEvent(c->stream, c->ev_in[b], 0));
-        CU(launch_encode(c->lc(), p->d_blob, p->build.hdr.total, d_sched, m, d_gen, lo));
+        CU(launch_encode_packed(c->lc(), p->d_blob, p->build.hdr.total, d_rows, fb, m, d_gen, lo));
         CU(run_score(c, p, f, cs, d_gen, m, d_pred, h_ids ? d_ids : nullptr));
         CU(cudaEventRecord(c->ev_done[b], c->stream));
         CU(cudaStreamWaitEvent(c->d2h, c->ev_done[b], 0));

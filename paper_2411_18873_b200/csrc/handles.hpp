@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "forest.hpp"
+#include "host_pool.hpp"
 #include "kernels.hpp"
 #include "plan.hpp"
 
@@ -43,6 +44,10 @@ struct etune_cu_ctx {
     bool prof_on = false;
     std::vector<std::array<cudaEvent_t, 3>> prof_ev;  // before score, after score, after select
     size_t prof_used = 0;
+    // *_host pipelines: pinned staging of narrowed Schedule rows, packed by a host pool
+    void* hpin = nullptr;
+    size_t hpin_bytes = 0;
+    std::unique_ptr<etune_b200::HostPool> pool;
     // *_host pipelines: copy-in / copy-out streams and per-buffer events
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};

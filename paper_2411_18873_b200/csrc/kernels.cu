@@ -105,10 +105,48 @@ __device__ __forceinline__ int find_tiling(const TilingRec* T, int n, int64_t bl
     return lo;
 }
 
+// One Schedule row as the encoder sees it: the reference layout (12 x int64), or the
+// same 12 fields narrowed by the host to u16 / u32 (score_host packs them so the
+// PCIe copy moves 24 or 48 instead of 96 bytes; values were range-checked there).
+struct RowsI64 {
+    const etune_schedule* p;
+    __device__ __forceinline__ etune_schedule operator[](int64_t i) const { return p[i]; }
+};
+struct RowsU16 {
+    const uint64_t* p;  // 3 words per row
+    __device__ __forceinline__ etune_schedule operator[](int64_t i) const {
+        const uint64_t w[3] = {p[3 * i], p[3 * i + 1], p[3 * i + 2]};
+        int64_t f[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) f[k] = int64_t((w[k >> 2] >> (16 * (k & 3))) & 0xffffu);
+        return unpack_fields(f);
+    }
+    __device__ __forceinline__ static etune_schedule unpack_fields(const int64_t* f) {
+        etune_schedule s;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) s.spatial[d][k] = f[3 * d + k];
+        s.k_tile = f[9];
+        s.unroll = f[10];
+        s.vectorize = f[11];
+        return s;
+    }
+};
+struct RowsU32 {
+    const uint4* p;  // 3 x 16 bytes per row
+    __device__ __forceinline__ etune_schedule operator[](int64_t i) const {
+        const uint4 a = p[3 * i], b = p[3 * i + 1], c = p[3 * i + 2];
+        const int64_t f[12] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, c.x, c.y, c.z, c.w};
+        return RowsU16::unpack_fields(f);
+    }
+};
+
+template <typename Rows>
 __global__ void __launch_bounds__(kThreads) encode_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
-                                                          int use_smem, const etune_schedule* __restrict__ sched,
-                                                          int64_t n, uint64_t* __restrict__ genome,
-                                                          unsigned long long* err, int64_t index_base) {
+                                                          int use_smem, const Rows sched, int64_t n,
+                                                          uint64_t* __restrict__ genome, unsigned long long* err,
+                                                          int64_t index_base) {
     extern __shared__ int4 smem[];
     const uint8_t* P = gplan;
     if (use_smem) {
@@ -561,7 +599,18 @@ int max_dynamic_smem(int device) {
 
 cudaError_t launch_encode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const etune_schedule* d_sched,
                           int64_t n, uint64_t* d_genome, int64_t index_base) {
-    return launch_plan_kernel(encode_kernel, c, d_plan, bytes, n, d_sched, n, d_genome, c.d_err, index_base);
+    return launch_plan_kernel(encode_kernel<RowsI64>, c, d_plan, bytes, n, RowsI64{d_sched}, n, d_genome, c.d_err,
+                              index_base);
+}
+cudaError_t launch_encode_packed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const void* d_rows,
+                                 int field_bytes, int64_t n, uint64_t* d_genome, int64_t index_base) {
+    if (field_bytes == 2)
+        return launch_plan_kernel(encode_kernel<RowsU16>, c, d_plan, bytes, n,
+                                  RowsU16{static_cast<const uint64_t*>(d_rows)}, n, d_genome, c.d_err, index_base);
+    if (field_bytes == 4)
+        return launch_plan_kernel(encode_kernel<RowsU32>, c, d_plan, bytes, n,
+                                  RowsU32{static_cast<const uint4*>(d_rows)}, n, d_genome, c.d_err, index_base);
+    return launch_encode(c, d_plan, bytes, static_cast<const etune_schedule*>(d_rows), n, d_genome, index_base);
 }
 cudaError_t launch_decode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
                           int64_t n, etune_schedule* d_sched) {

@@ -22,6 +22,9 @@ constexpr unsigned long long kNoError = ~0ull;
 cudaError_t launch_encode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                           const etune_schedule* d_sched, int64_t n, uint64_t* d_genome,
                           int64_t index_base = 0);
+// encode from host-narrowed rows: 12 fields of field_bytes (2, 4; 8 = the reference layout)
+cudaError_t launch_encode_packed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const void* d_rows,
+                                 int field_bytes, int64_t n, uint64_t* d_genome, int64_t index_base);
 cudaError_t launch_decode(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                           const uint64_t* d_genome, int64_t n, etune_schedule* d_sched);
 cudaError_t launch_ids(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,

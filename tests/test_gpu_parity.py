@@ -200,6 +200,36 @@ def test_score_host_e2e(golden, oracle, ctx, capi):
     assert e.value.code == 4 and e.value.index == 299999
 
 
+@pytest.mark.parametrize("text,n,pinned", [("mm:1,131072,256,256", 140000, False),
+                                           ("conv:1,56,56,64,64,3,1,1", 400001, False),
+                                           ("conv:1,56,56,64,64,3,1,1", 400001, True)])
+def test_score_host_row_widths(golden, oracle, ctx, capi, text, n, pinned):
+    """score_host narrows rows on the host: u16 fields, u32 when a value needs it
+    (M = 2^17 tilings), the reference layout when a field is negative; pinned and
+    pageable caller buffers.  The error index of an illegal row stays exact across
+    chunks."""
+    fl = forest_of(golden, "c2_r50_conv3x3")
+    op = parse_op(text)
+    s, ids = oracle.sample_random(op, n, 9)
+    if pinned:
+        s = torch.from_numpy(s).pin_memory().numpy()
+    ref = oracle.predict(fl, oracle.features(op, s))
+    plan = capi.Plan(ctx, op)
+    fo = capi.Forest.from_flat(ctx, fl)
+    pred = np.zeros(n)
+    hid = np.zeros(n, np.uint64)
+    fo.score_host(plan, s, pred, hid)
+    assert (pred.view(np.uint64) == ref.view(np.uint64)).all()
+    assert (hid == ids).all()
+    if text.startswith("mm"):
+        assert s[:, :9].max() >= 1 << 16  # the u32 path was taken
+    bad = n - 2
+    s[bad, 1] = -1
+    with pytest.raises(capi.EtuneError) as e:
+        fo.score_host(plan, s, pred, hid)
+    assert e.value.code == 4 and e.value.index == bad
+
+
 @pytest.mark.parametrize("depth,smooth", [(8, False), (6, True)])
 def test_score_general_walk_path(oracle, ctx, capi, depth, smooth):
     """Forests whose compiled form is unsupported (> 64 leaves per tree) or does not fit
