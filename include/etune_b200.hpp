@@ -25,6 +25,8 @@
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
+#include <fstream>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -142,6 +144,7 @@ struct Candidate {  // space.hpp:22-30
 struct EnergySample {  // energy_model.hpp:27-31
     FeatureVector features{};
     double measured_energy_mj = 0.0;
+    double normalized_energy = 0.0;
 };
 
 // ------------------------------------------------------- device plumbing
@@ -356,6 +359,52 @@ public:
         return out;
     }
 
+    // EnergyModel::to_json / from_json / save / load (energy_model.cpp:259-350): the
+    // reference's "etune-model-v1" text, byte-identical to its own writer.
+    std::string to_json() const {
+        int64_t len = 0;
+        check(etune_model_to_json(feature_.data(), threshold_.data(), left_.data(), right_.data(), value_.data(),
+                                  offsets_.data(), int64_t(offsets_.size()) - 1, &params_, base_score_,
+                                  reference_energy_mj_, nullptr, 0, &len));
+        std::string s(size_t(len) + 1, '\0');
+        check(etune_model_to_json(feature_.data(), threshold_.data(), left_.data(), right_.data(), value_.data(),
+                                  offsets_.data(), int64_t(offsets_.size()) - 1, &params_, base_score_,
+                                  reference_energy_mj_, &s[0], len + 1, &len));
+        s.resize(size_t(len));
+        return s;
+    }
+    static EnergyModel from_json(Device& dev, const std::string& text) {
+        etune_model_host h;
+        check(etune_model_from_json(text.data(), int64_t(text.size()), &h));
+        const size_t nn = size_t(h.num_nodes);
+        EnergyModel m(dev);
+        m.feature_.assign(h.feature, h.feature + nn);
+        m.threshold_.assign(h.threshold, h.threshold + nn);
+        m.left_.assign(h.left, h.left + nn);
+        m.right_.assign(h.right, h.right + nn);
+        m.value_.assign(h.value, h.value + nn);
+        m.offsets_.assign(h.tree_offsets, h.tree_offsets + h.num_trees + 1);
+        m.params_ = h.params;
+        m.base_score_ = h.base_score;
+        m.reference_energy_mj_ = h.reference_energy_mj;
+        etune_model_host_free(&h);
+        m.upload();
+        return m;
+    }
+    void save(const std::string& path) const {
+        std::ofstream out(path);
+        if (!out) throw IoError(ETUNE_ERR_IO, "cannot write model file '" + path + "'", -1);
+        out << to_json() << '\n';
+        if (!out) throw IoError(ETUNE_ERR_IO, "failed writing model file '" + path + "'", -1);
+    }
+    static EnergyModel load(Device& dev, const std::string& path) {
+        std::ifstream in(path);
+        if (!in) throw IoError(ETUNE_ERR_IO, "cannot open model file '" + path + "'", -1);
+        std::ostringstream buf;
+        buf << in.rdbuf();
+        return from_json(dev, buf.str());
+    }
+
     double base_score() const { return base_score_; }
     double reference_energy_mj() const { return reference_energy_mj_; }
     const BoostParams& params() const { return params_; }
@@ -401,6 +450,58 @@ inline double snr_db(Device& dev, const std::vector<double>& predicted, const st
 }
 
 // ------------------------------------------------------------- population
+// save_energy_samples / load_energy_samples (energy_model.cpp:372-420)
+inline void save_energy_samples(const std::vector<EnergySample>& samples, const std::string& path) {
+    std::vector<double> f, m, z;
+    for (const EnergySample& s : samples) {
+        f.insert(f.end(), s.features.begin(), s.features.end());
+        m.push_back(s.measured_energy_mj);
+        z.push_back(s.normalized_energy);
+    }
+    int64_t len = 0;
+    const int64_t n = int64_t(samples.size());
+    check(etune_samples_to_jsonl(f.data(), m.data(), z.data(), n, nullptr, 0, &len));
+    std::string text(size_t(len) + 1, '\0');
+    check(etune_samples_to_jsonl(f.data(), m.data(), z.data(), n, &text[0], len + 1, &len));
+    std::ofstream out(path);
+    if (!out) throw IoError(ETUNE_ERR_IO, "cannot write samples file '" + path + "'", -1);
+    out.write(text.data(), len);
+    if (!out) throw IoError(ETUNE_ERR_IO, "failed writing samples file '" + path + "'", -1);
+}
+inline std::vector<EnergySample> load_energy_samples(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw IoError(ETUNE_ERR_IO, "cannot open samples file '" + path + "'", -1);
+    std::ostringstream buf;
+    buf << in.rdbuf();
+    const std::string text = buf.str();
+    etune_samples_host h;
+    check(etune_samples_from_jsonl(text.data(), int64_t(text.size()), &h));
+    std::vector<EnergySample> out(static_cast<size_t>(h.n));
+    for (int64_t i = 0; i < h.n; ++i) {
+        std::copy(h.features + 16 * i, h.features + 16 * (i + 1), out[size_t(i)].features.begin());
+        out[size_t(i)].measured_energy_mj = h.measured_energy_mj[i];
+        out[size_t(i)].normalized_energy = h.normalized_energy[i];
+    }
+    etune_samples_host_free(&h);
+    return out;
+}
+// device_profile_to_json / device_profile_from_json (device.cpp:44-101)
+inline std::string device_profile_to_json(const DeviceConfig& dev, const std::string& name = "a100-like") {
+    int64_t len = 0;
+    check(etune_device_profile_to_json(&dev, name.c_str(), nullptr, 0, &len));
+    std::string s(size_t(len) + 1, '\0');
+    check(etune_device_profile_to_json(&dev, name.c_str(), &s[0], len + 1, &len));
+    s.resize(size_t(len));
+    return s;
+}
+inline DeviceConfig device_profile_from_json(const std::string& text, std::string* name = nullptr) {
+    DeviceConfig d{};
+    std::vector<char> nm(text.size() + 1);
+    check(etune_device_profile_from_json(text.data(), int64_t(text.size()), &d, nm.data(), int64_t(nm.size())));
+    if (name) *name = nm.data();
+    return d;
+}
+
 inline std::vector<Candidate> to_candidates(const Plan& plan, const DeviceBuffer<uint64_t>& g, size_t n) {
     DeviceBuffer<uint64_t> ids(n);
     check(etune_cu_candidate_ids(plan.device().get(), plan.get(), g.get(), int64_t(n), ids.get()));

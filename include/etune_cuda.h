@@ -435,6 +435,60 @@ etune_status etune_cu_score_select_sharded(etune_cu_ctx* ctx, const etune_cu_pla
                                            double* d_pred, uint64_t* d_ids /*nullable*/,
                                            int64_t* d_idx_global, double* d_score_out /*nullable*/);
 
+/* ---------------------------------------------------------------- persistence
+ * The reference's on-disk formats, host-only, no device needed:
+ * a forest trained on the device round-trips through the reference's own loader.
+ * Writers follow nlohmann::json's output (sorted keys, shortest round-trip doubles,
+ * nlohmann's number layout); readers parse numbers with strtod, so every double is
+ * preserved bit for bit.  Writers: out == NULL queries the length (*out_len, excluding
+ * the terminating NUL); otherwise cap must be >= *out_len + 1. */
+typedef struct etune_model_host {   /* library-allocated; release with etune_model_host_free */
+    int64_t num_trees, num_nodes;
+    int32_t* feature;
+    double* threshold;
+    int32_t* left;
+    int32_t* right;
+    double* value;
+    int64_t* tree_offsets;          /* num_trees + 1 */
+    etune_boost_params params;
+    double base_score, reference_energy_mj;
+} etune_model_host;
+
+/* EnergyModel::to_json (energy_model.cpp:259-284), "etune-model-v1". */
+etune_status etune_model_to_json(const int32_t* feature, const double* threshold, const int32_t* left,
+                                 const int32_t* right, const double* value, const int64_t* tree_offsets,
+                                 int64_t num_trees, const etune_boost_params* params, double base_score,
+                                 double reference_energy_mj, char* out /*nullable*/, int64_t cap,
+                                 int64_t* out_len);
+/* EnergyModel::from_json (energy_model.cpp:286-336): ETUNE_ERR_IO on unreadable text, missing
+ * keys or an empty tree; ETUNE_ERR_VERSION_MISMATCH on model_version / feature_schema. */
+etune_status etune_model_from_json(const char* text, int64_t len, etune_model_host* out);
+void etune_model_host_free(etune_model_host* m);
+
+typedef struct etune_samples_host { /* library-allocated; release with etune_samples_host_free */
+    int64_t n;
+    double* features;               /* n x 16 */
+    double* measured_energy_mj;
+    double* normalized_energy;
+} etune_samples_host;
+
+/* save_energy_samples (energy_model.cpp:372-383): one JSON object per line. */
+etune_status etune_samples_to_jsonl(const double* features, const double* measured_energy_mj,
+                                    const double* normalized_energy, int64_t n, char* out /*nullable*/,
+                                    int64_t cap, int64_t* out_len);
+/* load_energy_samples (energy_model.cpp:385-420): ETUNE_ERR_IO (bad line),
+ * ETUNE_ERR_SCHEMA_MISMATCH (width != 16), ETUNE_ERR_NON_POSITIVE_ENERGY. */
+etune_status etune_samples_from_jsonl(const char* text, int64_t len, etune_samples_host* out);
+void etune_samples_host_free(etune_samples_host* s);
+
+/* device_profile_to_json (device.cpp:44-62), "etune-profile-v1", dump(2) + newline. */
+etune_status etune_device_profile_to_json(const etune_device_config* dev, const char* name /*nullable*/,
+                                          char* out /*nullable*/, int64_t cap, int64_t* out_len);
+/* device_profile_from_json (device.cpp:64-101) incl. DeviceConfig::validate:
+ * ETUNE_ERR_PARSE, ETUNE_ERR_VERSION_MISMATCH, ETUNE_ERR_VALIDATION. */
+etune_status etune_device_profile_from_json(const char* text, int64_t len, etune_device_config* out,
+                                            char* name_out /*nullable*/, int64_t name_cap);
+
 /* ncclBroadcast of `bytes` device bytes from `root` (trained forest arrays). */
 etune_status etune_cu_broadcast(etune_cu_ctx* ctx, void* d_buf, int64_t bytes, int root);
 

@@ -454,4 +454,72 @@ int ref_score_threads(const int64_t* op, const int64_t* sched, int64_t n, int nu
     GUARD_END
 }
 
+// ---- persistence formats (device.cpp:44-101, energy_model.cpp:372-420)
+// dev: double[11] in etune_device_config field order (constant_power_w ..
+// noise_sigma_rel), plus num_sms, rng_seed and name.
+int64_t ref_device_profile_to_json(int num_sms, const double* dev, uint64_t seed, const char* name, char* out,
+                                   int64_t cap) {
+    DeviceConfig d;
+    d.name = name;
+    d.num_sms = num_sms;
+    d.constant_power_w = dev[0];
+    d.static_power_per_sm_w = dev[1];
+    d.dynamic_energy_per_flop_nj = dev[2];
+    d.dynamic_energy_per_glb_access_nj = dev[3];
+    d.dynamic_energy_per_shared_access_nj = dev[4];
+    d.base_throughput_flops_per_s_per_sm = dev[5];
+    d.mem_bandwidth_elems_per_s = dev[6];
+    d.latency_floor_ms = dev[7];
+    d.sampler_hz = dev[8];
+    d.warmup_s = dev[9];
+    d.noise_sigma_rel = dev[10];
+    d.rng_seed = seed;
+    const std::string s = device_profile_to_json(d);
+    const int64_t need = static_cast<int64_t>(s.size()) + 1;
+    if (out && cap >= need) std::memcpy(out, s.c_str(), static_cast<size_t>(need));
+    return need;
+}
+
+int ref_device_profile_from_json(const char* text, int* num_sms, double* dev, uint64_t* seed, char* name,
+                                 int64_t cap) {
+    GUARD_BEGIN
+    const DeviceConfig d = device_profile_from_json(text);
+    *num_sms = d.num_sms;
+    const double v[11] = {d.constant_power_w, d.static_power_per_sm_w, d.dynamic_energy_per_flop_nj,
+                          d.dynamic_energy_per_glb_access_nj, d.dynamic_energy_per_shared_access_nj,
+                          d.base_throughput_flops_per_s_per_sm, d.mem_bandwidth_elems_per_s, d.latency_floor_ms,
+                          d.sampler_hz, d.warmup_s, d.noise_sigma_rel};
+    std::memcpy(dev, v, sizeof(v));
+    *seed = d.rng_seed;
+    if (cap > 0) {
+        std::strncpy(name, d.name.c_str(), static_cast<size_t>(cap - 1));
+        name[cap - 1] = '\0';
+    }
+    GUARD_END
+}
+
+int ref_samples_save(const double* feats, const double* meas, const double* norm, int64_t n, const char* path) {
+    GUARD_BEGIN
+    std::vector<EnergySample> v(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        std::memcpy(v[static_cast<size_t>(i)].features.data(), feats + 16 * i, 16 * sizeof(double));
+        v[static_cast<size_t>(i)].measured_energy_mj = meas[i];
+        v[static_cast<size_t>(i)].normalized_energy = norm[i];
+    }
+    save_energy_samples(v, path);
+    GUARD_END
+}
+
+int ref_samples_load(const char* path, double* feats, double* meas, double* norm, int64_t cap, int64_t* n) {
+    GUARD_BEGIN
+    const std::vector<EnergySample> v = load_energy_samples(path);
+    *n = static_cast<int64_t>(v.size());
+    for (int64_t i = 0; i < cap && i < *n; ++i) {
+        std::memcpy(feats + 16 * i, v[static_cast<size_t>(i)].features.data(), 16 * sizeof(double));
+        meas[i] = v[static_cast<size_t>(i)].measured_energy_mj;
+        norm[i] = v[static_cast<size_t>(i)].normalized_energy;
+    }
+    GUARD_END
+}
+
 } // extern "C"

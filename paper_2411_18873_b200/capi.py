@@ -95,6 +95,19 @@ class RoundReport(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class ModelHost(C.Structure):
+    _fields_ = [("num_trees", C.c_int64), ("num_nodes", C.c_int64), ("feature", C.POINTER(C.c_int32)),
+                ("threshold", C.POINTER(C.c_double)), ("left", C.POINTER(C.c_int32)),
+                ("right", C.POINTER(C.c_int32)), ("value", C.POINTER(C.c_double)),
+                ("tree_offsets", C.POINTER(C.c_int64)), ("params", BoostParams), ("base_score", C.c_double),
+                ("reference_energy_mj", C.c_double)]
+
+
+class SamplesHost(C.Structure):
+    _fields_ = [("n", C.c_int64), ("features", C.POINTER(C.c_double)),
+                ("measured_energy_mj", C.POINTER(C.c_double)), ("normalized_energy", C.POINTER(C.c_double))]
+
+
 _VP = C.c_void_p
 _I64 = C.c_int64
 _PTR = C.c_void_p
@@ -127,6 +140,16 @@ _SIGS = {
     "etune_cu_score": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR]),
     "etune_cu_score_select": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _I64, _PTR, _PTR, _PTR]),
     "etune_cu_score_select_sharded": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _I64, _I64, _PTR, _PTR, _PTR, _PTR]),
+    "etune_model_to_json": (C.c_int, [_PTR, _PTR, _PTR, _PTR, _PTR, _PTR, _I64, C.POINTER(BoostParams), C.c_double,
+                                      C.c_double, C.c_char_p, _I64, C.POINTER(_I64)]),
+    "etune_model_from_json": (C.c_int, [C.c_char_p, _I64, C.POINTER(ModelHost)]),
+    "etune_model_host_free": (None, [C.POINTER(ModelHost)]),
+    "etune_samples_to_jsonl": (C.c_int, [_PTR, _PTR, _PTR, _I64, C.c_char_p, _I64, C.POINTER(_I64)]),
+    "etune_samples_from_jsonl": (C.c_int, [C.c_char_p, _I64, C.POINTER(SamplesHost)]),
+    "etune_samples_host_free": (None, [C.POINTER(SamplesHost)]),
+    "etune_device_profile_to_json": (C.c_int, [C.POINTER(DeviceConfig), C.c_char_p, C.c_char_p, _I64,
+                                               C.POINTER(_I64)]),
+    "etune_device_profile_from_json": (C.c_int, [C.c_char_p, _I64, C.POINTER(DeviceConfig), C.c_char_p, _I64]),
     "etune_cu_profile_score": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                          C.POINTER(_I64)]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
@@ -609,3 +632,86 @@ def topk(ctx: Context, score, k: int, out=None):
     out = out if out is not None else torch.empty(k, dtype=torch.int64, device=score.device)
     _check(lib().etune_cu_topk(ctx.h, _ptr(score), score.shape[0], k, _ptr(out)))
     return out
+
+
+# ------------------------------------------------------------------ persistence
+def _emit(call) -> str:
+    """Two-phase writer call: length query, then the text."""
+    n = _I64()
+    _check(call(None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(call(buf, n.value + 1, C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def model_to_json(feature, threshold, left, right, value, tree_offsets, params: BoostParams, base_score: float,
+                  reference_energy_mj: float) -> str:
+    """EnergyModel::to_json (energy_model.cpp:259-284) of host arrays."""
+    a = [np.ascontiguousarray(feature, np.int32), np.ascontiguousarray(threshold, np.float64),
+         np.ascontiguousarray(left, np.int32), np.ascontiguousarray(right, np.int32),
+         np.ascontiguousarray(value, np.float64), np.ascontiguousarray(tree_offsets, np.int64)]
+    nt = len(a[5]) - 1
+    return _emit(lambda out, cap, n: lib().etune_model_to_json(*[x.ctypes.data for x in a], nt, C.byref(params),
+                                                               float(base_score), float(reference_energy_mj),
+                                                               out, cap, n))
+
+
+def model_from_json(text: str) -> dict:
+    """EnergyModel::from_json (energy_model.cpp:286-336) -> flat host arrays + scalars."""
+    b = text.encode()
+    m = ModelHost()
+    _check(lib().etune_model_from_json(b, len(b), C.byref(m)))
+    try:
+        nn, nt = m.num_nodes, m.num_trees
+
+        def arr(ptr, k, dt):
+            return np.ctypeslib.as_array(ptr, shape=(k,)).astype(dt, copy=True) if k else np.zeros(0, dt)
+        out = {"feature": arr(m.feature, nn, np.int32), "threshold": arr(m.threshold, nn, np.float64),
+               "left": arr(m.left, nn, np.int32), "right": arr(m.right, nn, np.int32),
+               "value": arr(m.value, nn, np.float64), "tree_offsets": arr(m.tree_offsets, nt + 1, np.int64),
+               "params": BoostParams(m.params.num_trees, m.params.max_depth, m.params.learning_rate,
+                                     m.params.min_leaf_weight, m.params.reg_lambda),
+               "base_score": m.base_score, "reference_energy_mj": m.reference_energy_mj}
+    finally:
+        lib().etune_model_host_free(C.byref(m))
+    return out
+
+
+def samples_to_jsonl(features, measured, normalized) -> str:
+    """save_energy_samples (energy_model.cpp:372-383) as text."""
+    f = np.ascontiguousarray(features, np.float64).reshape(-1, 16)
+    m = np.ascontiguousarray(measured, np.float64)
+    z = np.ascontiguousarray(normalized, np.float64)
+    return _emit(lambda out, cap, n: lib().etune_samples_to_jsonl(f.ctypes.data, m.ctypes.data, z.ctypes.data,
+                                                                  len(m), out, cap, n))
+
+
+def samples_from_jsonl(text: str):
+    """load_energy_samples (energy_model.cpp:385-420) -> (features n x 16, measured, normalized)."""
+    b = text.encode()
+    s = SamplesHost()
+    _check(lib().etune_samples_from_jsonl(b, len(b), C.byref(s)))
+    try:
+        n = s.n
+        if n == 0:
+            return np.zeros((0, 16)), np.zeros(0), np.zeros(0)
+        return (np.ctypeslib.as_array(s.features, shape=(n * 16,)).reshape(n, 16).copy(),
+                np.ctypeslib.as_array(s.measured_energy_mj, shape=(n,)).copy(),
+                np.ctypeslib.as_array(s.normalized_energy, shape=(n,)).copy())
+    finally:
+        lib().etune_samples_host_free(C.byref(s))
+
+
+def device_profile_to_json(dev: DeviceConfig, name: str = "a100-like") -> str:
+    """device_profile_to_json (device.cpp:44-62)."""
+    nm = name.encode()
+    return _emit(lambda out, cap, n: lib().etune_device_profile_to_json(C.byref(dev), nm, out, cap, n))
+
+
+def device_profile_from_json(text: str):
+    """device_profile_from_json (device.cpp:64-101) -> (DeviceConfig, name)."""
+    b = text.encode()
+    d = DeviceConfig()
+    name = C.create_string_buffer(4096)
+    _check(lib().etune_device_profile_from_json(b, len(b), C.byref(d), name, 4096))
+    return d, name.value.decode()

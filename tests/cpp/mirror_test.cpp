@@ -99,6 +99,35 @@ int main() {
     }
     EXPECT(same_bits(model.predict(feats[3]), want[3]));
 
+    // persistence (energy_model.cpp:259-420, device.cpp:44-101): save -> load round trips
+    {
+        const std::string mp = "/tmp/etune_mirror_model.json", sp = "/tmp/etune_mirror_samples.jsonl";
+        model.save(mp);
+        const EnergyModel back = EnergyModel::load(dev, mp);
+        EXPECT(back.to_json() == model.to_json());
+        const std::vector<double> p3 = back.predict_many(feats);
+        for (int64_t i = 0; i < n; ++i) EXPECT(same_bits(p3[size_t(i)], want[size_t(i)]));
+        save_energy_samples(samples, sp);
+        const std::vector<EnergySample> sb = load_energy_samples(sp);
+        EXPECT(sb.size() == samples.size());
+        for (size_t i = 0; i < sb.size(); ++i) {
+            EXPECT(std::memcmp(sb[i].features.data(), samples[i].features.data(), 128) == 0);
+            EXPECT(same_bits(sb[i].measured_energy_mj, samples[i].measured_energy_mj));
+        }
+        std::string nm;
+        const DeviceConfig d2 = device_profile_from_json(device_profile_to_json(a100_like(), "dev"), &nm);
+        EXPECT(nm == "dev" && d2.num_sms == 108 && same_bits(d2.constant_power_w, 60.0));
+        bool threw = false;
+        try {
+            EnergyModel::from_json(dev, "{\"model_version\":\"v0\"}");
+        } catch (const VersionMismatch&) {
+            threw = true;
+        }
+        EXPECT(threw);
+        std::remove(mp.c_str());
+        std::remove(sp.c_str());
+    }
+
     // snr_db
     std::vector<double> meas(energy.begin(), energy.begin() + 100), pr(want.begin(), want.begin() + 100);
     double osnr = 0;

@@ -323,6 +323,12 @@ class RefLib(_Lib):
         L.ref_model_nodes.argtypes = [C.c_void_p, I32P, F64P, I32P, I32P, F64P, I64P]
         L.ref_training_loss.argtypes = [C.c_void_p, F64P, C.c_int64, C.POINTER(C.c_int64)]
         L.ref_predict.argtypes = [C.c_void_p, F64P, C.c_int64, F64P]
+        L.ref_device_profile_to_json.argtypes = [C.c_int, F64P, C.c_uint64, C.c_char_p, C.c_char_p, C.c_int64]
+        L.ref_device_profile_to_json.restype = C.c_int64
+        L.ref_device_profile_from_json.argtypes = [C.c_char_p, C.POINTER(C.c_int), F64P, C.POINTER(C.c_uint64),
+                                                   C.c_char_p, C.c_int64]
+        L.ref_samples_save.argtypes = [F64P, F64P, F64P, C.c_int64, C.c_char_p]
+        L.ref_samples_load.argtypes = [C.c_char_p, F64P, F64P, F64P, C.c_int64, C.POINTER(C.c_int64)]
         L.ref_snr_db.argtypes = [F64P, F64P, C.c_int64, C.POINTER(C.c_double)]
         L.ref_energy_loss.argtypes = [C.c_double, C.c_double, F64P]
         L.ref_spearman.argtypes = [F64P, F64P, C.c_int64, C.POINTER(C.c_double)]
@@ -406,6 +412,51 @@ class RefLib(_Lib):
         self._check(self.L.ref_train(feats, energy, len(feats), num_trees, max_depth, lr, min_leaf_weight,
                                      reg_lambda, C.byref(h)))
         return RefModel(self, h)
+
+    # ---- persistence formats (device.cpp:44-101, energy_model.cpp:372-420)
+    DEV_FIELDS = ("constant_power_w", "static_power_per_sm_w", "dynamic_energy_per_flop_nj",
+                  "dynamic_energy_per_glb_access_nj", "dynamic_energy_per_shared_access_nj",
+                  "base_throughput_flops_per_s_per_sm", "mem_bandwidth_elems_per_s", "latency_floor_ms",
+                  "sampler_hz", "warmup_s", "noise_sigma_rel")
+
+    def device_profile_to_json(self, num_sms: int, fields, seed: int, name: str) -> str:
+        f = np.ascontiguousarray(fields, np.float64)
+        need = self.L.ref_device_profile_to_json(num_sms, f, seed, name.encode(), None, 0)
+        buf = C.create_string_buffer(int(need))
+        self.L.ref_device_profile_to_json(num_sms, f, seed, name.encode(), buf, need)
+        return buf.value.decode()
+
+    def device_profile_from_json(self, text: str):
+        n = C.c_int()
+        f = np.zeros(11, np.float64)
+        seed = C.c_uint64()
+        name = C.create_string_buffer(4096)
+        self._check(self.L.ref_device_profile_from_json(text.encode(), C.byref(n), f, C.byref(seed), name, 4096))
+        return n.value, f, seed.value, name.value.decode()
+
+    def samples_to_jsonl(self, feats, meas, norm) -> str:
+        import tempfile
+        feats = np.ascontiguousarray(feats, np.float64).reshape(-1, 16)
+        meas = np.ascontiguousarray(meas, np.float64)
+        norm = np.ascontiguousarray(norm, np.float64)
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "s.jsonl")
+            self._check(self.L.ref_samples_save(feats, meas, norm, len(meas), path.encode()))
+            return open(path).read()
+
+    def samples_from_jsonl(self, text: str):
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            path = os.path.join(d, "s.jsonl")
+            open(path, "w").write(text)
+            cap = text.count("\n") + 1
+            f = np.zeros((cap, 16), np.float64)
+            m = np.zeros(cap, np.float64)
+            z = np.zeros(cap, np.float64)
+            n = C.c_int64()
+            self._check(self.L.ref_samples_load(path.encode(), f, m, z, cap, C.byref(n)))
+            k = n.value
+            return f[:k], m[:k], z[:k]
 
     def model_from_json(self, text: str) -> "RefModel":
         h = C.c_void_p()
