@@ -263,8 +263,8 @@ __global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int 
 // loads its smem operands one batch of 8 ahead.
 //   lists 0..15: exclusive prefix at every position (the `run` of cpp 95-121)
 //   list 16:     the node's (grad, hess) totals in sample order (cpp 73-76, 150-155)
-constexpr int kChainWarps = 4;
-constexpr int kChunk = 256;
+constexpr int kChainWarps = 1;
+constexpr int kChunk = 1024;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
     const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
@@ -280,7 +280,8 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
                                                                  double* __restrict__ pg, double* __restrict__ ph,
                                                                  TrainCtl* ctl) {
     // prefixes overwrite their operands in place (each operand is in registers by then)
-    __shared__ double ig[kChainWarps][2][kChunk + 8], ih[kChainWarps][2][kChunk + 8];
+    __shared__ __align__(16) double ig[kChainWarps][2][kChunk + 8];
+    __shared__ __align__(16) double ih[kChainWarps][2][kChunk + 8];
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     if (nseg <= 0) return;
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
     double* PG = pg + int64_t(l) * n;
     double* PH = ph + int64_t(l) * n;
     const bool prefixes = l != kSampleList;
-    double rg = 0.0, rh = 0.0;
+    double racc = 0.0;  // lane 0: running gradient sum, lane 1: running hessian sum
     if (s < e) {
         const int cnt0 = min(kChunk, e - s);
         for (int j = lane; j < cnt0; j += 32) {
@@ -318,49 +319,46 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
         cp_async_commit();
         cp_async_wait_prev();  // the current chunk has landed (for this lane's copies)
         __syncwarp();
-        if (lane == 0) {
-            double* cg = ig[w][buf];
-            double* ch = ih[w][buf];
-            // full batches of 8: each prefix lives in its own register until the batch is
-            // stored; the next batch's operands are loaded before this batch's adds
-            const int full = cnt & ~7;
-            double g[8], h[8];
-            if (full) {
+        if (lane < 2) {
+            // lane 0 chains the gradients, lane 1 the hessians: one instruction stream,
+            // two independent chains (SIMT), ~2 instructions per element per lane —
+            // batches of 8 through double2 shared loads/stores, two register sets
+            // alternating so the next batch is loaded while this one chains; the chain
+            // runs near the FP64 add latency (8 cycles, scripts/micro/dadd_latency.cu)
+            double* cx = lane == 0 ? ig[w][buf] : ih[w][buf];
+            double2* c2 = reinterpret_cast<double2*>(cx);
+            const int nb = cnt >> 3;
+            const int full = nb << 3;
+            double2 xa[4], xb[4];
+            auto ld = [&](double2* x, int bi) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    g[u] = cg[u];
-                    h[u] = ch[u];
+                for (int q = 0; q < 4; ++q) x[q] = c2[bi * 4 + q];
+            };
+            auto run = [&](const double2* x, int bi) {
+                double2 pv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    pv[q].x = racc;
+                    racc = __dadd_rn(racc, x[q].x);
+                    pv[q].y = racc;
+                    racc = __dadd_rn(racc, x[q].y);
                 }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) c2[bi * 4 + q] = pv[q];
+            };
+            if (nb > 0) ld(xa, 0);
+            int bi = 0;
+            for (; bi + 1 < nb; bi += 2) {
+                ld(xb, bi + 1);
+                run(xa, bi);
+                if (bi + 2 < nb) ld(xa, bi + 2);
+                run(xb, bi + 1);
             }
-            for (int j = 0; j < full; j += 8) {
-                double pgv[8], phv[8], gn[8], hn[8];
-                const int jn = j + 8 < full ? j + 8 : j;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    gn[u] = cg[jn + u];
-                    hn[u] = ch[jn + u];
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    pgv[u] = rg;
-                    phv[u] = rh;
-                    rg = __dadd_rn(rg, g[u]);
-                    rh = __dadd_rn(rh, h[u]);
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    cg[j + u] = pgv[u];
-                    ch[j + u] = phv[u];
-                    g[u] = gn[u];
-                    h[u] = hn[u];
-                }
-            }
+            if (bi < nb) run(xa, bi);
             for (int j = full; j < cnt; ++j) {
-                const double gg = cg[j], hh = ch[j];
-                cg[j] = rg;
-                ch[j] = rh;
-                rg = __dadd_rn(rg, gg);
-                rh = __dadd_rn(rh, hh);
+                const double v = cx[j];
+                cx[j] = racc;
+                racc = __dadd_rn(racc, v);
             }
         }
         __syncwarp();
@@ -373,6 +371,7 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
         __syncwarp();
     }
     cp_async_wait_all();
+    const double rg = __shfl_sync(0xffffffffu, racc, 0), rh = __shfl_sync(0xffffffffu, racc, 1);
     if (lane == 0) {
         if (!prefixes) {
             const int node = ctl->seg_node[b][k];
