@@ -8,6 +8,7 @@
 #include <cstdint>
 
 #include "kernels.hpp"
+#include "pdl.cuh"
 
 namespace etune_b200 {
 namespace {
@@ -37,6 +38,7 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t* total) {
 
 template <typename F>
 __global__ void __launch_bounds__(kScanT) tile_sums_kernel(int64_t n, F f, int64_t* __restrict__ sums) {
+    pdl_wait();
     const int64_t i = blockIdx.x * int64_t(kScanT) + threadIdx.x;
     int64_t tot;
     block_excl_scan(i < n ? f(i) : 0, &tot);
@@ -45,6 +47,7 @@ __global__ void __launch_bounds__(kScanT) tile_sums_kernel(int64_t n, F f, int64
 
 __global__ void __launch_bounds__(kScanT) scan_sums_kernel(int64_t* __restrict__ sums, int64_t nt,
                                                            int64_t* __restrict__ total) {
+    pdl_wait();
     __shared__ int64_t carry;
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
@@ -64,6 +67,7 @@ __global__ void __launch_bounds__(kScanT) scan_sums_kernel(int64_t* __restrict__
 // out(i, exclusive prefix) for every i
 template <typename F, typename G>
 __global__ void __launch_bounds__(kScanT) tile_apply_kernel(int64_t n, F f, const int64_t* __restrict__ sums, G g) {
+    pdl_wait();
     const int64_t i = blockIdx.x * int64_t(kScanT) + threadIdx.x;
     int64_t tot;
     const int64_t ex = block_excl_scan(i < n ? f(i) : 0, &tot);
@@ -77,11 +81,13 @@ cudaError_t scan_apply(cudaStream_t st, int64_t n, F f, G g, int64_t* sums, int6
         cudaMemsetAsync(total, 0, 8, st);
         return cudaGetLastError();
     }
-    tile_sums_kernel<<<unsigned(nt), kScanT, 0, st>>>(n, f, sums);
-    scan_sums_kernel<<<1, kScanT, 0, st>>>(sums, nt, total);
-    tile_apply_kernel<<<unsigned(nt), kScanT, 0, st>>>(n, f, sums, g);
+    // programmatic dependent launches: each kernel waits (pdl_wait) before reading
+    cudaError_t e = launch_pdl(tile_sums_kernel<F>, dim3(unsigned(nt)), dim3(kScanT), 0, st, n, f, sums);
+    if (e == cudaSuccess) e = launch_pdl(scan_sums_kernel, dim3(1), dim3(kScanT), 0, st, sums, nt, total);
+    if (e == cudaSuccess)
+        e = launch_pdl(tile_apply_kernel<F, G>, dim3(unsigned(nt)), dim3(kScanT), 0, st, n, f, sums, g);
     note_launches(3);
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace

@@ -31,6 +31,7 @@
 
 #include "etune_internal.hpp"
 #include "kernels.hpp"
+#include "pdl.cuh"
 #include "scan.cuh"
 
 namespace etune_b200 {
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(1024) sort_kernel(const double* __restrict__ f
 // ----------------------------------------------------- per tree: gradients
 __global__ void grad_kernel(const double* __restrict__ pred, const double* __restrict__ target, int64_t n,
                             double* __restrict__ grad, double* __restrict__ hess, TrainCtl* ctl) {
+    pdl_wait();
     const int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (i0 == 0) {  // fresh tree: a single root leaf holding every sample
         ctl->nseg[0] = 1;
@@ -224,6 +226,7 @@ __global__ void grad_kernel(const double* __restrict__ pred, const double* __res
 
 // segment (frontier index) of every position, -1 for dead ranges; identical for all lists
 __global__ void segmap_kernel(int64_t n, int lvl, const TrainCtl* __restrict__ ctl, int32_t* __restrict__ segmap) {
+    pdl_wait();
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     const int32_t* ss = ctl->seg_start[b];
@@ -245,6 +248,7 @@ __global__ void segmap_kernel(int64_t n, int lvl, const TrainCtl* __restrict__ c
 __global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int nl, const double* __restrict__ grad,
                               const double* __restrict__ hess, const double* __restrict__ feats,
                               double* __restrict__ gl, double* __restrict__ hl, double* __restrict__ fv) {
+    pdl_wait();
     const int64_t tot = int64_t(nl) * n;
     const int64_t off = int64_t(kLists - nl) * n;  // nl == 1: sample list only
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
@@ -279,6 +283,7 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
                                                                  const double* __restrict__ hl,
                                                                  double* __restrict__ pg, double* __restrict__ ph,
                                                                  TrainCtl* ctl) {
+    pdl_wait();
     // prefixes overwrite their operands in place (each operand is in registers by then)
     __shared__ __align__(16) double ig[kChainWarps][2][kChunk + 8];
     __shared__ __align__(16) double ih[kChainWarps][2][kChunk + 8];
@@ -389,6 +394,7 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
 __global__ void gain_kernel(int64_t n, int lvl, const int32_t* __restrict__ segmap, const double* __restrict__ fv,
                             const double* __restrict__ pg, const double* __restrict__ ph, double mlw, double lambda,
                             double* __restrict__ gains, TrainCtl* ctl) {
+    pdl_wait();
     const int b = lvl & 1;
     const int64_t tot = int64_t(kF) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
@@ -420,6 +426,7 @@ __global__ void gain_kernel(int64_t n, int lvl, const int32_t* __restrict__ segm
 // earliest position attaining the max (ties: the reference's strict > keeps the first)
 __global__ void gainpos_kernel(int64_t n, const int32_t* __restrict__ segmap, const double* __restrict__ gains,
                                TrainCtl* ctl) {
+    pdl_wait();
     const int64_t tot = int64_t(kF) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
         const double g = gains[q];
@@ -436,6 +443,7 @@ __global__ void gainpos_kernel(int64_t n, const int32_t* __restrict__ segmap, co
 // cpp 111-117), allocate children in frontier order (cpp 130-143).
 __global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const double* __restrict__ fv,
                                                       TrainCtl* ctl) {
+    pdl_wait();
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     __shared__ int wsum[32];
@@ -505,6 +513,7 @@ __global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const 
 __global__ void leftflag_kernel(const double* __restrict__ feats, const int32_t* __restrict__ lists, int64_t n,
                                 int lvl, const int32_t* __restrict__ segmap, const TrainCtl* __restrict__ ctl,
                                 uint8_t* __restrict__ lf) {
+    pdl_wait();
     const int b = lvl & 1;
     const int32_t* S = lists + int64_t(kSampleList) * n;
     for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
@@ -537,6 +546,7 @@ struct PrefixWrite {
 __global__ void scatter_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
                                const int64_t* __restrict__ pfx, const int32_t* __restrict__ segmap, int64_t n,
                                int lvl, TrainCtl* ctl) {
+    pdl_wait();
     const int b = lvl & 1;
     const int64_t tot = int64_t(kLists) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
@@ -567,6 +577,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl*
                                                        int32_t* __restrict__ o_feature, double* __restrict__ o_thr,
                                                        int32_t* __restrict__ o_left, int32_t* __restrict__ o_right,
                                                        double* __restrict__ o_value, int64_t* __restrict__ o_off) {
+    pdl_wait();
     const int nn = ctl->nnodes;
     const int64_t base = ctl->out_nodes;
     const int tree = ctl->tree;
@@ -590,6 +601,7 @@ __global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl*
 // pred[i] += lr * tree.eval(feat[i])  (cpp 236-238)
 __global__ void update_kernel(const double* __restrict__ feats, int64_t n, double lr, const TrainCtl* __restrict__ ctl,
                               double* __restrict__ pred) {
+    pdl_wait();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         int node = 0;
         int f = ctl->feature[0];
@@ -605,6 +617,7 @@ __global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ p
                                                    const double* __restrict__ target, int64_t n,
                                                    const TrainCtl* __restrict__ ctl, double* __restrict__ loss,
                                                    double* __restrict__ tmp) {
+    pdl_wait();
     __shared__ double stage[1024 + 8];
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = __dsub_rn(pred[i], target[i]);
@@ -640,6 +653,14 @@ size_t train_scratch_bytes(int64_t n) {
 }
 
 int train_max_depth() { return kMaxDepth; }
+
+// tree-graph launches carry the programmatic-dependency attribute: each kernel calls
+// pdl_wait() first, and the next node's launch overlaps the previous node's tail
+#define PDL(k, g, b, sm, st, ...)                                                     \
+    do {                                                                             \
+        const cudaError_t pe = launch_pdl(k, dim3(g), dim3(b), sm, st, __VA_ARGS__); \
+        if (pe != cudaSuccess && e == cudaSuccess) e = pe;                           \
+    } while (0)
 
 cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double* d_energy, int64_t n, int num_trees,
                          int max_depth, double lr, double mlw, double lambda, int32_t* o_feature, double* o_thr,
@@ -703,40 +724,41 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
         return int(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, int64_t(c.sm_count) * 16)));
     };
     int launches = 0;
-    grad_kernel<<<grid(n), 256, 0, cap>>>(pred, target, n, grad, hess, ctl);
+    PDL(grad_kernel, grid(n), 256, 0, cap, pred, target, n, grad, hess, ctl);
     ++launches;
     const int32_t* cur = base_lists;
     int wb = 0;
     int lvl = 0;
     for (int depth = 0; depth < max_depth; ++depth, ++lvl) {
         const int segs = 1 << depth;  // frontier bound at this depth
-        segmap_kernel<<<grid(n), 256, 0, cap>>>(n, lvl, ctl, segmap);
-        gather_kernel<<<grid(int64_t(L)), 256, 0, cap>>>(cur, n, kLists, grad, hess, d_feat, gl, hl, fv);
+        PDL(segmap_kernel, grid(n), 256, 0, cap, n, lvl, ctl, segmap);
+        PDL(gather_kernel, grid(int64_t(L)), 256, 0, cap, cur, n, kLists, grad, hess, d_feat, gl, hl, fv);
         const int warps = kLists * segs;
-        chain_kernel<<<(warps + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap>>>(n, lvl, 0, gl, hl, pg,
-                                                                                              ph, ctl);
-        gain_kernel<<<grid(int64_t(F)), 256, 0, cap>>>(n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
-        gainpos_kernel<<<grid(int64_t(F)), 256, 0, cap>>>(n, segmap, gains, ctl);
-        decide_kernel<<<1, 1024, 0, cap>>>(n, lvl, fv, ctl);
-        leftflag_kernel<<<grid(n), 256, 0, cap>>>(d_feat, cur, n, lvl, segmap, ctl, lf);
-        e = scan_apply(cap, int64_t(L), LeftFlagFn{cur, segmap, ctl->split, lf, n}, PrefixWrite{pfx}, sums,
-                       pfx + L);
+        PDL(chain_kernel, (warps + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap, n, lvl, 0, gl, hl, pg, ph,
+            ctl);
+        PDL(gain_kernel, grid(int64_t(F)), 256, 0, cap, n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
+        PDL(gainpos_kernel, grid(int64_t(F)), 256, 0, cap, n, segmap, gains, ctl);
+        PDL(decide_kernel, 1, 1024, 0, cap, n, lvl, fv, ctl);
+        PDL(leftflag_kernel, grid(n), 256, 0, cap, d_feat, cur, n, lvl, segmap, ctl, lf);
+        if (e == cudaSuccess)
+            e = scan_apply(cap, int64_t(L), LeftFlagFn{cur, segmap, ctl->split, lf, n}, PrefixWrite{pfx}, sums,
+                           pfx + L);
         if (e != cudaSuccess) break;
-        scatter_kernel<<<grid(int64_t(L)), 256, 0, cap>>>(cur, work[wb], pfx, segmap, n, lvl, ctl);
+        PDL(scatter_kernel, grid(int64_t(L)), 256, 0, cap, cur, work[wb], pfx, segmap, n, lvl, ctl);
         cur = work[wb];
         wb ^= 1;
         launches += 11;
     }
     // totals of the last frontier (children created at the deepest level)
-    gather_kernel<<<grid(n), 256, 0, cap>>>(cur, n, 1, grad, hess, d_feat, gl, hl, fv);
+    PDL(gather_kernel, grid(n), 256, 0, cap, cur, n, 1, grad, hess, d_feat, gl, hl, fv);
     const int segs = 1 << max_depth;
-    chain_kernel<<<(segs + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap>>>(n, lvl, 1, gl, hl, pg, ph,
-                                                                                       ctl);
-    finalize_kernel<<<1, 1024, 0, cap>>>(lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
-    update_kernel<<<grid(n), 256, 0, cap>>>(d_feat, n, lr, ctl, pred);
+    PDL(chain_kernel, (segs + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap, n, lvl, 1, gl, hl, pg, ph,
+        ctl);
+    PDL(finalize_kernel, 1, 1024, 0, cap, lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
+    PDL(update_kernel, grid(n), 256, 0, cap, d_feat, n, lr, ctl, pred);
     launches += 4;
     if (o_loss) {
-        loss_kernel<<<1, 1024, 0, cap>>>(pred, target, n, ctl, o_loss, gains);
+        PDL(loss_kernel, 1, 1024, 0, cap, pred, target, n, ctl, o_loss, gains);
         launches += 1;
     }
     cudaGraph_t graph = nullptr;
