@@ -47,6 +47,11 @@ UNIT = "candidates/s"
 ALGO_BYTES = 24
 
 
+def workload(k: int) -> str:
+    """config.workload, identical for both arms."""
+    return f"score (features -> 100-tree GBDT -> prediction) + top-{k} of {OP_TEXT} candidates"
+
+
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
@@ -218,8 +223,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"score+top-{args.k} of {OP_TEXT} candidates (CPU reference)", "op": OP_TEXT,
-                   "population_per_step": per_step, "k": args.k},
+        "config": {"workload": workload(args.k), "op": OP_TEXT, "population_per_step": per_step, "k": args.k,
+                   "implementation": "the reference's CPU path (oracle/_ref: unmodified sources) over all host threads, "
+                                     "bounded sample per step"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
@@ -379,8 +385,9 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"fused score (features -> 100-tree GBDT -> prediction + id, bucketed) + "
-                               f"top-{K} of {n} {OP_TEXT} candidates per GPU", "op": OP_TEXT, "population_per_gpu": n,
+        "config": {"workload": workload(K), "op": OP_TEXT, "population_per_gpu": n,
+                   "implementation": "etune_cu_score_select: fused score kernel (+ ids, + selection histogram) -> "
+                                     "bucket filter -> rank selection, PDL-chained",
                    "k": K, "model": "reference-trained 100-tree depth-6 GBDT (tests/golden c2 fixture)",
                    "parallelism": f"dp{world} (population sharded; NCCL all-gather of per-shard top-k records "
                                   f"inside the C ABI)",
