@@ -323,9 +323,10 @@ def run_ours(args):
     capi.profile_score(ctx, True)
     for i in range(args.steps):
         step(args.warmup + args.steps + i)
-    score_ms, select_ms, score_calls = capi.profile_score(ctx, False)
+    sort_ms, score_ms, select_ms, score_calls = capi.profile_score(ctx, False)
     kernel_ms = score_ms / max(score_calls, 1)
     select_ms = select_ms / max(score_calls, 1)
+    sort_ms = sort_ms / max(score_calls, 1)
     if world > 1:
         t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -398,7 +399,7 @@ def run_ours(args):
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else
                                     "fallback 6650 GB/s (B200_PROFILING.md)",
                      "note": "SM-bound by design (shared-memory pipe), see profiles/",
-                     "select_ms": select_ms},
+                     "select_ms": select_ms, "key_sort_ms": sort_ms},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }

@@ -151,7 +151,8 @@ _SIGS = {
                                                C.POINTER(_I64)]),
     "etune_device_profile_from_json": (C.c_int, [C.c_char_p, _I64, C.POINTER(DeviceConfig), C.c_char_p, _I64]),
     "etune_cu_profile_score": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
-                                         C.POINTER(_I64)]),
+                                         C.POINTER(C.c_double), C.POINTER(_I64)]),
+    "etune_cu_forest_set_keyed": (C.c_int, [_VP, C.c_int]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
     "etune_cu_train": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(BoostParams), _PTR, _PTR, _PTR, _PTR, _PTR, _PTR,
@@ -464,6 +465,11 @@ class Forest:
         _check(lib().etune_cu_score(self.ctx.h, plan.h, self.h, _ptr(genome), n, _ptr(pred), _ptr(ids)))
         return (pred, ids) if (with_ids or ids_out is not None) else pred
 
+    def set_keyed(self, on: bool):
+        """Keyed scoring path for large populations (default on) or the class-table kernel only."""
+        _check(lib().etune_cu_forest_set_keyed(self.h, int(bool(on))))
+        return self
+
     def score_select(self, plan: Plan, genome, k: int, pred, idx, ids=None):
         """Fused score + keep-the-best (etune_cu_score_select) into preallocated tensors."""
         _check(lib().etune_cu_score_select(self.ctx.h, plan.h, self.h, _ptr(genome), genome.shape[0], int(k),
@@ -618,13 +624,14 @@ class Search:
 
 
 def profile_score(ctx: Context, on: bool):
-    """(score-kernel ms, selection ms, calls) recorded inside score_select since the last call;
-    then timing on/off."""
+    """(key-sort ms, score-kernel ms, selection ms, calls) recorded inside score_select since
+    the last call; then timing on/off."""
+    srt = C.c_double()
     ms = C.c_double()
     sel = C.c_double()
     cnt = _I64()
-    _check(lib().etune_cu_profile_score(ctx.h, int(bool(on)), C.byref(ms), C.byref(sel), C.byref(cnt)))
-    return ms.value, sel.value, cnt.value
+    _check(lib().etune_cu_profile_score(ctx.h, int(bool(on)), C.byref(srt), C.byref(ms), C.byref(sel), C.byref(cnt)))
+    return srt.value, ms.value, sel.value, cnt.value
 
 
 def topk(ctx: Context, score, k: int, out=None):

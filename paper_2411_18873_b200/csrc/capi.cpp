@@ -37,6 +37,7 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->breed);
     cudaFree(c->shard);
     cudaFree(c->sel);
+    cudaFree(c->ksort);
     if (c->hpin) cudaFreeHost(c->hpin);
     c->pool.reset();
     for (auto& e : c->prof_ev)
@@ -209,7 +210,8 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     std::vector<uint8_t> blob;
     std::string err;
     CompiledScore cs;
-    const etune_status bst = build_score_blob(f->host, p->build, &blob, &cs.stats, &err);
+    KeyedBuild kb;
+    const etune_status bst = build_score_blob(f->host, p->build, &blob, &cs.stats, &err, &kb);
     if (bst != ETUNE_OK && bst != ETUNE_ERR_UNSUPPORTED) return fail(bst, err);
     const int cap = max_dynamic_smem(f->ctx->device) - score_static_smem();
     if (bst == ETUNE_ERR_UNSUPPORTED || blob.size() > size_t(cap)) {
@@ -234,20 +236,86 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     else
         std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
     selection_buckets(f->host, &cs.sel_kmin, &cs.sel_shift);
+    if (kb.ok && kb.blob.size() <= size_t(cap)) {
+        CU(cudaMalloc(&cs.d_kblob, kb.blob.size()));
+        CU(cudaMalloc(&cs.d_ktable, kb.table.size() * 4));
+        CU(cudaMemcpyAsync(cs.d_kblob, kb.blob.data(), kb.blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
+        CU(cudaMemcpyAsync(cs.d_ktable, kb.table.data(), kb.table.size() * 4, cudaMemcpyHostToDevice,
+                           f->ctx->stream));
+        CU(cudaStreamSynchronize(f->ctx->stream));
+        cs.kbytes = uint32_t(kb.blob.size());
+        cs.key_bits = kb.key_bits;
+        cs.nkeys = int(kb.nkeys);
+        cs.nt1 = p->build.hdr.nt[1];
+        cs.nt2 = p->build.hdr.nt[2];
+        CU(score_keyed_occupancy(cs.kbytes, &cs.keyed_per_sm));
+        cs.keyed = true;
+    }
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;
 }
 
-cudaError_t run_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
-                      const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids) {
-    if (cs->walk)
-        return launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
-                                 d_pred, d_ids);
-    return launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
-                        cs->per_sm);
+// Populations at least this large take the keyed path (its key sort is a fixed cost).
+constexpr int64_t kKeyedMinN = int64_t(1) << 15;
+
+bool use_keyed(const etune_cu_forest* f, const CompiledScore* cs, int64_t n) {
+    return cs->keyed && f->keyed_mode != 0 && n >= kKeyedMinN && n < (int64_t(1) << 32);
 }
 
+// Scoring pass of any compiled form; `ev` (nullable) = {before the key sort, before the
+// score kernel, after it} for etune_cu_profile_score.
+etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
+                            const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
+                            const SelHist& sel, const cudaEvent_t* ev) {
+    if (ev) CU(cudaEventRecord(ev[0], c->stream));
+    if (cs->walk) {
+        if (ev) CU(cudaEventRecord(ev[1], c->stream));
+        CU(launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
+                             d_pred, d_ids));
+    } else if (use_keyed(f, cs, n)) {
+        // key = tiling triple; grouping by key gives warps candidates that share
+        // key-table rows; results land at the original indices
+        const int nk = cs->nkeys;
+        const bool counting = nk <= kMaxSortKeys;
+        const size_t obytes = (4 * size_t(n) + 255) & ~size_t(255);
+        const size_t kbytes = counting ? 0 : (8 * size_t(n) + 255) & ~size_t(255);
+        const size_t cbytes = (8 * size_t(kMaxSortKeys) + 255) & ~size_t(255);
+        const size_t need = obytes + kbytes + cbytes + (counting ? 0 : sort_pairs_scratch_bytes(n));
+        if (c->ksort_bytes < need) {
+            if (c->ksort) {
+                CU(cudaStreamSynchronize(c->stream));
+                CU(cudaFree(c->ksort));
+                c->ksort = nullptr;
+                c->ksort_bytes = 0;
+            }
+            CU(cudaMalloc(&c->ksort, need));
+            c->ksort_bytes = need;
+            CU(cudaMemsetAsync(c->ksort, 0, need, c->stream));  // counting-sort counts start at zero
+        }
+        // layout: [counts | cursor] at a fixed offset (the counts stay zeroed between
+        // calls whatever n is), then the order, then the radix-sort keys and scratch
+        char* kp = static_cast<char*>(c->ksort);
+        auto* counts = reinterpret_cast<uint32_t*>(kp);
+        auto* order = reinterpret_cast<uint32_t*>(kp + cbytes);
+        if (counting) {
+            CU(launch_key_sort(c->lc(), d_genome, n, cs->nt1, cs->nt2, nk, counts, counts + kMaxSortKeys, order));
+        } else {
+            auto* keys = reinterpret_cast<uint64_t*>(kp + cbytes + obytes);
+            CU(launch_keygen(c->lc(), d_genome, n, cs->nt1, cs->nt2, keys, order));
+            CU(launch_sort_pairs(c->lc(), keys, order, n, cs->key_bits, kp + cbytes + obytes + kbytes));
+        }
+        if (ev) CU(cudaEventRecord(ev[1], c->stream));
+        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, d_genome, order, n, d_pred, d_ids,
+                              cs->keyed_per_sm, sel));
+    } else {
+        if (ev) CU(cudaEventRecord(ev[1], c->stream));
+        CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
+                        cs->per_sm, sel));
+    }
+    if (ev) CU(cudaEventRecord(ev[2], c->stream));
+    return ETUNE_OK;
+}
 
 // Fused score + keep-the-best on one shard: the score kernel fills the selection
 // histogram, sel_filter/sel_finish (sort.cu) resolve the k lowest (score, index).
@@ -256,7 +324,7 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
                                 const uint64_t* d_genome, int64_t n, int64_t k, double* d_pred, uint64_t* d_ids,
                                 int64_t* d_idx) {
     if (cs->walk || k > kSelMaxK || k == 0) {
-        CU(run_score(c, p, f, cs, d_genome, n, d_pred, d_ids));
+        if (etune_status st = score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, SelHist{}, nullptr)) return st;
         if (k == 0) return ETUNE_OK;
         if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
         CU(launch_topk(c->lc(), d_pred, n, k, d_idx, c->scratch));
@@ -278,19 +346,15 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
     c->sel_dirty = true;
     const SelHist sh{select_hist(c->sel), cs->sel_kmin, cs->sel_shift};
     const bool prof = c->prof_on;
-    if (prof) {
-        if (c->prof_used == c->prof_ev.size()) {
-            std::array<cudaEvent_t, 3> e{};
-            for (cudaEvent_t& x : e) CU(cudaEventCreate(&x));
-            c->prof_ev.push_back(e);
-        }
-        CU(cudaEventRecord(c->prof_ev[c->prof_used][0], c->stream));
+    if (prof && c->prof_used == c->prof_ev.size()) {
+        std::array<cudaEvent_t, 4> e{};
+        for (cudaEvent_t& x : e) CU(cudaEventCreate(&x));
+        c->prof_ev.push_back(e);
     }
-    CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
-                    cs->per_sm, sh));
-    if (prof) CU(cudaEventRecord(c->prof_ev[c->prof_used][1], c->stream));
+    const cudaEvent_t* ev = prof ? c->prof_ev[c->prof_used].data() : nullptr;
+    if (etune_status st = score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, sh, ev)) return st;
     CU(launch_select(c->lc(), d_pred, n, k, d_idx, c->sel, sh));
-    if (prof) CU(cudaEventRecord(c->prof_ev[c->prof_used++][2], c->stream));
+    if (prof) CU(cudaEventRecord(c->prof_ev[c->prof_used++][3], c->stream));
     c->sel_dirty = false;
     return ETUNE_OK;
 }
@@ -906,7 +970,11 @@ etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, con
 etune_status etune_cu_forest_destroy(etune_cu_forest* f) {
     if (!f) return ETUNE_OK;
     cudaFree(f->d_predict);
-    for (auto& kv : f->compiled) cudaFree(kv.second.d_blob);
+    for (auto& kv : f->compiled) {
+        cudaFree(kv.second.d_blob);
+        cudaFree(kv.second.d_kblob);
+        cudaFree(kv.second.d_ktable);
+    }
     etune_cu_ctx* c = f->ctx;
     delete f;
     ctx_release(c);
@@ -927,8 +995,7 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
-    CU(run_score(c, p, f, cs, d_genome, n, d_pred, d_ids));
-    return ETUNE_OK;
+    return score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, SelHist{}, nullptr);
 }
 
 etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
@@ -962,20 +1029,29 @@ etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan*
     return shard_merge(c, d_pred, kl, k, goff, sb, d_idx, d_sc);
 }
 
-etune_status etune_cu_profile_score(etune_cu_ctx* c, int on, double* score_ms, double* select_ms,
+etune_status etune_cu_forest_set_keyed(etune_cu_forest* f, int mode) {
+    if (!f || mode < 0 || mode > 1) return fail(ETUNE_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    f->keyed_mode = mode;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_profile_score(etune_cu_ctx* c, int on, double* prep_ms, double* score_ms, double* select_ms,
                                     int64_t* launches) {
     if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
-    double ms = 0.0, sel = 0.0;
+    double pre = 0.0, ms = 0.0, sel = 0.0;
     if (c->prof_used) {
         CU(cudaStreamSynchronize(c->stream));
         for (size_t i = 0; i < c->prof_used; ++i) {
-            float e = 0.f, f = 0.f;
-            CU(cudaEventElapsedTime(&e, c->prof_ev[i][0], c->prof_ev[i][1]));
-            CU(cudaEventElapsedTime(&f, c->prof_ev[i][1], c->prof_ev[i][2]));
+            float a = 0.f, e = 0.f, f = 0.f;
+            CU(cudaEventElapsedTime(&a, c->prof_ev[i][0], c->prof_ev[i][1]));
+            CU(cudaEventElapsedTime(&e, c->prof_ev[i][1], c->prof_ev[i][2]));
+            CU(cudaEventElapsedTime(&f, c->prof_ev[i][2], c->prof_ev[i][3]));
+            pre += a;
             ms += e;
             sel += f;
         }
     }
+    if (prep_ms) *prep_ms = pre;
     if (score_ms) *score_ms = ms;
     if (select_ms) *select_ms = sel;
     if (launches) *launches = int64_t(c->prof_used);
@@ -1045,7 +1121,8 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         CU(cudaEventRecord(c->ev_in[b], c->h2d));
         CU(cudaStreamWaitEvent(c->stream, c->ev_in[b], 0));
         CU(launch_encode_packed(c->lc(), p->d_blob, p->build.hdr.total, d_rows, fb, m, d_gen, lo));
-        CU(run_score(c, p, f, cs, d_gen, m, d_pred, h_ids ? d_ids : nullptr));
+        if (etune_status st = score_dispatch(c, p, f, cs, d_gen, m, d_pred, h_ids ? d_ids : nullptr, SelHist{}, nullptr))
+            return st;
         CU(cudaEventRecord(c->ev_done[b], c->stream));
         CU(cudaStreamWaitEvent(c->d2h, c->ev_done[b], 0));
         CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));

@@ -171,6 +171,28 @@ struct ScoreHdr {
     uint32_t total;
 };
 
+// --------------------------------------------------------- keyed score blob
+// Every channel except Kuv is a function of the three tiling indices alone, so the
+// forest compiler evaluates, per tiling triple ("key"), the AND of each tree's non-Kuv
+// channel masks: table[key][tree] (u32, global memory, L2-resident).  On the device a
+// candidate needs one 16-byte row load per 4 trees (broadcast when a warp's candidates
+// share the key — the population is sorted by key first), one Kuv-mask load per tree
+// and the leaf value.  Blob (shared memory): header, tilings, divisors of K, the Kuv
+// class table, per-tree Kuv masks [tree][kuv class] and the leaf blocks.
+struct KeyedHdr {
+    int64_t K;
+    uint64_t fnv_prefix;
+    double base, lr;
+    int32_t ntrees, tpad, nkc, key_bits;
+    int32_t nt[3], nd[3], ndk, pad;
+    uint32_t off_til[3];
+    uint32_t off_divk;
+    uint32_t off_clskuv;   // uint8 [(k*16+u)*4+v] -> Kuv class
+    uint32_t off_kuvtab;   // uint32 [tree][nkc]
+    uint32_t off_leaves;   // per tree 32 high words then 32 low words, de Bruijn slots
+    uint32_t total;
+};
+
 // ------------------------------------------------------- generic predict blob
 // EnergyModel::predict on arbitrary feature vectors: reference node order.
 struct GNode {

@@ -16,6 +16,7 @@
 //      every leaf left of it lies in the left subtree of a node that went right).
 // Leaf values are the reference's doubles, summed in tree order.
 #include "forest.hpp"
+#include "score_core.hpp"
 
 #include <algorithm>
 #include <cstring>
@@ -127,7 +128,7 @@ size_t debruijn_slot(int leaf, int mbits) {
 }
 
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
-                              ScoreStats* stats, std::string* err) {
+                              ScoreStats* stats, std::string* err, KeyedBuild* keyed, size_t max_table_bytes) {
     if (etune_status st = forest_validate(F, err)) return st;
     const PlanHdr& PH = P.hdr;
     const int nd1 = PH.nd[1], nd2 = PH.nd[2], ndk = PH.ndk;
@@ -483,6 +484,67 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
     H.total = uint32_t(blob->size());
     std::memcpy(blob->data(), &H, sizeof(H));
     if (stats) *stats = S;
+
+    // ---- keyed form: per tiling triple, each tree's AND of its non-Kuv channel masks
+    if (keyed) {
+        keyed->ok = false;
+        const int64_t nk = int64_t(PH.nt[0]) * PH.nt[1] * PH.nt[2];
+        const int tpad = int((T + 3) / 4 * 4);
+        if (mbits == 32 && T > 0 && nk > 0 && size_t(nk) * size_t(tpad) * 4 <= max_table_bytes) {
+            keyed->nkeys = nk;
+            int kb = 0;
+            while ((int64_t(1) << kb) < nk) ++kb;
+            keyed->key_bits = kb;
+            keyed->table.assign(size_t(nk) * size_t(tpad), 0xffffffffu);
+            const uint8_t* B = blob->data();  // the finished score blob: classes exactly as the device derives them
+            for (int64_t t0 = 0; t0 < PH.nt[0]; ++t0)
+                for (int64_t t1 = 0; t1 < PH.nt[1]; ++t1)
+                    for (int64_t t2 = 0; t2 < PH.nt[2]; ++t2) {
+                        const CandClasses cc =
+                            candidate_classes(B, H, genome_pack(uint32_t(t0), uint32_t(t1), uint32_t(t2), 0, 0, 0));
+                        const int64_t key = (t0 * PH.nt[1] + t1) * PH.nt[2] + t2;
+                        uint32_t* row = keyed->table.data() + size_t(key) * size_t(tpad);
+                        for (int64_t t = 0; t < T; ++t) {
+                            uint64_t m = full;
+                            for (int c = 0; c < kNumChannels; ++c)
+                                if (c != kChKuv && ((tree_used[size_t(t)] >> c) & 1u))
+                                    m &= tree_tl[size_t(t)][size_t(c)][cc.c[c]];
+                            row[t] = uint32_t(m);
+                        }
+                    }
+            const int nkc = int(rep[kChKuv].size());
+            std::vector<uint32_t> kuvtab(size_t(tpad) * size_t(nkc), 0xffffffffu);
+            for (int64_t t = 0; t < T; ++t)
+                if ((tree_used[size_t(t)] >> kChKuv) & 1u)
+                    for (int x = 0; x < nkc; ++x)
+                        kuvtab[size_t(t) * size_t(nkc) + size_t(x)] = uint32_t(tree_tl[size_t(t)][kChKuv][size_t(x)]);
+            KeyedHdr K{};
+            K.K = PH.K;
+            K.fnv_prefix = PH.fnv_prefix;
+            K.base = F.base;
+            K.lr = F.lr;
+            K.ntrees = int32_t(T);
+            K.tpad = tpad;
+            K.nkc = nkc;
+            K.key_bits = kb;
+            for (int d = 0; d < 3; ++d) {
+                K.nt[d] = PH.nt[d];
+                K.nd[d] = PH.nd[d];
+            }
+            K.ndk = PH.ndk;
+            std::vector<uint8_t>& kbl = keyed->blob;
+            kbl.assign(align16(sizeof(KeyedHdr)), 0);
+            for (int d = 0; d < 3; ++d) K.off_til[d] = put(kbl, P.til[d].data(), P.til[d].size());
+            K.off_divk = put(kbl, P.divk.data(), P.divk.size());
+            K.off_clskuv = put(kbl, cls[kChKuv].data(), cls[kChKuv].size());
+            K.off_kuvtab = put(kbl, kuvtab.data(), kuvtab.size());
+            K.off_leaves = put(kbl, leaves.data(), leaves.size());  // 32 doubles (256 B) per tree, in tree order
+            kbl.resize(align16(kbl.size()));
+            K.total = uint32_t(kbl.size());
+            std::memcpy(kbl.data(), &K, sizeof(K));
+            keyed->ok = true;
+        }
+    }
     return ETUNE_OK;
 }
 

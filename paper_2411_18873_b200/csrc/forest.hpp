@@ -30,7 +30,17 @@ struct ScoreStats {
     int total_leaves = 0;
     int channels_used = 0;           // bitmask of channels still tested after folding
 };
+// Keyed form (KeyedHdr): built alongside the score blob when every tree has <= 32 leaves
+// and the key table fits `max_table_bytes`; `ok` false otherwise.
+struct KeyedBuild {
+    bool ok = false;
+    std::vector<uint8_t> blob;
+    std::vector<uint32_t> table;  // [nkeys][tpad]
+    int64_t nkeys = 0;
+    int key_bits = 0;
+};
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
-                              ScoreStats* stats, std::string* err);
+                              ScoreStats* stats, std::string* err, KeyedBuild* keyed = nullptr,
+                              size_t max_table_bytes = size_t(64) << 20);
 
 }  // namespace etune_b200

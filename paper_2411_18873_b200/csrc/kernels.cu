@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <mutex>
 #include <cstdint>
 
 #include "etune_internal.hpp"
@@ -542,6 +543,169 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
     }
 }
 
+// ------------------------------------------------------------- keyed score
+// Candidates visited in key order (order[] from the key sort, so a warp's candidates
+// mostly share one key-table row: its 16-byte row loads are broadcasts from L1); results
+// written at the original index.  Per tree: one Kuv-mask load (a <= 32-word row per
+// tree, conflict-free), the exit slot, two leaf-word loads, one FP64 add in tree order.
+constexpr int kKeyedThreads = 256;
+
+__global__ void __launch_bounds__(kKeyedThreads) keygen_kernel(const uint64_t* __restrict__ genome, int64_t n,
+                                                               uint32_t nt1, uint32_t nt2, uint64_t* __restrict__ keys,
+                                                               uint32_t* __restrict__ vals) {
+    pdl_wait();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const Genome x = genome_unpack(__ldg(genome + i));
+        keys[i] = (uint64_t(x.t0) * nt1 + x.t1) * nt2 + x.t2;
+        vals[i] = uint32_t(i);
+    }
+}
+
+// Counting sort of candidate indices by key (nkeys <= kMaxSortKeys): per-CTA shared
+// histograms -> global counts; one CTA scans counts into start offsets (and re-zeroes
+// the counts for the next call); each CTA reserves one range per key it holds with one
+// global atomic and places its indices.  Order inside a key group is unspecified: the
+// score kernel's results do not depend on the visiting order.
+constexpr int kSortT = 256;
+constexpr int kSortPer = 16;  // candidates per thread per chunk (4096 per CTA)
+
+__device__ __forceinline__ uint32_t genome_key(uint64_t g, uint32_t nt1, uint32_t nt2) {
+    const Genome x = genome_unpack(g);
+    return (x.t0 * nt1 + x.t1) * nt2 + x.t2;
+}
+
+__global__ void __launch_bounds__(kSortT) key_hist_kernel(const uint64_t* __restrict__ genome, int64_t n,
+                                                          uint32_t nt1, uint32_t nt2, uint32_t nkeys,
+                                                          uint32_t* __restrict__ counts) {
+    extern __shared__ uint32_t sh[];
+    for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) sh[i] = 0u;
+    __syncthreads();
+    pdl_wait();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(&sh[genome_key(__ldg(genome + i), nt1, nt2)], 1u);
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x)
+        if (sh[i]) atomicAdd(counts + i, sh[i]);
+}
+
+__global__ void __launch_bounds__(1024) key_scan_kernel(uint32_t* __restrict__ counts, uint32_t nkeys,
+                                                        uint32_t* __restrict__ cursor) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry;
+    pdl_wait();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (uint32_t b = 0; b < nkeys; b += blockDim.x) {
+        const uint32_t i = b + threadIdx.x;
+        const uint32_t v = i < nkeys ? counts[i] : 0u;
+        uint32_t x = v;
+        for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
+            if (lane >= s) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        uint32_t before = carry;
+        for (int w = 0; w < warp; ++w) before += wsum[w];
+        if (i < nkeys) {
+            cursor[i] = before + x - v;
+            counts[i] = 0u;  // ready for the next call's histogram
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < int(blockDim.x >> 5); ++w) t += wsum[w];
+            carry += t;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kSortT) key_place_kernel(const uint64_t* __restrict__ genome, int64_t n,
+                                                           uint32_t nt1, uint32_t nt2, uint32_t nkeys,
+                                                           uint32_t* __restrict__ cursor,
+                                                           uint32_t* __restrict__ order) {
+    extern __shared__ uint32_t sh[];
+    uint32_t* cnt = sh;           // per-key count in this chunk, then running slot
+    uint32_t* base = sh + nkeys;  // reserved global start per key
+    pdl_wait();
+    const int64_t chunk = int64_t(kSortT) * kSortPer;
+    for (int64_t c0 = int64_t(blockIdx.x) * chunk; c0 < n; c0 += int64_t(gridDim.x) * chunk) {
+        for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) cnt[i] = 0u;
+        __syncthreads();
+        uint32_t key[kSortPer];
+#pragma unroll
+        for (int r = 0; r < kSortPer; ++r) {
+            const int64_t i = c0 + r * kSortT + threadIdx.x;
+            key[r] = i < n ? genome_key(__ldg(genome + i), nt1, nt2) : 0xffffffffu;
+            if (i < n) atomicAdd(&cnt[key[r]], 1u);
+        }
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) {
+            const uint32_t k = cnt[i];
+            base[i] = k ? atomicAdd(cursor + i, k) : 0u;
+            cnt[i] = 0u;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kSortPer; ++r) {
+            const int64_t i = c0 + r * kSortT + threadIdx.x;
+            if (i < n) order[base[key[r]] + atomicAdd(&cnt[key[r]], 1u)] = uint32_t(i);
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
+                                                                    const uint32_t* __restrict__ table,
+                                                                    const uint64_t* __restrict__ genome,
+                                                                    const uint32_t* __restrict__ order, int64_t n,
+                                                                    double* __restrict__ pred,
+                                                                    uint64_t* __restrict__ ids, const SelHist sel) {
+    extern __shared__ int4 smem[];
+    __shared__ uint32_t shist[kSelBins];
+    if (sel.hist)
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) shist[i] = 0u;
+    stage(gblob, bytes, smem);  // read-only blob: overlaps the previous kernel's tail (PDL)
+    __syncthreads();
+    pdl_wait();
+    const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
+    const KeyedHdr& K = *reinterpret_cast<const KeyedHdr*>(S);
+    const uint8_t* clskuv = S + K.off_clskuv;
+    const TilingRec* til0 = at<TilingRec>(S, K.off_til[0]);
+    const TilingRec* til1 = at<TilingRec>(S, K.off_til[1]);
+    const TilingRec* til2 = at<TilingRec>(S, K.off_til[2]);
+    const int64_t* divk = at<int64_t>(S, K.off_divk);
+    const uint32_t tpad = uint32_t(K.tpad);
+    for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < n; s += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t idx = order ? __ldg(order + s) : uint32_t(s);
+        const Genome x = genome_unpack(__ldg(genome + idx));
+        const uint32_t kc = clskuv[(x.k * 16u + x.u) * 4u + x.v];
+        const uint32_t* row = table + size_t(keyed_key(K, x)) * tpad;
+        const double p = keyed_finish(K, keyed_sum(S, K, row, kc));
+        pred[idx] = p;
+        if (sel.hist) atomicAdd(&shist[sel_bin(p, sel)], 1u);
+        if (ids) {
+            Knobs c;
+            c.r[0] = til0[x.t0];
+            c.r[1] = til1[x.t1];
+            c.r[2] = til2[x.t2];
+            c.k_tile = divk[x.k];
+            c.unroll = 1u << x.u;
+            c.vec = 1u << x.v;
+            ids[idx] = candidate_hash(K.fnv_prefix, c);
+        }
+    }
+    if (sel.hist) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) {
+            const uint32_t v = shist[i];
+            if (v) atomicAdd(sel.hist + i, v);
+        }
+    }
+}
+
 // ----------------------------------------------------------------- predict
 __global__ void __launch_bounds__(kThreads) predict_kernel(const uint8_t* __restrict__ gblob,
                                                            const double* __restrict__ feat, int64_t n,
@@ -680,6 +844,73 @@ cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t by
     if (n <= 0) return cudaSuccess;
     return mask_bits == 32 ? launch_score_t<uint32_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm, sel)
                            : launch_score_t<uint64_t>(c, d_score, bytes, d_genome, n, d_pred, d_ids, fp, per_sm, sel);
+}
+
+cudaError_t score_keyed_occupancy(uint32_t bytes, int* per_sm) {
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa{};
+    cudaError_t e = cudaFuncGetAttributes(&fa, score_keyed_kernel);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(score_keyed_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - int(fa.sharedSizeBytes));
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, score_keyed_kernel, kKeyedThreads, bytes);
+    if (e != cudaSuccess) return e;
+    return *per_sm < 1 ? cudaErrorInvalidConfiguration : cudaSuccess;
+}
+
+cudaError_t launch_key_sort(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, int nkeys,
+                            uint32_t* d_counts, uint32_t* d_cursor, uint32_t* d_order) {
+    if (n <= 0) return cudaSuccess;
+    if (nkeys > kMaxSortKeys) return cudaErrorInvalidValue;
+    static std::once_flag once;
+    static cudaError_t attr = cudaSuccess;
+    std::call_once(once, [] {
+        attr = cudaFuncSetAttribute(key_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortKeys * 4);
+        if (attr == cudaSuccess)
+            attr = cudaFuncSetAttribute(key_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        kMaxSortKeys * 8);
+    });
+    if (attr != cudaSuccess) return attr;
+    const int64_t chunk = int64_t(kSortT) * kSortPer;
+    int64_t g1 = (n + kSortT - 1) / kSortT;
+    if (g1 > int64_t(c.sm_count) * 4) g1 = int64_t(c.sm_count) * 4;
+    int64_t g3 = (n + chunk - 1) / chunk;
+    if (g3 > int64_t(c.sm_count) * 8) g3 = int64_t(c.sm_count) * 8;
+    cudaError_t e = launch_pdl(key_hist_kernel, dim3(unsigned(g1)), dim3(kSortT), size_t(nkeys) * 4, c.stream, d_genome,
+                               n, uint32_t(nt1), uint32_t(nt2), uint32_t(nkeys), d_counts);
+    if (e == cudaSuccess)
+        e = launch_pdl(key_scan_kernel, dim3(1), dim3(1024), 0, c.stream, d_counts, uint32_t(nkeys), d_cursor);
+    if (e == cudaSuccess)
+        e = launch_pdl(key_place_kernel, dim3(unsigned(g3)), dim3(kSortT), size_t(nkeys) * 8, c.stream, d_genome, n,
+                       uint32_t(nt1), uint32_t(nt2), uint32_t(nkeys), d_cursor, d_order);
+    note_launches(3);
+    return e;
+}
+
+cudaError_t launch_keygen(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, uint64_t* keys,
+                          uint32_t* vals) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + kKeyedThreads - 1) / kKeyedThreads;
+    const int64_t cap = int64_t(c.sm_count) * 8;
+    const int grid = int(want < cap ? want : cap);
+    note_launches(1);
+    return launch_pdl(keygen_kernel, dim3(grid), dim3(kKeyedThreads), 0, c.stream, d_genome, n, uint32_t(nt1),
+                      uint32_t(nt2), keys, vals);
+}
+
+cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint32_t* d_table,
+                               const uint64_t* d_genome, const uint32_t* d_order, int64_t n, double* d_pred,
+                               uint64_t* d_ids, int per_sm, const SelHist& sel) {
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + kKeyedThreads - 1) / kKeyedThreads;
+    const int64_t cap = int64_t(c.sm_count) * per_sm;
+    const int grid = int(want < cap ? want : cap);
+    note_launches(1);
+    return launch_pdl(score_keyed_kernel, dim3(grid), dim3(kKeyedThreads), bytes, c.stream, d_kblob, bytes, d_table,
+                      d_genome, d_order, n, d_pred, d_ids, sel);
 }
 
 int score_static_smem() {

@@ -210,6 +210,62 @@ __host__ __device__ __forceinline__ double forest_sum_pairs(const uint8_t* S, co
     return sum;
 }
 
+// Keyed form (KeyedHdr, etune_internal.hpp): sum of leaf values in tree order from the
+// candidate's key-table row (non-Kuv channels, 4 trees per 16-byte load) and its Kuv
+// class.  `row` is global memory on the device (read-only path), host memory in tests.
+#if defined(__CUDA_ARCH__)
+__device__ __forceinline__ uint4 ld_row4(const uint32_t* row, int q) {
+    return __ldg(reinterpret_cast<const uint4*>(row) + q);
+}
+#else
+struct RowQuad {
+    uint32_t x, y, z, w;
+};
+inline RowQuad ld_row4(const uint32_t* row, int q) { return RowQuad{row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]}; }
+#endif
+
+__host__ __device__ __forceinline__ double keyed_leaf(SAddr leaf_base, SAddr kuv_base, uint32_t stride, int t,
+                                                      uint32_t mrow) {
+    const uint32_t m = mrow & lds32(kuv_base + uint32_t(t) * stride);
+    const uint32_t slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
+    const SAddr blk = leaf_base + uint32_t(t) * 256u + slot * 4u;
+    return join_f64(lds32(blk), lds32(blk + 128u));
+}
+
+__host__ __device__ __forceinline__ double keyed_sum(const uint8_t* KB, const KeyedHdr& K, const uint32_t* row,
+                                                     uint32_t kc) {
+    const SAddr base = blob_saddr(KB);
+    const SAddr leaf = base + K.off_leaves;
+    const SAddr kuv = base + K.off_kuvtab + kc * 4u;
+    const uint32_t stride = uint32_t(K.nkc) * 4u;
+    const int T = K.ntrees;
+    double sum = 0.0;
+    int t = 0;
+    for (; t + 4 <= T; t += 4) {
+        const auto m4 = ld_row4(row, t >> 2);
+        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t, m4.x));
+        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 1, m4.y));
+        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 2, m4.z));
+        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 3, m4.w));
+    }
+    if (t < T) {  // 1-3 trees left (no runtime-indexed array: keeps the row in registers)
+        const auto m4 = ld_row4(row, t >> 2);
+        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t, m4.x));
+        if (t + 1 < T) sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 1, m4.y));
+        if (t + 2 < T) sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 2, m4.z));
+    }
+    return sum;
+}
+
+__host__ __device__ __forceinline__ uint32_t keyed_key(const KeyedHdr& K, const Genome& x) {
+    return (x.t0 * uint32_t(K.nt[1]) + x.t1) * uint32_t(K.nt[2]) + x.t2;
+}
+
+__host__ __device__ __forceinline__ double keyed_finish(const KeyedHdr& K, double sum) {
+    const double p = ETUNE_DADD(K.base, ETUNE_DMUL(K.lr, sum));  // energy_model.cpp:248
+    return (1e-6 < p) ? p : 1e-6;
+}
+
 __host__ __device__ __forceinline__ double finish_prediction(const ScoreHdr& H, double sum) {
     const double p = ETUNE_DADD(H.base, ETUNE_DMUL(H.lr, sum));  // energy_model.cpp:248
     return (1e-6 < p) ? p : 1e-6;                                // std::max(kPredictionFloor, p)

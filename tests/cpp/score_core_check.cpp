@@ -17,11 +17,12 @@ static thread_local std::string g_err;
 
 extern "C" const char* scc_last_error() { return g_err.c_str(); }
 
-// returns 0 ok; stats_out[8] like etune_cu_forest_compile_stats
-extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* feature, const double* threshold,
-                         const int32_t* left, const int32_t* right, const double* value, const int64_t* offsets,
-                         int64_t num_trees, double base, double lr, const int64_t* sched, int64_t n, double* out,
-                         int64_t* stats_out) {
+// returns 0 ok; stats_out[8] like etune_cu_forest_compile_stats.  keyed: score through the
+// keyed form (KeyedHdr + key table, score_core.hpp keyed_sum) instead of the class tables.
+static int score_impl(const int64_t* op_words, int num_sms, const int32_t* feature, const double* threshold,
+                      const int32_t* left, const int32_t* right, const double* value, const int64_t* offsets,
+                      int64_t num_trees, double base, double lr, const int64_t* sched, int64_t n, double* out,
+                      int64_t* stats_out, int keyed) {
     etune_op_spec op;
     std::memcpy(&op, op_words, sizeof(op));
     etune_device_config d{};
@@ -41,7 +42,16 @@ extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* fe
     F.lr = lr;
     std::vector<uint8_t> blob;
     ScoreStats S;
-    if (int st = build_score_blob(F, P, &blob, &S, &g_err)) return st;
+    KeyedBuild KBd;
+    if (int st = build_score_blob(F, P, &blob, &S, &g_err, keyed ? &KBd : nullptr)) return st;
+    if (keyed && !KBd.ok) {
+        g_err = "keyed form unavailable";
+        return ETUNE_ERR_UNSUPPORTED;
+    }
+    struct alignas(16) KChunk { unsigned char b[16]; };
+    std::vector<KChunk> kal(keyed ? (KBd.blob.size() + 15) / 16 : 0);
+    if (keyed) std::memcpy(kal.data(), KBd.blob.data(), KBd.blob.size());
+    const uint8_t* KB = keyed ? reinterpret_cast<const uint8_t*>(kal.data()) : nullptr;
     // 16-byte aligned copy, like the kernel's smem stage
     struct alignas(16) Chunk { unsigned char b[16]; };
     std::vector<Chunk> aligned((blob.size() + 15) / 16);
@@ -65,7 +75,16 @@ extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* fe
         const uint32_t k = uint32_t(std::lower_bound(P.divk.begin(), P.divk.end(), s[9]) - P.divk.begin());
         const uint32_t u = uint32_t(__builtin_ctzll(uint64_t(s[10])));
         const uint32_t v = uint32_t(__builtin_ctzll(uint64_t(s[11])));
-        const CandClasses cc = candidate_classes(B, H, genome_pack(ti[0], ti[1], ti[2], k, u, v));
+        const uint64_t gnm = genome_pack(ti[0], ti[1], ti[2], k, u, v);
+        if (keyed) {
+            const KeyedHdr& KH = *reinterpret_cast<const KeyedHdr*>(KB);
+            const Genome x = genome_unpack(gnm);
+            const uint32_t kc = KB[KH.off_clskuv + (x.k * 16u + x.u) * 4u + x.v];
+            const uint32_t* row = KBd.table.data() + size_t(keyed_key(KH, x)) * size_t(KH.tpad);
+            out[i] = keyed_finish(KH, keyed_sum(KB, KH, row, kc));
+            continue;
+        }
+        const CandClasses cc = candidate_classes(B, H, gnm);
         const TreeRec* trees = blob_at<TreeRec>(B, H.off_trees);
         const double sum = H.npairs > 0 ? forest_sum_pairs(B, H, blob_at<PairRec>(B, H.off_trees), cc.c)
                            : H.mask_bits == 32 ? forest_sum<uint32_t>(B, H, trees, cc.c)
@@ -83,4 +102,20 @@ extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* fe
         stats_out[7] = num_trees;
     }
     return 0;
+}
+
+extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* feature, const double* threshold,
+                         const int32_t* left, const int32_t* right, const double* value, const int64_t* offsets,
+                         int64_t num_trees, double base, double lr, const int64_t* sched, int64_t n, double* out,
+                         int64_t* stats_out) {
+    return score_impl(op_words, num_sms, feature, threshold, left, right, value, offsets, num_trees, base, lr, sched,
+                      n, out, stats_out, 0);
+}
+
+extern "C" int scc_score_keyed(const int64_t* op_words, int num_sms, const int32_t* feature, const double* threshold,
+                               const int32_t* left, const int32_t* right, const double* value,
+                               const int64_t* offsets, int64_t num_trees, double base, double lr,
+                               const int64_t* sched, int64_t n, double* out, int64_t* stats_out) {
+    return score_impl(op_words, num_sms, feature, threshold, left, right, value, offsets, num_trees, base, lr, sched,
+                      n, out, stats_out, 1);
 }

@@ -538,18 +538,20 @@ def have_ref() -> bool:
 SCC_SO = os.path.join(ROOT, "tests", "cpp", "libscorecheck.so")
 
 
-def host_compiled_score(op, forest: "FlatForest", sched, num_sms=108):
-    """Forest compiler + scoring core run on the CPU (tests/cpp/score_core_check.cpp)."""
+def host_compiled_score(op, forest: "FlatForest", sched, num_sms=108, keyed=False):
+    """Forest compiler + scoring core run on the CPU (tests/cpp/score_core_check.cpp);
+    keyed=True scores through the keyed form (per-tiling-triple key table)."""
     L = C.CDLL(SCC_SO)
     L.scc_last_error.restype = C.c_char_p
-    L.scc_score.argtypes = [I64P, C.c_int, I32P, F64P, I32P, I32P, F64P, I64P, C.c_int64, C.c_double, C.c_double,
-                            I64P, C.c_int64, F64P, I64P]
+    fn = L.scc_score_keyed if keyed else L.scc_score
+    fn.argtypes = [I64P, C.c_int, I32P, F64P, I32P, I32P, F64P, I64P, C.c_int64, C.c_double, C.c_double,
+                   I64P, C.c_int64, F64P, I64P]
     sched = np.ascontiguousarray(sched, np.int64).reshape(-1, 12)
     out = np.zeros(len(sched))
     stats = np.zeros(8, np.int64)
     f = forest
-    st = L.scc_score(np.ascontiguousarray(op, np.int64), num_sms, f.feature, f.threshold, f.left, f.right, f.value,
-                     f.offsets, f.num_trees, f.base_score, f.learning_rate, sched, len(sched), out, stats)
+    st = fn(np.ascontiguousarray(op, np.int64), num_sms, f.feature, f.threshold, f.left, f.right, f.value,
+            f.offsets, f.num_trees, f.base_score, f.learning_rate, sched, len(sched), out, stats)
     if st:
         raise EtuneError(st, L.scc_last_error().decode())
     return out, stats

@@ -25,13 +25,28 @@ def test_compiled_golden(golden, name):
 
 @pytest.mark.parametrize("name", MODEL_OPS)
 @pytest.mark.parametrize("sms", [108, 148])
-def test_compiled_bred_population(golden, oracle, name, sms):
+@pytest.mark.parametrize("keyed", [False, True])
+def test_compiled_bred_population(golden, oracle, name, sms, keyed):
     op = golden[f"{name}/op"]
     fl = forest_of(golden, name)
     par, _ = oracle.sample_random(op, 128, 11)
     s, _, _, _ = oracle.reproduce(op, par, 20000, 3)
     ref = oracle.predict(fl, oracle.features(op, s, sms))
-    pred, _ = host_compiled_score(op, fl, s, sms)
+    pred, _ = host_compiled_score(op, fl, s, sms, keyed=keyed)
+    assert (pred.view(np.uint64) == ref.view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("src,dst", [("c3_bert_ffn", "conv:1,7,7,512,512,3,1,1"), ("c2_r50_conv3x3", "mm:4,96,200,50"),
+                                     ("c1_gemm1024", "conv:2,14,14,64,32,3,1,1")])
+def test_keyed_form_cross_operator(golden, oracle, src, dst):
+    """The keyed form (per tiling-triple AND of non-Kuv masks) on other operators,
+    incl. batch > 1 (three-index keys)."""
+    op = parse_op(dst)
+    fl = forest_of(golden, src)
+    n = min(5000, oracle.count(op))
+    s, _ = oracle.sample_random(op, n, 21)
+    ref = oracle.predict(fl, oracle.features(op, s))
+    pred, _ = host_compiled_score(op, fl, s, keyed=True)
     assert (pred.view(np.uint64) == ref.view(np.uint64)).all()
 
 

@@ -140,5 +140,38 @@ def test_profile_score_events(oracle, ctx, capi, setup):
     capi.profile_score(ctx, True)
     for _ in range(3):
         forest.score_select(plan, g, 64, pred, idx)
-    ms, sel_ms, cnt = capi.profile_score(ctx, False)
-    assert cnt == 3 and ms > 0.0 and sel_ms > 0.0
+    sort_ms, ms, sel_ms, cnt = capi.profile_score(ctx, False)
+    assert cnt == 3 and ms > 0.0 and sel_ms > 0.0 and sort_ms > 0.0
+
+
+@pytest.mark.parametrize("text,model", [("conv:1,56,56,64,64,3,1,1", "c2_r50_conv3x3"),
+                                        ("mm:1,1024,1024,1024", "c1_gemm1024"),
+                                        ("mm:1,512,3072,768", "c3_bert_ffn"),
+                                        ("conv:4,14,14,64,32,3,1,1", "c2_r50_conv3x3")])
+def test_keyed_path_matches_class_tables_and_oracle(golden, oracle, ctx, capi, text, model):
+    """The keyed path (key sort + key-table rows) and the class-table kernel give the
+    same bits as the oracle, for scores, ids and the selection."""
+    k = f"{model}/model/"
+    flat = FlatForest(golden[k + "feature"], golden[k + "threshold"], golden[k + "left"], golden[k + "right"],
+                      golden[k + "value"], golden[k + "offsets"], float(golden[k + "base_score"][0]),
+                      float(golden[k + "learning_rate"][0]))
+    op = parse_op(text)
+    plan = capi.Plan(ctx, op)
+    n = 100000
+    par, _ = oracle.sample_random(op, 512, 3)
+    sched, ids_ref, _, _ = oracle.reproduce(op, par, n, 17)
+    p_ref = oracle.predict(flat, oracle.features(op, sched))
+    g = plan.encode(dev(sched))
+    outs = []
+    for keyed in (True, False):
+        fo = capi.Forest.from_flat(ctx, flat).set_keyed(keyed)
+        pred = torch.empty(n, dtype=torch.float64, device="cuda")
+        ids = torch.empty(n, dtype=torch.int64, device="cuda")
+        idx = torch.empty(1024, dtype=torch.int64, device="cuda")
+        fo.score_select(plan, g, 1024, pred, idx, ids=ids)
+        ctx.synchronize()
+        outs.append((pred.cpu().numpy(), capi.as_u64(ids), idx.cpu().numpy()))
+    for pred, ids, idx in outs:
+        assert (pred.view(np.uint64) == p_ref.view(np.uint64)).all()
+        assert (ids == ids_ref).all()
+        assert (idx == oracle.topk(p_ref, 1024)).all()
