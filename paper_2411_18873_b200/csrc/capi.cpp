@@ -9,6 +9,7 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -274,14 +275,14 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
         CU(launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
                              d_pred, d_ids));
     } else if (use_keyed(f, cs, n)) {
-        // key = tiling triple; grouping by key gives warps candidates that share
-        // key-table rows; results land at the original indices
-        const int nk = cs->nkeys;
-        const bool counting = nk <= kMaxSortKeys;
-        const size_t obytes = (4 * size_t(n) + 255) & ~size_t(255);
-        const size_t kbytes = counting ? 0 : (8 * size_t(n) + 255) & ~size_t(255);
+        // key = tiling triple; grouping by key (folded into <= 1024 bins) gives warps
+        // candidates that share key-table rows; results land at the original indices.
+        // layout: [counts | cursor] at a fixed offset (the counts stay zeroed between
+        // calls whatever n is), the order, the genomes in bin order
+        const int nbins = cs->nkeys;
         const size_t cbytes = (8 * size_t(kMaxSortKeys) + 255) & ~size_t(255);
-        const size_t need = obytes + kbytes + cbytes + (counting ? 0 : sort_pairs_scratch_bytes(n));
+        const size_t obytes = (4 * size_t(n) + 255) & ~size_t(255);
+        const size_t need = cbytes + obytes + 8 * size_t(n);
         if (c->ksort_bytes < need) {
             if (c->ksort) {
                 CU(cudaStreamSynchronize(c->stream));
@@ -291,23 +292,21 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
             }
             CU(cudaMalloc(&c->ksort, need));
             c->ksort_bytes = need;
-            CU(cudaMemsetAsync(c->ksort, 0, need, c->stream));  // counting-sort counts start at zero
+            CU(cudaMemsetAsync(c->ksort, 0, cbytes, c->stream));  // counting-sort counts start at zero
         }
-        // layout: [counts | cursor] at a fixed offset (the counts stay zeroed between
-        // calls whatever n is), then the order, then the radix-sort keys and scratch
         char* kp = static_cast<char*>(c->ksort);
         auto* counts = reinterpret_cast<uint32_t*>(kp);
         auto* order = reinterpret_cast<uint32_t*>(kp + cbytes);
-        if (counting) {
-            CU(launch_key_sort(c->lc(), d_genome, n, cs->nt1, cs->nt2, nk, counts, counts + kMaxSortKeys, order));
-        } else {
-            auto* keys = reinterpret_cast<uint64_t*>(kp + cbytes + obytes);
-            CU(launch_keygen(c->lc(), d_genome, n, cs->nt1, cs->nt2, keys, order));
-            CU(launch_sort_pairs(c->lc(), keys, order, n, cs->key_bits, kp + cbytes + obytes + kbytes));
-        }
+        auto* sgen = reinterpret_cast<uint64_t*>(kp + cbytes + obytes);
+        static const int grp = std::getenv("ETUNE_KEYED_SORT") ? std::atoi(std::getenv("ETUNE_KEYED_SORT")) : 2;
+        const bool nosort = grp == 0;  // EXPERIMENT
+        if (grp == 1) CU(launch_key_group(c->lc(), d_genome, n, cs->nt1, cs->nt2, nbins, counts, sgen, order));
+        if (grp == 2)
+            CU(launch_key_sort(c->lc(), d_genome, n, cs->nt1, cs->nt2, nbins, counts, counts + kMaxSortKeys, sgen,
+                               order));
         if (ev) CU(cudaEventRecord(ev[1], c->stream));
-        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, d_genome, order, n, d_pred, d_ids,
-                              cs->keyed_per_sm, sel));
+        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, nosort ? d_genome : sgen,
+                              nosort ? nullptr : order, n, d_pred, d_ids, cs->keyed_per_sm, sel));
     } else {
         if (ev) CU(cudaEventRecord(ev[1], c->stream));
         CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,

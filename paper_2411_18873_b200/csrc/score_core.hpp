@@ -241,15 +241,17 @@ __host__ __device__ __forceinline__ double keyed_sum(const uint8_t* KB, const Ke
     const int T = K.ntrees;
     double sum = 0.0;
     int t = 0;
+    // the row is read one quad ahead (its loads come from L1/L2)
+    auto m4 = ld_row4(row, 0);
     for (; t + 4 <= T; t += 4) {
-        const auto m4 = ld_row4(row, t >> 2);
+        const auto nx = ld_row4(row, t + 4 < K.tpad ? (t >> 2) + 1 : (t >> 2));
         sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t, m4.x));
         sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 1, m4.y));
         sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 2, m4.z));
         sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 3, m4.w));
+        m4 = nx;
     }
     if (t < T) {  // 1-3 trees left (no runtime-indexed array: keeps the row in registers)
-        const auto m4 = ld_row4(row, t >> 2);
         sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t, m4.x));
         if (t + 1 < T) sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 1, m4.y));
         if (t + 2 < T) sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 2, m4.z));
