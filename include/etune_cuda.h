@@ -263,17 +263,18 @@ etune_status etune_cu_score_select(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                    int64_t* d_idx);
 
 /* Device time, summed over the etune_cu_score_select calls since the last call, of
- * (a) the key sort of the keyed path (0 on the class-table path), (b) the score kernel,
+ * (a) work before the score kernel (0 on the current paths), (b) the score kernel,
  * (c) the selection kernels (CUDA events on the ctx stream; synchronises when any were
  * recorded); then switches that timing on (on != 0) or off.  For benchmarks and
  * profiling (the events serialise the launches they separate). */
-etune_status etune_cu_profile_score(etune_cu_ctx* ctx, int on, double* sort_ms /*nullable*/,
+etune_status etune_cu_profile_score(etune_cu_ctx* ctx, int on, double* pre_ms /*nullable*/,
                                     double* score_ms /*nullable*/, double* select_ms /*nullable*/,
                                     int64_t* calls /*nullable*/);
 
-/* Scoring form for populations of >= 2^15 candidates: 1 (default) = keyed path (per
- * tiling-triple key table in global memory, population visited in key order after a
- * stable radix sort by key), 0 = class-table kernel only.  Both are bit-identical. */
+/* Scoring form: 1 (default) = keyed path where the forest compiles to it (one byte per
+ * (tiling triple, tree) in an L2-resident key table: <= 128 trees of <= 32 leaves,
+ * <= 256 distinct non-Kuv masks per Kuv tree, table <= 64 MB), 0 = class-table kernel
+ * only.  Both are bit-identical. */
 etune_status etune_cu_forest_set_keyed(etune_cu_forest* forest, int mode);
 
 /* Reference-facing end-to-end call with HOST buffers: schedules in the reference's

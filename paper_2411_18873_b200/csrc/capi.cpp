@@ -38,7 +38,6 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->breed);
     cudaFree(c->shard);
     cudaFree(c->sel);
-    cudaFree(c->ksort);
     if (c->hpin) cudaFreeHost(c->hpin);
     c->pool.reset();
     for (auto& e : c->prof_ev)
@@ -239,12 +238,12 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     selection_buckets(f->host, &cs.sel_kmin, &cs.sel_shift);
     if (kb.ok && kb.blob.size() <= size_t(cap)) {
         CU(cudaMalloc(&cs.d_kblob, kb.blob.size()));
-        CU(cudaMalloc(&cs.d_ktable, kb.table.size() * 4));
+        CU(cudaMalloc(&cs.d_ktable, kb.table.size()));
         CU(cudaMemcpyAsync(cs.d_kblob, kb.blob.data(), kb.blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
-        CU(cudaMemcpyAsync(cs.d_ktable, kb.table.data(), kb.table.size() * 4, cudaMemcpyHostToDevice,
-                           f->ctx->stream));
+        CU(cudaMemcpyAsync(cs.d_ktable, kb.table.data(), kb.table.size(), cudaMemcpyHostToDevice, f->ctx->stream));
         CU(cudaStreamSynchronize(f->ctx->stream));
         cs.kbytes = uint32_t(kb.blob.size());
+        cs.kparams = std::make_shared<KeyedParams>(kb.params);
         cs.key_bits = kb.key_bits;
         cs.nkeys = int(kb.nkeys);
         cs.nt1 = p->build.hdr.nt[1];
@@ -257,15 +256,12 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     return ETUNE_OK;
 }
 
-// Populations at least this large take the keyed path (its key sort is a fixed cost).
-constexpr int64_t kKeyedMinN = int64_t(1) << 15;
-
 bool use_keyed(const etune_cu_forest* f, const CompiledScore* cs, int64_t n) {
-    return cs->keyed && f->keyed_mode != 0 && n >= kKeyedMinN && n < (int64_t(1) << 32);
+    return cs->keyed && f->keyed_mode != 0 && n < (int64_t(1) << 32);
 }
 
-// Scoring pass of any compiled form; `ev` (nullable) = {before the key sort, before the
-// score kernel, after it} for etune_cu_profile_score.
+// Scoring pass of any compiled form; `ev` (nullable) = {start, before the score kernel,
+// after it} for etune_cu_profile_score.
 etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
                             const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
                             const SelHist& sel, const cudaEvent_t* ev) {
@@ -275,38 +271,12 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
         CU(launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
                              d_pred, d_ids));
     } else if (use_keyed(f, cs, n)) {
-        // key = tiling triple; grouping by key (folded into <= 1024 bins) gives warps
-        // candidates that share key-table rows; results land at the original indices.
-        // layout: [counts | cursor] at a fixed offset (the counts stay zeroed between
-        // calls whatever n is), the order, the genomes in bin order
-        const int nbins = cs->nkeys;
-        const size_t cbytes = (8 * size_t(kMaxSortKeys) + 255) & ~size_t(255);
-        const size_t obytes = (4 * size_t(n) + 255) & ~size_t(255);
-        const size_t need = cbytes + obytes + 8 * size_t(n);
-        if (c->ksort_bytes < need) {
-            if (c->ksort) {
-                CU(cudaStreamSynchronize(c->stream));
-                CU(cudaFree(c->ksort));
-                c->ksort = nullptr;
-                c->ksort_bytes = 0;
-            }
-            CU(cudaMalloc(&c->ksort, need));
-            c->ksort_bytes = need;
-            CU(cudaMemsetAsync(c->ksort, 0, cbytes, c->stream));  // counting-sort counts start at zero
-        }
-        char* kp = static_cast<char*>(c->ksort);
-        auto* counts = reinterpret_cast<uint32_t*>(kp);
-        auto* order = reinterpret_cast<uint32_t*>(kp + cbytes);
-        auto* sgen = reinterpret_cast<uint64_t*>(kp + cbytes + obytes);
-        static const int grp = std::getenv("ETUNE_KEYED_SORT") ? std::atoi(std::getenv("ETUNE_KEYED_SORT")) : 2;
-        const bool nosort = grp == 0;  // EXPERIMENT
-        if (grp == 1) CU(launch_key_group(c->lc(), d_genome, n, cs->nt1, cs->nt2, nbins, counts, sgen, order));
-        if (grp == 2)
-            CU(launch_key_sort(c->lc(), d_genome, n, cs->nt1, cs->nt2, nbins, counts, counts + kMaxSortKeys, sgen,
-                               order));
         if (ev) CU(cudaEventRecord(ev[1], c->stream));
-        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, nosort ? d_genome : sgen,
-                              nosort ? nullptr : order, n, d_pred, d_ids, cs->keyed_per_sm, sel));
+        // candidates in population order: each reads its own 112-byte key-table row (L2);
+        // grouping the population by key first was measured slower (the sort costs more
+        // than the broadcast rows save)
+        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, d_genome, nullptr, n, d_pred, d_ids,
+                              cs->keyed_per_sm, *cs->kparams, sel));
     } else {
         if (ev) CU(cudaEventRecord(ev[1], c->stream));
         CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,

@@ -173,24 +173,38 @@ struct ScoreHdr {
 
 // --------------------------------------------------------- keyed score blob
 // Every channel except Kuv is a function of the three tiling indices alone, so the
-// forest compiler evaluates, per tiling triple ("key"), the AND of each tree's non-Kuv
-// channel masks: table[key][tree] (u32, global memory, L2-resident).  On the device a
-// candidate needs one 16-byte row load per 4 trees (broadcast when a warp's candidates
-// share the key — the population is sorted by key first), one Kuv-mask load per tree
-// and the leaf value.  Blob (shared memory): header, tilings, divisors of K, the Kuv
-// class table, per-tree Kuv masks [tree][kuv class] and the leaf blocks.
+// forest compiler evaluates, per tiling triple ("key"), each tree's AND of its non-Kuv
+// channel masks M_t(key) and stores one byte per (key, tree) in a key table in global
+// memory (L2-resident, rows of `row_bytes`, 16-byte aligned):
+//   trees that do not test Kuv: the exit leaf's de Bruijn slot of M_t(key) itself;
+//   trees that do:              the index of M_t(key) in the tree's list of distinct
+//                               masks (<= 256; lists packed, per-tree start in the
+//                               kernel-parameter bank), ANDed on the device with the
+//                               tree's Kuv-class mask.
+// A candidate reads its row with 16-byte loads (16 trees each), so the per-tree work is
+// one or three shared loads (+ the two leaf words) instead of one table load per channel.
+// Blob (shared memory): header, tilings, divisors of K, Kuv class table, Kuv flags,
+// packed mask lists, Kuv masks [tree][nkc], leaf blocks (32 hi + 32 lo words/tree).
 struct KeyedHdr {
     int64_t K;
     uint64_t fnv_prefix;
     double base, lr;
-    int32_t ntrees, tpad, nkc, key_bits;
-    int32_t nt[3], nd[3], ndk, pad;
+    int32_t ntrees, row_bytes, nkc, pad0;
+    int32_t nt[3], nd[3], ndk, pad1;
+    uint32_t kuv_flags[4];  // bit t: tree t tests Kuv (ntrees <= 128)
     uint32_t off_til[3];
     uint32_t off_divk;
     uint32_t off_clskuv;   // uint8 [(k*16+u)*4+v] -> Kuv class
+    uint32_t off_mlist;    // uint32: distinct non-Kuv masks of the Kuv trees, tree after tree
     uint32_t off_kuvtab;   // uint32 [tree][nkc]
     uint32_t off_leaves;   // per tree 32 high words then 32 low words, de Bruijn slots
-    uint32_t total;
+    uint32_t total, pad2;
+};
+constexpr int kKeyedMaxTrees = 128;
+struct KeyedParams {       // kernel parameter (constant bank: warp-uniform reads cost no shared-memory issue)
+    uint32_t moff[kKeyedMaxTrees];  // byte offset of tree t's mask list from the blob start
+    uint32_t kuv_flags[4];          // copy of KeyedHdr::kuv_flags
+    uint32_t off_kuvtab, off_leaves, nkc, ntrees;
 };
 
 // ------------------------------------------------------- generic predict blob

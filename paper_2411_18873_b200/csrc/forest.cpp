@@ -485,64 +485,107 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
     std::memcpy(blob->data(), &H, sizeof(H));
     if (stats) *stats = S;
 
-    // ---- keyed form: per tiling triple, each tree's AND of its non-Kuv channel masks
+    // ---- keyed form: per tiling triple, each tree's AND of its non-Kuv channel masks,
+    // as one byte per tree (the exit slot, or the index of the mask for Kuv trees)
     if (keyed) {
         keyed->ok = false;
         const int64_t nk = int64_t(PH.nt[0]) * PH.nt[1] * PH.nt[2];
-        const int tpad = int((T + 3) / 4 * 4);
-        if (mbits == 32 && T > 0 && nk > 0 && size_t(nk) * size_t(tpad) * 4 <= max_table_bytes) {
+        const int row_bytes = int((T + 15) / 16 * 16);
+        if (mbits == 32 && T > 0 && T <= kKeyedMaxTrees && nk > 0 &&
+            size_t(nk) * size_t(row_bytes) <= max_table_bytes) {
             keyed->nkeys = nk;
             int kb = 0;
             while ((int64_t(1) << kb) < nk) ++kb;
             keyed->key_bits = kb;
-            keyed->table.assign(size_t(nk) * size_t(tpad), 0xffffffffu);
+            keyed->table.assign(size_t(nk) * size_t(row_bytes), 0);
+            std::vector<std::map<uint32_t, int>> mcode(static_cast<size_t>(T));
+            std::vector<std::vector<uint32_t>> mlists(static_cast<size_t>(T));
+            bool fits = true;
             const uint8_t* B = blob->data();  // the finished score blob: classes exactly as the device derives them
-            for (int64_t t0 = 0; t0 < PH.nt[0]; ++t0)
-                for (int64_t t1 = 0; t1 < PH.nt[1]; ++t1)
-                    for (int64_t t2 = 0; t2 < PH.nt[2]; ++t2) {
+            for (int64_t t0 = 0; t0 < PH.nt[0] && fits; ++t0)
+                for (int64_t t1 = 0; t1 < PH.nt[1] && fits; ++t1)
+                    for (int64_t t2 = 0; t2 < PH.nt[2] && fits; ++t2) {
                         const CandClasses cc =
                             candidate_classes(B, H, genome_pack(uint32_t(t0), uint32_t(t1), uint32_t(t2), 0, 0, 0));
                         const int64_t key = (t0 * PH.nt[1] + t1) * PH.nt[2] + t2;
-                        uint32_t* row = keyed->table.data() + size_t(key) * size_t(tpad);
+                        uint8_t* row = keyed->table.data() + size_t(key) * size_t(row_bytes);
                         for (int64_t t = 0; t < T; ++t) {
                             uint64_t m = full;
                             for (int c = 0; c < kNumChannels; ++c)
                                 if (c != kChKuv && ((tree_used[size_t(t)] >> c) & 1u))
                                     m &= tree_tl[size_t(t)][size_t(c)][cc.c[c]];
-                            row[t] = uint32_t(m);
+                            const uint32_t m32 = uint32_t(m);
+                            if ((tree_used[size_t(t)] >> kChKuv) & 1u) {
+                                auto& mc = mcode[size_t(t)];
+                                auto it = mc.find(m32);
+                                int code;
+                                if (it == mc.end()) {
+                                    code = int(mc.size());
+                                    if (code >= 256) {
+                                        fits = false;
+                                        break;
+                                    }
+                                    mc.emplace(m32, code);
+                                    mlists[size_t(t)].push_back(m32);
+                                } else {
+                                    code = it->second;
+                                }
+                                row[t] = uint8_t(code);
+                            } else {
+                                // exit leaf = lowest set bit; unreachable keys (m == 0) never occur
+                                row[t] = uint8_t(((m32 & (0u - m32)) * 0x077CB531u) >> 27);
+                            }
                         }
                     }
-            const int nkc = int(rep[kChKuv].size());
-            std::vector<uint32_t> kuvtab(size_t(tpad) * size_t(nkc), 0xffffffffu);
-            for (int64_t t = 0; t < T; ++t)
-                if ((tree_used[size_t(t)] >> kChKuv) & 1u)
-                    for (int x = 0; x < nkc; ++x)
-                        kuvtab[size_t(t) * size_t(nkc) + size_t(x)] = uint32_t(tree_tl[size_t(t)][kChKuv][size_t(x)]);
-            KeyedHdr K{};
-            K.K = PH.K;
-            K.fnv_prefix = PH.fnv_prefix;
-            K.base = F.base;
-            K.lr = F.lr;
-            K.ntrees = int32_t(T);
-            K.tpad = tpad;
-            K.nkc = nkc;
-            K.key_bits = kb;
-            for (int d = 0; d < 3; ++d) {
-                K.nt[d] = PH.nt[d];
-                K.nd[d] = PH.nd[d];
+            if (fits) {
+                const int nkc = int(rep[kChKuv].size());
+                std::vector<uint32_t> kuvtab(size_t(T) * size_t(nkc), 0xffffffffu);
+                KeyedHdr K{};
+                for (int64_t t = 0; t < T; ++t)
+                    if ((tree_used[size_t(t)] >> kChKuv) & 1u) {
+                        K.kuv_flags[t >> 5] |= 1u << (t & 31);
+                        for (int x = 0; x < nkc; ++x)
+                            kuvtab[size_t(t) * size_t(nkc) + size_t(x)] =
+                                uint32_t(tree_tl[size_t(t)][kChKuv][size_t(x)]);
+                    }
+                K.K = PH.K;
+                K.fnv_prefix = PH.fnv_prefix;
+                K.base = F.base;
+                K.lr = F.lr;
+                K.ntrees = int32_t(T);
+                K.row_bytes = row_bytes;
+                K.nkc = nkc;
+                for (int d = 0; d < 3; ++d) {
+                    K.nt[d] = PH.nt[d];
+                    K.nd[d] = PH.nd[d];
+                }
+                K.ndk = PH.ndk;
+                std::vector<uint8_t>& kbl = keyed->blob;
+                kbl.assign(align16(sizeof(KeyedHdr)), 0);
+                for (int d = 0; d < 3; ++d) K.off_til[d] = put(kbl, P.til[d].data(), P.til[d].size());
+                K.off_divk = put(kbl, P.divk.data(), P.divk.size());
+                K.off_clskuv = put(kbl, cls[kChKuv].data(), cls[kChKuv].size());
+                std::vector<uint32_t> mlist;
+                std::vector<uint32_t> mstart(static_cast<size_t>(T), 0u);
+                for (int64_t t = 0; t < T; ++t) {
+                    mstart[size_t(t)] = uint32_t(mlist.size());
+                    mlist.insert(mlist.end(), mlists[size_t(t)].begin(), mlists[size_t(t)].end());
+                }
+                if (mlist.empty()) mlist.push_back(0u);
+                K.off_mlist = put(kbl, mlist.data(), mlist.size());
+                for (int64_t t = 0; t < T; ++t) keyed->params.moff[t] = K.off_mlist + 4u * mstart[size_t(t)];
+                K.off_kuvtab = put(kbl, kuvtab.data(), kuvtab.size());
+                K.off_leaves = put(kbl, leaves.data(), leaves.size());  // 32 doubles (256 B) per tree, tree order
+                kbl.resize(align16(kbl.size()));
+                K.total = uint32_t(kbl.size());
+                std::memcpy(kbl.data(), &K, sizeof(K));
+                for (int w = 0; w < 4; ++w) keyed->params.kuv_flags[w] = K.kuv_flags[w];
+                keyed->params.off_kuvtab = K.off_kuvtab;
+                keyed->params.off_leaves = K.off_leaves;
+                keyed->params.nkc = uint32_t(nkc);
+                keyed->params.ntrees = uint32_t(T);
+                keyed->ok = true;
             }
-            K.ndk = PH.ndk;
-            std::vector<uint8_t>& kbl = keyed->blob;
-            kbl.assign(align16(sizeof(KeyedHdr)), 0);
-            for (int d = 0; d < 3; ++d) K.off_til[d] = put(kbl, P.til[d].data(), P.til[d].size());
-            K.off_divk = put(kbl, P.divk.data(), P.divk.size());
-            K.off_clskuv = put(kbl, cls[kChKuv].data(), cls[kChKuv].size());
-            K.off_kuvtab = put(kbl, kuvtab.data(), kuvtab.size());
-            K.off_leaves = put(kbl, leaves.data(), leaves.size());  // 32 doubles (256 B) per tree, in tree order
-            kbl.resize(align16(kbl.size()));
-            K.total = uint32_t(kbl.size());
-            std::memcpy(kbl.data(), &K, sizeof(K));
-            keyed->ok = true;
         }
     }
     return ETUNE_OK;

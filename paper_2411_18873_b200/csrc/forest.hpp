@@ -35,7 +35,8 @@ struct ScoreStats {
 struct KeyedBuild {
     bool ok = false;
     std::vector<uint8_t> blob;
-    std::vector<uint32_t> table;  // [nkeys][tpad]
+    std::vector<uint8_t> table;   // [nkeys][row_bytes]
+    KeyedParams params{};
     int64_t nkeys = 0;
     int key_bits = 0;
 };

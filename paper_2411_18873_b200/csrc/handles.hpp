@@ -37,14 +37,12 @@ struct etune_cu_ctx {
     int nranks = 1, rank = 0;
     void* shard = nullptr;  // sharded-selection records
     size_t shard_bytes = 0;
-    void* ksort = nullptr;  // keyed path: sort keys / order / radix scratch
-    size_t ksort_bytes = 0;
     void* sel = nullptr;    // fused score_select work area (histogram, bucket lists)
     size_t sel_bytes = 0;
     bool sel_dirty = false; // a score_select sequence did not complete: re-zero first
     // optional device timing of the score kernel inside score_select (bench / profiling)
     bool prof_on = false;
-    std::vector<std::array<cudaEvent_t, 4>> prof_ev;  // before key sort, before score, after score, after select
+    std::vector<std::array<cudaEvent_t, 4>> prof_ev;  // start, before score, after score, after select
     size_t prof_used = 0;
     // *_host pipelines: pinned staging of narrowed Schedule rows, packed by a host pool
     void* hpin = nullptr;
@@ -81,7 +79,8 @@ struct CompiledScore {
     bool keyed = false;
     uint8_t* d_kblob = nullptr;
     uint32_t kbytes = 0;
-    uint32_t* d_ktable = nullptr;
+    uint8_t* d_ktable = nullptr;
+    std::shared_ptr<etune_b200::KeyedParams> kparams;
     int key_bits = 0, nkeys = 0, nt1 = 0, nt2 = 0, keyed_per_sm = 1;
     etune_b200::ScoreStats stats;
 };
@@ -93,6 +92,6 @@ struct etune_cu_forest {
     uint32_t predict_bytes = 0;
     std::mutex mu;
     std::map<uint64_t, CompiledScore> compiled;  // by plan serial
-    int keyed_mode = 1;  // 1: keyed path for large populations, 0: class-table kernel only
+    int keyed_mode = 1;  // 1: keyed path where the forest compiles to it, 0: class-table kernel only
 };
 

@@ -545,208 +545,19 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
 }
 
 // ------------------------------------------------------------- keyed score
-// Candidates visited in key order (order[] from the key sort, so a warp's candidates
-// mostly share one key-table row: its 16-byte row loads are broadcasts from L1); results
-// written at the original index.  Per tree: one Kuv-mask load (a <= 32-word row per
-// tree, conflict-free), the exit slot, two leaf-word loads, one FP64 add in tree order.
+// One candidate per thread: its key-table row (16 trees per 16-byte read-only load from
+// L2/L1), its Kuv class; per tree one or three shared loads and one FP64 add in tree
+// order (score_core.hpp keyed_sum).  `order` (nullable) visits candidates in another
+// order with genome[] already in that order; results land at the original index.
 constexpr int kKeyedThreads = 256;
 
-__global__ void __launch_bounds__(kKeyedThreads) keygen_kernel(const uint64_t* __restrict__ genome, int64_t n,
-                                                               uint32_t nt1, uint32_t nt2, uint64_t* __restrict__ keys,
-                                                               uint32_t* __restrict__ vals) {
-    pdl_wait();
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const Genome x = genome_unpack(__ldg(genome + i));
-        keys[i] = (uint64_t(x.t0) * nt1 + x.t1) * nt2 + x.t2;
-        vals[i] = uint32_t(i);
-    }
-}
-
-// Counting sort of candidate indices by key (nkeys <= kMaxSortKeys): per-CTA shared
-// histograms -> global counts; one CTA scans counts into start offsets (and re-zeroes
-// the counts for the next call); placement by warp-aggregated atomics on the cursors.
-// Order inside a key group is unspecified: the score kernel's results do not depend on
-// the visiting order.
-constexpr int kSortT = 256;
-
-// sort bin of a genome: its key folded into nbins (equal keys -> equal bins)
-__device__ __forceinline__ uint32_t genome_bin(uint64_t g, uint32_t nt1, uint32_t nt2, uint32_t nbins) {
-    const Genome x = genome_unpack(g);
-    return ((x.t0 * nt1 + x.t1) * nt2 + x.t2) % nbins;
-}
-
-__global__ void __launch_bounds__(kSortT) key_hist_kernel(const uint64_t* __restrict__ genome, int64_t n,
-                                                          uint32_t nt1, uint32_t nt2, uint32_t nkeys,
-                                                          uint32_t* __restrict__ counts) {
-    extern __shared__ uint32_t sh[];
-    for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x) sh[i] = 0u;
-    __syncthreads();
-    pdl_wait();
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-        atomicAdd(&sh[genome_bin(__ldg(genome + i), nt1, nt2, nkeys)], 1u);
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < nkeys; i += blockDim.x)
-        if (sh[i]) atomicAdd(counts + i, sh[i]);
-}
-
-__global__ void __launch_bounds__(1024) key_scan_kernel(uint32_t* __restrict__ counts, uint32_t nkeys,
-                                                        uint32_t* __restrict__ cursor) {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t carry;
-    pdl_wait();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (uint32_t b = 0; b < nkeys; b += blockDim.x) {
-        const uint32_t i = b + threadIdx.x;
-        const uint32_t v = i < nkeys ? counts[i] : 0u;
-        uint32_t x = v;
-        for (int s = 1; s < 32; s <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
-            if (lane >= s) x += y;
-        }
-        if (lane == 31) wsum[warp] = x;
-        __syncthreads();
-        uint32_t before = carry;
-        for (int w = 0; w < warp; ++w) before += wsum[w];
-        if (i < nkeys) {
-            cursor[i] = before + x - v;
-            counts[i] = 0u;  // ready for the next call's histogram
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < int(blockDim.x >> 5); ++w) t += wsum[w];
-            carry += t;
-        }
-        __syncthreads();
-    }
-}
-
-// Placement: each CTA takes a chunk of kSortPer x 256 candidates, counts its bins in
-// shared memory, reserves one range per bin it holds (one global atomic each) and writes
-// (genome, index) pairs into the ranges, so the score kernel reads both coalesced.
-constexpr int kSortPer = 16;
-
-__global__ void __launch_bounds__(kSortT) key_place_kernel(const uint64_t* __restrict__ genome, int64_t n,
-                                                           uint32_t nt1, uint32_t nt2, uint32_t nbins,
-                                                           uint32_t* __restrict__ cursor,
-                                                           uint64_t* __restrict__ sgenome,
-                                                           uint32_t* __restrict__ order) {
-    extern __shared__ uint32_t sh[];
-    uint32_t* cnt = sh;           // per-bin count in this chunk, then running slot
-    uint32_t* base = sh + nbins;  // reserved global start per bin
-    pdl_wait();
-    const int64_t chunk = int64_t(kSortT) * kSortPer;
-    for (int64_t c0 = int64_t(blockIdx.x) * chunk; c0 < n; c0 += int64_t(gridDim.x) * chunk) {
-        for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) cnt[i] = 0u;
-        __syncthreads();
-        uint64_t g[kSortPer];
-        uint32_t bin[kSortPer];
-#pragma unroll
-        for (int r = 0; r < kSortPer; ++r) {
-            const int64_t i = c0 + r * kSortT + threadIdx.x;
-            g[r] = i < n ? __ldg(genome + i) : 0ull;
-            bin[r] = genome_bin(g[r], nt1, nt2, nbins);
-            if (i < n) atomicAdd(&cnt[bin[r]], 1u);
-        }
-        __syncthreads();
-        for (uint32_t i = threadIdx.x; i < nbins; i += blockDim.x) {
-            const uint32_t k = cnt[i];
-            base[i] = k ? atomicAdd(cursor + i, k) : 0u;
-            cnt[i] = 0u;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < kSortPer; ++r) {
-            const int64_t i = c0 + r * kSortT + threadIdx.x;
-            if (i < n) {
-                const uint32_t pos = base[bin[r]] + atomicAdd(&cnt[bin[r]], 1u);
-                sgenome[pos] = g[r];
-                order[pos] = uint32_t(i);
-            }
-        }
-        __syncthreads();
-    }
-}
-
-// One cooperative launch that groups the population by exact key (one CTA per SM, a
-// contiguous chunk each): count keys in shared memory and reserve each key's per-CTA
-// range with one global atomic on the key's cursor (the returned value is the CTA's
-// offset inside the key group), grid barrier, every CTA scans the key totals itself
-// (exclusive prefix = the group start), place (genome, index) pairs, grid barrier,
-// re-zero the cursors.  The order inside a key group is unspecified: the score kernel's
-// results do not depend on it.
-constexpr int kGroupT = 1024;
-
-__global__ void __launch_bounds__(kGroupT, 1) key_group_kernel(const uint64_t* __restrict__ genome, int64_t n,
-                                                               uint32_t nt1, uint32_t nt2, uint32_t nkeys,
-                                                               uint32_t* __restrict__ cursor,
-                                                               uint64_t* __restrict__ sgenome,
-                                                               uint32_t* __restrict__ order) {
-    namespace cg = cooperative_groups;
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ uint32_t sh[];
-    uint32_t* cnt = sh;           // per-key count in this chunk, then running slot
-    uint32_t* base = sh + nkeys;  // this CTA's start per key (absent keys: unused)
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t carry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (uint32_t i = tid; i < nkeys; i += blockDim.x) cnt[i] = 0u;
-    __syncthreads();
-    pdl_wait();
-    const int64_t per = (n + gridDim.x - 1) / gridDim.x;
-    const int64_t lo = int64_t(blockIdx.x) * per;
-    const int64_t hi = lo + per < n ? lo + per : n;
-    for (int64_t i = lo + tid; i < hi; i += blockDim.x) atomicAdd(&cnt[genome_bin(__ldg(genome + i), nt1, nt2, nkeys)], 1u);
-    __syncthreads();
-    for (uint32_t k = tid; k < nkeys; k += blockDim.x) {
-        const uint32_t c = cnt[k];
-        base[k] = c ? atomicAdd(cursor + k, c) : 0u;  // offset of this CTA inside key k's group
-        cnt[k] = 0u;
-    }
-    grid.sync();
-    // group start of every key = exclusive prefix of the totals (each CTA scans them)
-    if (tid == 0) carry = 0u;
-    __syncthreads();
-    for (uint32_t b = 0; b < nkeys; b += blockDim.x) {
-        const uint32_t k = b + tid;
-        const uint32_t v = k < nkeys ? __ldcg(cursor + k) : 0u;
-        uint32_t x = v;
-        for (int s2 = 1; s2 < 32; s2 <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, s2);
-            if (lane >= s2) x += y;
-        }
-        if (lane == 31) wsum[warp] = x;
-        __syncthreads();
-        uint32_t before = carry;
-        for (int w = 0; w < warp; ++w) before += wsum[w];
-        if (k < nkeys) base[k] += before + x - v;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < int(blockDim.x >> 5); ++w) t += wsum[w];
-            carry += t;
-        }
-        __syncthreads();
-    }
-    for (int64_t i = lo + tid; i < hi; i += blockDim.x) {
-        const uint64_t g = __ldg(genome + i);
-        const uint32_t k = genome_bin(g, nt1, nt2, nkeys);
-        const uint32_t pos = base[k] + atomicAdd(&cnt[k], 1u);
-        sgenome[pos] = g;
-        order[pos] = uint32_t(i);
-    }
-    grid.sync();  // every CTA has read the totals: re-zero the cursors for the next call
-    for (uint32_t k = blockIdx.x * blockDim.x + tid; k < nkeys; k += gridDim.x * blockDim.x) cursor[k] = 0u;
-}
-
 __global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
-                                                                    const uint32_t* __restrict__ table,
+                                                                    const uint8_t* __restrict__ table,
                                                                     const uint64_t* __restrict__ genome,
                                                                     const uint32_t* __restrict__ order, int64_t n,
                                                                     double* __restrict__ pred,
-                                                                    uint64_t* __restrict__ ids, const SelHist sel) {
+                                                                    uint64_t* __restrict__ ids, const SelHist sel,
+                                                                    const __grid_constant__ KeyedParams kp) {
     extern __shared__ int4 smem[];
     __shared__ uint32_t shist[kSelBins];
     if (sel.hist)
@@ -761,14 +572,14 @@ __global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_
     const TilingRec* til1 = at<TilingRec>(S, K.off_til[1]);
     const TilingRec* til2 = at<TilingRec>(S, K.off_til[2]);
     const int64_t* divk = at<int64_t>(S, K.off_divk);
-    const uint32_t tpad = uint32_t(K.tpad);
+    const uint32_t row_bytes = uint32_t(K.row_bytes);
     for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < n; s += int64_t(gridDim.x) * blockDim.x) {
         // with an order, genome[] is the population in that order (key_place_kernel)
         const uint32_t idx = order ? __ldg(order + s) : uint32_t(s);
         const Genome x = genome_unpack(__ldg(genome + s));
         const uint32_t kc = clskuv[(x.k * 16u + x.u) * 4u + x.v];
-        const uint32_t* row = table + size_t(keyed_key(K, x)) * tpad;
-        const double p = keyed_finish(K, keyed_sum(S, K, row, kc));
+        const uint8_t* row = table + size_t(keyed_key(K, x)) * row_bytes;
+        const double p = keyed_finish(K, keyed_sum(S, kp, row, kc));
         pred[idx] = p;
         if (sel.hist) atomicAdd(&shist[sel_bin(p, sel)], 1u);
         if (ids) {
@@ -946,74 +757,16 @@ cudaError_t score_keyed_occupancy(uint32_t bytes, int* per_sm) {
     return *per_sm < 1 ? cudaErrorInvalidConfiguration : cudaSuccess;
 }
 
-cudaError_t launch_key_sort(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, int nbins,
-                            uint32_t* d_counts, uint32_t* d_cursor, uint64_t* d_sgenome, uint32_t* d_order) {
-    if (n <= 0) return cudaSuccess;
-    if (nbins > kMaxSortKeys) return cudaErrorInvalidValue;
-    int64_t g1 = (n + kSortT - 1) / kSortT;
-    if (g1 > int64_t(c.sm_count) * 2) g1 = int64_t(c.sm_count) * 2;  // few CTAs: few count flushes
-    const int64_t chunk = int64_t(kSortT) * kSortPer;
-    int64_t g3 = (n + chunk - 1) / chunk;
-    if (g3 > int64_t(c.sm_count) * 8) g3 = int64_t(c.sm_count) * 8;
-    cudaError_t e = launch_pdl(key_hist_kernel, dim3(unsigned(g1)), dim3(kSortT), size_t(nbins) * 4, c.stream, d_genome,
-                               n, uint32_t(nt1), uint32_t(nt2), uint32_t(nbins), d_counts);
-    if (e == cudaSuccess)
-        e = launch_pdl(key_scan_kernel, dim3(1), dim3(1024), 0, c.stream, d_counts, uint32_t(nbins), d_cursor);
-    if (e == cudaSuccess)
-        e = launch_pdl(key_place_kernel, dim3(unsigned(g3)), dim3(kSortT), size_t(nbins) * 8, c.stream, d_genome, n,
-                       uint32_t(nt1), uint32_t(nt2), uint32_t(nbins), d_cursor, d_sgenome, d_order);
-    note_launches(3);
-    return e;
-}
-
-cudaError_t launch_key_group(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, int nkeys,
-                             uint32_t* d_cursor, uint64_t* d_sgenome, uint32_t* d_order) {
-    if (n <= 0) return cudaSuccess;
-    if (nkeys > kMaxSortKeys) return cudaErrorInvalidValue;
-    static std::once_flag once;
-    static cudaError_t attr = cudaSuccess;
-    std::call_once(once, [] {
-        attr = cudaFuncSetAttribute(key_group_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortKeys * 8);
-    });
-    if (attr != cudaSuccess) return attr;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(unsigned(c.sm_count));
-    cfg.blockDim = dim3(kGroupT);
-    cfg.dynamicSmemBytes = size_t(nkeys) * 8;
-    cfg.stream = c.stream;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[1].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 2;
-    note_launches(1);
-    return cudaLaunchKernelEx(&cfg, key_group_kernel, d_genome, n, uint32_t(nt1), uint32_t(nt2), uint32_t(nkeys),
-                              d_cursor, d_sgenome, d_order);
-}
-
-cudaError_t launch_keygen(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, uint64_t* keys,
-                          uint32_t* vals) {
-    if (n <= 0) return cudaSuccess;
-    const int64_t want = (n + kKeyedThreads - 1) / kKeyedThreads;
-    const int64_t cap = int64_t(c.sm_count) * 8;
-    const int grid = int(want < cap ? want : cap);
-    note_launches(1);
-    return launch_pdl(keygen_kernel, dim3(grid), dim3(kKeyedThreads), 0, c.stream, d_genome, n, uint32_t(nt1),
-                      uint32_t(nt2), keys, vals);
-}
-
-cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint32_t* d_table,
+cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint8_t* d_table,
                                const uint64_t* d_genome, const uint32_t* d_order, int64_t n, double* d_pred,
-                               uint64_t* d_ids, int per_sm, const SelHist& sel) {
+                               uint64_t* d_ids, int per_sm, const KeyedParams& kp, const SelHist& sel) {
     if (n <= 0) return cudaSuccess;
     const int64_t want = (n + kKeyedThreads - 1) / kKeyedThreads;
     const int64_t cap = int64_t(c.sm_count) * per_sm;
     const int grid = int(want < cap ? want : cap);
     note_launches(1);
     return launch_pdl(score_keyed_kernel, dim3(grid), dim3(kKeyedThreads), bytes, c.stream, d_kblob, bytes, d_table,
-                      d_genome, d_order, n, d_pred, d_ids, sel);
+                      d_genome, d_order, n, d_pred, d_ids, sel, kp);
 }
 
 int score_static_smem() {

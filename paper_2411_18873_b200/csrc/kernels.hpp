@@ -59,25 +59,12 @@ int score_static_smem();
 cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t score_bytes,
                          const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
                          int mask_bits, const ForestParams& fp, int per_sm, const SelHist& sel = SelHist{});
-// Keyed score path (KeyedHdr): key = tiling triple of each genome; the population is
-// grouped by key (launch_key_sort), then score_keyed reads d_genome in that order and
-// writes results at the original indices d_order[s] (d_order null: index order).
-cudaError_t launch_keygen(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, uint64_t* keys,
-                          uint32_t* vals);
-// Counting sort of the population by key folded into nbins <= kMaxSortKeys bins:
-// d_counts (nbins, zero before the first call; left zeroed), d_cursor (nbins),
-// d_sgenome / d_order (n): the genomes in bin order and their original indices.
-constexpr int kMaxSortKeys = 16384;
-cudaError_t launch_key_sort(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, int nbins,
-                            uint32_t* d_counts, uint32_t* d_cursor, uint64_t* d_sgenome, uint32_t* d_order);
-// The same grouping by exact key in one cooperative launch (one CTA per SM, grid
-// barriers); d_cursor (nkeys) zero before the first call, left zeroed.
-cudaError_t launch_key_group(const LaunchCtx& c, const uint64_t* d_genome, int64_t n, int nt1, int nt2, int nkeys,
-                             uint32_t* d_cursor, uint64_t* d_sgenome, uint32_t* d_order);
+// Keyed score path (KeyedHdr / KeyedParams): one byte per (tiling-triple key, tree)
+// from the key table; results at the original index (d_order nullable).
 cudaError_t score_keyed_occupancy(uint32_t bytes, int* per_sm);
-cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint32_t* d_table,
+cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint8_t* d_table,
                                const uint64_t* d_genome, const uint32_t* d_order, int64_t n, double* d_pred,
-                               uint64_t* d_ids, int per_sm, const SelHist& sel = SelHist{});
+                               uint64_t* d_ids, int per_sm, const KeyedParams& kp, const SelHist& sel = SelHist{});
 // Selection from the histogram the score kernel filled: filter (keys below the k-th
 // key's bucket + the bucket itself) -> one-CTA radix select inside the bucket and
 // (key, index) sort of the k.  Leaves the histogram zeroed for the next call.

@@ -12,6 +12,11 @@
 #if !defined(__CUDACC__) && !defined(__forceinline__)
 #define __forceinline__ inline
 #endif
+#if defined(__CUDACC__)
+#define ETUNE_UNROLL _Pragma("unroll")
+#else
+#define ETUNE_UNROLL  // host builds (forest compiler, tests): plain loops
+#endif
 
 #if defined(__CUDA_ARCH__)
 #define ETUNE_DMUL(a, b) __dmul_rn(a, b)
@@ -127,7 +132,7 @@ __host__ __device__ __forceinline__ M lds_mask(SAddr a) {
 template <typename M>
 __host__ __device__ __forceinline__ M tree_mask(const TreeRec& r, const SAddr* cb) {
     M m = ~M(0);
-#pragma unroll
+ETUNE_UNROLL
     for (int ch = 0; ch < kNumChannels; ++ch)
         if ((r.meta >> (24 + ch)) & 1u) m &= lds_mask<M>(cb[ch] + r.lut[ch]);
     return m;
@@ -155,7 +160,7 @@ __host__ __device__ __forceinline__ double forest_sum(const uint8_t* S, const Sc
                                                       const uint32_t* c) {
     const SAddr base = blob_saddr(S);
     SAddr cb[kNumChannels];
-#pragma unroll
+ETUNE_UNROLL
     for (int ch = 0; ch < kNumChannels; ++ch) cb[ch] = base + c[ch] * uint32_t(sizeof(M));
     double sum = 0.0;
     int t = 0;
@@ -190,14 +195,14 @@ __host__ __device__ __forceinline__ double forest_sum_pairs(const uint8_t* S, co
                                                             const uint32_t* c) {
     const SAddr base = blob_saddr(S);
     SAddr cb[kNumChannels];
-#pragma unroll
+ETUNE_UNROLL
     for (int ch = 0; ch < kNumChannels; ++ch) cb[ch] = base + c[ch] * 8u;
     double sum = 0.0;
     const int np = H.npairs;
     for (int p = 0; p < np; ++p) {
         const PairRec r = pairs[p];
         uint64_t m = ~0ull;
-#pragma unroll
+ETUNE_UNROLL
         for (int ch = 0; ch < kNumChannels; ++ch)
             if ((r.meta_a >> (24 + ch)) & 1u) m &= lds64(cb[ch] + r.lut[ch]);
         const double va = leaf_value32(base, r.meta_a & 0xffffffu, uint32_t(m));
@@ -211,50 +216,54 @@ __host__ __device__ __forceinline__ double forest_sum_pairs(const uint8_t* S, co
 }
 
 // Keyed form (KeyedHdr, etune_internal.hpp): sum of leaf values in tree order from the
-// candidate's key-table row (non-Kuv channels, 4 trees per 16-byte load) and its Kuv
+// candidate's key-table row (one byte per tree, 16 trees per 16-byte load) and its Kuv
 // class.  `row` is global memory on the device (read-only path), host memory in tests.
 #if defined(__CUDA_ARCH__)
-__device__ __forceinline__ uint4 ld_row4(const uint32_t* row, int q) {
+__device__ __forceinline__ uint4 ld_row16(const uint8_t* row, int q) {
     return __ldg(reinterpret_cast<const uint4*>(row) + q);
 }
 #else
 struct RowQuad {
     uint32_t x, y, z, w;
 };
-inline RowQuad ld_row4(const uint32_t* row, int q) { return RowQuad{row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]}; }
+inline RowQuad ld_row16(const uint8_t* row, int q) {
+    RowQuad r;
+    std::memcpy(&r, row + 16 * q, 16);
+    return r;
+}
 #endif
 
-__host__ __device__ __forceinline__ double keyed_leaf(SAddr leaf_base, SAddr kuv_base, uint32_t stride, int t,
-                                                      uint32_t mrow) {
-    const uint32_t m = mrow & lds32(kuv_base + uint32_t(t) * stride);
-    const uint32_t slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
-    const SAddr blk = leaf_base + uint32_t(t) * 256u + slot * 4u;
+// tree t's leaf value from its row byte: Kuv trees AND their listed mask with the
+// Kuv-class mask (both conflict-free rows), the others hold the slot itself.  All tree
+// constants come from KeyedParams (the kernel-parameter bank on the device).
+__host__ __device__ __forceinline__ double keyed_leaf(const KeyedParams& P, SAddr base, uint32_t kc, uint32_t t,
+                                                      uint32_t code) {
+    uint32_t slot = code;
+    if ((P.kuv_flags[t >> 5] >> (t & 31)) & 1u) {
+        const uint32_t m = lds32(base + P.moff[t] + code * 4u) & lds32(base + P.off_kuvtab + (t * P.nkc + kc) * 4u);
+        slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
+    }
+    const SAddr blk = base + P.off_leaves + t * 256u + slot * 4u;
     return join_f64(lds32(blk), lds32(blk + 128u));
 }
 
-__host__ __device__ __forceinline__ double keyed_sum(const uint8_t* KB, const KeyedHdr& K, const uint32_t* row,
+__host__ __device__ __forceinline__ double keyed_sum(const uint8_t* KB, const KeyedParams& P, const uint8_t* row,
                                                      uint32_t kc) {
     const SAddr base = blob_saddr(KB);
-    const SAddr leaf = base + K.off_leaves;
-    const SAddr kuv = base + K.off_kuvtab + kc * 4u;
-    const uint32_t stride = uint32_t(K.nkc) * 4u;
-    const int T = K.ntrees;
     double sum = 0.0;
-    int t = 0;
-    // the row is read one quad ahead (its loads come from L1/L2)
-    auto m4 = ld_row4(row, 0);
-    for (; t + 4 <= T; t += 4) {
-        const auto nx = ld_row4(row, t + 4 < K.tpad ? (t >> 2) + 1 : (t >> 2));
-        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t, m4.x));
-        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 1, m4.y));
-        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 2, m4.z));
-        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 3, m4.w));
-        m4 = nx;
-    }
-    if (t < T) {  // 1-3 trees left (no runtime-indexed array: keeps the row in registers)
-        sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t, m4.x));
-        if (t + 1 < T) sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 1, m4.y));
-        if (t + 2 < T) sum = ETUNE_DADD(sum, keyed_leaf(leaf, kuv, stride, t + 2, m4.z));
+    const uint32_t T = P.ntrees;
+    // fully unrolled over the kKeyedMaxTrees bound: every tree constant is an immediate
+    // constant-bank operand (no per-tree index arithmetic)
+ETUNE_UNROLL
+    for (uint32_t t0 = 0; t0 < uint32_t(kKeyedMaxTrees); t0 += 16) {
+        if (t0 >= T) break;
+        const auto r = ld_row16(row, int(t0 >> 4));
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+ETUNE_UNROLL
+        for (uint32_t j = 0; j < 16; ++j) {
+            const uint32_t t = t0 + j;
+            if (t < T) sum = ETUNE_DADD(sum, keyed_leaf(P, base, kc, t, (w[j >> 2] >> (8 * (j & 3))) & 0xffu));
+        }
     }
     return sum;
 }

@@ -6,5 +6,5 @@ timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu_$TAG.log 2
 timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 timeout 600 python bench.py --steps 200 --warmup 5 --cpu-seconds 8 > gpurun_out/bench_$TAG.log 2>&1
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"score|sel_" -s 8 -c 20 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-search --bufs 2 > gpurun_out/ncu_bench_$TAG.log 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:score_kernel -s 2 -c 1 -o gpurun_out/prof_score_$TAG python bench.py --steps 2 --warmup 2 --no-cpu-baseline --no-e2e --no-search --bufs 2 > gpurun_out/ncu_full_$TAG.log 2>&1
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:score_keyed -s 2 -c 1 -o gpurun_out/prof_score_$TAG python bench.py --steps 2 --warmup 2 --no-cpu-baseline --no-e2e --no-search --bufs 2 > gpurun_out/ncu_full_$TAG.log 2>&1
 ls gpurun_out

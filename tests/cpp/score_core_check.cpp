@@ -80,8 +80,8 @@ static int score_impl(const int64_t* op_words, int num_sms, const int32_t* featu
             const KeyedHdr& KH = *reinterpret_cast<const KeyedHdr*>(KB);
             const Genome x = genome_unpack(gnm);
             const uint32_t kc = KB[KH.off_clskuv + (x.k * 16u + x.u) * 4u + x.v];
-            const uint32_t* row = KBd.table.data() + size_t(keyed_key(KH, x)) * size_t(KH.tpad);
-            out[i] = keyed_finish(KH, keyed_sum(KB, KH, row, kc));
+            const uint8_t* row = KBd.table.data() + size_t(keyed_key(KH, x)) * size_t(KH.row_bytes);
+            out[i] = keyed_finish(KH, keyed_sum(KB, KBd.params, row, kc));
             continue;
         }
         const CandClasses cc = candidate_classes(B, H, gnm);
