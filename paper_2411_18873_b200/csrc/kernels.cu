@@ -549,7 +549,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
 // L2/L1), its Kuv class; per tree one or three shared loads and one FP64 add in tree
 // order (score_core.hpp keyed_sum).  `order` (nullable) visits candidates in another
 // order with genome[] already in that order; results land at the original index.
-constexpr int kKeyedThreads = 256;
+constexpr int kKeyedThreads = 512;
 
 __global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
                                                                     const uint8_t* __restrict__ table,
