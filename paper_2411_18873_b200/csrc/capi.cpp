@@ -210,8 +210,7 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     std::vector<uint8_t> blob;
     std::string err;
     CompiledScore cs;
-    KeyedBuild kb;
-    const etune_status bst = build_score_blob(f->host, p->build, &blob, &cs.stats, &err, &kb);
+    const etune_status bst = build_score_blob(f->host, p->build, &blob, &cs.stats, &err);
     if (bst != ETUNE_OK && bst != ETUNE_ERR_UNSUPPORTED) return fail(bst, err);
     const int cap = max_dynamic_smem(f->ctx->device) - score_static_smem();
     if (bst == ETUNE_ERR_UNSUPPORTED || blob.size() > size_t(cap)) {
@@ -236,28 +235,46 @@ etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     else
         std::memcpy(cs.params->rec, blob.data() + hdr->off_trees, sizeof(TreeRec) * size_t(hdr->ntrees));
     selection_buckets(f->host, &cs.sel_kmin, &cs.sel_shift);
-    if (kb.ok && kb.blob.size() <= size_t(cap)) {
-        CU(cudaMalloc(&cs.d_kblob, kb.blob.size()));
-        CU(cudaMalloc(&cs.d_ktable, kb.table.size()));
-        CU(cudaMemcpyAsync(cs.d_kblob, kb.blob.data(), kb.blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
-        CU(cudaMemcpyAsync(cs.d_ktable, kb.table.data(), kb.table.size(), cudaMemcpyHostToDevice, f->ctx->stream));
-        CU(cudaStreamSynchronize(f->ctx->stream));
-        cs.kbytes = uint32_t(kb.blob.size());
-        cs.kparams = std::make_shared<KeyedParams>(kb.params);
-        cs.key_bits = kb.key_bits;
-        cs.nkeys = int(kb.nkeys);
-        cs.nt1 = p->build.hdr.nt[1];
-        cs.nt2 = p->build.hdr.nt[2];
-        CU(score_keyed_occupancy(cs.kbytes, &cs.keyed_per_sm));
-        cs.keyed = true;
-    }
     auto res = f->compiled.emplace(p->serial, cs);
     *out = &res.first->second;
     return ETUNE_OK;
 }
 
+// The keyed form is compiled on first use by a population of at least kKeyedMinN
+// (its table build is a few ms of host work per (forest, plan): small populations,
+// e.g. the search loop's per-round scoring, keep the class-table kernel).
+constexpr int64_t kKeyedMinN = int64_t(1) << 16;
+
+etune_status ensure_keyed(etune_cu_forest* f, const etune_cu_plan* p, CompiledScore* cs, int64_t n) {
+    if (cs->walk || f->keyed_mode == 0 || n < kKeyedMinN) return ETUNE_OK;
+    std::lock_guard<std::mutex> lock(f->mu);
+    if (cs->keyed_tried) return ETUNE_OK;
+    cs->keyed_tried = true;
+    std::vector<uint8_t> blob;
+    std::string err;
+    ScoreStats st;
+    KeyedBuild kb;
+    if (build_score_blob(f->host, p->build, &blob, &st, &err, &kb) != ETUNE_OK || !kb.ok) return ETUNE_OK;
+    const int cap = max_dynamic_smem(f->ctx->device) - score_static_smem();
+    if (kb.blob.size() > size_t(cap)) return ETUNE_OK;
+    CU(cudaMalloc(&cs->d_kblob, kb.blob.size()));
+    CU(cudaMalloc(&cs->d_ktable, kb.table.size()));
+    CU(cudaMemcpyAsync(cs->d_kblob, kb.blob.data(), kb.blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
+    CU(cudaMemcpyAsync(cs->d_ktable, kb.table.data(), kb.table.size(), cudaMemcpyHostToDevice, f->ctx->stream));
+    CU(cudaStreamSynchronize(f->ctx->stream));
+    cs->kbytes = uint32_t(kb.blob.size());
+    cs->kparams = std::make_shared<KeyedParams>(kb.params);
+    cs->key_bits = kb.key_bits;
+    cs->nkeys = int(kb.nkeys);
+    cs->nt1 = p->build.hdr.nt[1];
+    cs->nt2 = p->build.hdr.nt[2];
+    CU(score_keyed_occupancy(cs->kbytes, &cs->keyed_per_sm));
+    cs->keyed = true;
+    return ETUNE_OK;
+}
+
 bool use_keyed(const etune_cu_forest* f, const CompiledScore* cs, int64_t n) {
-    return cs->keyed && f->keyed_mode != 0 && n < (int64_t(1) << 32);
+    return cs->keyed && f->keyed_mode != 0 && n >= kKeyedMinN && n < (int64_t(1) << 32);
 }
 
 // Scoring pass of any compiled form; `ev` (nullable) = {start, before the score kernel,
@@ -964,6 +981,7 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
     return score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, SelHist{}, nullptr);
 }
 
@@ -977,6 +995,7 @@ etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etun
     if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
     return score_select_local(c, p, f, cs, d_genome, n, k, d_pred, d_ids, d_idx);
 }
 
@@ -991,6 +1010,7 @@ etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan*
     if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "shard >= 2^31");
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
     ShardBufs sb;
     if (etune_status st = shard_buffers(c, k, &sb)) return st;
     const int64_t kl = std::min(k, n);
@@ -1038,6 +1058,7 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
     if (n == 0) return ETUNE_OK;
     CompiledScore* cs = nullptr;
     if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = ensure_keyed(f, p, cs, std::min<int64_t>(n, int64_t(1) << 17))) return st;
     // Chunked pipeline over two staging buffers.  The host pool narrows chunk i's rows
     // into pinned staging (24 B/row when every field fits 16 bits) while the GPU works
     // on chunk i-1; then H2D of chunk i (copy-in stream) overlaps encode+score of chunk

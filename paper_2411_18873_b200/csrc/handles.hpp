@@ -76,7 +76,7 @@ struct CompiledScore {
     uint64_t sel_kmin = 0;    // fused selection buckets: order key of the lowest possible
     uint32_t sel_shift = 0;   // prediction, and the key bits one bucket spans
     // keyed form (forest.hpp KeyedBuild): blob, key table, sort key width, occupancy
-    bool keyed = false;
+    bool keyed = false, keyed_tried = false;
     uint8_t* d_kblob = nullptr;
     uint32_t kbytes = 0;
     uint8_t* d_ktable = nullptr;
