@@ -263,6 +263,7 @@ etune_status ensure_keyed(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     CU(cudaMemcpyAsync(cs->d_ktable, kb.table.data(), kb.table.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaStreamSynchronize(f->ctx->stream));
     cs->kbytes = uint32_t(kb.blob.size());
+    cs->ktable_bytes = kb.table.size();
     cs->kparams = std::make_shared<KeyedParams>(kb.params);
     cs->key_bits = kb.key_bits;
     cs->nkeys = int(kb.nkeys);
@@ -292,8 +293,8 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
         // candidates in population order: each reads its own 112-byte key-table row (L2);
         // grouping the population by key first was measured slower (the sort costs more
         // than the broadcast rows save)
-        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, d_genome, nullptr, n, d_pred, d_ids,
-                              cs->keyed_per_sm, *cs->kparams, sel));
+        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, cs->ktable_bytes, d_genome, nullptr, n,
+                              d_pred, d_ids, cs->keyed_per_sm, *cs->kparams, sel));
     } else {
         if (ev) CU(cudaEventRecord(ev[1], c->stream));
         CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,

@@ -63,8 +63,9 @@ cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t sc
 // from the key table; results at the original index (d_order nullable).
 cudaError_t score_keyed_occupancy(uint32_t bytes, int* per_sm);
 cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint8_t* d_table,
-                               const uint64_t* d_genome, const uint32_t* d_order, int64_t n, double* d_pred,
-                               uint64_t* d_ids, int per_sm, const KeyedParams& kp, const SelHist& sel = SelHist{});
+                               size_t table_bytes, const uint64_t* d_genome, const uint32_t* d_order, int64_t n,
+                               double* d_pred, uint64_t* d_ids, int per_sm, const KeyedParams& kp,
+                               const SelHist& sel = SelHist{});
 // Selection from the histogram the score kernel filled: filter (keys below the k-th
 // key's bucket + the bucket itself) -> one-CTA radix select inside the bucket and
 // (key, index) sort of the k.  Leaves the histogram zeroed for the next call.
