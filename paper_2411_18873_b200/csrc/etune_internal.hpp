@@ -203,6 +203,7 @@ struct KeyedHdr {
 constexpr int kKeyedMaxTrees = 128;
 struct KeyedParams {       // kernel parameter (constant bank: warp-uniform reads cost no shared-memory issue)
     uint32_t moff[kKeyedMaxTrees];  // byte offset of tree t's mask list from the blob start
+    uint32_t koff[kKeyedMaxTrees];  // byte offset of tree t's Kuv-mask row ([tree][nkc]) from the blob start
     uint32_t kuv_flags[4];          // copy of KeyedHdr::kuv_flags
     uint32_t off_kuvtab, off_leaves, nkc, ntrees;
 };

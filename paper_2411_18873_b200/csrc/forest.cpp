@@ -581,6 +581,7 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                 std::memcpy(kbl.data(), &K, sizeof(K));
                 for (int w = 0; w < 4; ++w) keyed->params.kuv_flags[w] = K.kuv_flags[w];
                 keyed->params.off_kuvtab = K.off_kuvtab;
+                for (int64_t t = 0; t < T; ++t) keyed->params.koff[t] = K.off_kuvtab + uint32_t(t) * uint32_t(nkc) * 4u;
                 keyed->params.off_leaves = K.off_leaves;
                 keyed->params.nkc = uint32_t(nkc);
                 keyed->params.ntrees = uint32_t(T);

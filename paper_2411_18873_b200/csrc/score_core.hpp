@@ -236,34 +236,54 @@ inline RowQuad ld_row16(const uint8_t* row, int q) {
 // tree t's leaf value from its row byte: Kuv trees AND their listed mask with the
 // Kuv-class mask (both conflict-free rows), the others hold the slot itself.  All tree
 // constants come from KeyedParams (the kernel-parameter bank on the device).
-__host__ __device__ __forceinline__ double keyed_leaf(const KeyedParams& P, SAddr base, uint32_t kc, uint32_t t,
+// `kc4` = Kuv class * 4; tree constants are immediates of the parameter bank
+__host__ __device__ __forceinline__ double keyed_leaf(const KeyedParams& P, SAddr base, uint32_t kc4, uint32_t t,
                                                       uint32_t code) {
     uint32_t slot = code;
     if ((P.kuv_flags[t >> 5] >> (t & 31)) & 1u) {
-        const uint32_t m = lds32(base + P.moff[t] + code * 4u) & lds32(base + P.off_kuvtab + (t * P.nkc + kc) * 4u);
+        const uint32_t m = lds32(base + P.moff[t] + code * 4u) & lds32(base + P.koff[t] + kc4);
         slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
     }
     const SAddr blk = base + P.off_leaves + t * 256u + slot * 4u;
     return join_f64(lds32(blk), lds32(blk + 128u));
 }
 
+// byte j of w (one PRMT on the device)
+__host__ __device__ __forceinline__ uint32_t byte_of(uint32_t w, uint32_t j) {
+#if defined(__CUDA_ARCH__)
+    return __byte_perm(w, 0u, 0x4440u + j);
+#else
+    return (w >> (8 * j)) & 0xffu;
+#endif
+}
+
+// 16 trees from one 16-byte row quad; FULL: no per-tree bound checks
+template <bool FULL>
+__host__ __device__ __forceinline__ double keyed_group(const KeyedParams& P, SAddr base, uint32_t kc4, uint32_t t0,
+                                                       const uint32_t* w, double sum) {
+ETUNE_UNROLL
+    for (uint32_t j = 0; j < 16; ++j) {
+        const uint32_t t = t0 + j;
+        if (FULL || t < P.ntrees) sum = ETUNE_DADD(sum, keyed_leaf(P, base, kc4, t, byte_of(w[j >> 2], j & 3)));
+    }
+    return sum;
+}
+
 __host__ __device__ __forceinline__ double keyed_sum(const uint8_t* KB, const KeyedParams& P, const uint8_t* row,
                                                      uint32_t kc) {
     const SAddr base = blob_saddr(KB);
+    const uint32_t kc4 = kc * 4u;
     double sum = 0.0;
     const uint32_t T = P.ntrees;
     // fully unrolled over the kKeyedMaxTrees bound: every tree constant is an immediate
-    // constant-bank operand (no per-tree index arithmetic)
+    // constant-bank operand; whole groups of 16 trees carry no per-tree bound check
 ETUNE_UNROLL
     for (uint32_t t0 = 0; t0 < uint32_t(kKeyedMaxTrees); t0 += 16) {
         if (t0 >= T) break;
         const auto r = ld_row16(row, int(t0 >> 4));
         const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-ETUNE_UNROLL
-        for (uint32_t j = 0; j < 16; ++j) {
-            const uint32_t t = t0 + j;
-            if (t < T) sum = ETUNE_DADD(sum, keyed_leaf(P, base, kc, t, (w[j >> 2] >> (8 * (j & 3))) & 0xffu));
-        }
+        if (t0 + 16 <= T) sum = keyed_group<true>(P, base, kc4, t0, w, sum);
+        else sum = keyed_group<false>(P, base, kc4, t0, w, sum);
     }
     return sum;
 }
