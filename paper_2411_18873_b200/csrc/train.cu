@@ -267,7 +267,6 @@ __global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int 
 // loads its smem operands one batch of 8 ahead.
 //   lists 0..15: exclusive prefix at every position (the `run` of cpp 95-121)
 //   list 16:     the node's (grad, hess) totals in sample order (cpp 73-76, 150-155)
-constexpr int kChainWarps = 1;
 constexpr int kChunk = 1024;
 
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
@@ -278,59 +277,82 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_prev() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-__global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int lvl, int only_totals,
-                                                                 const double* __restrict__ gl,
-                                                                 const double* __restrict__ hl,
-                                                                 double* __restrict__ pg, double* __restrict__ ph,
-                                                                 TrainCtl* ctl) {
+__device__ __forceinline__ void bar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+__device__ __forceinline__ void bar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
+
+// Two warps per (list, segment): warp 1 streams chunks in (cp.async, two buffers) and
+// the prefixes out, warp 0 only chains (lanes 0/1), so the chain never waits on memory.
+// Named barriers 1+b ("buffer b full") and 3+b ("buffer b chained") hand the buffers over.
+__global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_totals,
+                                                   const double* __restrict__ gl, const double* __restrict__ hl,
+                                                   double* __restrict__ pg, double* __restrict__ ph, TrainCtl* ctl) {
     pdl_wait();
     // prefixes overwrite their operands in place (each operand is in registers by then)
-    __shared__ __align__(16) double ig[kChainWarps][2][kChunk + 8];
-    __shared__ __align__(16) double ih[kChainWarps][2][kChunk + 8];
+    __shared__ __align__(16) double ig[2][kChunk + 8];
+    __shared__ __align__(16) double ih[2][kChunk + 8];
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     if (nseg <= 0) return;
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = blockIdx.x * kChainWarps + w;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t = blockIdx.x;
     const int l = only_totals ? kSampleList : t / nseg;
     const int k = only_totals ? t : t % nseg;
     if (k >= nseg || l >= kLists) return;
     const int s = ctl->seg_start[b][k], e = ctl->seg_end[b][k];
-    const double* G = gl + int64_t(l) * n;
-    const double* Hh = hl + int64_t(l) * n;
-    double* PG = pg + int64_t(l) * n;
-    double* PH = ph + int64_t(l) * n;
+    const int nch = (e - s + kChunk - 1) / kChunk;
     const bool prefixes = l != kSampleList;
-    double racc = 0.0;  // lane 0: running gradient sum, lane 1: running hessian sum
-    if (s < e) {
-        const int cnt0 = min(kChunk, e - s);
-        for (int j = lane; j < cnt0; j += 32) {
-            cp_async8(&ig[w][0][j], G + s + j);
-            cp_async8(&ih[w][0][j], Hh + s + j);
-        }
-    }
-    cp_async_commit();
-    int buf = 0;
-    for (int base = s; base < e; base += kChunk, buf ^= 1) {
-        const int cnt = min(kChunk, e - base);
-        const int nb = base + kChunk;
-        if (nb < e) {  // prefetch the next chunk into the other buffer
-            const int cn = min(kChunk, e - nb);
-            for (int j = lane; j < cn; j += 32) {
-                cp_async8(&ig[w][buf ^ 1][j], G + nb + j);
-                cp_async8(&ih[w][buf ^ 1][j], Hh + nb + j);
+    if (warp == 1) {  // ---- io warp
+        const double* G = gl + int64_t(l) * n;
+        const double* Hh = hl + int64_t(l) * n;
+        double* PG = pg + int64_t(l) * n;
+        double* PH = ph + int64_t(l) * n;
+        auto load = [&](int c) {
+            const int base = s + c * kChunk, cnt = min(kChunk, e - base), bb = c & 1;
+            for (int j = lane; j < cnt; j += 32) {
+                cp_async8(&ig[bb][j], G + base + j);
+                cp_async8(&ih[bb][j], Hh + base + j);
             }
+            cp_async_commit();
+        };
+        if (nch == 0) return;
+        load(0);
+        if (nch > 1) {
+            load(1);
+            cp_async_wait_prev();
+        } else {
+            cp_async_wait_all();
         }
-        cp_async_commit();
-        cp_async_wait_prev();  // the current chunk has landed (for this lane's copies)
-        __syncwarp();
+        bar_arrive(1);  // chunk 0 in buffer 0
+        for (int c = 0; c < nch; ++c) {
+            const int bb = c & 1;
+            if (c + 1 < nch) {
+                cp_async_wait_all();  // chunk c+1 (the only group in flight)
+                bar_arrive(1 + (bb ^ 1));
+            }
+            bar_sync(3 + bb);  // chunk c chained in place
+            if (prefixes) {
+                const int base = s + c * kChunk, cnt = min(kChunk, e - base);
+                for (int j = lane; j < cnt; j += 32) {
+                    PG[base + j] = ig[bb][j];
+                    PH[base + j] = ih[bb][j];
+                }
+            }
+            __syncwarp();
+            if (c + 2 < nch) load(c + 2);
+        }
+        return;
+    }
+    // ---- chain warp: lane 0 chains the gradients, lane 1 the hessians (one instruction
+    // stream, two independent chains), batches of 8 through double2 shared loads/stores,
+    // two register sets alternating; the chain runs near the FP64 add latency (8 cycles,
+    // scripts/micro/dadd_latency.cu)
+    double racc = 0.0;
+    for (int c = 0; c < nch; ++c) {
+        const int bb = c & 1;
+        const int cnt = min(kChunk, e - (s + c * kChunk));
+        bar_sync(1 + bb);
         if (lane < 2) {
-            // lane 0 chains the gradients, lane 1 the hessians: one instruction stream,
-            // two independent chains (SIMT), ~2 instructions per element per lane —
-            // batches of 8 through double2 shared loads/stores, two register sets
-            // alternating so the next batch is loaded while this one chains; the chain
-            // runs near the FP64 add latency (8 cycles, scripts/micro/dadd_latency.cu)
-            double* cx = lane == 0 ? ig[w][buf] : ih[w][buf];
+            double* cx = lane == 0 ? ig[bb] : ih[bb];
             double2* c2 = reinterpret_cast<double2*>(cx);
             const int nb = cnt >> 3;
             const int full = nb << 3;
@@ -367,15 +389,8 @@ __global__ void __launch_bounds__(32 * kChainWarps) chain_kernel(int64_t n, int 
             }
         }
         __syncwarp();
-        if (prefixes) {
-            for (int j = lane; j < cnt; j += 32) {
-                PG[base + j] = ig[w][buf][j];
-                PH[base + j] = ih[w][buf][j];
-            }
-        }
-        __syncwarp();
+        bar_arrive(3 + bb);
     }
-    cp_async_wait_all();
     const double rg = __shfl_sync(0xffffffffu, racc, 0), rh = __shfl_sync(0xffffffffu, racc, 1);
     if (lane == 0) {
         if (!prefixes) {
@@ -734,8 +749,7 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
         PDL(segmap_kernel, grid(n), 256, 0, cap, n, lvl, ctl, segmap);
         PDL(gather_kernel, grid(int64_t(L)), 256, 0, cap, cur, n, kLists, grad, hess, d_feat, gl, hl, fv);
         const int warps = kLists * segs;
-        PDL(chain_kernel, (warps + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap, n, lvl, 0, gl, hl, pg, ph,
-            ctl);
+        PDL(chain_kernel, warps, 64, 0, cap, n, lvl, 0, gl, hl, pg, ph, ctl);
         PDL(gain_kernel, grid(int64_t(F)), 256, 0, cap, n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
         PDL(gainpos_kernel, grid(int64_t(F)), 256, 0, cap, n, segmap, gains, ctl);
         PDL(decide_kernel, 1, 1024, 0, cap, n, lvl, fv, ctl);
@@ -752,8 +766,7 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
     // totals of the last frontier (children created at the deepest level)
     PDL(gather_kernel, grid(n), 256, 0, cap, cur, n, 1, grad, hess, d_feat, gl, hl, fv);
     const int segs = 1 << max_depth;
-    PDL(chain_kernel, (segs + kChainWarps - 1) / kChainWarps, 32 * kChainWarps, 0, cap, n, lvl, 1, gl, hl, pg, ph,
-        ctl);
+    PDL(chain_kernel, segs, 64, 0, cap, n, lvl, 1, gl, hl, pg, ph, ctl);
     PDL(finalize_kernel, 1, 1024, 0, cap, lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
     PDL(update_kernel, grid(n), 256, 0, cap, d_feat, n, lr, ctl, pred);
     launches += 4;
