@@ -225,46 +225,41 @@ __global__ void grad_kernel(const double* __restrict__ pred, const double* __res
 }
 
 // segment (frontier index) of every position, -1 for dead ranges; identical for all lists
-__global__ void segmap_kernel(int64_t n, int lvl, const TrainCtl* __restrict__ ctl, int32_t* __restrict__ segmap) {
-    pdl_wait();
-    const int b = lvl & 1;
-    const int nseg = ctl->nseg[b];
-    const int32_t* ss = ctl->seg_start[b];
-    const int32_t* se = ctl->seg_end[b];
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
-        int lo = 0, hi = nseg;
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (ss[mid] <= p) lo = mid + 1;
-            else hi = mid;
-        }
-        const int k = lo - 1;
-        segmap[p] = (k >= 0 && p < se[k]) ? k : -1;
+__device__ __forceinline__ int32_t seg_of(int64_t p, int nseg, const int32_t* ss, const int32_t* se) {
+    int lo = 0, hi = nseg;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (ss[mid] <= p) lo = mid + 1;
+        else hi = mid;
     }
+    const int k = lo - 1;
+    return (k >= 0 && p < se[k]) ? k : -1;
 }
 
 // gl/hl[l][p] = grad/hess[list[l][p]], fv[l][p] = feature l of that sample: everything the
-// chains and gains read afterwards is contiguous in list order
+// chains and gains read afterwards is contiguous in list order.  With segmap non-null the
+// same launch also maps every list position to its frontier segment (-1: a leaf's range).
 __global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int nl, const double* __restrict__ grad,
                               const double* __restrict__ hess, const double* __restrict__ feats,
-                              double* __restrict__ gl, double* __restrict__ hl, double* __restrict__ fv) {
+                              double* __restrict__ gl, double* __restrict__ hl, double* __restrict__ fv, int lvl,
+                              const TrainCtl* __restrict__ ctl, int32_t* __restrict__ segmap) {
     pdl_wait();
     const int64_t tot = int64_t(nl) * n;
     const int64_t off = int64_t(kLists - nl) * n;  // nl == 1: sample list only
+    const int b = lvl & 1;
+    const int nseg = ctl->nseg[b];
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
         const int64_t g = off + q;
         const int32_t idx = lists[g];
         gl[g] = grad[idx];
         hl[g] = hess[idx];
         if (g < int64_t(kF) * n) fv[g] = feats[int64_t(idx) * kF + g / n];
+        if (segmap && q < n) segmap[q] = seg_of(q, nseg, ctl->seg_start[b], ctl->seg_end[b]);
     }
 }
 
-// One warp per (list, frontier segment): the sequential running sums, kChunk elements
-// at a time staged through shared memory.  The next chunk's (grad, hess) is copied
-// with cp.async by all lanes BEFORE lane 0 starts chaining the current one, so the
-// global-load latency hides under the FP64 add chain (double buffer); the chain itself
-// loads its smem operands one batch of 8 ahead.
+// Per (list, frontier segment): the sequential running sums, kChunk elements at a time
+// staged through shared memory (chain_kernel below).
 //   lists 0..15: exclusive prefix at every position (the `run` of cpp 95-121)
 //   list 16:     the node's (grad, hess) totals in sample order (cpp 73-76, 150-155)
 constexpr int kChunk = 1024;
@@ -746,8 +741,8 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
     int lvl = 0;
     for (int depth = 0; depth < max_depth; ++depth, ++lvl) {
         const int segs = 1 << depth;  // frontier bound at this depth
-        PDL(segmap_kernel, grid(n), 256, 0, cap, n, lvl, ctl, segmap);
-        PDL(gather_kernel, grid(int64_t(L)), 256, 0, cap, cur, n, kLists, grad, hess, d_feat, gl, hl, fv);
+        PDL(gather_kernel, grid(int64_t(L)), 256, 0, cap, cur, n, kLists, grad, hess, d_feat, gl, hl, fv, lvl, ctl,
+            segmap);
         const int warps = kLists * segs;
         PDL(chain_kernel, warps, 64, 0, cap, n, lvl, 0, gl, hl, pg, ph, ctl);
         PDL(gain_kernel, grid(int64_t(F)), 256, 0, cap, n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
@@ -761,10 +756,11 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
         PDL(scatter_kernel, grid(int64_t(L)), 256, 0, cap, cur, work[wb], pfx, segmap, n, lvl, ctl);
         cur = work[wb];
         wb ^= 1;
-        launches += 11;
+        launches += 10;
     }
     // totals of the last frontier (children created at the deepest level)
-    PDL(gather_kernel, grid(n), 256, 0, cap, cur, n, 1, grad, hess, d_feat, gl, hl, fv);
+    PDL(gather_kernel, grid(n), 256, 0, cap, cur, n, 1, grad, hess, d_feat, gl, hl, fv, lvl, ctl,
+        static_cast<int32_t*>(nullptr));
     const int segs = 1 << max_depth;
     PDL(chain_kernel, segs, 64, 0, cap, n, lvl, 1, gl, hl, pg, ph, ctl);
     PDL(finalize_kernel, 1, 1024, 0, cap, lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
