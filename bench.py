@@ -381,9 +381,13 @@ def run_ours(args):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = n * ALGO_BYTES / (kernel_ms / 1e3) / 1e9
     traffic = None
-    try:  # DRAM bytes per launch from the committed ncu --set full capture of this kernel
+    sm_bound = None
+    try:  # DRAM bytes per launch + the binding SM unit from the committed ncu --set full capture
         t = json.load(open(os.path.join(ROOT, "profiles", "score_kernel_traffic.json")))
         traffic = int(t["dram_bytes_read_per_launch"]) + int(t["dram_bytes_write_per_launch"])
+        if "binding_unit" in t:
+            sm_bound = {"unit": t["binding_unit"], "pct_of_peak": t["l1tex_pct_of_peak"],
+                        "issue_active_pct": t["issue_active_pct"], "source": t["source"]}
     except Exception:
         pass
     line = {
@@ -405,7 +409,7 @@ def run_ours(args):
                                     "fallback 6650 GB/s (B200_PROFILING.md)",
                      "note": "SM-bound (issue + shared-memory pipe); per-candidate key-table row reads are "
                              "L2-resident, not HBM; see profiles/",
-                     "select_ms": select_ms},
+                     "select_ms": select_ms, "sm_bound": sm_bound},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
