@@ -585,6 +585,30 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                 keyed->params.off_leaves = K.off_leaves;
                 keyed->params.nkc = uint32_t(nkc);
                 keyed->params.ntrees = uint32_t(T);
+                keyed->params.kfull = 0;
+                // full form: every (key, Kuv class) row holds exit slots only
+                const size_t full_bytes = size_t(nk) * size_t(nkc) * size_t(row_bytes);
+                if (nkc > 0 && full_bytes <= max_table_bytes) {
+                    std::vector<uint8_t> ft(full_bytes, 0);
+                    for (int64_t key = 0; key < nk; ++key) {
+                        const uint8_t* row = keyed->table.data() + size_t(key) * size_t(row_bytes);
+                        for (int x = 0; x < nkc; ++x) {
+                            uint8_t* fr = ft.data() + (size_t(key) * size_t(nkc) + size_t(x)) * size_t(row_bytes);
+                            for (int64_t t = 0; t < T; ++t) {
+                                if ((tree_used[size_t(t)] >> kChKuv) & 1u) {
+                                    const uint32_t m = mlists[size_t(t)][row[t]] &
+                                                       kuvtab[size_t(t) * size_t(nkc) + size_t(x)];
+                                    fr[t] = uint8_t(((m & (0u - m)) * 0x077CB531u) >> 27);
+                                } else {
+                                    fr[t] = row[t];
+                                }
+                            }
+                        }
+                    }
+                    keyed->table.swap(ft);
+                    keyed->params.kfull = 1;
+                    for (int w = 0; w < 4; ++w) keyed->params.kuv_flags[w] = 0u;
+                }
                 keyed->ok = true;
             }
         }

@@ -292,6 +292,13 @@ __host__ __device__ __forceinline__ uint32_t keyed_key(const KeyedHdr& K, const 
     return (x.t0 * uint32_t(K.nt[1]) + x.t1) * uint32_t(K.nt[2]) + x.t2;
 }
 
+// row of a candidate in the key table: per key, or per (key, Kuv class) in the full form
+__host__ __device__ __forceinline__ uint32_t keyed_row_index(const KeyedParams& P, const KeyedHdr& K, const Genome& x,
+                                                             uint32_t kc) {
+    const uint32_t key = keyed_key(K, x);
+    return P.kfull ? key * P.nkc + kc : key;
+}
+
 __host__ __device__ __forceinline__ double keyed_finish(const KeyedHdr& K, double sum) {
     const double p = ETUNE_DADD(K.base, ETUNE_DMUL(K.lr, sum));  // energy_model.cpp:248
     return (1e-6 < p) ? p : 1e-6;

@@ -80,7 +80,7 @@ static int score_impl(const int64_t* op_words, int num_sms, const int32_t* featu
             const KeyedHdr& KH = *reinterpret_cast<const KeyedHdr*>(KB);
             const Genome x = genome_unpack(gnm);
             const uint32_t kc = KB[KH.off_clskuv + (x.k * 16u + x.u) * 4u + x.v];
-            const uint8_t* row = KBd.table.data() + size_t(keyed_key(KH, x)) * size_t(KH.row_bytes);
+            const uint8_t* row = KBd.table.data() + size_t(keyed_row_index(KBd.params, KH, x, kc)) * size_t(KH.row_bytes);
             out[i] = keyed_finish(KH, keyed_sum(KB, KBd.params, row, kc));
             continue;
         }
