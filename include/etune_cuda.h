@@ -271,10 +271,11 @@ etune_status etune_cu_profile_score(etune_cu_ctx* ctx, int on, double* pre_ms /*
                                     double* score_ms /*nullable*/, double* select_ms /*nullable*/,
                                     int64_t* calls /*nullable*/);
 
-/* Scoring form: 1 (default) = keyed path where the forest compiles to it (one byte per
- * (tiling triple, tree) in an L2-resident key table: <= 128 trees of <= 32 leaves,
- * <= 256 distinct non-Kuv masks per Kuv tree, table <= 64 MB), 0 = class-table kernel
- * only.  Both are bit-identical. */
+/* Scoring form for populations of >= 2^16 candidates: 1 (default) = keyed path where the
+ * forest compiles to it (<= 128 trees of <= 32 leaves, <= 256 distinct non-Kuv masks per
+ * Kuv tree): the full form (5-bit exit slots per (tiling triple, Kuv class), table
+ * <= 64 MB) or else the byte form (per tiling triple); 2 = byte form only; 0 = class-table
+ * kernel only.  All are bit-identical.  Set it before the first large scoring call. */
 etune_status etune_cu_forest_set_keyed(etune_cu_forest* forest, int mode);
 
 /* Reference-facing end-to-end call with HOST buffers: schedules in the reference's

@@ -465,9 +465,10 @@ class Forest:
         _check(lib().etune_cu_score(self.ctx.h, plan.h, self.h, _ptr(genome), n, _ptr(pred), _ptr(ids)))
         return (pred, ids) if (with_ids or ids_out is not None) else pred
 
-    def set_keyed(self, on: bool):
-        """Keyed scoring path for large populations (default on) or the class-table kernel only."""
-        _check(lib().etune_cu_forest_set_keyed(self.h, int(bool(on))))
+    def set_keyed(self, mode):
+        """Scoring form for large populations: True/1 keyed (full form when it fits, default),
+        2 keyed byte form only, False/0 class-table kernel only."""
+        _check(lib().etune_cu_forest_set_keyed(self.h, int(mode)))
         return self
 
     def score_select(self, plan: Plan, genome, k: int, pred, idx, ids=None):

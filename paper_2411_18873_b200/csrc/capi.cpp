@@ -254,7 +254,10 @@ etune_status ensure_keyed(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     std::string err;
     ScoreStats st;
     KeyedBuild kb;
-    if (build_score_blob(f->host, p->build, &blob, &st, &err, &kb) != ETUNE_OK || !kb.ok) return ETUNE_OK;
+    if (build_score_blob(f->host, p->build, &blob, &st, &err, &kb, size_t(64) << 20,
+                         f->keyed_mode == 2 ? 0 : size_t(64) << 20) != ETUNE_OK ||
+        !kb.ok)
+        return ETUNE_OK;
     const int cap = max_dynamic_smem(f->ctx->device) - score_static_smem();
     if (kb.blob.size() > size_t(cap)) return ETUNE_OK;
     CU(cudaMalloc(&cs->d_kblob, kb.blob.size()));
@@ -1020,7 +1023,7 @@ etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan*
 }
 
 etune_status etune_cu_forest_set_keyed(etune_cu_forest* f, int mode) {
-    if (!f || mode < 0 || mode > 1) return fail(ETUNE_ERR_INVALID_ARGUMENT, "mode must be 0 or 1");
+    if (!f || mode < 0 || mode > 2) return fail(ETUNE_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
     f->keyed_mode = mode;
     return ETUNE_OK;
 }

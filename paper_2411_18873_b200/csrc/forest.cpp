@@ -128,7 +128,8 @@ size_t debruijn_slot(int leaf, int mbits) {
 }
 
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
-                              ScoreStats* stats, std::string* err, KeyedBuild* keyed, size_t max_table_bytes) {
+                              ScoreStats* stats, std::string* err, KeyedBuild* keyed, size_t max_table_bytes,
+                              size_t max_full_bytes) {
     if (etune_status st = forest_validate(F, err)) return st;
     const PlanHdr& PH = P.hdr;
     const int nd1 = PH.nd[1], nd2 = PH.nd[2], ndk = PH.ndk;
@@ -587,27 +588,32 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                 keyed->params.ntrees = uint32_t(T);
                 keyed->params.kfull = 0;
                 // full form: every (key, Kuv class) row holds exit slots only
-                const size_t full_bytes = size_t(nk) * size_t(nkc) * size_t(row_bytes);
-                if (nkc > 0 && full_bytes <= max_table_bytes) {
+                // 5-bit slots, six per 32-bit word (24 trees per 16-byte quad)
+                const int frow = int((T + 23) / 24 * 16);
+                const size_t full_bytes = size_t(nk) * size_t(nkc) * size_t(frow);
+                if (nkc > 0 && full_bytes <= max_full_bytes) {
                     std::vector<uint8_t> ft(full_bytes, 0);
                     for (int64_t key = 0; key < nk; ++key) {
                         const uint8_t* row = keyed->table.data() + size_t(key) * size_t(row_bytes);
                         for (int x = 0; x < nkc; ++x) {
-                            uint8_t* fr = ft.data() + (size_t(key) * size_t(nkc) + size_t(x)) * size_t(row_bytes);
+                            uint32_t* fr =
+                                reinterpret_cast<uint32_t*>(ft.data() + (size_t(key) * size_t(nkc) + size_t(x)) * size_t(frow));
                             for (int64_t t = 0; t < T; ++t) {
+                                uint32_t slot = row[t];
                                 if ((tree_used[size_t(t)] >> kChKuv) & 1u) {
                                     const uint32_t m = mlists[size_t(t)][row[t]] &
                                                        kuvtab[size_t(t) * size_t(nkc) + size_t(x)];
-                                    fr[t] = uint8_t(((m & (0u - m)) * 0x077CB531u) >> 27);
-                                } else {
-                                    fr[t] = row[t];
+                                    slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
                                 }
+                                fr[t / 6] |= slot << (5 * (t % 6));
                             }
                         }
                     }
                     keyed->table.swap(ft);
                     keyed->params.kfull = 1;
                     for (int w = 0; w < 4; ++w) keyed->params.kuv_flags[w] = 0u;
+                    K.row_bytes = frow;
+                    std::memcpy(kbl.data(), &K, sizeof(K));
                 }
                 keyed->ok = true;
             }

@@ -42,6 +42,6 @@ struct KeyedBuild {
 };
 etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vector<uint8_t>* blob,
                               ScoreStats* stats, std::string* err, KeyedBuild* keyed = nullptr,
-                              size_t max_table_bytes = size_t(64) << 20);
+                              size_t max_table_bytes = size_t(64) << 20, size_t max_full_bytes = size_t(64) << 20);
 
 }  // namespace etune_b200

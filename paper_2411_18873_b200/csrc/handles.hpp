@@ -93,6 +93,6 @@ struct etune_cu_forest {
     uint32_t predict_bytes = 0;
     std::mutex mu;
     std::map<uint64_t, CompiledScore> compiled;  // by plan serial
-    int keyed_mode = 1;  // 1: keyed path where the forest compiles to it, 0: class-table kernel only
+    int keyed_mode = 1;  // 1: keyed path (full form when it fits), 2: keyed byte form only, 0: class tables only
 };
 

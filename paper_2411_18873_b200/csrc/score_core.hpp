@@ -269,6 +269,37 @@ ETUNE_UNROLL
     return sum;
 }
 
+// Full form: 24 trees per 16-byte quad (six 5-bit slots per word); FULL: no bound checks
+template <bool FULL>
+__host__ __device__ __forceinline__ double keyed_group5(const KeyedParams& P, SAddr base, uint32_t t0,
+                                                        const uint32_t* w, double sum) {
+ETUNE_UNROLL
+    for (uint32_t j = 0; j < 24; ++j) {
+        const uint32_t t = t0 + j;
+        if (FULL || t < P.ntrees) {
+            const uint32_t slot = (w[j / 6] >> (5 * (j % 6))) & 31u;
+            const SAddr blk = base + P.off_leaves + t * 256u + slot * 4u;
+            sum = ETUNE_DADD(sum, join_f64(lds32(blk), lds32(blk + 128u)));
+        }
+    }
+    return sum;
+}
+
+__host__ __device__ __forceinline__ double keyed_sum5(const uint8_t* KB, const KeyedParams& P, const uint8_t* row) {
+    const SAddr base = blob_saddr(KB);
+    double sum = 0.0;
+    const uint32_t T = P.ntrees;
+ETUNE_UNROLL
+    for (uint32_t t0 = 0; t0 < uint32_t(kKeyedMaxTrees); t0 += 24) {
+        if (t0 >= T) break;
+        const auto r = ld_row16(row, int(t0 / 24));
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+        if (t0 + 24 <= T) sum = keyed_group5<true>(P, base, t0, w, sum);
+        else sum = keyed_group5<false>(P, base, t0, w, sum);
+    }
+    return sum;
+}
+
 __host__ __device__ __forceinline__ double keyed_sum(const uint8_t* KB, const KeyedParams& P, const uint8_t* row,
                                                      uint32_t kc) {
     const SAddr base = blob_saddr(KB);

@@ -43,7 +43,9 @@ static int score_impl(const int64_t* op_words, int num_sms, const int32_t* featu
     std::vector<uint8_t> blob;
     ScoreStats S;
     KeyedBuild KBd;
-    if (int st = build_score_blob(F, P, &blob, &S, &g_err, keyed ? &KBd : nullptr)) return st;
+    if (int st = build_score_blob(F, P, &blob, &S, &g_err, keyed ? &KBd : nullptr, size_t(64) << 20,
+                                  keyed == 2 ? 0 : size_t(64) << 20))
+        return st;
     if (keyed && !KBd.ok) {
         g_err = "keyed form unavailable";
         return ETUNE_ERR_UNSUPPORTED;
@@ -81,7 +83,8 @@ static int score_impl(const int64_t* op_words, int num_sms, const int32_t* featu
             const Genome x = genome_unpack(gnm);
             const uint32_t kc = KB[KH.off_clskuv + (x.k * 16u + x.u) * 4u + x.v];
             const uint8_t* row = KBd.table.data() + size_t(keyed_row_index(KBd.params, KH, x, kc)) * size_t(KH.row_bytes);
-            out[i] = keyed_finish(KH, keyed_sum(KB, KBd.params, row, kc));
+            out[i] = keyed_finish(KH, KBd.params.kfull ? keyed_sum5(KB, KBd.params, row)
+                                                       : keyed_sum(KB, KBd.params, row, kc));
             continue;
         }
         const CandClasses cc = candidate_classes(B, H, gnm);
@@ -110,6 +113,14 @@ extern "C" int scc_score(const int64_t* op_words, int num_sms, const int32_t* fe
                          int64_t* stats_out) {
     return score_impl(op_words, num_sms, feature, threshold, left, right, value, offsets, num_trees, base, lr, sched,
                       n, out, stats_out, 0);
+}
+
+extern "C" int scc_score_keyed8(const int64_t* op_words, int num_sms, const int32_t* feature, const double* threshold,
+                                const int32_t* left, const int32_t* right, const double* value,
+                                const int64_t* offsets, int64_t num_trees, double base, double lr,
+                                const int64_t* sched, int64_t n, double* out, int64_t* stats_out) {
+    return score_impl(op_words, num_sms, feature, threshold, left, right, value, offsets, num_trees, base, lr, sched,
+                      n, out, stats_out, 2);
 }
 
 extern "C" int scc_score_keyed(const int64_t* op_words, int num_sms, const int32_t* feature, const double* threshold,

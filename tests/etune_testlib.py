@@ -540,10 +540,11 @@ SCC_SO = os.path.join(ROOT, "tests", "cpp", "libscorecheck.so")
 
 def host_compiled_score(op, forest: "FlatForest", sched, num_sms=108, keyed=False):
     """Forest compiler + scoring core run on the CPU (tests/cpp/score_core_check.cpp);
-    keyed=True scores through the keyed form (per-tiling-triple key table)."""
+    keyed=True scores through the keyed form (full (key, Kuv class) table when it fits),
+    keyed="byte" through the per-key byte table only."""
     L = C.CDLL(SCC_SO)
     L.scc_last_error.restype = C.c_char_p
-    fn = L.scc_score_keyed if keyed else L.scc_score
+    fn = L.scc_score_keyed8 if keyed == "byte" else L.scc_score_keyed if keyed else L.scc_score
     fn.argtypes = [I64P, C.c_int, I32P, F64P, I32P, I32P, F64P, I64P, C.c_int64, C.c_double, C.c_double,
                    I64P, C.c_int64, F64P, I64P]
     sched = np.ascontiguousarray(sched, np.int64).reshape(-1, 12)

@@ -25,7 +25,7 @@ def test_compiled_golden(golden, name):
 
 @pytest.mark.parametrize("name", MODEL_OPS)
 @pytest.mark.parametrize("sms", [108, 148])
-@pytest.mark.parametrize("keyed", [False, True])
+@pytest.mark.parametrize("keyed", [False, True, "byte"])
 def test_compiled_bred_population(golden, oracle, name, sms, keyed):
     op = golden[f"{name}/op"]
     fl = forest_of(golden, name)
@@ -38,15 +38,16 @@ def test_compiled_bred_population(golden, oracle, name, sms, keyed):
 
 @pytest.mark.parametrize("src,dst", [("c3_bert_ffn", "conv:1,7,7,512,512,3,1,1"), ("c2_r50_conv3x3", "mm:4,96,200,50"),
                                      ("c1_gemm1024", "conv:2,14,14,64,32,3,1,1")])
-def test_keyed_form_cross_operator(golden, oracle, src, dst):
-    """The keyed form (per tiling-triple AND of non-Kuv masks) on other operators,
-    incl. batch > 1 (three-index keys)."""
+@pytest.mark.parametrize("keyed", [True, "byte"])
+def test_keyed_form_cross_operator(golden, oracle, src, dst, keyed):
+    """The keyed forms (per tiling-triple AND of non-Kuv masks; full per (key, Kuv class)
+    5-bit slots) on other operators, incl. batch > 1 (three-index keys)."""
     op = parse_op(dst)
     fl = forest_of(golden, src)
     n = min(5000, oracle.count(op))
     s, _ = oracle.sample_random(op, n, 21)
     ref = oracle.predict(fl, oracle.features(op, s))
-    pred, _ = host_compiled_score(op, fl, s, keyed=True)
+    pred, _ = host_compiled_score(op, fl, s, keyed=keyed)
     assert (pred.view(np.uint64) == ref.view(np.uint64)).all()
 
 

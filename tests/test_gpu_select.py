@@ -163,7 +163,7 @@ def test_keyed_path_matches_class_tables_and_oracle(golden, oracle, ctx, capi, t
     p_ref = oracle.predict(flat, oracle.features(op, sched))
     g = plan.encode(dev(sched))
     outs = []
-    for keyed in (True, False):
+    for keyed in (1, 2, 0):
         fo = capi.Forest.from_flat(ctx, flat).set_keyed(keyed)
         pred = torch.empty(n, dtype=torch.float64, device="cuda")
         ids = torch.empty(n, dtype=torch.int64, device="cuda")
