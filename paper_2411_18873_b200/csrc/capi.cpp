@@ -19,6 +19,7 @@
 #include <thread>
 
 #include <sched.h>
+#include <immintrin.h>
 
 #include "forest.hpp"
 #include "kernels.hpp"
@@ -114,6 +115,31 @@ bool narrow_rows(const etune_schedule* src, W* dst, int64_t a, int64_t b) {
     return hi == 0;
 }
 
+// AVX-512 narrowing to u16 with non-temporal stores into the pinned staging (no
+// read-for-ownership of the staging lines: the packing is host-DRAM bound).  Element range
+// [lo, hi) of the int64 field array; lo must be a multiple of 8, dst 16-byte aligned.
+__attribute__((target("avx512f"))) bool narrow_u16_avx512(const int64_t* s, uint16_t* d, int64_t lo, int64_t hi) {
+    __m512i acc = _mm512_setzero_si512();
+    int64_t i = lo;
+    for (; i + 8 <= hi; i += 8) {
+        const __m512i v = _mm512_loadu_si512(reinterpret_cast<const void*>(s + i));
+        acc = _mm512_or_si512(acc, _mm512_srli_epi64(v, 16));
+        _mm_stream_si128(reinterpret_cast<__m128i*>(d + i), _mm512_cvtepi64_epi16(v));
+    }
+    uint64_t tail = 0;
+    for (; i < hi; ++i) {
+        tail |= uint64_t(s[i]) >> 16;
+        d[i] = uint16_t(s[i]);
+    }
+    _mm_sfence();  // the DMA engine reads the staging after the pool's hand-off
+    return _mm512_test_epi64_mask(acc, acc) == 0 && tail == 0;
+}
+
+bool have_avx512() {
+    static const bool ok = __builtin_cpu_supports("avx512f");
+    return ok;
+}
+
 int host_threads() {
     cpu_set_t set;
     if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, CPU_COUNT(&set));
@@ -124,15 +150,18 @@ int host_threads() {
 // 8 bytes), split over the host pool.  Returns the field width.
 int pack_rows(etune_cu_ctx* c, const etune_schedule* src, int64_t m, void* dst) {
     const int tasks = std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m / 2048));
-    auto range = [&](int t, int64_t* a, int64_t* b) {
-        *a = m * t / tasks;
-        *b = m * (t + 1) / tasks;
+    auto range = [&](int t, int64_t* a, int64_t* b) {  // even row boundaries: 24 fields = 3 AVX-512 words
+        *a = (m * t / tasks) & ~int64_t(1);
+        *b = t + 1 == tasks ? m : (m * (t + 1) / tasks) & ~int64_t(1);
     };
     std::vector<char> ok(size_t(tasks), 1);
+    const bool simd = have_avx512() && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
     c->pool->run(tasks, [&](int t) {
         int64_t a, b;
         range(t, &a, &b);
-        ok[size_t(t)] = narrow_rows(src, static_cast<uint16_t*>(dst), a, b);
+        ok[size_t(t)] = simd ? narrow_u16_avx512(reinterpret_cast<const int64_t*>(src), static_cast<uint16_t*>(dst),
+                                                 12 * a, 12 * b)
+                             : narrow_rows(src, static_cast<uint16_t*>(dst), a, b);
     });
     if (std::all_of(ok.begin(), ok.end(), [](char x) { return x != 0; })) return 2;
     c->pool->run(tasks, [&](int t) {
