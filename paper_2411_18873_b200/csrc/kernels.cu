@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_
         const uint32_t kc = clskuv[(x.k * 16u + x.u) * 4u + x.v];
         const uint8_t* row = table + size_t(keyed_row_index(kp, K, x, kc)) * row_bytes;
         const double p = keyed_finish(K, kp.kfull ? keyed_sum5(S, kp, row) : keyed_sum(S, kp, row, kc));
-        __stcs(pred + idx, p);  // streaming store: keep L2 for the key table
+        pred[idx] = p;  // stays in L2 for the selection filter that reads it next
         if (sel.hist) atomicAdd(&shist[sel_bin(p, sel)], 1u);
         if (ids) {
             Knobs c;
