@@ -12,11 +12,9 @@
 // memory, so the per-candidate work touches HBM only for its 8-byte genome and its
 // outputs.  Built with -fmad=false: every double op rounds exactly like the
 // reference's; no transcendental is evaluated on the device.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <atomic>
-#include <mutex>
 #include <cstdint>
 
 #include "etune_internal.hpp"
@@ -574,7 +572,7 @@ __global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_
     const int64_t* divk = at<int64_t>(S, K.off_divk);
     const uint32_t row_bytes = uint32_t(K.row_bytes);
     for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < n; s += int64_t(gridDim.x) * blockDim.x) {
-        // with an order, genome[] is the population in that order (key_place_kernel)
+        // with an order, genome[] is the population already in that order
         const uint32_t idx = order ? __ldg(order + s) : uint32_t(s);
         const Genome x = genome_unpack(__ldcs(genome + s));  // read once: evict first
         const uint32_t kc = clskuv[(x.k * 16u + x.u) * 4u + x.v];
