@@ -4,7 +4,9 @@
 //   ids                  candidate_id (space.cpp:22-45), FNV-1a, operator prefix hoisted
 //   counters             derive_counters (counters.cpp:9-49), int64 exact
 //   features             extract_features (features.cpp:15-51) via the plan's tables
-//   score                fused features -> 100-tree forest -> prediction (+ id)
+//   score                fused features -> 100-tree forest -> prediction (+ id), class-table form
+//   score_keyed          the same from the keyed forms (key-table rows of exit slots; default
+//                        for populations >= 2^16, see forest.cpp / score_core.hpp)
 //   predict              EnergyModel::predict on caller feature vectors
 //
 // All kernels are persistent grid-stride loops sized to the SM count; every kernel
