@@ -414,7 +414,7 @@ etune_status shard_merge(etune_cu_ctx* c, const double* d_score, int64_t kl, int
     double* gs = b.gs;
     int64_t* gg = b.gg;
     CU(launch_pack_records(c->lc(), d_score, b.lidx, kl, k, goff, b.ls, b.lg));
-    if (W > 1) {
+    if (c->comm) {  // any attached communicator, a single rank included (same code path as W > 1)
         ncclResult_t r = ncclGroupStart();
         if (r == ncclSuccess) r = ncclAllGather(b.ls, gs, size_t(k), ncclFloat64, c->comm, c->stream);
         if (r == ncclSuccess) r = ncclAllGather(b.lg, gg, size_t(k), ncclInt64, c->comm, c->stream);

@@ -1,5 +1,7 @@
 """GPU parity of the cost-model scalars (energy_loss, snr_db) and of the
 population-sharded selection (etune_cu_topk_sharded, NCCL all-gather merge)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -91,6 +93,26 @@ def test_topk_sharded_nccl_one_rank(oracle, ctx, capi):
     idx, sc = capi.topk_sharded(c2, dev(vals), 12345, 777)
     c2.synchronize()
     assert (idx.cpu().numpy() == 12345 + oracle.topk(vals, 777)).all()
+    # the fused per-shard score + select + all-gather merge through the communicator
+    from etune_testlib import FlatForest, parse_op
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "golden_reference.npz"))
+    mk = "c2_r50_conv3x3/model/"
+    flat = FlatForest(g[mk + "feature"], g[mk + "threshold"], g[mk + "left"], g[mk + "right"], g[mk + "value"],
+                      g[mk + "offsets"], float(g[mk + "base_score"][0]), float(g[mk + "learning_rate"][0]))
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    par, _ = oracle.sample_random(op, 256, 1)
+    s, _, _, _ = oracle.reproduce(op, par, 90000, 2)
+    ref = oracle.predict(flat, oracle.features(op, s))
+    plan = capi.Plan(c2, op)
+    fo = capi.Forest.from_flat(c2, flat)
+    pred = torch.empty(len(s), dtype=torch.float64, device="cuda")
+    gidx = torch.empty(1000, dtype=torch.int64, device="cuda")
+    gsc = torch.empty(1000, dtype=torch.float64, device="cuda")
+    fo.score_select_sharded(plan, plan.encode(dev(s)), 5000, 1000, pred, gidx, gsc)
+    c2.synchronize()
+    want = oracle.topk(ref, 1000)
+    assert (gidx.cpu().numpy() == 5000 + want).all()
+    assert (gsc.cpu().numpy().view(np.uint64) == ref[want].view(np.uint64)).all()
     buf = torch.arange(10, dtype=torch.float64, device="cuda")
     capi.broadcast(c2, buf, 0)
     c2.synchronize()
