@@ -23,10 +23,14 @@
 // Per level: gather (grad/hess/feature values into list order) -> chains (one warp per
 // (list, node): the sequential prefix sums, staged through shared memory) -> gains at
 // every position (parallel; per-(node, feature) argmax by two atomic passes) -> decide
-// -> left flags -> stable partition (global scan of the left flags + scatter).
+// -> stable partition (global scan of the routing flags + scatter).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cstdint>
 
 #include "etune_internal.hpp"
@@ -50,6 +54,8 @@ struct TrainCtl {
     int32_t nseg[2];
     int32_t seg_start[2][kMaxSeg], seg_end[2][kMaxSeg], seg_node[2][kMaxSeg];
     int32_t split[kMaxSeg];   // child rank r (children 2r, 2r+1 of the next frontier) or -1
+    int32_t sfeat[kMaxSeg];   // split feature of frontier segment k or -1, and its threshold:
+    double sthr[kMaxSeg];     // the routing flag of a list position without the node lookup
     int32_t nnodes;
     int32_t tree;             // trees finished
     int64_t out_nodes;        // nodes written to the output forest so far
@@ -75,7 +81,7 @@ __device__ __forceinline__ double obj(double g, double h, double lambda) {  // l
 // ---------------------------------------------------------------- init
 // Sequential sum of x[0..n) in index order by one thread, reading 256-element chunks the
 // whole CTA staged into shared memory (the reference's loops are one dependent chain).
-__device__ double cta_sequential_sum(const double* __restrict__ x, int64_t n, double* stage) {
+__device__ double cta_sequential_sum(const double* x, int64_t n, double* stage) {
     double acc = 0.0;
     for (int64_t base = 0; base < n; base += 1024) {
         const int cnt = int(n - base < 1024 ? n - base : 1024);
@@ -200,9 +206,12 @@ __global__ void __launch_bounds__(1024) sort_kernel(const double* __restrict__ f
 }
 
 // ----------------------------------------------------- per tree: gradients
-__global__ void grad_kernel(const double* __restrict__ pred, const double* __restrict__ target, int64_t n,
-                            double* __restrict__ grad, double* __restrict__ hess, TrainCtl* ctl) {
-    pdl_wait();
+// The per-tree phases below are device functions shared by the per-kernel graph path
+// (thin __global__ wrappers) and the cooperative megakernel (train_mega_kernel): their
+// pointers carry no __restrict__, since inside the megakernel every buffer but the
+// features and targets is rewritten between phases (no read-only-cache loads).
+__device__ __forceinline__ void grad_phase(const double* pred, const double* target, int64_t n, double* grad,
+                                           double* hess, TrainCtl* ctl) {
     const int64_t i0 = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
     if (i0 == 0) {  // fresh tree: a single root leaf holding every sample
         ctl->nseg[0] = 1;
@@ -223,6 +232,11 @@ __global__ void grad_kernel(const double* __restrict__ pred, const double* __res
         hess[i] = __ddiv_rn(2.0, m);
     }
 }
+__global__ void grad_kernel(const double* __restrict__ pred, const double* __restrict__ target, int64_t n,
+                            double* __restrict__ grad, double* __restrict__ hess, TrainCtl* ctl) {
+    pdl_wait();
+    grad_phase(pred, target, n, grad, hess, ctl);
+}
 
 // segment (frontier index) of every position, -1 for dead ranges; identical for all lists
 __device__ __forceinline__ int32_t seg_of(int64_t p, int nseg, const int32_t* ss, const int32_t* se) {
@@ -239,11 +253,9 @@ __device__ __forceinline__ int32_t seg_of(int64_t p, int nseg, const int32_t* ss
 // gl/hl[l][p] = grad/hess[list[l][p]], fv[l][p] = feature l of that sample: everything the
 // chains and gains read afterwards is contiguous in list order.  With segmap non-null the
 // same launch also maps every list position to its frontier segment (-1: a leaf's range).
-__global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int nl, const double* __restrict__ grad,
-                              const double* __restrict__ hess, const double* __restrict__ feats,
-                              double* __restrict__ gl, double* __restrict__ hl, double* __restrict__ fv, int lvl,
-                              const TrainCtl* __restrict__ ctl, int32_t* __restrict__ segmap) {
-    pdl_wait();
+__device__ __forceinline__ void gather_phase(const int32_t* lists, int64_t n, int nl, const double* grad,
+                                             const double* hess, const double* feats, double* gl, double* hl,
+                                             double* fv, int lvl, const TrainCtl* ctl, int32_t* segmap) {
     const int64_t tot = int64_t(nl) * n;
     const int64_t off = int64_t(kLists - nl) * n;  // nl == 1: sample list only
     const int b = lvl & 1;
@@ -256,6 +268,13 @@ __global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int 
         if (g < int64_t(kF) * n) fv[g] = feats[int64_t(idx) * kF + g / n];
         if (segmap && q < n) segmap[q] = seg_of(q, nseg, ctl->seg_start[b], ctl->seg_end[b]);
     }
+}
+__global__ void gather_kernel(const int32_t* __restrict__ lists, int64_t n, int nl, const double* __restrict__ grad,
+                              const double* __restrict__ hess, const double* __restrict__ feats,
+                              double* __restrict__ gl, double* __restrict__ hl, double* __restrict__ fv, int lvl,
+                              const TrainCtl* __restrict__ ctl, int32_t* __restrict__ segmap) {
+    pdl_wait();
+    gather_phase(lists, n, nl, grad, hess, feats, gl, hl, fv, lvl, ctl, segmap);
 }
 
 // Per (list, frontier segment): the sequential running sums, kChunk elements at a time
@@ -275,24 +294,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void bar_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ void bar_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 
-// Two warps per (list, segment): warp 1 streams chunks in (cp.async, two buffers) and
-// the prefixes out, warp 0 only chains (lanes 0/1), so the chain never waits on memory.
-// Named barriers 1+b ("buffer b full") and 3+b ("buffer b chained") hand the buffers over.
-__global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_totals,
-                                                   const double* __restrict__ gl, const double* __restrict__ hl,
-                                                   double* __restrict__ pg, double* __restrict__ ph, TrainCtl* ctl) {
-    pdl_wait();
-    // prefixes overwrite their operands in place (each operand is in registers by then)
-    __shared__ __align__(16) double ig[2][kChunk + 8];
-    __shared__ __align__(16) double ih[2][kChunk + 8];
-    const int b = lvl & 1;
-    const int nseg = ctl->nseg[b];
-    if (nseg <= 0) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t = blockIdx.x;
-    const int l = only_totals ? kSampleList : t / nseg;
-    const int k = only_totals ? t : t % nseg;
-    if (k >= nseg || l >= kLists) return;
+// One (list l, frontier segment k) chain by a 64-thread slot: warp 1 streams chunks in
+// (cp.async, two buffers) and the prefixes out, warp 0 only chains (lanes 0/1), so the
+// chain never waits on memory.  Named barriers bar0+b ("buffer b full") and bar0+2+b
+// ("buffer b chained") hand the buffers over; ig/ih are two (kChunk + 8)-double buffers
+// each.  Prefixes overwrite their operands in place (each operand is in registers by then).
+__device__ __forceinline__ void chain_task(int64_t n, int b, int l, int k, const double* gl, const double* hl,
+                                           double* pg, double* ph, TrainCtl* ctl, double* ig, double* ih,
+                                           int bar0, int warp, int lane) {
+    constexpr int kBuf = kChunk + 8;
     const int s = ctl->seg_start[b][k], e = ctl->seg_end[b][k];
     const int nch = (e - s + kChunk - 1) / kChunk;
     const bool prefixes = l != kSampleList;
@@ -304,8 +314,8 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
         auto load = [&](int c) {
             const int base = s + c * kChunk, cnt = min(kChunk, e - base), bb = c & 1;
             for (int j = lane; j < cnt; j += 32) {
-                cp_async8(&ig[bb][j], G + base + j);
-                cp_async8(&ih[bb][j], Hh + base + j);
+                cp_async8(&ig[bb * kBuf + j], G + base + j);
+                cp_async8(&ih[bb * kBuf + j], Hh + base + j);
             }
             cp_async_commit();
         };
@@ -317,19 +327,19 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
         } else {
             cp_async_wait_all();
         }
-        bar_arrive(1);  // chunk 0 in buffer 0
+        bar_arrive(bar0);  // chunk 0 in buffer 0
         for (int c = 0; c < nch; ++c) {
             const int bb = c & 1;
             if (c + 1 < nch) {
                 cp_async_wait_all();  // chunk c+1 (the only group in flight)
-                bar_arrive(1 + (bb ^ 1));
+                bar_arrive(bar0 + (bb ^ 1));
             }
-            bar_sync(3 + bb);  // chunk c chained in place
+            bar_sync(bar0 + 2 + bb);  // chunk c chained in place
             if (prefixes) {
                 const int base = s + c * kChunk, cnt = min(kChunk, e - base);
                 for (int j = lane; j < cnt; j += 32) {
-                    PG[base + j] = ig[bb][j];
-                    PH[base + j] = ih[bb][j];
+                    PG[base + j] = ig[bb * kBuf + j];
+                    PH[base + j] = ih[bb * kBuf + j];
                 }
             }
             __syncwarp();
@@ -345,9 +355,9 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
     for (int c = 0; c < nch; ++c) {
         const int bb = c & 1;
         const int cnt = min(kChunk, e - (s + c * kChunk));
-        bar_sync(1 + bb);
+        bar_sync(bar0 + bb);
         if (lane < 2) {
-            double* cx = lane == 0 ? ig[bb] : ih[bb];
+            double* cx = (lane == 0 ? ig : ih) + bb * kBuf;
             double2* c2 = reinterpret_cast<double2*>(cx);
             const int nb = cnt >> 3;
             const int full = nb << 3;
@@ -357,16 +367,15 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
                 for (int q = 0; q < 4; ++q) x[q] = c2[bi * 4 + q];
             };
             auto run = [&](const double2* x, int bi) {
-                double2 pv[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                    pv[q].x = racc;
+                    double2 pv;
+                    pv.x = racc;
                     racc = __dadd_rn(racc, x[q].x);
-                    pv[q].y = racc;
+                    pv.y = racc;
                     racc = __dadd_rn(racc, x[q].y);
+                    c2[bi * 4 + q] = pv;
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) c2[bi * 4 + q] = pv[q];
             };
             if (nb > 0) ld(xa, 0);
             int bi = 0;
@@ -384,7 +393,7 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
             }
         }
         __syncwarp();
-        bar_arrive(3 + bb);
+        bar_arrive(bar0 + 2 + bb);
     }
     const double rg = __shfl_sync(0xffffffffu, racc, 0), rh = __shfl_sync(0xffffffffu, racc, 1);
     if (lane == 0) {
@@ -399,12 +408,26 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
     }
 }
 
+// graph path: one CTA (one slot) per (list, segment)
+__global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_totals,
+                                                   const double* __restrict__ gl, const double* __restrict__ hl,
+                                                   double* __restrict__ pg, double* __restrict__ ph, TrainCtl* ctl) {
+    pdl_wait();
+    __shared__ __align__(16) double ig[2 * (kChunk + 8)];
+    __shared__ __align__(16) double ih[2 * (kChunk + 8)];
+    const int b = lvl & 1;
+    const int nseg = ctl->nseg[b];
+    if (nseg <= 0) return;
+    const int t = blockIdx.x;
+    const int l = only_totals ? kSampleList : t / nseg;
+    const int k = only_totals ? t : t % nseg;
+    if (k >= nseg || l >= kLists) return;
+    chain_task(n, b, l, k, gl, hl, pg, ph, ctl, ig, ih, 1, threadIdx.x >> 5, threadIdx.x & 31);
+}
+
 // split gain at every (feature list, position) (cpp 97-118); per-(node, feature) max
 // gain by atomicMax on the (positive) gain's bits
-__global__ void gain_kernel(int64_t n, int lvl, const int32_t* __restrict__ segmap, const double* __restrict__ fv,
-                            const double* __restrict__ pg, const double* __restrict__ ph, double mlw, double lambda,
-                            double* __restrict__ gains, TrainCtl* ctl) {
-    pdl_wait();
+__device__ __forceinline__ void gain_phase(int64_t n, int lvl, const int32_t* segmap, const double* fv, const double* pg, const double* ph, double mlw, double lambda, double* gains, TrainCtl* ctl) {
     const int b = lvl & 1;
     const int64_t tot = int64_t(kF) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
@@ -432,11 +455,15 @@ __global__ void gain_kernel(int64_t n, int lvl, const int32_t* __restrict__ segm
         gains[q] = gain;
     }
 }
+__global__ void gain_kernel(int64_t n, int lvl, const int32_t* __restrict__ segmap, const double* __restrict__ fv,
+                            const double* __restrict__ pg, const double* __restrict__ ph, double mlw, double lambda,
+                            double* __restrict__ gains, TrainCtl* ctl) {
+    pdl_wait();
+    gain_phase(n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
+}
 
 // earliest position attaining the max (ties: the reference's strict > keeps the first)
-__global__ void gainpos_kernel(int64_t n, const int32_t* __restrict__ segmap, const double* __restrict__ gains,
-                               TrainCtl* ctl) {
-    pdl_wait();
+__device__ __forceinline__ void gainpos_phase(int64_t n, const int32_t* segmap, const double* gains, TrainCtl* ctl) {
     const int64_t tot = int64_t(kF) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
         const double g = gains[q];
@@ -448,12 +475,15 @@ __global__ void gainpos_kernel(int64_t n, const int32_t* __restrict__ segmap, co
             atomicMin(&ctl->gpos[k][l], int32_t(p));
     }
 }
+__global__ void gainpos_kernel(int64_t n, const int32_t* __restrict__ segmap, const double* __restrict__ gains,
+                               TrainCtl* ctl) {
+    pdl_wait();
+    gainpos_phase(n, segmap, gains, ctl);
+}
 
 // One CTA: choose each node's split (features in order, strictly larger gain wins,
 // cpp 111-117), allocate children in frontier order (cpp 130-143).
-__global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const double* __restrict__ fv,
-                                                      TrainCtl* ctl) {
-    pdl_wait();
+__device__ __forceinline__ void decide_phase(int64_t n, int lvl, const double* fv, TrainCtl* ctl) {
     const int b = lvl & 1;
     const int nseg = ctl->nseg[b];
     __shared__ int wsum[32];
@@ -465,17 +495,22 @@ __global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const 
         int bf = -1;
         double bg = 0.0, bt = 0.0;
         if (k < nseg) {
+            unsigned long long bits[kF];  // all 16 loads in flight, then the scan in feature order
+#pragma unroll
+            for (int f = 0; f < kF; ++f) bits[f] = ctl->gbits[k][f];
+#pragma unroll
             for (int f = 0; f < kF; ++f) {
-                const unsigned long long bits = ctl->gbits[k][f];
-                if (bits == 0ull) continue;
-                const double g = __longlong_as_double(static_cast<long long>(bits));
+                if (bits[f] == 0ull) continue;
+                const double g = __longlong_as_double(static_cast<long long>(bits[f]));
                 if (g > kMinSplitGain && g > bg) {
                     bg = g;
                     bf = f;
-                    const int64_t pos = ctl->gpos[k][f];
-                    const double* F = fv + int64_t(f) * n;
-                    bt = __dmul_rn(0.5, __dadd_rn(F[pos - 1], F[pos]));  // cpp 115-116
                 }
+            }
+            if (bf >= 0) {
+                const int64_t pos = ctl->gpos[k][bf];
+                const double* F = fv + int64_t(bf) * n;
+                bt = __dmul_rn(0.5, __dadd_rn(F[pos - 1], F[pos]));  // cpp 115-116
             }
         }
         const int flag = bf >= 0;
@@ -508,6 +543,8 @@ __global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const 
             } else {
                 ctl->split[k] = -1;
             }
+            ctl->sfeat[k] = bf;
+            ctl->sthr[k] = bt;
         }
         __syncthreads();
         if (threadIdx.x == 0) s_base += total;
@@ -518,32 +555,23 @@ __global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const 
         ctl->nseg[b ^ 1] = 2 * s_base;
     }
 }
-
-// routing decision per sample of a split node: value < threshold goes left (cpp 146-148)
-__global__ void leftflag_kernel(const double* __restrict__ feats, const int32_t* __restrict__ lists, int64_t n,
-                                int lvl, const int32_t* __restrict__ segmap, const TrainCtl* __restrict__ ctl,
-                                uint8_t* __restrict__ lf) {
+__global__ void __launch_bounds__(1024) decide_kernel(int64_t n, int lvl, const double* __restrict__ fv,
+                                                      TrainCtl* ctl) {
     pdl_wait();
-    const int b = lvl & 1;
-    const int32_t* S = lists + int64_t(kSampleList) * n;
-    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
-        const int k = segmap[p];
-        if (k < 0 || ctl->split[k] < 0) continue;
-        const int node = ctl->seg_node[b][k];
-        const int32_t idx = S[p];
-        lf[idx] = feats[int64_t(idx) * kF + ctl->feature[node]] < ctl->thr[node] ? 1 : 0;
-    }
+    decide_phase(n, lvl, fv, ctl);
 }
 
-struct LeftFlagFn {  // flag of list position q (0 outside split segments)
+struct LeftFlagFn {  // routing flag of list position q (0 outside split segments), cpp 146-148
     const int32_t* lists;
     const int32_t* segmap;
-    const int32_t* split;
-    const uint8_t* lf;
+    const TrainCtl* ctl;
+    const double* feats;
     int64_t n;
     __device__ int64_t operator()(int64_t q) const {
         const int k = segmap[q % n];
-        return (k >= 0 && split[k] >= 0) ? int64_t(lf[lists[q]]) : 0;
+        const int f = k >= 0 ? ctl->sfeat[k] : -1;
+        if (f < 0) return 0;
+        return feats[int64_t(lists[q]) * kF + f] < ctl->sthr[k] ? 1 : 0;
     }
 };
 struct PrefixWrite {
@@ -551,43 +579,58 @@ struct PrefixWrite {
     __device__ void operator()(int64_t q, int64_t ex) const { pfx[q] = ex; }
 };
 
-// stable partition of every split segment into [left | right] in every list; list 16
-// also writes the children's segment bounds
-__global__ void scatter_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
-                               const int64_t* __restrict__ pfx, const int32_t* __restrict__ segmap, int64_t n,
-                               int lvl, TrainCtl* ctl) {
-    pdl_wait();
+// Stable partition of every split segment into [left | right] in every list (list 16
+// also writes the children's segment bounds), fused with the next level's gather: each
+// element's (grad, hess, feature value) row and segment (2r / 2r + 1 for the children
+// of split rank r, -1 for a leaf's range) are written at its destination.
+__device__ __forceinline__ void scatter_phase(const int32_t* src, int32_t* dst, const int64_t* pfx,
+                                              const int32_t* segmap, int32_t* nsegmap, int64_t n, int lvl,
+                                              TrainCtl* ctl, const double* grad, const double* hess,
+                                              const double* feats, double* gl, double* hl, double* fv) {
     const int b = lvl & 1;
     const int64_t tot = int64_t(kLists) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
         const int64_t l = q / n, p = q % n;
         const int k = segmap[p];
+        const int r = k >= 0 ? ctl->split[k] : -1;
         int64_t d = p;
-        if (k >= 0 && ctl->split[k] >= 0) {
+        int nk = -1;
+        if (r >= 0) {
             const int64_t s = ctl->seg_start[b][k], e = ctl->seg_end[b][k];
             const int64_t* P = pfx + l * n;
             const int64_t pl = P[p] - P[s];
             const int64_t L = P[e] - P[s];
             const int64_t left = P[p + 1] - P[p];
             d = left ? s + pl : s + L + (p - s - pl);
+            nk = left ? 2 * r : 2 * r + 1;
             if (l == kSampleList && p == s) {
-                const int r = ctl->split[k];
                 ctl->seg_start[b ^ 1][2 * r] = int32_t(s);
                 ctl->seg_end[b ^ 1][2 * r] = int32_t(s + L);
                 ctl->seg_start[b ^ 1][2 * r + 1] = int32_t(s + L);
                 ctl->seg_end[b ^ 1][2 * r + 1] = int32_t(e);
             }
         }
-        dst[l * n + d] = src[q];
+        const int32_t idx = src[q];
+        const int64_t g = l * n + d;
+        dst[g] = idx;
+        gl[g] = grad[idx];
+        hl[g] = hess[idx];
+        if (l < kF) fv[g] = feats[int64_t(idx) * kF + l];
+        else nsegmap[d] = nk;
     }
+}
+__global__ void scatter_kernel(const int32_t* __restrict__ src, int32_t* __restrict__ dst,
+                               const int64_t* __restrict__ pfx, const int32_t* __restrict__ segmap,
+                               int32_t* __restrict__ nsegmap, int64_t n, int lvl, TrainCtl* ctl,
+                               const double* __restrict__ grad, const double* __restrict__ hess,
+                               const double* __restrict__ feats, double* __restrict__ gl, double* __restrict__ hl,
+                               double* __restrict__ fv) {
+    pdl_wait();
+    scatter_phase(src, dst, pfx, segmap, nsegmap, n, lvl, ctl, grad, hess, feats, gl, hl, fv);
 }
 
 // Leaf Newton weights (cpp 161-166) and the tree appended to the output forest.
-__global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl* ctl,
-                                                       int32_t* __restrict__ o_feature, double* __restrict__ o_thr,
-                                                       int32_t* __restrict__ o_left, int32_t* __restrict__ o_right,
-                                                       double* __restrict__ o_value, int64_t* __restrict__ o_off) {
-    pdl_wait();
+__device__ __forceinline__ void finalize_phase(double lambda, TrainCtl* ctl, int32_t* o_feature, double* o_thr, int32_t* o_left, int32_t* o_right, double* o_value, int64_t* o_off) {
     const int nn = ctl->nnodes;
     const int64_t base = ctl->out_nodes;
     const int tree = ctl->tree;
@@ -607,11 +650,16 @@ __global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl*
         ctl->tree = tree + 1;
     }
 }
+__global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl* ctl,
+                                                       int32_t* __restrict__ o_feature, double* __restrict__ o_thr,
+                                                       int32_t* __restrict__ o_left, int32_t* __restrict__ o_right,
+                                                       double* __restrict__ o_value, int64_t* __restrict__ o_off) {
+    pdl_wait();
+    finalize_phase(lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
+}
 
 // pred[i] += lr * tree.eval(feat[i])  (cpp 236-238)
-__global__ void update_kernel(const double* __restrict__ feats, int64_t n, double lr, const TrainCtl* __restrict__ ctl,
-                              double* __restrict__ pred) {
-    pdl_wait();
+__device__ __forceinline__ void update_phase(const double* feats, int64_t n, double lr, const TrainCtl* ctl, double* pred) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         int node = 0;
         int f = ctl->feature[0];
@@ -622,12 +670,13 @@ __global__ void update_kernel(const double* __restrict__ feats, int64_t n, doubl
         pred[i] = __dadd_rn(pred[i], __dmul_rn(lr, ctl->value[node]));
     }
 }
-
-__global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ pred,
-                                                   const double* __restrict__ target, int64_t n,
-                                                   const TrainCtl* __restrict__ ctl, double* __restrict__ loss,
-                                                   double* __restrict__ tmp) {
+__global__ void update_kernel(const double* __restrict__ feats, int64_t n, double lr, const TrainCtl* __restrict__ ctl,
+                              double* __restrict__ pred) {
     pdl_wait();
+    update_phase(feats, n, lr, ctl, pred);
+}
+
+__device__ __forceinline__ void loss_phase(const double* pred, const double* target, int64_t n, const TrainCtl* ctl, double* loss, double* tmp) {
     __shared__ double stage[1024 + 8];
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = __dsub_rn(pred[i], target[i]);
@@ -637,6 +686,148 @@ __global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ p
     const double tot = cta_sequential_sum(tmp, n, stage);
     if (threadIdx.x == 0) loss[ctl->tree] = __ddiv_rn(tot, static_cast<double>(n));  // after finalize: round t+1
 }
+__global__ void __launch_bounds__(1024) loss_kernel(const double* __restrict__ pred,
+                                                   const double* __restrict__ target, int64_t n,
+                                                   const TrainCtl* __restrict__ ctl, double* __restrict__ loss,
+                                                   double* __restrict__ tmp) {
+    pdl_wait();
+    loss_phase(pred, target, n, ctl, loss, tmp);
+}
+
+// ------------------------------------------------------------ megakernel
+// Opt-in alternative (ETUNE_TRAIN_MEGA=1): the whole training (every tree, every
+// level) as ONE cooperative launch, the phases above separated by grid-wide barriers
+// instead of kernel boundaries.  Every CTA (one per SM) runs kMegaSlots chain slots of
+// 64 threads (named barriers 1..12) over dynamic shared memory.  Measured slower than
+// the PDL graph ("Training"): with one 512-thread CTA per SM the grid-wide
+// phases have 4x fewer loads in flight than the graph's 1-element-per-thread grids,
+// and 128 registers per thread leave the chains ~20% slower; kept as a parity-tested
+// variant.
+constexpr int kMegaSlots = 3;
+constexpr int kMegaT = 512;  // warps 0..5: chain slots; all 16 warps run the grid-wide phases
+constexpr size_t kMegaSmem = size_t(kMegaSlots) * 4 * (kChunk + 8) * sizeof(double);
+
+struct MegaArgs {
+    int64_t n;
+    int num_trees, max_depth;
+    double lr, mlw, lambda;
+    const double* feats;
+    const double* target;
+    double *pred, *grad, *hess, *gl, *hl, *fv, *pg, *ph, *gains;
+    const int32_t* base_lists;
+    int32_t* work[2];
+    int32_t* segmap[2];
+    int64_t* pfx;
+    int64_t* sums;
+    TrainCtl* ctl;
+    int32_t *o_feature, *o_left, *o_right;
+    double *o_thr, *o_value, *o_loss;
+    int64_t* o_off;
+    unsigned long long* trace;  // diagnostic: %globaltimer after every barrier of tree 0 (or null)
+};
+
+// routing flag of list position q at frontier parity b (leftflag_kernel + LeftFlagFn)
+__device__ __forceinline__ int64_t mega_flag(const MegaArgs& a, const int32_t* cur, const int32_t* segmap, int b,
+                                             int64_t q) {
+    const int k = segmap[q % a.n];
+    const int f = k >= 0 ? a.ctl->sfeat[k] : -1;
+    if (f < 0) return 0;
+    const int32_t idx = cur[q];
+    return a.feats[int64_t(idx) * kF + f] < a.ctl->sthr[k] ? 1 : 0;
+}
+
+// the CTA's contiguous share [r0, r1) of the L list positions
+__device__ __forceinline__ void mega_range(int64_t L, int64_t* r0, int64_t* r1) {
+    const int64_t per = (L + gridDim.x - 1) / gridDim.x;
+    *r0 = min(L, int64_t(blockIdx.x) * per);
+    *r1 = min(L, *r0 + per);
+}
+
+__global__ void __launch_bounds__(kMegaT, 1) train_mega_kernel(const __grid_constant__ MegaArgs a) {
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(16) double mega_smem[];
+    const int slot = threadIdx.x >> 6, warp = (threadIdx.x >> 5) & 1, lane = threadIdx.x & 31;
+    double* ig = mega_smem + slot * 4 * (kChunk + 8);
+    double* ih = ig + 2 * (kChunk + 8);
+    const int bar0 = 1 + 4 * slot;
+    const int64_t n = a.n, L = int64_t(kLists) * n;
+    TrainCtl* ctl = a.ctl;
+    const bool chainer = threadIdx.x < 64 * kMegaSlots;
+    // task t -> CTA t % grid: one chain per SM before any SM takes a second
+    const int slot_id = slot * gridDim.x + blockIdx.x, nslots = gridDim.x * kMegaSlots;
+    int tick = 0;
+    auto sync = [&]() {
+        grid.sync();
+        if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && tick < 256) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[tick] = t;
+        }
+        ++tick;
+    };
+    for (int tree = 0; tree < a.num_trees; ++tree) {
+        grad_phase(a.pred, a.target, n, a.grad, a.hess, ctl);
+        sync();
+        gather_phase(a.base_lists, n, kLists, a.grad, a.hess, a.feats, a.gl, a.hl, a.fv, 0, ctl, a.segmap[0]);
+        sync();
+        const int32_t* cur = a.base_lists;
+        for (int depth = 0; depth < a.max_depth; ++depth) {
+            const int b = depth & 1;
+            const int nseg = ctl->nseg[b];
+            for (int t = slot_id; chainer && t < kLists * nseg; t += nslots)
+                chain_task(n, b, t / nseg, t % nseg, a.gl, a.hl, a.pg, a.ph, ctl, ig, ih, bar0, warp, lane);
+            sync();
+            gain_phase(n, b, a.segmap[b], a.fv, a.pg, a.ph, a.mlw, a.lambda, a.gains, ctl);
+            sync();
+            gainpos_phase(n, a.segmap[b], a.gains, ctl);
+            sync();
+            if (blockIdx.x == 0) decide_phase(n, b, a.fv, ctl);
+            sync();
+            // global exclusive scan of the left flags: CTA counts, then CTA prefixes
+            int64_t r0, r1, tot;
+            mega_range(L, &r0, &r1);
+            int64_t cnt = 0;
+            for (int64_t q = r0 + threadIdx.x; q < r1; q += blockDim.x) cnt += mega_flag(a, cur, a.segmap[b], b, q);
+            block_excl_scan(cnt, &tot);
+            if (threadIdx.x == 0) a.sums[blockIdx.x] = tot;
+            sync();
+            int64_t carry = 0;
+            for (int i0 = 0; i0 < int(blockIdx.x); i0 += blockDim.x) {
+                const int i = i0 + threadIdx.x;
+                block_excl_scan(i < int(blockIdx.x) ? a.sums[i] : 0, &tot);
+                carry += tot;
+            }
+            for (int64_t q0 = r0; q0 < r1; q0 += blockDim.x) {
+                const int64_t q = q0 + threadIdx.x;
+                const int64_t ex = block_excl_scan(q < r1 ? mega_flag(a, cur, a.segmap[b], b, q) : 0, &tot);
+                if (q < r1) a.pfx[q] = carry + ex;
+                carry += tot;
+            }
+            if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0) a.pfx[L] = carry;
+            sync();
+            int32_t* dst = a.work[b];
+            scatter_phase(cur, dst, a.pfx, a.segmap[b], a.segmap[b ^ 1], n, b, ctl, a.grad, a.hess, a.feats, a.gl,
+                          a.hl, a.fv);
+            sync();
+            cur = dst;
+        }
+        // totals of the last frontier, leaf values, the tree appended, predictions
+        {
+            const int b = a.max_depth & 1;
+            const int nseg = ctl->nseg[b];
+            for (int t = slot_id; chainer && t < nseg; t += nslots)
+                chain_task(n, b, kSampleList, t, a.gl, a.hl, a.pg, a.ph, ctl, ig, ih, bar0, warp, lane);
+        }
+        sync();
+        if (blockIdx.x == 0)
+            finalize_phase(a.lambda, ctl, a.o_feature, a.o_thr, a.o_left, a.o_right, a.o_value, a.o_off);
+        sync();
+        update_phase(a.feats, n, a.lr, ctl, a.pred);
+        sync();
+        if (a.o_loss && blockIdx.x == 0) loss_phase(a.pred, a.target, n, ctl, a.o_loss, a.gains);
+    }
+}
 
 int64_t pow2_at_least(int64_t v) {
     int64_t p = 1;
@@ -645,6 +836,50 @@ int64_t pow2_at_least(int64_t v) {
 }
 
 size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ETUNE_TRAIN_TRACE=1 (diagnostic): the megakernel records a timestamp after every grid
+// barrier into a managed buffer, printed to stderr by the next launch_train
+unsigned long long* train_trace_buffer() {
+    static unsigned long long* buf = nullptr;
+    static bool init = false;
+    if (!init) {
+        init = true;
+        const char* ev = std::getenv("ETUNE_TRAIN_TRACE");
+        if (ev && std::atoi(ev) > 0 && cudaMallocManaged(&buf, 256 * sizeof(unsigned long long)) != cudaSuccess)
+            buf = nullptr;
+    } else if (buf) {
+        cudaDeviceSynchronize();
+        for (int i = 1; i < 256 && buf[i] > buf[i - 1]; ++i)
+            std::fprintf(stderr, "mega %3d %8.2f us\n", i, double(buf[i] - buf[i - 1]) * 1e-3);
+    }
+    if (buf) std::memset(buf, 0, 256 * sizeof(unsigned long long));
+    return buf;
+}
+
+// CTAs per SM for the megakernel on the current device (0: use the tree graph)
+int train_mega_ctas_per_sm() {
+    static int cached[64];
+    static bool init[64];
+    int device = -1;
+    cudaGetDevice(&device);
+    if (device < 0 || device >= 64) return 0;
+    if (init[device]) return cached[device];
+    int want = 0;
+    if (const char* ev = std::getenv("ETUNE_TRAIN_MEGA")) want = std::atoi(ev);
+    int coop = 0, occ = 0;
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    if (want > 0 && coop &&
+        cudaFuncSetAttribute(train_mega_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMegaSmem)) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, train_mega_kernel, kMegaT, kMegaSmem) == cudaSuccess)
+        want = std::min(want, occ);
+    else
+        want = 0;
+    cudaGetLastError();
+    cached[device] = want;
+    init[device] = true;
+    return want;
+}
 
 }  // namespace
 
@@ -657,8 +892,8 @@ size_t train_scratch_bytes(int64_t n) {
            + 4 * al256(8 * F)                                     // fv, pg, ph, gains
            + 3 * al256(4 * L)                                     // base lists + 2 work buffers
            + al256(8 * (L + 1))                                   // partition prefix
-           + al256(4 * size_t(n)) + al256(size_t(n))              // segmap, left flags
-           + al256(8 * ((L + 1023) / 1024 + 2))                   // scan tile sums
+           + 2 * al256(4 * size_t(n))                             // segment maps
+           + al256(8 * ((L + 1023) / 1024 + 4096))                // scan tile / CTA sums
            + al256(size_t(kF) * n2 * 12);                         // sort keys + indices
 }
 
@@ -700,8 +935,8 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
     int32_t* work[2] = {reinterpret_cast<int32_t*>(take(4 * L)), reinterpret_cast<int32_t*>(take(4 * L))};
     int64_t* pfx = reinterpret_cast<int64_t*>(take(8 * (L + 1)));
     int32_t* segmap = reinterpret_cast<int32_t*>(take(4 * size_t(n)));
-    uint8_t* lf = reinterpret_cast<uint8_t*>(take(size_t(n)));
-    int64_t* sums = reinterpret_cast<int64_t*>(take(8 * ((L + 1023) / 1024 + 2)));
+    int32_t* segmap2 = reinterpret_cast<int32_t*>(take(4 * size_t(n)));
+    int64_t* sums = reinterpret_cast<int64_t*>(take(8 * ((L + 1023) / 1024 + 4096)));
     uint64_t* kbuf = reinterpret_cast<uint64_t*>(take(size_t(kF) * n2 * 12));
     uint32_t* ibuf = reinterpret_cast<uint32_t*>(kbuf + size_t(kF) * n2);
 
@@ -719,6 +954,53 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
         cudaMemsetAsync(o_off, 0, sizeof(int64_t), c.stream);
         cudaMemcpyAsync(o_scalars, &ctl->base, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
         return cudaGetLastError();
+    }
+
+    // ETUNE_TRAIN_MEGA=1: the whole training as one cooperative launch (default: the
+    // per-kernel tree graph below)
+    if (const int per_sm = train_mega_ctas_per_sm(); per_sm > 0) {
+        MegaArgs a{};
+        a.n = n;
+        a.num_trees = num_trees;
+        a.max_depth = max_depth;
+        a.lr = lr;
+        a.mlw = mlw;
+        a.lambda = lambda;
+        a.feats = d_feat;
+        a.target = target;
+        a.pred = pred;
+        a.grad = grad;
+        a.hess = hess;
+        a.gl = gl;
+        a.hl = hl;
+        a.fv = fv;
+        a.pg = pg;
+        a.ph = ph;
+        a.gains = gains;
+        a.base_lists = base_lists;
+        a.work[0] = work[0];
+        a.work[1] = work[1];
+        a.segmap[0] = segmap;
+        a.segmap[1] = segmap2;
+        a.pfx = pfx;
+        a.sums = sums;
+        a.ctl = ctl;
+        a.o_feature = o_feature;
+        a.o_left = o_left;
+        a.o_right = o_right;
+        a.o_thr = o_thr;
+        a.o_value = o_value;
+        a.o_loss = o_loss;
+        a.o_off = o_off;
+        a.trace = train_trace_buffer();
+        void* args[] = {&a};
+        cudaError_t em = cudaLaunchCooperativeKernel(reinterpret_cast<void*>(train_mega_kernel),
+                                                     dim3(unsigned(c.sm_count * per_sm)), dim3(kMegaT), args,
+                                                     kMegaSmem, c.stream);
+        note_launches(1);
+        if (em == cudaSuccess)
+            em = cudaMemcpyAsync(o_scalars, &ctl->base, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
+        return em;
     }
 
     // one tree as a fixed launch sequence, captured once and replayed num_trees times
@@ -739,33 +1021,34 @@ cudaError_t launch_train(const LaunchCtx& c, const double* d_feat, const double*
     const int32_t* cur = base_lists;
     int wb = 0;
     int lvl = 0;
+    // level 0 rows and segment map; every later level's come from the previous scatter
+    PDL(gather_kernel, grid(int64_t(L)), 256, 0, cap, cur, n, kLists, grad, hess, d_feat, gl, hl, fv, 0, ctl, segmap);
+    launches += 1;
+    int32_t* segmaps[2] = {segmap, segmap2};
     for (int depth = 0; depth < max_depth; ++depth, ++lvl) {
+        const int b = lvl & 1;
         const int segs = 1 << depth;  // frontier bound at this depth
-        PDL(gather_kernel, grid(int64_t(L)), 256, 0, cap, cur, n, kLists, grad, hess, d_feat, gl, hl, fv, lvl, ctl,
-            segmap);
         const int warps = kLists * segs;
         PDL(chain_kernel, warps, 64, 0, cap, n, lvl, 0, gl, hl, pg, ph, ctl);
-        PDL(gain_kernel, grid(int64_t(F)), 256, 0, cap, n, lvl, segmap, fv, pg, ph, mlw, lambda, gains, ctl);
-        PDL(gainpos_kernel, grid(int64_t(F)), 256, 0, cap, n, segmap, gains, ctl);
+        PDL(gain_kernel, grid(int64_t(F)), 256, 0, cap, n, lvl, segmaps[b], fv, pg, ph, mlw, lambda, gains, ctl);
+        PDL(gainpos_kernel, grid(int64_t(F)), 256, 0, cap, n, segmaps[b], gains, ctl);
         PDL(decide_kernel, 1, 1024, 0, cap, n, lvl, fv, ctl);
-        PDL(leftflag_kernel, grid(n), 256, 0, cap, d_feat, cur, n, lvl, segmap, ctl, lf);
         if (e == cudaSuccess)
-            e = scan_apply(cap, int64_t(L), LeftFlagFn{cur, segmap, ctl->split, lf, n}, PrefixWrite{pfx}, sums,
+            e = scan_apply(cap, int64_t(L), LeftFlagFn{cur, segmaps[b], ctl, d_feat, n}, PrefixWrite{pfx}, sums,
                            pfx + L);
         if (e != cudaSuccess) break;
-        PDL(scatter_kernel, grid(int64_t(L)), 256, 0, cap, cur, work[wb], pfx, segmap, n, lvl, ctl);
+        PDL(scatter_kernel, grid(int64_t(L)), 256, 0, cap, cur, work[wb], pfx, segmaps[b], segmaps[b ^ 1], n, lvl,
+            ctl, grad, hess, d_feat, gl, hl, fv);
         cur = work[wb];
         wb ^= 1;
-        launches += 10;
+        launches += 8;
     }
     // totals of the last frontier (children created at the deepest level)
-    PDL(gather_kernel, grid(n), 256, 0, cap, cur, n, 1, grad, hess, d_feat, gl, hl, fv, lvl, ctl,
-        static_cast<int32_t*>(nullptr));
     const int segs = 1 << max_depth;
     PDL(chain_kernel, segs, 64, 0, cap, n, lvl, 1, gl, hl, pg, ph, ctl);
     PDL(finalize_kernel, 1, 1024, 0, cap, lambda, ctl, o_feature, o_thr, o_left, o_right, o_value, o_off);
     PDL(update_kernel, grid(n), 256, 0, cap, d_feat, n, lr, ctl, pred);
-    launches += 4;
+    launches += 3;
     if (o_loss) {
         PDL(loss_kernel, 1, 1024, 0, cap, pred, target, n, ctl, o_loss, gains);
         launches += 1;

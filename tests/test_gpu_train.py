@@ -121,3 +121,20 @@ def test_train_errors(ctx, capi):
     with pytest.raises(capi.EtuneError) as ex:
         capi.train(ctx, f, torch.ones(10, dtype=torch.float64, device="cuda"), max_depth=11)
     assert ex.value.code == 67
+
+
+def test_train_megakernel_variant():
+    """The opt-in cooperative megakernel (ETUNE_TRAIN_MEGA=1, train.cu) passes the same
+    parity tests; the switch is read once per process, hence the subprocess."""
+    import os
+    import subprocess
+    import sys
+
+    if os.environ.get("ETUNE_TRAIN_MEGA"):
+        pytest.skip("already running under the variant")
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, ETUNE_TRAIN_MEGA="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_train.py"), "-k", "not megakernel"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
