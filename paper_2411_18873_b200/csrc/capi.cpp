@@ -229,12 +229,30 @@ void selection_buckets(const ForestHost& F, uint64_t* kmin, uint32_t* shift) {
     *shift = s;
 }
 
-etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledScore** out) {
+constexpr int64_t kLazyWalkMaxN = int64_t(1) << 15;
+constexpr int64_t kLazyWalkBudget = int64_t(1) << 18;
+
+// `n` = the population about to be scored (-1: compile regardless)
+etune_status get_compiled(etune_cu_forest* f, const etune_cu_plan* p, CompiledScore** out, int64_t n = -1) {
     std::lock_guard<std::mutex> lock(f->mu);
     auto it = f->compiled.find(p->serial);
     if (it != f->compiled.end()) {
         *out = &it->second;
         return ETUNE_OK;
+    }
+    if (f->lazy_compile && n >= 0 && n <= kLazyWalkMaxN) {
+        int64_t& w = f->walked[p->serial];
+        const int cap = max_dynamic_smem(f->ctx->device) - score_static_smem();
+        if (w + n <= kLazyWalkBudget && p->build.hdr.total <= uint32_t(cap)) {
+            static CompiledScore walk_only = [] {
+                CompiledScore w0;
+                w0.walk = true;
+                return w0;
+            }();
+            w += n;
+            *out = &walk_only;
+            return ETUNE_OK;
+        }
     }
     std::vector<uint8_t> blob;
     std::string err;
@@ -1013,7 +1031,7 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     CHECK_PLAN_ARGS(d_genome && d_pred);
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
     CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
     if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
     return score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, SelHist{}, nullptr);
 }
@@ -1027,7 +1045,7 @@ etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etun
     if (k > 0 && !d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null index buffer");
     if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
     CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
     if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
     return score_select_local(c, p, f, cs, d_genome, n, k, d_pred, d_ids, d_idx);
 }
@@ -1042,7 +1060,7 @@ etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan*
     if (!d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
     if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "shard >= 2^31");
     CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
     if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
     ShardBufs sb;
     if (etune_status st = shard_buffers(c, k, &sb)) return st;
@@ -1090,7 +1108,7 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
     if (first_bad) *first_bad = -1;
     if (n == 0) return ETUNE_OK;
     CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
     if (etune_status st = ensure_keyed(f, p, cs, std::min<int64_t>(n, int64_t(1) << 17))) return st;
     // Chunked pipeline over two staging buffers.  The host pool narrows chunk i's rows
     // into pinned staging (24 B/row when every field fits 16 bits) while the GPU works

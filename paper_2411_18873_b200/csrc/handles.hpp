@@ -94,5 +94,10 @@ struct etune_cu_forest {
     std::mutex mu;
     std::map<uint64_t, CompiledScore> compiled;  // by plan serial
     int keyed_mode = 1;  // 1: keyed path (full form when it fits), 2: keyed byte form only, 0: class tables only
+    // Lazy compile (set on the search loop's per-round models, each scored once): small
+    // populations take the tree-walk kernel until kLazyWalkBudget candidates per plan
+    // have been walked, instead of paying the ms-scale host compile per model.
+    bool lazy_compile = false;
+    std::map<uint64_t, int64_t> walked;  // by plan serial
 };
 

@@ -13,6 +13,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -115,6 +117,7 @@ etune_status retrain(etune_cu_search* s) {
     etune_cu_forest* f = nullptr;
     SOK(etune_cu_forest_from_device(c, s->m_feature, s->m_thr, s->m_left, s->m_right, s->m_value, s->m_off,
                                     s->cfg.boost.num_trees, s->m_sc, s->cfg.boost.learning_rate, &f));
+    f->lazy_compile = true;  // scored once per round (M candidates): walk instead of compiling
     if (s->model) etune_cu_forest_destroy(s->model);
     s->model = f;
     return ETUNE_OK;
@@ -340,21 +343,36 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     const double t0 = now_ms();
     const int64_t G = s->cfg.generation_size, M = s->cfg.M;
     const int64_t r = s->round + 1;
+    // ETUNE_SEARCH_TRACE=1 (diagnostic): synchronise after every stage and print its time
+    static const bool trace = std::getenv("ETUNE_SEARCH_TRACE") != nullptr;
+    double tl = t0;
+    auto stage = [&](const char* name) {
+        if (!trace) return;
+        cudaStreamSynchronize(c->stream);
+        const double t = now_ms();
+        std::fprintf(stderr, "round %lld %-10s %9.3f ms (samples %lld)\n", static_cast<long long>(r), name, t - tl,
+                     static_cast<long long>(s->nsamples));
+        tl = t;
+    };
     // 1. GeneticReproduction(Kernel_parents)
     SOK(etune_cu_reproduce(c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
                            nullptr, nullptr));
+    stage("reproduce");
     // 2. LatencyEvaAndPick(Kernel_generation, M)
     SOK(measure_latency(s, s->pop, G, s->lat));
     SOK(etune_cu_topk(c, s->lat, G, M, s->idx));
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
+    stage("latency");
     // 3. EnergyModelEvaAndPick(Kernel_M, EnergyModel, k*M)
     SOK(etune_cu_score(c, s->plan, s->model, s->mgen, M, s->mpred, nullptr));
     const int64_t km = ceil_fifths(s->k5, M);
     SOK(etune_cu_topk(c, s->mpred, M, km, s->sel));
     SCU(launch_gather_u64(c->lc(), s->mgen, s->sel, km, s->selgen));
     SCU(launch_gather_u64(c->lc(), s->mpred, s->sel, km, s->psel));
+    stage("score");
     // 4. NVMLMeasurement(Kernel_kM)
     SOK(measure_energy(s, s->selgen, km));
+    stage("energy");
     // 6. SNR of step-3 predictions vs the measurements in the model's normalised units
     SCU(launch_div_scalar(c->lc(), s->men, km, s->m_sc + 1, s->mnorm));
     double snr = 0.0;
@@ -364,9 +382,12 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     SOK(etune_cu_topk(c, s->mpred, M, np, s->idx));
     SCU(launch_gather_u64(c->lc(), s->mgen, s->idx, np, s->par));
     s->np = np;
+    stage("snr+parents");
     // 5. ModelUpdate on all accumulated samples
     SOK(append_samples(s, s->selgen, s->men, km));
+    stage("append");
     SOK(retrain(s));
+    stage("retrain");
     // 7. k controller, k in integer fifths
     const int kb = s->k5;
     const bool poor = s->cfg.inverted_semantics ? !(snr < s->cfg.mu_db) : (snr < s->cfg.mu_db);
