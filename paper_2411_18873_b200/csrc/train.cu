@@ -427,7 +427,9 @@ __global__ void __launch_bounds__(64) chain_kernel(int64_t n, int lvl, int only_
 
 // split gain at every (feature list, position) (cpp 97-118); per-(node, feature) max
 // gain by atomicMax on the (positive) gain's bits
-__device__ __forceinline__ void gain_phase(int64_t n, int lvl, const int32_t* segmap, const double* fv, const double* pg, const double* ph, double mlw, double lambda, double* gains, TrainCtl* ctl) {
+__device__ __forceinline__ void gain_phase(int64_t n, int lvl, const int32_t* segmap, const double* fv,
+                                           const double* pg, const double* ph, double mlw, double lambda,
+                                           double* gains, TrainCtl* ctl) {
     const int b = lvl & 1;
     const int64_t tot = int64_t(kF) * n;
     for (int64_t q = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; q < tot; q += int64_t(gridDim.x) * blockDim.x) {
@@ -630,7 +632,9 @@ __global__ void scatter_kernel(const int32_t* __restrict__ src, int32_t* __restr
 }
 
 // Leaf Newton weights (cpp 161-166) and the tree appended to the output forest.
-__device__ __forceinline__ void finalize_phase(double lambda, TrainCtl* ctl, int32_t* o_feature, double* o_thr, int32_t* o_left, int32_t* o_right, double* o_value, int64_t* o_off) {
+__device__ __forceinline__ void finalize_phase(double lambda, TrainCtl* ctl, int32_t* o_feature, double* o_thr,
+                                               int32_t* o_left, int32_t* o_right, double* o_value,
+                                               int64_t* o_off) {
     const int nn = ctl->nnodes;
     const int64_t base = ctl->out_nodes;
     const int tree = ctl->tree;
@@ -659,7 +663,8 @@ __global__ void __launch_bounds__(1024) finalize_kernel(double lambda, TrainCtl*
 }
 
 // pred[i] += lr * tree.eval(feat[i])  (cpp 236-238)
-__device__ __forceinline__ void update_phase(const double* feats, int64_t n, double lr, const TrainCtl* ctl, double* pred) {
+__device__ __forceinline__ void update_phase(const double* feats, int64_t n, double lr, const TrainCtl* ctl,
+                                             double* pred) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         int node = 0;
         int f = ctl->feature[0];
@@ -676,7 +681,8 @@ __global__ void update_kernel(const double* __restrict__ feats, int64_t n, doubl
     update_phase(feats, n, lr, ctl, pred);
 }
 
-__device__ __forceinline__ void loss_phase(const double* pred, const double* target, int64_t n, const TrainCtl* ctl, double* loss, double* tmp) {
+__device__ __forceinline__ void loss_phase(const double* pred, const double* target, int64_t n, const TrainCtl* ctl,
+                                           double* loss, double* tmp) {
     __shared__ double stage[1024 + 8];
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const double d = __dsub_rn(pred[i], target[i]);
