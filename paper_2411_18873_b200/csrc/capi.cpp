@@ -88,16 +88,18 @@ etune_status cuda_fail(cudaError_t e, const char* where) {
         if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
     } while (0)
 
+// Grows by at least 1.5x, so a caller whose size creeps up (the search loop retraining on
+// a growing sample set) reallocates O(log) times; stream-ordered, no device-wide sync.
 etune_status ensure_scratch(etune_cu_ctx* c, size_t bytes) {
     if (c->scratch_bytes >= bytes) return ETUNE_OK;
+    const size_t want = std::max(bytes, c->scratch_bytes + c->scratch_bytes / 2);
     if (c->scratch) {
-        CU(cudaStreamSynchronize(c->stream));
-        CU(cudaFree(c->scratch));
+        CU(cudaFreeAsync(c->scratch, c->stream));
         c->scratch = nullptr;
         c->scratch_bytes = 0;
     }
-    CU(cudaMalloc(&c->scratch, bytes));
-    c->scratch_bytes = bytes;
+    CU(cudaMallocAsync(&c->scratch, want, c->stream));
+    c->scratch_bytes = want;
     return ETUNE_OK;
 }
 
@@ -511,6 +513,14 @@ etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out) {
     c->stream = static_cast<cudaStream_t>(stream);  // NULL = the default stream
     CU(cudaMalloc(&c->d_err, sizeof(unsigned long long)));
     CU(cudaMemsetAsync(c->d_err, 0xff, sizeof(unsigned long long), c->stream));
+    // scratch and forest tables are stream-ordered allocations: keep freed blocks in the
+    // device pool instead of returning them to the driver at every synchronisation
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = ~uint64_t(0);
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
     *out = c.release();
     return ETUNE_OK;
 }
@@ -995,7 +1005,7 @@ etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, con
     std::string err;
     if (etune_status st = build_predict_blob(f->host, &blob, &err)) return fail(st, err);
     CU(cudaSetDevice(c->device));
-    CU(cudaMalloc(&f->d_predict, blob.size()));
+    CU(cudaMallocAsync(&f->d_predict, blob.size(), c->stream));
     CU(cudaMemcpyAsync(f->d_predict, blob.data(), blob.size(), cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     f->predict_bytes = uint32_t(blob.size());
@@ -1006,7 +1016,7 @@ etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, con
 
 etune_status etune_cu_forest_destroy(etune_cu_forest* f) {
     if (!f) return ETUNE_OK;
-    cudaFree(f->d_predict);
+    cudaFreeAsync(f->d_predict, f->ctx->stream);  // stream-ordered: after the forest's last use on the ctx stream
     for (auto& kv : f->compiled) {
         cudaFree(kv.second.d_blob);
         cudaFree(kv.second.d_kblob);

@@ -51,6 +51,11 @@ struct etune_cu_search {
     int64_t* m_off = nullptr;
     etune_cu_forest* model = nullptr;
     std::vector<void*> allocs;
+    // the next round's reproduce, launched on a side stream as soon as its parents exist
+    // so that it runs beside this round's retrain (one CTA: the rest of the GPU trains)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_par = nullptr, ev_pop = nullptr;
+    int64_t pop_round = -1;  // round whose generation is in flight / in `pop`
 };
 
 namespace {
@@ -80,6 +85,30 @@ etune_status dalloc(etune_cu_search* s, T** p, int64_t n) {
     return ETUNE_OK;
 }
 
+// reproduce(parents, G, seed + r) for round r on the side stream, ordered after the
+// parents on the ctx stream; round r waits for ev_pop before it reads `pop`
+etune_status prelaunch_reproduce(etune_cu_search* s, int64_t r) {
+    etune_cu_ctx* c = s->ctx;
+    if (!s->side) {
+        int least = 0, greatest = 0;  // the single breed CTA is dispatched ahead of the training grids
+        SCU(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        SCU(cudaStreamCreateWithPriority(&s->side, cudaStreamNonBlocking, greatest));
+        SCU(cudaEventCreateWithFlags(&s->ev_par, cudaEventDisableTiming));
+        SCU(cudaEventCreateWithFlags(&s->ev_pop, cudaEventDisableTiming));
+    }
+    SCU(cudaEventRecord(s->ev_par, c->stream));
+    SCU(cudaStreamWaitEvent(s->side, s->ev_par, 0));
+    const cudaStream_t main_stream = c->stream;
+    c->stream = s->side;  // the ctx's launches go to the side stream for this call only
+    const etune_status st = etune_cu_reproduce(c, s->plan, s->par, s->np, s->cfg.generation_size, &s->cfg.rates,
+                                               s->cfg.rng_seed + uint64_t(r), s->pop, nullptr, nullptr);
+    c->stream = main_stream;
+    SOK(st);
+    SCU(cudaEventRecord(s->ev_pop, s->side));
+    s->pop_round = r;
+    return ETUNE_OK;
+}
+
 int64_t ceil_fifths(int k5, int64_t M) {  // ceil(k * M) with k = k5 / 5, minimum 1
     const int64_t v = (int64_t(k5) * M + 4) / 5;
     return v < 1 ? 1 : v;
@@ -91,15 +120,16 @@ etune_status append_samples(etune_cu_search* s, const uint64_t* gen, const doubl
     if (s->nsamples + n > s->cap) {
         int64_t nc = std::max<int64_t>(s->cap * 2, s->nsamples + n);
         double *f2 = nullptr, *e2 = nullptr;
-        SCU(cudaMalloc(&f2, size_t(nc) * 16 * 8));
-        SCU(cudaMalloc(&e2, size_t(nc) * 8));
+        // stream-ordered: no device-wide synchronisation (the next round's reproduce may
+        // be running on the side stream)
+        SCU(cudaMallocAsync(&f2, size_t(nc) * 16 * 8, c->stream));
+        SCU(cudaMallocAsync(&e2, size_t(nc) * 8, c->stream));
         if (s->nsamples) {
             SCU(cudaMemcpyAsync(f2, s->feat, size_t(s->nsamples) * 16 * 8, cudaMemcpyDeviceToDevice, c->stream));
             SCU(cudaMemcpyAsync(e2, s->energy, size_t(s->nsamples) * 8, cudaMemcpyDeviceToDevice, c->stream));
         }
-        SCU(cudaStreamSynchronize(c->stream));
-        cudaFree(s->feat);
-        cudaFree(s->energy);
+        if (s->feat) SCU(cudaFreeAsync(s->feat, c->stream));
+        if (s->energy) SCU(cudaFreeAsync(s->energy, c->stream));
         s->feat = f2;
         s->energy = e2;
         s->cap = nc;
@@ -110,10 +140,21 @@ etune_status append_samples(etune_cu_search* s, const uint64_t* gen, const doubl
     return ETUNE_OK;
 }
 
+double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 etune_status retrain(etune_cu_search* s) {
     etune_cu_ctx* c = s->ctx;
+    static const bool trace = std::getenv("ETUNE_SEARCH_TRACE") != nullptr;
+    const double t0 = trace ? now_ms() : 0.0;
     SOK(etune_cu_train(c, s->feat, s->energy, s->nsamples, &s->cfg.boost, s->m_feature, s->m_thr, s->m_left,
                        s->m_right, s->m_value, s->m_off, s->m_sc, nullptr));
+    if (trace) {
+        const double t1 = now_ms();
+        cudaStreamSynchronize(c->stream);
+        std::fprintf(stderr, "  train: issue %.3f ms, device %.3f ms\n", t1 - t0, now_ms() - t1);
+    }
     etune_cu_forest* f = nullptr;
     SOK(etune_cu_forest_from_device(c, s->m_feature, s->m_thr, s->m_left, s->m_right, s->m_value, s->m_off,
                                     s->cfg.boost.num_trees, s->m_sc, s->cfg.boost.learning_rate, &f));
@@ -222,9 +263,6 @@ etune_status measure_energy(etune_cu_search* s, const uint64_t* gen, int64_t n) 
     return etune_cu_synchronize(s->ctx, nullptr);
 }
 
-double now_ms() {
-    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-}
 
 }  // namespace
 
@@ -302,6 +340,12 @@ etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, con
 etune_status etune_cu_search_destroy(etune_cu_search* s) {
     if (!s) return ETUNE_OK;
     cudaStreamSynchronize(s->ctx->stream);
+    if (s->side) {
+        cudaStreamSynchronize(s->side);
+        cudaStreamDestroy(s->side);
+        cudaEventDestroy(s->ev_par);
+        cudaEventDestroy(s->ev_pop);
+    }
     if (s->model) etune_cu_forest_destroy(s->model);
     for (void* p : s->allocs) cudaFree(p);
     cudaFree(s->feat);
@@ -323,10 +367,11 @@ etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* rep
     SOK(etune_cu_topk(c, s->lat, G, M, s->idx));  // LatencyEvaAndPick(Kernel_generation, M)
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
     SOK(measure_energy(s, s->mgen, M));
-    SOK(append_samples(s, s->mgen, s->men, M));
-    SOK(retrain(s));
     SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(M) * 8, cudaMemcpyDeviceToDevice, c->stream));
     s->np = M;
+    if (s->cfg.max_rounds >= 1) SOK(prelaunch_reproduce(s, 1));
+    SOK(append_samples(s, s->mgen, s->men, M));
+    SOK(retrain(s));
     s->round = 0;
     s->cumulative = M;
     bool improved = false;
@@ -354,9 +399,14 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
                      static_cast<long long>(s->nsamples));
         tl = t;
     };
-    // 1. GeneticReproduction(Kernel_parents)
-    SOK(etune_cu_reproduce(c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
-                           nullptr, nullptr));
+    // 1. GeneticReproduction(Kernel_parents): usually already running beside the previous
+    // retrain (prelaunch_reproduce)
+    if (s->pop_round == r) {
+        SCU(cudaStreamWaitEvent(c->stream, s->ev_pop, 0));
+    } else {
+        SOK(etune_cu_reproduce(c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
+                               nullptr, nullptr));
+    }
     stage("reproduce");
     // 2. LatencyEvaAndPick(Kernel_generation, M)
     SOK(measure_latency(s, s->pop, G, s->lat));
@@ -382,6 +432,7 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     SOK(etune_cu_topk(c, s->mpred, M, np, s->idx));
     SCU(launch_gather_u64(c->lc(), s->mgen, s->idx, np, s->par));
     s->np = np;
+    if (r + 1 <= s->cfg.max_rounds) SOK(prelaunch_reproduce(s, r + 1));
     stage("snr+parents");
     // 5. ModelUpdate on all accumulated samples
     SOK(append_samples(s, s->selgen, s->men, km));

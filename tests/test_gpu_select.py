@@ -113,6 +113,32 @@ def test_score_select_large_k_falls_back(oracle, ctx, capi, setup):
     assert (got == want).all()
 
 
+def test_score_select_empty_and_k0(oracle, ctx, capi, setup):
+    """Edge sizes of the fused call: an empty population (k = 0), k = 0 on a non-empty one
+    (predictions still written, no selection), and the k > n / negative-k errors."""
+    op, plan, forest, flat, parents = setup
+    g0 = plan.encode(dev(parents[:0]))
+    forest.score_select(plan, g0, 0, torch.empty(0, dtype=torch.float64, device="cuda"),
+                        torch.empty(1, dtype=torch.int64, device="cuda"))
+    sched = parents[:777]
+    p_ref, _ = expect(oracle, op, flat, sched, 1)
+    pred, got = run_select(capi, ctx, plan, forest, sched, 0)
+    assert len(got) == 0
+    assert (pred.view(np.uint64) == p_ref.view(np.uint64)).all()
+    g = plan.encode(dev(sched))
+    pr = torch.empty(len(sched), dtype=torch.float64, device="cuda")
+    ix = torch.empty(1024, dtype=torch.int64, device="cuda")
+    for bad_k in (len(sched) + 1, -1):
+        with pytest.raises(capi.EtuneError):
+            forest.score_select(plan, g, bad_k, pr, ix)
+    # the host-buffer entry point on an empty and a one-row population
+    forest.score_host(plan, np.ascontiguousarray(sched[:0]), np.zeros(0), np.zeros(0, np.uint64))
+    p1, h1 = np.zeros(1), np.zeros(1, np.uint64)
+    forest.score_host(plan, np.ascontiguousarray(sched[:1]), p1, h1)
+    assert p1.view(np.uint64)[0] == p_ref.view(np.uint64)[0]
+    assert h1[0] == np.uint64(oracle.ids(op, sched[:1])[0])
+
+
 def test_score_select_sharded_single_rank(oracle, ctx, capi, setup):
     """Shards scored + selected locally, merged (single-rank communicator semantics):
     per-shard results equal the oracle's shard top-k with global indices."""
