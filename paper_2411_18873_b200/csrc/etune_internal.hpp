@@ -184,7 +184,8 @@ struct ScoreHdr {
 // A candidate reads its row with 16-byte loads (16 trees each), so the per-tree work is
 // one or three shared loads (+ the two leaf words) instead of one table load per channel.
 // Full form (when the table stays <= 64 MB): one row per (key, Kuv class) holding every
-// tree's exit slot as 5 bits, six per 32-bit word, so a tree costs only its leaf words.
+// tree's exit slot as 5 bits, 25 per 16-byte quad (100 trees: 64-byte rows), so a tree costs
+// only its leaf words.
 // Blob (shared memory): header, tilings, divisors of K, Kuv class table, Kuv flags,
 // packed mask lists, Kuv masks [tree][nkc], leaf blocks (32 hi + 32 lo words/tree).
 struct KeyedHdr {
@@ -208,7 +209,7 @@ struct KeyedParams {       // kernel parameter (constant bank: warp-uniform read
     uint32_t koff[kKeyedMaxTrees];  // byte offset of tree t's Kuv-mask row ([tree][nkc]) from the blob start
     uint32_t kuv_flags[4];          // copy of KeyedHdr::kuv_flags (all zero in the full form)
     uint32_t off_kuvtab, off_leaves, nkc, ntrees;
-    uint32_t kfull;                 // 1: rows per (key, Kuv class) of 5-bit exit slots (6 per word)
+    uint32_t kfull;                 // 1: rows per (key, Kuv class) of 5-bit exit slots (25 per quad)
 };
 
 // ------------------------------------------------------- generic predict blob

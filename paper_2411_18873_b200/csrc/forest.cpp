@@ -588,8 +588,9 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                 keyed->params.ntrees = uint32_t(T);
                 keyed->params.kfull = 0;
                 // full form: every (key, Kuv class) row holds exit slots only
-                // 5-bit slots, six per 32-bit word (24 trees per 16-byte quad)
-                const int frow = int((T + 23) / 24 * 16);
+                // 5-bit slots, 25 trees per 16-byte quad (slot j of a quad at bits [5j, 5j + 5)),
+                // rows padded to whole 32-byte sectors (read with 256-bit loads)
+                const int frow = int((T + 49) / 50 * 32);
                 const size_t full_bytes = size_t(nk) * size_t(nkc) * size_t(frow);
                 if (nkc > 0 && full_bytes <= max_full_bytes) {
                     std::vector<uint8_t> ft(full_bytes, 0);
@@ -605,7 +606,10 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                                                        kuvtab[size_t(t) * size_t(nkc) + size_t(x)];
                                     slot = ((m & (0u - m)) * 0x077CB531u) >> 27;
                                 }
-                                fr[t / 6] |= slot << (5 * (t % 6));
+                                const uint32_t q = uint32_t(t) / 25u, b = 5u * (uint32_t(t) % 25u), sh = b & 31u;
+                                uint32_t* quad = fr + 4 * q;
+                                quad[b >> 5] |= slot << sh;
+                                if (sh > 27u) quad[(b >> 5) + 1] |= slot >> (32u - sh);
                             }
                         }
                     }

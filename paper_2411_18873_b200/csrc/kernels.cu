@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* 
 // order with genome[] already in that order; results land at the original index.
 constexpr int kKeyedThreads = 512;
 
-__global__ void __launch_bounds__(kKeyedThreads) score_keyed_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
+__global__ void __launch_bounds__(kKeyedThreads, 3) score_keyed_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
                                                                     const uint8_t* __restrict__ table,
                                                                     const uint64_t* __restrict__ genome,
                                                                     const uint32_t* __restrict__ order, int64_t n,

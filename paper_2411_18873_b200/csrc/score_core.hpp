@@ -222,6 +222,18 @@ ETUNE_UNROLL
 __device__ __forceinline__ uint4 ld_row16(const uint8_t* row, int q) {
     return __ldg(reinterpret_cast<const uint4*>(row) + q);
 }
+// 32 bytes (one sector) per thread in one 256-bit load (sm_100: LDG.256)
+struct RowOct {
+    uint32_t w[8];
+};
+__device__ __forceinline__ RowOct ld_row32(const uint8_t* row, int o) {
+    RowOct r;
+    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
+          "=r"(r.w[7])
+        : "l"(row + 32 * o));
+    return r;
+}
 #else
 struct RowQuad {
     uint32_t x, y, z, w;
@@ -229,6 +241,14 @@ struct RowQuad {
 inline RowQuad ld_row16(const uint8_t* row, int q) {
     RowQuad r;
     std::memcpy(&r, row + 16 * q, 16);
+    return r;
+}
+struct RowOct {
+    uint32_t w[8];
+};
+inline RowOct ld_row32(const uint8_t* row, int o) {
+    RowOct r;
+    std::memcpy(&r, row + 32 * o, 32);
     return r;
 }
 #endif
@@ -269,15 +289,27 @@ ETUNE_UNROLL
     return sum;
 }
 
-// Full form: 24 trees per 16-byte quad (six 5-bit slots per word); FULL: no bound checks
+// Full form: 25 trees per 16-byte quad, slot j of a quad at bits [5j, 5j + 5) of its
+// 128 bits (little-endian words; slots 6, 12 and 19 straddle two words); rows are padded to
+// whole 32-byte sectors and read one sector per load, so 100 trees are two 256-bit loads.
+// FULL: no bound checks in the quad.
+__host__ __device__ __forceinline__ uint32_t funnel_r(uint32_t lo, uint32_t hi, uint32_t sh) {
+#if defined(__CUDA_ARCH__)
+    return __funnelshift_r(lo, hi, sh);
+#else
+    return sh ? (lo >> sh) | (hi << (32u - sh)) : lo;
+#endif
+}
+
 template <bool FULL>
 __host__ __device__ __forceinline__ double keyed_group5(const KeyedParams& P, SAddr base, uint32_t t0,
                                                         const uint32_t* w, double sum) {
 ETUNE_UNROLL
-    for (uint32_t j = 0; j < 24; ++j) {
+    for (uint32_t j = 0; j < 25; ++j) {
         const uint32_t t = t0 + j;
         if (FULL || t < P.ntrees) {
-            const uint32_t slot = (w[j / 6] >> (5 * (j % 6))) & 31u;
+            const uint32_t b = 5u * j, i = b >> 5, sh = b & 31u;
+            const uint32_t slot = (sh <= 27u ? (w[i] >> sh) : funnel_r(w[i], w[i + 1], sh)) & 31u;
             const SAddr blk = base + P.off_leaves + t * 256u + slot * 4u;
             sum = ETUNE_DADD(sum, join_f64(lds32(blk), lds32(blk + 128u)));
         }
@@ -289,13 +321,16 @@ __host__ __device__ __forceinline__ double keyed_sum5(const uint8_t* KB, const K
     const SAddr base = blob_saddr(KB);
     double sum = 0.0;
     const uint32_t T = P.ntrees;
+    // rows are whole 32-byte sectors: two quads (50 trees) per 256-bit load
 ETUNE_UNROLL
-    for (uint32_t t0 = 0; t0 < uint32_t(kKeyedMaxTrees); t0 += 24) {
+    for (uint32_t t0 = 0; t0 < uint32_t(kKeyedMaxTrees); t0 += 50) {
         if (t0 >= T) break;
-        const auto r = ld_row16(row, int(t0 / 24));
-        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
-        if (t0 + 24 <= T) sum = keyed_group5<true>(P, base, t0, w, sum);
-        else sum = keyed_group5<false>(P, base, t0, w, sum);
+        const RowOct r = ld_row32(row, int(t0 / 50));
+        if (t0 + 25 <= T) sum = keyed_group5<true>(P, base, t0, r.w, sum);
+        else sum = keyed_group5<false>(P, base, t0, r.w, sum);
+        if (t0 + 25 >= T) break;
+        if (t0 + 50 <= T) sum = keyed_group5<true>(P, base, t0 + 25, r.w + 4, sum);
+        else sum = keyed_group5<false>(P, base, t0 + 25, r.w + 4, sum);
     }
     return sum;
 }
