@@ -311,6 +311,9 @@ etune_status ensure_keyed(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     if (kb.blob.size() > size_t(cap)) return ETUNE_OK;
     CU(cudaMalloc(&cs->d_kblob, kb.blob.size()));
     CU(cudaMalloc(&cs->d_ktable, kb.table.size()));
+    CU(cudaMalloc(&cs->d_khash, kb.khash.size() * sizeof(uint64_t)));
+    CU(cudaMemcpyAsync(cs->d_khash, kb.khash.data(), kb.khash.size() * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                       f->ctx->stream));
     CU(cudaMemcpyAsync(cs->d_kblob, kb.blob.data(), kb.blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaMemcpyAsync(cs->d_ktable, kb.table.data(), kb.table.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaStreamSynchronize(f->ctx->stream));
@@ -345,7 +348,8 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
         // candidates in population order: each reads its own 112-byte key-table row (L2);
         // grouping the population by key first was measured slower (the sort costs more
         // than the broadcast rows save)
-        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, cs->ktable_bytes, d_genome, nullptr, n,
+        CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, cs->ktable_bytes, cs->d_khash, d_genome,
+                              nullptr, n,
                               d_pred, d_ids, cs->keyed_per_sm, *cs->kparams, sel));
     } else {
         if (ev) CU(cudaEventRecord(ev[1], c->stream));
@@ -1021,6 +1025,7 @@ etune_status etune_cu_forest_destroy(etune_cu_forest* f) {
         cudaFree(kv.second.d_blob);
         cudaFree(kv.second.d_kblob);
         cudaFree(kv.second.d_ktable);
+        cudaFree(kv.second.d_khash);
     }
     etune_cu_ctx* c = f->ctx;
     delete f;

@@ -619,6 +619,24 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                     K.row_bytes = frow;
                     std::memcpy(kbl.data(), &K, sizeof(K));
                 }
+                // candidate_id's FNV-1a state per key: operator prefix, then (blocks, threads,
+                // pt) of the key's three tilings (space.cpp:12-45 word order), each word hashed as
+                // 8 little-endian bytes
+                keyed->khash.assign(size_t(nk), 0);
+                for (int64_t key = 0; key < nk; ++key) {
+                    const int64_t t2 = key % PH.nt[2], t1 = (key / PH.nt[2]) % PH.nt[1], t0 = key / (int64_t(PH.nt[2]) * PH.nt[1]);
+                    const int64_t tt[3] = {t0, t1, t2};
+                    uint64_t h = PH.fnv_prefix;
+                    for (int d = 0; d < 3; ++d) {
+                        const TilingRec& r = P.til[d][size_t(tt[d])];
+                        for (uint32_t v : {r.blocks, r.threads, r.pt})
+                            for (int b = 0; b < 8; ++b) {
+                                h ^= (uint64_t(v) >> (8 * b)) & 0xffu;
+                                h *= 1099511628211ull;
+                            }
+                    }
+                    keyed->khash[size_t(key)] = h;
+                }
                 keyed->ok = true;
             }
         }

@@ -36,6 +36,7 @@ struct KeyedBuild {
     bool ok = false;
     std::vector<uint8_t> blob;
     std::vector<uint8_t> table;   // [nkeys][row_bytes]
+    std::vector<uint64_t> khash;  // [nkeys]: FNV-1a state after the operator words and the key's tilings
     KeyedParams params{};
     int64_t nkeys = 0;
     int key_bits = 0;

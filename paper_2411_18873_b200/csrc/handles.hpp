@@ -80,6 +80,7 @@ struct CompiledScore {
     uint8_t* d_kblob = nullptr;
     uint32_t kbytes = 0;
     uint8_t* d_ktable = nullptr;
+    uint64_t* d_khash = nullptr;  // per key: FNV-1a state after the operator and the three tilings
     size_t ktable_bytes = 0;
     std::shared_ptr<etune_b200::KeyedParams> kparams;
     int key_bits = 0, nkeys = 0, nt1 = 0, nt2 = 0, keyed_per_sm = 1;

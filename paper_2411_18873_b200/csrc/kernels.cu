@@ -553,6 +553,7 @@ constexpr int kKeyedThreads = 512;
 
 __global__ void __launch_bounds__(kKeyedThreads, 3) score_keyed_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
                                                                     const uint8_t* __restrict__ table,
+                                                                    const uint64_t* __restrict__ khash,
                                                                     const uint64_t* __restrict__ genome,
                                                                     const uint32_t* __restrict__ order, int64_t n,
                                                                     double* __restrict__ pred,
@@ -568,9 +569,6 @@ __global__ void __launch_bounds__(kKeyedThreads, 3) score_keyed_kernel(const uin
     const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
     const KeyedHdr& K = *reinterpret_cast<const KeyedHdr*>(S);
     const uint8_t* clskuv = S + K.off_clskuv;
-    const TilingRec* til0 = at<TilingRec>(S, K.off_til[0]);
-    const TilingRec* til1 = at<TilingRec>(S, K.off_til[1]);
-    const TilingRec* til2 = at<TilingRec>(S, K.off_til[2]);
     const int64_t* divk = at<int64_t>(S, K.off_divk);
     const uint32_t row_bytes = uint32_t(K.row_bytes);
     for (int64_t s = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; s < n; s += int64_t(gridDim.x) * blockDim.x) {
@@ -578,20 +576,19 @@ __global__ void __launch_bounds__(kKeyedThreads, 3) score_keyed_kernel(const uin
         const uint32_t idx = order ? __ldg(order + s) : uint32_t(s);
         const Genome x = genome_unpack(__ldcs(genome + s));  // read once: evict first
         const uint32_t kc = clskuv[(x.k * 16u + x.u) * 4u + x.v];
-        const uint8_t* row = table + size_t(keyed_row_index(kp, K, x, kc)) * row_bytes;
+        const uint32_t key = keyed_key(K, x);
+        // the FNV-1a state after the operator and the three tilings is per key (host-built,
+        // L1-resident): only k_tile, unroll and vec are hashed here
+        const uint64_t h9 = ids ? __ldg(khash + key) : 0ull;
+        const uint8_t* row = table + size_t(kp.kfull ? key * kp.nkc + kc : key) * row_bytes;
         const double p = keyed_finish(K, kp.kfull ? keyed_sum5(S, kp, row) : keyed_sum(S, kp, row, kc));
         pred[idx] = p;  // stays in L2 for the selection filter that reads it next
         if (sel.hist) atomicAdd(&shist[sel_bin(p, sel)], 1u);
         if (ids) {
-            Knobs c;
-            c.r[0] = til0[x.t0];
-            c.r[1] = til1[x.t1];
-            c.r[2] = til2[x.t2];
-            c.k_tile = divk[x.k];
-            c.unroll = 1u << x.u;
-            c.vec = 1u << x.v;
-            __stcs(reinterpret_cast<unsigned long long*>(ids) + idx,
-                   static_cast<unsigned long long>(candidate_hash(K.fnv_prefix, c)));
+            uint64_t h = fnv_small(h9, static_cast<uint32_t>(divk[x.k]));
+            h = fnv_small(h, 1u << x.u);
+            h = fnv_small(h, 1u << x.v);
+            __stcs(reinterpret_cast<unsigned long long*>(ids) + idx, static_cast<unsigned long long>(h));
         }
     }
     if (sel.hist) {
@@ -759,7 +756,8 @@ cudaError_t score_keyed_occupancy(uint32_t bytes, int* per_sm) {
 }
 
 cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint8_t* d_table,
-                               size_t table_bytes, const uint64_t* d_genome, const uint32_t* d_order, int64_t n,
+                               size_t table_bytes, const uint64_t* d_khash, const uint64_t* d_genome,
+                               const uint32_t* d_order, int64_t n,
                                double* d_pred, uint64_t* d_ids, int per_sm, const KeyedParams& kp,
                                const SelHist& sel) {
     if (n <= 0) return cudaSuccess;
@@ -781,8 +779,8 @@ cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint3
     cfg.attrs = at;
     cfg.numAttrs = 1;
     note_launches(1);
-    return cudaLaunchKernelEx(&cfg, score_keyed_kernel, d_kblob, bytes, d_table, d_genome, d_order, n, d_pred, d_ids,
-                              sel, kp);
+    return cudaLaunchKernelEx(&cfg, score_keyed_kernel, d_kblob, bytes, d_table, d_khash, d_genome, d_order, n,
+                              d_pred, d_ids, sel, kp);
 }
 
 int score_static_smem() {

@@ -60,10 +60,12 @@ cudaError_t launch_score(const LaunchCtx& c, const uint8_t* d_score, uint32_t sc
                          const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
                          int mask_bits, const ForestParams& fp, int per_sm, const SelHist& sel = SelHist{});
 // Keyed score path (KeyedHdr / KeyedParams): one byte per (tiling-triple key, tree)
-// from the key table; results at the original index (d_order nullable).
+// from the key table; results at the original index (d_order nullable).  d_khash: per key,
+// the FNV-1a state after the operator words and the key's three tiling records.
 cudaError_t score_keyed_occupancy(uint32_t bytes, int* per_sm);
 cudaError_t launch_score_keyed(const LaunchCtx& c, const uint8_t* d_kblob, uint32_t bytes, const uint8_t* d_table,
-                               size_t table_bytes, const uint64_t* d_genome, const uint32_t* d_order, int64_t n,
+                               size_t table_bytes, const uint64_t* d_khash, const uint64_t* d_genome,
+                               const uint32_t* d_order, int64_t n,
                                double* d_pred, uint64_t* d_ids, int per_sm, const KeyedParams& kp,
                                const SelHist& sel = SelHist{});
 // Selection from the histogram the score kernel filled: filter (keys below the k-th
