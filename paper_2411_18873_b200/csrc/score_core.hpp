@@ -228,7 +228,7 @@ struct RowOct {
 };
 __device__ __forceinline__ RowOct ld_row32(const uint8_t* row, int o) {
     RowOct r;
-    asm("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+    asm("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
         : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]),
           "=r"(r.w[7])
         : "l"(row + 32 * o));
