@@ -398,9 +398,10 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload(K), "op": OP_TEXT, "population_per_gpu": n,
-                   "implementation": "etune_cu_score_select: keyed score kernel (one byte per tiling-triple x tree "
-                                     "from an L2-resident key table, + ids, + selection histogram) -> bucket filter "
-                                     "-> rank selection, PDL-chained",
+                   "implementation": "etune_cu_score_select: keyed score kernel (per candidate one 64-byte row of "
+                                     "5-bit exit slots per (tiling triple, Kuv class) from an L2-resident key table, "
+                                     "two 256-bit loads; leaf words from shared memory; + ids, + selection histogram) "
+                                     "-> bucket filter -> rank selection, PDL-chained",
                    "k": K, "model": "reference-trained 100-tree depth-6 GBDT (tests/golden c2 fixture)",
                    "parallelism": f"dp{world} (population sharded; NCCL all-gather of per-shard top-k records "
                                   f"inside the C ABI)",
