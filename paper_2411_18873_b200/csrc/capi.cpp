@@ -317,7 +317,9 @@ etune_status ensure_keyed(etune_cu_forest* f, const etune_cu_plan* p, CompiledSc
     CU(cudaMemcpyAsync(cs->d_kblob, kb.blob.data(), kb.blob.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaMemcpyAsync(cs->d_ktable, kb.table.data(), kb.table.size(), cudaMemcpyHostToDevice, f->ctx->stream));
     CU(cudaStreamSynchronize(f->ctx->stream));
-    cs->kbytes = uint32_t(kb.blob.size());
+    // the full form's kernel stages (and sizes its shared memory for) the blob prefix it reads
+    cs->kbytes = kb.params.kfull ? reinterpret_cast<const KeyedHdr*>(kb.blob.data())->full_bytes
+                                 : uint32_t(kb.blob.size());
     cs->ktable_bytes = kb.table.size();
     cs->kparams = std::make_shared<KeyedParams>(kb.params);
     cs->key_bits = kb.key_bits;

@@ -186,8 +186,9 @@ struct ScoreHdr {
 // Full form (when the table stays <= 64 MB): one row per (key, Kuv class) holding every
 // tree's exit slot as 5 bits, 25 per 16-byte quad (100 trees: 64-byte rows), so a tree costs
 // only its leaf words.
-// Blob (shared memory): header, tilings, divisors of K, Kuv class table, Kuv flags,
-// packed mask lists, Kuv masks [tree][nkc], leaf blocks (32 hi + 32 lo words/tree).
+// Blob (shared memory): header, divisors of K, Kuv class table, leaf blocks (32 hi + 32 lo
+// words/tree) -- the full form stages only this prefix -- then tilings, packed mask lists,
+// Kuv masks [tree][nkc].
 struct KeyedHdr {
     int64_t K;
     uint64_t fnv_prefix;
@@ -201,7 +202,8 @@ struct KeyedHdr {
     uint32_t off_mlist;    // uint32: distinct non-Kuv masks of the Kuv trees, tree after tree
     uint32_t off_kuvtab;   // uint32 [tree][nkc]
     uint32_t off_leaves;   // per tree 32 high words then 32 low words, de Bruijn slots
-    uint32_t total, pad2;
+    uint32_t total;
+    uint32_t full_bytes;   // prefix the full form reads (header, divk, Kuv classes, leaves)
 };
 constexpr int kKeyedMaxTrees = 128;
 struct KeyedParams {       // kernel parameter (constant bank: warp-uniform reads cost no shared-memory issue)

@@ -563,9 +563,15 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                 K.ndk = PH.ndk;
                 std::vector<uint8_t>& kbl = keyed->blob;
                 kbl.assign(align16(sizeof(KeyedHdr)), 0);
-                for (int d = 0; d < 3; ++d) K.off_til[d] = put(kbl, P.til[d].data(), P.til[d].size());
+                // what the full form reads comes first (header, divisors of K, Kuv classes, leaf
+                // blocks: the `full_bytes` prefix its kernel stages); tilings and the byte form's
+                // mask lists follow
                 K.off_divk = put(kbl, P.divk.data(), P.divk.size());
                 K.off_clskuv = put(kbl, cls[kChKuv].data(), cls[kChKuv].size());
+                K.off_leaves = put(kbl, leaves.data(), leaves.size());  // 32 doubles (256 B) per tree, tree order
+                kbl.resize(align16(kbl.size()));
+                K.full_bytes = uint32_t(kbl.size());
+                for (int d = 0; d < 3; ++d) K.off_til[d] = put(kbl, P.til[d].data(), P.til[d].size());
                 std::vector<uint32_t> mlist;
                 std::vector<uint32_t> mstart(static_cast<size_t>(T), 0u);
                 for (int64_t t = 0; t < T; ++t) {
@@ -576,7 +582,6 @@ etune_status build_score_blob(const ForestHost& F, const PlanBuild& P, std::vect
                 K.off_mlist = put(kbl, mlist.data(), mlist.size());
                 for (int64_t t = 0; t < T; ++t) keyed->params.moff[t] = K.off_mlist + 4u * mstart[size_t(t)];
                 K.off_kuvtab = put(kbl, kuvtab.data(), kuvtab.size());
-                K.off_leaves = put(kbl, leaves.data(), leaves.size());  // 32 doubles (256 B) per tree, tree order
                 kbl.resize(align16(kbl.size()));
                 K.total = uint32_t(kbl.size());
                 std::memcpy(kbl.data(), &K, sizeof(K));
