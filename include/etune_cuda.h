@@ -278,6 +278,11 @@ etune_status etune_cu_profile_score(etune_cu_ctx* ctx, int on, double* pre_ms /*
  * kernel only.  All are bit-identical.  Set it before the first large scoring call. */
 etune_status etune_cu_forest_set_keyed(etune_cu_forest* forest, int mode);
 
+/* Which form scores populations of >= 2^16 candidates of this plan (compiling it now if
+ * needed): 0 = class-table kernel, 1 = keyed byte form, 2 = keyed full form, 3 = the
+ * general tree-walk kernel.  Diagnostic. */
+etune_status etune_cu_forest_score_form(etune_cu_forest* forest, const etune_cu_plan* plan, int* form);
+
 /* Reference-facing end-to-end call with HOST buffers: schedules in the reference's
  * Schedule layout -> predictions (+ ids).  Host->device copy, encode (legality check),
  * fused score and device->host copy, synchronised.  Equivalent to

@@ -153,6 +153,7 @@ _SIGS = {
     "etune_cu_profile_score": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double), C.POINTER(_I64)]),
     "etune_cu_forest_set_keyed": (C.c_int, [_VP, C.c_int]),
+    "etune_cu_forest_score_form": (C.c_int, [_VP, _VP, C.POINTER(C.c_int)]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
     "etune_cu_train": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(BoostParams), _PTR, _PTR, _PTR, _PTR, _PTR, _PTR,
@@ -198,6 +199,13 @@ def lib():
     if _lib is None:
         if not os.path.exists(LIB_PATH):
             raise EtuneError(65, f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        # libetune_cuda.so and torch both need libnccl.so.2; whichever loads first provides
+        # it process-wide.  Load torch's (newer) copy first so a later `import torch` still
+        # finds every symbol it expects.
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         L = C.CDLL(LIB_PATH)
         for name, (res, args) in _SIGS.items():
             f = getattr(L, name)
@@ -470,6 +478,12 @@ class Forest:
         2 keyed byte form only, False/0 class-table kernel only."""
         _check(lib().etune_cu_forest_set_keyed(self.h, int(mode)))
         return self
+
+    def score_form(self, plan: Plan) -> str:
+        """Form that scores large populations of `plan`: 'class', 'keyed-byte', 'keyed-full' or 'walk'."""
+        v = C.c_int(-1)
+        _check(lib().etune_cu_forest_score_form(self.h, plan.h, C.byref(v)))
+        return ("class", "keyed-byte", "keyed-full", "walk")[v.value]
 
     def score_select(self, plan: Plan, genome, k: int, pred, idx, ids=None):
         """Fused score + keep-the-best (etune_cu_score_select) into preallocated tensors."""

@@ -1092,6 +1092,15 @@ etune_status etune_cu_forest_set_keyed(etune_cu_forest* f, int mode) {
     return ETUNE_OK;
 }
 
+etune_status etune_cu_forest_score_form(etune_cu_forest* f, const etune_cu_plan* p, int* form) {
+    if (!f || !p || !form) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    CompiledScore* cs = nullptr;
+    if (etune_status st = get_compiled(f, p, &cs)) return st;
+    if (etune_status st = ensure_keyed(f, p, cs, kKeyedMinN)) return st;
+    *form = cs->walk ? 3 : !use_keyed(f, cs, kKeyedMinN) ? 0 : cs->kparams->kfull ? 2 : 1;
+    return ETUNE_OK;
+}
+
 etune_status etune_cu_profile_score(etune_cu_ctx* c, int on, double* prep_ms, double* score_ms, double* select_ms,
                                     int64_t* launches) {
     if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");

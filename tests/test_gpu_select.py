@@ -201,3 +201,30 @@ def test_keyed_path_matches_class_tables_and_oracle(golden, oracle, ctx, capi, t
         assert (pred.view(np.uint64) == p_ref.view(np.uint64)).all()
         assert (ids == ids_ref).all()
         assert (idx == oracle.topk(p_ref, 1024)).all()
+
+
+@pytest.mark.parametrize("trees", [1, 24, 25, 26, 49, 50, 51, 77, 128])
+def test_keyed_full_form_tree_counts(golden, oracle, ctx, capi, trees):
+    """Full-form rows hold 25 exit slots per 16-byte quad and are read one 32-byte sector
+    at a time: forests whose tree count ends inside a quad, on a quad or sector edge, or
+    at the 128-tree limit (the golden forest's trees repeated) score bit-exactly."""
+    k = "c2_r50_conv3x3/model/"
+    off0 = np.asarray(golden[k + "offsets"], np.int64)
+    reps = (trees + 99) // 100
+    cols = {c: np.concatenate([golden[k + c]] * reps) for c in ("feature", "threshold", "left", "right", "value")}
+    off = np.concatenate([off0[:-1] + r * off0[-1] for r in range(reps)] + [[reps * off0[-1]]])[: trees + 1]
+    nn = int(off[-1])
+    flat = FlatForest(*(np.ascontiguousarray(cols[c][:nn]) for c in ("feature", "threshold", "left", "right",
+                                                                     "value")),
+                      off, float(golden[k + "base_score"][0]), float(golden[k + "learning_rate"][0]))
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    plan = capi.Plan(ctx, op)
+    parents, _ = oracle.sample_random(op, 1024, 42)
+    sched = oracle.reproduce(op, parents, 1 << 16, 5 + trees)[0]  # >= 2^16: the keyed form is compiled
+    p_ref = oracle.predict(flat, oracle.features(op, sched))
+    fo = capi.Forest.from_flat(ctx, flat).set_keyed(1)
+    assert fo.score_form(plan) == "keyed-full"
+    pred, ids = fo.score(plan, plan.encode(dev(sched)), with_ids=True)
+    ctx.synchronize()
+    assert (pred.cpu().numpy().view(np.uint64) == p_ref.view(np.uint64)).all()
+    assert (ids.cpu().numpy().view(np.uint64) == oracle.ids(op, sched).astype(np.uint64)).all()
