@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <fstream>
@@ -502,6 +504,75 @@ inline DeviceConfig device_profile_from_json(const std::string& text, std::strin
     return d;
 }
 
+// MeasurementRecord / MeasurementLog / log_append / log_load (measure.hpp:17-83)
+struct MeasurementRecord {
+    uint64_t candidate_id = 0;
+    double latency_ms = 0.0, avg_power_w = 0.0, energy_mj = 0.0;
+    int64_t iterations = 0;
+    std::string backend, timestamp;
+};
+class MeasurementLog {
+public:
+    void add(const MeasurementRecord& r) {
+        by_id_[r.candidate_id] = records_.size();
+        records_.push_back(r);
+    }
+    const std::vector<MeasurementRecord>& records() const { return records_; }
+    bool contains(uint64_t id) const { return by_id_.count(id) != 0; }
+    const MeasurementRecord& lookup(uint64_t id) const {  // most recent record; TraceMiss when absent
+        const auto it = by_id_.find(id);
+        if (it == by_id_.end())
+            throw TraceMiss(ETUNE_ERR_TRACE_MISS, "candidate id " + std::to_string(id) + " is not in the log", -1);
+        return records_[it->second];
+    }
+
+private:
+    std::vector<MeasurementRecord> records_;
+    std::map<uint64_t, size_t> by_id_;
+};
+inline etune_log_record to_log_record(const MeasurementRecord& r) {
+    etune_log_record x{};
+    x.m.candidate_id = r.candidate_id;
+    x.m.latency_ms = r.latency_ms;
+    x.m.avg_power_w = r.avg_power_w;
+    x.m.energy_mj = r.energy_mj;
+    x.m.iterations = r.iterations;
+    x.m.feasible = 1;
+    std::strncpy(x.backend, r.backend.c_str(), sizeof(x.backend) - 1);
+    std::strncpy(x.timestamp, r.timestamp.c_str(), sizeof(x.timestamp) - 1);
+    return x;
+}
+inline void log_append(const std::string& path, const MeasurementRecord& r) {
+    const etune_log_record x = to_log_record(r);
+    int64_t len = 0;
+    check(etune_measurement_log_to_jsonl(&x, 1, nullptr, 0, &len));
+    std::string text(size_t(len) + 1, '\0');
+    check(etune_measurement_log_to_jsonl(&x, 1, &text[0], len + 1, &len));
+    std::ofstream out(path, std::ios::app);
+    if (!out) throw IoError(ETUNE_ERR_IO, "cannot append to measurement log '" + path + "'", -1);
+    out.write(text.data(), len);
+    if (!out) throw IoError(ETUNE_ERR_IO, "failed writing measurement log '" + path + "'", -1);
+}
+inline MeasurementLog log_load(const std::string& path) {
+    std::ifstream in(path);
+    if (!in) throw IoError(ETUNE_ERR_IO, "cannot open measurement log '" + path + "'", -1);
+    std::ostringstream buf;
+    buf << in.rdbuf();
+    const std::string text = buf.str();
+    etune_log_record* recs = nullptr;
+    int64_t n = 0;
+    check(etune_measurement_log_from_jsonl(text.data(), int64_t(text.size()), &recs, &n));
+    MeasurementLog log;
+    for (int64_t i = 0; i < n; ++i) {
+        const etune_log_record& x = recs[i];
+        log.add(MeasurementRecord{x.m.candidate_id, x.m.latency_ms, x.m.avg_power_w, x.m.energy_mj, x.m.iterations,
+                                  std::string(x.backend, strnlen(x.backend, sizeof(x.backend))),
+                                  std::string(x.timestamp, strnlen(x.timestamp, sizeof(x.timestamp)))});
+    }
+    etune_measurement_log_free(recs);
+    return log;
+}
+
 inline std::vector<Candidate> to_candidates(const Plan& plan, const DeviceBuffer<uint64_t>& g, size_t n) {
     DeviceBuffer<uint64_t> ids(n);
     check(etune_cu_candidate_ids(plan.device().get(), plan.get(), g.get(), int64_t(n), ids.get()));
@@ -555,10 +626,17 @@ inline std::vector<int64_t> select_lowest(Device& dev, const std::vector<double>
 }
 
 // ------------------------------------------------------------------ search
-class Search {  // Algorithm 1 with the SimBackend
+class Search {  // Algorithm 1: SimBackend, the GPU itself, or a ReplayBackend log
 public:
     Search(Plan& plan, const etune_search_config& cfg) : plan_(&plan) {
         check(etune_cu_search_create(plan.device().get(), plan.get(), &cfg, &h_));
+    }
+    // ReplayBackend (measure.hpp:116-128) for cfg.backend == 2
+    void set_replay(const MeasurementLog& log) {
+        std::vector<etune_measurement> m;
+        m.reserve(log.records().size());
+        for (const MeasurementRecord& r : log.records()) m.push_back(to_log_record(r).m);
+        check(etune_cu_search_set_replay(h_, m.data(), int64_t(m.size())));
     }
     ~Search() { etune_cu_search_destroy(h_); }
     Search(const Search&) = delete;

@@ -385,7 +385,8 @@ typedef struct etune_search_config {
     etune_genetic_rates rates;
     etune_boost_params boost;
     int32_t backend;           /* 0: SimBackend (device formula), 1: the GPU itself (candidate kernels:
-                                  CUDA-event latency filter, NVML energy of the selected) */
+                                  CUDA-event latency filter, NVML energy of the selected), 2: ReplayBackend
+                                  (measure.hpp:116-128: records of a log, etune_cu_search_set_replay) */
     int32_t latency_reps;      /* backend 1: timed runs per candidate in the latency filter */
     etune_nvml_params nvml;    /* backend 1: energy measurement protocol */
 } etune_search_config;
@@ -408,6 +409,10 @@ void etune_default_search_config(etune_search_config* out);
 etune_status etune_cu_search_create(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                     const etune_search_config* cfg, etune_cu_search** out);
 etune_status etune_cu_search_destroy(etune_cu_search* s);
+/* ReplayBackend's log (backend 2): latency filter and energy measurements are looked up by
+ * candidate id, the most recent record of an id winning (MeasurementLog::lookup); an id
+ * the log lacks fails the round with ETUNE_ERR_TRACE_MISS.  Copies the records. */
+etune_status etune_cu_search_set_replay(etune_cu_search* s, const etune_measurement* records, int64_t n);
 etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* out);  /* initial_round */
 etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* out);    /* round */
 /* run_search: initial round (if not yet run) then rounds until max_rounds or patience;
@@ -494,6 +499,22 @@ etune_status etune_samples_to_jsonl(const double* features, const double* measur
  * ETUNE_ERR_SCHEMA_MISMATCH (width != 16), ETUNE_ERR_NON_POSITIVE_ENERGY. */
 etune_status etune_samples_from_jsonl(const char* text, int64_t len, etune_samples_host* out);
 void etune_samples_host_free(etune_samples_host* s);
+
+/* MeasurementLog (measure.hpp:63-83): append-only JSONL, one
+ * MeasurementRecord per line.  The reference declares the log but ships no writer, so the
+ * line layout follows its other JSONL files (nlohmann dump(), keys in sorted order). */
+typedef struct etune_log_record {
+    etune_measurement m;          /* candidate_id, latency_ms, avg_power_w, energy_mj, iterations */
+    char backend[16];             /* NUL-terminated backend tag ("sim", "nvml", ...) */
+    char timestamp[32];           /* NUL-terminated UTC timestamp */
+} etune_log_record;
+/* log_append: the JSONL text of n records (append it to the log file). */
+etune_status etune_measurement_log_to_jsonl(const etune_log_record* records, int64_t n, char* out /*nullable*/,
+                                            int64_t cap, int64_t* out_len);
+/* log_load: empty text = empty log; ETUNE_ERR_IO (unparsable line), ETUNE_ERR_CONSISTENCY
+ * (energy_mj != avg_power_w * latency_ms beyond 1e-9 relative, line number in the message). */
+etune_status etune_measurement_log_from_jsonl(const char* text, int64_t len, etune_log_record** out, int64_t* n);
+void etune_measurement_log_free(etune_log_record* records);
 
 /* device_profile_to_json (device.cpp:44-62), "etune-profile-v1", dump(2) + newline. */
 etune_status etune_device_profile_to_json(const etune_device_config* dev, const char* name /*nullable*/,

@@ -146,6 +146,10 @@ _SIGS = {
     "etune_model_host_free": (None, [C.POINTER(ModelHost)]),
     "etune_samples_to_jsonl": (C.c_int, [_PTR, _PTR, _PTR, _I64, C.c_char_p, _I64, C.POINTER(_I64)]),
     "etune_samples_from_jsonl": (C.c_int, [C.c_char_p, _I64, C.POINTER(SamplesHost)]),
+    "etune_measurement_log_to_jsonl": (C.c_int, [_PTR, _I64, C.c_char_p, _I64, C.POINTER(_I64)]),
+    "etune_measurement_log_from_jsonl": (C.c_int, [C.c_char_p, _I64, C.POINTER(_VP), C.POINTER(_I64)]),
+    "etune_measurement_log_free": (None, [_VP]),
+    "etune_cu_search_set_replay": (C.c_int, [_VP, _PTR, _I64]),
     "etune_samples_host_free": (None, [C.POINTER(SamplesHost)]),
     "etune_device_profile_to_json": (C.c_int, [C.POINTER(DeviceConfig), C.c_char_p, C.c_char_p, _I64,
                                                C.POINTER(_I64)]),
@@ -606,6 +610,15 @@ class Search:
         except Exception:
             pass
 
+    def set_replay(self, records):
+        """ReplayBackend log (backend 2): MEASUREMENT_DTYPE records (or LOG_RECORD_DTYPE)."""
+        r = np.asarray(records)
+        if r.dtype == LOG_RECORD_DTYPE:
+            r = r["m"]
+        r = np.ascontiguousarray(r, MEASUREMENT_DTYPE)
+        _check(lib().etune_cu_search_set_replay(self.h, r.ctypes.data, len(r)))
+        return self
+
     def initial(self) -> RoundReport:
         r = RoundReport()
         _check(lib().etune_cu_search_initial(self.h, C.byref(r)))
@@ -722,6 +735,32 @@ def samples_from_jsonl(text: str):
                 np.ctypeslib.as_array(s.normalized_energy, shape=(n,)).copy())
     finally:
         lib().etune_samples_host_free(C.byref(s))
+
+
+# etune_measurement (MeasurementRecord) and etune_log_record (one MeasurementLog line)
+MEASUREMENT_DTYPE = np.dtype([("candidate_id", "<u8"), ("latency_ms", "<f8"), ("avg_power_w", "<f8"),
+                              ("energy_mj", "<f8"), ("iterations", "<i8"), ("feasible", "<i4"), ("reserved", "<i4")])
+LOG_RECORD_DTYPE = np.dtype([("m", MEASUREMENT_DTYPE), ("backend", "S16"), ("timestamp", "S32")])
+
+
+def measurement_log_to_jsonl(records) -> str:
+    """log_append text of LOG_RECORD_DTYPE records (measure.hpp:76-77)."""
+    r = np.ascontiguousarray(records, LOG_RECORD_DTYPE)
+    return _emit(lambda out, cap, n: lib().etune_measurement_log_to_jsonl(r.ctypes.data, len(r), out, cap, n))
+
+
+def measurement_log_from_jsonl(text: str):
+    """log_load (measure.hpp:79-83): LOG_RECORD_DTYPE records; ConsistencyError (13) names the line."""
+    b = text.encode()
+    p, n = C.c_void_p(), C.c_int64()
+    _check(lib().etune_measurement_log_from_jsonl(b, len(b), C.byref(p), C.byref(n)))
+    try:
+        if n.value == 0:
+            return np.zeros(0, LOG_RECORD_DTYPE)
+        buf = (C.c_char * (n.value * LOG_RECORD_DTYPE.itemsize)).from_address(p.value)
+        return np.frombuffer(bytes(buf), LOG_RECORD_DTYPE).copy()
+    finally:
+        lib().etune_measurement_log_free(p)
 
 
 def device_profile_to_json(dev: DeviceConfig, name: str = "a100-like") -> str:

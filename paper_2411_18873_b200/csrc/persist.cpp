@@ -8,6 +8,7 @@
 // the writer below follows that layout, and the parser reads numbers with strtod like
 // nlohmann's lexer, so every double survives bit for bit.  Host code only: these are
 // the data formats either side of the device path, not part of it.
+#include <algorithm>
 #include <cerrno>
 #include <cstdint>
 #include <cmath>
@@ -773,6 +774,78 @@ void etune_samples_host_free(etune_samples_host* s) {
     std::free(s->normalized_energy);
     std::memset(s, 0, sizeof(*s));
 }
+
+etune_status etune_measurement_log_to_jsonl(const etune_log_record* r, int64_t n, char* out, int64_t cap,
+                                            int64_t* out_len) {
+    if (n < 0 || (n > 0 && !r)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad record array");
+    std::string s;
+    s.reserve(size_t(n) * 200);
+    for (int64_t i = 0; i < n; ++i) {
+        const etune_log_record& x = r[i];
+        s += "{\"avg_power_w\":";
+        put_double(s, x.m.avg_power_w);
+        s += ",\"backend\":";
+        put_string(s, std::string(x.backend, strnlen(x.backend, sizeof(x.backend))));
+        s += ",\"candidate_id\":" + std::to_string(x.m.candidate_id);
+        s += ",\"energy_mj\":";
+        put_double(s, x.m.energy_mj);
+        s += ",\"iterations\":" + std::to_string(x.m.iterations);
+        s += ",\"latency_ms\":";
+        put_double(s, x.m.latency_ms);
+        s += ",\"timestamp\":";
+        put_string(s, std::string(x.timestamp, strnlen(x.timestamp, sizeof(x.timestamp))));
+        s += "}\n";
+    }
+    return emit(s, out, cap, out_len);
+}
+
+etune_status etune_measurement_log_from_jsonl(const char* text, int64_t len, etune_log_record** out, int64_t* n) {
+    if (!text || len < 0 || !out || !n) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    *out = nullptr;
+    *n = 0;
+    std::vector<etune_log_record> recs;
+    const char* p = text;
+    const char* e = text + len;
+    int line_no = 0;
+    while (p < e) {
+        const char* q = static_cast<const char*>(std::memchr(p, '\n', size_t(e - p)));
+        if (!q) q = e;
+        ++line_no;
+        const std::string ln = "line " + std::to_string(line_no);
+        if (q > p) {
+            etune_log_record x;
+            std::memset(&x, 0, sizeof(x));
+            try {
+                const JVal j = Parser(p, size_t(q - p)).document();
+                x.m.candidate_id = as_u64(at(j, "candidate_id"));
+                x.m.latency_ms = as_double(at(j, "latency_ms"));
+                x.m.avg_power_w = as_double(at(j, "avg_power_w"));
+                x.m.energy_mj = as_double(at(j, "energy_mj"));
+                const JVal* it = find(j, "iterations");
+                x.m.iterations = it ? as_int(*it) : 0;
+                x.m.feasible = 1;
+                const std::string be = str_or(j, "backend", ""), ts = str_or(j, "timestamp", "");
+                std::memcpy(x.backend, be.data(), std::min(be.size(), sizeof(x.backend) - 1));
+                std::memcpy(x.timestamp, ts.data(), std::min(ts.size(), sizeof(x.timestamp) - 1));
+            } catch (const JsonError& er) {
+                return fail(ETUNE_ERR_IO, "bad measurement log at " + ln + ": " + er.what);
+            }
+            // energy_mj = avg_power_w x latency_ms within 1e-9 relative
+            const double want = x.m.avg_power_w * x.m.latency_ms;
+            if (!(std::fabs(x.m.energy_mj - want) <= 1e-9 * std::fabs(want)))
+                return fail(ETUNE_ERR_CONSISTENCY, "measurement log " + ln + ": energy_mj != avg_power_w * latency_ms");
+            recs.push_back(x);
+        }
+        p = q + 1;
+    }
+    *n = int64_t(recs.size());
+    *out = static_cast<etune_log_record*>(std::malloc(sizeof(etune_log_record) * recs.size() + 1));
+    if (!*out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "out of host memory");
+    if (!recs.empty()) std::memcpy(*out, recs.data(), sizeof(etune_log_record) * recs.size());
+    return ETUNE_OK;
+}
+
+void etune_measurement_log_free(etune_log_record* r) { std::free(r); }
 
 etune_status etune_device_profile_to_json(const etune_device_config* d, const char* name, char* out, int64_t cap,
                                           int64_t* out_len) {

@@ -18,6 +18,7 @@
 #include <cstring>
 #include <limits>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "handles.hpp"
@@ -56,6 +57,10 @@ struct etune_cu_search {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_par = nullptr, ev_pop = nullptr;
     int64_t pop_round = -1;  // round whose generation is in flight / in `pop`
+    // ReplayBackend (backend 2): the log's records by candidate id, most recent winning
+    std::unordered_map<uint64_t, etune_measurement> replay;
+    bool replay_set = false;
+    uint64_t* gids = nullptr;  // generation-sized id buffer for replay lookups
 };
 
 namespace {
@@ -229,8 +234,36 @@ etune_status host_schedules(etune_cu_search* s, const uint64_t* gen, int64_t n, 
 }
 
 // LatencyEvaAndPick's measurement: the backend's latency of n device genomes into d_lat
+// ReplayBackend (measure.hpp:116-128): the logged records of n device genomes, by id;
+// TraceMiss names the first id the log lacks
+etune_status replay_lookup(etune_cu_search* s, const uint64_t* gen, int64_t n, std::vector<etune_measurement>* rec) {
+    if (!s->gids) SOK(dalloc(s, &s->gids, s->cfg.generation_size));
+    SOK(etune_cu_candidate_ids(s->ctx, s->plan, gen, n, s->gids));
+    std::vector<uint64_t> ids(static_cast<size_t>(n));
+    SCU(cudaMemcpyAsync(ids.data(), s->gids, size_t(n) * 8, cudaMemcpyDeviceToHost, s->ctx->stream));
+    SOK(etune_cu_synchronize(s->ctx, nullptr));
+    rec->resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        const auto it = s->replay.find(ids[size_t(i)]);
+        if (it == s->replay.end())
+            return sfail(ETUNE_ERR_TRACE_MISS, "candidate id " + std::to_string(ids[size_t(i)]) +
+                                                   " is not in the replay log");
+        (*rec)[size_t(i)] = it->second;
+        (*rec)[size_t(i)].feasible = 1;  // a logged record is a completed measurement
+    }
+    return ETUNE_OK;
+}
+
 etune_status measure_latency(etune_cu_search* s, const uint64_t* gen, int64_t n, double* d_lat) {
     if (s->cfg.backend == 0) return etune_cu_sim_measure(s->ctx, s->plan, gen, n, d_lat, nullptr, nullptr, nullptr);
+    if (s->cfg.backend == 2) {
+        std::vector<etune_measurement> rec;
+        SOK(replay_lookup(s, gen, n, &rec));
+        std::vector<double> lat(static_cast<size_t>(n));
+        for (int64_t i = 0; i < n; ++i) lat[size_t(i)] = rec[size_t(i)].latency_ms;
+        SCU(cudaMemcpyAsync(d_lat, lat.data(), size_t(n) * 8, cudaMemcpyHostToDevice, s->ctx->stream));
+        return etune_cu_synchronize(s->ctx, nullptr);
+    }
     std::vector<etune_schedule> h;
     SOK(host_schedules(s, gen, n, &h));
     std::vector<double> lat(static_cast<size_t>(n));
@@ -245,10 +278,14 @@ etune_status measure_latency(etune_cu_search* s, const uint64_t* gen, int64_t n,
 etune_status measure_energy(etune_cu_search* s, const uint64_t* gen, int64_t n) {
     if (s->cfg.backend == 0)
         return etune_cu_sim_measure(s->ctx, s->plan, gen, n, s->mlat, s->mpow, s->men, nullptr);
-    std::vector<etune_schedule> h;
-    SOK(host_schedules(s, gen, n, &h));
     std::vector<etune_measurement> rec(static_cast<size_t>(n));
-    SOK(etune_cu_nvml_measure(s->ctx, s->plan, h.data(), n, &s->cfg.nvml, rec.data(), nullptr));
+    if (s->cfg.backend == 2) {
+        SOK(replay_lookup(s, gen, n, &rec));
+    } else {
+        std::vector<etune_schedule> h;
+        SOK(host_schedules(s, gen, n, &h));
+        SOK(etune_cu_nvml_measure(s->ctx, s->plan, h.data(), n, &s->cfg.nvml, rec.data(), nullptr));
+    }
     std::vector<double> lat(static_cast<size_t>(n)), pw(static_cast<size_t>(n)), en(static_cast<size_t>(n));
     for (int64_t i = 0; i < n; ++i) {
         const etune_measurement& r = rec[size_t(i)];
@@ -296,7 +333,8 @@ etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, con
         return sfail(ETUNE_ERR_VALIDATION, "SearchConfig needs 0 < M <= generation_size");
     if (C.k_init_fifths < 0 || C.k_init_fifths > 5) return sfail(ETUNE_ERR_VALIDATION, "k must lie in [0, 1]");
     if (!std::isfinite(C.mu_db)) return sfail(ETUNE_ERR_VALIDATION, "mu_db must be finite");
-    if (C.backend != 0 && C.backend != 1) return sfail(ETUNE_ERR_VALIDATION, "backend must be 0 (sim) or 1 (gpu)");
+    if (C.backend < 0 || C.backend > 2)
+        return sfail(ETUNE_ERR_VALIDATION, "backend must be 0 (sim), 1 (gpu) or 2 (replay)");
     if (C.backend == 1) {
         std::string why;
         if (!nvml_device_handle(c->device, &why))
@@ -356,9 +394,20 @@ etune_status etune_cu_search_destroy(etune_cu_search* s) {
     return ETUNE_OK;
 }
 
+etune_status etune_cu_search_set_replay(etune_cu_search* s, const etune_measurement* records, int64_t n) {
+    if (!s || n < 0 || (n > 0 && !records)) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "bad replay records");
+    s->replay.clear();
+    s->replay.reserve(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) s->replay[records[i].candidate_id] = records[i];  // later lines win
+    s->replay_set = true;
+    return ETUNE_OK;
+}
+
 // initial_round: sample, latency-filter to M, measure all M, first model.
 etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* rep) {
     if (!s) return sfail(ETUNE_ERR_INVALID_ARGUMENT, "null search");
+    if (s->cfg.backend == 2 && !s->replay_set)
+        return sfail(ETUNE_ERR_BACKEND_UNAVAILABLE, "replay backend without a log (etune_cu_search_set_replay)");
     etune_cu_ctx* c = s->ctx;
     const double t0 = now_ms();
     const int64_t G = s->cfg.generation_size, M = s->cfg.M;

@@ -126,6 +126,27 @@ int main() {
         EXPECT(threw);
         std::remove(mp.c_str());
         std::remove(sp.c_str());
+        // MeasurementLog (measure.hpp:63-83): append -> load keeps every record; lookup returns
+        // the most recent record of an id; an unknown id throws TraceMiss
+        const std::string lp = "/tmp/etune_mirror_measurements.jsonl";
+        std::remove(lp.c_str());
+        MeasurementRecord r1{12345678901234567890ull, 0.0347, 239.0, 239.0 * 0.0347, 1000, "sim", "2026-10-17T00:00:00Z"};
+        MeasurementRecord r2 = r1;
+        r2.latency_ms = 0.05;
+        r2.energy_mj = r2.avg_power_w * r2.latency_ms;
+        log_append(lp, r1);
+        log_append(lp, r2);
+        const MeasurementLog lg = log_load(lp);
+        EXPECT(lg.records().size() == 2 && lg.contains(r1.candidate_id));
+        EXPECT(same_bits(lg.lookup(r1.candidate_id).latency_ms, 0.05) && lg.records()[0].backend == "sim");
+        threw = false;
+        try {
+            lg.lookup(7);
+        } catch (const TraceMiss&) {
+            threw = true;
+        }
+        EXPECT(threw);
+        std::remove(lp.c_str());
     }
 
     // snr_db

@@ -62,3 +62,38 @@ def test_search_vs_oracle(oracle, ctx, capi, text, kw):
     assert bid == reps[-1].best_id and en == reps[-1].best_energy_mj
     assert oracle.ids(op, sched[None, :])[0] == bid
     print(f"{text}: round wall ms = {[round(r.wall_ms, 2) for r in reps]}")
+
+
+def test_replay_search_reproduces_sim_search(oracle, ctx, capi):
+    """ReplayBackend (backend 2, measure.hpp:116-128): a JSONL measurement log of the
+    SimBackend records of every schedule in the space replays the sim search round for
+    round; a log lacking a candidate fails with TraceMiss."""
+    op = parse_op("mm:1,64,64,64")
+    plan = capi.Plan(ctx, op)
+    sched = oracle.enumerate(op)
+    g = plan.encode(torch.from_numpy(np.ascontiguousarray(sched)).cuda())
+    lat, pw, en, it = (t.cpu().numpy() for t in plan.sim_measure(g))
+    rec = np.zeros(len(sched), capi.LOG_RECORD_DTYPE)
+    rec["m"]["candidate_id"] = plan.ids(g).cpu().numpy().view(np.uint64)
+    rec["m"]["latency_ms"], rec["m"]["avg_power_w"], rec["m"]["energy_mj"] = lat, pw, en
+    rec["m"]["iterations"] = it
+    rec["backend"], rec["timestamp"] = b"sim", b"2026-10-17T00:00:00Z"
+    log = capi.measurement_log_from_jsonl(capi.measurement_log_to_jsonl(rec))  # through the JSONL file format
+    assert len(log) == len(sched)
+    kw = dict(M=64, generation_size=256, rng_seed=42, max_rounds=6)
+    sim = capi.Search(plan, capi.search_config(**kw)).run()
+    rep = capi.Search(plan, capi.search_config(backend=2, **kw)).set_replay(log).run()
+    assert len(rep) == len(sim)
+    for a, b in zip(rep, sim):
+        assert (a.round, a.k_before_fifths, a.k_after_fifths, a.measured, a.cumulative_measured, a.best_id) == \
+               (b.round, b.k_before_fifths, b.k_after_fifths, b.measured, b.cumulative_measured, b.best_id)
+        for f in ("snr_db", "best_latency_ms", "best_energy_mj", "best_power_w"):
+            x, y = getattr(a, f), getattr(b, f)
+            assert f64bits(x) == f64bits(y) or (np.isnan(x) and np.isnan(y))
+    miss = capi.Search(plan, capi.search_config(backend=2, **kw)).set_replay(log[:100])
+    with pytest.raises(capi.EtuneError) as e:
+        miss.run()
+    assert e.value.code == 15  # ETUNE_ERR_TRACE_MISS
+    with pytest.raises(capi.EtuneError) as e:
+        capi.Search(plan, capi.search_config(backend=2, **kw)).run()  # no log attached
+    assert e.value.code == 14

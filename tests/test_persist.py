@@ -5,6 +5,7 @@ The fixtures in tests/golden/persist/ were written by the UNMODIFIED reference
 byte for byte (nlohmann::json layout: sorted keys, shortest round-trip doubles) and
 its readers must parse every double bit for bit.  Host-only functions: no GPU."""
 import glob
+import json
 import os
 
 import numpy as np
@@ -138,3 +139,35 @@ def test_device_trained_model_round_trips_through_reference(golden, capi):
     f = feats.cpu().numpy()
     dev_pred = m.forest().predict(feats).cpu().numpy()
     assert (bits(rm.predict(f)) == bits(dev_pred)).all()
+
+
+def test_measurement_log_jsonl():
+    """MeasurementLog (measure.hpp:63-83): round trip of n records (u64 ids
+    intact), empty text -> empty log, tampered energy -> ConsistencyError naming the line,
+    unparsable line -> IoError."""
+    from paper_2411_18873_b200 import capi
+    rng = np.random.default_rng(5)
+    r = np.zeros(50, capi.LOG_RECORD_DTYPE)
+    r["m"]["candidate_id"] = rng.integers(0, 2**63, 50).astype(np.uint64) * 2 + 1
+    r["m"]["latency_ms"] = rng.uniform(1e-3, 10, 50)
+    r["m"]["avg_power_w"] = rng.uniform(50, 400, 50)
+    r["m"]["energy_mj"] = r["m"]["avg_power_w"] * r["m"]["latency_ms"]
+    r["m"]["iterations"] = rng.integers(1, 10**6, 50)
+    r["backend"], r["timestamp"] = b"sim", b"2026-10-17T12:34:56Z"
+    text = capi.measurement_log_to_jsonl(r)
+    assert text.count("\n") == 50 and text.startswith('{"avg_power_w":')
+    back = capi.measurement_log_from_jsonl(text)
+    for f in ("candidate_id", "latency_ms", "avg_power_w", "energy_mj", "iterations"):
+        assert (back["m"][f] == r["m"][f]).all(), f
+    assert (back["backend"] == r["backend"]).all() and (back["timestamp"] == r["timestamp"]).all()
+    assert len(capi.measurement_log_from_jsonl("")) == 0
+    lines = text.splitlines(keepends=True)
+    j = json.loads(lines[7])
+    j["energy_mj"] = j["energy_mj"] * (1 + 1e-6)
+    lines[7] = json.dumps(j, separators=(",", ":")) + "\n"
+    with pytest.raises(capi.EtuneError) as e:
+        capi.measurement_log_from_jsonl("".join(lines))
+    assert e.value.code == 13 and "line 8" in str(e.value)
+    with pytest.raises(capi.EtuneError) as e:
+        capi.measurement_log_from_jsonl(text + "{not json\n")
+    assert e.value.code == 12
