@@ -389,6 +389,10 @@ typedef struct etune_search_config {
                                   (measure.hpp:116-128: records of a log, etune_cu_search_set_replay) */
     int32_t latency_reps;      /* backend 1: timed runs per candidate in the latency filter */
     etune_nvml_params nvml;    /* backend 1: energy measurement protocol */
+    int32_t latency_only;      /* 1: run_latency_only: no cost model; parents = the
+                                  ceil(M/2) fastest of the M; best = lowest latency (then id), whose
+                                  energy is measured for the report (one measurement per round) */
+    int32_t reserved0;
 } etune_search_config;
 
 typedef struct etune_round_report {   /* RoundReport */

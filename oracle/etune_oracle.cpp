@@ -1029,7 +1029,8 @@ int orc_score_threads(const int64_t* op, const int64_t* sched, int64_t n, int nu
 // CPU restatement of the search loop (the reference has no
 // code) built from the restated primitives above, step for step what
 // paper_2411_18873_b200/csrc/search.cpp does on the device.  cfg_i: M, generation_size,
-// k_init_fifths, max_rounds, patience, inverted, num_trees, max_depth; cfg_d: mu_db,
+// k_init_fifths, max_rounds, patience, inverted, num_trees, max_depth, latency_only
+// (run_latency_only); cfg_d: mu_db,
 // improve_rel, mutation, crossover, copy, learning_rate, min_leaf_weight, reg_lambda.
 // Reports: rep_i n x {round, k_before, k_after, measured, cumulative, best_id},
 // rep_d n x {snr_db, best_latency_ms, best_energy_mj, best_power_w}.
@@ -1041,6 +1042,7 @@ extern "C" int orc_run_search(const int64_t* op, const int64_t* limits, const do
     int k5 = int(cfg_i[2]);
     const int64_t max_rounds = cfg_i[3], patience = cfg_i[4], inverted = cfg_i[5];
     const int trees = int(cfg_i[6]), depth = int(cfg_i[7]);
+    const bool latency_only = cfg_i[8] != 0;
     const double mu = cfg_d[0], improve = cfg_d[1], rates[3] = {cfg_d[2], cfg_d[3], cfg_d[4]};
     const double lr = cfg_d[5], mlw = cfg_d[6], lam = cfg_d[7];
     const int sms = int(dev12[0]);
@@ -1085,6 +1087,23 @@ extern "C" int orc_run_search(const int64_t* op, const int64_t* limits, const do
         }
         return best_en < before * (1.0 - improve);
     };
+    // run_latency_only: best = lowest latency (then id) of the rounds' fastest candidates,
+    // whose energy is measured for the report
+    auto update_best_latency = [&](const VI& s1) -> bool {
+        VD m1(4);
+        orc_sim_measure(op, s1.data(), 1, dev12, dev_seed, m1.data());
+        uint64_t id = 0;
+        orc_candidate_ids(op, s1.data(), 1, &id);
+        const double before = have_best ? best_lat : std::numeric_limits<double>::infinity();
+        if (!have_best || m1[0] < best_lat || (m1[0] == best_lat && id < best_id)) {
+            have_best = true;
+            best_lat = m1[0];
+            best_pow = m1[1];
+            best_en = m1[2];
+            best_id = id;
+        }
+        return best_lat < before * (1.0 - improve);
+    };
     auto report = [&](int64_t round, int kb, double snr, int64_t measured) {
         if (nrep < max_reports) {
             int64_t* ri = rep_i + 6 * nrep;
@@ -1113,6 +1132,35 @@ extern "C" int orc_run_search(const int64_t* op, const int64_t* limits, const do
     VI idx(static_cast<size_t>(M));
     orc_topk(lat.data(), G, M, idx.data());
     VI mg = sched_rows(pop, idx);
+    if (latency_only) {
+        VI par = mg;
+        cumulative = 1;
+        update_best_latency(VI(mg.begin(), mg.begin() + 12));
+        report(0, k5, std::numeric_limits<double>::quiet_NaN(), 1);
+        for (int64_t r = 1; r <= max_rounds && stall < patience; ++r) {
+            const int64_t np = int64_t(par.size() / 12);
+            VI off_s(size_t(G) * 12);
+            std::vector<uint64_t> oid(static_cast<size_t>(G)), lin(size_t(G) * 2);
+            std::vector<int8_t> ll(static_cast<size_t>(G));
+            if (int st = orc_reproduce(op, par.data(), np, G, rates, seed + uint64_t(r), limits, off_s.data(),
+                                       oid.data(), lin.data(), ll.data()))
+                return st;
+            orc_sim_measure(op, off_s.data(), G, dev12, dev_seed, m4.data());
+            for (int64_t i = 0; i < G; ++i) lat[i] = m4[4 * i];
+            orc_topk(lat.data(), G, M, idx.data());
+            mg = sched_rows(off_s, idx);
+            const int64_t npar = (M + 1) / 2;  // the ceil(M/2) fastest
+            par.assign(mg.begin(), mg.begin() + 12 * npar);
+            cumulative += 1;
+            const bool improved = update_best_latency(VI(mg.begin(), mg.begin() + 12));
+            stall = improved ? 0 : stall + 1;
+            report(r, k5, std::numeric_limits<double>::quiet_NaN(), 1);
+        }
+        *n_reports = nrep;
+        *n_parents = int64_t(par.size() / 12);
+        if (out_parents) std::copy(par.begin(), par.end(), out_parents);
+        return OK;
+    }
     VD mm(size_t(M) * 4);
     orc_sim_measure(op, mg.data(), M, dev12, dev_seed, mm.data());
     feats.resize(size_t(M) * 16);

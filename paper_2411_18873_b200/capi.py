@@ -82,7 +82,8 @@ class SearchConfig(C.Structure):
                 ("max_rounds", C.c_int32), ("patience", C.c_int32), ("inverted_semantics", C.c_int32),
                 ("mu_db", C.c_double), ("improve_rel", C.c_double), ("rng_seed", C.c_uint64),
                 ("rates", GeneticRates), ("boost", BoostParams), ("backend", C.c_int32),
-                ("latency_reps", C.c_int32), ("nvml", NvmlParams)]
+                ("latency_reps", C.c_int32), ("nvml", NvmlParams), ("latency_only", C.c_int32),
+                ("reserved0", C.c_int32)]
 
 
 class RoundReport(C.Structure):

@@ -169,6 +169,36 @@ etune_status retrain(etune_cu_search* s) {
     return ETUNE_OK;
 }
 
+etune_status measure_energy(etune_cu_search* s, const uint64_t* gen, int64_t n);
+
+// run_latency_only: best-so-far = lowest latency (then id) among the rounds' fastest
+// candidates; the fastest of this round (gen[0], the latency-sorted M) has its energy
+// measured for the report.  improved = best latency dropped by more than improve_rel.
+etune_status update_best_latency(etune_cu_search* s, const uint64_t* gen, bool* improved) {
+    etune_cu_ctx* c = s->ctx;
+    SOK(measure_energy(s, gen, 1));
+    SOK(etune_cu_candidate_ids(c, s->plan, gen, 1, s->ids));
+    uint64_t id = 0, g = 0;
+    double l = 0, p = 0, e = 0;
+    SCU(cudaMemcpyAsync(&id, s->ids, 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(&g, gen, 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(&l, s->mlat, 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(&p, s->mpow, 8, cudaMemcpyDeviceToHost, c->stream));
+    SCU(cudaMemcpyAsync(&e, s->men, 8, cudaMemcpyDeviceToHost, c->stream));
+    SOK(etune_cu_synchronize(c, nullptr));
+    const double before = s->have_best ? s->best_lat : std::numeric_limits<double>::infinity();
+    if (!s->have_best || l < s->best_lat || (l == s->best_lat && id < s->best_id)) {
+        s->have_best = true;
+        s->best_lat = l;
+        s->best_en = e;
+        s->best_pow = p;
+        s->best_id = id;
+        s->best_genome = g;
+    }
+    *improved = s->best_lat < before * (1.0 - s->cfg.improve_rel);
+    return ETUNE_OK;
+}
+
 // best-so-far over the n measured records of this round
 etune_status update_best(etune_cu_search* s, const uint64_t* gen, int64_t n, bool* improved) {
     etune_cu_ctx* c = s->ctx;
@@ -415,6 +445,16 @@ etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* rep
     SOK(measure_latency(s, s->pop, G, s->lat));
     SOK(etune_cu_topk(c, s->lat, G, M, s->idx));  // LatencyEvaAndPick(Kernel_generation, M)
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
+    if (s->cfg.latency_only) {  // run_latency_only: no energy model at all
+        SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(M) * 8, cudaMemcpyDeviceToDevice, c->stream));
+        s->np = M;
+        s->round = 0;
+        s->cumulative = 1;
+        bool improved = false;
+        SOK(update_best_latency(s, s->mgen, &improved));
+        fill_report(s, s->k5, std::numeric_limits<double>::quiet_NaN(), 1, now_ms() - t0, rep);
+        return ETUNE_OK;
+    }
     SOK(measure_energy(s, s->mgen, M));
     SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(M) * 8, cudaMemcpyDeviceToDevice, c->stream));
     s->np = M;
@@ -462,6 +502,18 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     SOK(etune_cu_topk(c, s->lat, G, M, s->idx));
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
     stage("latency");
+    if (s->cfg.latency_only) {  // steps 3-8 replaced by parent selection on latency
+        const int64_t np = (M + 1) / 2;  // the ceil(M/2) fastest (mgen is latency-sorted)
+        SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(np) * 8, cudaMemcpyDeviceToDevice, c->stream));
+        s->np = np;
+        s->round = r;
+        s->cumulative += 1;
+        bool improved = false;
+        SOK(update_best_latency(s, s->mgen, &improved));
+        s->stall = improved ? 0 : s->stall + 1;
+        fill_report(s, s->k5, std::numeric_limits<double>::quiet_NaN(), 1, now_ms() - t0, rep);
+        return ETUNE_OK;
+    }
     // 3. EnergyModelEvaAndPick(Kernel_M, EnergyModel, k*M)
     SOK(etune_cu_score(c, s->plan, s->model, s->mgen, M, s->mpred, nullptr));
     const int64_t km = ceil_fifths(s->k5, M);

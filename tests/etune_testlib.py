@@ -197,12 +197,13 @@ class Oracle(_Lib):
 
     def run_search(self, op, M, G, seed, max_rounds=10, patience=5, k_init_fifths=5, inverted=0, num_trees=100,
                    max_depth=6, mu_db=20.0, improve_rel=0.001, rates=(0.85, 0.10, 0.05), lr=0.1,
-                   min_leaf_weight=1e-3, reg_lambda=1.0, dev=None, limits=None):
+                   min_leaf_weight=1e-3, reg_lambda=1.0, dev=None, limits=None, latency_only=0):
         """Algorithm 1 restatement -> (reports_int n x 6, reports_f64 n x 4, parent schedules)."""
         d = dict(DEFAULT_DEVICE)
         d.update(dev or {})
         dev12 = np.array([d[k] for k in DEVICE_FIELDS], np.float64)
-        cfg_i = np.array([M, G, k_init_fifths, max_rounds, patience, inverted, num_trees, max_depth], np.int64)
+        cfg_i = np.array([M, G, k_init_fifths, max_rounds, patience, inverted, num_trees, max_depth, latency_only],
+                         np.int64)
         cfg_d = np.array([mu_db, improve_rel, *rates, lr, min_leaf_weight, reg_lambda], np.float64)
         cap = max_rounds + 1
         ri = np.zeros((cap, 6), np.int64)

@@ -97,3 +97,24 @@ def test_replay_search_reproduces_sim_search(oracle, ctx, capi):
     with pytest.raises(capi.EtuneError) as e:
         capi.Search(plan, capi.search_config(backend=2, **kw)).run()  # no log attached
     assert e.value.code == 14
+
+
+@pytest.mark.parametrize("text,kw", [("mm:1,64,64,64", dict(M=64, G=256, seed=42, max_rounds=6)),
+                                     ("conv:1,56,56,64,64,3,1,1", dict(M=256, G=1024, seed=7, max_rounds=5))])
+def test_latency_only_search_vs_oracle(oracle, ctx, capi, text, kw):
+    """run_latency_only: the same loop with steps 3-8 replaced by parent
+    selection on latency; every report and the final parents equal the restatement's."""
+    op = parse_op(text)
+    kw = dict(kw)
+    M, G, seed = kw.pop("M"), kw.pop("G"), kw.pop("seed")
+    ri, rd, par = oracle.run_search(op, M, G, seed, latency_only=1, **kw)
+    plan = capi.Plan(ctx, op)
+    reps = capi.Search(plan, capi.search_config(M=M, generation_size=G, rng_seed=seed, latency_only=1, **kw)).run()
+    assert len(reps) == len(ri)
+    for r, a, b in zip(reps, ri, rd):
+        assert (r.round, r.k_before_fifths, r.k_after_fifths, r.measured, r.cumulative_measured) == tuple(a[:5])
+        assert r.best_id == np.int64(a[5]).view(np.uint64) and np.isnan(r.snr_db)
+        assert f64bits(r.best_latency_ms) == f64bits(b[1]) and f64bits(r.best_energy_mj) == f64bits(b[2])
+    s = capi.Search(plan, capi.search_config(M=M, generation_size=G, rng_seed=seed, latency_only=1, **kw))
+    s.run()
+    assert (plan.decode(s.parents()).cpu().numpy() == par).all()
