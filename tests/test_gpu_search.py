@@ -118,3 +118,32 @@ def test_latency_only_search_vs_oracle(oracle, ctx, capi, text, kw):
     s = capi.Search(plan, capi.search_config(M=M, generation_size=G, rng_seed=seed, latency_only=1, **kw))
     s.run()
     assert (plan.decode(s.parents()).cpu().numpy() == par).all()
+
+
+def _space(capi, ctx, oracle, text):
+    op = parse_op(text)
+    plan = capi.Plan(ctx, op)
+    g = plan.encode(torch.from_numpy(np.ascontiguousarray(oracle.enumerate(op))).cuda())
+    lat, pw, en, _ = (t.cpu().numpy() for t in plan.sim_measure(g))
+    return plan, lat, pw, en
+
+
+def test_spec_acceptance_search_optimality(oracle, ctx, capi):
+    """SPEC acceptance 6: on MM(1,16,16,16) the search's best measured energy is within 5 %
+    of the brute-force optimum over the whole space on >= 9 of 10 seeds."""
+    plan, _, _, en = _space(capi, ctx, oracle, "mm:1,16,16,16")
+    best = [capi.Search(plan, capi.search_config(M=64, generation_size=256, rng_seed=s, max_rounds=30)).run()[-1]
+            .best_energy_mj for s in range(10)]
+    assert sum(b <= 1.05 * en.min() for b in best) >= 9
+
+
+def test_spec_acceptance_measurement_budget_and_correlation(oracle, ctx, capi):
+    """SPEC acceptance 8: cumulative energy measurements over 15 rounds at mu = 20 dB are
+    <= 0.55x a forced k = 1.0 run; 9: Spearman(latency, power) < 0 over MM(1,64,64,64)."""
+    from scipy.stats import spearmanr
+    plan, lat, pw, _ = _space(capi, ctx, oracle, "mm:1,64,64,64")
+    kw = dict(M=64, generation_size=256, rng_seed=3, max_rounds=15, patience=1 << 30)
+    dyn = capi.Search(plan, capi.search_config(mu_db=20.0, **kw)).run()[-1].cumulative_measured
+    forced = capi.Search(plan, capi.search_config(mu_db=1e9, **kw)).run()[-1].cumulative_measured
+    assert forced == 64 * 16 and dyn <= 0.55 * forced
+    assert spearmanr(lat, pw).correlation < 0
