@@ -138,3 +138,19 @@ def test_train_megakernel_variant():
                         os.path.join(here, "test_gpu_train.py"), "-k", "not megakernel"],
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("text", ["mm:1,512,512,512", "mv:1,1,1000,2048", "conv:1,28,28,128,128,3,1,1"])
+def test_spec_acceptance_cost_model_quality(ctx, capi, text):
+    """SPEC acceptance 5 (Fig. 5 analog): a device-trained model on >= 500 SimBackend
+    samples ranks held-out candidates with Spearman >= 0.9."""
+    from scipy.stats import spearmanr
+    plan = capi.Plan(ctx, parse_op(text))
+    g = plan.sample_random(1000, 11)
+    _, _, en, _ = plan.sim_measure(g)
+    feats = plan.features(g)
+    m = capi.train(ctx, feats[:700].contiguous(), en[:700].contiguous(), with_loss=False)
+    pred = m.forest().predict(feats[700:].contiguous()).cpu().numpy()
+    rho = spearmanr(pred, en[700:].cpu().numpy()).correlation
+    print(f"{text}: held-out Spearman {rho:.4f}")
+    assert rho >= 0.9
