@@ -1166,6 +1166,20 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
             CU(cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming));
         }
     }
+    // When the caller's rows are pinned, every raw_every-th chunk skips the host narrowing:
+    // the copy engine moves its 96-byte rows as they are (the device encodes 8-byte
+    // fields) while the host pool narrows the next chunks, so copy engine and host
+    // memory bandwidth both work (ETUNE_E2E_RAW_EVERY, default 4; 0 disables).
+    static const int raw_every = [] {
+        const char* ev = std::getenv("ETUNE_E2E_RAW_EVERY");
+        return ev ? std::atoi(ev) : 4;
+    }();
+    bool pinned = false;
+    {
+        cudaPointerAttributes pa{};
+        pinned = cudaPointerGetAttributes(&pa, h_sched) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+    }
     // the caller's earlier work on the ctx stream happens-before this call's copies
     CU(cudaEventRecord(c->ev_done[0], c->stream));
     CU(cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
@@ -1181,10 +1195,15 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         auto* d_ids = reinterpret_cast<uint64_t*>(base + size_t(cap) * (sizeof(etune_schedule) + 16));
         void* h_rows = pin + size_t(b) * size_t(cap) * sizeof(etune_schedule);
         const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
-        if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));  // pinned buffer b read by chunk i-2's H2D
-        const int fb = pack_rows(c, h_sched + lo, m, h_rows);
+        const bool raw = pinned && raw_every > 0 && i % raw_every == 0 && n > chunk;
+        int fb = 8;
+        if (!raw) {
+            if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));  // pinned buffer b read by chunk i-2's H2D
+            fb = pack_rows(c, h_sched + lo, m, h_rows);
+        }
         if (i >= 2) CU(cudaStreamWaitEvent(c->h2d, c->ev_out[b], 0));  // buffer b drained by chunk i-2's D2H
-        CU(cudaMemcpyAsync(d_rows, h_rows, size_t(m) * 12 * size_t(fb), cudaMemcpyHostToDevice, c->h2d));
+        CU(cudaMemcpyAsync(d_rows, raw ? static_cast<const void*>(h_sched + lo) : h_rows,
+                           size_t(m) * 12 * size_t(fb), cudaMemcpyHostToDevice, c->h2d));
         CU(cudaEventRecord(c->ev_in[b], c->h2d));
         CU(cudaStreamWaitEvent(c->stream, c->ev_in[b], 0));
         CU(launch_encode_packed(c->lc(), p->d_blob, p->build.hdr.total, d_rows, fb, m, d_gen, lo));

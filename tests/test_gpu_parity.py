@@ -228,6 +228,12 @@ def test_score_host_row_widths(golden, oracle, ctx, capi, text, n, pinned):
     with pytest.raises(capi.EtuneError) as e:
         fo.score_host(plan, s, pred, hid)
     assert e.value.code == 4 and e.value.index == bad
+    # an illegal row in the first chunk (copied raw, without host narrowing, when pinned)
+    s[bad, 1] = s[bad + 1, 1]
+    s[5, 1] = -1
+    with pytest.raises(capi.EtuneError) as e:
+        fo.score_host(plan, s, pred, hid)
+    assert e.value.code == 4 and e.value.index == 5
 
 
 @pytest.mark.parametrize("depth,smooth", [(8, False), (6, True)])
