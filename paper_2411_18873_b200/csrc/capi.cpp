@@ -1141,7 +1141,12 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
     // on chunk i-1; then H2D of chunk i (copy-in stream) overlaps encode+score of chunk
     // i-1 (ctx stream) and D2H of chunk i-2 (copy-out stream).  One synchronisation at
     // the end.
-    const int64_t chunk = int64_t(1) << 17;
+    static const int chunk_log2 = [] {  // ETUNE_E2E_CHUNK_LOG2 (diagnostic), default 2^17 rows
+        const char* ev = std::getenv("ETUNE_E2E_CHUNK_LOG2");
+        const int v = ev ? std::atoi(ev) : 17;
+        return v < 12 ? 12 : v > 22 ? 22 : v;
+    }();
+    const int64_t chunk = int64_t(1) << chunk_log2;
     const size_t per = sizeof(etune_schedule) + 8 + 8 + 8;  // rows (widest), genome, pred, id
     const int64_t cap = n < chunk ? n : chunk;
     if (etune_status st = ensure_io(c, 2 * size_t(cap) * per)) return st;
