@@ -1,26 +1,34 @@
-"""Benchmark: candidate schedules scored per second and search-round latency (BASELINE.json metric).
+"""Benchmark: candidate schedules scored/sec and search-round latency (BASELINE.json metric).
 
-Step = one pass of the hot path over one batch: fused score (features -> 100-tree
-energy model -> prediction + candidate id) of the rank's population shard, then
-"keep the best": top-k by (score, index); for N>1 the per-shard top-k records are
-all-gathered over NCCL and merged identically on every rank.
+Step = one pass of the hot path over one batch: score the rank's population shard with the
+energy cost model (features -> 100-tree GBDT -> prediction + candidate id) and keep the best,
+top-k by (prediction, index); for N>1 the per-shard top-k records are all-gathered over NCCL
+and merged identically on every rank.
 
     python bench.py [--gpus N --steps K --warmup W]            # our B200 path
-    python bench.py --impl reference [--gpus N ...]            # reference CPU path
+    python bench.py --impl reference [--gpus N ...]            # the reference's CPU path
     torchrun --nproc-per-node N bench.py --gpus N ...          # N>1
 
 Workload (config.workload): the ResNet-50 3x3 conv layer of BASELINE configs[1]
-(conv:1,56,56,64,64,3,1,1), population 2^20 per GPU (north_star / configs[3] top
-size), bred exactly like SURVEY §8(d): reproduce(sample_random(op,1024,42), 2^20,
-GeneticRates{}, seed 7); model = the reference-trained 100-tree forest on
-sample_random(op,2048,1234) (tests/golden fixture).  L2: 16 distinct population
-buffers (384 MB incl. outputs) are cycled so no step reads another's data from the
-126 MB L2.
+(conv:1,56,56,64,64,3,1,1), population 2^20 per GPU (north_star / configs[3] top size), bred
+exactly like SURVEY §8(d): reproduce(sample_random(op,1024,42), 2^20, GeneticRates{}, seed 7 +
+rank); model = the reference-trained 100-tree forest on sample_random(op,2048,1234)
+(tests/golden fixture).  L2: 16 distinct population buffers (384 MB incl. outputs) are cycled
+so no step reads another's data from the 126 MB L2.
 
-Also reported: e2e (the same scoring through the reference-facing C-ABI call on HOST
-Schedule[] buffers, H2D/D2H inside the timed region), search_round_latency (Algorithm 1
-rounds of BASELINE configs[1]: generation 16384, M 4096, on the device), roofline of the
-score kernel and the reference CPU path (cpu_baseline).
+The JSON line also carries:
+  fresh_model   the same step with a model the library has never seen: forest created from the
+                host arrays, compiled on the device (row table), scored + selected, destroyed
+  sweep         configs[3]: populations 2^14 .. 2^20, frozen and fresh-model steps
+  e2e           the reference-facing call on HOST Schedule rows (pageable, like the reference's
+                std::vector<Candidate>), H2D/D2H inside the timed region: etune_cu_score_select_host
+                (predictions + top-k back); the pinned-buffer figure beside it
+  search_round_latency   Algorithm 1 rounds of BASELINE configs[1] on the device, with the
+                reference's own single-threaded train + reproduce + predict of one such round
+                timed on the host beside it (cpu_round)
+  roofline      the step kernel (score_select_rows_kernel) against the measured HBM peak
+  cpu_baseline  the reference's CPU path (oracle/_ref, unmodified sources) on all host threads:
+                extract_features + predict + the k best by (prediction, index) via partial_sort
 """
 from __future__ import annotations
 
@@ -28,7 +36,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -44,7 +51,7 @@ MODEL_KEY = "c2_r50_conv3x3"
 METRIC = "candidate schedules scored/sec"
 UNIT = "candidates/s"
 # algorithmic bytes per candidate, score mode: 48 B schedule in (12 x int32 SoA) + 8 B f64
-# prediction + 8 B u64 id out.  This design's population is an 8-byte genome, so the kernel itself moves
+# prediction + 8 B u64 id out.  This design's population is an 8-byte genome, so the kernel itself must move
 # DESIGN_BYTES (8 in + 16 out); both fractions are reported.
 ALGO_BYTES = 64
 DESIGN_BYTES = 24
@@ -67,6 +74,7 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="target CPU-baseline sample duration")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-search", action="store_true", help="skip the search-round latency measurement")
     p.add_argument("--search-rounds", type=int, default=5)
     return p.parse_args()
@@ -110,40 +118,44 @@ def forest_json(f) -> str:
                        "base_score": f.base_score, "reference_energy_mj": 1.0, "trees": trees})
 
 
-def cpu_score_runner():
-    """Returns (kind, fn(op, sched) -> preds, threads).  Prefers the unmodified reference
-    (oracle/_ref) over the restatement (oracle/lib)."""
+def cpu_select_runner(k: int):
+    """Returns (kind, fn(op, sched) -> (preds, top-k idx), threads): the reference's scoring + keep-the-best
+    on every host thread.  Prefers the unmodified reference (oracle/_ref) over the restatement (oracle/lib)."""
     from etune_testlib import Oracle, RefLib, have_ref
     forest = load_forest()
     threads = cpu_threads()
     if have_ref():
         R = RefLib()
         model = R.model_from_json(forest_json(forest))
-        return "reference", (lambda op, s: model.score_threads(op, s, threads)), threads
+        return "reference", (lambda op, s: model.score_select_threads(op, s, threads, min(k, len(s)))), threads
     O = Oracle()
-    return "port", (lambda op, s: O.score_threads(op, s, forest, threads)), threads
+
+    def port(op, s):
+        p = O.score_threads(op, s, forest, threads)
+        kk = min(k, len(p))
+        part = np.argpartition(p, kk - 1)[:kk] if kk < len(p) else np.arange(len(p))
+        return p, part[np.lexsort((part, p[part]))]
+    return "port", port, threads
 
 
-def time_cpu(op, sched, target_s: float):
-    """Bounded CPU sample: whole passes over (a prefix of) the population until
-    ~target_s of work has been timed."""
-    kind, fn, threads = cpu_score_runner()
+def time_cpu(op, sched, target_s: float, k: int):
+    """Bounded CPU sample: whole passes over (a prefix of) the population until ~target_s of work."""
+    kind, fn, threads = cpu_select_runner(k)
     m = min(len(sched), 20000)
     t0 = time.perf_counter()
     fn(op, sched[:m])
     rate = m / max(time.perf_counter() - t0, 1e-9)
-    total = int(max(m, rate * target_s))
+    per = int(min(len(sched), max(m, rate * target_s / 4)))
     done, dt = 0, 0.0
-    while done < total:
-        chunk = sched[: min(len(sched), total - done)]
+    while dt < target_s * 0.75 and done < 4 * per:
         t0 = time.perf_counter()
-        fn(op, chunk)
+        fn(op, sched[:per])
         dt += time.perf_counter() - t0
-        done += len(chunk)
+        done += per
     return {"value": done / dt, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"{done} candidates (passes over the bench population, {OP_TEXT}); the reference's "
-                      f"extract_features + EnergyModel::predict per candidate over {threads} std::threads; "
-                      f"{dt:.1f} s"}
+            "sample": f"{done} candidates in passes of {per} over the bench population ({OP_TEXT}): the reference's "
+                      f"extract_features + EnergyModel::predict per candidate and the {k} best by (prediction, index) "
+                      f"(per-thread std::partial_sort + merge) over {threads} std::threads; {dt:.1f} s"}
 
 
 class ClockSampler:
@@ -184,6 +196,7 @@ class ClockSampler:
             self.sample()
 
     def __enter__(self):
+        self.stop.clear()
         self.t = threading.Thread(target=self._loop, daemon=True)
         self.t.start()
         return self
@@ -202,7 +215,7 @@ def run_reference(args):
     if rank != 0:
         return
     op, sched = make_population(args.pop)
-    kind, fn, threads = cpu_score_runner()
+    kind, fn, threads = cpu_select_runner(args.k)
     # bounded sample per step so the whole run ends in a few minutes
     m = min(len(sched), 20000)
     t0 = time.perf_counter()
@@ -215,13 +228,12 @@ def run_reference(args):
     for s in range(args.steps):
         lo = (s * per_step) % max(1, len(sched) - per_step)
         t0 = time.perf_counter()
-        preds = fn(op, sched[lo:lo + per_step])
-        order = np.lexsort((np.arange(len(preds)), preds))[: args.k]  # keep the best (score, index)
+        fn(op, sched[lo:lo + per_step])
         times.append(time.perf_counter() - t0)
-        del order
     value = per_step * len(times) / sum(times)
     sample = (f"{per_step} candidates/step of the bench population ({OP_TEXT}): the reference's "
-              f"extract_features + EnergyModel::predict over {threads} threads + top-{args.k}")
+              f"extract_features + EnergyModel::predict and the {args.k} best by (prediction, index) "
+              f"(std::partial_sort per thread + merge) over {threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
@@ -234,6 +246,38 @@ def run_reference(args):
     }), flush=True)
 
 
+def cpu_round_baseline(rounds_info):
+    """The reference's own work of one search round (train and reproduce timed
+    single-threaded), at the sample count of the median GPU round: EnergyModel::train on that
+    many SimBackend samples (energies from the oracle's SPEC:317 formula), reproduce(2048 parents
+    -> 16384), extract_features + predict of the 4096 kept + keep-the-best.  oracle/_ref only."""
+    from etune_testlib import Oracle, RefLib, have_ref, parse_op
+    if not have_ref():
+        return None
+    R, O = RefLib(), Oracle()
+    op = parse_op(OP_TEXT)
+    n_train = int(rounds_info.get("median_samples") or 8192)
+    s, _ = O.sample_random(op, n_train, 1234)
+    f = O.features(op, s)
+    en = O.sim_measure(op, s)[:, 2]
+    t0 = time.perf_counter()
+    model = R.train(f, en, num_trees=100, max_depth=6)
+    t_train = time.perf_counter() - t0
+    par = s[:2048]
+    t0 = time.perf_counter()
+    kids = R.reproduce(op, par, 16384, 43)[0]
+    t_repro = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    model.score_select_threads(op, kids[:4096], 1, 2048)
+    t_pred = time.perf_counter() - t0
+    total = t_train + t_repro + t_pred
+    return {"value": total * 1e3, "unit": "ms", "cores": 1, "kind": "reference",
+            "train_ms": t_train * 1e3, "reproduce_ms": t_repro * 1e3, "predict_select_ms": t_pred * 1e3,
+            "sample": f"EnergyModel::train on {n_train} SimBackend samples (the median GPU round's sample count), "
+                      f"reproduce(2048 parents -> 16384), extract_features + predict + top-2048 of 4096; "
+                      f"one thread (the reference is single-threaded); latency filter and measurement excluded"}
+
+
 def search_round_latency(ctx, capi, rounds: int):
     """Algorithm-1 round latency on the device: BASELINE configs[1] search
     (conv R50 3x3, generation 16384, M = 4096, SimBackend), median wall ms of `rounds`
@@ -244,9 +288,11 @@ def search_round_latency(ctx, capi, rounds: int):
     cfg = capi.search_config(M=4096, generation_size=16384, rng_seed=42, max_rounds=rounds, patience=1 << 30)
     s = capi.Search(plan, cfg)
     init = s.initial()
-    ms = [s.round().wall_ms for _ in range(rounds)]
+    reps = [s.round() for _ in range(rounds)]
+    ms = [r.wall_ms for r in reps]
+    samples = sorted(int(r.cumulative_measured) for r in reps)
     return {"value": statistics.median(ms), "unit": "ms", "rounds": rounds, "per_round_ms": [round(x, 3) for x in ms],
-            "initial_round_ms": round(init.wall_ms, 3),
+            "initial_round_ms": round(init.wall_ms, 3), "median_samples": samples[len(samples) // 2],
             "config": "conv:1,56,56,64,64,3,1,1 generation 16384, M 4096, k from 1.0, mu 20 dB, SimBackend, "
                       "100-tree retrain on all accumulated samples every round"}
 
@@ -294,19 +340,28 @@ def run_ours(args):
     top = torch.empty(K, dtype=torch.int64, device="cuda")
     top_sc = torch.empty(K, dtype=torch.float64, device="cuda")
 
-    def step(i):
+    def step(fo, i, m=n):
         b = i % nb
+        g = genomes[b] if m == n else genomes[b][:m]
+        kk = min(K, m)
         if world > 1:  # fused score + local top-k -> ncclAllGather of (score, global idx) -> identical merge
-            forest.score_select_sharded(plan, genomes[b], rank * n, K, preds[b], top, sc=top_sc, ids=ids[b])
+            fo.score_select_sharded(plan, g, rank * m, kk, preds[b], top, sc=top_sc, ids=ids[b])
         else:  # fused score + top-k (etune_cu_score_select)
-            forest.score_select(plan, genomes[b], K, preds[b], top, ids=ids[b])
+            fo.score_select(plan, g, kk, preds[b], top, ids=ids[b])
+
+    # compile the row table of the bench model (timed: device events around the asynchronous compile)
+    e_c0, e_c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_c0.record(stream)
+    forest.compile(plan)
+    e_c1.record(stream)
+    torch.cuda.synchronize()
+    compile_ms = e_c0.elapsed_time(e_c1)
 
     # NVML is initialised before the warm-up: its first queries perturb a running GPU
-    # (measured: one ~25 % slower timed loop when nvmlInit ran inside it)
     clk = ClockSampler(local)
     clk.sample()
     for i in range(args.warmup):
-        step(i)
+        step(forest, i)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -319,18 +374,17 @@ def run_ours(args):
         ev0.record(stream)
         clk.sample()
         for i in range(args.steps):
-            step(args.warmup + i)
+            step(forest, args.warmup + i)
         ev1.record(stream)
         clk.sample()
         torch.cuda.synchronize()
     launches = capi.lib().etune_cu_launch_count() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
-    # kernel split: a separate pass with CUDA events around the score kernel and the
-    # selection kernels of each call (events serialise the PDL overlap, so the timed
-    # loop above runs without them)
+    # kernel duration: CUDA events around the step kernel of each call (a separate pass: the events
+    # separate the launches the timed loop runs back to back)
     capi.profile_score(ctx, True)
     for i in range(args.steps):
-        step(args.warmup + args.steps + i)
+        step(forest, args.warmup + args.steps + i)
     _, score_ms, select_ms, score_calls = capi.profile_score(ctx, False)
     kernel_ms = score_ms / max(score_calls, 1)
     select_ms = select_ms / max(score_calls, 1)
@@ -341,45 +395,108 @@ def run_ours(args):
         dist.barrier()
     value = world * n / (ms / 1e3)
 
-    # ---- e2e through the reference-facing C-ABI call with host buffers
+    # ---- fresh model: every step a model the library has not seen (created from the host arrays,
+    # compiled on the device, scored + selected, destroyed); host wall clock around synchronised steps
+    def fresh_steps(m, reps):
+        walls = []
+        for i in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            fo = capi.Forest.from_flat(ctx, forest_flat)
+            step(fo, i, m)
+            del fo
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        return statistics.median(walls[1:] if len(walls) > 2 else walls)
+
+    fresh_s = fresh_steps(n, 12)
+    if world > 1:
+        t = torch.tensor([fresh_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        fresh_s = t.item()
+    fresh = {"value": world * n / fresh_s, "unit": UNIT, "ms_per_step": fresh_s * 1e3, "compile_ms": compile_ms,
+             "what": "per step: etune_cu_forest_create from the host arrays (H2D of the nodes), the device compile "
+                     "(Kuv classes, row predictions, rows in prediction order), score_select, destroy; host wall "
+                     "clock around a synchronised step, median of 11"}
+
+    # ---- configs[3] sweep 2^14 .. 2^20 (frozen and fresh model)
+    sweep = []
+    if not args.no_sweep and world == 1:
+        for lg in range(14, 21):
+            m = 1 << lg
+            if m > n:
+                break
+            reps = 50
+            for i in range(3):
+                step(forest, i, m)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for i in range(reps):
+                step(forest, i, m)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            fm = a0.elapsed_time(a1) / reps
+            fs = fresh_steps(m, 6)
+            sweep.append({"population": m, "frozen_ms": fm, "frozen_value": m / (fm / 1e3),
+                          "fresh_ms": fs * 1e3, "fresh_value": m / fs})
+
+    # ---- e2e through the reference-facing C-ABI call with HOST buffers
     e2e = None
     if not args.no_e2e:
-        h_sched = torch.from_numpy(sched).pin_memory()
-        h_pred = torch.empty(n, dtype=torch.float64).pin_memory()
-        h_ids = torch.empty(n, dtype=torch.int64).pin_memory()
-        hs, hp, hi = h_sched.numpy(), h_pred.numpy(), h_ids.numpy()
-        for _ in range(2):
-            forest.score_host(plan, hs, hp, hi)
-        if world > 1:
-            dist.barrier()
-        reps = max(3, args.steps // 4)
-        t0 = time.perf_counter()
-        for _ in range(reps):
-            forest.score_host(plan, hs, hp, hi)
-        dt = (time.perf_counter() - t0) / reps
-        if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dt = t.item()
-        # score_host narrows each row to the smallest field width holding it (u16 here); with a
-        # pinned caller buffer every 4th 2^17-row chunk is copied raw (96 B/row) instead
-        fb = 2 if (sched.min() >= 0 and sched.max() < 1 << 16) else 4 if sched.max() < 1 << 32 else 8
-        chunk, raw_every = 1 << int(os.environ.get("ETUNE_E2E_CHUNK_LOG2", "17")), \
-            int(os.environ.get("ETUNE_E2E_RAW_EVERY", "4"))
-        h2d = 0
-        for i, lo in enumerate(range(0, n, chunk)):
-            m = min(chunk, n - lo)
-            raw = raw_every > 0 and i % raw_every == 0 and n > chunk
-            h2d += m * 12 * (8 if raw else fb)
-        e2e = {"value": world * n / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(n * 16), "ms_per_step": dt * 1e3,
-               "api": "etune_cu_score_host (host Schedule[] 96 B/row -> host-pool narrowing into pinned "
-                      "staging (every 4th chunk copied raw from the pinned caller buffer) -> H2D -> "
-                      "encode+validate -> score -> D2H, chunked 3-stream pipeline)"}
+        h_pred = np.zeros(n)
+        h_idx = np.zeros(K, np.int64)
+        pageable = np.ascontiguousarray(sched)
+        pinned = torch.from_numpy(sched).pin_memory().numpy()
+
+        def e2e_time(hs, reps):
+            for _ in range(2):
+                forest.score_select_host(plan, hs, K, h_idx, h_pred)
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                forest.score_select_host(plan, hs, K, h_idx, h_pred)
+            dt = (time.perf_counter() - t0) / reps
+            if world > 1:
+                t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+                dt = t.item()
+            return dt
+
+        def h2d_bytes(pinned_rows):
+            # the host pool narrows each 2^17-row chunk to the smallest field width holding it (u16 here);
+            # with a pinned caller buffer every 4th chunk is copied raw (96 B/row) instead
+            fb = 2 if (sched.min() >= 0 and sched.max() < 1 << 16) else 4 if sched.max() < 1 << 32 else 8
+            chunk, raw_every = 1 << int(os.environ.get("ETUNE_E2E_CHUNK_LOG2", "17")), \
+                int(os.environ.get("ETUNE_E2E_RAW_EVERY", "4"))
+            tot = 0
+            for i, lo in enumerate(range(0, n, chunk)):
+                mm = min(chunk, n - lo)
+                raw = pinned_rows and raw_every > 0 and i % raw_every == 0 and n > chunk
+                tot += mm * 12 * (8 if raw else fb)
+            return tot
+
+        reps = max(3, args.steps // 8)
+        dt_pg = e2e_time(pageable, reps)
+        dt_pin = e2e_time(pinned, reps)
+        e2e = {"value": world * n / dt_pg, "unit": UNIT, "h2d_bytes_per_step": int(h2d_bytes(False)),
+               "d2h_bytes_per_step": int(n * 8 + K * 8), "ms_per_step": dt_pg * 1e3, "input": "pageable",
+               "pinned": {"value": world * n / dt_pin, "ms_per_step": dt_pin * 1e3,
+                          "h2d_bytes_per_step": int(h2d_bytes(True))},
+               "api": f"etune_cu_score_select_host (host Schedule[] 96 B/row -> host-pool narrowing into pinned "
+                      f"staging -> H2D -> encode+validate -> score -> predictions D2H; top-{K} by (prediction, "
+                      f"index) on the device -> indices D2H; chunked 3-stream pipeline)"}
 
     round_latency = None
+    cpu_round = None
     if rank == 0 and world == 1 and not args.no_search:
         round_latency = search_round_latency(ctx, capi, args.search_rounds)
+        if not args.no_cpu_baseline:
+            try:
+                cpu_round = cpu_round_baseline(round_latency)
+            except Exception as e:  # the baseline is reported, never required
+                cpu_round = {"unavailable": str(e)[:200]}
 
     if rank != 0:
         if world > 1:
@@ -393,13 +510,9 @@ def run_ours(args):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = n * ALGO_BYTES / (kernel_ms / 1e3) / 1e9
     traffic = None
-    sm_bound = None
-    try:  # DRAM bytes per launch + the binding SM unit from the committed ncu --set full capture
+    try:  # DRAM bytes per launch from the committed ncu --set full capture
         t = json.load(open(os.path.join(ROOT, "profiles", "score_kernel_traffic.json")))
         traffic = int(t["dram_bytes_read_per_launch"]) + int(t["dram_bytes_write_per_launch"])
-        if "binding_unit" in t:
-            sm_bound = {"unit": t["binding_unit"], "pct_of_peak": t["l1tex_pct_of_peak"],
-                        "issue_active_pct": t["issue_active_pct"], "source": t["source"]}
     except Exception:
         pass
     line = {
@@ -407,16 +520,17 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload(K), "op": OP_TEXT, "population_per_gpu": n,
-                   "implementation": "etune_cu_score_select: keyed score kernel (per candidate one 64-byte row of "
-                                     "5-bit exit slots per (tiling triple, Kuv class) from an L2-resident key table, "
-                                     "two 256-bit loads; leaf words from shared memory; + ids, + selection histogram) "
-                                     "-> bucket filter -> rank selection, PDL-chained",
-                   "k": K, "model": "reference-trained 100-tree depth-6 GBDT (tests/golden c2 fixture)",
+                   "implementation": "etune_cu_score_select on the device-compiled row table: ONE cooperative "
+                                     "kernel per step (genome -> (tiling-triple key, Kuv class) row -> prediction "
+                                     "+ id, per-row candidate counts; k-th prediction from the rows in prediction "
+                                     "order; ties by index; k sorted)",
+                   "k": K, "model": "reference-trained 100-tree depth-6 GBDT (tests/golden c2 fixture), frozen "
+                                    "(compiled once; fresh_model times a new model every step)",
                    "parallelism": f"dp{world} (population sharded; NCCL all-gather of per-shard top-k records "
                                   f"inside the C ABI)",
                    "l2": f"{nb} distinct population buffers cycled ({nb * n * 24 / 2**20:.0f} MB > 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                     "traffic": traffic, "kernel": "score_keyed_kernel", "kernel_ms": kernel_ms,
+                     "traffic": traffic, "kernel": "score_select_rows_kernel", "kernel_ms": kernel_ms,
                      "algorithmic_bytes_per_candidate": ALGO_BYTES,
                      "algorithmic_bytes_source": "SURVEY.md §8(d) score mode: 48 B schedule (12 x int32) in + 8 B "
                                                  "prediction + 8 B id out",
@@ -424,18 +538,25 @@ def run_ours(args):
                      "design_frac": n * DESIGN_BYTES / (kernel_ms / 1e3) / 1e9 / hbm,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else
                                     "fallback 6650 GB/s (B200_PROFILING.md)",
-                     "note": "SM-bound (issue + shared-memory pipe); per-candidate key-table row reads are "
-                             "L2-resident, not HBM; see profiles/",
-                     "select_ms": select_ms, "sm_bound": sm_bound},
+                     "note": "the step is this one kernel (score + select fused); design_frac is the HBM utilisation "
+                             "on the bytes it must move (8 B genome in, 8 B prediction + 8 B id out); row-table "
+                             "gathers and per-row counters are L2 traffic; see profiles/",
+                     "select_ms": select_ms},
+        "compile_ms": compile_ms,
+        "fresh_model": fresh,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if sweep:
+        line["sweep"] = sweep
     if e2e:
         line["e2e"] = e2e
     if round_latency:
         line["search_round_latency"] = round_latency
+        if cpu_round:
+            line["search_round_latency"]["cpu_round"] = cpu_round
     if not args.no_cpu_baseline and world == 1:
-        line["cpu_baseline"] = time_cpu(op, sched, args.cpu_seconds)
+        line["cpu_baseline"] = time_cpu(op, sched, args.cpu_seconds, K)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

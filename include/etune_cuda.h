@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define ETUNE_CUDA_ABI_VERSION 1
+#define ETUNE_CUDA_ABI_VERSION 2
 
 typedef enum etune_status {
     ETUNE_OK = 0,
@@ -271,7 +271,35 @@ etune_status etune_cu_profile_score(etune_cu_ctx* ctx, int on, double* pre_ms /*
                                     double* score_ms /*nullable*/, double* select_ms /*nullable*/,
                                     int64_t* calls /*nullable*/);
 
-/* Scoring form for populations of >= 2^16 candidates: 1 (default) = keyed path where the
+/* Scoring forms (all bit-identical; the choice only affects speed):
+ *  ROWS   the default for populations of >= 2^16 candidates per (forest, plan): the forest is
+ *         compiled ON THE DEVICE (three launches, no host work) into one prediction per
+ *         (tiling-triple key, Kuv class) row -- a candidate's prediction depends only on which
+ *         side of each threshold its features fall, and only f6/f7/f10 vary with (k_tile,
+ *         unroll, vectorize) -- so scoring is one 8-byte gather per candidate (rowtab.cu);
+ *  WALK   features + the reference tree walk per candidate (any forest; no compile);
+ *  CLASS / KEYED / KEYED_BYTE  the host-compiled QuickScorer forms of round 1 (forest.cpp).
+ * AUTO (default) = ROWS once the (forest, plan) has scored >= 2^16 candidates in total (or
+ * one call has), WALK before; CLASS tables when the operator's row table would exceed
+ * 2^25 rows. */
+#define ETUNE_FORM_AUTO 0
+#define ETUNE_FORM_ROWS 1
+#define ETUNE_FORM_WALK 2
+#define ETUNE_FORM_CLASS 3
+#define ETUNE_FORM_KEYED 4
+#define ETUNE_FORM_KEYED_BYTE 5
+etune_status etune_cu_forest_set_form(etune_cu_forest* forest, int form);
+/* Compiles the forest for the plan in the form the next large scoring call would use (ROWS:
+ * enqueued on the ctx stream, asynchronous; host forms: synchronous).  Lets a caller time
+ * or overlap the compile of a freshly trained model. */
+etune_status etune_cu_forest_compile(etune_cu_ctx* ctx, etune_cu_forest* forest, const etune_cu_plan* plan);
+/* Row-table diagnostics (synchronises the ctx stream): {tiling-triple keys, Kuv classes,
+ * rows, row-table bytes, thresholds on f10, f7, f6, legal (k, u, v) triples}; all zero when
+ * the table has not been compiled. */
+etune_status etune_cu_forest_rows_info(etune_cu_ctx* ctx, etune_cu_forest* forest, const etune_cu_plan* plan,
+                                       int64_t out[8]);
+/* Legacy selector (round 1), kept for the tests of the host-compiled forms: 1 = KEYED, 2 = KEYED_BYTE, 0 = CLASS.
+ * Scoring form for populations of >= 2^16 candidates: 1 (default) = keyed path where the
  * forest compiles to it (<= 128 trees of <= 32 leaves, <= 256 distinct non-Kuv masks per
  * Kuv tree): the full form (5-bit exit slots per (tiling triple, Kuv class), table
  * <= 64 MB) or else the byte form (per tiling triple); 2 = byte form only; 0 = class-table
@@ -280,7 +308,7 @@ etune_status etune_cu_forest_set_keyed(etune_cu_forest* forest, int mode);
 
 /* Which form scores populations of >= 2^16 candidates of this plan (compiling it now if
  * needed): 0 = class-table kernel, 1 = keyed byte form, 2 = keyed full form, 3 = the
- * general tree-walk kernel.  Diagnostic. */
+ * general tree-walk kernel, 4 = the row table.  Diagnostic. */
 etune_status etune_cu_forest_score_form(etune_cu_forest* forest, const etune_cu_plan* plan, int* form);
 
 /* Reference-facing end-to-end call with HOST buffers: schedules in the reference's
@@ -293,6 +321,16 @@ etune_status etune_cu_score_host(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                  int64_t n, double* h_pred, uint64_t* h_ids /*nullable*/,
                                  int64_t* first_bad /*nullable*/);
 
+/* The reference-facing "score the population and keep the best" with HOST buffers (the
+ * reference's predict_many + partial sort by (prediction, index)): schedules in
+ * the reference's 96-byte layout (pinned or pageable), all predictions back into h_pred
+ * (nullable) and the k best indices, sorted, into h_idx.  Same pipeline as etune_cu_score_host;
+ * the predictions stay on the device and the selection runs there, so only k indices come back
+ * besides the predictions.  ILLEGAL_SCHEDULE (with *first_bad) like etune_cu_score_host. */
+etune_status etune_cu_score_select_host(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                        etune_cu_forest* forest, const etune_schedule* h_sched,
+                                        int64_t n, int64_t k, double* h_pred /*nullable*/,
+                                        int64_t* h_idx, int64_t* first_bad /*nullable*/);
 /* Diagnostics of the per-plan forest compilation: {reference interior nodes, tests
  * folded for this operator, class->mask table entries, max leaves per tree, total
  * leaves, blob bytes, bitmask of feature channels still tested, trees}. */

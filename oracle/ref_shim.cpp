@@ -454,6 +454,57 @@ int ref_score_threads(const int64_t* op, const int64_t* sched, int64_t n, int nu
     GUARD_END
 }
 
+// The reference's scoring path followed by "keep the best" (the k lowest
+// predictions, ties by index -- SURVEY H3), both over `threads` std::threads: each thread
+// scores its contiguous chunk and keeps its chunk's k best by (prediction, index) with
+// std::partial_sort; the chunk winners (threads x k) are merged by one more partial_sort.
+// out_idx[0..k) sorted.  bench.py --impl reference times exactly this (like for like with
+// etune_cu_score_select).
+int ref_score_select_threads(const int64_t* op, const int64_t* sched, int64_t n, int num_sms, void* h,
+                             int threads, int64_t k, double* out_pred, int64_t* out_idx) {
+    GUARD_BEGIN
+    const OperatorSpec o = op_from(op);
+    const DeviceConfig dev = dev_with_sms(num_sms);
+    const EnergyModel& m = static_cast<RefModel*>(h)->model;
+    if (threads < 1) threads = 1;
+    if (k < 0 || k > n) throw ValidationError("need 0 <= k <= n");
+    using Rec = std::pair<double, int64_t>;
+    std::vector<std::vector<Rec>> best{size_t(threads)};
+    std::atomic<int> failed{0};
+    auto work = [&](int t, int64_t lo, int64_t hi) {
+        try {
+            std::vector<Rec> recs;
+            recs.reserve(size_t(hi - lo));
+            for (int64_t i = lo; i < hi; ++i) {
+                const double p = m.predict(extract_features(o, sched_from(sched + 12 * i), dev));
+                out_pred[i] = p;
+                recs.emplace_back(p, i);
+            }
+            const int64_t kk = std::min<int64_t>(k, hi - lo);
+            std::partial_sort(recs.begin(), recs.begin() + kk, recs.end());
+            recs.resize(size_t(kk));
+            best[size_t(t)] = std::move(recs);
+        } catch (...) {
+            failed = 1;
+        }
+    };
+    std::vector<std::thread> pool;
+    const int64_t chunk = (n + threads - 1) / threads;
+    for (int t = 0; t < threads; ++t) {
+        const int64_t lo = t * chunk;
+        const int64_t hi = std::min(n, lo + chunk);
+        if (lo >= hi) break;
+        pool.emplace_back(work, t, lo, hi);
+    }
+    for (auto& th : pool) th.join();
+    if (failed) throw IllegalSchedule("scoring failed in a worker thread");
+    std::vector<Rec> all;
+    for (auto& b : best) all.insert(all.end(), b.begin(), b.end());
+    std::partial_sort(all.begin(), all.begin() + k, all.end());
+    for (int64_t j = 0; j < k; ++j) out_idx[j] = all[size_t(j)].second;
+    GUARD_END
+}
+
 // ---- persistence formats (device.cpp:44-101, energy_model.cpp:372-420)
 // dev: double[11] in etune_device_config field order (constant_power_w ..
 // noise_sigma_rel), plus num_sms, rng_seed and name.

@@ -158,8 +158,12 @@ _SIGS = {
     "etune_cu_profile_score": (C.c_int, [_VP, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                          C.POINTER(C.c_double), C.POINTER(_I64)]),
     "etune_cu_forest_set_keyed": (C.c_int, [_VP, C.c_int]),
+    "etune_cu_forest_set_form": (C.c_int, [_VP, C.c_int]),
+    "etune_cu_forest_compile": (C.c_int, [_VP, _VP, _VP]),
+    "etune_cu_forest_rows_info": (C.c_int, [_VP, _VP, _VP, _PTR]),
     "etune_cu_forest_score_form": (C.c_int, [_VP, _VP, C.POINTER(C.c_int)]),
     "etune_cu_score_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _PTR, _PTR, C.POINTER(_I64)]),
+    "etune_cu_score_select_host": (C.c_int, [_VP, _VP, _VP, _PTR, _I64, _I64, _PTR, _PTR, C.POINTER(_I64)]),
     "etune_cu_topk": (C.c_int, [_VP, _PTR, _I64, _I64, _PTR]),
     "etune_cu_train": (C.c_int, [_VP, _PTR, _PTR, _I64, C.POINTER(BoostParams), _PTR, _PTR, _PTR, _PTR, _PTR, _PTR,
                                  _PTR, _PTR]),
@@ -484,11 +488,32 @@ class Forest:
         _check(lib().etune_cu_forest_set_keyed(self.h, int(mode)))
         return self
 
+    FORMS = {"auto": 0, "rows": 1, "walk": 2, "class": 3, "keyed": 4, "keyed-byte": 5}
+
+    def set_form(self, form: str):
+        """Scoring form (ETUNE_FORM_*): 'auto' (default: device-compiled row table for large
+        populations, tree walk for small ones), 'rows', 'walk', 'class', 'keyed', 'keyed-byte'."""
+        _check(lib().etune_cu_forest_set_form(self.h, self.FORMS[form]))
+        return self
+
+    def compile(self, plan: Plan):
+        """Compile for `plan` now (row table: enqueued on the ctx stream, asynchronous)."""
+        _check(lib().etune_cu_forest_compile(self.ctx.h, self.h, plan.h))
+        return self
+
+    def rows_info(self, plan: Plan) -> dict:
+        """Row-table diagnostics (synchronises): keys, Kuv classes, rows, bytes, thresholds on f10/f7/f6,
+        legal (k, u, v) triples."""
+        out = np.zeros(8, np.int64)
+        _check(lib().etune_cu_forest_rows_info(self.ctx.h, self.h, plan.h, out.ctypes.data))
+        keys = ("keys", "kuv_classes", "rows", "bytes", "thr_f10", "thr_f7", "thr_f6", "kuv_domain")
+        return dict(zip(keys, (int(x) for x in out)))
+
     def score_form(self, plan: Plan) -> str:
-        """Form that scores large populations of `plan`: 'class', 'keyed-byte', 'keyed-full' or 'walk'."""
+        """Form that scores large populations of `plan`: 'class', 'keyed-byte', 'keyed-full', 'walk' or 'rows'."""
         v = C.c_int(-1)
         _check(lib().etune_cu_forest_score_form(self.h, plan.h, C.byref(v)))
-        return ("class", "keyed-byte", "keyed-full", "walk")[v.value]
+        return ("class", "keyed-byte", "keyed-full", "walk", "rows")[v.value]
 
     def score_select(self, plan: Plan, genome, k: int, pred, idx, ids=None):
         """Fused score + keep-the-best (etune_cu_score_select) into preallocated tensors."""
@@ -510,6 +535,16 @@ class Forest:
         st = lib().etune_cu_score_host(self.ctx.h, plan.h, self.h, _ptr(sched), n, _ptr(pred), _ptr(ids),
                                        C.byref(bad))
         _check(st, bad.value)
+
+    def score_select_host(self, plan: Plan, sched: np.ndarray, k: int, idx: np.ndarray,
+                          pred: Optional[np.ndarray] = None):
+        """Score HOST schedules and keep the k best (etune_cu_score_select_host); idx int64[k] out."""
+        n = sched.shape[0]
+        bad = C.c_int64(-1)
+        st = lib().etune_cu_score_select_host(self.ctx.h, plan.h, self.h, _ptr(sched), n, int(k), _ptr(pred),
+                                              _ptr(idx), C.byref(bad))
+        _check(st, bad.value)
+        return idx
 
 
 def nvml_available(ctx: Context) -> bool:

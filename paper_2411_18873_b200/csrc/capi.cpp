@@ -39,6 +39,8 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->breed);
     cudaFree(c->shard);
     cudaFree(c->sel);
+    cudaFree(c->rowsel);
+    cudaFree(c->e2e);
     if (c->hpin) cudaFreeHost(c->hpin);
     c->pool.reset();
     for (auto& e : c->prof_ev)
@@ -335,26 +337,138 @@ bool use_keyed(const etune_cu_forest* f, const CompiledScore* cs, int64_t n) {
     return cs->keyed && f->keyed_mode != 0 && n >= kKeyedMinN && n < (int64_t(1) << 32);
 }
 
+// ------------------------------------------------------------ scoring forms
+// AUTO: the device-compiled row table (rowtab.cu) once the (forest, plan) has scored
+// kRowsMinN candidates (or one call brings that many); the tree walk before that (a model
+// scored once on a few thousand candidates -- the search loop's per-round model -- is
+// cheaper to walk than to tabulate).  Host-compiled forms only on request, or when the
+// operator's row table would be too large.
+constexpr int64_t kRowsMinN = int64_t(1) << 16;
+
+void free_rowtab(RowTab& rt, cudaStream_t st) {
+    cudaFreeAsync(rt.d_meta, st);
+    cudaFreeAsync(rt.d_clskuv, st);
+    cudaFreeAsync(rt.d_crep, st);
+    cudaFreeAsync(rt.d_rowpred, st);
+    cudaFreeAsync(rt.d_srows, st);
+    cudaFreeAsync(rt.d_rowgid, st);
+    rt = RowTab{};
+}
+
+void free_compiled(CompiledScore& cs) {
+    cudaFree(cs.d_blob);
+    cudaFree(cs.d_kblob);
+    cudaFree(cs.d_ktable);
+    cudaFree(cs.d_khash);
+    cs.d_blob = cs.d_kblob = cs.d_ktable = nullptr;
+    cs.d_khash = nullptr;
+}
+
+// Row table of (forest, plan), compiled on the device on first use: asynchronous on the ctx
+// stream, no host arithmetic and no synchronisation.
+etune_status ensure_rows(etune_cu_ctx* c, etune_cu_forest* f, const etune_cu_plan* p, RowTab** out) {
+    std::lock_guard<std::mutex> lock(f->mu);
+    auto it = f->rowtabs.find(p->serial);
+    if (it != f->rowtabs.end()) {
+        *out = &it->second;
+        return ETUNE_OK;
+    }
+    if (p->rows_cap <= 0)
+        return fail(ETUNE_ERR_UNSUPPORTED, "the operator's row table would exceed 2^25 rows (use another form)");
+    const int ndk = p->build.hdr.ndk;
+    const cudaStream_t st = c->stream;
+    RowTab rt;
+    void* scratch = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_meta), sizeof(RowTabMeta), st));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_clskuv), size_t(ndk) * 64 * 2, st));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_crep), size_t(p->kuv_domain) * 4, st));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_rowpred), size_t(p->rows_cap) * 8, st));
+    CU(cudaMallocAsync(&scratch, rowtab_scratch_bytes(f->nnodes), st));
+    const cudaError_t e = launch_rowtab_compile(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes,
+                                                f->nnodes, ndk, p->rows_cap, scratch, rt.d_meta, rt.d_clskuv,
+                                                rt.d_crep, rt.d_rowpred);
+    cudaFreeAsync(scratch, st);
+    if (e != cudaSuccess) {
+        free_rowtab(rt, st);
+        return cuda_fail(e, "launch_rowtab_compile");
+    }
+    // rows in prediction order and their groups (dense ranks) for the fused selection (device radix sort)
+    void* sscratch = nullptr;
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_srows), size_t(p->rows_cap) * 4, st));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_rowgid), size_t(p->rows_cap) * 4, st));
+    CU(cudaMallocAsync(&sscratch, rowtab_sort_scratch_bytes(p->rows_cap), st));
+    const cudaError_t e2 = launch_rowtab_sort(c->lc(), rt.d_meta, rt.d_rowpred, p->rows_cap, rt.d_srows, rt.d_rowgid,
+                                              sscratch);
+    cudaFreeAsync(sscratch, st);
+    if (e2 != cudaSuccess) {
+        free_rowtab(rt, st);
+        return cuda_fail(e2, "launch_rowtab_sort");
+    }
+    auto res = f->rowtabs.emplace(p->serial, rt);
+    *out = &res.first->second;
+    return ETUNE_OK;
+}
+
+struct Route {
+    int kind = 0;  // 0: tree walk, 1: host-compiled form (cs), 2: row table (rt)
+    CompiledScore* cs = nullptr;
+    RowTab* rt = nullptr;
+};
+
+bool walk_fits(const etune_cu_ctx* c, const etune_cu_plan* p) {
+    return p->build.hdr.total <= uint32_t(max_dynamic_smem(c->device));
+}
+
+// `n` = the population about to be scored; -1 = compile the form a large population would use
+etune_status route(etune_cu_ctx* c, etune_cu_forest* f, const etune_cu_plan* p, int64_t n, Route* r) {
+    int form = f->form;
+    if (form == ETUNE_FORM_AUTO && p->rows_cap > 0) {
+        bool have = false;
+        int64_t cum = 0;
+        {
+            std::lock_guard<std::mutex> lock(f->mu);
+            have = f->rowtabs.count(p->serial) != 0;
+            cum = (f->seen[p->serial] += std::max<int64_t>(n, 0));
+        }
+        if (have || n < 0 || n >= kRowsMinN || cum >= kRowsMinN || !walk_fits(c, p)) form = ETUNE_FORM_ROWS;
+        else form = ETUNE_FORM_WALK;
+    }
+    if (form == ETUNE_FORM_ROWS) {
+        r->kind = 2;
+        return ensure_rows(c, f, p, &r->rt);
+    }
+    if (form == ETUNE_FORM_WALK) {
+        if (!walk_fits(c, p)) return fail(ETUNE_ERR_UNSUPPORTED, "plan tables exceed shared memory");
+        r->kind = 0;
+        return ETUNE_OK;
+    }
+    // host-compiled forms (AUTO without a row table: the keyed form, as in round 1)
+    if (etune_status st = get_compiled(f, p, &r->cs, n)) return st;
+    if (etune_status st = ensure_keyed(f, p, r->cs, n < 0 ? kKeyedMinN : n)) return st;
+    r->kind = r->cs->walk ? 0 : 1;
+    return ETUNE_OK;
+}
+
 // Scoring pass of any compiled form; `ev` (nullable) = {start, before the score kernel,
 // after it} for etune_cu_profile_score.
-etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
+etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const Route& r,
                             const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
                             const SelHist& sel, const cudaEvent_t* ev) {
     if (ev) CU(cudaEventRecord(ev[0], c->stream));
-    if (cs->walk) {
-        if (ev) CU(cudaEventRecord(ev[1], c->stream));
+    if (ev) CU(cudaEventRecord(ev[1], c->stream));
+    if (r.kind == 0) {
         CU(launch_score_walk(c->lc(), p->d_blob, p->build.hdr.total, f->d_predict, f->predict_bytes, d_genome, n,
                              d_pred, d_ids));
-    } else if (use_keyed(f, cs, n)) {
-        if (ev) CU(cudaEventRecord(ev[1], c->stream));
-        // candidates in population order: each reads its own 112-byte key-table row (L2);
-        // grouping the population by key first was measured slower (the sort costs more
-        // than the broadcast rows save)
+    } else if (r.kind == 2) {
+        // one 8-byte gather per candidate from the row table; ids from the per-key FNV state
+        CU(launch_score_rows(c->lc(), p->d_blob, p->build.hdr.ndk, r.rt->d_clskuv, r.rt->d_meta, r.rt->d_rowpred,
+                             p->d_khash, d_genome, n, d_pred, d_ids, sel));
+    } else if (use_keyed(f, r.cs, n)) {
+        const CompiledScore* cs = r.cs;
         CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, cs->ktable_bytes, cs->d_khash, d_genome,
-                              nullptr, n,
-                              d_pred, d_ids, cs->keyed_per_sm, *cs->kparams, sel));
+                              nullptr, n, d_pred, d_ids, cs->keyed_per_sm, *cs->kparams, sel));
     } else {
-        if (ev) CU(cudaEventRecord(ev[1], c->stream));
+        const CompiledScore* cs = r.cs;
         CU(launch_score(c->lc(), cs->d_blob, cs->bytes, d_genome, n, d_pred, d_ids, cs->mask_bits, *cs->params,
                         cs->per_sm, sel));
     }
@@ -362,19 +476,9 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     return ETUNE_OK;
 }
 
-// Fused score + keep-the-best on one shard: the score kernel fills the selection
-// histogram, sel_filter/sel_finish (sort.cu) resolve the k lowest (score, index).
-// Forests on the tree-walk path and k > kSelMaxK use score + the cooperative top-k.
-etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const CompiledScore* cs,
-                                const uint64_t* d_genome, int64_t n, int64_t k, double* d_pred, uint64_t* d_ids,
-                                int64_t* d_idx) {
-    if (cs->walk || k > kSelMaxK || k == 0) {
-        if (etune_status st = score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, SelHist{}, nullptr)) return st;
-        if (k == 0) return ETUNE_OK;
-        if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
-        CU(launch_topk(c->lc(), d_pred, n, k, d_idx, c->scratch));
-        return ETUNE_OK;
-    }
+// Work area of the bucketed selection (sort.cu launch_select), its histogram and list counters
+// zeroed unless the previous sequence completed (the finish kernel leaves them zeroed).
+etune_status select_work(etune_cu_ctx* c, int64_t n, int64_t k) {
     const size_t need = select_scratch_bytes(n, k);
     if (c->sel_bytes < need) {
         if (c->sel) {
@@ -389,7 +493,61 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
     }
     if (c->sel_dirty) CU(cudaMemsetAsync(c->sel, 0, 8192, c->stream));  // histogram + list counters
     c->sel_dirty = true;
-    const SelHist sh{select_hist(c->sel), cs->sel_kmin, cs->sel_shift};
+    return ETUNE_OK;
+}
+
+// Fused score + keep-the-best on one shard: the score kernel fills the selection
+// histogram, sel_filter/sel_finish (sort.cu) resolve the k lowest (score, index).
+// Forests on the tree-walk path and k > kSelMaxK use score + the cooperative top-k.
+etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const Route& r,
+                                const uint64_t* d_genome, int64_t n, int64_t k, double* d_pred, uint64_t* d_ids,
+                                int64_t* d_idx) {
+    if (r.kind == 2 && k > 0 && k <= kSelMaxK) {  // one cooperative kernel: score, row counts, k-th, ties, sort
+        if (!c->rowsel) {
+            CU(cudaMalloc(&c->rowsel, rowsel_work_bytes()));
+            CU(cudaMemsetAsync(c->rowsel, 0, rowsel_work_bytes(), c->stream));
+        }
+        const bool prof = c->prof_on;
+        if (prof && c->prof_used == c->prof_ev.size()) {
+            std::array<cudaEvent_t, 4> e{};
+            for (cudaEvent_t& x : e) CU(cudaEventCreate(&x));
+            c->prof_ev.push_back(e);
+        }
+        const cudaEvent_t* ev = prof ? c->prof_ev[c->prof_used].data() : nullptr;
+        if (ev) {
+            CU(cudaEventRecord(ev[0], c->stream));
+            CU(cudaEventRecord(ev[1], c->stream));
+        }
+        const cudaError_t e =
+            launch_score_select_rows(c->lc(), p->d_blob, p->build.hdr.ndk, r.rt->d_clskuv, r.rt->d_meta,
+                                     r.rt->d_rowpred, r.rt->d_rowgid, p->rows_cap, p->d_khash, d_genome, n, k,
+                                     d_pred,
+                                     d_ids, d_idx, c->rowsel);
+        if (e == cudaSuccess) {
+            if (ev) {
+                CU(cudaEventRecord(ev[2], c->stream));
+                CU(cudaEventRecord(ev[3], c->stream));
+                ++c->prof_used;
+            }
+            return ETUNE_OK;
+        }
+        if (e != cudaErrorNotSupported) return cuda_fail(e, "launch_score_select_rows");
+        cudaGetLastError();  // population beyond the grid's registers: the bucketed selection below
+    }
+    if (r.kind == 0 || k > kSelMaxK || k == 0) {
+        if (etune_status st = score_dispatch(c, p, f, r, d_genome, n, d_pred, d_ids, SelHist{}, nullptr)) return st;
+        if (k == 0) return ETUNE_OK;
+        if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
+        CU(launch_topk(c->lc(), d_pred, n, k, d_idx, c->scratch));
+        return ETUNE_OK;
+    }
+    if (etune_status st = select_work(c, n, k)) return st;
+    SelHist sh{select_hist(c->sel), 0, 0};
+    if (r.kind == 2) sh.dbounds = r.rt->d_meta->bounds;  // exact range of the row predictions
+    else {
+        sh.kmin = r.cs->sel_kmin;
+        sh.shift = r.cs->sel_shift;
+    }
     const bool prof = c->prof_on;
     if (prof && c->prof_used == c->prof_ev.size()) {
         std::array<cudaEvent_t, 4> e{};
@@ -397,7 +555,7 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
         c->prof_ev.push_back(e);
     }
     const cudaEvent_t* ev = prof ? c->prof_ev[c->prof_used].data() : nullptr;
-    if (etune_status st = score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, sh, ev)) return st;
+    if (etune_status st = score_dispatch(c, p, f, r, d_genome, n, d_pred, d_ids, sh, ev)) return st;
     CU(launch_select(c->lc(), d_pred, n, k, d_idx, c->sel, sh));
     if (prof) CU(cudaEventRecord(c->prof_ev[c->prof_used++][3], c->stream));
     c->sel_dirty = false;
@@ -594,6 +752,19 @@ etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, cons
     CU(cudaSetDevice(c->device));
     CU(cudaMalloc(&p->d_blob, p->build.blob.size()));
     CU(cudaMemcpyAsync(p->d_blob, p->build.blob.data(), p->build.blob.size(), cudaMemcpyHostToDevice, c->stream));
+    // row-table form: keys x legal (k_tile, unroll, vec) triples bound the table; per-key FNV state
+    {
+        const PlanHdr& H = p->build.hdr;
+        const int64_t nkeys = int64_t(H.nt[0]) * H.nt[1] * H.nt[2];
+        const int64_t dom = rowtab_kuv_domain(p->build.divk.data(), H.ndk);
+        p->nkeys = nkeys;
+        p->kuv_domain = dom;
+        if (H.ndk <= 1024 && nkeys > 0 && nkeys <= (int64_t(1) << 24) && nkeys * dom <= (int64_t(1) << 25)) {
+            p->rows_cap = nkeys * dom;
+            CU(cudaMalloc(&p->d_khash, size_t(nkeys) * 8));
+            CU(launch_key_hash(c->lc(), p->d_blob, nkeys, p->d_khash));
+        }
+    }
     CU(cudaStreamSynchronize(c->stream));
     {
         std::lock_guard<std::mutex> lock(g_serial_mu);
@@ -607,6 +778,26 @@ etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, cons
 etune_status etune_cu_plan_destroy(etune_cu_plan* p) {
     if (!p) return ETUNE_OK;
     etune_cu_ctx* c = p->ctx;
+    {  // evict every form compiled for this plan (plan serials are never reused)
+        std::lock_guard<std::mutex> lk(c->forests_mu);
+        for (etune_cu_forest* f : c->forests) {
+            std::lock_guard<std::mutex> lock(f->mu);
+            auto it = f->compiled.find(p->serial);
+            if (it != f->compiled.end()) {
+                free_compiled(it->second);
+                f->compiled.erase(it);
+            }
+            auto rt = f->rowtabs.find(p->serial);
+            if (rt != f->rowtabs.end()) {
+                free_rowtab(rt->second, c->stream);
+                f->rowtabs.erase(rt);
+            }
+            f->seen.erase(p->serial);
+            f->walked.erase(p->serial);
+        }
+    }
+    cudaStreamSynchronize(c->stream);  // kernels still reading the plan's tables
+    cudaFree(p->d_khash);
     cudaFree(p->d_blob);
     delete p;
     ctx_release(c);
@@ -1015,21 +1206,26 @@ etune_status etune_cu_forest_create(etune_cu_ctx* c, const int32_t* feature, con
     CU(cudaMemcpyAsync(f->d_predict, blob.data(), blob.size(), cudaMemcpyHostToDevice, c->stream));
     CU(cudaStreamSynchronize(c->stream));
     f->predict_bytes = uint32_t(blob.size());
+    f->nnodes = int(nn);
     ctx_retain(c);
+    {
+        std::lock_guard<std::mutex> lk(c->forests_mu);
+        c->forests.insert(f.get());
+    }
     *out = f.release();
     return ETUNE_OK;
 }
 
 etune_status etune_cu_forest_destroy(etune_cu_forest* f) {
     if (!f) return ETUNE_OK;
-    cudaFreeAsync(f->d_predict, f->ctx->stream);  // stream-ordered: after the forest's last use on the ctx stream
-    for (auto& kv : f->compiled) {
-        cudaFree(kv.second.d_blob);
-        cudaFree(kv.second.d_kblob);
-        cudaFree(kv.second.d_ktable);
-        cudaFree(kv.second.d_khash);
-    }
     etune_cu_ctx* c = f->ctx;
+    {
+        std::lock_guard<std::mutex> lk(c->forests_mu);
+        c->forests.erase(f);
+    }
+    cudaFreeAsync(f->d_predict, c->stream);  // stream-ordered: after the forest's last use on the ctx stream
+    for (auto& kv : f->compiled) free_compiled(kv.second);
+    for (auto& kv : f->rowtabs) free_rowtab(kv.second, c->stream);
     delete f;
     ctx_release(c);
     return ETUNE_OK;
@@ -1047,10 +1243,9 @@ etune_status etune_cu_score(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
                             int64_t n, double* d_pred, uint64_t* d_ids) {
     CHECK_PLAN_ARGS(d_genome && d_pred);
     if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
-    CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
-    if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
-    return score_dispatch(c, p, f, cs, d_genome, n, d_pred, d_ids, SelHist{}, nullptr);
+    Route r;
+    if (etune_status st = route(c, f, p, n, &r)) return st;
+    return score_dispatch(c, p, f, r, d_genome, n, d_pred, d_ids, SelHist{}, nullptr);
 }
 
 etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
@@ -1061,10 +1256,9 @@ etune_status etune_cu_score_select(etune_cu_ctx* c, const etune_cu_plan* p, etun
     if (k < 0 || k > n) return fail(ETUNE_ERR_INVALID_ARGUMENT, "need 0 <= k <= n");
     if (k > 0 && !d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null index buffer");
     if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
-    CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
-    if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
-    return score_select_local(c, p, f, cs, d_genome, n, k, d_pred, d_ids, d_idx);
+    Route r;
+    if (etune_status st = route(c, f, p, n, &r)) return st;
+    return score_select_local(c, p, f, r, d_genome, n, k, d_pred, d_ids, d_idx);
 }
 
 etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
@@ -1076,28 +1270,69 @@ etune_status etune_cu_score_select_sharded(etune_cu_ctx* c, const etune_cu_plan*
     if (k == 0) return ETUNE_OK;
     if (!d_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null buffer");
     if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "shard >= 2^31");
-    CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
-    if (etune_status st = ensure_keyed(f, p, cs, n)) return st;
+    Route r;
+    if (etune_status st = route(c, f, p, n, &r)) return st;
     ShardBufs sb;
     if (etune_status st = shard_buffers(c, k, &sb)) return st;
     const int64_t kl = std::min(k, n);
-    if (etune_status st = score_select_local(c, p, f, cs, d_genome, n, kl, d_pred, d_ids, sb.lidx)) return st;
+    if (etune_status st = score_select_local(c, p, f, r, d_genome, n, kl, d_pred, d_ids, sb.lidx)) return st;
     return shard_merge(c, d_pred, kl, k, goff, sb, d_idx, d_sc);
 }
 
 etune_status etune_cu_forest_set_keyed(etune_cu_forest* f, int mode) {
     if (!f || mode < 0 || mode > 2) return fail(ETUNE_ERR_INVALID_ARGUMENT, "mode must be 0, 1 or 2");
     f->keyed_mode = mode;
+    f->form = mode == 0 ? ETUNE_FORM_CLASS : mode == 1 ? ETUNE_FORM_KEYED : ETUNE_FORM_KEYED_BYTE;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_forest_set_form(etune_cu_forest* f, int form) {
+    if (!f || form < ETUNE_FORM_AUTO || form > ETUNE_FORM_KEYED_BYTE)
+        return fail(ETUNE_ERR_INVALID_ARGUMENT, "form must be one of ETUNE_FORM_*");
+    f->form = form;
+    if (form == ETUNE_FORM_CLASS) f->keyed_mode = 0;
+    if (form == ETUNE_FORM_KEYED) f->keyed_mode = 1;
+    if (form == ETUNE_FORM_KEYED_BYTE) f->keyed_mode = 2;
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_forest_compile(etune_cu_ctx* c, etune_cu_forest* f, const etune_cu_plan* p) {
+    if (!c || !f || !p) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    Route r;
+    return route(c, f, p, -1, &r);
+}
+
+etune_status etune_cu_forest_rows_info(etune_cu_ctx* c, etune_cu_forest* f, const etune_cu_plan* p, int64_t out[8]) {
+    if (!c || !f || !p || !out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
+    for (int i = 0; i < 8; ++i) out[i] = 0;
+    RowTab* rt = nullptr;
+    {
+        std::lock_guard<std::mutex> lock(f->mu);
+        auto it = f->rowtabs.find(p->serial);
+        if (it != f->rowtabs.end()) rt = &it->second;
+    }
+    if (!rt) return ETUNE_OK;
+    RowTabMeta m{};
+    CU(cudaMemcpyAsync(&m, rt->d_meta, sizeof(m), cudaMemcpyDeviceToHost, c->stream));
+    CU(cudaStreamSynchronize(c->stream));
+    out[0] = p->nkeys;
+    out[1] = m.nkc;
+    out[2] = p->nkeys * m.nkc;
+    out[3] = p->nkeys * m.nkc * 8;
+    out[4] = m.nthr[0];
+    out[5] = m.nthr[1];
+    out[6] = m.nthr[2];
+    out[7] = p->kuv_domain;
     return ETUNE_OK;
 }
 
 etune_status etune_cu_forest_score_form(etune_cu_forest* f, const etune_cu_plan* p, int* form) {
     if (!f || !p || !form) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
-    CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs)) return st;
-    if (etune_status st = ensure_keyed(f, p, cs, kKeyedMinN)) return st;
-    *form = cs->walk ? 3 : !use_keyed(f, cs, kKeyedMinN) ? 0 : cs->kparams->kfull ? 2 : 1;
+    Route r;
+    if (etune_status st = route(f->ctx, f, p, -1, &r)) return st;
+    if (r.kind == 2) *form = 4;
+    else if (r.kind == 0) *form = 3;
+    else *form = !use_keyed(f, r.cs, kKeyedMinN) ? 0 : r.cs->kparams->kfull ? 2 : 1;
     return ETUNE_OK;
 }
 
@@ -1126,16 +1361,48 @@ etune_status etune_cu_profile_score(etune_cu_ctx* c, int on, double* prep_ms, do
     return ETUNE_OK;
 }
 
-etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
-                                 const etune_schedule* h_sched, int64_t n, double* h_pred, uint64_t* h_ids,
-                                 int64_t* first_bad) {
-    CHECK_PLAN_ARGS(h_sched && h_pred);
-    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+}  // extern "C"
+
+namespace {
+
+// Host-buffer pipeline of etune_cu_score_host / etune_cu_score_select_host.  k > 0: the chunks'
+// predictions stay on the device (d_all) and every score kernel also fills the selection
+// histogram; after the last chunk the k best by (prediction, index) are resolved on the device
+// and only the k indices come back besides the predictions.
+etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f, const etune_schedule* h_sched,
+                           int64_t n, double* h_pred, uint64_t* h_ids, int64_t k, int64_t* h_idx,
+                           int64_t* first_bad) {
     if (first_bad) *first_bad = -1;
     if (n == 0) return ETUNE_OK;
-    CompiledScore* cs = nullptr;
-    if (etune_status st = get_compiled(f, p, &cs, n)) return st;
-    if (etune_status st = ensure_keyed(f, p, cs, std::min<int64_t>(n, int64_t(1) << 17))) return st;
+    Route r;
+    if (etune_status st = route(c, f, p, n, &r)) return st;
+    double* d_all = nullptr;
+    int64_t* d_idx = nullptr;
+    SelHist sh{};
+    if (k > 0) {
+        const size_t need = size_t(n) * 8 + size_t(k) * 8 + 256;
+        if (c->e2e_bytes < need) {
+            if (c->e2e) {
+                CU(cudaStreamSynchronize(c->stream));
+                CU(cudaFree(c->e2e));
+                c->e2e = nullptr;
+                c->e2e_bytes = 0;
+            }
+            CU(cudaMalloc(&c->e2e, need));
+            c->e2e_bytes = need;
+        }
+        d_all = static_cast<double*>(c->e2e);
+        d_idx = reinterpret_cast<int64_t*>(static_cast<char*>(c->e2e) + ((size_t(n) * 8 + 255) & ~size_t(255)));
+        if (r.kind != 0 && k <= kSelMaxK) {
+            if (etune_status st = select_work(c, n, k)) return st;
+            sh.hist = select_hist(c->sel);
+            if (r.kind == 2) sh.dbounds = r.rt->d_meta->bounds;
+            else {
+                sh.kmin = r.cs->sel_kmin;
+                sh.shift = r.cs->sel_shift;
+            }
+        }
+    }
     // Chunked pipeline over two staging buffers.  The host pool narrows chunk i's rows
     // into pinned staging (24 B/row when every field fits 16 bits) while the GPU works
     // on chunk i-1; then H2D of chunk i (copy-in stream) overlaps encode+score of chunk
@@ -1196,7 +1463,7 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         char* base = io + size_t(b) * size_t(cap) * per;
         void* d_rows = base;
         auto* d_gen = reinterpret_cast<uint64_t*>(base + size_t(cap) * sizeof(etune_schedule));
-        auto* d_pred = reinterpret_cast<double*>(base + size_t(cap) * (sizeof(etune_schedule) + 8));
+        auto* d_pred = d_all ? d_all + lo : reinterpret_cast<double*>(base + size_t(cap) * (sizeof(etune_schedule) + 8));
         auto* d_ids = reinterpret_cast<uint64_t*>(base + size_t(cap) * (sizeof(etune_schedule) + 16));
         void* h_rows = pin + size_t(b) * size_t(cap) * sizeof(etune_schedule);
         const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
@@ -1212,17 +1479,50 @@ etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_
         CU(cudaEventRecord(c->ev_in[b], c->h2d));
         CU(cudaStreamWaitEvent(c->stream, c->ev_in[b], 0));
         CU(launch_encode_packed(c->lc(), p->d_blob, p->build.hdr.total, d_rows, fb, m, d_gen, lo));
-        if (etune_status st = score_dispatch(c, p, f, cs, d_gen, m, d_pred, h_ids ? d_ids : nullptr, SelHist{}, nullptr))
+        if (etune_status st = score_dispatch(c, p, f, r, d_gen, m, d_pred, h_ids ? d_ids : nullptr, sh, nullptr))
             return st;
         CU(cudaEventRecord(c->ev_done[b], c->stream));
         CU(cudaStreamWaitEvent(c->d2h, c->ev_done[b], 0));
-        CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+        if (h_pred) CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
         if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
         CU(cudaEventRecord(c->ev_out[b], c->d2h));
+    }
+    if (k > 0) {  // keep the best over the whole population (its predictions are on the device)
+        if (sh.hist) {
+            CU(launch_select(c->lc(), d_all, n, k, d_idx, c->sel, sh));
+            c->sel_dirty = false;
+        } else {
+            if (etune_status st = ensure_scratch(c, topk_scratch_bytes(n))) return st;
+            CU(launch_topk(c->lc(), d_all, n, k, d_idx, c->scratch));
+        }
+        CU(cudaMemcpyAsync(h_idx, d_idx, size_t(k) * 8, cudaMemcpyDeviceToHost, c->stream));
     }
     CU(cudaEventRecord(c->ev_out[0], c->d2h));
     CU(cudaStreamWaitEvent(c->stream, c->ev_out[0], 0));
     return etune_cu_synchronize(c, first_bad);
+}
+
+}  // namespace
+
+extern "C" {
+
+etune_status etune_cu_score_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
+                                 const etune_schedule* h_sched, int64_t n, double* h_pred, uint64_t* h_ids,
+                                 int64_t* first_bad) {
+    CHECK_PLAN_ARGS(h_sched && h_pred);
+    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+    return host_pipeline(c, p, f, h_sched, n, h_pred, h_ids, 0, nullptr, first_bad);
+}
+
+etune_status etune_cu_score_select_host(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_forest* f,
+                                        const etune_schedule* h_sched, int64_t n, int64_t k, double* h_pred,
+                                        int64_t* h_idx, int64_t* first_bad) {
+    CHECK_PLAN_ARGS(h_sched);
+    if (!f) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null forest");
+    if (k < 0 || k > n) return fail(ETUNE_ERR_INVALID_ARGUMENT, "need 0 <= k <= n");
+    if (k > 0 && !h_idx) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null index buffer");
+    if (n >= (int64_t(1) << 31)) return fail(ETUNE_ERR_UNSUPPORTED, "n >= 2^31");
+    return host_pipeline(c, p, f, h_sched, n, h_pred, nullptr, k, h_idx, first_bad);
 }
 
 etune_status etune_cu_train(etune_cu_ctx* c, const double* d_feat, const double* d_energy, int64_t n,

@@ -10,6 +10,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <set>
 #include <utility>
 #include <vector>
 
@@ -37,6 +38,9 @@ struct etune_cu_ctx {
     int nranks = 1, rank = 0;
     void* shard = nullptr;  // sharded-selection records
     size_t shard_bytes = 0;
+    void* e2e = nullptr;    // score_select_host: the population's predictions + the k indices on the device
+    size_t e2e_bytes = 0;
+    void* rowsel = nullptr; // row-table score_select work area (RowSelWork, rowtab.cu), zeroed once
     void* sel = nullptr;    // fused score_select work area (histogram, bucket lists)
     size_t sel_bytes = 0;
     bool sel_dirty = false; // a score_select sequence did not complete: re-zero first
@@ -51,6 +55,9 @@ struct etune_cu_ctx {
     // *_host pipelines: copy-in / copy-out streams and per-buffer events
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
+    // forests alive on this ctx: a destroyed plan evicts its compiled forms from each of them
+    std::mutex forests_mu;
+    std::set<etune_cu_forest*> forests;
     etune_b200::LaunchCtx lc() const { return etune_b200::LaunchCtx{stream, sm_count, d_err}; }
 };
 
@@ -64,6 +71,22 @@ struct etune_cu_plan {
     etune_b200::PlanBuild build;
     uint8_t* d_blob = nullptr;
     uint64_t serial = 0;
+    // row-table form (rowtab.cu): per tiling-triple key the FNV-1a state of candidate_id after
+    // the operator and the three tilings; rows_cap = keys x legal (k_tile, unroll, vec) triples
+    // (0: the operator's row table would be too large, the form is not offered)
+    uint64_t* d_khash = nullptr;
+    int64_t nkeys = 0, kuv_domain = 0, rows_cap = 0;
+};
+
+// Row-table form of one (forest, plan): Kuv class table, class representatives, row
+// predictions and the selection bounds, all written on the device (rowtab.cu).
+struct RowTab {
+    etune_b200::RowTabMeta* d_meta = nullptr;
+    uint16_t* d_clskuv = nullptr;
+    uint32_t* d_crep = nullptr;
+    double* d_rowpred = nullptr;
+    uint32_t* d_srows = nullptr;   // rows in prediction order (ties by row)
+    uint32_t* d_rowgid = nullptr;  // a row's group: the dense rank of its prediction
 };
 
 struct CompiledScore {
@@ -92,8 +115,12 @@ struct etune_cu_forest {
     etune_b200::ForestHost host;
     uint8_t* d_predict = nullptr;
     uint32_t predict_bytes = 0;
+    int nnodes = 0;
     std::mutex mu;
-    std::map<uint64_t, CompiledScore> compiled;  // by plan serial
+    std::map<uint64_t, CompiledScore> compiled;  // by plan serial (host-compiled class / keyed forms)
+    std::map<uint64_t, RowTab> rowtabs;          // by plan serial (device-compiled row tables)
+    std::map<uint64_t, int64_t> seen;            // by plan serial: candidates scored so far (AUTO form)
+    int form = ETUNE_FORM_AUTO;
     int keyed_mode = 1;  // 1: keyed path (full form when it fits), 2: keyed byte form only, 0: class tables only
     // Lazy compile (set on the search loop's per-round models, each scored once): small
     // populations take the tree-walk kernel until kLazyWalkBudget candidates per plan

@@ -22,77 +22,13 @@
 #include "etune_internal.hpp"
 #include "kernels.hpp"
 #include "pdl.cuh"
+#include "plan_core.cuh"
 #include "score_core.hpp"
 
 namespace etune_b200 {
 
 namespace {
-
-constexpr uint64_t kFnvPrime = 1099511628211ull;
-constexpr uint64_t mulmod64(uint64_t a, uint64_t b) { return a * b; }
-constexpr uint64_t kFnvPrime4 = mulmod64(mulmod64(kFnvPrime, kFnvPrime), mulmod64(kFnvPrime, kFnvPrime));
-
 constexpr int kThreads = 256;
-
-__device__ __forceinline__ void stage(const uint8_t* __restrict__ g, uint32_t bytes, int4* s) {
-    const int4* src = reinterpret_cast<const int4*>(g);
-    const uint32_t n16 = bytes >> 4;
-    for (uint32_t i = threadIdx.x; i < n16; i += blockDim.x) s[i] = __ldg(src + i);
-}
-
-__device__ __forceinline__ void report(unsigned long long* err, int64_t index, int code) {
-    atomicMin(err, (static_cast<unsigned long long>(index) << 8) | static_cast<unsigned>(code));
-}
-
-// FNV-1a over one 8-byte little-endian word whose upper 4 bytes are zero (every
-// schedule value is < 2^32): 4 byte steps, then the 4 zero bytes as one multiply.
-__device__ __forceinline__ uint64_t fnv_small(uint64_t h, uint32_t v) {
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        h ^= (v >> (8 * b)) & 0xffu;
-        h *= kFnvPrime;
-    }
-    return h * kFnvPrime4;
-}
-
-template <typename T>
-__device__ __forceinline__ const T* at(const uint8_t* base, uint32_t off) {
-    return reinterpret_cast<const T*>(base + off);
-}
-
-struct Knobs {
-    TilingRec r[3];
-    int64_t k_tile;
-    uint32_t unroll, vec;
-    uint32_t k;
-};
-
-__device__ __forceinline__ uint64_t candidate_hash(uint64_t prefix, const Knobs& c) {
-    uint64_t h = prefix;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        h = fnv_small(h, c.r[d].blocks);
-        h = fnv_small(h, c.r[d].threads);
-        h = fnv_small(h, c.r[d].pt);
-    }
-    h = fnv_small(h, static_cast<uint32_t>(c.k_tile));
-    h = fnv_small(h, c.unroll);
-    h = fnv_small(h, c.vec);
-    return h;
-}
-
-__device__ __forceinline__ Knobs load_knobs(const uint8_t* P, const PlanHdr& H, uint64_t g) {
-    const Genome x = genome_unpack(g);
-    Knobs c;
-    c.r[0] = at<TilingRec>(P, H.off_til[0])[x.t0];
-    c.r[1] = at<TilingRec>(P, H.off_til[1])[x.t1];
-    c.r[2] = at<TilingRec>(P, H.off_til[2])[x.t2];
-    c.k = x.k;
-    c.k_tile = at<int64_t>(P, H.off_divk)[x.k];
-    c.unroll = 1u << x.u;
-    c.vec = 1u << x.v;
-    return c;
-}
 
 // ------------------------------------------------------------------ encode
 __device__ __forceinline__ int find_tiling(const TilingRec* T, int n, int64_t blocks, int64_t threads) {
@@ -381,34 +317,6 @@ __global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __
     }
 }
 
-// ---------------------------------------------------------------- features
-// features_from_counters (features.cpp:15-46) through the plan's tables.
-__device__ __forceinline__ void plan_features(const uint8_t* P, const PlanHdr& H, const Knobs& c, double f[16]) {
-    const int nd1 = H.nd[1], nd2 = H.nd[2];
-    const uint32_t block = c.r[0].threads * c.r[1].threads * c.r[2].threads;
-    const uint32_t gk = at<uint16_t>(P, H.off_gridkey)[(c.r[0].db * nd1 + c.r[1].db) * nd2 + c.r[2].db];
-    const GridRec gr = at<GridRec>(P, H.off_grid)[gk];
-    const GlbRec gl = at<GlbRec>(P, H.off_glb2)[c.r[1].dbt * nd2 + c.r[2].dbt];
-    const double lint = at<double>(P, H.off_int2)[c.r[1].dpt * nd2 + c.r[2].dpt];
-    const BlockRec br = at<BlockRec>(P, H.off_block)[block <= 1024 ? block : 1024];
-    const int lv = (c.r[0].pt > 1) + (c.r[1].pt > 1) + (c.r[2].pt > 1);
-    f[0] = H.f0;
-    f[1] = lint;
-    f[2] = gl.lg_glb_ld;
-    f[3] = H.f3;
-    f[4] = lint;
-    f[5] = gl.lg_glb_ld;
-    f[6] = static_cast<double>(c.vec);
-    f[7] = static_cast<double>(c.unroll);
-    f[8] = at<double>(P, H.off_lvl)[lv];
-    f[9] = at<double>(P, H.off_ptn)[c.r[2].dpt];
-    f[10] = at<double>(P, H.off_steps)[c.k];
-    f[11] = gr.lg_grid;
-    f[12] = br.lg_block;
-    f[13] = __dmul_rn(gr.a, br.b);
-    f[14] = gr.lg_active;
-    f[15] = gl.f15;
-}
 
 __global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
                                                             int use_smem, const uint64_t* __restrict__ genome,
@@ -431,26 +339,6 @@ __global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __res
         for (int j = 0; j < 8; ++j) o[j] = make_double2(f[2 * j], f[2 * j + 1]);
         if (ids) ids[i] = candidate_hash(H.fnv_prefix, c);
     }
-}
-
-// RegressionTree::eval summed in tree order (energy_model.cpp:36-44, 245-249)
-__device__ __forceinline__ double walk_forest(const PredictHdr& H, const int32_t* roots, const GNode* nodes,
-                                              const double f[16]) {
-    double sum = 0.0;
-    for (int t = 0; t < H.ntrees; ++t) {
-        int node = roots[t];
-        int feature = nodes[node].feature;
-        while (feature >= 0) {
-            double v = 0.0;
-#pragma unroll
-            for (int j = 0; j < 16; ++j) v = (j == feature) ? f[j] : v;
-            node = v < nodes[node].thr ? nodes[node].left : nodes[node].right;
-            feature = nodes[node].feature;
-        }
-        sum = __dadd_rn(sum, nodes[node].value);
-    }
-    const double p = __dadd_rn(H.base, __dmul_rn(H.lr, sum));
-    return (1e-6 < p) ? p : 1e-6;
 }
 
 // General scoring path for forests whose compiled form does not fit shared memory
@@ -490,29 +378,20 @@ __global__ void __launch_bounds__(kThreads) score_walk_kernel(const uint8_t* __r
 // One candidate per thread per iteration; the whole compiled forest lives in smem.
 constexpr int kScoreThreads = 512;
 
-// Bucket of a prediction for the fused selection (SelHist in kernels.hpp): monotone in
-// the (score) order, so every key of a lower bucket is smaller than every key above it.
-__device__ __forceinline__ uint32_t sel_bin(double p, const SelHist& s) {
-    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(p));
-    const uint64_t key = (b >> 63) ? ~b : (b | 0x8000000000000000ull);
-    if (key < s.kmin) return 0u;
-    const uint64_t d = (key - s.kmin) >> s.shift;
-    return d < uint64_t(kSelBins - 1) ? uint32_t(d) : uint32_t(kSelBins - 1);
-}
-
 template <typename M>
 __global__ void __launch_bounds__(kScoreThreads, 2) score_kernel(const uint8_t* __restrict__ gblob, uint32_t bytes,
                                                                 const uint64_t* __restrict__ genome, int64_t n,
                                                                 double* __restrict__ pred,
-                                                                uint64_t* __restrict__ ids, const SelHist sel,
+                                                                uint64_t* __restrict__ ids, const SelHist sel_in,
                                                                 const __grid_constant__ ForestParams fp) {
     extern __shared__ int4 smem[];
     __shared__ uint32_t shist[kSelBins];
-    if (sel.hist)
+    if (sel_in.hist)
         for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) shist[i] = 0u;
     stage(gblob, bytes, smem);  // read-only blob: overlaps the previous kernel's tail (PDL)
     __syncthreads();
     pdl_wait();
+    const SelHist sel = sel_resolve(sel_in);
     const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
     const ScoreHdr& H = *reinterpret_cast<const ScoreHdr*>(S);
     const int64_t* divk = at<int64_t>(S, H.off_divk);
@@ -557,15 +436,16 @@ __global__ void __launch_bounds__(kKeyedThreads, 3) score_keyed_kernel(const uin
                                                                     const uint64_t* __restrict__ genome,
                                                                     const uint32_t* __restrict__ order, int64_t n,
                                                                     double* __restrict__ pred,
-                                                                    uint64_t* __restrict__ ids, const SelHist sel,
+                                                                    uint64_t* __restrict__ ids, const SelHist sel_in,
                                                                     const __grid_constant__ KeyedParams kp) {
     extern __shared__ int4 smem[];
     __shared__ uint32_t shist[kSelBins];
-    if (sel.hist)
+    if (sel_in.hist)
         for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) shist[i] = 0u;
     stage(gblob, bytes, smem);  // read-only blob: overlaps the previous kernel's tail (PDL)
     __syncthreads();
     pdl_wait();
+    const SelHist sel = sel_resolve(sel_in);
     const uint8_t* S = reinterpret_cast<const uint8_t*>(smem);
     const KeyedHdr& K = *reinterpret_cast<const KeyedHdr*>(S);
     const uint8_t* clskuv = S + K.off_clskuv;

@@ -45,12 +45,16 @@ cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t 
 // kSelBins buckets of its order-preserving key.  The bucket function is monotone
 // (keys below kmin -> 0, above the range -> last bucket), so it is exact for any
 // bounds; the forest's leaf-value bounds only decide how finely the buckets resolve.
-constexpr int kSelBins = 1024;
+constexpr int kSelBins = 1024;  // selbin.cuh derives the bucket shift from this being 2^10
 constexpr int kSelMaxK = 4096;  // one-CTA final sort bound
 struct SelHist {
     uint32_t* hist;  // kSelBins global counters (null: no histogram)
     uint64_t kmin;
     uint32_t shift;
+    // non-null: the bounds are device-resident {lowest, highest order key} written by an
+    // earlier kernel (the row-table build); kmin / shift are derived from them on the
+    // device (sel_resolve, plan_core.cuh) after the kernel's dependency wait
+    const uint64_t* dbounds = nullptr;
 };
 // resident CTAs per SM of the compiled score kernel for a blob size (sets the smem ceiling)
 cudaError_t score_occupancy(int mask_bits, uint32_t bytes, int* per_sm);
@@ -76,6 +80,43 @@ size_t select_scratch_bytes(int64_t n, int64_t k);
 uint32_t* select_hist(void* d_sel);
 cudaError_t launch_select(const LaunchCtx& c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx,
                           void* d_sel, const SelHist& sel);
+// Row-table form (rowtab.cu): the prediction as a function of (tiling-triple key, Kuv class),
+// compiled on the device from the plan and the forest's predict blob.
+struct RowTabMeta {
+    uint64_t bounds[2];  // lowest / highest order key of the row predictions (SelHist::dbounds)
+    int32_t nkc;         // Kuv classes = rows per key
+    int32_t nthr[3];     // thresholds the forest tests on f10, f7, f6
+    int64_t rows;        // keys x nkc
+    int64_t groups;      // distinct row predictions (dense ranks 0 .. groups-1)
+};
+// rows per key before class compression: the legal (k_tile, unroll, vectorize) triples
+int64_t rowtab_kuv_domain(const int64_t* divk, int ndk);
+size_t rowtab_scratch_bytes(int nnodes);
+cudaError_t launch_key_hash(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, uint64_t* d_khash);
+// d_clskuv: ndk * 64 u16; d_crep: one u32 per class (<= rowtab_kuv_domain); d_rowpred: rows_cap doubles
+cudaError_t launch_rowtab_compile(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                                  const uint8_t* d_pred, uint32_t pred_bytes, int nnodes, int ndk, int64_t rows_cap,
+                                  void* d_scratch, RowTabMeta* d_meta, uint16_t* d_clskuv, uint32_t* d_crep,
+                                  double* d_rowpred);
+// Rows in prediction order and each row's group (dense rank of its prediction) for the fused
+// selection: d_srows[p] = the row at position p, d_rowgid[row] = its group, both rows_cap u32;
+// scratch rowtab_sort_scratch_bytes(rows_cap).
+size_t rowtab_sort_scratch_bytes(int64_t rows_cap);
+cudaError_t launch_rowtab_sort(const LaunchCtx& c, RowTabMeta* d_meta, const double* d_rowpred, int64_t rows_cap,
+                               uint32_t* d_srows, uint32_t* d_rowgid, void* d_scratch);
+// Fused score + keep-the-best on the row table in ONE cooperative kernel (rowtab.cu): every
+// candidate's prediction and id, group counts, the k-th group, ties by index, the k sorted by
+// (prediction, index).  0 < k <= kSelMaxK; returns cudaErrorNotSupported when n exceeds what the
+// grid holds in registers (the caller falls back to the bucketed selection).
+size_t rowsel_work_bytes();
+cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,
+                                     const RowTabMeta* d_meta, const double* d_rowpred, const uint32_t* d_rowgid,
+                                     int64_t rows_cap, const uint64_t* d_khash, const uint64_t* d_genome, int64_t n,
+                                     int64_t k, double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work);
+cudaError_t launch_score_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,
+                              const RowTabMeta* d_meta, const double* d_rowpred, const uint64_t* d_khash,
+                              const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
+                              const SelHist& sel = SelHist{});
 // General path: features + reference tree walk (any forest the reference can train).
 cudaError_t launch_score_walk(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint8_t* d_pred,
                               uint32_t pred_bytes, const uint64_t* d_genome, int64_t n, double* d_out,
@@ -121,6 +162,9 @@ cudaError_t launch_gather_records(const LaunchCtx& c, const double* d_gs, const 
 size_t sort_pairs_scratch_bytes(int64_t n);
 cudaError_t launch_sort_pairs(const LaunchCtx& c, uint64_t* keys, uint32_t* vals, int64_t n, int bits,
                               void* scratch);
+// the same with the count (<= n_cap) and key bit length in device memory (scratch: sort_pairs_scratch_bytes(n_cap))
+cudaError_t launch_sort_pairs_dev(const LaunchCtx& c, uint64_t* keys, uint32_t* vals, int64_t n_cap,
+                                  const int64_t* d_n, const int32_t* d_bits, void* scratch);
 
 // sample_random (space.cpp:170-251): large-space attempts / small-space enumerate + Fisher-Yates.
 // Scratch: sample_scratch_bytes(attempts, 0, false) / (n, odometer product, true).

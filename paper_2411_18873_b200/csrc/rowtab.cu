@@ -1,0 +1,1212 @@
+// Row-table form of the cost model: the default scoring form, compiled on the device.
+//
+// Every feature of features_from_counters (features.cpp:15-46) is a function of the
+// candidate's three spatial tilings ("key", e.g. glb_ld of the block tiles) except f6
+// (vectorize), f7 (unroll) and f10 (log1p of K / k_tile), which depend on the reduction
+// knobs (k_tile, unroll, vectorize) alone.  A tree's path (RegressionTree::eval,
+// energy_model.cpp:36-44) only depends on which side of each threshold a feature falls,
+// so two (k, u, v) triples whose f6 / f7 / f10 values pass exactly the same thresholds
+// of the forest take the same path in every tree: they form one "Kuv class".  The
+// prediction (energy_model.cpp:245-249) is therefore a pure function of the row
+// (key, Kuv class), and there are far fewer rows than candidates (C2: 4704 keys x 21
+// classes = 98,784 rows vs 2^20 candidates).
+//
+//   rowtab_classes_kernel  one CTA: the forest's thresholds on f6 / f7 / f10, each knob
+//                          value's count of thresholds it does not fall below, the
+//                          distinct attained count triples over the legal (k, u, v)
+//                          -> Kuv class table [k][u][v] and one representative per class
+//   rowtab_build_kernel    one thread per row: the representative genome's features from
+//                          the plan tables, the reference tree walk over the forest, the
+//                          row's prediction (+ the lowest / highest order key for the
+//                          fused selection's buckets)
+//   score_rows_kernel      per candidate: genome -> row -> prediction (one 8-byte gather
+//                          from the L2-resident table), candidate_id from the per-key FNV
+//                          state, + the selection histogram
+//
+// Nothing is evaluated on the host: a model trained on the device is scorable without a
+// host round trip, and the compile is three launches (tens of microseconds).  The row's
+// prediction is computed by exactly the walk score_walk_kernel runs per candidate (same
+// features, same doubles, tree-order sum, no FMA), so every form is bit-identical.
+#include <cuda_runtime.h>
+
+#include <cooperative_groups.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+
+#include "etune_internal.hpp"
+#include "kernels.hpp"
+#include "pdl.cuh"
+#include "plan_core.cuh"
+
+namespace etune_b200 {
+
+namespace {
+
+constexpr int kClsT = 1024;
+constexpr int kThrCache = 1024;  // thresholds per feature staged in shared memory
+constexpr int kMaxJointWords = 2048;  // A10 * A7 * A6 <= 1024 * 16 * 3 bits
+
+// Knob value domain of the Kuv channel: every (k_tile index, log2 unroll, log2 vec) a
+// legal schedule can hold (validate_schedule, schedule.cpp:26-61: unroll a power of two
+// dividing k_tile -- at most 2^15 in a genome -- and vectorize in {1, 2, 4}).
+constexpr int kKuvU = 16;
+constexpr int kKuvV = 3;
+
+__device__ __forceinline__ int ctz64(int64_t x) { return x ? __ffsll(x) - 1 : 63; }
+
+// thresholds t of one feature with !(x < t): the tests x passes to the right
+__device__ __forceinline__ int count_right(double x, const double* t, int n) {
+    int c = 0;
+    for (int i = 0; i < n; ++i) c += !(x < t[i]);
+    return c;
+}
+
+struct ClsSmem {
+    double thr[3][kThrCache];   // f10, f7, f6 thresholds
+    int cnt[3];
+    int A[3];                   // attained distinct counts per feature (k, u, v)
+    int c10[1024], a10[1024], rep10[1024], f10[1024];
+    int c7[kKuvU], a7[kKuvU], rep7[kKuvU], f7[kKuvU];
+    int c6[4], a6[4], rep6[4], f6[4];
+    uint32_t bits[kMaxJointWords];
+    uint32_t pre[kMaxJointWords];
+    uint32_t scan[32];
+};
+
+__global__ void __launch_bounds__(kClsT, 1) rowtab_classes_kernel(const uint8_t* __restrict__ P,
+                                                                  const uint8_t* __restrict__ Q,
+                                                                  double* __restrict__ gthr, int nnodes,
+                                                                  RowTabMeta* __restrict__ meta,
+                                                                  uint16_t* __restrict__ clskuv,
+                                                                  uint32_t* __restrict__ crep) {
+    extern __shared__ int4 dsm[];
+    ClsSmem& S = *reinterpret_cast<ClsSmem*>(dsm);
+    const int tid = threadIdx.x;
+    pdl_wait();
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const PredictHdr& QH = *reinterpret_cast<const PredictHdr*>(Q);
+    const GNode* nodes = at<GNode>(Q, QH.off_nodes);
+    const int64_t* divk = at<int64_t>(P, H.off_divk);
+    const double* steps = at<double>(P, H.off_steps);  // f10 = log1p(K / k_tile) per k index
+    const int ndk = H.ndk;
+    if (tid < 3) S.cnt[tid] = 0;
+    __syncthreads();
+    // 1. the forest's thresholds on f10 / f7 / f6 (order within a list is irrelevant: only counts are used)
+    for (int i = tid; i < nnodes; i += blockDim.x) {
+        const int f = nodes[i].feature;
+        const int s = f == 10 ? 0 : f == 7 ? 1 : f == 6 ? 2 : -1;
+        if (s >= 0) gthr[size_t(s) * nnodes + atomicAdd(&S.cnt[s], 1)] = nodes[i].thr;
+    }
+    __syncthreads();
+    const double* T[3];
+    for (int s = 0; s < 3; ++s) {
+        const int n = S.cnt[s];
+        if (n <= kThrCache) {
+            for (int i = tid; i < n; i += blockDim.x) S.thr[s][i] = gthr[size_t(s) * nnodes + i];
+            T[s] = S.thr[s];
+        } else {
+            T[s] = gthr + size_t(s) * nnodes;
+        }
+    }
+    __syncthreads();
+    // 2. per knob value: how many of the feature's thresholds it passes to the right
+    for (int k = tid; k < ndk; k += blockDim.x) S.c10[k] = count_right(steps[k], T[0], S.cnt[0]);
+    if (tid < kKuvU) S.c7[tid] = count_right(double(1u << tid), T[1], S.cnt[1]);
+    if (tid < kKuvV) S.c6[tid] = count_right(double(1u << tid), T[2], S.cnt[2]);
+    __syncthreads();
+    // 3. dense rank of each value's count among the distinct counts; the first value with
+    //    each count represents its class
+    for (int k = tid; k < ndk; k += blockDim.x) {
+        bool first = true;
+        for (int j = 0; j < k && first; ++j) first = S.c10[j] != S.c10[k];
+        S.f10[k] = first;
+    }
+    if (tid < kKuvU) {
+        bool first = true;
+        for (int j = 0; j < tid && first; ++j) first = S.c7[j] != S.c7[tid];
+        S.f7[tid] = first;
+    }
+    if (tid < kKuvV) {
+        bool first = true;
+        for (int j = 0; j < tid && first; ++j) first = S.c6[j] != S.c6[tid];
+        S.f6[tid] = first;
+    }
+    __syncthreads();
+    for (int k = tid; k < ndk; k += blockDim.x) {
+        int a = 0;
+        for (int j = 0; j < ndk; ++j) a += S.f10[j] && S.c10[j] < S.c10[k];
+        S.a10[k] = a;
+        if (S.f10[k]) S.rep10[a] = k;
+    }
+    if (tid < kKuvU) {
+        int a = 0;
+        for (int j = 0; j < kKuvU; ++j) a += S.f7[j] && S.c7[j] < S.c7[tid];
+        S.a7[tid] = a;
+        if (S.f7[tid]) S.rep7[a] = tid;
+    }
+    if (tid < kKuvV) {
+        int a = 0;
+        for (int j = 0; j < kKuvV; ++j) a += S.f6[j] && S.c6[j] < S.c6[tid];
+        S.a6[tid] = a;
+        if (S.f6[tid]) S.rep6[a] = tid;
+    }
+    if (tid == 0) {
+        int a = 0, b = 0, d = 0;
+        for (int k = 0; k < ndk; ++k) a += S.f10[k];
+        for (int u = 0; u < kKuvU; ++u) b += S.f7[u];
+        for (int v = 0; v < kKuvV; ++v) d += S.f6[v];
+        S.A[0] = a;
+        S.A[1] = b;
+        S.A[2] = d;
+    }
+    __syncthreads();
+    const int A10 = S.A[0], A7 = S.A[1], A6 = S.A[2];
+    const int J = A10 * A7 * A6;
+    const int words = (J + 31) >> 5;
+    for (int w = tid; w < words; w += blockDim.x) S.bits[w] = 0u;
+    __syncthreads();
+    // 4. joint count triples attained by legal (k, u, v): one bit each
+    const int ncombo = ndk * 64;
+    for (int idx = tid; idx < ncombo; idx += blockDim.x) {
+        const int k = idx >> 6, u = (idx >> 2) & 15, v = idx & 3;
+        if (v < kKuvV && u <= ctz64(divk[k])) {
+            const int j = (S.a10[k] * A7 + S.a7[u]) * A6 + S.a6[v];
+            atomicOr(&S.bits[j >> 5], 1u << (j & 31));
+        }
+    }
+    __syncthreads();
+    // exclusive popcount prefix over the words (<= 2048 words: two per thread)
+    {
+        const int w0 = 2 * tid;
+        const uint32_t p0 = w0 < words ? __popc(S.bits[w0]) : 0u;
+        const uint32_t p1 = w0 + 1 < words ? __popc(S.bits[w0 + 1]) : 0u;
+        const uint32_t mine = p0 + p1;
+        uint32_t x = mine;
+        for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
+            if ((tid & 31) >= s) x += y;
+        }
+        if ((tid & 31) == 31) S.scan[tid >> 5] = x;
+        __syncthreads();
+        if (tid < 32) {
+            uint32_t z = S.scan[tid];
+            for (int s = 1; s < 32; s <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, z, s);
+                if (tid >= s) z += y;
+            }
+            S.scan[tid] = z;  // inclusive per warp
+        }
+        __syncthreads();
+        const uint32_t before = (tid >> 5) ? S.scan[(tid >> 5) - 1] : 0u;
+        const uint32_t ex = before + x - mine;
+        if (w0 < words) S.pre[w0] = ex;
+        if (w0 + 1 < words) S.pre[w0 + 1] = ex + p0;
+    }
+    __syncthreads();
+    // 5. class of every (k, u, v) and the representative knob values of every class
+    for (int idx = tid; idx < ncombo; idx += blockDim.x) {
+        const int k = idx >> 6, u = (idx >> 2) & 15, v = idx & 3;
+        uint16_t cls = 0xffffu;
+        if (v < kKuvV && u <= ctz64(divk[k])) {
+            const int j = (S.a10[k] * A7 + S.a7[u]) * A6 + S.a6[v];
+            cls = uint16_t(S.pre[j >> 5] + __popc(S.bits[j >> 5] & ((1u << (j & 31)) - 1u)));
+        }
+        clskuv[idx] = cls;
+    }
+    for (int j = tid; j < J; j += blockDim.x) {
+        if ((S.bits[j >> 5] >> (j & 31)) & 1u) {
+            const uint32_t cls = S.pre[j >> 5] + __popc(S.bits[j >> 5] & ((1u << (j & 31)) - 1u));
+            const int i6 = j % A6, i7 = (j / A6) % A7, i10 = j / (A6 * A7);
+            crep[cls] = (uint32_t(S.rep10[i10]) << 8) | (uint32_t(S.rep7[i7]) << 2) | uint32_t(S.rep6[i6]);
+        }
+    }
+    if (tid == 0) {
+        meta->nkc = int32_t(words ? S.pre[words - 1] + __popc(S.bits[words - 1]) : 0);
+        meta->bounds[0] = ~0ull;
+        meta->bounds[1] = 0ull;
+        meta->nthr[0] = S.cnt[0];
+        meta->nthr[1] = S.cnt[1];
+        meta->nthr[2] = S.cnt[2];
+        meta->rows = int64_t(H.nt[0]) * H.nt[1] * H.nt[2] * int64_t(meta->nkc);
+    }
+}
+
+constexpr int kBuildT = 256;
+
+__device__ __forceinline__ uint64_t order_key(double p) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(p));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+// Node of the build walk: 16 bytes in shared memory (vs the 32-byte GNode) so the forest and
+// the per-thread feature vectors fit two CTAs per SM.  tv = threshold (interior) or leaf value;
+// lr = left | right << 16 (absolute node indices, forests of < 65536 nodes).
+struct CNode {
+    double tv;
+    uint32_t lr;
+    int32_t feature;
+};
+static_assert(sizeof(CNode) == 16, "CNode layout");
+
+// One thread per row: features of the row's representative genome, then RegressionTree::eval
+// summed in tree order (energy_model.cpp:36-44, 245-249) -- the same comparisons, the same leaf
+// doubles and the same DADD order as walk_forest / the reference.  COMPACT: nodes staged as CNode
+// and features in shared memory ([16][kBuildT], one LDS per visited node); else the GNode walk
+// over global memory (forests of >= 65536 nodes or too large for shared memory).
+template <bool COMPACT>
+__global__ void __launch_bounds__(kBuildT) rowtab_build_kernel(const uint8_t* __restrict__ P,
+                                                               const uint8_t* __restrict__ Q, int nnodes,
+                                                               RowTabMeta* __restrict__ meta,
+                                                               const uint32_t* __restrict__ crep,
+                                                               double* __restrict__ rowpred) {
+    extern __shared__ int4 smem[];
+    const PredictHdr& QH = *reinterpret_cast<const PredictHdr*>(Q);
+    const int32_t* groots = at<int32_t>(Q, QH.off_roots);
+    const GNode* gnodes = at<GNode>(Q, QH.off_nodes);
+    const int ntrees = QH.ntrees;
+    CNode* sn = reinterpret_cast<CNode*>(smem);
+    int32_t* sroots = reinterpret_cast<int32_t*>(sn + nnodes);
+    double* fs = reinterpret_cast<double*>(smem) + ((size_t(nnodes) * 16 + size_t(ntrees) * 4 + 15) / 16) * 2;
+    if (COMPACT) {  // read-only forest: staged before the dependency wait (PDL)
+        for (int i = threadIdx.x; i < nnodes; i += blockDim.x) {
+            const GNode g = gnodes[i];
+            CNode c;
+            c.tv = g.feature >= 0 ? g.thr : g.value;
+            c.lr = uint32_t(g.left & 0xffff) | (uint32_t(g.right & 0xffff) << 16);
+            c.feature = g.feature;
+            sn[i] = c;
+        }
+        for (int t = threadIdx.x; t < ntrees; t += blockDim.x) sroots[t] = groots[t];
+        __syncthreads();
+    }
+    pdl_wait();
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const TilingRec* T0 = at<TilingRec>(P, H.off_til[0]);
+    const TilingRec* T1 = at<TilingRec>(P, H.off_til[1]);
+    const TilingRec* T2 = at<TilingRec>(P, H.off_til[2]);
+    const int64_t* divk = at<int64_t>(P, H.off_divk);
+    const uint32_t nkc = uint32_t(meta->nkc);
+    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
+    const int64_t rows = int64_t(H.nt[0]) * nt1 * nt2 * nkc;
+    const double base = QH.base, lr = QH.lr;
+    uint64_t lo = ~0ull, hi = 0ull;
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rows; r += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t key = uint32_t(r / nkc), kc = uint32_t(r - int64_t(key) * nkc);
+        const uint32_t t2 = key % nt2, q = key / nt2, t1 = q % nt1, t0 = q / nt1;
+        const uint32_t rep = __ldg(crep + kc);
+        Knobs c;
+        c.r[0] = T0[t0];
+        c.r[1] = T1[t1];
+        c.r[2] = T2[t2];
+        c.k = rep >> 8;
+        c.k_tile = divk[c.k];
+        c.unroll = 1u << ((rep >> 2) & 15u);
+        c.vec = 1u << (rep & 3u);
+        double f[16];
+        plan_features(P, H, c, f);
+        double p;
+        if (COMPACT) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) fs[j * kBuildT + threadIdx.x] = f[j];
+            const double* myf = fs + threadIdx.x;
+            double sum = 0.0;
+            for (int t = 0; t < ntrees; ++t) {
+                CNode nd = sn[sroots[t]];
+                while (nd.feature >= 0) {
+                    const double v = myf[nd.feature * kBuildT];
+                    nd = sn[v < nd.tv ? (nd.lr & 0xffffu) : (nd.lr >> 16)];
+                }
+                sum = __dadd_rn(sum, nd.tv);
+            }
+            const double s = __dadd_rn(base, __dmul_rn(lr, sum));
+            p = (1e-6 < s) ? s : 1e-6;
+        } else {
+            p = walk_forest(QH, groots, gnodes, f);
+        }
+        rowpred[r] = p;
+        const uint64_t o = order_key(p);
+        lo = o < lo ? o : lo;
+        hi = o > hi ? o : hi;
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        const uint64_t a = __shfl_xor_sync(0xffffffffu, lo, s), b = __shfl_xor_sync(0xffffffffu, hi, s);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    if ((threadIdx.x & 31) == 0 && lo <= hi) {
+        atomicMin(reinterpret_cast<unsigned long long*>(&meta->bounds[0]), static_cast<unsigned long long>(lo));
+        atomicMax(reinterpret_cast<unsigned long long*>(&meta->bounds[1]), static_cast<unsigned long long>(hi));
+    }
+}
+
+// Per key: candidate_id's FNV-1a state (space.cpp:22-45) after the 12 operator words and
+// the key's three DimTiling records; the score kernel hashes only k_tile, unroll, vec.
+__global__ void key_hash_kernel(const uint8_t* __restrict__ P, int64_t nkeys, uint64_t* __restrict__ out) {
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const TilingRec* T[3] = {at<TilingRec>(P, H.off_til[0]), at<TilingRec>(P, H.off_til[1]),
+                             at<TilingRec>(P, H.off_til[2])};
+    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
+    for (int64_t key = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; key < nkeys;
+         key += int64_t(gridDim.x) * blockDim.x) {
+        const uint32_t t[3] = {uint32_t(key / (int64_t(nt1) * nt2)), uint32_t((key / nt2) % nt1),
+                               uint32_t(key % nt2)};
+        uint64_t h = H.fnv_prefix;
+        for (int d = 0; d < 3; ++d) {
+            const TilingRec r = T[d][t[d]];
+            h = fnv_small(h, r.blocks);
+            h = fnv_small(h, r.threads);
+            h = fnv_small(h, r.pt);
+        }
+        out[key] = h;
+    }
+}
+
+// ------------------------------------------------------------------- scoring
+constexpr int kRowsT = 512;
+constexpr int kRowsPer = 4;  // candidates per thread per pass (independent gathers in flight)
+
+__global__ void __launch_bounds__(kRowsT) score_rows_kernel(const uint8_t* __restrict__ gplan,
+                                                            const uint16_t* __restrict__ clskuv,
+                                                            const RowTabMeta* __restrict__ meta,
+                                                            const double* __restrict__ rowpred,
+                                                            const uint64_t* __restrict__ khash,
+                                                            const uint64_t* __restrict__ genome, int64_t n,
+                                                            double* __restrict__ pred, uint64_t* __restrict__ ids,
+                                                            const SelHist sel_in) {
+    extern __shared__ uint32_t rsm[];  // Kuv class table [ndk][16][4] (u16 pairs), then k_tile low words [ndk]
+    __shared__ uint32_t shist[kSelBins];
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
+    const int ndk = H.ndk;
+    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
+    const int64_t* divk = at<int64_t>(gplan, H.off_divk);
+    uint32_t* sdivk = rsm + ndk * 32;
+    if (sel_in.hist)
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) shist[i] = 0u;
+    for (int i = threadIdx.x; i < ndk; i += blockDim.x) sdivk[i] = uint32_t(divk[i]);
+    pdl_wait();  // the class table, row table and bounds may come from the kernels just before
+    const SelHist sel = sel_resolve(sel_in);
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(clskuv);
+        for (int i = threadIdx.x; i < ndk * 32; i += blockDim.x) rsm[i] = __ldg(src + i);
+    }
+    const uint32_t nkc = uint32_t(meta->nkc);
+    __syncthreads();
+    const uint16_t* scls = reinterpret_cast<const uint16_t*>(rsm);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t base = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; base < n; base += kRowsPer * stride) {
+        uint64_t g[kRowsPer];
+#pragma unroll
+        for (int j = 0; j < kRowsPer; ++j) {
+            const int64_t i = base + j * stride;
+            g[j] = i < n ? __ldcs(genome + i) : 0ull;
+        }
+        uint32_t key[kRowsPer];
+        double p[kRowsPer];
+        uint64_t h[kRowsPer];
+#pragma unroll
+        for (int j = 0; j < kRowsPer; ++j) {
+            const Genome x = genome_unpack(g[j]);
+            key[j] = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
+            const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);  // in bounds for any genome
+            p[j] = base + j * stride < n ? __ldg(rowpred + (size_t(key[j]) * nkc + kc)) : 0.0;
+            h[j] = (ids && base + j * stride < n) ? __ldg(khash + key[j]) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < kRowsPer; ++j) {
+            const int64_t i = base + j * stride;
+            if (i >= n) break;
+            pred[i] = p[j];  // plain store: stays in L2 for the selection filter that re-reads it
+            if (sel.hist) atomicAdd(&shist[sel_bin(p[j], sel)], 1u);
+            if (ids) {
+                const Genome x = genome_unpack(g[j]);
+                uint64_t hh = fnv_small(h[j], sdivk[x.k]);
+                hh = fnv_small(hh, 1u << x.u);
+                hh = fnv_small(hh, 1u << x.v);
+                __stcs(reinterpret_cast<unsigned long long*>(ids) + i, static_cast<unsigned long long>(hh));
+            }
+        }
+    }
+    if (sel.hist) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x) {
+            const uint32_t v = shist[i];
+            if (v) atomicAdd(sel.hist + i, v);
+        }
+    }
+}
+
+// ------------------------------------------------------- rows in prediction order
+// The fused selection walks the rows in prediction order, so the compile sorts them: a stable
+// LSD radix sort (four 8-bit passes) on the top 32 bits of each row's order key relative to the
+// lowest, then an exact fix-up of the (rare) runs whose truncated keys collide, by (full key,
+// row).  Everything is sized on the device (meta->rows): no host synchronisation.
+constexpr int kRsT = 512;
+constexpr int kRsTile = 4096;  // items per tile
+
+__device__ __forceinline__ int rs_shift32(const RowTabMeta* meta) {
+    const uint64_t kmin = meta->bounds[0], kmax = meta->bounds[1];
+    const uint64_t span = kmax > kmin ? kmax - kmin : 0ull;
+    const int bits = span ? 64 - __clzll(static_cast<long long>(span)) : 0;
+    return bits > 32 ? bits - 32 : 0;
+}
+
+__global__ void rowtab_keys_kernel(const RowTabMeta* __restrict__ meta, const double* __restrict__ rowpred,
+                                   uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    pdl_wait();
+    const int64_t R = meta->rows;
+    const uint64_t kmin = meta->bounds[0];
+    const int sh = rs_shift32(meta);
+    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < R; r += int64_t(gridDim.x) * blockDim.x) {
+        keys[r] = uint32_t((order_key(rowpred[r]) - kmin) >> sh);
+        vals[r] = uint32_t(r);
+    }
+}
+
+__device__ __forceinline__ void rs_agg_inc(uint32_t* bin, unsigned d, bool valid) {
+    const unsigned act = __ballot_sync(0xffffffffu, valid);
+    if (!valid) return;
+    const unsigned peers = __match_any_sync(act, d);
+    if ((__ffs(peers) - 1) == int(threadIdx.x & 31)) atomicAdd(&bin[d], unsigned(__popc(peers)));
+}
+
+// per tile: digit counts -> cnt[d * ntiles + t]
+__global__ void __launch_bounds__(kRsT) rs_hist_kernel(const RowTabMeta* __restrict__ meta,
+                                                      const uint32_t* __restrict__ keys, int shift, int ntiles,
+                                                      uint32_t* __restrict__ cnt) {
+    __shared__ uint32_t h[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    pdl_wait();
+    const int64_t R = meta->rows;
+    __syncthreads();
+    const int64_t base = int64_t(blockIdx.x) * kRsTile;
+    for (int r = 0; r < kRsTile / kRsT; ++r) {
+        const int64_t i = base + r * kRsT + threadIdx.x;
+        const bool v = i < R;
+        rs_agg_inc(h, v ? (keys[i] >> shift) & 0xffu : 0u, v);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += blockDim.x) cnt[int64_t(d) * ntiles + blockIdx.x] = h[d];
+}
+
+// one CTA per digit: exclusive scan of its tile counts in place, digit total -> tot[d]
+__global__ void __launch_bounds__(256) rs_scan_kernel(uint32_t* __restrict__ cnt, int ntiles,
+                                                     uint32_t* __restrict__ tot) {
+    __shared__ uint32_t ws[8];
+    __shared__ uint32_t carry;
+    pdl_wait();
+    const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    uint32_t* row = cnt + int64_t(d) * ntiles;
+    for (int b = 0; b < ntiles; b += 256) {
+        const int i = b + tid;
+        const uint32_t v = i < ntiles ? row[i] : 0u;
+        uint32_t x = v;
+        for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
+            if (lane >= s) x += y;
+        }
+        if (lane == 31) ws[wid] = x;
+        __syncthreads();
+        uint32_t before = carry, all = carry;
+        for (int w = 0; w < 8; ++w) {
+            before += w < wid ? ws[w] : 0u;
+            all += ws[w];
+        }
+        if (i < ntiles) row[i] = before + x - v;
+        __syncthreads();
+        if (tid == 0) carry = all;
+        __syncthreads();
+    }
+    if (tid == 0) tot[d] = carry;
+}
+
+// stable scatter of one tile: digit base (scan of the 256 totals) + tile prefix + rank in tile
+__global__ void __launch_bounds__(kRsT) rs_scatter_kernel(const RowTabMeta* __restrict__ meta,
+                                                         const uint32_t* __restrict__ kin,
+                                                         const uint32_t* __restrict__ vin, int shift,
+                                                         const uint32_t* __restrict__ cnt,
+                                                         const uint32_t* __restrict__ tot, int ntiles,
+                                                         uint32_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+    constexpr int W = kRsT / 32;
+    __shared__ uint32_t base[256];
+    __shared__ uint32_t gofs[256];
+    __shared__ uint32_t wc[W][257];
+    pdl_wait();
+    const int64_t R = meta->rows;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid < 256) {  // exclusive scan of the digit totals (8 warps x 32)
+        const uint32_t v = tot[tid];
+        uint32_t x = v;
+        for (int s = 1; s < 32; s <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
+            if (lane >= s) x += y;
+        }
+        wc[0][tid] = x;  // inclusive within the warp; combined below
+        base[tid] = 0;
+    }
+    __syncthreads();
+    if (tid < 256) {
+        uint32_t before = 0;
+        for (int w = 0; w < (tid >> 5); ++w) before += wc[0][w * 32 + 31];
+        gofs[tid] = before + wc[0][tid] - tot[tid] + cnt[int64_t(tid) * ntiles + blockIdx.x];
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    const int64_t tbase = int64_t(blockIdx.x) * kRsTile;
+    for (int r = 0; r < kRsTile / kRsT; ++r) {
+        for (int j = tid; j < W * 257; j += blockDim.x) (&wc[0][0])[j] = 0;
+        __syncthreads();
+        const int64_t i = tbase + r * kRsT + tid;
+        const bool valid = i < R;
+        uint32_t key = 0, val = 0;
+        unsigned d = 256;
+        if (valid) {
+            key = kin[i];
+            val = vin[i];
+            d = (key >> shift) & 0xffu;
+        }
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned wrank = __popc(peers & lt);
+        if (valid && (__ffs(peers) - 1) == lane) wc[warp][d] = __popc(peers);
+        __syncthreads();
+        if (tid < 256) {
+            uint32_t run = base[tid];
+            for (int w = 0; w < W; ++w) {
+                const uint32_t c = wc[w][tid];
+                wc[w][tid] = run;
+                run += c;
+            }
+            base[tid] = run;
+        }
+        __syncthreads();
+        if (valid) {
+            const uint32_t pos = gofs[d] + wc[warp][d] + wrank;
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+    }
+}
+
+// After the radix sort on truncated keys, rows whose truncated keys collide but whose full keys
+// are out of order are rare.  rowtab_inv_kernel (one thread per position) marks the start of
+// every run of equal truncated keys that holds such an inversion; rowtab_runsort_kernel sorts
+// only the marked runs by (full key, row) -- one thread per run, insertion sort.
+__device__ __forceinline__ bool rs_after(const double* rowpred, uint32_t q, uint32_t r) {
+    const uint64_t kq = order_key(rowpred[q]), kr = order_key(rowpred[r]);
+    return kq > kr || (kq == kr && q > r);
+}
+
+__global__ void rowtab_inv_kernel(const RowTabMeta* __restrict__ meta, const double* __restrict__ rowpred,
+                                  const uint32_t* __restrict__ k32, const uint32_t* __restrict__ srows,
+                                  uint32_t* __restrict__ mark) {
+    pdl_wait();
+    const int64_t R = meta->rows;
+    for (int64_t p = 1 + blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < R; p += int64_t(gridDim.x) * blockDim.x) {
+        if (k32[p - 1] != k32[p] || !rs_after(rowpred, srows[p - 1], srows[p])) continue;
+        int64_t st = p - 1;
+        while (st > 0 && k32[st - 1] == k32[p]) --st;
+        atomicOr(mark + (st >> 5), 1u << (st & 31));
+    }
+}
+
+__global__ void rowtab_runsort_kernel(const RowTabMeta* __restrict__ meta, const double* __restrict__ rowpred,
+                                      const uint32_t* __restrict__ k32, uint32_t* __restrict__ srows,
+                                      uint32_t* __restrict__ mark) {
+    pdl_wait();
+    const int64_t R = meta->rows;
+    for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < R; p += int64_t(gridDim.x) * blockDim.x) {
+        if (!((mark[p >> 5] >> (p & 31)) & 1u)) continue;
+        int64_t e = p + 1;
+        while (e < R && k32[e] == k32[p]) ++e;
+        for (int64_t i = p + 1; i < e; ++i) {
+            const uint32_t r = srows[i];
+            int64_t j = i - 1;
+            while (j >= p && rs_after(rowpred, srows[j], r)) {
+                srows[j + 1] = srows[j];
+                --j;
+            }
+            srows[j + 1] = r;
+        }
+    }
+}
+
+// Dense rank ("group") of every row in prediction order: position p starts a new group when its
+// full key differs from position p-1's.  Per tile of kRsTile positions: the group starts counted
+// (rowtab_gcount_kernel), one CTA scans the tile counts (rowtab_gscan_kernel), then each tile
+// assigns gid = groups started before it + its inclusive block scan - 1 and scatters
+// rowgid[row] = gid (rowtab_gapply_kernel); meta->groups = the number of distinct predictions.
+__device__ __forceinline__ uint32_t rs_newgroup(const double* rowpred, const uint32_t* srows, int64_t p) {
+    return p == 0 || order_key(rowpred[srows[p - 1]]) != order_key(rowpred[srows[p]]) ? 1u : 0u;
+}
+
+__global__ void __launch_bounds__(kRsT) rowtab_gcount_kernel(const RowTabMeta* __restrict__ meta,
+                                                            const double* __restrict__ rowpred,
+                                                            const uint32_t* __restrict__ srows,
+                                                            uint32_t* __restrict__ tcnt) {
+    __shared__ uint32_t red[kRsT / 32];
+    pdl_wait();
+    const int64_t R = meta->rows;
+    uint32_t c = 0;
+    for (int r = 0; r < kRsTile / kRsT; ++r) {
+        const int64_t p = int64_t(blockIdx.x) * kRsTile + r * kRsT + threadIdx.x;
+        if (p < R) c += rs_newgroup(rowpred, srows, p);
+    }
+    for (int sft = 16; sft > 0; sft >>= 1) c += __shfl_xor_sync(0xffffffffu, c, sft);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kRsT / 32; ++w) t += red[w];
+        tcnt[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(1024) rowtab_gscan_kernel(RowTabMeta* __restrict__ meta, uint32_t* __restrict__ tcnt,
+                                                           int ntiles) {
+    __shared__ uint32_t ws[32];
+    __shared__ uint32_t carry;
+    pdl_wait();
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int b = 0; b < ntiles; b += 1024) {
+        const int i = b + tid;
+        const uint32_t v = i < ntiles ? tcnt[i] : 0u;
+        uint32_t x = v;
+        for (int sft = 1; sft < 32; sft <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, sft);
+            if (lane >= sft) x += y;
+        }
+        if (lane == 31) ws[wid] = x;
+        __syncthreads();
+        uint32_t before = carry, all = carry;
+        for (int w = 0; w < 32; ++w) {
+            before += w < wid ? ws[w] : 0u;
+            all += ws[w];
+        }
+        if (i < ntiles) tcnt[i] = before + x - v;  // exclusive
+        __syncthreads();
+        if (tid == 0) carry = all;
+        __syncthreads();
+    }
+    if (tid == 0) meta->groups = int64_t(carry);
+}
+
+__global__ void __launch_bounds__(kRsT) rowtab_gapply_kernel(const RowTabMeta* __restrict__ meta,
+                                                            const double* __restrict__ rowpred,
+                                                            const uint32_t* __restrict__ srows,
+                                                            const uint32_t* __restrict__ tcnt,
+                                                            uint32_t* __restrict__ rowgid) {
+    __shared__ uint32_t ws[kRsT / 32];
+    __shared__ uint32_t carry;
+    pdl_wait();
+    const int64_t R = meta->rows;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry = tcnt[blockIdx.x];
+    __syncthreads();
+    for (int r = 0; r < kRsTile / kRsT; ++r) {
+        const int64_t p = int64_t(blockIdx.x) * kRsTile + r * kRsT + tid;
+        const uint32_t v = p < R ? rs_newgroup(rowpred, srows, p) : 0u;
+        uint32_t x = v;
+        for (int sft = 1; sft < 32; sft <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, sft);
+            if (lane >= sft) x += y;
+        }
+        if (lane == 31) ws[wid] = x;
+        __syncthreads();
+        uint32_t before = carry, all = carry;
+        for (int w = 0; w < kRsT / 32; ++w) {
+            before += w < wid ? ws[w] : 0u;
+            all += ws[w];
+        }
+        if (p < R) rowgid[srows[p]] = before + x - 1u;  // inclusive count of group starts - 1
+        __syncthreads();
+        if (tid == 0) carry = all;
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------ fused score + keep-the-best
+// One cooperative grid.  Every candidate's prediction is its row's, and its rank in prediction
+// order is its row's group g (the dense rank of the row's prediction: equal predictions, equal
+// g).  Every thread keeps up to kSRPer candidates' g in registers across three grid barriers, so
+// nothing is re-read and there is no per-candidate global atomic (hot rows -- copies of the same
+// parent -- would serialise in L2):
+//   A   score: genome -> row -> prediction (+ id) out; shared-memory histogram of g >> segshift,
+//       flushed with one atomic per non-empty segment per CTA;
+//   B1  (every CTA) the segment s* holding the k-th candidate from the segment counts; each CTA
+//       histograms its candidates inside s* by g, flushed the same way;
+//   B2  (every CTA) the k-th candidate's group g* inside s*; candidates with g < g* (fewer than k)
+//       are appended; each CTA counts its candidates at g*;
+//   C   ties at g* are taken by index: CTA b owns the contiguous indices [b*per*T, (b+1)*per*T)
+//       in (j, thread) order, so its quota is need - (ties of CTAs before it), taken in that
+//       order; the last CTA to finish sorts the k records by (g, index) = (prediction, index),
+//       SPEC:403-404 with the SURVEY H3 tie rule, and clears the counters.
+constexpr int kSRT = 512;
+constexpr int kSRPer = 8;
+constexpr int kSRMaxCtas = 1024;
+constexpr int kSRMaxSeg = 4096;  // segment histogram bins (shared memory)
+constexpr int kSRBatch = 4;      // candidates per thread whose loads are in flight together
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+struct RowSelWork {
+    uint32_t nlist, ticket, pad[2];
+    uint32_t tiecnt[kSRMaxCtas];
+    uint32_t seg[kSRMaxSeg];      // candidates per segment of groups
+    uint32_t fine[kSRMaxSeg];     // candidates per group inside the crossing segment (segment size <= kSRMaxSeg)
+    uint64_t lkey[kSelMaxK];      // g << 32 | index of the selected
+};
+
+// exclusive block scan of one u32 per thread (blockDim = kSRT); *total = block sum
+__device__ __forceinline__ uint32_t sr_block_scan(uint32_t v, uint32_t* ws, uint32_t* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+    for (int s = 1; s < 32; s <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
+        if (lane >= s) x += y;
+    }
+    if (lane == 31) ws[wid] = x;
+    __syncthreads();
+    uint32_t before = 0, tot = 0;
+#pragma unroll
+    for (int i = 0; i < kSRT / 32; ++i) {
+        const uint32_t w = ws[i];
+        before += i < wid ? w : 0u;
+        tot += w;
+    }
+    __syncthreads();
+    *total = tot;
+    return before + x - v;
+}
+
+__device__ __forceinline__ void sr_append(RowSelWork* W, bool take, uint64_t key) {
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&W->nlist, uint32_t(__popc(m)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (take) {
+        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+        if (pos < uint32_t(kSelMaxK)) W->lkey[pos] = key;
+    }
+}
+
+// smem histogram hs[0..nb) -> global g[0..nb), one atomic per non-empty bin
+__device__ __forceinline__ void sr_flush(const uint32_t* hs, uint32_t* g, int nb) {
+    for (int i = threadIdx.x; i < nb; i += kSRT) {
+        const uint32_t v = hs[i];
+        if (v) atomicAdd(g + i, v);
+    }
+}
+
+// the bin holding the k-th item (1-based rank kk) among nb counters (read through L2): bin and
+// the count before it.  Every thread returns the same pair.
+__device__ __forceinline__ void sr_cross(const uint32_t* g, int nb, uint32_t kk, uint32_t* ws, uint32_t* s_bin,
+                                         uint32_t* s_before) {
+    uint32_t run = 0;
+    for (int b0 = 0; b0 < nb; b0 += kSRT) {
+        const int i = b0 + int(threadIdx.x);
+        const uint32_t c = i < nb ? __ldcg(g + i) : 0u;
+        uint32_t tot;
+        const uint32_t ex = sr_block_scan(c, ws, &tot);
+        if (c && run + ex < kk && run + ex + c >= kk) {
+            *s_bin = uint32_t(i);
+            *s_before = run + ex;
+        }
+        __syncthreads();
+        if (run + tot >= kk) break;  // block-uniform
+        run += tot;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kSRT, 2) score_select_rows_kernel(
+    const uint8_t* __restrict__ gplan, const uint16_t* __restrict__ clskuv, const RowTabMeta* __restrict__ meta,
+    const double* __restrict__ rowpred, const uint32_t* __restrict__ rowgid, const uint64_t* __restrict__ khash,
+    const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, int segshift, double* __restrict__ pred,
+    uint64_t* __restrict__ ids, int64_t* __restrict__ out, RowSelWork* __restrict__ W,
+    unsigned long long* __restrict__ trace) {
+    namespace cg = cooperative_groups;
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[6] = globaltimer();
+    extern __shared__ uint32_t rsm[];  // [Kuv class table | k_tile words], then the histograms; the final sort
+    __shared__ uint32_t ws[kSRT / 32];
+    __shared__ uint32_t s_bin, s_before, s_last;
+    const int tid = threadIdx.x;
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
+    const int ndk = H.ndk;
+    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
+    const int64_t* divk = at<int64_t>(gplan, H.off_divk);
+    uint32_t* sdivk = rsm + ndk * 32;
+    uint32_t* hist = sdivk + ndk;  // kSRMaxSeg bins
+    for (int i = tid; i < ndk; i += kSRT) sdivk[i] = uint32_t(divk[i]);
+    {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(clskuv);
+        for (int i = tid; i < ndk * 32; i += kSRT) rsm[i] = __ldg(src + i);
+    }
+    const int64_t groups = meta->groups;
+    const int nseg = int((groups + (int64_t(1) << segshift) - 1) >> segshift);
+    for (int i = tid; i < nseg; i += kSRT) hist[i] = 0u;
+    const uint32_t nkc = uint32_t(meta->nkc);
+    __syncthreads();
+    const uint16_t* scls = reinterpret_cast<const uint16_t*>(rsm);
+    const int64_t base = int64_t(blockIdx.x) * per * kSRT;
+    // ---- A: score, in batches of kSRBatch candidates per thread with every load of a batch in
+    //      flight together (genomes, then the row-table / group / key-hash gathers)
+    uint32_t gg[kSRPer];
+#pragma unroll
+    for (int j0 = 0; j0 < kSRPer; j0 += kSRBatch) {
+        uint64_t g[kSRBatch];
+#pragma unroll
+        for (int b = 0; b < kSRBatch; ++b) {
+            const int64_t i = base + int64_t(j0 + b) * kSRT + tid;
+            g[b] = (j0 + b < per && i < n) ? __ldcs(genome + i) : ~0ull;  // ~0: no candidate
+        }
+        uint32_t row[kSRBatch], key[kSRBatch];
+#pragma unroll
+        for (int b = 0; b < kSRBatch; ++b) {
+            const Genome x = genome_unpack(g[b]);
+            key[b] = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
+            const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
+            row[b] = key[b] * nkc + kc;
+        }
+        double p[kSRBatch];
+        uint64_t kh[kSRBatch];
+#pragma unroll
+        for (int b = 0; b < kSRBatch; ++b) {
+            const bool v = g[b] != ~0ull;
+            p[b] = v ? __ldg(rowpred + row[b]) : 0.0;
+            gg[j0 + b] = v ? __ldg(rowgid + row[b]) : 0xffffffffu;
+            kh[b] = (v && ids) ? __ldg(khash + key[b]) : 0ull;
+        }
+#pragma unroll
+        for (int b = 0; b < kSRBatch; ++b) {
+            if (g[b] == ~0ull) continue;
+            const int64_t i = base + int64_t(j0 + b) * kSRT + tid;
+            pred[i] = p[b];
+            atomicAdd(hist + (gg[j0 + b] >> segshift), 1u);
+            if (ids) {
+                const Genome x = genome_unpack(g[b]);
+                uint64_t h = fnv_small(kh[b], sdivk[x.k]);
+                h = fnv_small(h, 1u << x.u);
+                h = fnv_small(h, 1u << x.v);
+                __stcs(reinterpret_cast<unsigned long long*>(ids) + i, static_cast<unsigned long long>(h));
+            }
+        }
+    }
+    if (trace && blockIdx.x == 0 && tid == 0) trace[0] = globaltimer();
+    __syncthreads();
+    sr_flush(hist, W->seg, nseg);
+    cg::this_grid().sync();
+    if (trace && blockIdx.x == 0 && tid == 0) trace[1] = globaltimer();
+    // ---- B1: the segment of the k-th candidate, then this CTA's candidates inside it by group
+    const uint32_t kk = uint32_t(k);
+    sr_cross(W->seg, nseg, kk, ws, &s_bin, &s_before);
+    const uint32_t sstar = s_bin, cb1 = s_before;
+    const int segsz = 1 << segshift;
+    for (int i = tid; i < segsz; i += kSRT) hist[i] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j)
+        if (gg[j] != 0xffffffffu && (gg[j] >> segshift) == sstar) atomicAdd(hist + (gg[j] & uint32_t(segsz - 1)), 1u);
+    __syncthreads();
+    sr_flush(hist, W->fine, segsz);
+    cg::this_grid().sync();
+    if (trace && blockIdx.x == 0 && tid == 0) trace[2] = globaltimer();
+    // ---- B2: the k-th candidate's group; candidates below it; ties at it counted per CTA
+    sr_cross(W->fine, segsz, kk - cb1, ws, &s_bin, &s_before);
+    const uint32_t gstar = (sstar << segshift) | s_bin;
+    const uint32_t need = kk - cb1 - s_before;  // >= 1 ties to take at g*
+    uint32_t my_ties = 0;
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j) {
+        const int64_t i = base + int64_t(j) * kSRT + tid;
+        sr_append(W, gg[j] < gstar, (uint64_t(gg[j]) << 32) | uint64_t(i));
+        my_ties += gg[j] == gstar;
+    }
+    uint32_t cta_ties;
+    sr_block_scan(my_ties, ws, &cta_ties);
+    if (tid == 0) W->tiecnt[blockIdx.x] = cta_ties;
+    cg::this_grid().sync();
+    if (trace && blockIdx.x == 0 && tid == 0) trace[3] = globaltimer();
+    // ---- C: ties by index; the last CTA sorts and clears
+    uint32_t before = 0;
+    for (uint32_t b = tid; b < blockIdx.x; b += kSRT) before += __ldcg(W->tiecnt + b);
+    uint32_t tot_before;
+    sr_block_scan(before, ws, &tot_before);
+    const uint32_t quota = need > tot_before ? min(need - tot_before, cta_ties) : 0u;
+    uint32_t taken = 0;
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j) {
+        if (taken >= quota) break;  // block-uniform
+        const bool tie = gg[j] == gstar;
+        uint32_t tot;
+        const uint32_t o = sr_block_scan(tie ? 1u : 0u, ws, &tot);
+        sr_append(W, tie && taken + o < quota, (uint64_t(gstar) << 32) | uint64_t(base + int64_t(j) * kSRT + tid));
+        taken += tot;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&W->ticket, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (trace && tid == 0) trace[4] = globaltimer();
+    // bitonic sort of the k records by (g, index) in shared memory
+    const int K = int(k);
+    int P = 1;
+    while (P < K) P <<= 1;
+    unsigned long long* xk = reinterpret_cast<unsigned long long*>(rsm);
+    for (int i = tid; i < P; i += kSRT)
+        xk[i] = i < K ? __ldcg(reinterpret_cast<const unsigned long long*>(W->lkey) + i) : ~0ull;
+    for (int i = tid; i < nseg; i += kSRT) W->seg[i] = 0u;
+    for (int i = tid; i < segsz; i += kSRT) W->fine[i] = 0u;
+    __syncthreads();
+    for (int size = 2; size <= P; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = tid; i < P; i += kSRT) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool up = (i & size) == 0;
+                    if ((xk[i] > xk[j]) == up) {
+                        const unsigned long long t = xk[i];
+                        xk[i] = xk[j];
+                        xk[j] = t;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = tid; i < K; i += kSRT) out[i] = int64_t(uint32_t(xk[i]));
+    if (tid == 0) {
+        W->nlist = 0u;
+        W->ticket = 0u;
+        if (trace) trace[5] = globaltimer();
+    }
+}
+
+constexpr uint32_t kPlanSmemMax = 96 * 1024;
+
+}  // namespace
+
+int64_t rowtab_kuv_domain(const int64_t* divk, int ndk) {
+    int64_t s = 0;
+    for (int k = 0; k < ndk; ++k) {
+        int z = 0;
+        while (z < 15 && divk[k] % (int64_t(2) << z) == 0) ++z;
+        s += int64_t(z + 1) * kKuvV;
+    }
+    return s;
+}
+
+size_t rowtab_scratch_bytes(int nnodes) { return size_t(3) * size_t(nnodes > 0 ? nnodes : 1) * sizeof(double); }
+
+cudaError_t launch_key_hash(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, uint64_t* d_khash) {
+    if (nkeys <= 0) return cudaSuccess;
+    const int64_t want = (nkeys + 255) / 256;
+    const int grid = int(want < int64_t(c.sm_count) * 4 ? want : int64_t(c.sm_count) * 4);
+    key_hash_kernel<<<grid, 256, 0, c.stream>>>(d_plan, nkeys, d_khash);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rowtab_compile(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
+                                  const uint8_t* d_pred, uint32_t pred_bytes, int nnodes, int ndk, int64_t rows_cap,
+                                  void* d_scratch, RowTabMeta* d_meta, uint16_t* d_clskuv, uint32_t* d_crep,
+                                  double* d_rowpred) {
+    (void)plan_bytes;
+    (void)pred_bytes;
+    if (ndk > 1024) return cudaErrorInvalidValue;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(rowtab_classes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sizeof(ClsSmem)));
+    if (attr != cudaSuccess) return attr;
+    cudaError_t e = launch_pdl(rowtab_classes_kernel, dim3(1), dim3(kClsT), sizeof(ClsSmem), c.stream, d_plan, d_pred,
+                               static_cast<double*>(d_scratch), nnodes, d_meta, d_clskuv, d_crep);
+    if (e != cudaSuccess) return e;
+    int dev = 0, optin = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    // compact walk: 16-byte nodes + roots + the threads' feature vectors in shared memory
+    int ntrees = 0;
+    const size_t node_bytes = size_t(nnodes) * 16;
+    {  // the tree count is in the predict blob's header (host mirror not needed: bound by nnodes)
+        ntrees = nnodes;  // roots region sized for the worst case (one node per tree)
+    }
+    const size_t sm_c = ((node_bytes + size_t(ntrees) * 4 + 15) / 16) * 16 + size_t(16) * kBuildT * 8;
+    const bool compact = nnodes < 65536 && sm_c <= size_t(optin);
+    int per_sm = 0;
+    const int64_t want = (rows_cap + kBuildT - 1) / kBuildT;
+    if (compact) {
+        e = cudaFuncSetAttribute(rowtab_build_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_c));
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rowtab_build_kernel<true>, kBuildT, sm_c);
+        if (e != cudaSuccess) return e;
+        if (per_sm < 1) return cudaErrorInvalidConfiguration;
+        const int64_t cap = int64_t(c.sm_count) * per_sm;
+        e = launch_pdl(rowtab_build_kernel<true>, dim3(int(want < cap ? (want > 0 ? want : 1) : cap)), dim3(kBuildT),
+                       sm_c, c.stream, d_plan, d_pred, nnodes, d_meta, static_cast<const uint32_t*>(d_crep),
+                       d_rowpred);
+    } else {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rowtab_build_kernel<false>, kBuildT, 0);
+        if (e != cudaSuccess) return e;
+        const int64_t cap = int64_t(c.sm_count) * (per_sm > 0 ? per_sm : 1);
+        e = launch_pdl(rowtab_build_kernel<false>, dim3(int(want < cap ? (want > 0 ? want : 1) : cap)), dim3(kBuildT),
+                       0, c.stream, d_plan, d_pred, nnodes, d_meta, static_cast<const uint32_t*>(d_crep), d_rowpred);
+    }
+    note_launches(2);
+    return e;
+}
+
+cudaError_t launch_score_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,
+                              const RowTabMeta* d_meta, const double* d_rowpred, const uint64_t* d_khash,
+                              const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
+                              const SelHist& sel) {
+    if (n <= 0) return cudaSuccess;
+    const size_t sm = size_t(ndk) * 64 * 2 + size_t(ndk) * 4;
+    if (sm > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(score_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_rows_kernel, kRowsT, sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int64_t want = (n + int64_t(kRowsT) * kRowsPer - 1) / (int64_t(kRowsT) * kRowsPer);
+    const int64_t cap = int64_t(c.sm_count) * per_sm;
+    const int grid = int(want < cap ? want : cap);
+    e = launch_pdl(score_rows_kernel, dim3(grid), dim3(kRowsT), sm, c.stream, d_plan, d_clskuv, d_meta, d_rowpred,
+                   d_khash, d_genome, n, d_pred, d_ids, sel);
+    note_launches(1);
+    return e;
+}
+
+}  // namespace etune_b200
+
+namespace etune_b200 {
+
+size_t rowtab_sort_scratch_bytes(int64_t rows_cap) {
+    const int64_t nt = (rows_cap + kRsTile - 1) / kRsTile;
+    return size_t(rows_cap) * 16 + size_t(nt) * 256 * 4 + 256 * 4 + size_t(nt) * 4 + size_t((rows_cap + 31) / 32) * 4 +
+           2048;
+}
+
+cudaError_t launch_rowtab_sort(const LaunchCtx& c, RowTabMeta* d_meta, const double* d_rowpred, int64_t rows_cap,
+                               uint32_t* d_srows, uint32_t* d_rowgid, void* d_scratch) {
+    if (rows_cap <= 0) return cudaSuccess;
+    const int64_t nt64 = (rows_cap + kRsTile - 1) / kRsTile;
+    const int nt = int(nt64);
+    char* p = static_cast<char*>(d_scratch);
+    uint32_t* k0 = reinterpret_cast<uint32_t*>(p);
+    uint32_t* k1 = k0 + rows_cap;
+    uint32_t* v1 = k1 + rows_cap;
+    uint32_t* cnt = v1 + rows_cap;
+    uint32_t* tot = cnt + size_t(nt) * 256;
+    uint32_t* tcnt = tot + 256;
+    uint32_t* mark = tcnt + nt;
+    cudaError_t e = cudaMemsetAsync(mark, 0, size_t((rows_cap + 31) / 32) * 4, c.stream);
+    if (e != cudaSuccess) return e;
+    const int64_t want = (rows_cap + 255) / 256;
+    const int grid = int(want < int64_t(c.sm_count) * 8 ? want : int64_t(c.sm_count) * 8);
+    const RowTabMeta* cm = d_meta;
+    e = launch_pdl(rowtab_keys_kernel, dim3(grid), dim3(256), 0, c.stream, cm, d_rowpred, k0, d_srows);
+    uint32_t* kk[2] = {k0, k1};
+    uint32_t* vv[2] = {d_srows, v1};
+    int cur = 0;
+    for (int shift = 0; shift < 32 && e == cudaSuccess; shift += 8) {  // four passes: the result ends in k0 / d_srows
+        e = launch_pdl(rs_hist_kernel, dim3(nt), dim3(kRsT), 0, c.stream, cm, static_cast<const uint32_t*>(kk[cur]),
+                       shift, nt, cnt);
+        if (e == cudaSuccess) e = launch_pdl(rs_scan_kernel, dim3(256), dim3(256), 0, c.stream, cnt, nt, tot);
+        if (e == cudaSuccess)
+            e = launch_pdl(rs_scatter_kernel, dim3(nt), dim3(kRsT), 0, c.stream, cm,
+                           static_cast<const uint32_t*>(kk[cur]), static_cast<const uint32_t*>(vv[cur]), shift,
+                           static_cast<const uint32_t*>(cnt), static_cast<const uint32_t*>(tot), nt, kk[cur ^ 1],
+                           vv[cur ^ 1]);
+        cur ^= 1;
+    }
+    const uint32_t* ck0 = k0;
+    const uint32_t* csr = d_srows;
+    if (e == cudaSuccess)
+        e = launch_pdl(rowtab_inv_kernel, dim3(grid), dim3(256), 0, c.stream, cm, d_rowpred, ck0, csr, mark);
+    if (e == cudaSuccess)
+        e = launch_pdl(rowtab_runsort_kernel, dim3(grid), dim3(256), 0, c.stream, cm, d_rowpred, ck0, d_srows, mark);
+    if (e == cudaSuccess)
+        e = launch_pdl(rowtab_gcount_kernel, dim3(nt), dim3(kRsT), 0, c.stream, cm, d_rowpred, csr, tcnt);
+    if (e == cudaSuccess) e = launch_pdl(rowtab_gscan_kernel, dim3(1), dim3(1024), 0, c.stream, d_meta, tcnt, nt);
+    if (e == cudaSuccess)
+        e = launch_pdl(rowtab_gapply_kernel, dim3(nt), dim3(kRsT), 0, c.stream, cm, d_rowpred, csr,
+                       static_cast<const uint32_t*>(tcnt), d_rowgid);
+    note_launches(1 + 12 + 5);
+    return e;
+}
+
+size_t rowsel_work_bytes() { return sizeof(RowSelWork); }
+
+int rowsel_segshift(int64_t rows_cap) {
+    int sh = 8;
+    while ((rows_cap >> sh) >= kSRMaxSeg) ++sh;
+    return sh;
+}
+
+cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,
+                                     const RowTabMeta* d_meta, const double* d_rowpred, const uint32_t* d_rowgid,
+                                     int64_t rows_cap, const uint64_t* d_khash, const uint64_t* d_genome, int64_t n,
+                                     int64_t k, double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work) {
+    if (n <= 0 || k <= 0) return cudaSuccess;
+    if (k > kSelMaxK || k > n) return cudaErrorInvalidValue;
+    int segshift = rowsel_segshift(rows_cap);
+    if ((1 << segshift) > kSRMaxSeg) return cudaErrorNotSupported;
+    size_t sm = size_t(ndk) * 64 * 2 + size_t(ndk) * 4 + size_t(kSRMaxSeg) * 4;
+    const size_t sort_sm = size_t(kSelMaxK) * 8;
+    if (sm < sort_sm) sm = sort_sm;
+    static int per_sm = -1;
+    static size_t attr_sm = 0;
+    if (sm > attr_sm) {
+        cudaError_t e = cudaFuncSetAttribute(score_select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(sm));
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_select_rows_kernel, kSRT, sm);
+        if (e != cudaSuccess) return e;
+        attr_sm = sm;
+    }
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t gmax = int64_t(c.sm_count) * per_sm;
+    if (gmax > kSRMaxCtas) gmax = kSRMaxCtas;
+    const int64_t per = (n + gmax * kSRT - 1) / (gmax * kSRT);
+    if (per > kSRPer) return cudaErrorNotSupported;
+    const int64_t grid = (n + per * kSRT - 1) / (per * kSRT);
+    int per_i = int(per);
+    RowSelWork* W = static_cast<RowSelWork*>(d_work);
+    // ETUNE_ROWSEL_TRACE=1 (diagnostic): globaltimer at each phase boundary, printed per call
+    static const bool want_trace = std::getenv("ETUNE_ROWSEL_TRACE") != nullptr;
+    static unsigned long long* trace = nullptr;
+    if (want_trace && !trace) cudaMallocManaged(&trace, 8 * sizeof(unsigned long long));
+    unsigned long long* tr = want_trace ? trace : nullptr;
+    void* args[] = {(void*)&d_plan,   (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowpred, (void*)&d_rowgid,
+                    (void*)&d_khash,  (void*)&d_genome, (void*)&n,      (void*)&k,         (void*)&per_i,
+                    (void*)&segshift, (void*)&d_pred,   (void*)&d_ids,  (void*)&d_idx,     (void*)&W,
+                    (void*)&tr};
+    note_launches(1);
+    const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(score_select_rows_kernel),
+                                                      dim3(unsigned(grid)), dim3(kSRT), args, sm, c.stream);
+    if (tr && e == cudaSuccess) {
+        cudaStreamSynchronize(c.stream);
+        std::fprintf(stderr, "rowsel n=%lld grid=%lld per=%d: A %.2f | sync1 %.2f | B1+sync2 %.2f | B2+sync3 %.2f | "
+                     "C->last %.2f | sort %.2f us\n", (long long)n, (long long)grid, per_i,
+                     (tr[0] - tr[6]) * 1e-3, (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3,
+                     (tr[4] - tr[3]) * 1e-3, (tr[5] - tr[4]) * 1e-3);
+    }
+    return e;
+}
+
+}  // namespace etune_b200

@@ -21,6 +21,7 @@
 
 #include "kernels.hpp"
 #include "pdl.cuh"
+#include "selbin.cuh"
 
 namespace etune_b200 {
 
@@ -351,8 +352,15 @@ __global__ void __launch_bounds__(kCoopT, 1) topk_coop_kernel(const double* __re
 // ------------------------------------------------------- stable LSD radix sort
 constexpr int kLsdT = 512;
 
+// dn / dbits (nullable): item count and key bit length read from device memory (a sort whose
+// size is only known on the device, e.g. the row table's rows); passes at or beyond dbits are
+// skipped (the scatter copies its tile through so the ping-pong buffers stay consistent).
 __global__ void __launch_bounds__(kLsdT) lsd_hist_kernel(const uint64_t* __restrict__ keys, int64_t n, int shift,
-                                                        uint32_t* __restrict__ hist, int ntiles) {
+                                                        uint32_t* __restrict__ hist, int ntiles,
+                                                        const int64_t* __restrict__ dn,
+                                                        const int32_t* __restrict__ dbits) {
+    if (dbits && shift >= *dbits) return;
+    if (dn) n = *dn;
     __shared__ uint32_t h[256];
     for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
     __syncthreads();
@@ -367,7 +375,9 @@ __global__ void __launch_bounds__(kLsdT) lsd_hist_kernel(const uint64_t* __restr
 }
 
 // exclusive scan of hist[256][ntiles] in digit-major order: warp per digit row
-__global__ void __launch_bounds__(1024) lsd_scan_kernel(uint32_t* __restrict__ hist, int ntiles) {
+__global__ void __launch_bounds__(1024) lsd_scan_kernel(uint32_t* __restrict__ hist, int ntiles, int shift,
+                                                        const int32_t* __restrict__ dbits) {
+    if (dbits && shift >= *dbits) return;
     __shared__ uint32_t tot[256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int d = warp; d < 256; d += 32) {
@@ -409,7 +419,18 @@ __global__ void __launch_bounds__(1024) lsd_scan_kernel(uint32_t* __restrict__ h
 __global__ void __launch_bounds__(kLsdT) lsd_scatter_kernel(const uint64_t* __restrict__ kin,
                                                            const uint32_t* __restrict__ vin, int64_t n, int shift,
                                                            const uint32_t* __restrict__ offs, int ntiles,
-                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+                                                           uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                           const int64_t* __restrict__ dn,
+                                                           const int32_t* __restrict__ dbits) {
+    if (dn) n = *dn;
+    if (dbits && shift >= *dbits) {  // skipped pass: carry the tile over unchanged
+        for (int64_t i = int64_t(blockIdx.x) * kTile + threadIdx.x; i < n && i < int64_t(blockIdx.x + 1) * kTile;
+             i += blockDim.x) {
+            kout[i] = kin[i];
+            vout[i] = vin[i];
+        }
+        return;
+    }
     constexpr int W = kLsdT / 32;
     __shared__ uint32_t base[256];
     __shared__ uint32_t gofs[256];
@@ -515,7 +536,7 @@ SelLayout sel_layout(void* base, int64_t n) {
 constexpr int kFiltPer = 8;
 
 __global__ void __launch_bounds__(kSelT) sel_filter_kernel(const double* __restrict__ score, int64_t n, int64_t k,
-                                                           SelLayout L, const SelHist sel) {
+                                                           SelLayout L, const SelHist sel_in) {
     __shared__ unsigned int scanbuf[72];
     __shared__ unsigned int s_d;
     const int tid = threadIdx.x;
@@ -528,6 +549,7 @@ __global__ void __launch_bounds__(kSelT) sel_filter_kernel(const double* __restr
         v[r] = 0.0;
     }
     pdl_wait();
+    const SelHist sel = sel_resolve(sel_in);  // device-resident bounds: written by an earlier kernel
 #pragma unroll
     for (int r = 0; r < kFiltPer; ++r) {
         const int64_t j = base + r * kSelT + tid;
@@ -1000,15 +1022,42 @@ cudaError_t launch_sort_pairs(const LaunchCtx& c, uint64_t* keys, uint32_t* vals
     uint32_t* vv[2] = {vals, v2};
     int cur = 0;
     for (int shift = 0; shift < bits; shift += 8) {
-        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], n, shift, hist, kt);
-        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(hist, kt);
-        lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], vv[cur], n, shift, hist, kt, kk[cur ^ 1], vv[cur ^ 1]);
+        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], n, shift, hist, kt, nullptr, nullptr);
+        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(hist, kt, shift, nullptr);
+        lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], vv[cur], n, shift, hist, kt, kk[cur ^ 1], vv[cur ^ 1],
+                                                       nullptr, nullptr);
         cur ^= 1;
         note_launches(3);
     }
     if (cur) {
         cudaMemcpyAsync(keys, k2, 8 * size_t(n), cudaMemcpyDeviceToDevice, c.stream);
         cudaMemcpyAsync(vals, v2, 4 * size_t(n), cudaMemcpyDeviceToDevice, c.stream);
+    }
+    return cudaGetLastError();
+}
+
+// Same sort with the item count (<= n_cap) and key bit length in device memory: all eight
+// 8-bit passes are launched, those at or beyond *d_bits only copy through.  Result in place.
+cudaError_t launch_sort_pairs_dev(const LaunchCtx& c, uint64_t* keys, uint32_t* vals, int64_t n_cap,
+                                  const int64_t* d_n, const int32_t* d_bits, void* scratch) {
+    if (n_cap <= 0) return cudaSuccess;
+    char* p = static_cast<char*>(scratch);
+    uint64_t* k2 = reinterpret_cast<uint64_t*>(p);
+    p += al256(8 * size_t(n_cap));
+    uint32_t* v2 = reinterpret_cast<uint32_t*>(p);
+    p += al256(4 * size_t(n_cap));
+    uint32_t* hist = reinterpret_cast<uint32_t*>(p);
+    const int kt = int((n_cap + kTile - 1) / kTile);
+    uint64_t* kk[2] = {keys, k2};
+    uint32_t* vv[2] = {vals, v2};
+    int cur = 0;
+    for (int shift = 0; shift < 64; shift += 8) {  // eight passes: the data ends in keys / vals
+        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], n_cap, shift, hist, kt, d_n, d_bits);
+        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(hist, kt, shift, d_bits);
+        lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(kk[cur], vv[cur], n_cap, shift, hist, kt, kk[cur ^ 1],
+                                                       vv[cur ^ 1], d_n, d_bits);
+        cur ^= 1;
+        note_launches(3);
     }
     return cudaGetLastError();
 }
@@ -1073,10 +1122,10 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
     const int kt = int((k + kTile - 1) / kTile);
     int cur = 0;
     for (int shift = 0; shift < 64; shift += 8) {
-        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(sk[cur], k, shift, lsd_hist, kt);
-        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(lsd_hist, kt);
+        lsd_hist_kernel<<<kt, kLsdT, 0, c.stream>>>(sk[cur], k, shift, lsd_hist, kt, nullptr, nullptr);
+        lsd_scan_kernel<<<1, 1024, 0, c.stream>>>(lsd_hist, kt, shift, nullptr);
         lsd_scatter_kernel<<<kt, kLsdT, 0, c.stream>>>(sk[cur], sv[cur], k, shift, lsd_hist, kt, sk[cur ^ 1],
-                                                        sv[cur ^ 1]);
+                                                        sv[cur ^ 1], nullptr, nullptr);
         cur ^= 1;
         note_launches(3);
     }

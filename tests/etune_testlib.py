@@ -334,6 +334,8 @@ class RefLib(_Lib):
         L.ref_energy_loss.argtypes = [C.c_double, C.c_double, F64P]
         L.ref_spearman.argtypes = [F64P, F64P, C.c_int64, C.POINTER(C.c_double)]
         L.ref_score_threads.argtypes = [I64P, I64P, C.c_int64, C.c_int, C.c_void_p, C.c_int, F64P]
+        L.ref_score_select_threads.argtypes = [I64P, I64P, C.c_int64, C.c_int, C.c_void_p, C.c_int, C.c_int64,
+                                               F64P, I64P]
 
     def parse(self, text):
         out = np.zeros(12, np.int64)
@@ -530,6 +532,16 @@ class RefModel:
         out = np.zeros(len(sched), np.float64)
         self.lib._check(self.lib.L.ref_score_threads(op, sched, len(sched), num_sms, self.h, threads, out))
         return out
+
+    def score_select_threads(self, op, sched, threads, k, num_sms=108):
+        """extract_features + predict + k best by (prediction, index), all on `threads` threads
+        (ref_shim.cpp ref_score_select_threads) -> (predictions, sorted indices)."""
+        sched = np.ascontiguousarray(sched, np.int64).reshape(-1, 12)
+        out = np.zeros(len(sched), np.float64)
+        idx = np.zeros(max(k, 1), np.int64)
+        self.lib._check(self.lib.L.ref_score_select_threads(op, sched, len(sched), num_sms, self.h, threads, int(k),
+                                                            out, idx))
+        return out, idx[:k]
 
 
 def have_ref() -> bool:

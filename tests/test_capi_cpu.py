@@ -17,7 +17,7 @@ def test_exports_every_header_symbol():
 
 
 def test_abi_version_and_defaults():
-    assert capi.lib().etune_cu_abi_version() == 1
+    assert capi.lib().etune_cu_abi_version() == 2
     d = capi.default_device_config()
     assert d.num_sms == 108 and d.constant_power_w == 60.0 and d.rng_seed == 1234  # device.hpp:17-36
 
