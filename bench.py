@@ -490,8 +490,16 @@ def run_ours(args):
 
     round_latency = None
     cpu_round = None
-    if rank == 0 and world == 1 and not args.no_search:
+    if not args.no_search:
+        # N>1: the population-sharded search (per-shard latency filter + merge, measurements split
+        # over the ranks, training on rank 0 + model broadcast, all over the ctx's NCCL communicator)
         round_latency = search_round_latency(ctx, capi, args.search_rounds)
+        if world > 1:
+            t = torch.tensor([round_latency["value"]], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            round_latency["value"] = t.item()
+            round_latency["sharded_over_ranks"] = world
+    if rank == 0 and world == 1 and not args.no_search:
         if not args.no_cpu_baseline:
             try:
                 cpu_round = cpu_round_baseline(round_latency)

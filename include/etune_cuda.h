@@ -125,6 +125,13 @@ etune_status etune_cu_ctx_create(int device, void* stream, etune_cu_ctx** out);
 etune_status etune_cu_ctx_destroy(etune_cu_ctx* ctx);
 etune_status etune_cu_ctx_set_stream(etune_cu_ctx* ctx, void* stream);
 void* etune_cu_ctx_stream(etune_cu_ctx* ctx);
+/* Device memory and copies on the ctx's device / stream, so a C or C++ caller (e.g. the reference-side
+ * binding) needs no CUDA runtime of its own.  The copies are asynchronous on the ctx
+ * stream (host memory pinned or pageable); etune_cu_synchronize waits for them. */
+etune_status etune_cu_device_alloc(etune_cu_ctx* ctx, void** out, int64_t bytes);
+etune_status etune_cu_device_free(etune_cu_ctx* ctx, void* p);
+etune_status etune_cu_memcpy_h2d(etune_cu_ctx* ctx, void* d_dst, const void* h_src, int64_t bytes);
+etune_status etune_cu_memcpy_d2h(etune_cu_ctx* ctx, void* h_dst, const void* d_src, int64_t bytes);
 /* Waits for the ctx stream; reports a device-detected data error (first bad index). */
 etune_status etune_cu_synchronize(etune_cu_ctx* ctx, int64_t* first_bad_index);
 
@@ -395,6 +402,18 @@ etune_status etune_cu_reproduce(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                 uint64_t* d_offspring, int32_t* d_partner /*nullable*/,
                                 uint64_t* d_ids /*nullable*/);
 
+/* reproduce with the opt-in counter-based RNG (NOT the reference's stream): the same decisions,
+ * transforms and word order per offspring (coin, knob, Lemire draws, partner redraws, mask, repair),
+ * but offspring i draws from its own stream word_j = splitmix64(key_i + j), key_i =
+ * splitmix64(seed ^ splitmix64(i)), so the generation has no sequential chain: one thread per
+ * offspring (2^20 offspring in about a millisecond, where the exact mode resolves the reference's
+ * one mt19937_64 stream on a single CTA).  Its oracle is orc_reproduce_counter (oracle/), bit for
+ * bit.  Same arguments and errors as etune_cu_reproduce. */
+etune_status etune_cu_reproduce_counter(etune_cu_ctx* ctx, const etune_cu_plan* plan,
+                                        const uint64_t* d_parents, int64_t num_parents, int64_t n,
+                                        const etune_genetic_rates* rates, uint64_t seed,
+                                        uint64_t* d_offspring, int32_t* d_partner /*nullable*/,
+                                        uint64_t* d_ids /*nullable*/);
 /* ------------------------------------------------------------- selection */
 /* The k smallest of d_score[0..n) under the total order (score asc, index asc)
  * ("lowest predicted energy"; SURVEY H3 tie rule), written sorted to
@@ -430,7 +449,7 @@ typedef struct etune_search_config {
     int32_t latency_only;      /* 1: run_latency_only: no cost model; parents = the
                                   ceil(M/2) fastest of the M; best = lowest latency (then id), whose
                                   energy is measured for the report (one measurement per round) */
-    int32_t reserved0;
+    int32_t counter_rng;       /* 1: reproduce with etune_cu_reproduce_counter (not the reference's stream) */
 } etune_search_config;
 
 typedef struct etune_round_report {   /* RoundReport */
@@ -474,6 +493,19 @@ etune_status etune_cu_search_parents(etune_cu_search* s, uint64_t* d_out, int64_
  * broadcast of trained model arrays (north_star); everything else is shard-local. */
 #define ETUNE_NCCL_UNIQUE_ID_BYTES 128
 etune_status etune_cu_nccl_unique_id(void* out_id /* ETUNE_NCCL_UNIQUE_ID_BYTES */);
+/* Caller-provided collectives, used when no NCCL communicator is attached (e.g. ranks that
+ * share one GPU, or a host-side transport in tests).  Device pointers on the ctx's device;
+ * `stream` is the ctx stream (cudaStream_t): the callback must order its work after the
+ * stream's pending work and before the stream's subsequent work (synchronising it is enough).
+ * allgather: every rank contributes `bytes` at d_send; d_recv receives nranks * bytes in rank
+ * order.  broadcast: root's d_buf to every rank.  Return 0 on success.  NULL detaches. */
+typedef struct etune_transport {
+    void* user;
+    int32_t nranks, rank;
+    int32_t (*allgather)(void* user, const void* d_send, void* d_recv, int64_t bytes, void* stream);
+    int32_t (*broadcast)(void* user, void* d_buf, int64_t bytes, int32_t root, void* stream);
+} etune_transport;
+etune_status etune_cu_ctx_attach_transport(etune_cu_ctx* ctx, const etune_transport* t);
 /* Collective over all ranks: binds an NCCL communicator to the ctx (its device/stream). */
 etune_status etune_cu_ctx_attach_nccl(etune_cu_ctx* ctx, const void* unique_id, int nranks, int rank);
 

@@ -301,7 +301,8 @@ struct Mt64 {
 
 // libstdc++ uniform_int_distribution<size_t>(0, range-1) on a 64-bit engine:
 // _S_nd<unsigned __int128> (Lemire, threshold (-range % range)).
-uint64_t lemire(Mt64& g, uint64_t range) {
+template <typename G>
+uint64_t lemire(G& g, uint64_t range) {
     unsigned __int128 prod = static_cast<unsigned __int128>(g()) * range;
     uint64_t low = static_cast<uint64_t>(prod);
     if (low < range) {
@@ -314,10 +315,12 @@ uint64_t lemire(Mt64& g, uint64_t range) {
     return static_cast<uint64_t>(prod >> 64);
 }
 // uniform_int_distribution<size_t>(a, b)
-uint64_t uniform_ab(Mt64& g, uint64_t a, uint64_t b) { return lemire(g, b - a + 1) + a; }
+template <typename G>
+uint64_t uniform_ab(G& g, uint64_t a, uint64_t b) { return lemire(g, b - a + 1) + a; }
 
 // uniform_real_distribution<double>(0,1) == generate_canonical<double,53>: one word.
-double canonical(Mt64& g) {
+template <typename G>
+double canonical(G& g) {
     double r = static_cast<double>(g()) / 18446744073709551616.0;
     if (r >= 1.0) r = std::nextafter(1.0, 0.0);
     return r;
@@ -391,8 +394,8 @@ std::vector<int64_t> legal_vectors(int64_t ptn, const Limits& l) {  // genetic.c
         if (ptn % v == 0) out.push_back(v);
     return out;
 }
-template <typename T>
-T pick_different(const std::vector<T>& opts, const T& avoid, Mt64& g) {  // genetic.cpp:32-44
+template <typename T, typename G>
+T pick_different(const std::vector<T>& opts, const T& avoid, G& g) {  // genetic.cpp:32-44
     if (opts.size() <= 1) return opts.empty() ? avoid : opts.front();
     std::vector<T> alt;
     for (const T& o : opts)
@@ -401,7 +404,8 @@ T pick_different(const std::vector<T>& opts, const T& avoid, Mt64& g) {  // gene
     return alt[uniform_ab(g, 0, alt.size() - 1)];
 }
 
-Sched mutate_knob(const Op& o, const Sched& s, int knob, const Limits& l, Mt64& g) {
+template <typename G>
+Sched mutate_knob(const Op& o, const Sched& s, int knob, const Limits& l, G& g) {
     // genetic.cpp:60-87
     const Nest nest = op_nest(o);
     Sched out = s;
@@ -425,7 +429,8 @@ Sched mutate_knob(const Op& o, const Sched& s, int knob, const Limits& l, Mt64& 
     return out;
 }
 
-int repair(const Op& o, Sched s, const Limits& l, Mt64& g, Sched* out) {  // genetic.cpp:89-135
+template <typename G>
+int repair(const Op& o, Sched s, const Limits& l, G& g, Sched* out) {  // genetic.cpp:89-135
     const int64_t cap = std::min<int64_t>(l.max_block, 1024);
     const Nest nest = op_nest(o);
     const int64_t ext[3] = {nest.b, nest.m, nest.n};
@@ -732,10 +737,22 @@ int orc_sample_random(const int64_t* op, int64_t n, uint64_t seed, const int64_t
     return OK;
 }
 
-int orc_reproduce(const int64_t* op, const int64_t* parent_sched, int64_t num_parents, int64_t n,
-                  const double* rates, uint64_t seed, const int64_t* limits, int64_t* out_sched,
-                  uint64_t* out_ids, uint64_t* out_lineage, int8_t* out_lineage_len) {
-    // genetic.cpp:137-187
+}  // extern "C"
+
+namespace {
+// Counter-based word source of the opt-in counter reproduce mode (breed.cu CounterCursor): offspring
+// i draws word_j = splitmix64(key_i + j) with key_i = splitmix64(seed ^ splitmix64(i)).
+struct CounterGen {
+    uint64_t key, j = 0;
+    uint64_t operator()() { return splitmix(key + (j++)); }
+};
+
+// genetic.cpp:137-187 with the offspring's word source from `gen_of(i)` (the reference's one
+// mt19937_64 stream, or a counter-based stream per offspring)
+template <typename GenOf>
+int reproduce_body(const int64_t* op, const int64_t* parent_sched, int64_t num_parents, int64_t n,
+                   const double* rates, const int64_t* limits, int64_t* out_sched, uint64_t* out_ids,
+                   uint64_t* out_lineage, int8_t* out_lineage_len, GenOf gen_of) {
     if (num_parents < 1) return fail(VALIDATION, "reproduce requires at least one parent");
     const Op o = op_of(op);
     const Limits l = limits_of(limits);
@@ -748,8 +765,8 @@ int orc_reproduce(const int64_t* op, const int64_t* parent_sched, int64_t num_pa
         par[p] = sched_of(parent_sched + 12 * p);
         pid[p] = cand_id(o, par[p]);
     }
-    Mt64 g(seed);
     for (int64_t i = 0; i < n; ++i) {
+        auto& g = gen_of(i);
         const size_t bi = static_cast<size_t>(i) % par.size();
         const double u = canonical(g) * total;
         Sched s;
@@ -789,6 +806,30 @@ int orc_reproduce(const int64_t* op, const int64_t* parent_sched, int64_t num_pa
         out_ids[i] = cand_id(o, s);
     }
     return OK;
+}
+}  // namespace
+
+extern "C" {
+
+int orc_reproduce(const int64_t* op, const int64_t* parent_sched, int64_t num_parents, int64_t n,
+                  const double* rates, uint64_t seed, const int64_t* limits, int64_t* out_sched,
+                  uint64_t* out_ids, uint64_t* out_lineage, int8_t* out_lineage_len) {
+    Mt64 g(seed);  // ONE sequential stream for the whole generation (genetic.cpp:155)
+    return reproduce_body(op, parent_sched, num_parents, n, rates, limits, out_sched, out_ids, out_lineage,
+                          out_lineage_len, [&](int64_t) -> Mt64& { return g; });
+}
+
+/* The opt-in counter mode (etune_cu_reproduce_counter): the same decisions, each offspring on its own
+ * counter-based stream.  Test infrastructure like every orc_* function. */
+int orc_reproduce_counter(const int64_t* op, const int64_t* parent_sched, int64_t num_parents, int64_t n,
+                          const double* rates, uint64_t seed, const int64_t* limits, int64_t* out_sched,
+                          uint64_t* out_ids, uint64_t* out_lineage, int8_t* out_lineage_len) {
+    CounterGen g{0};
+    return reproduce_body(op, parent_sched, num_parents, n, rates, limits, out_sched, out_ids, out_lineage,
+                          out_lineage_len, [&](int64_t i) -> CounterGen& {
+                              g = CounterGen{splitmix(seed ^ splitmix(static_cast<uint64_t>(i)))};
+                              return g;
+                          });
 }
 
 int orc_predict(const int32_t* feature, const double* threshold, const int32_t* left,

@@ -83,7 +83,7 @@ class SearchConfig(C.Structure):
                 ("mu_db", C.c_double), ("improve_rel", C.c_double), ("rng_seed", C.c_uint64),
                 ("rates", GeneticRates), ("boost", BoostParams), ("backend", C.c_int32),
                 ("latency_reps", C.c_int32), ("nvml", NvmlParams), ("latency_only", C.c_int32),
-                ("reserved0", C.c_int32)]
+                ("counter_rng", C.c_int32)]
 
 
 class RoundReport(C.Structure):
@@ -112,6 +112,15 @@ class SamplesHost(C.Structure):
 _VP = C.c_void_p
 _I64 = C.c_int64
 _PTR = C.c_void_p
+
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+_BROADCAST_FN = C.CFUNCTYPE(C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p)
+
+
+class Transport(C.Structure):
+    """etune_transport (include/etune_cuda.h): caller-provided collectives."""
+    _fields_ = [("user", C.c_void_p), ("nranks", C.c_int32), ("rank", C.c_int32), ("allgather", _ALLGATHER_FN),
+                ("broadcast", _BROADCAST_FN)]
 
 _SIGS = {
     "etune_default_device_config": (None, [C.POINTER(DeviceConfig)]),
@@ -181,6 +190,11 @@ _SIGS = {
     "etune_cu_ctx_attach_nccl": (C.c_int, [_VP, _PTR, C.c_int, C.c_int]),
     "etune_cu_topk_sharded": (C.c_int, [_VP, _PTR, _I64, _I64, _I64, _PTR, _PTR]),
     "etune_cu_broadcast": (C.c_int, [_VP, _PTR, _I64, C.c_int]),
+    "etune_cu_ctx_attach_transport": (C.c_int, [_VP, C.POINTER(Transport)]),
+    "etune_cu_device_alloc": (C.c_int, [_VP, C.POINTER(_VP), _I64]),
+    "etune_cu_device_free": (C.c_int, [_VP, _VP]),
+    "etune_cu_memcpy_h2d": (C.c_int, [_VP, _PTR, _PTR, _I64]),
+    "etune_cu_memcpy_d2h": (C.c_int, [_VP, _PTR, _PTR, _I64]),
     "etune_default_search_config": (None, [C.POINTER(SearchConfig)]),
     "etune_cu_search_create": (C.c_int, [_VP, _VP, C.POINTER(SearchConfig), C.POINTER(_VP)]),
     "etune_cu_search_destroy": (C.c_int, [_VP]),
@@ -192,6 +206,8 @@ _SIGS = {
     "etune_cu_search_parents": (C.c_int, [_VP, _PTR, _I64, C.POINTER(_I64)]),
     "etune_cu_reproduce": (C.c_int, [_VP, _VP, _PTR, _I64, _I64, C.POINTER(GeneticRates), C.c_uint64, _PTR, _PTR,
                                      _PTR]),
+    "etune_cu_reproduce_counter": (C.c_int, [_VP, _VP, _PTR, _I64, _I64, C.POINTER(GeneticRates), C.c_uint64, _PTR,
+                                             _PTR, _PTR]),
 }
 
 _lib = None
@@ -378,17 +394,19 @@ class Plan:
         return (f, ids) if with_ids else f
 
 
-def reproduce(plan: "Plan", parents, n: int, seed: int, rates=(0.85, 0.10, 0.05)):
+def reproduce(plan: "Plan", parents, n: int, seed: int, rates=(0.85, 0.10, 0.05), counter: bool = False):
     """reproduce (genetic.cpp:137-187) on device genomes -> (offspring genomes, partner idx, ids).
-    Offspring i's base parent is i % len(parents); partner[i] = -1 unless a crossover."""
+    Offspring i's base parent is i % len(parents); partner[i] = -1 unless a crossover.
+    counter=True: the opt-in counter-based RNG mode (etune_cu_reproduce_counter), not the reference's stream."""
     import torch
     dev = parents.device
     out = torch.empty(n, dtype=torch.int64, device=dev)
     partner = torch.empty(n, dtype=torch.int32, device=dev)
     ids = torch.empty(n, dtype=torch.int64, device=dev)
     r = GeneticRates(*[float(x) for x in rates])
-    _check(lib().etune_cu_reproduce(plan.ctx.h, plan.h, _ptr(parents), parents.shape[0], n, C.byref(r),
-                                    C.c_uint64(seed), _ptr(out), _ptr(partner), _ptr(ids)))
+    fn = lib().etune_cu_reproduce_counter if counter else lib().etune_cu_reproduce
+    _check(fn(plan.ctx.h, plan.h, _ptr(parents), parents.shape[0], n, C.byref(r), C.c_uint64(seed), _ptr(out),
+              _ptr(partner), _ptr(ids)))
     return out, partner, ids
 
 
@@ -598,6 +616,62 @@ def nccl_unique_id() -> bytes:
 def attach_nccl(ctx: Context, unique_id: bytes, nranks: int, rank: int):
     buf = C.create_string_buffer(bytes(unique_id), 128)
     _check(lib().etune_cu_ctx_attach_nccl(ctx.h, buf, int(nranks), int(rank)))
+
+
+class _CudaBuf:
+    """A raw device range as a torch tensor (__cuda_array_interface__), no copy."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (int(nbytes),), "typestr": "|u1", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _dev_bytes(ptr: int, nbytes: int):
+    import torch
+    return torch.as_tensor(_CudaBuf(ptr, nbytes), device="cuda")
+
+
+def attach_torch_transport(ctx: Context, group=None):
+    """Route the library's collectives (per-shard top-k all-gather, model broadcast) through
+    torch.distributed (any backend -- gloo lets several ranks share one GPU) instead of NCCL.
+    The callbacks synchronise the device, stage through host memory and synchronise again."""
+    import traceback
+
+    import torch
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+
+    def allgather(user, d_send, d_recv, nbytes, stream):
+        try:
+            torch.cuda.synchronize()
+            src = _dev_bytes(d_send, nbytes).cpu() if nbytes else torch.empty(0, dtype=torch.uint8)
+            outs = [torch.empty(int(nbytes), dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(outs, src, group=group)
+            if nbytes:
+                _dev_bytes(d_recv, nbytes * world).copy_(torch.cat(outs).cuda())
+            torch.cuda.synchronize()
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+    def broadcast(user, d_buf, nbytes, root, stream):
+        try:
+            torch.cuda.synchronize()
+            buf = _dev_bytes(d_buf, nbytes)
+            host = buf.cpu()
+            dist.broadcast(host, src=int(root), group=group)
+            buf.copy_(host.cuda())
+            torch.cuda.synchronize()
+            return 0
+        except Exception:
+            traceback.print_exc()
+            return 1
+
+    t = Transport(None, world, rank, _ALLGATHER_FN(allgather), _BROADCAST_FN(broadcast))
+    ctx._transport = t  # the callbacks must outlive the ctx's use of them
+    _check(lib().etune_cu_ctx_attach_transport(ctx.h, C.byref(t)))
+    return ctx
 
 
 def topk_sharded(ctx: Context, score, global_offset: int, k: int, idx=None, sc=None):

@@ -65,7 +65,8 @@ struct Cursor {
 
 // uniform_int_distribution<size_t>(0, r-1)(rng) of libstdc++ (GCC 13) on a 64-bit
 // engine: Lemire's multiply-shift with the (-r % r) rejection threshold.
-__device__ __forceinline__ uint64_t lemire(Cursor& c, uint64_t r) {
+template <typename Cur>
+__device__ __forceinline__ uint64_t lemire(Cur& c, uint64_t r) {
     uint64_t x = c.next();
     uint64_t lo = x * r;
     uint64_t hi = __umul64hi(x, r);
@@ -99,7 +100,8 @@ struct Child {
 
 // pick_different over options {0..m-1} (index space) avoiding index `a` that is one
 // of them: alternatives are all options but `a`, in order (genetic.cpp:32-44).
-__device__ __forceinline__ uint32_t pick_other(Cursor& c, uint32_t m, uint32_t a) {
+template <typename Cur>
+__device__ __forceinline__ uint32_t pick_other(Cur& c, uint32_t m, uint32_t a) {
     if (m <= 1) return a;
     const uint32_t j = uint32_t(lemire(c, m - 1));
     return j < a ? j : j + 1;
@@ -108,7 +110,8 @@ __device__ __forceinline__ uint32_t pick_other(Cursor& c, uint32_t m, uint32_t a
 // pick_different over the power-of-two list {2^0..2^cap} avoiding 2^a (a may lie
 // outside the list: then every option is an alternative) — legal_unrolls /
 // legal_vectors in log2 form (genetic.cpp:11-29).
-__device__ __forceinline__ uint32_t pick_pow2(Cursor& c, uint32_t cap, uint32_t a) {
+template <typename Cur>
+__device__ __forceinline__ uint32_t pick_pow2(Cur& c, uint32_t cap, uint32_t a) {
     const uint32_t m = cap + 1;
     if (m <= 1) return 0;  // options.front() == 1
     if (a <= cap) {
@@ -118,10 +121,37 @@ __device__ __forceinline__ uint32_t pick_pow2(Cursor& c, uint32_t cap, uint32_t 
     return uint32_t(lemire(c, m));
 }
 
+// Counter-based word source (opt-in "counter" reproduce mode, etune_cu_reproduce_counter): offspring
+// i draws its own stream word_j = splitmix64(key_i + j), key_i = splitmix64(seed ^ splitmix64(i)),
+// so every offspring is independent of the others (one thread each) while consuming the words in
+// exactly the reference's order and transforms (canonical, Lemire, masks).  Not the reference's
+// mt19937_64 stream: its oracle is orc_reproduce_counter (oracle/etune_oracle.cpp).
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+struct CounterCursor {
+    uint64_t key;
+    uint64_t p;  // words drawn
+    bool ok;
+    __device__ __forceinline__ uint64_t next() { return splitmix64(key + (p++)); }
+};
+
 // One offspring evaluated at word offset `start` (genetic.cpp:160-185).
+template <typename Cur>
+__device__ Child breed_body(const BreedConst& K, const PlanHdr& H, int64_t i, Cur& c, uint64_t start);
+
 __device__ Child breed_one(const BreedConst& K, const PlanHdr& H, int64_t i, const uint64_t* ring, uint64_t start,
                            uint64_t hi) {
     Cursor c{ring, start, hi, true};
+    return breed_body(K, H, i, c, start);
+}
+
+template <typename Cur>
+__device__ Child breed_body(const BreedConst& K, const PlanHdr& H, int64_t i, Cur& c, uint64_t start) {
     Child out{0, -1, kUnknown};
     const int64_t base = i % K.np;
     Genome x = genome_unpack(__ldg(K.par + base));
@@ -435,7 +465,71 @@ __global__ void __launch_bounds__(kBreedThreads, 1)
     }
 }
 
+// Counter mode: one thread per offspring (grid-stride), no chain between them.
+__global__ void __launch_bounds__(256) breed_counter_kernel(const uint8_t* __restrict__ gplan, uint32_t plan_bytes,
+                                                           int use_smem, const uint64_t* __restrict__ par,
+                                                           const uint64_t* __restrict__ pid, int64_t np, int64_t n,
+                                                           double mut, double mutcro, double total, uint64_t seed,
+                                                           uint64_t* __restrict__ out, int32_t* __restrict__ partner,
+                                                           unsigned long long* err) {
+    extern __shared__ int4 bsm[];
+    __shared__ int s_other;
+    const uint8_t* P = gplan;
+    if (use_smem) {
+        for (uint32_t i = threadIdx.x; i < (plan_bytes >> 4); i += blockDim.x)
+            bsm[i] = __ldg(reinterpret_cast<const int4*>(gplan) + i);
+        P = reinterpret_cast<const uint8_t*>(bsm);
+    }
+    if (threadIdx.x == 0) s_other = 0;
+    __syncthreads();
+    {  // has_other (genetic.cpp:172-174): every CTA derives it from the parent ids
+        const uint64_t id0 = __ldg(pid);
+        int diff = 0;
+        for (int64_t j = threadIdx.x; j < np; j += blockDim.x) diff |= __ldg(pid + j) != id0;
+        if (__syncthreads_or(diff) && threadIdx.x == 0) s_other = 1;
+    }
+    __syncthreads();
+    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
+    const BreedConst K{P, par, pid, np, mut, mutcro, total, s_other};
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        CounterCursor c{splitmix64(seed ^ splitmix64(uint64_t(i))), 0, true};
+        const Child ch = breed_body(K, H, i, c, 0);
+        if (ch.words == kIllegal) {
+            atomicMin(err, (static_cast<unsigned long long>(i) << 8) | unsigned(ETUNE_ERR_ILLEGAL_SCHEDULE));
+            out[i] = 0;
+            if (partner) partner[i] = -1;
+            continue;
+        }
+        out[i] = ch.g;
+        if (partner) partner[i] = ch.partner;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_breed_counter(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
+                                 const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
+                                 uint64_t seed, uint64_t* d_out, int32_t* d_partner) {
+    if (n <= 0) return cudaSuccess;
+    const double mutcro = mut + cro;
+    const double total = mutcro + cpy;
+    const int use_smem = plan_bytes <= 96 * 1024 ? 1 : 0;
+    const size_t dyn = use_smem ? plan_bytes : 0;
+    if (dyn > 48 * 1024) {
+        const cudaError_t e =
+            cudaFuncSetAttribute(breed_counter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(dyn));
+        if (e != cudaSuccess) return e;
+    }
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, breed_counter_kernel, 256, dyn);
+    if (e != cudaSuccess) return e;
+    const int64_t want = (n + 255) / 256;
+    const int64_t cap = int64_t(c.sm_count) * (per_sm > 0 ? per_sm : 1);
+    breed_counter_kernel<<<int(want < cap ? want : cap), 256, dyn, c.stream>>>(
+        d_plan, plan_bytes, use_smem, d_par, d_pid, np, n, mut, mutcro, total, seed, d_out, d_partner, c.d_err);
+    note_launches(1);
+    return cudaGetLastError();
+}
 
 size_t breed_state_bytes() { return sizeof(BreedState); }
 

@@ -68,6 +68,56 @@ void ctx_release(etune_cu_ctx* c) {
     if (c->refs.fetch_sub(1) == 1 && c->closing.load()) ctx_free_now(c);
 }
 void set_error(const std::string& msg) { g_error = msg; }
+
+// ------------------------------------------------------------ collectives
+// NCCL when a communicator is attached (one rank per GPU over NVLink / NVSwitch), else the
+// caller's transport callbacks (etune_cu_ctx_attach_transport: e.g. a test running two ranks on
+// one GPU over gloo), else a single rank (all-gather = copy, broadcast = no-op).
+int ctx_world(const etune_cu_ctx* c) { return c->comm ? c->nranks : c->has_transport ? c->transport.nranks : 1; }
+int ctx_rank(const etune_cu_ctx* c) { return c->comm ? c->rank : c->has_transport ? c->transport.rank : 0; }
+
+etune_status coll_allgather(etune_cu_ctx* c, const void* d_send, void* d_recv, size_t bytes) {
+    if (c->comm) {
+        const ncclResult_t r = ncclAllGather(d_send, d_recv, bytes, ncclUint8, c->comm, c->stream);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+            return ETUNE_ERR_CUDA;
+        }
+        return ETUNE_OK;
+    }
+    if (c->has_transport) {
+        if (c->transport.allgather(c->transport.user, d_send, d_recv, int64_t(bytes), c->stream) != 0) {
+            set_error("transport all-gather failed");
+            return ETUNE_ERR_BACKEND_UNAVAILABLE;
+        }
+        return ETUNE_OK;
+    }
+    if (d_send != d_recv && bytes) {
+        const cudaError_t e = cudaMemcpyAsync(d_recv, d_send, bytes, cudaMemcpyDeviceToDevice, c->stream);
+        if (e != cudaSuccess) {
+            set_error(std::string("all-gather copy: ") + cudaGetErrorString(e));
+            return ETUNE_ERR_CUDA;
+        }
+    }
+    return ETUNE_OK;
+}
+
+etune_status coll_broadcast(etune_cu_ctx* c, void* d_buf, size_t bytes, int root) {
+    if (ctx_world(c) == 1 || bytes == 0) return ETUNE_OK;
+    if (c->comm) {
+        const ncclResult_t r = ncclBroadcast(d_buf, d_buf, bytes, ncclUint8, root, c->comm, c->stream);
+        if (r != ncclSuccess) {
+            set_error(std::string("ncclBroadcast: ") + ncclGetErrorString(r));
+            return ETUNE_ERR_CUDA;
+        }
+        return ETUNE_OK;
+    }
+    if (c->transport.broadcast(c->transport.user, d_buf, int64_t(bytes), root, c->stream) != 0) {
+        set_error("transport broadcast failed");
+        return ETUNE_ERR_BACKEND_UNAVAILABLE;
+    }
+    return ETUNE_OK;
+}
 }  // namespace etune_b200
 
 namespace {
@@ -144,10 +194,20 @@ bool have_avx512() {
     return ok;
 }
 
+// Host threads for the *_host pipelines: the cores this process may run on, shared with the
+// other ranks of the node when several run on it (LOCAL_WORLD_SIZE, set by torchrun), so that
+// eight ranks do not oversubscribe the host; ETUNE_HOST_THREADS overrides.
 int host_threads() {
+    if (const char* e = std::getenv("ETUNE_HOST_THREADS")) return std::max(1, std::atoi(e));
+    int n = 0;
     cpu_set_t set;
-    if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, CPU_COUNT(&set));
-    return std::max(1u, std::thread::hardware_concurrency());
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) n = CPU_COUNT(&set);
+    if (n < 1) n = int(std::max(1u, std::thread::hardware_concurrency()));
+    if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) {
+        const int w = std::atoi(lw);
+        if (w > 1) n = std::max(1, n / w);
+    }
+    return n;
 }
 
 // Packs m rows into pinned `dst` with the narrowest field width that holds them (2, 4 or
@@ -352,6 +412,7 @@ void free_rowtab(RowTab& rt, cudaStream_t st) {
     cudaFreeAsync(rt.d_rowpred, st);
     cudaFreeAsync(rt.d_srows, st);
     cudaFreeAsync(rt.d_rowgid, st);
+    cudaFreeAsync(rt.d_rowrec, st);
     rt = RowTab{};
 }
 
@@ -396,9 +457,10 @@ etune_status ensure_rows(etune_cu_ctx* c, etune_cu_forest* f, const etune_cu_pla
     void* sscratch = nullptr;
     CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_srows), size_t(p->rows_cap) * 4, st));
     CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_rowgid), size_t(p->rows_cap) * 4, st));
+    CU(cudaMallocAsync(reinterpret_cast<void**>(&rt.d_rowrec), size_t(p->rows_cap) * sizeof(RowRec), st));
     CU(cudaMallocAsync(&sscratch, rowtab_sort_scratch_bytes(p->rows_cap), st));
     const cudaError_t e2 = launch_rowtab_sort(c->lc(), rt.d_meta, rt.d_rowpred, p->rows_cap, rt.d_srows, rt.d_rowgid,
-                                              sscratch);
+                                              rt.d_rowrec, sscratch);
     cudaFreeAsync(sscratch, st);
     if (e2 != cudaSuccess) {
         free_rowtab(rt, st);
@@ -462,7 +524,7 @@ etune_status score_dispatch(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_fo
     } else if (r.kind == 2) {
         // one 8-byte gather per candidate from the row table; ids from the per-key FNV state
         CU(launch_score_rows(c->lc(), p->d_blob, p->build.hdr.ndk, r.rt->d_clskuv, r.rt->d_meta, r.rt->d_rowpred,
-                             p->d_khash, d_genome, n, d_pred, d_ids, sel));
+                             p->d_khk, d_genome, n, d_pred, d_ids, sel));
     } else if (use_keyed(f, r.cs, n)) {
         const CompiledScore* cs = r.cs;
         CU(launch_score_keyed(c->lc(), cs->d_kblob, cs->kbytes, cs->d_ktable, cs->ktable_bytes, cs->d_khash, d_genome,
@@ -519,9 +581,8 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
             CU(cudaEventRecord(ev[1], c->stream));
         }
         const cudaError_t e =
-            launch_score_select_rows(c->lc(), p->d_blob, p->build.hdr.ndk, r.rt->d_clskuv, r.rt->d_meta,
-                                     r.rt->d_rowpred, r.rt->d_rowgid, p->rows_cap, p->d_khash, d_genome, n, k,
-                                     d_pred,
+            launch_score_select_rows(c->lc(), p->d_blob, p->build.hdr.ndk, p->nkeys, r.rt->d_clskuv, r.rt->d_meta,
+                                     r.rt->d_rowrec, p->d_khash, d_genome, n, k, d_pred,
                                      d_ids, d_idx, c->rowsel);
         if (e == cudaSuccess) {
             if (ev) {
@@ -562,15 +623,16 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
     return ETUNE_OK;
 }
 
-// records: [k local scores | k local gidx | W*k gathered scores | W*k gathered gidx | k positions]
+// records: [k local records | W*k gathered records | k local indices | merge scratch]
 struct ShardBufs {
-    double *ls, *gs;
-    int64_t *lg, *gg, *pos, *lidx;
+    ShardRec *lrec, *grec;
+    int64_t* lidx;
+    void* mscratch;
 };
 
 etune_status shard_buffers(etune_cu_ctx* c, int64_t k, ShardBufs* b) {
-    const int W = c->comm ? c->nranks : 1;
-    const size_t need = size_t(k) * 16 * (1 + size_t(W)) + size_t(k) * 8 + 1024;
+    const int W = ctx_world(c);
+    const size_t need = size_t(k) * 16 * (1 + size_t(W)) + size_t(k) * 8 + merge_scratch_bytes(W, k) + 1024;
     if (c->shard_bytes < need) {
         if (c->shard) {
             CU(cudaStreamSynchronize(c->stream));
@@ -581,40 +643,21 @@ etune_status shard_buffers(etune_cu_ctx* c, int64_t k, ShardBufs* b) {
         CU(cudaMalloc(&c->shard, need));
         c->shard_bytes = need;
     }
-    b->ls = static_cast<double*>(c->shard);
-    b->lg = reinterpret_cast<int64_t*>(b->ls + k);
-    b->gs = reinterpret_cast<double*>(b->lg + k);
-    b->gg = reinterpret_cast<int64_t*>(b->gs + size_t(W) * k);
-    b->pos = b->gg + size_t(W) * k;
-    b->lidx = b->pos;  // local selection reuses the position buffer
+    b->lrec = static_cast<ShardRec*>(c->shard);
+    b->grec = b->lrec + k;
+    b->lidx = reinterpret_cast<int64_t*>(b->grec + size_t(W) * k);
+    b->mscratch = b->lidx + k;
     return ETUNE_OK;
 }
 
-// Local top-kl indices in b.lidx -> (score, global index) records -> ncclAllGather ->
-// the identical merged top-k on every rank.
+// Local top-kl indices in b.lidx -> (score, global index) records -> all-gather -> the identical
+// merged top-k on every rank (one-CTA W-way merge of the rank-major sorted lists).
 etune_status shard_merge(etune_cu_ctx* c, const double* d_score, int64_t kl, int64_t k, int64_t goff,
                          const ShardBufs& b, int64_t* d_idx, double* d_sc) {
-    const int W = c->comm ? c->nranks : 1;
-    double* gs = b.gs;
-    int64_t* gg = b.gg;
-    CU(launch_pack_records(c->lc(), d_score, b.lidx, kl, k, goff, b.ls, b.lg));
-    if (c->comm) {  // any attached communicator, a single rank included (same code path as W > 1)
-        ncclResult_t r = ncclGroupStart();
-        if (r == ncclSuccess) r = ncclAllGather(b.ls, gs, size_t(k), ncclFloat64, c->comm, c->stream);
-        if (r == ncclSuccess) r = ncclAllGather(b.lg, gg, size_t(k), ncclInt64, c->comm, c->stream);
-        const ncclResult_t r2 = ncclGroupEnd();
-        if (r != ncclSuccess || r2 != ncclSuccess)
-            return fail(ETUNE_ERR_CUDA, std::string("ncclAllGather: ") + ncclGetErrorString(r != ncclSuccess ? r : r2));
-    } else {
-        gs = b.ls;
-        gg = b.lg;
-    }
-    // shards are contiguous and ascending by rank, each list sorted by (score, gidx):
-    // (score, position) order over the rank-major concatenation == (score, gidx) order
-    const int64_t tot = int64_t(W) * k;
-    if (etune_status st = ensure_scratch(c, topk_scratch_bytes(tot))) return st;
-    CU(launch_topk(c->lc(), gs, tot, k, b.pos, c->scratch));
-    CU(launch_gather_records(c->lc(), gs, gg, b.pos, k, d_idx, d_sc));
+    const int W = ctx_world(c);
+    CU(launch_pack_records(c->lc(), d_score, b.lidx, kl, k, goff, b.lrec));
+    if (etune_status st = coll_allgather(c, b.lrec, b.grec, size_t(k) * sizeof(ShardRec))) return st;
+    CU(launch_merge_records(c->lc(), b.grec, W, k, d_idx, d_sc, b.mscratch));
     return ETUNE_OK;
 }
 
@@ -736,6 +779,33 @@ etune_status etune_cu_synchronize(etune_cu_ctx* c, int64_t* first_bad) {
     return fail(st, what);
 }
 
+etune_status etune_cu_device_alloc(etune_cu_ctx* c, void** out, int64_t bytes) {
+    if (!c || !out || bytes < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    CU(cudaSetDevice(c->device));
+    CU(cudaMalloc(out, size_t(bytes > 0 ? bytes : 1)));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_device_free(etune_cu_ctx* c, void* p) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    if (!p) return ETUNE_OK;
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaFree(p));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_memcpy_h2d(etune_cu_ctx* c, void* d_dst, const void* h_src, int64_t bytes) {
+    if (!c || bytes < 0 || (bytes > 0 && (!d_dst || !h_src))) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (bytes) CU(cudaMemcpyAsync(d_dst, h_src, size_t(bytes), cudaMemcpyHostToDevice, c->stream));
+    return ETUNE_OK;
+}
+
+etune_status etune_cu_memcpy_d2h(etune_cu_ctx* c, void* h_dst, const void* d_src, int64_t bytes) {
+    if (!c || bytes < 0 || (bytes > 0 && (!h_dst || !d_src))) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
+    if (bytes) CU(cudaMemcpyAsync(h_dst, d_src, size_t(bytes), cudaMemcpyDeviceToHost, c->stream));
+    return ETUNE_OK;
+}
+
 etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, const etune_device_config* dev,
                                   const etune_space_limits* limits, etune_cu_plan** out) {
     if (!c || !op || !out) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null argument");
@@ -761,8 +831,9 @@ etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, cons
         p->kuv_domain = dom;
         if (H.ndk <= 1024 && nkeys > 0 && nkeys <= (int64_t(1) << 24) && nkeys * dom <= (int64_t(1) << 25)) {
             p->rows_cap = nkeys * dom;
+            CU(cudaMalloc(&p->d_khk, size_t(nkeys) * size_t(H.ndk) * 8));
             CU(cudaMalloc(&p->d_khash, size_t(nkeys) * 8));
-            CU(launch_key_hash(c->lc(), p->d_blob, nkeys, p->d_khash));
+            CU(launch_key_hash(c->lc(), p->d_blob, nkeys, p->d_khk, p->d_khash));
         }
     }
     CU(cudaStreamSynchronize(c->stream));
@@ -798,6 +869,7 @@ etune_status etune_cu_plan_destroy(etune_cu_plan* p) {
     }
     cudaStreamSynchronize(c->stream);  // kernels still reading the plan's tables
     cudaFree(p->d_khash);
+    cudaFree(p->d_khk);
     cudaFree(p->d_blob);
     delete p;
     ctx_release(c);
@@ -1599,9 +1671,10 @@ etune_status etune_cu_forest_from_device(etune_cu_ctx* c, const int32_t* d_featu
                                   sc[0], learning_rate, out);
 }
 
-etune_status etune_cu_reproduce(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np,
-                                int64_t n, const etune_genetic_rates* rates, uint64_t seed, uint64_t* d_out,
-                                int32_t* d_partner, uint64_t* d_ids) {
+namespace {
+etune_status reproduce_impl(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np, int64_t n,
+                            const etune_genetic_rates* rates, uint64_t seed, uint64_t* d_out, int32_t* d_partner,
+                            uint64_t* d_ids, bool counter) {
     if (!c || !p) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx/plan");
     if (n < 0) return fail(ETUNE_ERR_INVALID_ARGUMENT, "negative n");
     if (np < 1 || !d_par) return fail(ETUNE_ERR_VALIDATION, "reproduce requires at least one parent");
@@ -1626,10 +1699,28 @@ etune_status etune_cu_reproduce(etune_cu_ctx* c, const etune_cu_plan* p, const u
     }
     uint64_t* d_pid = reinterpret_cast<uint64_t*>(static_cast<char*>(c->breed) + 256);
     CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_par, np, d_pid));
-    CU(launch_breed(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover, r.copy,
-                    seed, d_out, d_partner, c->breed));
+    if (counter)
+        CU(launch_breed_counter(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover,
+                                r.copy, seed, d_out, d_partner));
+    else
+        CU(launch_breed(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover, r.copy,
+                        seed, d_out, d_partner, c->breed));
     if (d_ids) CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_out, n, d_ids));
     return ETUNE_OK;
+}
+
+}  // namespace
+
+etune_status etune_cu_reproduce(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np,
+                                int64_t n, const etune_genetic_rates* rates, uint64_t seed, uint64_t* d_out,
+                                int32_t* d_partner, uint64_t* d_ids) {
+    return reproduce_impl(c, p, d_par, np, n, rates, seed, d_out, d_partner, d_ids, false);
+}
+
+etune_status etune_cu_reproduce_counter(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np,
+                                        int64_t n, const etune_genetic_rates* rates, uint64_t seed, uint64_t* d_out,
+                                        int32_t* d_partner, uint64_t* d_ids) {
+    return reproduce_impl(c, p, d_par, np, n, rates, seed, d_out, d_partner, d_ids, true);
 }
 
 etune_status etune_cu_topk(etune_cu_ctx* c, const double* d_score, int64_t n, int64_t k, int64_t* d_idx) {
@@ -1692,10 +1783,21 @@ etune_status etune_cu_topk_sharded(etune_cu_ctx* c, const double* d_score, int64
 
 etune_status etune_cu_broadcast(etune_cu_ctx* c, void* d_buf, int64_t bytes, int root) {
     if (!c || bytes < 0 || (bytes > 0 && !d_buf)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad arguments");
-    if (!c->comm || c->nranks == 1 || bytes == 0) return ETUNE_OK;
-    if (root < 0 || root >= c->nranks) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad root");
-    const ncclResult_t r = ncclBroadcast(d_buf, d_buf, size_t(bytes), ncclUint8, root, c->comm, c->stream);
-    if (r != ncclSuccess) return fail(ETUNE_ERR_CUDA, std::string("ncclBroadcast: ") + ncclGetErrorString(r));
+    if (root < 0 || root >= ctx_world(c)) return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad root");
+    return coll_broadcast(c, d_buf, size_t(bytes), root);
+}
+
+etune_status etune_cu_ctx_attach_transport(etune_cu_ctx* c, const etune_transport* t) {
+    if (!c) return fail(ETUNE_ERR_INVALID_ARGUMENT, "null ctx");
+    if (!t) {
+        c->has_transport = false;
+        return ETUNE_OK;
+    }
+    if (t->nranks < 1 || t->rank < 0 || t->rank >= t->nranks || !t->allgather || !t->broadcast)
+        return fail(ETUNE_ERR_INVALID_ARGUMENT, "bad transport");
+    if (c->comm) return fail(ETUNE_ERR_INVALID_ARGUMENT, "an NCCL communicator is already attached");
+    c->transport = *t;
+    c->has_transport = true;
     return ETUNE_OK;
 }
 

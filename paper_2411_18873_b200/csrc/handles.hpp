@@ -36,6 +36,8 @@ struct etune_cu_ctx {
     size_t breed_bytes = 0;
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
+    etune_transport transport{};  // caller's collectives when no NCCL communicator is attached
+    bool has_transport = false;
     void* shard = nullptr;  // sharded-selection records
     size_t shard_bytes = 0;
     void* e2e = nullptr;    // score_select_host: the population's predictions + the k indices on the device
@@ -64,6 +66,11 @@ struct etune_cu_ctx {
 namespace etune_b200 {
 void ctx_retain(etune_cu_ctx* c);
 void ctx_release(etune_cu_ctx* c);
+// collectives over the ctx's ranks (capi.cpp): NCCL, else the attached transport, else one rank
+int ctx_world(const etune_cu_ctx* c);
+int ctx_rank(const etune_cu_ctx* c);
+etune_status coll_allgather(etune_cu_ctx* c, const void* d_send, void* d_recv, size_t bytes);
+etune_status coll_broadcast(etune_cu_ctx* c, void* d_buf, size_t bytes, int root);
 }  // namespace etune_b200
 
 struct etune_cu_plan {
@@ -74,7 +81,8 @@ struct etune_cu_plan {
     // row-table form (rowtab.cu): per tiling-triple key the FNV-1a state of candidate_id after
     // the operator and the three tilings; rows_cap = keys x legal (k_tile, unroll, vec) triples
     // (0: the operator's row table would be too large, the form is not offered)
-    uint64_t* d_khash = nullptr;
+    uint64_t* d_khash = nullptr;  // per key: after the three tilings
+    uint64_t* d_khk = nullptr;    // per (key, k_tile index): after k_tile as well
     int64_t nkeys = 0, kuv_domain = 0, rows_cap = 0;
 };
 
@@ -87,6 +95,7 @@ struct RowTab {
     double* d_rowpred = nullptr;
     uint32_t* d_srows = nullptr;   // rows in prediction order (ties by row)
     uint32_t* d_rowgid = nullptr;  // a row's group: the dense rank of its prediction
+    etune_b200::RowRec* d_rowrec = nullptr;  // {prediction, group} per row: the fused selection's gather
 };
 
 struct CompiledScore {

@@ -89,10 +89,19 @@ struct RowTabMeta {
     int64_t rows;        // keys x nkc
     int64_t groups;      // distinct row predictions (dense ranks 0 .. groups-1)
 };
+// the fused selection's per-row record: prediction and group (dense rank of the prediction)
+struct RowRec {
+    double pred;
+    uint32_t gid, pad;
+};
+static_assert(sizeof(RowRec) == 16, "one 16-byte gather per candidate");
 // rows per key before class compression: the legal (k_tile, unroll, vectorize) triples
 int64_t rowtab_kuv_domain(const int64_t* divk, int ndk);
 size_t rowtab_scratch_bytes(int nnodes);
-cudaError_t launch_key_hash(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, uint64_t* d_khash);
+// candidate_id's FNV state per (tiling-triple key, k_tile index) after k_tile (d_khk, nkeys * ndk)
+// and per key after the three tilings (d_khash, nkeys)
+cudaError_t launch_key_hash(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, uint64_t* d_khk,
+                            uint64_t* d_khash);
 // d_clskuv: ndk * 64 u16; d_crep: one u32 per class (<= rowtab_kuv_domain); d_rowpred: rows_cap doubles
 cudaError_t launch_rowtab_compile(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes,
                                   const uint8_t* d_pred, uint32_t pred_bytes, int nnodes, int ndk, int64_t rows_cap,
@@ -103,16 +112,16 @@ cudaError_t launch_rowtab_compile(const LaunchCtx& c, const uint8_t* d_plan, uin
 // scratch rowtab_sort_scratch_bytes(rows_cap).
 size_t rowtab_sort_scratch_bytes(int64_t rows_cap);
 cudaError_t launch_rowtab_sort(const LaunchCtx& c, RowTabMeta* d_meta, const double* d_rowpred, int64_t rows_cap,
-                               uint32_t* d_srows, uint32_t* d_rowgid, void* d_scratch);
+                               uint32_t* d_srows, uint32_t* d_rowgid, RowRec* d_rowrec, void* d_scratch);
 // Fused score + keep-the-best on the row table in ONE cooperative kernel (rowtab.cu): every
 // candidate's prediction and id, group counts, the k-th group, ties by index, the k sorted by
 // (prediction, index).  0 < k <= kSelMaxK; returns cudaErrorNotSupported when n exceeds what the
 // grid holds in registers (the caller falls back to the bucketed selection).
 size_t rowsel_work_bytes();
-cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,
-                                     const RowTabMeta* d_meta, const double* d_rowpred, const uint32_t* d_rowgid,
-                                     int64_t rows_cap, const uint64_t* d_khash, const uint64_t* d_genome, int64_t n,
-                                     int64_t k, double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work);
+cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, int64_t nkeys,
+                                     const uint16_t* d_clskuv, const RowTabMeta* d_meta, const RowRec* d_rowrec,
+                                     const uint64_t* d_khash, const uint64_t* d_genome, int64_t n, int64_t k,
+                                     double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work);
 cudaError_t launch_score_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,
                               const RowTabMeta* d_meta, const double* d_rowpred, const uint64_t* d_khash,
                               const uint64_t* d_genome, int64_t n, double* d_pred, uint64_t* d_ids,
@@ -136,6 +145,12 @@ cudaError_t launch_breed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t pla
                          const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
                          uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_state);
 
+// reproduce in the opt-in counter mode: offspring i draws from its own counter-based stream
+// (breed.cu CounterCursor), one thread per offspring; same decision logic as the exact mode.
+cudaError_t launch_breed_counter(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
+                                 const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
+                                 uint64_t seed, uint64_t* d_out, int32_t* d_partner);
+
 // EnergyModel::train (energy_model.cpp:173-243), bit-exact; scratch from train_scratch_bytes(n).
 size_t train_scratch_bytes(int64_t n);
 int train_max_depth();
@@ -151,12 +166,19 @@ cudaError_t launch_energy_loss(const LaunchCtx& c, const double* d_pred, const d
 cudaError_t launch_snr_sums(const LaunchCtx& c, const double* d_pred, const double* d_meas, int64_t n,
                             double* d_out2);
 
-// sharded selection helpers (model.cu): records of the local top-k (padded to k with
-// +inf / INT64_MAX), and the final gather of (gidx, score) by merged positions
+// sharded selection (model.cu): a rank's local top-k as (score, global index) records, padded to
+// k with (+inf, INT64_MAX); the merge of W such sorted lists (rank-major) into the global top-k:
+// one CTA merging in shared memory when W * k * 24 bytes fit, else round by round in global
+// memory (scratch merge_scratch_bytes(W, k))
+struct ShardRec {
+    double s;
+    int64_t g;
+};
 cudaError_t launch_pack_records(const LaunchCtx& c, const double* d_score, const int64_t* d_lidx, int64_t kl,
-                                int64_t k, int64_t goff, double* d_rs, int64_t* d_rg);
-cudaError_t launch_gather_records(const LaunchCtx& c, const double* d_gs, const int64_t* d_gg, const int64_t* d_pos,
-                                  int64_t k, int64_t* d_idx, double* d_sc);
+                                int64_t k, int64_t goff, ShardRec* d_rec);
+size_t merge_scratch_bytes(int W, int64_t k);
+cudaError_t launch_merge_records(const LaunchCtx& c, const ShardRec* d_rec, int W, int64_t k, int64_t* d_idx,
+                                 double* d_sc, void* d_scratch);
 
 // stable LSD radix sort of (u64 key, u32 value) pairs by the low `bits` bits, in place
 size_t sort_pairs_scratch_bytes(int64_t n);

@@ -55,6 +55,18 @@ void append_exponent(std::string& s, int e) {
 }
 
 // ------------------------------------------------------------------ Grisu2
+// Third-party notice: the double-to-text routine below restates the algorithm (and, where the
+// output must match byte for byte, the cached-power table and rounding conditions) of
+// nlohmann::json 3.11.3's dtoa_impl, which is distributed under the MIT License:
+//   Copyright (c) 2013-2022 Niels Lohmann <https://nlohmann.me>; the Grisu2 implementation in
+//   dtoa_impl is based on Florian Loitsch's reference code.  Permission is hereby granted, free
+//   of charge, to any person obtaining a copy of this software and associated documentation files
+//   (the "Software"), to deal in the Software without restriction, including without limitation
+//   the rights to use, copy, modify, merge, publish, distribute, sublicense, and/or sell copies of
+//   the Software, and to permit persons to whom the Software is furnished to do so, subject to
+//   the following conditions: The above copyright notice and this permission notice shall be
+//   included in all copies or substantial portions of the Software.  THE SOFTWARE IS PROVIDED
+//   "AS IS", WITHOUT WARRANTY OF ANY KIND, EXPRESS OR IMPLIED.
 // nlohmann::json 3.11.3 (the reference's pinned JSON library, nlohmann/json.hpp
 // dtoa_impl) prints doubles with Grisu2 (Loitsch, "Printing Floating-Point Numbers
 // Quickly and Accurately with Integers", PLDI 2010): digits of a value inside the

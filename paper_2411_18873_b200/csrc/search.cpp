@@ -40,7 +40,7 @@ struct etune_cu_search {
     // device buffers
     uint64_t *pop = nullptr, *mgen = nullptr, *selgen = nullptr, *par = nullptr, *ids = nullptr;
     double *lat = nullptr, *mpred = nullptr, *psel = nullptr, *mlat = nullptr, *mpow = nullptr, *men = nullptr,
-           *mnorm = nullptr;
+           *mnorm = nullptr, *psel_scratch = nullptr;
     int64_t *idx = nullptr, *sel = nullptr;
     int64_t np = 0;
     // training samples (grow by doubling)
@@ -105,8 +105,10 @@ etune_status prelaunch_reproduce(etune_cu_search* s, int64_t r) {
     SCU(cudaStreamWaitEvent(s->side, s->ev_par, 0));
     const cudaStream_t main_stream = c->stream;
     c->stream = s->side;  // the ctx's launches go to the side stream for this call only
-    const etune_status st = etune_cu_reproduce(c, s->plan, s->par, s->np, s->cfg.generation_size, &s->cfg.rates,
-                                               s->cfg.rng_seed + uint64_t(r), s->pop, nullptr, nullptr);
+    const etune_status st =
+        (s->cfg.counter_rng ? etune_cu_reproduce_counter : etune_cu_reproduce)(
+            c, s->plan, s->par, s->np, s->cfg.generation_size, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
+            nullptr, nullptr);
     c->stream = main_stream;
     SOK(st);
     SCU(cudaEventRecord(s->ev_pop, s->side));
@@ -153,8 +155,22 @@ etune_status retrain(etune_cu_search* s) {
     etune_cu_ctx* c = s->ctx;
     static const bool trace = std::getenv("ETUNE_SEARCH_TRACE") != nullptr;
     const double t0 = trace ? now_ms() : 0.0;
-    SOK(etune_cu_train(c, s->feat, s->energy, s->nsamples, &s->cfg.boost, s->m_feature, s->m_thr, s->m_left,
-                       s->m_right, s->m_value, s->m_off, s->m_sc, nullptr));
+    // population-sharded search: rank 0 trains, the model arrays are broadcast (north_star: NCCL
+    // carries only the per-shard top-k records and the model); a single rank just trains
+    const int W = ctx_world(c);
+    if (W == 1 || ctx_rank(c) == 0)
+        SOK(etune_cu_train(c, s->feat, s->energy, s->nsamples, &s->cfg.boost, s->m_feature, s->m_thr, s->m_left,
+                           s->m_right, s->m_value, s->m_off, s->m_sc, nullptr));
+    if (W > 1) {
+        const size_t nodes = size_t(s->cfg.boost.num_trees) * ((size_t(1) << (s->cfg.boost.max_depth + 1)) - 1);
+        SOK(coll_broadcast(c, s->m_feature, nodes * 4, 0));
+        SOK(coll_broadcast(c, s->m_left, nodes * 4, 0));
+        SOK(coll_broadcast(c, s->m_right, nodes * 4, 0));
+        SOK(coll_broadcast(c, s->m_thr, nodes * 8, 0));
+        SOK(coll_broadcast(c, s->m_value, nodes * 8, 0));
+        SOK(coll_broadcast(c, s->m_off, size_t(s->cfg.boost.num_trees + 1) * 8, 0));
+        SOK(coll_broadcast(c, s->m_sc, 16, 0));
+    }
     if (trace) {
         const double t1 = now_ms();
         cudaStreamSynchronize(c->stream);
@@ -284,6 +300,24 @@ etune_status replay_lookup(etune_cu_search* s, const uint64_t* gen, int64_t n, s
     return ETUNE_OK;
 }
 
+etune_status measure_latency(etune_cu_search* s, const uint64_t* gen, int64_t n, double* d_lat);
+
+// LatencyEvaAndPick(gen, M) -> the M fastest by (latency, index) into s->idx.  Sharded: every rank
+// holds the whole generation (reproduce is replicated: one RNG stream), measures the latencies of
+// its contiguous slice only, keeps its slice's M fastest and the all-gathered per-rank lists are
+// merged into the identical global M on every rank (etune_cu_topk_sharded).
+etune_status latency_pick(etune_cu_search* s, const uint64_t* gen, int64_t n, int64_t M) {
+    etune_cu_ctx* c = s->ctx;
+    const int W = ctx_world(c), R = ctx_rank(c);
+    if (W == 1) {
+        SOK(measure_latency(s, gen, n, s->lat));
+        return etune_cu_topk(c, s->lat, n, M, s->idx);
+    }
+    const int64_t lo = n * R / W, hi = n * (R + 1) / W;
+    SOK(measure_latency(s, gen + lo, hi - lo, s->lat + lo));
+    return etune_cu_topk_sharded(c, s->lat + lo, hi - lo, lo, M, s->idx, s->psel_scratch);
+}
+
 etune_status measure_latency(etune_cu_search* s, const uint64_t* gen, int64_t n, double* d_lat) {
     if (s->cfg.backend == 0) return etune_cu_sim_measure(s->ctx, s->plan, gen, n, d_lat, nullptr, nullptr, nullptr);
     if (s->cfg.backend == 2) {
@@ -305,9 +339,40 @@ etune_status measure_latency(etune_cu_search* s, const uint64_t* gen, int64_t n,
 // NVMLMeasurement: latency, power and energy of n device genomes into mlat/mpow/men.
 // A selected schedule the candidate kernel cannot run gets a finite penalty energy
 // (1e30 mJ) so that training stays finite; it is never the best.
+etune_status measure_energy_local(etune_cu_search* s, const uint64_t* gen, int64_t n, double* lat, double* pw,
+                                  double* en);
+
+// Sharded: rank r measures the slice [n r / W, n (r+1) / W) (on the GPU backend, every GPU runs
+// its own candidates at once), the three arrays are all-gathered in slices padded to ceil(n / W).
 etune_status measure_energy(etune_cu_search* s, const uint64_t* gen, int64_t n) {
+    etune_cu_ctx* c = s->ctx;
+    const int W = ctx_world(c), R = ctx_rank(c);
+    if (W == 1) return measure_energy_local(s, gen, n, s->mlat, s->mpow, s->men);
+    const int64_t per = (n + W - 1) / W;
+    const int64_t lo = n * R / W, hi = n * (R + 1) / W;
+    double* st = nullptr;  // [3][per] local, then [W][3][per] gathered
+    SCU(cudaMallocAsync(reinterpret_cast<void**>(&st), size_t(per) * 3 * 8 * size_t(1 + W), c->stream));
+    double* g = st + 3 * per;
+    etune_status rs = measure_energy_local(s, gen + lo, hi - lo, st, st + per, st + 2 * per);
+    if (rs == ETUNE_OK) rs = coll_allgather(c, st, g, size_t(per) * 3 * 8);
+    for (int w = 0; w < W && rs == ETUNE_OK; ++w) {
+        const int64_t a = n * w / W, m = n * (w + 1) / W - a;
+        double* dst[3] = {s->mlat, s->mpow, s->men};
+        for (int q = 0; q < 3 && m > 0; ++q) {
+            const cudaError_t e = cudaMemcpyAsync(dst[q] + a, g + (int64_t(w) * 3 + q) * per, size_t(m) * 8,
+                                                  cudaMemcpyDeviceToDevice, c->stream);
+            if (e != cudaSuccess) rs = sfail(ETUNE_ERR_CUDA, cudaGetErrorString(e));
+        }
+    }
+    cudaFreeAsync(st, c->stream);
+    return rs;
+}
+
+etune_status measure_energy_local(etune_cu_search* s, const uint64_t* gen, int64_t n, double* mlat, double* mpow,
+                                  double* men) {
+    if (n <= 0) return ETUNE_OK;
     if (s->cfg.backend == 0)
-        return etune_cu_sim_measure(s->ctx, s->plan, gen, n, s->mlat, s->mpow, s->men, nullptr);
+        return etune_cu_sim_measure(s->ctx, s->plan, gen, n, mlat, mpow, men, nullptr);
     std::vector<etune_measurement> rec(static_cast<size_t>(n));
     if (s->cfg.backend == 2) {
         SOK(replay_lookup(s, gen, n, &rec));
@@ -324,9 +389,9 @@ etune_status measure_energy(etune_cu_search* s, const uint64_t* gen, int64_t n) 
         en[size_t(i)] = r.feasible ? r.energy_mj : 1e30;
     }
     cudaStream_t st = s->ctx->stream;
-    SCU(cudaMemcpyAsync(s->mlat, lat.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
-    SCU(cudaMemcpyAsync(s->mpow, pw.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
-    SCU(cudaMemcpyAsync(s->men, en.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    SCU(cudaMemcpyAsync(mlat, lat.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    SCU(cudaMemcpyAsync(mpow, pw.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
+    SCU(cudaMemcpyAsync(men, en.data(), size_t(n) * 8, cudaMemcpyHostToDevice, st));
     return etune_cu_synchronize(s->ctx, nullptr);
 }
 
@@ -386,6 +451,7 @@ etune_status etune_cu_search_create(etune_cu_ctx* c, const etune_cu_plan* p, con
     SOK(dalloc(s.get(), &s->sel, M));
     SOK(dalloc(s.get(), &s->selgen, M));
     SOK(dalloc(s.get(), &s->psel, M));
+    SOK(dalloc(s.get(), &s->psel_scratch, M));  // scores of the merged sharded latency pick
     SOK(dalloc(s.get(), &s->mlat, M));
     SOK(dalloc(s.get(), &s->mpow, M));
     SOK(dalloc(s.get(), &s->men, M));
@@ -442,8 +508,7 @@ etune_status etune_cu_search_initial(etune_cu_search* s, etune_round_report* rep
     const double t0 = now_ms();
     const int64_t G = s->cfg.generation_size, M = s->cfg.M;
     SOK(etune_cu_sample_random(c, s->plan, G, s->cfg.rng_seed, s->pop, nullptr));
-    SOK(measure_latency(s, s->pop, G, s->lat));
-    SOK(etune_cu_topk(c, s->lat, G, M, s->idx));  // LatencyEvaAndPick(Kernel_generation, M)
+    SOK(latency_pick(s, s->pop, G, M));  // LatencyEvaAndPick(Kernel_generation, M)
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
     if (s->cfg.latency_only) {  // run_latency_only: no energy model at all
         SCU(cudaMemcpyAsync(s->par, s->mgen, size_t(M) * 8, cudaMemcpyDeviceToDevice, c->stream));
@@ -493,13 +558,12 @@ etune_status etune_cu_search_round(etune_cu_search* s, etune_round_report* rep) 
     if (s->pop_round == r) {
         SCU(cudaStreamWaitEvent(c->stream, s->ev_pop, 0));
     } else {
-        SOK(etune_cu_reproduce(c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop,
-                               nullptr, nullptr));
+        SOK((s->cfg.counter_rng ? etune_cu_reproduce_counter : etune_cu_reproduce)(
+            c, s->plan, s->par, s->np, G, &s->cfg.rates, s->cfg.rng_seed + uint64_t(r), s->pop, nullptr, nullptr));
     }
     stage("reproduce");
     // 2. LatencyEvaAndPick(Kernel_generation, M)
-    SOK(measure_latency(s, s->pop, G, s->lat));
-    SOK(etune_cu_topk(c, s->lat, G, M, s->idx));
+    SOK(latency_pick(s, s->pop, G, M));
     SCU(launch_gather_u64(c->lc(), s->pop, s->idx, M, s->mgen));
     stage("latency");
     if (s->cfg.latency_only) {  // steps 3-8 replaced by parent selection on latency

@@ -131,6 +131,7 @@ class Oracle(_Lib):
         L.orc_sample_random.argtypes = [I64P, C.c_int64, C.c_uint64, I64P, I64P, U64P]
         L.orc_reproduce.argtypes = [I64P, I64P, C.c_int64, C.c_int64, F64P, C.c_uint64, I64P,
                                     I64P, U64P, U64P, I8P]
+        L.orc_reproduce_counter.argtypes = L.orc_reproduce.argtypes
         L.orc_predict.argtypes = [I32P, F64P, I32P, I32P, F64P, I64P, C.c_int64, C.c_double,
                                   C.c_double, F64P, C.c_int64, F64P]
         L.orc_train.argtypes = [F64P, F64P, C.c_int64, C.c_int, C.c_int, C.c_double, C.c_double,
@@ -232,6 +233,17 @@ class Oracle(_Lib):
         ll = np.zeros(n, np.int8)
         self._check(self.L.orc_reproduce(op, parents, len(parents), n, np.array(rates, np.float64), seed,
                                          default_limits() if limits is None else limits, s, ids, lin, ll))
+        return s, ids, lin, ll
+
+    def reproduce_counter(self, op, parents, n, seed, rates=(0.85, 0.10, 0.05), limits=None):
+        """The opt-in counter-based reproduce mode (per-offspring splitmix64 streams)."""
+        parents = np.ascontiguousarray(parents, np.int64).reshape(-1, 12)
+        s = np.zeros((n, 12), np.int64)
+        ids = np.zeros(n, np.uint64)
+        lin = np.zeros((n, 2), np.uint64)
+        ll = np.zeros(n, np.int8)
+        self._check(self.L.orc_reproduce_counter(op, parents, len(parents), n, np.array(rates, np.float64), seed,
+                                                 default_limits() if limits is None else limits, s, ids, lin, ll))
         return s, ids, lin, ll
 
     # --- cost model

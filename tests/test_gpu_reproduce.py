@@ -122,3 +122,46 @@ def test_reproduce_errors(ctx, capi):
     with pytest.raises(capi.EtuneError) as e:
         capi.reproduce(plan, g, 10, 1, (0.0, 0.0, 0.0))
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("text,np_,n,seed,rates", [
+    ("conv:1,56,56,64,64,3,1,1", 1024, 1 << 20, 7, (0.85, 0.10, 0.05)),
+    ("mm:1,512,3072,768", 512, 200003, 9, (0.85, 0.10, 0.05)),
+    ("mm:1,1024,1024,1024", 64, 100000, 3, (0.2, 0.7, 0.1)),
+    ("mv:1,1,1000,2048", 3, 50000, 11, (0.0, 1.0, 0.0)),
+])
+def test_reproduce_counter_mode_vs_oracle(oracle, ctx, capi, text, np_, n, seed, rates):
+    """The opt-in counter-based mode (etune_cu_reproduce_counter): schedules, ids and lineage
+    identical to its oracle restatement (orc_reproduce_counter), including 2^20 offspring."""
+    op = parse_op(text)
+    parents, _ = oracle.sample_random(op, np_, 42)
+    plan = capi.Plan(ctx, op)
+    g = plan.encode(dev(parents))
+    out, partner, ids = capi.reproduce(plan, g, n, seed, rates, counter=True)
+    sched = plan.decode(out)
+    ctx.synchronize()
+    s, oid, lin, ll = oracle.reproduce_counter(op, parents, n, seed, rates)
+    assert (sched.cpu().numpy() == s).all()
+    assert (capi.as_u64(ids) == oid).all()
+    gp = partner.cpu().numpy()
+    assert (ll == np.where(gp >= 0, 2, 1)).all()
+    pid = oracle.ids(op, parents)
+    assert (lin[gp >= 0, 1] == pid[gp[gp >= 0]]).all()
+
+
+def test_reproduce_counter_mode_speed(oracle, ctx, capi):
+    """2^20 offspring in the counter mode well under the exact mode's single-CTA chain."""
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    plan = capi.Plan(ctx, op)
+    g = plan.sample_random(1024, 42)
+    capi.reproduce(plan, g, 1 << 20, 7, counter=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for r in range(5):
+        capi.reproduce(plan, g, 1 << 20, 7 + r, counter=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    print(f"counter-mode reproduce 2^20: {ms:.3f} ms")
+    assert ms < 10.0

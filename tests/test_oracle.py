@@ -169,3 +169,24 @@ def test_sim_measure_spec_examples(oracle):
     r0 = oracle.sim_measure(op, full[:200], {"noise_sigma_rel": 0.0})
     assert (r1 == r2).all()
     assert np.abs(r1[:, 1] / r0[:, 1] - 1).max() < 0.02
+
+
+def test_reproduce_counter_restatement(oracle):
+    """The counter-mode restatement: deterministic, prefix-stable (offspring i depends only on
+    (seed, i, parents)), every child legal with a correct id and lineage, and the move mix of
+    GeneticRates (mutation / crossover / copy) like the exact mode's."""
+    from etune_testlib import parse_op
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    par, pid = oracle.sample_random(op, 256, 42)
+    s, ids, lin, ll = oracle.reproduce_counter(op, par, 30000, 7)
+    s2, _, _, _ = oracle.reproduce_counter(op, par, 30000, 7)
+    assert (s == s2).all()
+    s3, _, _, _ = oracle.reproduce_counter(op, par, 1000, 7)
+    assert (s3 == s[:1000]).all()
+    assert (oracle.ids(op, s) == ids).all()
+    assert (lin[:, 0] == pid[np.arange(30000) % 256]).all()
+    frac_cro = (ll == 2).mean()
+    _, _, _, lle = oracle.reproduce(op, par, 30000, 7)
+    assert abs(frac_cro - 0.10) < 0.01 and abs((lle == 2).mean() - 0.10) < 0.01
+    s4, _, _, _ = oracle.reproduce_counter(op, par, 30000, 8)
+    assert (s4 != s).any(axis=1).mean() > 0.5  # a different seed, a different generation
