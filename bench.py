@@ -147,7 +147,7 @@ def time_cpu(op, sched, target_s: float, k: int):
     rate = m / max(time.perf_counter() - t0, 1e-9)
     per = int(min(len(sched), max(m, rate * target_s / 4)))
     done, dt = 0, 0.0
-    while dt < target_s * 0.75 and done < 4 * per:
+    while dt < target_s:
         t0 = time.perf_counter()
         fn(op, sched[:per])
         dt += time.perf_counter() - t0

@@ -42,6 +42,7 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->rowsel);
     cudaFree(c->e2e);
     if (c->hpin) cudaFreeHost(c->hpin);
+    if (c->hout) cudaFreeHost(c->hout);
     c->pool.reset();
     for (auto& e : c->prof_ev)
         for (cudaEvent_t x : e) cudaEventDestroy(x);
@@ -832,7 +833,7 @@ etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, cons
         if (H.ndk <= 1024 && nkeys > 0 && nkeys <= (int64_t(1) << 24) && nkeys * dom <= (int64_t(1) << 25)) {
             p->rows_cap = nkeys * dom;
             CU(cudaMalloc(&p->d_khk, size_t(nkeys) * size_t(H.ndk) * 8));
-            CU(cudaMalloc(&p->d_khash, size_t(nkeys) * 8));
+            CU(cudaMalloc(&p->d_khash, size_t(nkeys + 2) * 8));  // + padding: whole 16-byte bulk copies
             CU(launch_key_hash(c->lc(), p->d_blob, nkeys, p->d_khk, p->d_khash));
         }
     }
@@ -1518,12 +1519,43 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         const char* ev = std::getenv("ETUNE_E2E_RAW_EVERY");
         return ev ? std::atoi(ev) : 4;
     }();
-    bool pinned = false;
-    {
+    auto is_pinned = [](const void* ptr) {
         cudaPointerAttributes pa{};
-        pinned = cudaPointerGetAttributes(&pa, h_sched) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        const bool r = ptr && cudaPointerGetAttributes(&pa, ptr) == cudaSuccess && pa.type == cudaMemoryTypeHost;
         cudaGetLastError();
+        return r;
+    };
+    const bool pinned = is_pinned(h_sched);
+    // Outputs into pageable memory (a std::vector<double>, a numpy array) would make every D2H
+    // synchronous: they land in pinned staging instead and the host pool copies them out while the
+    // next chunks run.
+    const bool stage_out = (h_pred && !is_pinned(h_pred)) || (h_ids && !is_pinned(h_ids));
+    if (stage_out && c->hout_bytes < 2 * size_t(cap) * 16) {
+        if (c->hout) {
+            CU(cudaStreamSynchronize(c->d2h));
+            CU(cudaFreeHost(c->hout));
+            c->hout = nullptr;
+            c->hout_bytes = 0;
+        }
+        CU(cudaHostAlloc(&c->hout, 2 * size_t(cap) * 16, cudaHostAllocDefault));
+        c->hout_bytes = 2 * size_t(cap) * 16;
     }
+    int64_t pend_lo[2] = {-1, -1}, pend_m[2] = {0, 0};  // staged chunk waiting in hout buffer b
+    auto drain = [&](int b) -> etune_status {
+        if (pend_lo[b] < 0) return ETUNE_OK;
+        CU(cudaEventSynchronize(c->ev_out[b]));
+        const double* sp = reinterpret_cast<const double*>(static_cast<char*>(c->hout) + size_t(b) * size_t(cap) * 16);
+        const uint64_t* si = reinterpret_cast<const uint64_t*>(sp + cap);
+        const int64_t lo2 = pend_lo[b], m2 = pend_m[b];
+        const int tasks = int(std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m2 / 4096)));
+        c->pool->run(tasks, [&](int t) {
+            const int64_t a = m2 * t / tasks, e = m2 * (t + 1) / tasks;
+            if (h_pred) std::memcpy(h_pred + lo2 + a, sp + a, size_t(e - a) * 8);
+            if (h_ids) std::memcpy(h_ids + lo2 + a, si + a, size_t(e - a) * 8);
+        });
+        pend_lo[b] = -1;
+        return ETUNE_OK;
+    };
     // the caller's earlier work on the ctx stream happens-before this call's copies
     CU(cudaEventRecord(c->ev_done[0], c->stream));
     CU(cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
@@ -1555,8 +1587,17 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
             return st;
         CU(cudaEventRecord(c->ev_done[b], c->stream));
         CU(cudaStreamWaitEvent(c->d2h, c->ev_done[b], 0));
-        if (h_pred) CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
-        if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+        if (stage_out) {
+            if (etune_status st = drain(b)) return st;  // chunk i-2's outputs out of staging buffer b
+            double* sp = reinterpret_cast<double*>(static_cast<char*>(c->hout) + size_t(b) * size_t(cap) * 16);
+            if (h_pred) CU(cudaMemcpyAsync(sp, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+            if (h_ids) CU(cudaMemcpyAsync(sp + cap, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+            pend_lo[b] = lo;
+            pend_m[b] = m;
+        } else {
+            if (h_pred) CU(cudaMemcpyAsync(h_pred + lo, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+            if (h_ids) CU(cudaMemcpyAsync(h_ids + lo, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
+        }
         CU(cudaEventRecord(c->ev_out[b], c->d2h));
     }
     if (k > 0) {  // keep the best over the whole population (its predictions are on the device)
@@ -1569,6 +1610,9 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         }
         CU(cudaMemcpyAsync(h_idx, d_idx, size_t(k) * 8, cudaMemcpyDeviceToHost, c->stream));
     }
+    if (stage_out)
+        for (int b = 0; b < 2; ++b)
+            if (etune_status st = drain(b)) return st;
     CU(cudaEventRecord(c->ev_out[0], c->d2h));
     CU(cudaStreamWaitEvent(c->stream, c->ev_out[0], 0));
     return etune_cu_synchronize(c, first_bad);

@@ -53,6 +53,8 @@ struct etune_cu_ctx {
     // *_host pipelines: pinned staging of narrowed Schedule rows, packed by a host pool
     void* hpin = nullptr;
     size_t hpin_bytes = 0;
+    void* hout = nullptr;  // pinned staging of outputs bound for pageable caller memory
+    size_t hout_bytes = 0;
     std::unique_ptr<etune_b200::HostPool> pool;
     // *_host pipelines: copy-in / copy-out streams and per-buffer events
     cudaStream_t h2d = nullptr, d2h = nullptr;

@@ -784,6 +784,7 @@ constexpr int kSRT = 512;
 constexpr int kSRPer = 8;
 constexpr int kSRMaxCtas = 1024;
 constexpr int kSRMaxSeg = 4096;    // segment histogram bins (shared memory)
+constexpr uint32_t kSRDirect = 4096;  // level-0 crossing: rank directly when below + in-bin are this few
 constexpr int kSRBatch = 4;        // candidates per thread whose loads are in flight together
 constexpr int kSRListCap = 8192;   // records ranked directly (64 KB of shared memory per CTA)
 static_assert(kSRListCap >= kSelMaxK, "the tie path appends at most k records");
@@ -794,12 +795,12 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+constexpr int kSRLevels = 3;  // radix-select levels over the group index (<= 2^25 groups)
 struct RowSelWork {
     uint32_t nlist, ticket, pad[2];
     uint32_t tiecnt[kSRMaxCtas];
-    uint32_t seg[kSRMaxSeg];   // candidates per segment of groups
-    uint32_t fine[kSRMaxSeg];  // tie path: candidates per group of the crossing segment
-    uint64_t lkey[kSRListCap]; // g << 32 | index of the appended records
+    uint32_t lvl[kSRLevels][kSRMaxSeg];  // candidates per bin of each radix-select level
+    uint64_t lkey[kSRListCap];           // g << 32 | index of the appended records
 };
 
 // exclusive block scan of one u32 per thread (blockDim = kSRT); *total = block sum
@@ -822,19 +823,6 @@ __device__ __forceinline__ uint32_t sr_block_scan(uint32_t v, uint32_t* ws, uint
     __syncthreads();
     *total = tot;
     return before + x - v;
-}
-
-__device__ __forceinline__ void sr_append(RowSelWork* W, bool take, uint64_t key) {
-    const unsigned m = __ballot_sync(0xffffffffu, take);
-    if (!m) return;
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&W->nlist, uint32_t(__popc(m)));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (take) {
-        const uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-        if (pos < uint32_t(kSRListCap)) W->lkey[pos] = key;
-    }
 }
 
 // smem histogram hs[0..nb) -> global g[0..nb), one atomic per non-empty bin
@@ -871,22 +859,81 @@ __device__ __forceinline__ void sr_cross(const uint32_t* g, int nb, uint32_t kk,
     __syncthreads();
 }
 
-// every CTA: stage the m appended records in shared memory, rank its share warp by warp
+// one-dimensional bulk copy global -> shared (TMA, cp.async.bulk) completing on an mbarrier
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// The m appended records (<= kSRListCap) get their output positions by counting: rank = records
+// with a smaller (g, index).  CTA c ranks records [32c, 32c + 32): lane l of every warp owns record
+// 32c + l, warp w compares it with the w-th sixteenth of the list (broadcast shared loads, staged
+// by one bulk copy), the sixteen partial counts are summed; rank < k goes to out[rank].
 __device__ __forceinline__ void sr_rank_out(const RowSelWork* W, uint32_t m, uint32_t k, unsigned long long* xk,
-                                            int64_t* out) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    const unsigned long long* lk = reinterpret_cast<const unsigned long long*>(W->lkey);
-    for (uint32_t i = tid; i < m; i += kSRT) xk[i] = __ldcg(lk + i);
-    __syncthreads();
-    const uint32_t nwarps = gridDim.x * (kSRT / 32);
-    for (uint32_t r = blockIdx.x * (kSRT / 32) + (tid >> 5); r < m; r += nwarps) {
-        const unsigned long long mine = xk[r];
+                                            int64_t* out, uint64_t* mbar, uint32_t phase, uint32_t* part) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int kW = kSRT / 32;
+    if (blockIdx.x * 32u >= m) return;  // block-uniform: this CTA owns no record
+    if (tid == 0) {
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // the list was written by generic stores
+        bulk_g2s(xk, W->lkey, (m * 8u + 15u) & ~15u, mbar);
+    }
+    mbar_wait(mbar, phase);
+    const uint32_t per = (m + kW - 1) / kW, j0 = warp * per, j1 = min(m, j0 + per);
+    for (uint32_t r0 = blockIdx.x * 32u; r0 < m; r0 += gridDim.x * 32u) {
+        const uint32_t r = r0 + lane;
+        const unsigned long long mine = r < m ? xk[r] : ~0ull;
         uint32_t cnt = 0;
-        for (uint32_t j = lane; j < m; j += 32) cnt += xk[j] < mine ? 1u : 0u;
-        for (int sft = 16; sft > 0; sft >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, sft);
-        if (lane == 0 && cnt < k) out[cnt] = int64_t(uint32_t(mine));
+#pragma unroll 8
+        for (uint32_t j = j0; j < j1; ++j) cnt += xk[j] < mine ? 1u : 0u;
+        part[warp * 32 + lane] = cnt;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t c = 0;
+#pragma unroll
+            for (int w = 0; w < kW; ++w) c += part[w * 32 + lane];
+            if (r < m && c < k) out[c] = int64_t(uint32_t(mine));
+        }
+        __syncthreads();
     }
 }
+
+// CTA-aggregated append of each thread's records (one global atomic per CTA): take(j) / key(j)
+template <typename Take, typename Key>
+__device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uint32_t* s_base, Take take, Key key) {
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j) cnt += take(j) ? 1u : 0u;
+    uint32_t tot;
+    uint32_t off = sr_block_scan(cnt, ws, &tot);
+    if (threadIdx.x == 0) *s_base = tot ? atomicAdd(&W->nlist, tot) : 0u;
+    __syncthreads();
+    off += *s_base;
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j)
+        if (take(j)) {
+            if (off < uint32_t(kSRListCap)) W->lkey[off] = key(j);
+            ++off;
+        }
+}
+
 
 __global__ void __launch_bounds__(kSRT, 2) score_select_rows_kernel(
     const uint8_t* __restrict__ gplan, const uint16_t* __restrict__ clskuv, const RowTabMeta* __restrict__ meta,
@@ -896,155 +943,179 @@ __global__ void __launch_bounds__(kSRT, 2) score_select_rows_kernel(
     unsigned long long* __restrict__ trace, int only_a) {
     namespace cg = cooperative_groups;
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[6] = globaltimer();
-    extern __shared__ uint32_t rsm[];  // [Kuv class table | histogram]; the ranked list in C
+    extern __shared__ __align__(16) uint32_t rsm[];  // [Kuv classes | histogram | k_tile words | key FNV]; list in C
     __shared__ uint32_t ws[kSRT / 32];
-    __shared__ uint32_t s_bin, s_before;
+    __shared__ uint32_t s_bin, s_before, s_base;
+    __shared__ uint32_t s_part[kSRT];
+    __shared__ __align__(8) uint64_t s_mbar;
     const int tid = threadIdx.x;
+    const uint32_t base = uint32_t(blockIdx.x) * uint32_t(per) * kSRT;  // n < 2^31
+    // the first batch's genomes are requested before anything else: they do not need the tables
+    uint64_t g0[kSRBatch];
+#pragma unroll
+    for (int b = 0; b < kSRBatch; ++b) {
+        const uint32_t i = base + uint32_t(b) * kSRT + tid;
+        g0[b] = (b < per && int64_t(i) < n) ? __ldcs(genome + i) : ~0ull;
+    }
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
     const int ndk = H.ndk;
     const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
     uint32_t* hist = rsm + ndk * 32;  // kSRMaxSeg bins
     uint32_t* sdivk = hist + kSRMaxSeg;
-    uint64_t* skh = reinterpret_cast<uint64_t*>(sdivk + ((ndk + 1) & ~1));  // per-key FNV state (when it fits)
+    uint64_t* skh = reinterpret_cast<uint64_t*>(sdivk + ((ndk + 3) & ~3));  // 16-byte aligned
     const uint32_t nkeys = uint32_t(H.nt[0]) * nt1 * nt2;
+    const bool bulk = khash_smem && ids;
+    uint32_t mphase = 0;  // parity of the next wait on s_mbar
+    if (tid == 0) mbar_init(&s_mbar);
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(clskuv);
         for (int i = tid; i < ndk * 32; i += kSRT) rsm[i] = __ldg(src + i);
         const int64_t* divk = at<int64_t>(gplan, H.off_divk);
         for (int i = tid; i < ndk; i += kSRT) sdivk[i] = uint32_t(divk[i]);
-        if (khash_smem && ids)
-            for (uint32_t i = tid; i < nkeys; i += kSRT) skh[i] = __ldg(khash + i);
     }
     const uint32_t groups = uint32_t(meta->groups);
     const int gbits = groups > 1 ? 32 - __clz(int(groups - 1)) : 0;
-    const int segshift = gbits > 12 ? gbits - 12 : 0;  // <= kSRMaxSeg segments of <= kSRMaxSeg groups
+    // level 0 of the radix select: <= 4096 bins of the group index
+    const int segshift = gbits > 12 ? gbits - 12 : 0;
     const int nseg = int((groups + (1u << segshift) - 1) >> segshift);
     for (int i = tid; i < nseg; i += kSRT) hist[i] = 0u;
     const uint32_t nkc = uint32_t(meta->nkc);
     __syncthreads();
+    if (bulk && tid == 0) bulk_g2s(skh, khash, (nkeys * 8u + 15u) & ~15u, &s_mbar);  // per-key FNV states (TMA)
     const uint16_t* scls = reinterpret_cast<const uint16_t*>(rsm);
-    const uint32_t base = uint32_t(blockIdx.x) * uint32_t(per) * kSRT;  // n < 2^31
     // ---- A: score, kSRBatch candidates per thread with all their loads in flight together
     uint32_t gg[kSRPer];
+    bool khash_ready = !bulk;
 #pragma unroll
     for (int j0 = 0; j0 < kSRPer; j0 += kSRBatch) {
         uint64_t g[kSRBatch];
-        bool v[kSRBatch];
 #pragma unroll
         for (int b = 0; b < kSRBatch; ++b) {
-            const uint32_t i = base + uint32_t(j0 + b) * kSRT + tid;
-            v[b] = j0 + b < per && int64_t(i) < n;
-            g[b] = v[b] ? __ldcs(genome + i) : 0ull;
+            if (j0 == 0) {
+                g[b] = g0[b];
+            } else {
+                const uint32_t i = base + uint32_t(j0 + b) * kSRT + tid;
+                g[b] = (j0 + b < per && int64_t(i) < n) ? __ldcs(genome + i) : ~0ull;  // ~0: no candidate
+            }
         }
         uint32_t row[kSRBatch], key[kSRBatch];
 #pragma unroll
         for (int b = 0; b < kSRBatch; ++b) {
-            const Genome x = genome_unpack(g[b]);
+            const Genome x = genome_unpack(g[b] != ~0ull ? g[b] : 0ull);
             key[b] = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
             const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
             row[b] = key[b] * nkc + kc;
         }
         double p[kSRBatch];
-        uint64_t h[kSRBatch];
 #pragma unroll
         for (int b = 0; b < kSRBatch; ++b) {  // one 16-byte gather per candidate: {prediction, group}
-            const double2 r = v[b] ? __ldg(reinterpret_cast<const double2*>(rowrec) + row[b]) : make_double2(0.0, 0.0);
+            const bool v = g[b] != ~0ull;
+            const double2 r = v ? __ldg(reinterpret_cast<const double2*>(rowrec) + row[b]) : make_double2(0.0, 0.0);
             p[b] = r.x;
-            gg[j0 + b] = v[b] ? uint32_t(__double_as_longlong(r.y)) : 0xffffffffu;
-            h[b] = (v[b] && ids) ? (khash_smem ? skh[key[b]] : __ldg(khash + key[b])) : 0ull;
+            gg[j0 + b] = v ? uint32_t(__double_as_longlong(r.y)) : 0xffffffffu;
+        }
+        if (ids && !khash_ready) {
+            mbar_wait(&s_mbar, 0);
+            khash_ready = true;
         }
 #pragma unroll
         for (int b = 0; b < kSRBatch; ++b) {
-            if (!v[b]) continue;
+            if (g[b] == ~0ull) continue;
             const uint32_t i = base + uint32_t(j0 + b) * kSRT + tid;
             pred[i] = p[b];
             atomicAdd(hist + (gg[j0 + b] >> segshift), 1u);
             if (ids) {
                 const Genome x = genome_unpack(g[b]);
+                const uint64_t h = bulk ? skh[key[b]] : __ldg(khash + key[b]);
                 __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
-                       static_cast<unsigned long long>(fnv_tail(fnv_small(h[b], sdivk[x.k]), x.u, x.v)));
+                       static_cast<unsigned long long>(fnv_tail(fnv_small(h, sdivk[x.k]), x.u, x.v)));
             }
         }
     }
+    if (bulk && !khash_ready) mbar_wait(&s_mbar, 0);  // the copy lands before the smem is reused
+    if (bulk) mphase = 1;
     __syncthreads();
-    sr_flush(hist, W->seg, nseg);
+    sr_flush(hist, W->lvl[0], nseg);
     if (trace && blockIdx.x == 0 && tid == 0) trace[0] = globaltimer();
     if (only_a) return;  // diagnostic: phase A alone (profilers cannot split a cooperative kernel)
     cg::this_grid().sync();
     if (trace && blockIdx.x == 0 && tid == 0) trace[1] = globaltimer();
-    // ---- B: the segment of the k-th candidate
+    // ---- B: radix select of the k-th candidate's group g* over the group index: at each level the
+    //      bin holding the k-th candidate still in play (every CTA, identically), then -- until a bin
+    //      is a single group -- the next 12 bits of g of the candidates in that bin, histogrammed per
+    //      CTA and flushed (one grid barrier per level; two levels for up to 2^20 groups)
     const uint32_t kk = uint32_t(k);
-    sr_cross(W->seg, nseg, kk, ws, &s_bin, &s_before);
-    const uint32_t sstar = s_bin, cb1 = s_before;
-    const uint32_t m = cb1 + __ldcg(W->seg + sstar);  // candidates below and in s*
+    uint32_t kr = kk, below = 0, P = 0;
+    int Sc = segshift, nbc = nseg, L = 0;
     unsigned long long* xk = reinterpret_cast<unsigned long long*>(rsm);
-    if (m <= uint32_t(kSRListCap)) {  // grid-uniform
-#pragma unroll
-        for (int j = 0; j < kSRPer; ++j)
-            sr_append(W, gg[j] != 0xffffffffu && (gg[j] >> segshift) <= sstar,
-                      (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid));
+    // the usual case: the candidates below and in the level-0 bin of the k-th are few -- rank them all
+    sr_cross(W->lvl[0], nbc, kr, ws, &s_bin, &s_before);
+    const uint32_t b0 = s_bin, m1 = s_before + __ldcg(W->lvl[0] + b0);
+    if (m1 <= kSRDirect) {  // grid-uniform
+        sr_append_block(W, ws, &s_base, [&](int j) { return gg[j] != 0xffffffffu && (gg[j] >> Sc) <= b0; },
+                        [&](int j) { return (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); });
         cg::this_grid().sync();
         if (trace && blockIdx.x == 0 && tid == 0) trace[2] = trace[3] = globaltimer();
-        for (int i = blockIdx.x * kSRT + tid; i < nseg; i += gridDim.x * kSRT) W->seg[i] = 0u;
-        // ---- C: ranks of the m records; the k smallest are the answer
-        sr_rank_out(W, m, kk, xk, out);
+        for (int i = blockIdx.x * kSRT + tid; i < nbc; i += gridDim.x * kSRT) W->lvl[0][i] = 0u;
+        sr_rank_out(W, m1, kk, xk, out, &s_mbar, mphase, s_part);
     } else {
-        // ---- B2: the k-th candidate's group inside s*, candidates below it, ties at it per CTA
-        const int segsz = 1 << segshift;
-        for (int i = tid; i < segsz; i += kSRT) hist[i] = 0u;
+    for (;; ++L) {
+        sr_cross(W->lvl[L], nbc, kr, ws, &s_bin, &s_before);
+        const uint32_t bin = s_bin;
+        below += s_before;
+        kr -= s_before;
+        P = (L == 0) ? bin : ((P << (nbc > 1 ? 31 - __clz(int(nbc)) : 0)) | bin);  // candidates with g >> Sc == P
+        if (Sc == 0) break;
+        const int Sn = Sc > 12 ? Sc - 12 : 0, nbn = 1 << (Sc - Sn);
+        for (int i = tid; i < nbn; i += kSRT) hist[i] = 0u;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kSRPer; ++j)
-            if (gg[j] != 0xffffffffu && (gg[j] >> segshift) == sstar)
-                atomicAdd(hist + (gg[j] & uint32_t(segsz - 1)), 1u);
+            if (gg[j] != 0xffffffffu && (gg[j] >> Sc) == P) atomicAdd(hist + ((gg[j] >> Sn) & uint32_t(nbn - 1)), 1u);
         __syncthreads();
-        sr_flush(hist, W->fine, segsz);
+        sr_flush(hist, W->lvl[L + 1], nbn);
         cg::this_grid().sync();
-        sr_cross(W->fine, segsz, kk - cb1, ws, &s_bin, &s_before);
-        const uint32_t gstar = (sstar << segshift) | s_bin;
-        const uint32_t need = kk - cb1 - s_before;  // >= 1 ties to take at g*
-        uint32_t my_ties = 0;
+        for (int i = blockIdx.x * kSRT + tid; i < nbc; i += gridDim.x * kSRT) W->lvl[L][i] = 0u;  // read by all
+        Sc = Sn;
+        nbc = nbn;
+    }
+    const uint32_t gstar = P;
+    const uint32_t need = kk - below;  // >= 1 candidates at g* are taken, by index
+    if (trace && blockIdx.x == 0 && tid == 0) trace[2] = globaltimer();
+    // ---- C: the candidates below g* (fewer than k) are appended; each CTA counts its ties at g*
+    auto gkey = [&](int j) { return (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); };
+    sr_append_block(W, ws, &s_base, [&](int j) { return gg[j] < gstar; }, gkey);
+    uint32_t my_ties = 0;
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j) my_ties += gg[j] == gstar;
+    uint32_t cta_ties;
+    sr_block_scan(my_ties, ws, &cta_ties);
+    if (tid == 0) W->tiecnt[blockIdx.x] = cta_ties;
+    cg::this_grid().sync();
+    if (trace && blockIdx.x == 0 && tid == 0) trace[3] = globaltimer();
+    for (int i = blockIdx.x * kSRT + tid; i < nbc; i += gridDim.x * kSRT) W->lvl[L][i] = 0u;
+    // ---- D: output positions without a sort.  A tie's position is below + its rank among the ties
+    //      by index: CTA b owns the contiguous indices [b*per*T, (b+1)*per*T) in (j, thread) order,
+    //      so that rank is (ties of the CTAs before b) + its order in the CTA; ranks < need are
+    //      written.  The records below g* are ranked among themselves by counting.
+    uint32_t before = 0;
+    for (uint32_t b2 = tid; b2 < blockIdx.x; b2 += kSRT) before += __ldcg(W->tiecnt + b2);
+    uint32_t tot_before;
+    sr_block_scan(before, ws, &tot_before);
+    if (cta_ties && tot_before < need) {  // block-uniform
+        uint32_t run = tot_before;
 #pragma unroll
         for (int j = 0; j < kSRPer; ++j) {
-            sr_append(W, gg[j] < gstar, (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid));
-            my_ties += gg[j] == gstar;
+            if (run >= need) break;  // block-uniform
+            const bool tie = gg[j] == gstar;
+            uint32_t tot;
+            const uint32_t o = sr_block_scan(tie ? 1u : 0u, ws, &tot);
+            if (tie && run + o < need) out[below + run + o] = int64_t(base + uint32_t(j) * kSRT + tid);
+            run += tot;
         }
-        uint32_t cta_ties;
-        sr_block_scan(my_ties, ws, &cta_ties);
-        if (tid == 0) W->tiecnt[blockIdx.x] = cta_ties;
-        cg::this_grid().sync();
-        if (trace && blockIdx.x == 0 && tid == 0) trace[2] = globaltimer();
-        // ---- C2: ties by index: a CTA whose quota covers all its ties appends them unordered,
-        //      only the CTA at the quota boundary takes its first ties in index order
-        uint32_t before = 0;
-        for (uint32_t b = tid; b < blockIdx.x; b += kSRT) before += __ldcg(W->tiecnt + b);
-        uint32_t tot_before;
-        sr_block_scan(before, ws, &tot_before);
-        const uint32_t quota = need > tot_before ? min(need - tot_before, cta_ties) : 0u;
-        if (quota == cta_ties) {
-#pragma unroll
-            for (int j = 0; j < kSRPer; ++j)
-                sr_append(W, gg[j] == gstar, (uint64_t(gstar) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid));
-        } else if (quota > 0) {
-            uint32_t taken = 0;
-#pragma unroll
-            for (int j = 0; j < kSRPer; ++j) {
-                if (taken >= quota) break;  // block-uniform
-                const bool tie = gg[j] == gstar;
-                uint32_t tot;
-                const uint32_t o = sr_block_scan(tie ? 1u : 0u, ws, &tot);
-                sr_append(W, tie && taken + o < quota,
-                          (uint64_t(gstar) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid));
-                taken += tot;
-            }
-        }
-        for (int i = blockIdx.x * kSRT + tid; i < nseg; i += gridDim.x * kSRT) W->seg[i] = 0u;
-        for (int i = blockIdx.x * kSRT + tid; i < segsz; i += gridDim.x * kSRT) W->fine[i] = 0u;
-        cg::this_grid().sync();
-        if (trace && blockIdx.x == 0 && tid == 0) trace[3] = globaltimer();
-        // ---- D2: the k records ranked like C
-        sr_rank_out(W, kk, kk, xk, out);
     }
+    if (below) sr_rank_out(W, below, kk, xk, out, &s_mbar, mphase, s_part);
+    }  // radix-select path
     if (trace && blockIdx.x == 0 && tid == 0) trace[4] = globaltimer();
     // the last CTA out resets the list for the next call
     __syncthreads();
@@ -1227,8 +1298,8 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
     if (k > kSelMaxK || k > n || n >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
     // [Kuv classes | histogram | k_tile words | per-key FNV states when <= 64 KB]; the ranked list reuses it
     int khash_smem = nkeys * 8 <= 64 * 1024 ? 1 : 0;
-    size_t sm = size_t(ndk) * 128 + size_t(kSRMaxSeg) * 4 + size_t((ndk + 1) & ~1) * 4 +
-                (khash_smem ? size_t(nkeys) * 8 : 0);
+    size_t sm = size_t(ndk) * 128 + size_t(kSRMaxSeg) * 4 + size_t((ndk + 3) & ~3) * 4 +
+                (khash_smem ? size_t((nkeys * 8 + 15) & ~int64_t(15)) : 0);
     if (sm < size_t(kSRListCap) * 8) sm = size_t(kSRListCap) * 8;
     static int per_sm = -1;
     static size_t attr_sm = 0;
@@ -1266,7 +1337,7 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
                                                       dim3(unsigned(grid)), dim3(kSRT), args, sm, c.stream);
     if (tr && e == cudaSuccess) {
         cudaStreamSynchronize(c.stream);
-        std::fprintf(stderr, "rowsel n=%lld grid=%lld per=%d: A %.2f | sync1 %.2f | B+sync %.2f | tie path %.2f | "
+        std::fprintf(stderr, "rowsel n=%lld grid=%lld per=%d: A %.2f | sync1 %.2f | select levels %.2f | append+sync %.2f | "
                      "rank %.2f | tail %.2f us\n", (long long)n, (long long)grid, per_i, (tr[0] - tr[6]) * 1e-3,
                      (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3,
                      (tr[5] - tr[4]) * 1e-3);
