@@ -75,87 +75,65 @@ __device__ __forceinline__ uint64_t rec_key(double x) {
     return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
 }
 
-// Merge of W sorted lists (rank-major, k records each) keeping the first k: the lists come from
-// ranks owning ascending, disjoint global index ranges, so (score, global index) order equals
-// (score key, position in the concatenation) order and the comparison needs no 64-bit index.
-// log2(W) rounds of pairwise merge-path merges (co-rank binary search per output) in shared
-// memory, ping-pong between two halves; one CTA.
-struct MergeView {
-    uint64_t* key;
-    uint32_t* pos;
-};
-
-__device__ __forceinline__ bool mless(const MergeView& v, uint32_t a, uint32_t b) {
-    return v.key[a] < v.key[b] || (v.key[a] == v.key[b] && v.pos[a] < v.pos[b]);
-}
-
-// element q (< k) of merge(A, B), A = [a0, a0 + k), B = [b0, b0 + k)
-__device__ __forceinline__ uint32_t merge_at(const MergeView& v, uint32_t a0, uint32_t b0, uint32_t k, uint32_t q) {
-    uint32_t lo = 0, hi = q;  // elements of A among the first q outputs
+// Merge of W sorted lists (rank-major, k records each) keeping the first k.  The lists come from
+// ranks owning ascending, disjoint global index ranges, so the (score, global index) order is the
+// (score key, list, position) order: a record at position j of list w has rank
+//   j + sum over lists w' < w of #(keys <= its key) + sum over lists w' > w of #(keys < its key),
+// each count one binary search.  CTA w ranks list w's k records against every other list staged in
+// shared memory (W * k keys); ranks < k are written.  W CTAs, no merge rounds.
+__device__ __forceinline__ uint32_t count_le(const uint64_t* a, uint32_t n, uint64_t x) {  // upper_bound
+    uint32_t lo = 0, hi = n;
     while (lo < hi) {
-        const uint32_t i = (lo + hi) >> 1, j = q - i;
-        if (j > 0 && mless(v, a0 + i, b0 + j - 1)) lo = i + 1;
-        else hi = i;
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] <= x) lo = mid + 1;
+        else hi = mid;
     }
-    const uint32_t i = lo, j = q - lo;
-    const bool take_a = j >= k || (i < k && mless(v, a0 + i, b0 + j));
-    return take_a ? a0 + i : b0 + j;
+    return lo;
+}
+__device__ __forceinline__ uint32_t count_lt(const uint64_t* a, uint32_t n, uint64_t x) {  // lower_bound
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
 }
 
-__global__ void __launch_bounds__(1024, 1) merge_records_kernel(const ShardRec* __restrict__ rec, int W, int k,
-                                                                int64_t* __restrict__ idx, double* __restrict__ sc) {
+__global__ void __launch_bounds__(1024) merge_records_kernel(const ShardRec* __restrict__ rec, int W, int k,
+                                                             int64_t* __restrict__ idx, double* __restrict__ sc) {
     extern __shared__ unsigned long long msm[];
+    uint64_t* keys = reinterpret_cast<uint64_t*>(msm);  // [W][k]
     const int tot = W * k;
-    MergeView v[2];
-    v[0].key = reinterpret_cast<uint64_t*>(msm);
-    v[1].key = v[0].key + tot;
-    v[0].pos = reinterpret_cast<uint32_t*>(v[1].key + tot);
-    v[1].pos = v[0].pos + tot;
-    for (int i = threadIdx.x; i < tot; i += blockDim.x) {
-        v[0].key[i] = rec_key(rec[i].s);
-        v[0].pos[i] = uint32_t(i);
+    // 8 independent loads in flight per thread (one dependent round trip per 8 K records, not per record)
+    for (int base = 0; base < tot; base += 8 * int(blockDim.x)) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + u * int(blockDim.x) + int(threadIdx.x);
+            v[u] = i < tot ? __ldg(&rec[i].s) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = base + u * int(blockDim.x) + int(threadIdx.x);
+            if (i < tot) keys[i] = rec_key(v[u]);
+        }
     }
     __syncthreads();
-    int cur = 0, L = W;
-    while (L > 1) {
-        const int pairs = L >> 1;
-        const MergeView& a = v[cur];
-        MergeView& b = v[cur ^ 1];
-        for (int t = threadIdx.x; t < pairs * k; t += blockDim.x) {
-            const int pr = t / k, q = t - pr * k;
-            const uint32_t src = merge_at(a, uint32_t(2 * pr * k), uint32_t((2 * pr + 1) * k), uint32_t(k), uint32_t(q));
-            b.key[pr * k + q] = a.key[src];
-            b.pos[pr * k + q] = a.pos[src];
+    const int w = blockIdx.x;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) {
+        const uint64_t x = keys[w * k + j];
+        uint32_t r = uint32_t(j);
+        // stop as soon as the rank reaches k: deep records leave after one or two searches
+        for (int d = 1; d < W && r < uint32_t(k); ++d) {
+            const int v = (w + d) % W;
+            r += v < w ? count_le(keys + v * k, uint32_t(k), x) : count_lt(keys + v * k, uint32_t(k), x);
         }
-        if (L & 1)  // the odd list moves down unchanged
-            for (int t = threadIdx.x; t < k; t += blockDim.x) {
-                b.key[pairs * k + t] = a.key[(L - 1) * k + t];
-                b.pos[pairs * k + t] = a.pos[(L - 1) * k + t];
-            }
-        __syncthreads();
-        cur ^= 1;
-        L = pairs + (L & 1);
-    }
-    for (int t = threadIdx.x; t < k; t += blockDim.x) {
-        const ShardRec r = rec[v[cur].pos[t]];
-        idx[t] = r.g;
-        if (sc) sc[t] = r.s;
-    }
-}
-
-// the same merge round by round in global memory (W * k beyond shared memory): one launch per round
-__global__ void merge_round_kernel(const uint64_t* __restrict__ ka, const uint32_t* __restrict__ pa, int L, int k,
-                                   uint64_t* __restrict__ kb, uint32_t* __restrict__ pb) {
-    const MergeView a{const_cast<uint64_t*>(ka), const_cast<uint32_t*>(pa)};
-    const int pairs = L >> 1;
-    for (int64_t t = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; t < int64_t(pairs + (L & 1)) * k;
-         t += int64_t(gridDim.x) * blockDim.x) {
-        const int pr = int(t / k), q = int(t - int64_t(pr) * k);
-        uint32_t src;
-        if (pr < pairs) src = merge_at(a, uint32_t(2 * pr * k), uint32_t((2 * pr + 1) * k), uint32_t(k), uint32_t(q));
-        else src = uint32_t((L - 1) * k + q);
-        kb[t] = ka[src];
-        pb[t] = pa[src];
+        if (r < uint32_t(k)) {
+            const ShardRec q = rec[w * k + j];
+            idx[r] = q.g;
+            if (sc) sc[r] = q.s;
+        }
     }
 }
 
@@ -167,12 +145,22 @@ __global__ void merge_keys_kernel(const ShardRec* __restrict__ rec, int64_t tot,
     }
 }
 
-__global__ void merge_out_kernel(const ShardRec* __restrict__ rec, const uint32_t* __restrict__ pos, int k,
-                                 int64_t* __restrict__ idx, double* __restrict__ sc) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < k; t += gridDim.x * blockDim.x) {
-        const ShardRec r = rec[pos[t]];
-        idx[t] = r.g;
-        if (sc) sc[t] = r.s;
+// the same ranking with the keys in global memory (W * k beyond shared memory): one thread per record
+__global__ void merge_rank_kernel(const ShardRec* __restrict__ rec, const uint64_t* __restrict__ keys, int W, int k,
+                                  int64_t* __restrict__ idx, double* __restrict__ sc) {
+    const int64_t tot = int64_t(W) * k;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < tot; i += int64_t(gridDim.x) * blockDim.x) {
+        const int w = int(i / k), j = int(i - int64_t(w) * k);
+        const uint64_t x = keys[i];
+        uint32_t r = uint32_t(j);
+        for (int d = 1; d < W && r < uint32_t(k); ++d) {
+            const int v = (w + d) % W;
+            r += v < w ? count_le(keys + int64_t(v) * k, uint32_t(k), x) : count_lt(keys + int64_t(v) * k, uint32_t(k), x);
+        }
+        if (r < uint32_t(k)) {
+            idx[r] = rec[i].g;
+            if (sc) sc[r] = rec[i].s;
+        }
     }
 }
 
@@ -222,11 +210,11 @@ cudaError_t launch_merge_records(const LaunchCtx& c, const ShardRec* d_rec, int 
                                  double* d_sc, void* d_scratch) {
     if (k <= 0 || W <= 0) return cudaSuccess;
     const int64_t tot = int64_t(W) * k;
-    const size_t smem = size_t(tot) * 24;
+    const size_t smem = size_t(tot) * 8;
     int dev = 0, optin = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (smem <= size_t(optin) && tot < (int64_t(1) << 31)) {
+    if (smem <= size_t(optin)) {
         static size_t attr = 0;
         if (smem > attr) {
             const cudaError_t e =
@@ -234,28 +222,15 @@ cudaError_t launch_merge_records(const LaunchCtx& c, const ShardRec* d_rec, int 
             if (e != cudaSuccess) return e;
             attr = size_t(optin);
         }
-        merge_records_kernel<<<1, 1024, smem, c.stream>>>(d_rec, W, int(k), d_idx, d_sc);
+        merge_records_kernel<<<W, 1024, smem, c.stream>>>(d_rec, W, int(k), d_idx, d_sc);
         note_launches(1);
         return cudaGetLastError();
     }
-    uint64_t* k0 = static_cast<uint64_t*>(d_scratch);
-    uint64_t* k1 = k0 + tot;
-    uint32_t* p0 = reinterpret_cast<uint32_t*>(k1 + tot);
-    uint32_t* p1 = p0 + tot;
+    uint64_t* keys = static_cast<uint64_t*>(d_scratch);
     const int grid = int(std::min<int64_t>((tot + 255) / 256, int64_t(c.sm_count) * 8));
-    merge_keys_kernel<<<grid, 256, 0, c.stream>>>(d_rec, tot, k0, p0);
-    int L = W, launches = 2;
-    uint64_t* kk[2] = {k0, k1};
-    uint32_t* pp[2] = {p0, p1};
-    int cur = 0;
-    while (L > 1) {
-        merge_round_kernel<<<grid, 256, 0, c.stream>>>(kk[cur], pp[cur], L, int(k), kk[cur ^ 1], pp[cur ^ 1]);
-        cur ^= 1;
-        L = (L >> 1) + (L & 1);
-        ++launches;
-    }
-    merge_out_kernel<<<int((k + 255) / 256), 256, 0, c.stream>>>(d_rec, pp[cur], int(k), d_idx, d_sc);
-    note_launches(launches);
+    merge_keys_kernel<<<grid, 256, 0, c.stream>>>(d_rec, tot, keys, reinterpret_cast<uint32_t*>(keys + tot));
+    merge_rank_kernel<<<grid, 256, 0, c.stream>>>(d_rec, keys, W, int(k), d_idx, d_sc);
+    note_launches(2);
     return cudaGetLastError();
 }
 

@@ -780,7 +780,7 @@ __global__ void rowtab_pack_kernel(const RowTabMeta* __restrict__ meta, const do
 //   k-th group g*, appends the candidates below g* and counts each CTA's ties at g*; C2 takes the
 //   ties by index (CTA b owns the contiguous indices [b*per*T, (b+1)*per*T) in (j, thread)
 //   order, so its quota is need - (ties of CTAs before it)); D2 ranks the k records like C.
-constexpr int kSRT = 512;
+constexpr int kSRT = 1024;  // one CTA per SM (64 registers x 1024 threads): half the CTAs to synchronise and to stage tables
 constexpr int kSRPer = 8;
 constexpr int kSRMaxCtas = 1024;
 constexpr int kSRMaxSeg = 4096;    // segment histogram bins (shared memory)
@@ -796,11 +796,13 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 constexpr int kSRLevels = 3;  // radix-select levels over the group index (<= 2^25 groups)
+constexpr int kSRRep = 8;  // replicas of the appended list: the ranking CTAs read different L2 lines
 struct RowSelWork {
-    uint32_t nlist, ticket, pad[2];
+    uint32_t nlist, ticket, ticket1, pad;
+    uint32_t cross[4];                   // level-0 crossing {bin, count below, candidates below + in bin}
     uint32_t tiecnt[kSRMaxCtas];
     uint32_t lvl[kSRLevels][kSRMaxSeg];  // candidates per bin of each radix-select level
-    uint64_t lkey[kSRListCap];           // g << 32 | index of the appended records
+    uint64_t lkey[kSRRep][kSRListCap];   // g << 32 | index of the appended records, kSRRep copies
 };
 
 // exclusive block scan of one u32 per thread (blockDim = kSRT); *total = block sum
@@ -893,7 +895,7 @@ __device__ __forceinline__ void sr_rank_out(const RowSelWork* W, uint32_t m, uin
     if (blockIdx.x * 32u >= m) return;  // block-uniform: this CTA owns no record
     if (tid == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");  // the list was written by generic stores
-        bulk_g2s(xk, W->lkey, (m * 8u + 15u) & ~15u, mbar);
+        bulk_g2s(xk, W->lkey[blockIdx.x % kSRRep], (m * 8u + 15u) & ~15u, mbar);
     }
     mbar_wait(mbar, phase);
     const uint32_t per = (m + kW - 1) / kW, j0 = warp * per, j1 = min(m, j0 + per);
@@ -929,13 +931,17 @@ __device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uin
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j)
         if (take(j)) {
-            if (off < uint32_t(kSRListCap)) W->lkey[off] = key(j);
+            if (off < uint32_t(kSRListCap)) {
+                const uint64_t kv = key(j);
+#pragma unroll
+                for (int r = 0; r < kSRRep; ++r) W->lkey[r][off] = kv;
+            }
             ++off;
         }
 }
 
 
-__global__ void __launch_bounds__(kSRT, 2) score_select_rows_kernel(
+__global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const uint8_t* __restrict__ gplan, const uint16_t* __restrict__ clskuv, const RowTabMeta* __restrict__ meta,
     const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash, int khash_smem,
     const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, double* __restrict__ pred,
@@ -1038,6 +1044,22 @@ __global__ void __launch_bounds__(kSRT, 2) score_select_rows_kernel(
     sr_flush(hist, W->lvl[0], nseg);
     if (trace && blockIdx.x == 0 && tid == 0) trace[0] = globaltimer();
     if (only_a) return;  // diagnostic: phase A alone (profilers cannot split a cooperative kernel)
+    // the last CTA to flush finds the level-0 crossing once (every CTA reading the same counts would
+    // queue on the same L2 lines) and publishes it before the barrier
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_base = atomicAdd(&W->ticket1, 1u) == gridDim.x - 1 ? 1u : 0u;
+    __syncthreads();
+    if (s_base) {  // block-uniform
+        __threadfence();
+        sr_cross(W->lvl[0], nseg, uint32_t(k), ws, &s_bin, &s_before);
+        if (tid == 0) {
+            W->cross[0] = s_bin;
+            W->cross[1] = s_before;
+            W->cross[2] = s_before + __ldcg(W->lvl[0] + s_bin);
+            W->ticket1 = 0u;
+        }
+    }
     cg::this_grid().sync();
     if (trace && blockIdx.x == 0 && tid == 0) trace[1] = globaltimer();
     // ---- B: radix select of the k-th candidate's group g* over the group index: at each level the
@@ -1049,8 +1071,7 @@ __global__ void __launch_bounds__(kSRT, 2) score_select_rows_kernel(
     int Sc = segshift, nbc = nseg, L = 0;
     unsigned long long* xk = reinterpret_cast<unsigned long long*>(rsm);
     // the usual case: the candidates below and in the level-0 bin of the k-th are few -- rank them all
-    sr_cross(W->lvl[0], nbc, kr, ws, &s_bin, &s_before);
-    const uint32_t b0 = s_bin, m1 = s_before + __ldcg(W->lvl[0] + b0);
+    const uint32_t b0 = __ldcg(W->cross + 0), m1 = __ldcg(W->cross + 2);
     if (m1 <= kSRDirect) {  // grid-uniform
         sr_append_block(W, ws, &s_base, [&](int j) { return gg[j] != 0xffffffffu && (gg[j] >> Sc) <= b0; },
                         [&](int j) { return (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); });
