@@ -37,6 +37,7 @@ void ctx_free_now(etune_cu_ctx* c) {
     cudaFree(c->scratch);
     cudaFree(c->io);
     cudaFree(c->breed);
+    cudaFree(c->breedpar);
     cudaFree(c->shard);
     cudaFree(c->sel);
     cudaFree(c->rowsel);
@@ -1716,6 +1717,24 @@ etune_status etune_cu_forest_from_device(etune_cu_ctx* c, const int32_t* d_featu
 }
 
 namespace {
+// generations of at least this many offspring take the block-parallel exact path.  Diagnostic
+// knobs (read per call; tests use them to force every fallback): ETUNE_BREED_PAR_MIN (a huge
+// value keeps every call on the single-CTA chain), ETUNE_BREED_PAR_SD (window half-width in
+// standard deviations; small values force window misses), ETUNE_BREED_PAR_WORDS (stream
+// capacity; small values force the single-CTA fallback).
+int64_t breed_par_min() {
+    if (const char* e = std::getenv("ETUNE_BREED_PAR_MIN")) return int64_t(std::atoll(e));
+    return int64_t(4096);
+}
+double breed_par_sd() {
+    if (const char* e = std::getenv("ETUNE_BREED_PAR_SD")) return std::atof(e);
+    return 5.0;
+}
+size_t breed_par_words() {
+    if (const char* e = std::getenv("ETUNE_BREED_PAR_WORDS")) return size_t(std::atoll(e));
+    return 0;
+}
+
 etune_status reproduce_impl(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_par, int64_t np, int64_t n,
                             const etune_genetic_rates* rates, uint64_t seed, uint64_t* d_out, int32_t* d_partner,
                             uint64_t* d_ids, bool counter) {
@@ -1746,9 +1765,34 @@ etune_status reproduce_impl(etune_cu_ctx* c, const etune_cu_plan* p, const uint6
     if (counter)
         CU(launch_breed_counter(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover,
                                 r.copy, seed, d_out, d_partner));
-    else
+    else {
+        // exact mode: the block-parallel path for large generations (the single-CTA chain
+        // kernel after it exits at once unless the parallel path could not hold the generation)
+        const int32_t* d_done = nullptr;
+        if (n >= breed_par_min()) {
+            const int S = breed_par_block(n);
+            size_t words = 0, pool = 0;
+            const size_t pneed = breed_par_bytes(n, S, &words, &pool);
+            if (c->breedpar_bytes < pneed) {
+                if (c->breedpar) {
+                    CU(cudaStreamSynchronize(c->stream));
+                    CU(cudaFree(c->breedpar));
+                    c->breedpar = nullptr;
+                    c->breedpar_bytes = 0;
+                }
+                CU(cudaMalloc(&c->breedpar, pneed));
+                c->breedpar_bytes = pneed;
+            }
+            int32_t* done = nullptr;
+            CU(launch_breed_par(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover,
+                                r.copy, seed, d_out, d_partner, c->breedpar, S, breed_par_sd(), breed_par_words(),
+                                (std::getenv("ETUNE_BREED_PAR_SPLITGEN") ? 1 : 0) | (std::getenv("ETUNE_BREED_PAR_PROF") ? 2 : 0) |
+                                    (std::getenv("ETUNE_BREED_PAR_CHECK") ? 4 : 0), p->build.hdr.off_gridkey, &done));
+            d_done = done;
+        }
         CU(launch_breed(c->lc(), p->d_blob, p->build.hdr.total, d_par, d_pid, np, n, r.mutation, r.crossover, r.copy,
-                        seed, d_out, d_partner, c->breed));
+                        seed, d_out, d_partner, c->breed, d_done));
+    }
     if (d_ids) CU(launch_ids(c->lc(), p->d_blob, p->build.hdr.total, d_out, n, d_ids));
     return ETUNE_OK;
 }

@@ -34,6 +34,8 @@ struct etune_cu_ctx {
     size_t io_bytes = 0;
     void* breed = nullptr;  // BreedState + parent ids
     size_t breed_bytes = 0;
+    void* breedpar = nullptr;  // block-parallel exact reproduce work area (breed_par.cu)
+    size_t breedpar_bytes = 0;
     ncclComm_t comm = nullptr;
     int nranks = 1, rank = 0;
     etune_transport transport{};  // caller's collectives when no NCCL communicator is attached

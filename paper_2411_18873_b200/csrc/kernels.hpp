@@ -143,7 +143,20 @@ cudaError_t launch_topk(const LaunchCtx& c, const double* d_score, int64_t n, in
 size_t breed_state_bytes();
 cudaError_t launch_breed(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
                          const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
-                         uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_state);
+                         uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_state,
+                         const int32_t* d_skip = nullptr);
+
+// reproduce, exact and block-parallel (breed_par.cu): the same children as launch_breed on the
+// whole GPU.  Work area from breed_par_bytes(n, S, ...), S = breed_par_block(n).  *d_done is set
+// to 1 on the device when the parallel path produced the generation; launch_breed(..., d_done)
+// after it produces the generation otherwise (a stream or snapshot capacity did not fit).
+int breed_par_block(int64_t n);
+size_t breed_par_bytes(int64_t n, int S, size_t* stream_words, size_t* pool_cap);
+cudaError_t launch_breed_par(const LaunchCtx& c, const uint8_t* d_plan, uint32_t plan_bytes, const uint64_t* d_par,
+                             const uint64_t* d_pid, int64_t np, int64_t n, double mut, double cro, double cpy,
+                             uint64_t seed, uint64_t* d_out, int32_t* d_partner, void* d_work, int S,
+                             double sd_mult, size_t words_cap, int split_gen, uint32_t plan_pre,
+                             int32_t** d_done);
 
 // reproduce in the opt-in counter mode: offspring i draws from its own counter-based stream
 // (breed.cu CounterCursor), one thread per offspring; same decision logic as the exact mode.

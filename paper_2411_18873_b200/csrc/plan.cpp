@@ -275,15 +275,7 @@ etune_status build_plan(const etune_op_spec& op, const etune_device_config& dev,
     blob.assign(align16(sizeof(PlanHdr)), 0);
     for (int d = 0; d < 3; ++d) H.off_til[d] = put(blob, P->til[d].data(), P->til[d].size());
     H.off_divk = put(blob, P->divk.data(), P->divk.size());
-    H.off_gridkey = put(blob, P->gridkey.data(), P->gridkey.size());
-    H.off_grid = put(blob, P->grid.data(), P->grid.size());
-    H.off_int2 = put(blob, P->int2.data(), P->int2.size());
-    H.off_glb2 = put(blob, P->glb2.data(), P->glb2.size());
-    H.off_block = put(blob, P->block.data(), P->block.size());
-    H.off_ptn = put(blob, P->ptn.data(), P->ptn.size());
-    H.off_steps = put(blob, P->steps.data(), P->steps.size());
-    H.off_lvl = put(blob, P->lvl, 4);
-    for (int d = 0; d < 3; ++d) {  // repair fit tables (breed_kernel)
+    for (int d = 0; d < 3; ++d) {  // repair fit tables (reproduce); the breed kernels stage [0, off_gridkey)
         std::vector<uint32_t> tv;
         for (const TilingRec& r : P->til[d]) tv.push_back(r.threads);
         std::sort(tv.begin(), tv.end());
@@ -307,6 +299,14 @@ etune_status build_plan(const etune_op_spec& op, const etune_device_config& dev,
         if (!list.empty()) std::memcpy(blk.data() + o, list.data(), 2 * list.size());
         H.off_fit[d] = put(blob, blk.data(), blk.size());
     }
+    H.off_gridkey = put(blob, P->gridkey.data(), P->gridkey.size());
+    H.off_grid = put(blob, P->grid.data(), P->grid.size());
+    H.off_int2 = put(blob, P->int2.data(), P->int2.size());
+    H.off_glb2 = put(blob, P->glb2.data(), P->glb2.size());
+    H.off_block = put(blob, P->block.data(), P->block.size());
+    H.off_ptn = put(blob, P->ptn.data(), P->ptn.size());
+    H.off_steps = put(blob, P->steps.data(), P->steps.size());
+    H.off_lvl = put(blob, P->lvl, 4);
     blob.resize(align16(blob.size()));
     H.total = uint32_t(blob.size());
     std::memcpy(blob.data(), &H, sizeof(H));

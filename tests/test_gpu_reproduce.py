@@ -165,3 +165,106 @@ def test_reproduce_counter_mode_speed(oracle, ctx, capi):
     ms = e0.elapsed_time(e1) / 5
     print(f"counter-mode reproduce 2^20: {ms:.3f} ms")
     assert ms < 10.0
+
+
+# ---- the block-parallel exact path (breed_par.cu): every generation of >= 4096 offspring above
+# already runs it; these pin the bench-scale case, each fallback and the speed.
+
+@pytest.fixture
+def envset():
+    import os
+    saved = {}
+
+    def set_(k, v):
+        saved.setdefault(k, os.environ.get(k))
+        os.environ[k] = str(v)
+    yield set_
+    for k, v in saved.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
+
+
+def test_reproduce_exact_bench_config(oracle, ctx, capi):
+    """bench.py's generation: reproduce(sample_random(conv3x3, 1024, 42), 2^20, seed 7) — the
+    reference's single mt19937_64 stream, bit-exact, on the block-parallel path."""
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    par, _ = oracle.sample_random(op, 1024, 42)
+    n = 1 << 20
+    check(oracle, capi, op, par, n, run(capi, ctx, op, par, n, 7), 7)
+
+
+@pytest.mark.parametrize("sd", ["0.05", "1.0"])
+def test_reproduce_exact_window_misses(oracle, ctx, capi, envset, sd):
+    """Windows far too narrow: most block starts fall outside them and the chain kernel walks
+    those blocks exactly on the spot; the children are unchanged."""
+    envset("ETUNE_BREED_PAR_SD", sd)
+    op = parse_op("mm:1,512,3072,768")
+    par, _ = oracle.sample_random(op, 333, 42)
+    n = 70001
+    check(oracle, capi, op, par, n, run(capi, ctx, op, par, n, 13), 13)
+
+
+def test_reproduce_exact_capacity_fallback(oracle, ctx, capi, envset):
+    """A stream capacity too small for the generation: the parallel path stands down on the
+    device and the single-CTA chain produces the generation."""
+    envset("ETUNE_BREED_PAR_WORDS", "1000")
+    op = parse_op("conv:1,28,28,128,512,1,1,0")
+    par, _ = oracle.sample_random(op, 200, 4)
+    check(oracle, capi, op, par, 30000, run(capi, ctx, op, par, 30000, 3), 3)
+
+
+def test_reproduce_exact_single_cta_agrees(oracle, ctx, capi, envset):
+    """The single-CTA chain (ETUNE_BREED_PAR_MIN above n) and the parallel path give identical
+    children on the same call."""
+    op = parse_op("mm:4,96,200,50")
+    par, _ = oracle.sample_random(op, 300, 5)
+    a = run(capi, ctx, op, par, 40000, 17)
+    envset("ETUNE_BREED_PAR_MIN", str(1 << 40))
+    b = run(capi, ctx, op, par, 40000, 17)
+    for x, y in zip(a, b):
+        assert (x == y).all()
+
+
+@pytest.mark.parametrize("n", [4096, 4097, 8191, 65537, 262143])
+def test_reproduce_exact_sizes(oracle, ctx, capi, n):
+    """Block-size boundaries (S adapts to n; ragged last blocks and sub-blocks)."""
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    par, _ = oracle.sample_random(op, 1000, 9)
+    check(oracle, capi, op, par, n, run(capi, ctx, op, par, n, n), n)
+
+
+def test_reproduce_exact_speed(ctx, capi):
+    """2^20 offspring of the reference's own stream in well under the single-CTA chain's 252 ms."""
+    op = parse_op("conv:1,56,56,64,64,3,1,1")
+    plan = capi.Plan(ctx, op)
+    g = plan.sample_random(1024, 42)
+    capi.reproduce(plan, g, 1 << 20, 7)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for r in range(3):
+        capi.reproduce(plan, g, 1 << 20, 7 + r)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 3
+    print(f"exact reproduce 2^20 (block-parallel): {ms:.3f} ms")
+    assert ms < 25.0
+
+
+@pytest.mark.parametrize("text,npar,n,rates,limits", [
+    ("conv:1,56,56,64,64,3,1,1", 1024, 1 << 18, (0.85, 0.10, 0.05), None),
+    ("mm:1,512,3072,768", 97, 100000, (0.2, 0.7, 0.1), None),
+    ("mm:1,256,512,384", 100, 100000, (0.85, 0.10, 0.05), (128, 8, 4)),   # tight block cap: re-picks
+    ("mm:1,256,512,384", 100, 60000, (0.5, 0.5, 0.0), (64, 1, 2)),
+    ("mm:4,96,200,50", 300, 60000, (1.0, 0.0, 0.0), None),
+])
+def test_reproduce_exact_fast_count_agrees(oracle, ctx, capi, envset, text, npar, n, rates, limits):
+    """ETUNE_BREED_PAR_CHECK: every window walker's straight-line word count is re-derived by
+    breed_body (the reference's decision code) and a disagreement fails the call; children exact."""
+    envset("ETUNE_BREED_PAR_CHECK", "1")
+    op = parse_op(text)
+    lim = None if limits is None else np.array(limits, np.int64)
+    par, _ = oracle.sample_random(op, npar, 42, lim)
+    check(oracle, capi, op, par, n, run(capi, ctx, op, par, n, 23, rates, lim), 23, rates, lim)
