@@ -77,6 +77,7 @@ def parse():
     p.add_argument("--no-sweep", action="store_true")
     p.add_argument("--no-search", action="store_true", help="skip the search-round latency measurement")
     p.add_argument("--search-rounds", type=int, default=5)
+    p.add_argument("--no-reproduce", action="store_true", help="skip the reproduce (2^20 offspring) timing")
     return p.parse_args()
 
 
@@ -297,6 +298,57 @@ def search_round_latency(ctx, capi, rounds: int):
                       "100-tree retrain on all accumulated samples every round"}
 
 
+def reproduce_timing(ctx, capi, plan, parents, n: int, with_cpu: bool):
+    """reproduce (genetic.cpp:137-187) of an n-offspring generation from the bench's 1024 parents:
+    the exact mode (the reference's one mt19937_64 stream, block-parallel), the same call on the
+    single-CTA chain, the opt-in counter mode; device time with CUDA events on the ctx stream,
+    median of 3 after one warm-up.  Beside it the reference's own reproduce (oracle/_ref,
+    single-threaded, as the reference runs) on a 2^17 sample of the same generation."""
+    import torch
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        out = []
+        for r in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            out.append(e0.elapsed_time(e1))
+        return statistics.median(out)
+
+    res = {"offspring": n, "parents": int(parents.shape[0]), "unit": "ms"}
+    res["exact_ms"] = timed(lambda: capi.reproduce(plan, parents, n, 7))
+    res["counter_ms"] = timed(lambda: capi.reproduce(plan, parents, n, 7, counter=True))
+    os.environ["ETUNE_BREED_PAR_MIN"] = str(1 << 62)
+    try:
+        res["single_cta_exact_ms"] = timed(lambda: capi.reproduce(plan, parents, n, 7), reps=1)
+    finally:
+        del os.environ["ETUNE_BREED_PAR_MIN"]
+    res["exact_offspring_per_s"] = n / (res["exact_ms"] / 1e3)
+    if with_cpu:
+        try:
+            from etune_testlib import RefLib, have_ref
+            if have_ref():
+                import numpy as np
+                par = plan.decode(parents).cpu().numpy().astype(np.int64)
+                m = 1 << 17
+                t0 = time.perf_counter()
+                RefLib().reproduce(parse_op_text(OP_TEXT), par, m, 7)
+                dt = time.perf_counter() - t0
+                res["cpu_reference"] = {"offspring_per_s": m / dt, "cores": 1, "kind": "reference",
+                                        "projected_ms": n / (m / dt) * 1e3,
+                                        "sample": f"etune::reproduce(1024 parents -> {m}) of oracle/_ref, one thread"}
+        except Exception as e:  # reported, never required
+            res["cpu_reference"] = {"unavailable": str(e)[:200]}
+    res["what"] = ("exact: block-parallel resolution of the reference's single RNG stream (breed_par.cu), "
+                   "bit-exact; single_cta_exact: the same children on round 1's one-CTA chain; counter: the opt-in "
+                   "per-offspring counter-based stream (not the reference's)")
+    return res
+
+
 def parse_op_text(text):
     from etune_testlib import parse_op
     return parse_op(text)
@@ -499,6 +551,9 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             round_latency["value"] = t.item()
             round_latency["sharded_over_ranks"] = world
+    repro = None
+    if rank == 0 and not args.no_reproduce:
+        repro = reproduce_timing(ctx, capi, plan, parents, 1 << 20, with_cpu=(world == 1 and not args.no_cpu_baseline))
     if rank == 0 and world == 1 and not args.no_search:
         if not args.no_cpu_baseline:
             try:
@@ -559,6 +614,8 @@ def run_ours(args):
         line["sweep"] = sweep
     if e2e:
         line["e2e"] = e2e
+    if repro:
+        line["reproduce"] = repro
     if round_latency:
         line["search_round_latency"] = round_latency
         if cpu_round:
