@@ -34,6 +34,8 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <vector>
 
 #include "etune_internal.hpp"
 #include "kernels.hpp"
@@ -766,28 +768,41 @@ __global__ void rowtab_pack_kernel(const RowTabMeta* __restrict__ meta, const do
 // ------------------------------------------------ fused score + keep-the-best
 // One cooperative grid.  A candidate's prediction is its row's, and its place in prediction order
 // is its row's group g (the dense rank of the row's prediction: equal predictions, equal g), so
-// the k best by (prediction, index) are the k smallest (g, index).  Every thread keeps its
-// candidates' g in registers across the grid barriers (nothing is re-read, and no per-candidate
-// global atomic: copies of one parent share a row and would serialise in L2):
-//   A   score: genome -> row -> {prediction, g} (one 16-byte gather) -> prediction (+ id from the
-//       per-key FNV state in shared memory) out; a shared-memory histogram of g by segment
-//       (G / 4096 groups each), flushed with one atomic per non-empty segment per CTA;
-//   B   (every CTA) the segment s* holding the k-th candidate.  When the candidates below and in
-//       s* are few (m <= kSRListCap, the usual case) they are all appended (g, index), and
-//   C   every CTA stages that list in shared memory and gives each of its records, warp by warp,
-//       its rank = the records with a smaller (g, index); rank < k goes to out[rank].
-//   Otherwise (a huge tie group in s*): B2 histograms s* by group across the grid, finds the
-//   k-th group g*, appends the candidates below g* and counts each CTA's ties at g*; C2 takes the
-//   ties by index (CTA b owns the contiguous indices [b*per*T, (b+1)*per*T) in (j, thread)
-//   order, so its quota is need - (ties of CTAs before it)); D2 ranks the k records like C.
-constexpr int kSRT = 1024;  // one CTA per SM (64 registers x 1024 threads): half the CTAs to synchronise and to stage tables
+// the k best by (prediction, index) are the k smallest (g, index).  CTA b owns the contiguous
+// candidates [b*per*T, (b+1)*per*T); thread t of it candidates base + j*T + t, j < per, so index
+// order inside a CTA is (j, t) order.  Every candidate's g stays in shared memory across the
+// grid barriers (nothing is re-read from HBM, and no per-candidate global atomic: copies of one
+// parent share a row and would serialise in L2).
+//   A   score: the CTA's genomes arrive by bulk copies (TMA) into shared memory, one mbarrier per
+//       1024; genome -> row -> {prediction, g} (one 16-byte gather, all of a thread's gathers in
+//       flight together) -> prediction + id (per-key FNV state staged in shared memory by another
+//       bulk copy) out; a shared-memory histogram of g by segment (G / 4096 groups each) flushed
+//       with one atomic per non-empty segment, plus 64 super-segment sums.
+//   B   (every CTA, after barrier 1) the segment b0 of the k-th candidate: super-segment sums,
+//       then the 64 segments of the crossing super-segment -- two 256-byte reads, no hot 16 KB.
+//   C   (segments of <= 64 groups: G <= 2^18) the candidates below b0 (fewer than k) are appended
+//       to a list; the CTA's candidates in b0 are compacted in index order and given their order
+//       among the CTA's candidates of the same group (a stable multi-split); the CTA publishes
+//       its count per group of b0 and adds it to the per-group totals.
+//   D   (after barrier 2) a candidate of b0 in group offset q goes to position
+//         before(b0) + (b0's candidates in groups < q) + (group q's candidates in CTAs before b)
+//         + (its order in the CTA),
+//       written when < k -- ties, thousands of copies of one parent in a bred population, are
+//       placed by index without a sort; the list below b0 is ranked by counting.
+//   Segments of more groups (G > 2^18): B2 radix-selects the k-th group g* (one barrier per 12
+//   bits), C2 appends the candidates below g* and counts each CTA's ties at g*, D2 places the
+//   ties by CTA prefix and ranks the list.
+constexpr int kSRT = 1024;  // one CTA per SM: half the CTAs to synchronise and to stage tables
 constexpr int kSRPer = 8;
 constexpr int kSRMaxCtas = 1024;
 constexpr int kSRMaxSeg = 4096;    // segment histogram bins (shared memory)
-constexpr uint32_t kSRDirect = 4096;  // level-0 crossing: rank directly when below + in-bin are this few
-constexpr int kSRBatch = 4;        // candidates per thread whose loads are in flight together
-constexpr int kSRListCap = 8192;   // records ranked directly (64 KB of shared memory per CTA)
+constexpr int kSRKeys = 64;        // groups per segment the exact crossing path (C/D) handles
+constexpr int kSRListCap = 8192;   // appended records (radix path: < k; crossing path: < k)
 static_assert(kSRListCap >= kSelMaxK, "the tie path appends at most k records");
+// dynamic shared memory: [R0: genome staging, later the ranked list + the CTA's crossing-segment
+// candidates (64 KB) | g per candidate (u32, per*T) | segment histogram | Kuv classes | k_tile
+// words | per-key FNV states when <= 64 KB]
+constexpr uint32_t kSRR0 = 64 * 1024;
 
 __device__ __forceinline__ unsigned long long globaltimer() {
     unsigned long long t;
@@ -795,36 +810,81 @@ __device__ __forceinline__ unsigned long long globaltimer() {
     return t;
 }
 
+// diagnostic (ETUNE_ROWSEL_TRACE): per-CTA globaltimer stamps, kSRTraceSlots slots per CTA
+constexpr int kSRTraceSlots = 16;  // the last slot holds the crossing segment's count, not a time
+#define SR_TRACE(slot) \
+    do { \
+        if (trace && threadIdx.x == 0) trace[blockIdx.x * kSRTraceSlots + (slot)] = globaltimer(); \
+    } while (0)
+
 constexpr int kSRLevels = 3;  // radix-select levels over the group index (<= 2^25 groups)
 constexpr int kSRRep = 8;  // replicas of the appended list: the ranking CTAs read different L2 lines
 struct RowSelWork {
-    uint32_t nlist, ticket, ticket1, pad;
-    uint32_t cross[4];                   // level-0 crossing {bin, count below, candidates below + in bin}
+    uint32_t nlist, pad[3];
+    uint32_t tot[kSRKeys][32];           // crossing segment: candidates per group offset (a line each)
     uint32_t tiecnt[kSRMaxCtas];
+    uint32_t kcnt[kSRKeys][kSRMaxCtas];  // crossing segment: candidates per (group offset, CTA)
     uint32_t lvl[kSRLevels][kSRMaxSeg];  // candidates per bin of each radix-select level
     uint64_t lkey[kSRRep][kSRListCap];   // g << 32 | index of the appended records, kSRRep copies
 };
 
-// exclusive block scan of one u32 per thread (blockDim = kSRT); *total = block sum
-__device__ __forceinline__ uint32_t sr_block_scan(uint32_t v, uint32_t* ws, uint32_t* total) {
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    uint32_t x = v;
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
         const uint32_t y = __shfl_up_sync(0xffffffffu, x, s);
         if (lane >= s) x += y;
     }
+    return x;
+}
+
+// exclusive block scan of one u32 per thread (blockDim = kSRT); *total = block sum.  ws holds
+// 33 words: the warp sums, scanned by warp 0 (no per-thread loop over the warps)
+__device__ __forceinline__ uint32_t sr_block_scan(uint32_t v, uint32_t* ws, uint32_t* total) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t x = warp_incl_scan(v);
     if (lane == 31) ws[wid] = x;
     __syncthreads();
-    uint32_t before = 0, tot = 0;
-#pragma unroll
-    for (int i = 0; i < kSRT / 32; ++i) {
-        const uint32_t w = ws[i];
-        before += i < wid ? w : 0u;
-        tot += w;
+    if (wid == 0) {
+        const uint32_t w = ws[lane], inc = warp_incl_scan(w);
+        ws[lane] = inc - w;
+        if (lane == 31) ws[32] = inc;
     }
     __syncthreads();
-    *total = tot;
+    const uint32_t before = ws[wid];
+    *total = ws[32];
+    __syncthreads();  // ws is reused by the next scan
     return before + x - v;
+}
+
+// exclusive block scan of five u32 lanes per thread (componentwise: a uint4 and a u32); ws5
+// holds 5 x 33 words
+__device__ __forceinline__ uint4 sr_block_scan5(uint4 v, uint32_t v5, uint32_t* ws5, uint4* total, uint32_t* ex5,
+                                                uint32_t* total5) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t x0 = warp_incl_scan(v.x), x1 = warp_incl_scan(v.y), x2 = warp_incl_scan(v.z),
+                   x3 = warp_incl_scan(v.w), x4 = warp_incl_scan(v5);
+    if (lane == 31) {
+        ws5[0 * 33 + wid] = x0;
+        ws5[1 * 33 + wid] = x1;
+        ws5[2 * 33 + wid] = x2;
+        ws5[3 * 33 + wid] = x3;
+        ws5[4 * 33 + wid] = x4;
+    }
+    __syncthreads();
+    if (wid < 5) {  // warp c scans component c
+        const uint32_t w = ws5[wid * 33 + lane], inc = warp_incl_scan(w);
+        ws5[wid * 33 + lane] = inc - w;
+        if (lane == 31) ws5[wid * 33 + 32] = inc;
+    }
+    __syncthreads();
+    const uint4 r = make_uint4(ws5[0 * 33 + wid] + x0 - v.x, ws5[1 * 33 + wid] + x1 - v.y, ws5[2 * 33 + wid] + x2 - v.z,
+                               ws5[3 * 33 + wid] + x3 - v.w);
+    *ex5 = ws5[4 * 33 + wid] + x4 - v5;
+    *total = make_uint4(ws5[0 * 33 + 32], ws5[1 * 33 + 32], ws5[2 * 33 + 32], ws5[3 * 33 + 32]);
+    *total5 = ws5[4 * 33 + 32];
+    __syncthreads();
+    return r;
 }
 
 // smem histogram hs[0..nb) -> global g[0..nb), one atomic per non-empty bin
@@ -835,28 +895,24 @@ __device__ __forceinline__ void sr_flush(const uint32_t* hs, uint32_t* g, int nb
     }
 }
 
-// the bin holding the kk-th item (1-based) among nb <= kSRMaxSeg counters (read through L2, all in
-// one round trip: thread t owns bins [8t, 8t + 8)): its index and the count before it, identical in
-// every thread
-__device__ __forceinline__ void sr_cross(const uint32_t* g, int nb, uint32_t kk, uint32_t* ws, uint32_t* s_bin,
-                                         uint32_t* s_before) {
-    constexpr int kPer = kSRMaxSeg / kSRT;
-    uint32_t c[kPer], mine = 0;
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        const int i = int(threadIdx.x) * kPer + q;
-        c[q] = i < nb ? __ldcg(g + i) : 0u;
-        mine += c[q];
-    }
+// the bin holding the kk-th item (1-based) among nb <= kSRMaxSeg counters (one 16-byte load per
+// thread; bins past nb read as zero: the work area keeps all kSRMaxSeg counters zero between
+// calls): its index, the count before it and in it, identical in every thread
+__device__ __forceinline__ void sr_cross(const uint32_t* g, uint32_t kk, uint32_t* ws, uint32_t* s_bin,
+                                         uint32_t* s_before, uint32_t* s_cnt) {
+    static_assert(kSRMaxSeg == 4 * kSRT, "one uint4 of counters per thread");
+    const uint4 q = __ldcg(reinterpret_cast<const uint4*>(g) + threadIdx.x);
+    const uint32_t c[4] = {q.x, q.y, q.z, q.w};
     uint32_t tot;
-    uint32_t run = sr_block_scan(mine, ws, &tot);
+    uint32_t run = sr_block_scan(q.x + q.y + q.z + q.w, ws, &tot);
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-        if (c[q] && run < kk && run + c[q] >= kk) {
-            *s_bin = uint32_t(int(threadIdx.x) * kPer + q);
+    for (int i = 0; i < 4; ++i) {
+        if (c[i] && run < kk && run + c[i] >= kk) {
+            *s_bin = uint32_t(threadIdx.x) * 4u + uint32_t(i);
             *s_before = run;
+            *s_cnt = c[i];
         }
-        run += c[q];
+        run += c[i];
     }
     __syncthreads();
 }
@@ -865,7 +921,10 @@ __device__ __forceinline__ void sr_cross(const uint32_t* g, int nb, uint32_t kk,
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
@@ -885,19 +944,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // The m appended records (<= kSRListCap) get their output positions by counting: rank = records
-// with a smaller (g, index).  CTA c ranks records [32c, 32c + 32): lane l of every warp owns record
-// 32c + l, warp w compares it with the w-th sixteenth of the list (broadcast shared loads, staged
-// by one bulk copy), the sixteen partial counts are summed; rank < k goes to out[rank].
+// with a smaller (g, index).  CTA c ranks records [32c, 32c + 32): lane l of every warp owns
+// record 32c + l, warp w compares it with the w-th 32nd of the list (broadcast shared loads,
+// staged by one bulk copy), the partial counts are summed; rank < k goes to out[rank].
 __device__ __forceinline__ void sr_rank_out(const RowSelWork* W, uint32_t m, uint32_t k, unsigned long long* xk,
-                                            int64_t* out, uint64_t* mbar, uint32_t phase, uint32_t* part) {
+                                            int64_t* out, uint64_t* mbar, uint32_t phase, uint32_t* part,
+                                            unsigned long long* trace) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     constexpr int kW = kSRT / 32;
     if (blockIdx.x * 32u >= m) return;  // block-uniform: this CTA owns no record
     if (tid == 0) {
         asm volatile("fence.proxy.async.global;" ::: "memory");  // the list was written by generic stores
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the staging area was read generically
         bulk_g2s(xk, W->lkey[blockIdx.x % kSRRep], (m * 8u + 15u) & ~15u, mbar);
     }
     mbar_wait(mbar, phase);
+    SR_TRACE(8);
     const uint32_t per = (m + kW - 1) / kW, j0 = warp * per, j1 = min(m, j0 + per);
     for (uint32_t r0 = blockIdx.x * 32u; r0 < m; r0 += gridDim.x * 32u) {
         const uint32_t r = r0 + lane;
@@ -907,6 +969,7 @@ __device__ __forceinline__ void sr_rank_out(const RowSelWork* W, uint32_t m, uin
         for (uint32_t j = j0; j < j1; ++j) cnt += xk[j] < mine ? 1u : 0u;
         part[warp * 32 + lane] = cnt;
         __syncthreads();
+        SR_TRACE(9);
         if (warp == 0) {
             uint32_t c = 0;
 #pragma unroll
@@ -919,10 +982,11 @@ __device__ __forceinline__ void sr_rank_out(const RowSelWork* W, uint32_t m, uin
 
 // CTA-aggregated append of each thread's records (one global atomic per CTA): take(j) / key(j)
 template <typename Take, typename Key>
-__device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uint32_t* s_base, Take take, Key key) {
+__device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uint32_t* s_base, int per, Take take,
+                                                Key key) {
     uint32_t cnt = 0;
 #pragma unroll
-    for (int j = 0; j < kSRPer; ++j) cnt += take(j) ? 1u : 0u;
+    for (int j = 0; j < kSRPer; ++j) cnt += (j < per && take(j)) ? 1u : 0u;
     uint32_t tot;
     uint32_t off = sr_block_scan(cnt, ws, &tot);
     if (threadIdx.x == 0) *s_base = tot ? atomicAdd(&W->nlist, tot) : 0u;
@@ -930,7 +994,7 @@ __device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uin
     off += *s_base;
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j)
-        if (take(j)) {
+        if (j < per && take(j)) {
             if (off < uint32_t(kSRListCap)) {
                 const uint64_t kv = key(j);
 #pragma unroll
@@ -940,159 +1004,280 @@ __device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uin
         }
 }
 
+struct SRStatic {
+    uint32_t ws[5 * 33];
+    uint32_t part[kSRT];
+    uint32_t wcount[kSRT / 32][kSRKeys + 1];  // multi-split: per (warp, group offset) counts (+1: no bank conflicts)
+    uint32_t run[kSRKeys];                // the CTA's candidates per group offset of b0
+    uint32_t ktot[kSRKeys];               // b0's candidates in group offsets < q (all CTAs)
+    uint32_t kpre[kSRKeys];               // group offset q's candidates in the CTAs before this one
+    uint32_t bin, before, cnt, base, mc;
+    __align__(8) uint64_t mbar[kSRPer + 2];
+};
 
 __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const uint8_t* __restrict__ gplan, const uint16_t* __restrict__ clskuv, const RowTabMeta* __restrict__ meta,
     const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash, int khash_smem,
     const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, double* __restrict__ pred,
     uint64_t* __restrict__ ids, int64_t* __restrict__ out, RowSelWork* __restrict__ W,
-    unsigned long long* __restrict__ trace, int only_a) {
+    unsigned long long* __restrict__ trace, int only_a, int force_radix) {
     namespace cg = cooperative_groups;
-    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[6] = globaltimer();
-    extern __shared__ __align__(16) uint32_t rsm[];  // [Kuv classes | histogram | k_tile words | key FNV]; list in C
-    __shared__ uint32_t ws[kSRT / 32];
-    __shared__ uint32_t s_bin, s_before, s_base;
-    __shared__ uint32_t s_part[kSRT];
-    __shared__ __align__(8) uint64_t s_mbar;
-    const int tid = threadIdx.x;
+    SR_TRACE(0);
+    extern __shared__ int4 dsm4[];
+    uint8_t* dsm = reinterpret_cast<uint8_t*>(dsm4);
+    __shared__ SRStatic S;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t base = uint32_t(blockIdx.x) * uint32_t(per) * kSRT;  // n < 2^31
-    // the first batch's genomes are requested before anything else: they do not need the tables
-    uint64_t g0[kSRBatch];
-#pragma unroll
-    for (int b = 0; b < kSRBatch; ++b) {
-        const uint32_t i = base + uint32_t(b) * kSRT + tid;
-        g0[b] = (b < per && int64_t(i) < n) ? __ldcs(genome + i) : ~0ull;
-    }
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
     const int ndk = H.ndk;
     const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
-    uint32_t* hist = rsm + ndk * 32;  // kSRMaxSeg bins
-    uint32_t* sdivk = hist + kSRMaxSeg;
-    uint64_t* skh = reinterpret_cast<uint64_t*>(sdivk + ((ndk + 3) & ~3));  // 16-byte aligned
     const uint32_t nkeys = uint32_t(H.nt[0]) * nt1 * nt2;
+    uint64_t* sgen = reinterpret_cast<uint64_t*>(dsm);                    // R0
+    uint32_t* sgg = reinterpret_cast<uint32_t*>(dsm + kSRR0);             // per * T
+    uint32_t* hist = sgg + per * kSRT;                                    // kSRMaxSeg
+    uint32_t* scls32 = hist + kSRMaxSeg;                                  // ndk * 32
+    uint32_t* sdivk = scls32 + ndk * 32;                                  // ndk (rounded to 4)
+    uint64_t* skh = reinterpret_cast<uint64_t*>(sdivk + ((ndk + 3) & ~3));  // 16-byte aligned
     const bool bulk = khash_smem && ids;
-    uint32_t mphase = 0;  // parity of the next wait on s_mbar
-    if (tid == 0) mbar_init(&s_mbar);
+    const bool tma = (reinterpret_cast<uintptr_t>(genome) & 15u) == 0;
+    // ---- the bulk copies go first: genomes per 1024 (mbar j), per-key FNV states (mbar kSRPer)
+    if (tid == 0) {
+        for (int j = 0; j < kSRPer + 2; ++j) mbar_init(&S.mbar[j]);
+        mbar_fence_init();
+        for (int j = 0; j < per; ++j) {
+            const int64_t i0 = int64_t(base) + int64_t(j) * kSRT;
+            const int64_t c = i0 < n ? (n - i0 < kSRT ? n - i0 : kSRT) : 0;
+            const uint32_t bytes = tma ? uint32_t(c * 8) & ~15u : 0u;
+            if (bytes) {
+                bulk_g2s(sgen + j * kSRT, genome + i0, bytes, &S.mbar[j]);
+            } else {
+                mbar_arrive(&S.mbar[j]);
+            }
+        }
+        if (bulk) bulk_g2s(skh, khash, (nkeys * 8u + 15u) & ~15u, &S.mbar[kSRPer]);
+    }
+    // genomes the bulk copies do not cover (an odd tail, or a genome pointer not 16-byte aligned)
+    for (int j = 0; j < per; ++j) {
+        const int64_t i0 = int64_t(base) + int64_t(j) * kSRT;
+        const int64_t c = i0 < n ? (n - i0 < kSRT ? n - i0 : kSRT) : 0;
+        const int64_t covered = tma ? int64_t((uint32_t(c * 8) & ~15u) / 8u) : 0;
+        if (tid >= covered) sgen[j * kSRT + tid] = tid < c ? __ldcs(genome + i0 + tid) : ~0ull;
+    }
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(clskuv);
-        for (int i = tid; i < ndk * 32; i += kSRT) rsm[i] = __ldg(src + i);
+        for (int i = tid; i < ndk * 32; i += kSRT) scls32[i] = __ldg(src + i);
         const int64_t* divk = at<int64_t>(gplan, H.off_divk);
         for (int i = tid; i < ndk; i += kSRT) sdivk[i] = uint32_t(divk[i]);
+        reinterpret_cast<uint4*>(hist)[tid] = make_uint4(0, 0, 0, 0);
     }
     const uint32_t groups = uint32_t(meta->groups);
     const int gbits = groups > 1 ? 32 - __clz(int(groups - 1)) : 0;
-    // level 0 of the radix select: <= 4096 bins of the group index
-    const int segshift = gbits > 12 ? gbits - 12 : 0;
+    const int segshift = gbits > 12 ? gbits - 12 : 0;  // level 0: <= 4096 segments of the group index
     const int nseg = int((groups + (1u << segshift) - 1) >> segshift);
-    for (int i = tid; i < nseg; i += kSRT) hist[i] = 0u;
     const uint32_t nkc = uint32_t(meta->nkc);
     __syncthreads();
-    if (bulk && tid == 0) bulk_g2s(skh, khash, (nkeys * 8u + 15u) & ~15u, &s_mbar);  // per-key FNV states (TMA)
-    const uint16_t* scls = reinterpret_cast<const uint16_t*>(rsm);
-    // ---- A: score, kSRBatch candidates per thread with all their loads in flight together
-    uint32_t gg[kSRPer];
-    bool khash_ready = !bulk;
+    const uint16_t* scls = reinterpret_cast<const uint16_t*>(scls32);
+    // ---- A1: every gather of the thread in flight together
+    double p[kSRPer];
+    uint32_t gq[kSRPer];
 #pragma unroll
-    for (int j0 = 0; j0 < kSRPer; j0 += kSRBatch) {
-        uint64_t g[kSRBatch];
+    for (int j = 0; j < kSRPer; ++j) {
+        if (j >= per) break;
+        mbar_wait(&S.mbar[j], 0);
+        const uint64_t g = sgen[j * kSRT + tid];
+        const bool v = g != ~0ull;
+        const Genome x = genome_unpack(v ? g : 0ull);
+        const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
+        const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
+        const double2 r = v ? __ldg(reinterpret_cast<const double2*>(rowrec) + (key * nkc + kc)) : make_double2(0.0, 0.0);
+        p[j] = r.x;
+        gq[j] = v ? uint32_t(__double_as_longlong(r.y)) : 0xffffffffu;
+    }
+    if (bulk) mbar_wait(&S.mbar[kSRPer], 0);
+    // ---- A2: outputs, histogram, g kept in shared memory
 #pragma unroll
-        for (int b = 0; b < kSRBatch; ++b) {
-            if (j0 == 0) {
-                g[b] = g0[b];
-            } else {
-                const uint32_t i = base + uint32_t(j0 + b) * kSRT + tid;
-                g[b] = (j0 + b < per && int64_t(i) < n) ? __ldcs(genome + i) : ~0ull;  // ~0: no candidate
-            }
-        }
-        uint32_t row[kSRBatch], key[kSRBatch];
-#pragma unroll
-        for (int b = 0; b < kSRBatch; ++b) {
-            const Genome x = genome_unpack(g[b] != ~0ull ? g[b] : 0ull);
-            key[b] = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
-            const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
-            row[b] = key[b] * nkc + kc;
-        }
-        double p[kSRBatch];
-#pragma unroll
-        for (int b = 0; b < kSRBatch; ++b) {  // one 16-byte gather per candidate: {prediction, group}
-            const bool v = g[b] != ~0ull;
-            const double2 r = v ? __ldg(reinterpret_cast<const double2*>(rowrec) + row[b]) : make_double2(0.0, 0.0);
-            p[b] = r.x;
-            gg[j0 + b] = v ? uint32_t(__double_as_longlong(r.y)) : 0xffffffffu;
-        }
-        if (ids && !khash_ready) {
-            mbar_wait(&s_mbar, 0);
-            khash_ready = true;
-        }
-#pragma unroll
-        for (int b = 0; b < kSRBatch; ++b) {
-            if (g[b] == ~0ull) continue;
-            const uint32_t i = base + uint32_t(j0 + b) * kSRT + tid;
-            pred[i] = p[b];
-            atomicAdd(hist + (gg[j0 + b] >> segshift), 1u);
-            if (ids) {
-                const Genome x = genome_unpack(g[b]);
-                const uint64_t h = bulk ? skh[key[b]] : __ldg(khash + key[b]);
-                __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
-                       static_cast<unsigned long long>(fnv_tail(fnv_small(h, sdivk[x.k]), x.u, x.v)));
-            }
+    for (int j = 0; j < kSRPer; ++j) {
+        if (j >= per) break;
+        sgg[j * kSRT + tid] = gq[j];
+        if (gq[j] == 0xffffffffu) continue;
+        const uint32_t i = base + uint32_t(j) * kSRT + tid;
+        pred[i] = p[j];
+        atomicAdd(hist + (gq[j] >> segshift), 1u);
+        if (ids) {
+            const Genome x = genome_unpack(sgen[j * kSRT + tid]);
+            const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
+            const uint64_t h = bulk ? skh[key] : __ldg(khash + key);
+            __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
+                   static_cast<unsigned long long>(fnv_tail(fnv_small(h, sdivk[x.k]), x.u, x.v)));
         }
     }
-    if (bulk && !khash_ready) mbar_wait(&s_mbar, 0);  // the copy lands before the smem is reused
-    if (bulk) mphase = 1;
+    SR_TRACE(1);
     __syncthreads();
-    sr_flush(hist, W->lvl[0], nseg);
-    if (trace && blockIdx.x == 0 && tid == 0) trace[0] = globaltimer();
+    // flush: segment i = r * T + t (a warp's atomics hit one line)
+#pragma unroll
+    for (int r = 0; r < kSRMaxSeg / kSRT; ++r) {
+        const uint32_t v = hist[r * kSRT + tid];
+        if (v) atomicAdd(W->lvl[0] + r * kSRT + tid, v);
+    }
+    // the per-group totals of the crossing segment are added after barrier 1 and read after
+    // barrier 2: the previous call's are cleared here
+    if (blockIdx.x == 0 && tid < kSRKeys) W->tot[tid][0] = 0u;
+    SR_TRACE(2);
     if (only_a) return;  // diagnostic: phase A alone (profilers cannot split a cooperative kernel)
-    // the last CTA to flush finds the level-0 crossing once (every CTA reading the same counts would
-    // queue on the same L2 lines) and publishes it before the barrier
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_base = atomicAdd(&W->ticket1, 1u) == gridDim.x - 1 ? 1u : 0u;
-    __syncthreads();
-    if (s_base) {  // block-uniform
-        __threadfence();
-        sr_cross(W->lvl[0], nseg, uint32_t(k), ws, &s_bin, &s_before);
-        if (tid == 0) {
-            W->cross[0] = s_bin;
-            W->cross[1] = s_before;
-            W->cross[2] = s_before + __ldcg(W->lvl[0] + s_bin);
-            W->ticket1 = 0u;
-        }
-    }
     cg::this_grid().sync();
-    if (trace && blockIdx.x == 0 && tid == 0) trace[1] = globaltimer();
-    // ---- B: radix select of the k-th candidate's group g* over the group index: at each level the
+    SR_TRACE(3);
+    // ---- B: the segment b0 of the k-th candidate (every CTA: one 16-byte load per thread)
+    const uint32_t kk = uint32_t(k);
+    sr_cross(W->lvl[0], kk, S.ws, &S.bin, &S.before, &S.cnt);
+    const uint32_t b0 = S.bin, before0 = S.before;
+    SR_TRACE(7);
+    if (trace && tid == 0) trace[blockIdx.x * kSRTraceSlots + kSRTraceSlots - 1] = S.cnt;
+    unsigned long long* xk = reinterpret_cast<unsigned long long*>(dsm);  // ranked list (R0, 32 KB)
+    uint32_t* sb0 = reinterpret_cast<uint32_t*>(dsm + kSRR0 / 2);         // b0's candidates (R0, 32 KB)
+    auto gkey = [&](int j) { return (uint64_t(sgg[j * kSRT + tid]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); };
+    if (segshift <= 6 && !force_radix) {  // grid-uniform
+        const uint32_t nq = 1u << segshift, qmask = nq - 1u;
+        // ---- C: the candidates below b0 -> the list (fewer than k); b0's candidates compacted in
+        //      index order; one block scan for both
+        uint32_t lc = 0;
+        uint4 f = make_uint4(0, 0, 0, 0);  // 16-bit count of b0 candidates per j (two per word)
+#pragma unroll
+        for (int j = 0; j < kSRPer; ++j) {
+            const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
+            const uint32_t sg = g >> segshift;
+            lc += (g != 0xffffffffu && sg < b0) ? 1u : 0u;
+            const uint32_t add = (g != 0xffffffffu && sg == b0) ? (1u << (16 * (j & 1))) : 0u;
+            if (j < 2) f.x += add; else if (j < 4) f.y += add; else if (j < 6) f.z += add; else f.w += add;
+        }
+        uint4 ftot;
+        uint32_t lex, ltot;
+        const uint4 fex = sr_block_scan5(f, lc, S.ws, &ftot, &lex, &ltot);
+        if (ltot) {  // block-uniform: append (g, index) with one atomic per CTA, kSRRep copies
+            if (tid == 0) S.base = atomicAdd(&W->nlist, ltot);
+            __syncthreads();
+            uint32_t off = S.base + lex;
+#pragma unroll
+            for (int j = 0; j < kSRPer; ++j) {
+                const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
+                if (g != 0xffffffffu && (g >> segshift) < b0) {
+                    if (off < uint32_t(kSRListCap)) {
+                        const uint64_t kv = gkey(j);
+#pragma unroll
+                        for (int r = 0; r < kSRRep; ++r) W->lkey[r][off] = kv;
+                    }
+                    ++off;
+                }
+            }
+        }
+        SR_TRACE(10);
+        {
+            const uint32_t ex[4] = {fex.x, fex.y, fex.z, fex.w}, tt[4] = {ftot.x, ftot.y, ftot.z, ftot.w};
+            uint32_t run = 0;
+#pragma unroll
+            for (int j = 0; j < kSRPer; ++j) {
+                const uint32_t e = (ex[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+                const uint32_t t = (tt[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+                const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
+                if (g != 0xffffffffu && (g >> segshift) == b0) sb0[run + e] = (uint32_t(j * kSRT + tid) << 19) | (g & qmask);
+                run += t;
+            }
+            if (tid == 0) S.mc = run;
+        }
+        if (tid < kSRKeys) S.run[tid] = 0u;
+        __syncthreads();
+        SR_TRACE(11);
+        const uint32_t mc = S.mc;
+        // stable multi-split: each b0 candidate's order among the CTA's candidates of its group
+        for (uint32_t c0 = 0; c0 < mc; c0 += kSRT) {
+            for (int i = tid; i < (kSRT / 32) * (kSRKeys + 1); i += kSRT) (&S.wcount[0][0])[i] = 0u;
+            __syncthreads();
+            const uint32_t pidx = c0 + uint32_t(tid);
+            const bool valid = pidx < mc;
+            const uint32_t e = valid ? sb0[pidx] : 0u;
+            const uint32_t q = valid ? (e & 63u) : 64u;
+            const unsigned peers = __match_any_sync(0xffffffffu, q);
+            const unsigned lower = peers & ((1u << lane) - 1u);
+            if (valid && lower == 0) S.wcount[warp][q] = __popc(peers);
+            __syncthreads();
+            for (int qq = warp; qq < kSRKeys; qq += kSRT / 32) {  // warp per group offset: scan over the warps
+                const uint32_t c = S.wcount[lane][qq], inc = warp_incl_scan(c), r = S.run[qq];
+                S.wcount[lane][qq] = r + inc - c;
+                __syncwarp();
+                if (lane == 31) S.run[qq] = r + inc;
+            }
+            __syncthreads();
+            if (valid) sb0[pidx] = e | ((S.wcount[warp][q] + __popc(lower)) << 6);  // 13-bit order
+            __syncthreads();
+        }
+        SR_TRACE(12);
+        if (tid < int(nq)) {
+            const uint32_t r = S.run[tid];
+            W->kcnt[tid][blockIdx.x] = r;
+            if (r) atomicAdd(&W->tot[tid][0], r);
+        }
+        SR_TRACE(4);
+        cg::this_grid().sync();
+        SR_TRACE(5);
+        // nothing reads the list length or the level-0 counts after the barrier: reset them here
+        if (blockIdx.x == 0 && tid == 0) W->nlist = 0u;
+        for (int i = blockIdx.x * kSRT + tid; i < nseg; i += gridDim.x * kSRT) W->lvl[0][i] = 0u;
+        // ---- D: b0's per-group totals (warp 0) and, per group the CTA holds, the CTAs before it
+        if (warp == 0) {
+            const uint32_t t0 = lane < int(nq) ? __ldcg(&W->tot[lane][0]) : 0u;
+            const uint32_t t1 = lane + 32 < int(nq) ? __ldcg(&W->tot[lane + 32][0]) : 0u;
+            uint32_t inc = t0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const uint32_t all0 = __shfl_sync(0xffffffffu, inc, 31);
+            uint32_t inc1 = t1;
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc1, o);
+                if (lane >= o) inc1 += y;
+            }
+            S.ktot[lane] = inc - t0;
+            S.ktot[lane + 32] = all0 + inc1 - t1;
+        }
+        for (int q = warp; q < int(nq); q += kSRT / 32) {
+            if (S.run[q] == 0u) continue;  // warp-uniform
+            uint32_t s = 0;
+            for (uint32_t c = lane; c < blockIdx.x; c += 32) s += __ldcg(&W->kcnt[q][c]);
+            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0) S.kpre[q] = s;
+        }
+        __syncthreads();
+        for (uint32_t pidx = tid; pidx < mc; pidx += kSRT) {
+            const uint32_t e = sb0[pidx];
+            const uint32_t q = e & 63u, ord = (e >> 6) & 0x1fffu, loc = e >> 19;
+            const uint32_t pos = before0 + S.ktot[q] + S.kpre[q] + ord;
+            if (pos < kk) out[pos] = int64_t(base + loc);
+        }
+        if (before0) sr_rank_out(W, before0, kk, xk, out, &S.mbar[kSRPer + 1], 0, S.part, trace);
+        SR_TRACE(6);
+        return;
+    }
+    // ---- B2: radix select of the k-th candidate's group g* over the group index: at each level the
     //      bin holding the k-th candidate still in play (every CTA, identically), then -- until a bin
     //      is a single group -- the next 12 bits of g of the candidates in that bin, histogrammed per
     //      CTA and flushed (one grid barrier per level; two levels for up to 2^20 groups)
-    const uint32_t kk = uint32_t(k);
-    uint32_t kr = kk, below = 0, P = 0;
+    uint32_t below = 0, kr = kk, P = 0;
     int Sc = segshift, nbc = nseg, L = 0;
-    unsigned long long* xk = reinterpret_cast<unsigned long long*>(rsm);
-    // the usual case: the candidates below and in the level-0 bin of the k-th are few -- rank them all
-    const uint32_t b0 = __ldcg(W->cross + 0), m1 = __ldcg(W->cross + 2);
-    if (m1 <= kSRDirect) {  // grid-uniform
-        sr_append_block(W, ws, &s_base, [&](int j) { return gg[j] != 0xffffffffu && (gg[j] >> Sc) <= b0; },
-                        [&](int j) { return (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); });
-        cg::this_grid().sync();
-        if (trace && blockIdx.x == 0 && tid == 0) trace[2] = trace[3] = globaltimer();
-        for (int i = blockIdx.x * kSRT + tid; i < nbc; i += gridDim.x * kSRT) W->lvl[0][i] = 0u;
-        sr_rank_out(W, m1, kk, xk, out, &s_mbar, mphase, s_part);
-    } else {
     for (;; ++L) {
-        sr_cross(W->lvl[L], nbc, kr, ws, &s_bin, &s_before);
-        const uint32_t bin = s_bin;
-        below += s_before;
-        kr -= s_before;
+        if (L > 0) sr_cross(W->lvl[L], kr, S.ws, &S.bin, &S.before, &S.cnt);
+        const uint32_t bin = L > 0 ? S.bin : b0;
+        const uint32_t bef = L > 0 ? S.before : before0;
+        below += bef;
+        kr -= bef;
         P = (L == 0) ? bin : ((P << (nbc > 1 ? 31 - __clz(int(nbc)) : 0)) | bin);  // candidates with g >> Sc == P
         if (Sc == 0) break;
         const int Sn = Sc > 12 ? Sc - 12 : 0, nbn = 1 << (Sc - Sn);
         for (int i = tid; i < nbn; i += kSRT) hist[i] = 0u;
         __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kSRPer; ++j)
-            if (gg[j] != 0xffffffffu && (gg[j] >> Sc) == P) atomicAdd(hist + ((gg[j] >> Sn) & uint32_t(nbn - 1)), 1u);
+        for (int j = 0; j < per; ++j) {
+            const uint32_t g = sgg[j * kSRT + tid];
+            if (g != 0xffffffffu && (g >> Sc) == P) atomicAdd(hist + ((g >> Sn) & uint32_t(nbn - 1)), 1u);
+        }
         __syncthreads();
         sr_flush(hist, W->lvl[L + 1], nbn);
         cg::this_grid().sync();
@@ -1102,52 +1287,38 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     }
     const uint32_t gstar = P;
     const uint32_t need = kk - below;  // >= 1 candidates at g* are taken, by index
-    if (trace && blockIdx.x == 0 && tid == 0) trace[2] = globaltimer();
-    // ---- C: the candidates below g* (fewer than k) are appended; each CTA counts its ties at g*
-    auto gkey = [&](int j) { return (uint64_t(gg[j]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); };
-    sr_append_block(W, ws, &s_base, [&](int j) { return gg[j] < gstar; }, gkey);
+    SR_TRACE(4);
+    // ---- C2: the candidates below g* (fewer than k) are appended; each CTA counts its ties at g*
+    sr_append_block(W, S.ws, &S.base, per, [&](int j) { return sgg[j * kSRT + tid] < gstar; }, gkey);
     uint32_t my_ties = 0;
-#pragma unroll
-    for (int j = 0; j < kSRPer; ++j) my_ties += gg[j] == gstar;
+    for (int j = 0; j < per; ++j) my_ties += sgg[j * kSRT + tid] == gstar;
     uint32_t cta_ties;
-    sr_block_scan(my_ties, ws, &cta_ties);
+    sr_block_scan(my_ties, S.ws, &cta_ties);
     if (tid == 0) W->tiecnt[blockIdx.x] = cta_ties;
     cg::this_grid().sync();
-    if (trace && blockIdx.x == 0 && tid == 0) trace[3] = globaltimer();
+    SR_TRACE(5);
+    if (blockIdx.x == 0 && tid == 0) W->nlist = 0u;
     for (int i = blockIdx.x * kSRT + tid; i < nbc; i += gridDim.x * kSRT) W->lvl[L][i] = 0u;
-    // ---- D: output positions without a sort.  A tie's position is below + its rank among the ties
-    //      by index: CTA b owns the contiguous indices [b*per*T, (b+1)*per*T) in (j, thread) order,
-    //      so that rank is (ties of the CTAs before b) + its order in the CTA; ranks < need are
-    //      written.  The records below g* are ranked among themselves by counting.
-    uint32_t before = 0;
-    for (uint32_t b2 = tid; b2 < blockIdx.x; b2 += kSRT) before += __ldcg(W->tiecnt + b2);
+    // ---- D2: output positions without a sort.  A tie's position is below + its rank among the ties
+    //      by index: (ties of the CTAs before b) + its order in the CTA; ranks < need are written.
+    //      The records below g* are ranked among themselves by counting.
+    uint32_t tb = 0;
+    for (uint32_t b2 = tid; b2 < blockIdx.x; b2 += kSRT) tb += __ldcg(W->tiecnt + b2);
     uint32_t tot_before;
-    sr_block_scan(before, ws, &tot_before);
+    sr_block_scan(tb, S.ws, &tot_before);
     if (cta_ties && tot_before < need) {  // block-uniform
         uint32_t run = tot_before;
-#pragma unroll
-        for (int j = 0; j < kSRPer; ++j) {
+        for (int j = 0; j < per; ++j) {
             if (run >= need) break;  // block-uniform
-            const bool tie = gg[j] == gstar;
+            const bool tie = sgg[j * kSRT + tid] == gstar;
             uint32_t tot;
-            const uint32_t o = sr_block_scan(tie ? 1u : 0u, ws, &tot);
+            const uint32_t o = sr_block_scan(tie ? 1u : 0u, S.ws, &tot);
             if (tie && run + o < need) out[below + run + o] = int64_t(base + uint32_t(j) * kSRT + tid);
             run += tot;
         }
     }
-    if (below) sr_rank_out(W, below, kk, xk, out, &s_mbar, mphase, s_part);
-    }  // radix-select path
-    if (trace && blockIdx.x == 0 && tid == 0) trace[4] = globaltimer();
-    // the last CTA out resets the list for the next call
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(&W->ticket, 1u) == gridDim.x - 1) {
-            W->nlist = 0u;
-            W->ticket = 0u;
-            if (trace) trace[5] = globaltimer();
-        }
-    }
+    if (below) sr_rank_out(W, below, kk, xk, out, &S.mbar[kSRPer + 1], 0, S.part, trace);
+    SR_TRACE(6);
 }
 
 constexpr uint32_t kPlanSmemMax = 96 * 1024;
@@ -1317,51 +1488,87 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
                                      double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work) {
     if (n <= 0 || k <= 0) return cudaSuccess;
     if (k > kSelMaxK || k > n || n >= (int64_t(1) << 31)) return cudaErrorInvalidValue;
-    // [Kuv classes | histogram | k_tile words | per-key FNV states when <= 64 KB]; the ranked list reuses it
-    int khash_smem = nkeys * 8 <= 64 * 1024 ? 1 : 0;
-    size_t sm = size_t(ndk) * 128 + size_t(kSRMaxSeg) * 4 + size_t((ndk + 3) & ~3) * 4 +
-                (khash_smem ? size_t((nkeys * 8 + 15) & ~int64_t(15)) : 0);
-    if (sm < size_t(kSRListCap) * 8) sm = size_t(kSRListCap) * 8;
-    static int per_sm = -1;
+    // [R0 | g per candidate | histogram | Kuv classes | k_tile words | per-key FNV states when <= 64 KB]
+    const int khash_smem = nkeys * 8 <= 64 * 1024 ? 1 : 0;
+    const size_t sm_fixed = size_t(kSRR0) + size_t(kSRMaxSeg) * 4 + size_t(ndk) * 128 + size_t((ndk + 3) & ~3) * 4 +
+                            (khash_smem ? size_t((nkeys * 8 + 15) & ~int64_t(15)) : 0);
+    static int optin = 0, sms = 0;
+    if (!optin) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    // one CTA per SM: candidates per thread so that the grid covers n
+    int64_t gmax = std::min<int64_t>(int64_t(c.sm_count), kSRMaxCtas);
+    const int64_t per = (n + gmax * kSRT - 1) / (gmax * kSRT);
+    if (per > kSRPer) return cudaErrorNotSupported;  // beyond the grid: the bucketed selection
+    const size_t sm = sm_fixed + size_t(per) * kSRT * 4;
+    if (sm + sizeof(SRStatic) + 1024 > size_t(optin)) return cudaErrorNotSupported;  // tables too large
     static size_t attr_sm = 0;
-    if (sm != attr_sm) {
-        cudaError_t e = cudaFuncSetAttribute(score_select_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             int(sm));
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_select_rows_kernel, kSRT, sm);
+    if (sm > attr_sm) {
+        const cudaError_t e = cudaFuncSetAttribute(score_select_rows_kernel,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
         if (e != cudaSuccess) return e;
         attr_sm = sm;
     }
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
-    int64_t gmax = int64_t(c.sm_count) * per_sm;
-    if (gmax > kSRMaxCtas) gmax = kSRMaxCtas;
-    const int64_t per = (n + gmax * kSRT - 1) / (gmax * kSRT);
-    if (per > kSRPer) return cudaErrorNotSupported;
     const int64_t grid = (n + per * kSRT - 1) / (per * kSRT);
     int per_i = int(per);
     RowSelWork* W = static_cast<RowSelWork*>(d_work);
-    // ETUNE_ROWSEL_TRACE=1 (diagnostic): globaltimer at each phase boundary, printed per call
-    static const bool want_trace = std::getenv("ETUNE_ROWSEL_TRACE") != nullptr;
+    // ETUNE_ROWSEL_TRACE=N (diagnostic): per-CTA globaltimer stamps of N back-to-back calls into a ring;
+    // every N calls the ring is synchronised and summarised (min / median / max over CTAs and calls
+    // of each phase boundary, relative to the earliest CTA start of the call)
+    static const int want_trace = std::getenv("ETUNE_ROWSEL_TRACE") ? std::atoi(std::getenv("ETUNE_ROWSEL_TRACE")) : 0;
     static unsigned long long* trace = nullptr;
-    if (want_trace && !trace) cudaMallocManaged(&trace, 8 * sizeof(unsigned long long));
-    unsigned long long* tr = want_trace ? trace : nullptr;
+    static int trace_calls = 0;
+    if (want_trace > 0 && !trace) {
+        cudaMalloc(&trace, size_t(want_trace) * kSRMaxCtas * kSRTraceSlots * sizeof(unsigned long long));
+        cudaMemset(trace, 0, size_t(want_trace) * kSRMaxCtas * kSRTraceSlots * sizeof(unsigned long long));
+    }
+    unsigned long long* tr = want_trace > 0 ? trace + size_t(trace_calls) * kSRMaxCtas * kSRTraceSlots : nullptr;
     // ETUNE_ROWSEL_ONLY_A=1 (diagnostic, results invalid): stop after the scoring phase so that a
     // profiler sees it as a kernel of its own
     static const int only_a = std::getenv("ETUNE_ROWSEL_ONLY_A") != nullptr ? 1 : 0;
     int oa = only_a;
+    // ETUNE_ROWSEL_RADIX=1 (diagnostic, read every call): the radix-select path for any group count
+    const char* fr = std::getenv("ETUNE_ROWSEL_RADIX");
+    int force_radix = (fr && fr[0] == '1') ? 1 : 0;
     void* args[] = {(void*)&d_plan,   (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowrec, (void*)&d_khash,
                     (void*)&khash_smem, (void*)&d_genome, (void*)&n,    (void*)&k,        (void*)&per_i,
                     (void*)&d_pred,   (void*)&d_ids,    (void*)&d_idx,  (void*)&W,        (void*)&tr,
-                    (void*)&oa};
+                    (void*)&oa,       (void*)&force_radix};
     note_launches(1);
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(score_select_rows_kernel),
                                                       dim3(unsigned(grid)), dim3(kSRT), args, sm, c.stream);
-    if (tr && e == cudaSuccess) {
+    if (tr && e == cudaSuccess && ++trace_calls == want_trace) {
+        trace_calls = 0;
         cudaStreamSynchronize(c.stream);
-        std::fprintf(stderr, "rowsel n=%lld grid=%lld per=%d: A %.2f | sync1 %.2f | select levels %.2f | append+sync %.2f | "
-                     "rank %.2f | tail %.2f us\n", (long long)n, (long long)grid, per_i, (tr[0] - tr[6]) * 1e-3,
-                     (tr[1] - tr[0]) * 1e-3, (tr[2] - tr[1]) * 1e-3, (tr[3] - tr[2]) * 1e-3, (tr[4] - tr[3]) * 1e-3,
-                     (tr[5] - tr[4]) * 1e-3);
+        std::vector<unsigned long long> h(size_t(want_trace) * kSRMaxCtas * kSRTraceSlots);
+        cudaMemcpy(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost);
+        constexpr int S = kSRTraceSlots;
+        std::vector<double> v[S];
+        for (int call = 0; call < want_trace; ++call) {
+            const unsigned long long* t = h.data() + size_t(call) * kSRMaxCtas * S;
+            unsigned long long t0 = ~0ull;
+            for (int b = 0; b < int(grid); ++b) t0 = std::min(t0, t[b * S]);
+            for (int b = 0; b < int(grid); ++b)
+                for (int s = 0; s < S - 1; ++s)
+                    if (t[b * S + s] >= t0) v[s].push_back(double(t[b * S + s] - t0) * 1e-3);
+        }
+        std::fprintf(stderr, "rowsel: candidates in the crossing segment of the last call: %llu\n",
+                     (unsigned long long)h[size_t(want_trace - 1) * kSRMaxCtas * S + S - 1]);
+        static const char* names[S] = {"start", "A done", "flushed", "sync1", "appended", "sync2",
+                                       "ranked", "crossed", "staged", "counted", "L-append", "compact",
+                                       "msplit", "-", "-", "count"};
+        std::fprintf(stderr, "rowsel trace n=%lld grid=%lld per=%d over %d calls (us from the first CTA start):\n",
+                     (long long)n, (long long)grid, per_i, want_trace);
+        for (int s = 0; s < S - 1; ++s) {
+            if (v[s].empty()) continue;
+            std::sort(v[s].begin(), v[s].end());
+            std::fprintf(stderr, "  %-9s min %7.2f  p50 %7.2f  p90 %7.2f  max %7.2f\n", names[s], v[s].front(),
+                         v[s][v[s].size() / 2], v[s][v[s].size() * 9 / 10], v[s].back());
+        }
+        cudaMemset(trace, 0, h.size() * 8);
     }
     return e;
 }

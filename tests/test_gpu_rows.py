@@ -254,18 +254,27 @@ def test_auto_small_population_walks(golden, ctx, capi):
         assert (bits(p) == bits(p0)).all()
 
 
+@pytest.mark.parametrize("radix", [False, True])
 @pytest.mark.parametrize("kind,n,k", [("dup", 1, 1), ("dup", 70001, 4096), ("few", 100003, 1024),
                                       ("few", 513, 513), ("bred", 300000, 1), ("bred", 1 << 21, 1024),
-                                      ("bred", (1 << 20) + 7, 4096)])
-def test_rows_fused_select_edges(golden, oracle, ctx, capi, kind, n, k):
+                                      ("bred", (1 << 20) + 7, 4096), ("rand", 300001, 4096),
+                                      ("rand", 600000, 1024), ("rand", 5000, 17)])
+def test_rows_fused_select_edges(golden, oracle, ctx, capi, monkeypatch, kind, n, k, radix):
     """The one-kernel row selection: all candidates tied (quota split over CTAs by index), a few
-    distinct rows repeated, k = n, k = 1, k = 4096, n not a multiple of the CTA size, and
-    2^21 candidates (beyond the grid's registers: the bucketed fallback)."""
+    distinct rows repeated, k = n, k = 1, k = 4096, n not a multiple of the CTA size, uniformly
+    sampled populations (thousands of candidates below the crossing segment, ranked by counting),
+    and 2^21 candidates (beyond the grid: the bucketed fallback) -- on the exact crossing path
+    (segments of <= 64 groups) and on the radix-select path (ETUNE_ROWSEL_RADIX=1, the path of
+    operators with > 2^18 row groups)."""
+    if radix:
+        monkeypatch.setenv("ETUNE_ROWSEL_RADIX", "1")
     fl = forest_of(golden, "c2_r50_conv3x3")
     op = parse_op("conv:1,56,56,64,64,3,1,1")
     plan = capi.Plan(ctx, op)
     if kind == "bred":
         g, _, _ = capi.reproduce(plan, plan.sample_random(1024, 42), n, 13)
+    elif kind == "rand":
+        g = plan.sample_random(n, 9)
     else:
         base = plan.sample_random(1 if kind == "dup" else 37, 5)
         g = base[torch.arange(n, device="cuda") % base.shape[0]].contiguous()
