@@ -583,7 +583,8 @@ etune_status score_select_local(etune_cu_ctx* c, const etune_cu_plan* p, etune_c
             CU(cudaEventRecord(ev[1], c->stream));
         }
         const cudaError_t e =
-            launch_score_select_rows(c->lc(), p->d_blob, p->build.hdr.ndk, p->nkeys, r.rt->d_clskuv, r.rt->d_meta,
+            launch_score_select_rows(c->lc(), p->d_blob, p->build.hdr.ndk, p->nkeys, p->build.hdr.nt,
+                                     p->build.hdr.off_divk, r.rt->d_clskuv, r.rt->d_meta,
                                      r.rt->d_rowrec, p->d_khash, d_genome, n, k, d_pred,
                                      d_ids, d_idx, c->rowsel);
         if (e == cudaSuccess) {

@@ -119,7 +119,7 @@ cudaError_t launch_rowtab_sort(const LaunchCtx& c, RowTabMeta* d_meta, const dou
 // grid holds in registers (the caller falls back to the bucketed selection).
 size_t rowsel_work_bytes();
 cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, int64_t nkeys,
-                                     const uint16_t* d_clskuv, const RowTabMeta* d_meta, const RowRec* d_rowrec,
+                                     const int32_t* nt, uint32_t off_divk, const uint16_t* d_clskuv, const RowTabMeta* d_meta, const RowRec* d_rowrec,
                                      const uint64_t* d_khash, const uint64_t* d_genome, int64_t n, int64_t k,
                                      double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work);
 cudaError_t launch_score_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, const uint16_t* d_clskuv,

@@ -811,7 +811,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // diagnostic (ETUNE_ROWSEL_TRACE): per-CTA globaltimer stamps, kSRTraceSlots slots per CTA
-constexpr int kSRTraceSlots = 16;  // the last slot holds the crossing segment's count, not a time
+constexpr int kSRTraceSlots = 16;  // slot 15 holds the crossing segment's count, not a time
 #define SR_TRACE(slot) \
     do { \
         if (trace && threadIdx.x == 0) trace[blockIdx.x * kSRTraceSlots + (slot)] = globaltimer(); \
@@ -1011,13 +1011,23 @@ struct SRStatic {
     uint32_t run[kSRKeys];                // the CTA's candidates per group offset of b0
     uint32_t ktot[kSRKeys];               // b0's candidates in group offsets < q (all CTAs)
     uint32_t kpre[kSRKeys];               // group offset q's candidates in the CTAs before this one
+    uint32_t jw[kSRPer * 32];             // b0's candidates per (j, warp), then their offsets
+    uint32_t lw[32];                      // candidates below b0 per warp, then their offsets
     uint32_t bin, before, cnt, base, mc;
     __align__(8) uint64_t mbar[kSRPer + 2];
 };
 
+// host-known plan scalars of the step kernel (kernel arguments: no dependent header loads)
+struct SRPlan {
+    uint32_t nt1, nt2, nkeys;
+    int ndk;
+    uint32_t off_divk;
+    int khash_smem;
+};
+
 __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
-    const uint8_t* __restrict__ gplan, const uint16_t* __restrict__ clskuv, const RowTabMeta* __restrict__ meta,
-    const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash, int khash_smem,
+    const uint8_t* __restrict__ gplan, SRPlan PL, const uint16_t* __restrict__ clskuv,
+    const RowTabMeta* __restrict__ meta, const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash,
     const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, double* __restrict__ pred,
     uint64_t* __restrict__ ids, int64_t* __restrict__ out, RowSelWork* __restrict__ W,
     unsigned long long* __restrict__ trace, int only_a, int force_radix) {
@@ -1028,77 +1038,73 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     __shared__ SRStatic S;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t base = uint32_t(blockIdx.x) * uint32_t(per) * kSRT;  // n < 2^31
-    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
-    const int ndk = H.ndk;
-    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
-    const uint32_t nkeys = uint32_t(H.nt[0]) * nt1 * nt2;
+    // ---- A0: the thread's genomes first (coalesced, all in flight), then the tables
+    uint64_t x0[kSRPer];
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j) {
+        const uint32_t i = base + uint32_t(j) * kSRT + tid;
+        x0[j] = (j < per && i < uint32_t(n)) ? __ldcs(genome + i) : ~0ull;
+    }
+    const int ndk = PL.ndk;
+    const uint32_t nt1 = PL.nt1, nt2 = PL.nt2;
     uint64_t* sgen = reinterpret_cast<uint64_t*>(dsm);                    // R0
     uint32_t* sgg = reinterpret_cast<uint32_t*>(dsm + kSRR0);             // per * T
     uint32_t* hist = sgg + per * kSRT;                                    // kSRMaxSeg
     uint32_t* scls32 = hist + kSRMaxSeg;                                  // ndk * 32
     uint32_t* sdivk = scls32 + ndk * 32;                                  // ndk (rounded to 4)
     uint64_t* skh = reinterpret_cast<uint64_t*>(sdivk + ((ndk + 3) & ~3));  // 16-byte aligned
-    const bool bulk = khash_smem && ids;
-    const bool tma = (reinterpret_cast<uintptr_t>(genome) & 15u) == 0;
-    // ---- the bulk copies go first: genomes per 1024 (mbar j), per-key FNV states (mbar kSRPer)
-    if (tid == 0) {
+    const bool bulk = PL.khash_smem && ids;
+    if (tid == 0) {  // per-key FNV states: one bulk copy (mbar kSRPer), needed only for the ids
         for (int j = 0; j < kSRPer + 2; ++j) mbar_init(&S.mbar[j]);
         mbar_fence_init();
-        for (int j = 0; j < per; ++j) {
-            const int64_t i0 = int64_t(base) + int64_t(j) * kSRT;
-            const int64_t c = i0 < n ? (n - i0 < kSRT ? n - i0 : kSRT) : 0;
-            const uint32_t bytes = tma ? uint32_t(c * 8) & ~15u : 0u;
-            if (bytes) {
-                bulk_g2s(sgen + j * kSRT, genome + i0, bytes, &S.mbar[j]);
-            } else {
-                mbar_arrive(&S.mbar[j]);
-            }
-        }
-        if (bulk) bulk_g2s(skh, khash, (nkeys * 8u + 15u) & ~15u, &S.mbar[kSRPer]);
+        if (bulk) bulk_g2s(skh, khash, (PL.nkeys * 8u + 15u) & ~15u, &S.mbar[kSRPer]);
     }
-    // genomes the bulk copies do not cover (an odd tail, or a genome pointer not 16-byte aligned)
-    for (int j = 0; j < per; ++j) {
-        const int64_t i0 = int64_t(base) + int64_t(j) * kSRT;
-        const int64_t c = i0 < n ? (n - i0 < kSRT ? n - i0 : kSRT) : 0;
-        const int64_t covered = tma ? int64_t((uint32_t(c * 8) & ~15u) / 8u) : 0;
-        if (tid >= covered) sgen[j * kSRT + tid] = tid < c ? __ldcs(genome + i0 + tid) : ~0ull;
-    }
+    const RowTabMeta M = *meta;
     {
         const uint32_t* src = reinterpret_cast<const uint32_t*>(clskuv);
         for (int i = tid; i < ndk * 32; i += kSRT) scls32[i] = __ldg(src + i);
-        const int64_t* divk = at<int64_t>(gplan, H.off_divk);
-        for (int i = tid; i < ndk; i += kSRT) sdivk[i] = uint32_t(divk[i]);
+        const int64_t* divk = at<int64_t>(gplan, PL.off_divk);
+        for (int i = tid; i < ndk; i += kSRT) sdivk[i] = uint32_t(__ldg(divk + i));
         reinterpret_cast<uint4*>(hist)[tid] = make_uint4(0, 0, 0, 0);
+        if (tid < kSRPer * 32) S.jw[tid] = 0u;  // phase C: only warps holding candidates at or below b0 write
+        if (tid < 32) S.lw[tid] = 0u;
     }
-    const uint32_t groups = uint32_t(meta->groups);
+    const uint32_t groups = uint32_t(M.groups);
     const int gbits = groups > 1 ? 32 - __clz(int(groups - 1)) : 0;
     const int segshift = gbits > 12 ? gbits - 12 : 0;  // level 0: <= 4096 segments of the group index
     const int nseg = int((groups + (1u << segshift) - 1) >> segshift);
-    const uint32_t nkc = uint32_t(meta->nkc);
+    const uint32_t nkc = uint32_t(M.nkc);
     __syncthreads();
+    SR_TRACE(13);
     const uint16_t* scls = reinterpret_cast<const uint16_t*>(scls32);
-    // ---- A1: every gather of the thread in flight together
+    // ---- A1: every gather of the thread in flight together; the genomes go to shared memory
     double p[kSRPer];
     uint32_t gq[kSRPer];
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j) {
         if (j >= per) break;
-        mbar_wait(&S.mbar[j], 0);
-        const uint64_t g = sgen[j * kSRT + tid];
+        const uint64_t g = x0[j];
+        sgen[j * kSRT + tid] = g;
         const bool v = g != ~0ull;
         const Genome x = genome_unpack(v ? g : 0ull);
         const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
         const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
-        const double2 r = v ? __ldg(reinterpret_cast<const double2*>(rowrec) + (key * nkc + kc)) : make_double2(0.0, 0.0);
+        // unconditional gather (an absent candidate reads row 0): a select on the loaded value here
+        // would wait for it and serialise the thread's gathers
+        const double2 r = __ldg(reinterpret_cast<const double2*>(rowrec) + (key * nkc + kc));
         p[j] = r.x;
-        gq[j] = v ? uint32_t(__double_as_longlong(r.y)) : 0xffffffffu;
+        gq[j] = uint32_t(__double_as_longlong(r.y));
     }
+    SR_TRACE(14);
     if (bulk) mbar_wait(&S.mbar[kSRPer], 0);
-    // ---- A2: outputs, histogram, g kept in shared memory
+    // ---- A2: outputs, histogram, g kept in shared memory; the thread's lowest g
+    uint32_t gmin = 0xffffffffu;
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j) {
         if (j >= per) break;
+        if (sgen[j * kSRT + tid] == ~0ull) gq[j] = 0xffffffffu;  // no candidate
         sgg[j * kSRT + tid] = gq[j];
+        gmin = min(gmin, gq[j]);
         if (gq[j] == 0xffffffffu) continue;
         const uint32_t i = base + uint32_t(j) * kSRT + tid;
         pred[i] = p[j];
@@ -1131,64 +1137,98 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     sr_cross(W->lvl[0], kk, S.ws, &S.bin, &S.before, &S.cnt);
     const uint32_t b0 = S.bin, before0 = S.before;
     SR_TRACE(7);
-    if (trace && tid == 0) trace[blockIdx.x * kSRTraceSlots + kSRTraceSlots - 1] = S.cnt;
+    if (trace && tid == 0) trace[blockIdx.x * kSRTraceSlots + 15] = S.cnt;
     unsigned long long* xk = reinterpret_cast<unsigned long long*>(dsm);  // ranked list (R0, 32 KB)
     uint32_t* sb0 = reinterpret_cast<uint32_t*>(dsm + kSRR0 / 2);         // b0's candidates (R0, 32 KB)
     auto gkey = [&](int j) { return (uint64_t(sgg[j * kSRT + tid]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); };
     if (segshift <= 6 && !force_radix) {  // grid-uniform
         const uint32_t nq = 1u << segshift, qmask = nq - 1u;
+        const unsigned lt = (1u << lane) - 1u;
         // ---- C: the candidates below b0 -> the list (fewer than k); b0's candidates compacted in
-        //      index order; one block scan for both
-        uint32_t lc = 0;
-        uint4 f = make_uint4(0, 0, 0, 0);  // 16-bit count of b0 candidates per j (two per word)
-#pragma unroll
-        for (int j = 0; j < kSRPer; ++j) {
-            const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
-            const uint32_t sg = g >> segshift;
-            lc += (g != 0xffffffffu && sg < b0) ? 1u : 0u;
-            const uint32_t add = (g != 0xffffffffu && sg == b0) ? (1u << (16 * (j & 1))) : 0u;
-            if (j < 2) f.x += add; else if (j < 4) f.y += add; else if (j < 6) f.z += add; else f.w += add;
-        }
-        uint4 ftot;
-        uint32_t lex, ltot;
-        const uint4 fex = sr_block_scan5(f, lc, S.ws, &ftot, &lex, &ltot);
-        if (ltot) {  // block-uniform: append (g, index) with one atomic per CTA, kSRRep copies
-            if (tid == 0) S.base = atomicAdd(&W->nlist, ltot);
-            __syncthreads();
-            uint32_t off = S.base + lex;
+        //      index order (j, warp, lane).  Warp ballots per j, one warp scans the (j, warp) counts.
+        // a warp none of whose candidates is at or below b0 (nearly all of them) skips C
+        const bool wact = __any_sync(0xffffffffu, gmin != 0xffffffffu && (gmin >> segshift) <= b0);
+        uint32_t mb = 0, ml = 0;  // per j: in b0 / below b0
+        uint32_t lw = 0;
+        if (wact) {
 #pragma unroll
             for (int j = 0; j < kSRPer; ++j) {
                 const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
-                if (g != 0xffffffffu && (g >> segshift) < b0) {
-                    if (off < uint32_t(kSRListCap)) {
-                        const uint64_t kv = gkey(j);
-#pragma unroll
-                        for (int r = 0; r < kSRRep; ++r) W->lkey[r][off] = kv;
-                    }
-                    ++off;
+                const uint32_t sg = g >> segshift;
+                if (g != 0xffffffffu) {
+                    if (sg < b0) ml |= 1u << j;
+                    else if (sg == b0) mb |= 1u << j;
                 }
             }
-        }
-        SR_TRACE(10);
-        {
-            const uint32_t ex[4] = {fex.x, fex.y, fex.z, fex.w}, tt[4] = {ftot.x, ftot.y, ftot.z, ftot.w};
-            uint32_t run = 0;
 #pragma unroll
             for (int j = 0; j < kSRPer; ++j) {
-                const uint32_t e = (ex[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-                const uint32_t t = (tt[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-                const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
-                if (g != 0xffffffffu && (g >> segshift) == b0) sb0[run + e] = (uint32_t(j * kSRT + tid) << 19) | (g & qmask);
-                run += t;
+                const unsigned bb = __ballot_sync(0xffffffffu, (mb >> j) & 1u);
+                const unsigned bl = __ballot_sync(0xffffffffu, (ml >> j) & 1u);
+                if (lane == 0) S.jw[j * 32 + warp] = __popc(bb);
+                lw += __popc(bl);
             }
-            if (tid == 0) S.mc = run;
         }
+        if (wact && lane == 0) S.lw[warp] = lw;
         if (tid < kSRKeys) S.run[tid] = 0u;
         __syncthreads();
-        SR_TRACE(11);
+        if (warp == 0) {
+            uint32_t c[kSRPer], sum = 0;  // lane l: (j, warp) entries [8l, 8l + 8) in j-major order
+#pragma unroll
+            for (int i = 0; i < kSRPer; ++i) {
+                c[i] = S.jw[kSRPer * lane + i];
+                sum += c[i];
+            }
+            const uint32_t inc = warp_incl_scan(sum);
+            uint32_t run = inc - sum;
+#pragma unroll
+            for (int i = 0; i < kSRPer; ++i) {
+                S.jw[kSRPer * lane + i] = run;
+                run += c[i];
+            }
+            const uint32_t l = S.lw[lane], li = warp_incl_scan(l);
+            S.lw[lane] = li - l;
+            const uint32_t lt_all = __shfl_sync(0xffffffffu, li, 31);
+            if (lane == 31) {
+                S.mc = inc;
+                S.base = lt_all ? atomicAdd(&W->nlist, lt_all) : 0u;
+            }
+        }
+        __syncthreads();
         const uint32_t mc = S.mc;
+        uint32_t loff = S.base + S.lw[warp];
+#pragma unroll
+        for (int j = 0; j < kSRPer; ++j) {
+            if (!wact) break;  // warp-uniform
+            const unsigned bb = __ballot_sync(0xffffffffu, (mb >> j) & 1u);
+            const unsigned bl = __ballot_sync(0xffffffffu, (ml >> j) & 1u);
+            if ((mb >> j) & 1u)
+                sb0[S.jw[j * 32 + warp] + __popc(bb & lt)] = (uint32_t(j * kSRT + tid) << 19) | (sgg[j * kSRT + tid] & qmask);
+            if ((ml >> j) & 1u) {
+                const uint32_t off = loff + __popc(bl & lt);
+                if (off < uint32_t(kSRListCap)) {
+                    const uint64_t kv = gkey(j);
+#pragma unroll
+                    for (int r = 0; r < kSRRep; ++r) W->lkey[r][off] = kv;
+                }
+            }
+            loff += __popc(bl);
+        }
+        __syncthreads();
+        SR_TRACE(11);
         // stable multi-split: each b0 candidate's order among the CTA's candidates of its group
-        for (uint32_t c0 = 0; c0 < mc; c0 += kSRT) {
+        if (mc <= 32) {  // block-uniform: one warp, records already in index order
+            if (warp == 0) {
+                const bool valid = lane < int(mc);
+                const uint32_t e = valid ? sb0[lane] : 0u;
+                const uint32_t q = valid ? (e & 63u) : 64u;
+                const unsigned peers = __match_any_sync(0xffffffffu, q);
+                const unsigned lower = peers & lt;
+                if (valid) sb0[lane] = e | (uint32_t(__popc(lower)) << 6);
+                if (valid && lower == 0) S.run[q] = __popc(peers);
+            }
+            __syncthreads();
+        }
+        for (uint32_t c0 = 0; mc > 32 && c0 < mc; c0 += kSRT) {
             for (int i = tid; i < (kSRT / 32) * (kSRKeys + 1); i += kSRT) (&S.wcount[0][0])[i] = 0u;
             __syncthreads();
             const uint32_t pidx = c0 + uint32_t(tid);
@@ -1196,7 +1236,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             const uint32_t e = valid ? sb0[pidx] : 0u;
             const uint32_t q = valid ? (e & 63u) : 64u;
             const unsigned peers = __match_any_sync(0xffffffffu, q);
-            const unsigned lower = peers & ((1u << lane) - 1u);
+            const unsigned lower = peers & lt;
             if (valid && lower == 0) S.wcount[warp][q] = __popc(peers);
             __syncthreads();
             for (int qq = warp; qq < kSRKeys; qq += kSRT / 32) {  // warp per group offset: scan over the warps
@@ -1483,7 +1523,7 @@ cudaError_t launch_rowtab_sort(const LaunchCtx& c, RowTabMeta* d_meta, const dou
 size_t rowsel_work_bytes() { return sizeof(RowSelWork); }
 
 cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk, int64_t nkeys,
-                                     const uint16_t* d_clskuv, const RowTabMeta* d_meta, const RowRec* d_rowrec,
+                                     const int32_t* nt, uint32_t off_divk, const uint16_t* d_clskuv, const RowTabMeta* d_meta, const RowRec* d_rowrec,
                                      const uint64_t* d_khash, const uint64_t* d_genome, int64_t n, int64_t k,
                                      double* d_pred, uint64_t* d_ids, int64_t* d_idx, void* d_work) {
     if (n <= 0 || k <= 0) return cudaSuccess;
@@ -1492,6 +1532,13 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
     const int khash_smem = nkeys * 8 <= 64 * 1024 ? 1 : 0;
     const size_t sm_fixed = size_t(kSRR0) + size_t(kSRMaxSeg) * 4 + size_t(ndk) * 128 + size_t((ndk + 3) & ~3) * 4 +
                             (khash_smem ? size_t((nkeys * 8 + 15) & ~int64_t(15)) : 0);
+    SRPlan PL{};
+    PL.nt1 = uint32_t(nt[1]);
+    PL.nt2 = uint32_t(nt[2]);
+    PL.nkeys = uint32_t(nkeys);
+    PL.ndk = ndk;
+    PL.off_divk = off_divk;
+    PL.khash_smem = khash_smem;
     static int optin = 0, sms = 0;
     if (!optin) {
         int dev = 0;
@@ -1533,8 +1580,8 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
     // ETUNE_ROWSEL_RADIX=1 (diagnostic, read every call): the radix-select path for any group count
     const char* fr = std::getenv("ETUNE_ROWSEL_RADIX");
     int force_radix = (fr && fr[0] == '1') ? 1 : 0;
-    void* args[] = {(void*)&d_plan,   (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowrec, (void*)&d_khash,
-                    (void*)&khash_smem, (void*)&d_genome, (void*)&n,    (void*)&k,        (void*)&per_i,
+    void* args[] = {(void*)&d_plan,   (void*)&PL,       (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowrec,
+                    (void*)&d_khash,  (void*)&d_genome, (void*)&n,    (void*)&k,        (void*)&per_i,
                     (void*)&d_pred,   (void*)&d_ids,    (void*)&d_idx,  (void*)&W,        (void*)&tr,
                     (void*)&oa,       (void*)&force_radix};
     note_launches(1);
@@ -1552,17 +1599,17 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
             unsigned long long t0 = ~0ull;
             for (int b = 0; b < int(grid); ++b) t0 = std::min(t0, t[b * S]);
             for (int b = 0; b < int(grid); ++b)
-                for (int s = 0; s < S - 1; ++s)
+                for (int s = 0; s < 15; ++s)
                     if (t[b * S + s] >= t0) v[s].push_back(double(t[b * S + s] - t0) * 1e-3);
         }
         std::fprintf(stderr, "rowsel: candidates in the crossing segment of the last call: %llu\n",
-                     (unsigned long long)h[size_t(want_trace - 1) * kSRMaxCtas * S + S - 1]);
+                     (unsigned long long)h[size_t(want_trace - 1) * kSRMaxCtas * S + 15]);
         static const char* names[S] = {"start", "A done", "flushed", "sync1", "appended", "sync2",
                                        "ranked", "crossed", "staged", "counted", "L-append", "compact",
-                                       "msplit", "-", "-", "count"};
+                                       "msplit", "prologue", "A1 issued", "count"};
         std::fprintf(stderr, "rowsel trace n=%lld grid=%lld per=%d over %d calls (us from the first CTA start):\n",
                      (long long)n, (long long)grid, per_i, want_trace);
-        for (int s = 0; s < S - 1; ++s) {
+        for (int s = 0; s < 15; ++s) {
             if (v[s].empty()) continue;
             std::sort(v[s].begin(), v[s].end());
             std::fprintf(stderr, "  %-9s min %7.2f  p50 %7.2f  p90 %7.2f  max %7.2f\n", names[s], v[s].front(),

@@ -22,6 +22,7 @@ ap.add_argument("--model", default="c2_r50_conv3x3")
 ap.add_argument("--n", type=int, default=1 << 20)
 ap.add_argument("--k", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=200)
+ap.add_argument("--bufs", type=int, default=16)
 a = ap.parse_args()
 g = np.load(os.path.join(ROOT, "tests", "golden", "golden_reference.npz"))
 k = f"{a.model}/model/"
@@ -34,7 +35,7 @@ ctx = capi.Context(0)
 plan = capi.Plan(ctx, parse_op(a.op))
 par = plan.sample_random(1024, 42)
 gen, _, _ = capi.reproduce(plan, par, a.n, 7)
-nb = 16
+nb = a.bufs
 bufs = [gen.clone() for _ in range(nb)]
 preds = [torch.empty(a.n, dtype=torch.float64, device="cuda") for _ in range(nb)]
 idss = [torch.empty(a.n, dtype=torch.int64, device="cuda") for _ in range(nb)]
