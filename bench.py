@@ -78,6 +78,7 @@ def parse():
     p.add_argument("--no-search", action="store_true", help="skip the search-round latency measurement")
     p.add_argument("--search-rounds", type=int, default=5)
     p.add_argument("--no-reproduce", action="store_true", help="skip the reproduce (2^20 offspring) timing")
+    p.add_argument("--no-graph", action="store_true", help="time the eager launch loop only (no CUDA graph replay)")
     return p.parse_args()
 
 
@@ -417,29 +418,66 @@ def run_ours(args):
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # The K timed steps are captured once into a CUDA graph (the library launches on the ctx stream,
+    # which is the capture stream) and replayed: back-to-back launches of a 148-CTA cooperative kernel
+    # cost ~2 us less per launch from a graph than from the stream (scripts/micro/step_floor.cu).  The
+    # eager launch loop is timed as well (eager_ms_per_step).  N > 1 (NCCL inside the step) stays eager.
+    use_graph = world == 1 and not args.no_graph
+    graph = None
     launches0 = capi.lib().etune_cu_launch_count()
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(args.steps):
+                step(forest, args.warmup + i)
+        launches = capi.lib().etune_cu_launch_count() - launches0  # our kernels in the graph (one per step)
+        graph.replay()  # untimed: the graph's first launch uploads it
+        torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    clk.sm.clear()
-    with clk:
+
+    def timed_loop():
+        clk.sm.clear()
+        with clk:
+            torch.cuda.synchronize()
+            ev0.record(stream)
+            clk.sample()
+            if graph is not None:
+                graph.replay()
+            else:
+                for i in range(args.steps):
+                    step(forest, args.warmup + i)
+            ev1.record(stream)
+            clk.sample()
+            torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1) / args.steps
+
+    if world > 1:
+        dist.barrier()
+    ms = timed_loop()
+    clocks = clk.summary()
+    if graph is None:
+        launches = capi.lib().etune_cu_launch_count() - launches0
+        eager_ms = ms
+    else:
         torch.cuda.synchronize()
-        ev0.record(stream)
-        clk.sample()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
         for i in range(args.steps):
             step(forest, args.warmup + i)
-        ev1.record(stream)
-        clk.sample()
+        e1.record(stream)
         torch.cuda.synchronize()
-    launches = capi.lib().etune_cu_launch_count() - launches0
-    ms = ev0.elapsed_time(ev1) / args.steps
+        eager_ms = e0.elapsed_time(e1) / args.steps
     # kernel duration: CUDA events around the step kernel of each call (a separate pass: the events
     # separate the launches the timed loop runs back to back)
     capi.profile_score(ctx, True)
     for i in range(args.steps):
         step(forest, args.warmup + args.steps + i)
     _, score_ms, select_ms, score_calls = capi.profile_score(ctx, False)
-    kernel_ms = score_ms / max(score_calls, 1)
+    event_kernel_ms = score_ms / max(score_calls, 1)
     select_ms = select_ms / max(score_calls, 1)
+    # the roofline's per-launch duration: the graph-replayed step is this one kernel back to back
+    kernel_ms = ms if graph is not None else event_kernel_ms
     if world > 1:
         t = torch.tensor([ms, kernel_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -482,13 +520,25 @@ def run_ours(args):
             for i in range(3):
                 step(forest, i, m)
             torch.cuda.synchronize()
+            sg = None
+            if use_graph:
+                sg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(sg, stream=stream):
+                    for i in range(reps):
+                        step(forest, i, m)
+                sg.replay()
+                torch.cuda.synchronize()
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record(stream)
-            for i in range(reps):
-                step(forest, i, m)
+            if sg is not None:
+                sg.replay()
+            else:
+                for i in range(reps):
+                    step(forest, i, m)
             a1.record(stream)
             torch.cuda.synchronize()
             fm = a0.elapsed_time(a1) / reps
+            del sg
             fs = fresh_steps(m, 6)
             sweep.append({"population": m, "frozen_ms": fm, "frozen_value": m / (fm / 1e3),
                           "fresh_ms": fs * 1e3, "fresh_value": m / fs})
@@ -604,11 +654,16 @@ def run_ours(args):
                      "note": "the step is this one kernel (score + select fused); design_frac is the HBM utilisation "
                              "on the bytes it must move (8 B genome in, 8 B prediction + 8 B id out); row-table "
                              "gathers and per-row counters are L2 traffic; see profiles/",
-                     "select_ms": select_ms},
+                     "select_ms": select_ms, "event_kernel_ms": event_kernel_ms,
+                     "kernel_ms_source": "CUDA-graph replay of the K timed steps (one kernel per step, back to "
+                                         "back) / K" if graph is not None else "CUDA events around each launch"},
         "compile_ms": compile_ms,
         "fresh_model": fresh,
         "gpu_launches": int(launches),
-        "clocks": clk.summary(),
+        "launch": "CUDA graph of the K steps (captured on the ctx stream, replayed once)" if graph is not None
+                  else "eager stream launches",
+        "eager_ms_per_step": eager_ms,
+        "clocks": clocks,
     }
     if sweep:
         line["sweep"] = sweep

@@ -165,6 +165,30 @@ int main() {
         cfg.numAttrs = 1;
         run("cooperative empty (LaunchKernelEx)", [&](int) { cudaLaunchKernelEx(&cfg, empty_kernel, d); });
     }
+    // the same launches replayed from a CUDA graph (200 kernels per graph)
+    for (int coop = 0; coop < 2; ++coop) {
+        const size_t smem = 80 * 1024;
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
+        void* args[] = {&d};
+        for (int i = 0; i < R; ++i) {
+            if (coop) cudaLaunchCooperativeKernel((void*)cg_sync_kernel<1>, G, T, args, smem, st);
+            else empty_kernel<<<G, T, smem, st>>>(d);
+        }
+        cudaStreamEndCapture(st, &g);
+        cudaGraphInstantiate(&ge, g, 0);
+        cudaGraphLaunch(ge, st);
+        cudaStreamSynchronize(st);
+        cudaEventRecord(a, st);
+        cudaGraphLaunch(ge, st);
+        cudaEventRecord(b, st);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        printf("%-52s %8.2f us/launch  (%s)\n", coop ? "graph: cooperative cg 1 sync, 80 KB smem" : "graph: regular empty, 80 KB smem",
+               ms * 1e3 / R, cudaGetErrorString(cudaGetLastError()));
+    }
     // streams of the step's traffic (16 buffers cycled: 384 MB > L2)
     run("stream 8B in 16B out, 2^20, per=7 (147 CTAs)", [&](int i) {
         stream_kernel<7><<<(n + 7 * 1024 - 1) / (7 * 1024), 1024, 0, st>>>(gs[i % NB], ps[i % NB], is[i % NB], n);
