@@ -190,8 +190,9 @@ etune_status etune_cu_features(etune_cu_ctx* ctx, const etune_cu_plan* plan,
  * (measure_latency_ms); d_power_w / d_energy_mj / d_iterations are nullable — all
  * three NULL is the cheap latency-only evaluation used by the latency filter.
  * The reference ships no implementation of these; parity is against the repo's CPU
- * restatement (oracle/), whose operation order and noise generator (Irwin-Hall over
- * splitmix64, no libm) this kernel follows bit for bit. */
+ * restatement (oracle/), whose operation order and noise generator (SPEC:327's
+ * multiplicative Gaussian: a polar-method normal over splitmix64 words with a log built
+ * from IEEE +, *, / -- no libm) this kernel follows bit for bit. */
 etune_status etune_cu_sim_measure(etune_cu_ctx* ctx, const etune_cu_plan* plan,
                                   const uint64_t* d_genome, int64_t n, double* d_latency_ms,
                                   double* d_power_w, double* d_energy_mj, int64_t* d_iterations);

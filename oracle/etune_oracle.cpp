@@ -542,8 +542,9 @@ int orc_enumerate(const int64_t* op, const int64_t* limits, int64_t cap, int64_t
 // (measure.hpp:29-60, 102-114) but ships no implementation; SPEC:314-322 fixes the
 // formula: latency = max(compute, memory, floor), power = constant + static*active +
 // dynamic_energy / latency.  This restatement (parity unpinned by the reference) fixes
-// the operation order, and the sampler noise is made bit-reproducible on any IEEE
-// machine: z = (sum of 12 uniforms from splitmix64) - 6 (Irwin-Hall), no libm.  The
+// the operation order, and the sampler noise -- SPEC:327's multiplicative Gaussian -- is made
+// bit-reproducible on any IEEE machine: a standard normal per sample by Marsaglia's polar method
+// over splitmix64 words, with ln built from +, *, / only (det_log), no libm.  The
 // device kernel (paper_2411_18873_b200/csrc/measure.cu) follows it operation by
 // operation.  Constants: 1000 iterations / 2 s sample window, samples
 // capped at 4096 per measurement.
@@ -553,6 +554,42 @@ uint64_t splitmix(uint64_t x) {
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
     x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
     return x ^ (x >> 31);
+}
+// ln s for s in (0, 1) from IEEE +, *, / only: s = m 2^e, m in [sqrt(1/2), sqrt(2)),
+// ln m = 2 atanh((m - 1) / (m + 1)) by the odd series to t^23 (Horner in t^2), ln s =
+// e ln2_hi + (e ln2_lo + ln m) -- the device kernel evaluates the same operations
+const double kLogC[12] = {0x1p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3, 0x1.2492492492492p-3, 0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4, 0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4, 0x1.e1e1e1e1e1e1ep-5, 0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5};
+double det_log(double s) {
+    uint64_t b;
+    std::memcpy(&b, &s, 8);
+    int e = int((b >> 52) & 0x7ffu) - 1023;
+    const uint64_t mb = (b & 0x000fffffffffffffull) | 0x3ff0000000000000ull;
+    double m;
+    std::memcpy(&m, &mb, 8);
+    if (m > 0x1.6a09e667f3bcdp+0) {
+        m = m * 0.5;
+        e += 1;
+    }
+    const double t = (m - 1.0) / (m + 1.0);
+    const double t2 = t * t;
+    double q = kLogC[11];
+    for (int i = 10; i >= 0; --i) q = q * t2 + kLogC[i];
+    const double lm = (t * q) * 2.0;
+    const double de = static_cast<double>(e);
+    return de * 0x1.62e42feep-1 + (de * 0x1.a39ef35793c76p-33 + lm);
+}
+// standard normal j of the stream `key`: Marsaglia's polar method, attempt a from the words
+// key + 64 j + 2a and + 2a + 1 (v = 2u - 1, exact); 0 after 32 rejections
+double det_normal(uint64_t key, int64_t j) {
+    for (int a = 0; a < 32; ++a) {
+        const uint64_t h1 = splitmix(key + static_cast<uint64_t>(j) * 64u + static_cast<uint64_t>(2 * a));
+        const uint64_t h2 = splitmix(key + static_cast<uint64_t>(j) * 64u + static_cast<uint64_t>(2 * a + 1));
+        const double v1 = static_cast<double>(h1 >> 11) * 0x1p-52 - 1.0;
+        const double v2 = static_cast<double>(h2 >> 11) * 0x1p-52 - 1.0;
+        const double s = v1 * v1 + v2 * v2;
+        if (s > 0.0 && s < 1.0) return v1 * std::sqrt((-2.0 * det_log(s)) / s);
+    }
+    return 0.0;
 }
 struct SimDev {
     double num_sms, constant, static_sm, e_flop, e_glb, e_shared, tput, bw, floor_ms, hz, warmup, sigma;
@@ -579,14 +616,7 @@ void sim_measure(const Counters& c, const SimDev& d, uint64_t id, double* out4) 
         const uint64_t key = splitmix(d.seed ^ id);
         double sum = 0.0;
         for (int64_t j = 0; j < S; ++j) {
-            // z ~ Irwin-Hall(12) - 6: twelve 16-bit uniforms from three splitmix64 words,
-            // summed as integers (exact), one conversion
-            uint64_t usum = 0;
-            for (int q = 0; q < 3; ++q) {
-                const uint64_t h = splitmix(key + static_cast<uint64_t>(j * 3 + q));
-                for (int b = 0; b < 4; ++b) usum += (h >> (16 * b)) & 0xffffu;
-            }
-            const double z = static_cast<double>(usum) * 0x1p-16 - 6.0;
+            const double z = det_normal(key, j);  // N(0, 1)
             sum += power * (1.0 + d.sigma * z);
         }
         avg = sum / static_cast<double>(S);

@@ -227,8 +227,10 @@ __global__ void __launch_bounds__(kThreads) counters_kernel(const uint8_t* __res
 // ------------------------------------------------------ SimBackend measure
 // sim_true_power_and_latency + nvml_sim_measure (measure.hpp:29-60; formula SPEC:314-322).
 // No reference implementation exists: this follows the oracle restatement
-// (oracle/etune_oracle.cpp, sim_measure) operation by operation; the sampler noise is
-// Irwin-Hall over splitmix64 words, so it is bit-reproducible without libm.
+// (oracle/etune_oracle.cpp, sim_measure) operation by operation.  The sampler noise is the
+// multiplicative Gaussian of SPEC:327: a standard normal per sample by Marsaglia's polar method
+// over splitmix64 words, with a natural log built from IEEE +, *, / only, so the device and the
+// restatement agree bit for bit without libm.
 __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
     x += 0x9e3779b97f4a7c15ull;
     x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -236,16 +238,46 @@ __device__ __forceinline__ uint64_t splitmix(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-// sample j of the simulated sampler: power * (1 + sigma * z_j), z_j = Irwin-Hall(12) - 6
-// from twelve 16-bit uniforms of three splitmix64 words (integer sum, one conversion)
-__device__ __forceinline__ double sim_sample(double power, double sigma, uint64_t key, int64_t j) {
-    uint64_t usum = 0;
-#pragma unroll
-    for (int q = 0; q < 3; ++q) {
-        const uint64_t h = splitmix(key + uint64_t(j * 3 + q));
-        usum += (h & 0xffffu) + ((h >> 16) & 0xffffu) + ((h >> 32) & 0xffffu) + (h >> 48);
+// ln s for s in (0, 1): s = m 2^e with m in [sqrt(1/2), sqrt(2)), ln m = 2 atanh(t),
+// t = (m - 1) / (m + 1), |t| <= 0.1716, by the odd series to t^23 (Horner in t^2), and
+// ln s = e ln2_hi + (e ln2_lo + ln m) (fdlibm's split of ln 2: e ln2_hi is exact)
+__device__ __constant__ double kLogC[12] = {0x1p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3, 0x1.2492492492492p-3, 0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4, 0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4, 0x1.e1e1e1e1e1e1ep-5, 0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5};
+__device__ __forceinline__ double det_log(double s) {
+    const uint64_t b = static_cast<uint64_t>(__double_as_longlong(s));
+    int e = int((b >> 52) & 0x7ffu) - 1023;
+    double m = __longlong_as_double(static_cast<long long>((b & 0x000fffffffffffffull) | 0x3ff0000000000000ull));
+    if (m > 0x1.6a09e667f3bcdp+0) {
+        m = __dmul_rn(m, 0.5);
+        e += 1;
     }
-    const double z = __dsub_rn(__dmul_rn(static_cast<double>(usum), 0x1p-16), 6.0);
+    const double t = __ddiv_rn(__dsub_rn(m, 1.0), __dadd_rn(m, 1.0));
+    const double t2 = __dmul_rn(t, t);
+    double q = kLogC[11];
+#pragma unroll
+    for (int i = 10; i >= 0; --i) q = __dadd_rn(__dmul_rn(q, t2), kLogC[i]);
+    const double lm = __dmul_rn(__dmul_rn(t, q), 2.0);
+    const double de = static_cast<double>(e);
+    return __dadd_rn(__dmul_rn(de, 0x1.62e42feep-1), __dadd_rn(__dmul_rn(de, 0x1.a39ef35793c76p-33), lm));
+}
+
+// standard normal number j of the stream `key`: Marsaglia's polar method, attempt a drawing
+// the words key + 64 j + 2a, + 2a + 1 (v = 2u - 1 from the top 53 bits, exact); 0 after 32
+// rejections (probability 0.2146^32)
+__device__ __forceinline__ double det_normal(uint64_t key, int64_t j) {
+    for (int a = 0; a < 32; ++a) {
+        const uint64_t h1 = splitmix(key + uint64_t(j) * 64u + uint64_t(2 * a));
+        const uint64_t h2 = splitmix(key + uint64_t(j) * 64u + uint64_t(2 * a + 1));
+        const double v1 = __dsub_rn(__dmul_rn(static_cast<double>(h1 >> 11), 0x1p-52), 1.0);
+        const double v2 = __dsub_rn(__dmul_rn(static_cast<double>(h2 >> 11), 0x1p-52), 1.0);
+        const double s = __dadd_rn(__dmul_rn(v1, v1), __dmul_rn(v2, v2));
+        if (s > 0.0 && s < 1.0) return __dmul_rn(v1, __dsqrt_rn(__ddiv_rn(__dmul_rn(-2.0, det_log(s)), s)));
+    }
+    return 0.0;
+}
+
+// sample j of the simulated sampler: power * (1 + sigma * z_j), z_j standard normal
+__device__ __forceinline__ double sim_sample(double power, double sigma, uint64_t key, int64_t j) {
+    const double z = det_normal(key, j);
     return __dmul_rn(power, __dadd_rn(1.0, __dmul_rn(sigma, z)));
 }
 

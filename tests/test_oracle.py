@@ -171,6 +171,28 @@ def test_sim_measure_spec_examples(oracle):
     assert np.abs(r1[:, 1] / r0[:, 1] - 1).max() < 0.02
 
 
+def test_sim_noise_is_gaussian_spec(oracle):
+    """SPEC:327/331: the sampler's multiplicative noise is Gaussian with sigma noise_sigma_rel;
+    at sigma 0.05 with >= 2 s of 50 Hz samples the average power is within 2 % of the true power
+    for >= 99 of 100 seeds.  The standardised deviations of the averages over seeds and
+    candidates, (avg / true - 1) / (sigma / sqrt(S)), have mean ~0 and variance ~1."""
+    from etune_testlib import parse_op
+    op = parse_op("mm:1,64,64,64")
+    full = oracle.enumerate(op)[:40]
+    r0 = oracle.sim_measure(op, full, {"noise_sigma_rel": 0.0})
+    lat_s = r0[:, 0] / 1000.0
+    S = np.clip(np.floor(r0[:, 3] * lat_s * 50.0), 1, 4096)
+    zs, within = [], 0
+    for seed in range(100):
+        r = oracle.sim_measure(op, full, {"noise_sigma_rel": 0.05, "sampler_hz": 50.0, "rng_seed": seed})
+        dev = r[:, 1] / r0[:, 1] - 1.0
+        within += int(abs(dev[0]) < 0.02)
+        zs.append(dev / (0.05 / np.sqrt(S)))
+    z = np.concatenate(zs)
+    assert within >= 99
+    assert abs(z.mean()) < 0.05 and 0.9 < z.var() < 1.1
+
+
 def test_reproduce_counter_restatement(oracle):
     """The counter-mode restatement: deterministic, prefix-stable (offspring i depends only on
     (seed, i, parents)), every child legal with a correct id and lineage, and the move mix of
