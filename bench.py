@@ -485,6 +485,42 @@ def run_ours(args):
         dist.barrier()
     value = world * n / (ms / 1e3)
 
+    # ---- feature mode: etune_cu_features, genome -> 16 f64 features + id; HBM-bound
+    feature_mode = None
+    if world == 1:
+        fb = min(nb, 4)
+        fbufs = [torch.empty((n, 16), dtype=torch.float64, device="cuda") for _ in range(fb)]
+
+        def fstep(i):
+            b = i % fb
+            capi._check(capi.lib().etune_cu_features(ctx.h, plan.h, capi._ptr(genomes[i % nb]), n,
+                                                     capi._ptr(fbufs[b]), capi._ptr(ids[i % nb])))
+
+        for i in range(3):
+            fstep(i)
+        torch.cuda.synchronize()
+        fe0, fe1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fe0.record(stream)
+        for i in range(args.steps):
+            fstep(i)
+        fe1.record(stream)
+        torch.cuda.synchronize()
+        fms = fe0.elapsed_time(fe1) / args.steps
+        del fbufs
+        feature_mode = {
+            "value": n / (fms / 1e3), "unit": UNIT, "ms_per_step": fms,
+            "what": "etune_cu_features over the bench population: the 16 f64 features of features_from_counters "
+                    "(features.cpp:15-51, bit-exact) + candidate_id per candidate, eager launches, "
+                    f"{min(nb, 4)} output buffers cycled ({min(nb, 4) * n * 128 / 2**20:.0f} MB)",
+            "roofline": {"bound": "hbm", "achieved": n * 192 / (fms / 1e3) / 1e9, "peak": None, "unit": "GB/s",
+                         "algorithmic_bytes_per_candidate": 192,
+                         "algorithmic_bytes_source": "SURVEY.md §8(d) feature mode: 48 B schedule in + 8 B "
+                                                     "prediction + 8 B id + 128 B features",
+                         "design_bytes_per_candidate": 144,
+                         "design_achieved": n * 144 / (fms / 1e3) / 1e9,
+                         "note": "design bytes: 8 B genome in, 128 B features + 8 B id out"},
+        }
+
     # ---- fresh model: every step a model the library has not seen (created from the host arrays,
     # compiled on the device, scored + selected, destroyed); host wall clock around synchronised steps
     def fresh_steps(m, reps):
@@ -665,6 +701,12 @@ def run_ours(args):
         "eager_ms_per_step": eager_ms,
         "clocks": clocks,
     }
+    if feature_mode:
+        fr = feature_mode["roofline"]
+        fr["peak"] = hbm
+        fr["frac"] = fr["achieved"] / hbm
+        fr["design_frac"] = fr["design_achieved"] / hbm
+        line["feature_mode"] = feature_mode
     if sweep:
         line["sweep"] = sweep
     if e2e:

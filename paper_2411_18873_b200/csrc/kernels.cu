@@ -350,26 +350,46 @@ __global__ void __launch_bounds__(kThreads) sim_measure_kernel(const uint8_t* __
 }
 
 
-__global__ void __launch_bounds__(kThreads) features_kernel(const uint8_t* __restrict__ gplan, uint32_t bytes,
-                                                            int use_smem, const uint64_t* __restrict__ genome,
-                                                            int64_t n, double* __restrict__ feat,
-                                                            uint64_t* __restrict__ ids) {
-    extern __shared__ int4 smem[];
+// Feature mode (etune_cu_features): 16 f64 features + id per candidate, 136 of its 144 bytes
+// output.  HBM-bound, so: no plan staging (the per-operator tables are read through L1, where
+// they stay), and each warp's 32 x 128-byte feature rows leave through a shared-memory
+// transpose as fully coalesced 16-byte stores (a thread storing its own row touches 32 lines
+// per instruction: 57 -> 37 us at 2^20).  Shared rows are padded to 17 doubles (2-way bank
+// conflicts; 144-byte rows with 16-byte accesses measured no faster).  What bounds it now is
+// the L1 tag stage: ~12.5 sectors of table lookups per candidate (profiles/r02z_features_ncu.md).
+constexpr int kFeatT = 256;
+__global__ void __launch_bounds__(kFeatT, 5) features_kernel(const uint8_t* __restrict__ gplan,
+                                                             const uint64_t* __restrict__ genome, int64_t n,
+                                                             double* __restrict__ feat, uint64_t* __restrict__ ids) {
+    __shared__ double tr[kFeatT / 32][32 * 17];
     const uint8_t* P = gplan;
-    if (use_smem) {
-        stage(gplan, bytes, smem);
-        __syncthreads();
-        P = reinterpret_cast<const uint8_t*>(smem);
-    }
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        const Knobs c = load_knobs(P, H, genome[i]);
-        double f[16];  // features.cpp:27-45 layout
-        plan_features(P, H, c, f);
-        double2* o = reinterpret_cast<double2*>(feat + 16 * i);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* t = tr[warp];
+    for (int64_t w0 = (blockIdx.x * int64_t(kFeatT) + threadIdx.x) & ~int64_t(31); w0 < n;
+         w0 += int64_t(gridDim.x) * kFeatT) {
+        const int64_t i = w0 + lane;
+        const int m = int(n - w0 < 32 ? n - w0 : 32);  // candidates of this warp
+        if (i < n) {
+            const Knobs c = load_knobs(P, H, __ldcs(genome + i));
+            double f[16];  // features.cpp:27-45 layout
+            plan_features(P, H, c, f);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) o[j] = make_double2(f[2 * j], f[2 * j + 1]);
-        if (ids) ids[i] = candidate_hash(H.fnv_prefix, c);
+            for (int j = 0; j < 16; ++j) t[lane * 17 + j] = f[j];
+            if (ids) __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
+                            static_cast<unsigned long long>(candidate_hash(H.fnv_prefix, c)));
+        }
+        __syncwarp();
+        // the warp's m rows are m * 16 consecutive doubles of `feat`: lane l stores doubles
+        // 2 (32 r + l), +1 of them (16 bytes), r = 0..7
+        double2* o = reinterpret_cast<double2*>(feat + 16 * w0);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            const int d = 2 * (32 * r + lane);  // first double of the pair in the warp's block
+            const int row = d >> 4, col = d & 15;
+            if (row < m) __stcs(o + 32 * r + lane, make_double2(t[row * 17 + col], t[row * 17 + col + 1]));
+        }
+        __syncwarp();
     }
 }
 
@@ -607,7 +627,13 @@ cudaError_t launch_sim_measure(const LaunchCtx& c, const uint8_t* d_plan, uint32
 }
 cudaError_t launch_features(const LaunchCtx& c, const uint8_t* d_plan, uint32_t bytes, const uint64_t* d_genome,
                             int64_t n, double* d_feat, uint64_t* d_ids) {
-    return launch_plan_kernel(features_kernel, c, d_plan, bytes, n, d_genome, n, d_feat, d_ids);
+    (void)bytes;
+    if (n <= 0) return cudaSuccess;
+    const int64_t want = (n + kFeatT - 1) / kFeatT;
+    const int64_t cap = int64_t(c.sm_count) * 64;
+    features_kernel<<<int(want < cap ? want : cap), kFeatT, 0, c.stream>>>(d_plan, d_genome, n, d_feat, d_ids);
+    note_launches(1);
+    return cudaGetLastError();
 }
 
 template <typename M>
