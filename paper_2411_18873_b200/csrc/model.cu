@@ -79,8 +79,10 @@ __device__ __forceinline__ uint64_t rec_key(double x) {
 // ranks owning ascending, disjoint global index ranges, so the (score, global index) order is the
 // (score key, list, position) order: a record at position j of list w has rank
 //   j + sum over lists w' < w of #(keys <= its key) + sum over lists w' > w of #(keys < its key),
-// each count one binary search.  CTA w ranks list w's k records against every other list staged in
-// shared memory (W * k keys); ranks < k are written.  W CTAs, no merge rounds.
+// each count one binary search.  Every CTA stages the W * k keys in shared memory (16-byte record
+// loads, all in flight); a record gets TPR = pow2 >= W threads, thread v of them searches list v,
+// and the counts meet by shuffles -- one binary search of latency per record instead of W - 1 in
+// sequence.  CTAs split the W * k records (1024 / TPR per CTA); ranks < k are written.
 __device__ __forceinline__ uint32_t count_le(const uint64_t* a, uint32_t n, uint64_t x) {  // upper_bound
     uint32_t lo = 0, hi = n;
     while (lo < hi) {
@@ -100,18 +102,18 @@ __device__ __forceinline__ uint32_t count_lt(const uint64_t* a, uint32_t n, uint
     return lo;
 }
 
-__global__ void __launch_bounds__(1024) merge_records_kernel(const ShardRec* __restrict__ rec, int W, int k,
+__global__ void __launch_bounds__(1024) merge_records_kernel(const ShardRec* __restrict__ rec, int W, int k, int tpr,
                                                              int64_t* __restrict__ idx, double* __restrict__ sc) {
     extern __shared__ unsigned long long msm[];
     uint64_t* keys = reinterpret_cast<uint64_t*>(msm);  // [W][k]
     const int tot = W * k;
-    // 8 independent loads in flight per thread (one dependent round trip per 8 K records, not per record)
+    const double2* r2 = reinterpret_cast<const double2*>(rec);  // {score, index bits}
     for (int base = 0; base < tot; base += 8 * int(blockDim.x)) {
         double v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const int i = base + u * int(blockDim.x) + int(threadIdx.x);
-            v[u] = i < tot ? __ldg(&rec[i].s) : 0.0;
+            v[u] = i < tot ? __ldg(r2 + i).x : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -120,20 +122,23 @@ __global__ void __launch_bounds__(1024) merge_records_kernel(const ShardRec* __r
         }
     }
     __syncthreads();
-    const int w = blockIdx.x;
-    for (int j = threadIdx.x; j < k; j += blockDim.x) {
-        const uint64_t x = keys[w * k + j];
-        uint32_t r = uint32_t(j);
-        // stop as soon as the rank reaches k: deep records leave after one or two searches
-        for (int d = 1; d < W && r < uint32_t(k); ++d) {
-            const int v = (w + d) % W;
-            r += v < w ? count_le(keys + v * k, uint32_t(k), x) : count_lt(keys + v * k, uint32_t(k), x);
-        }
-        if (r < uint32_t(k)) {
-            const ShardRec q = rec[w * k + j];
-            idx[r] = q.g;
-            if (sc) sc[r] = q.s;
-        }
+    const int per_cta = int(blockDim.x) / tpr;
+    const int sub = int(threadIdx.x) % tpr;                          // the list this thread searches
+    const int g = blockIdx.x * per_cta + int(threadIdx.x) / tpr;     // record (list-major)
+    const bool valid = g < tot;
+    const int w = valid ? g / k : 0, j = valid ? g - w * k : 0;
+    const uint64_t x = valid ? keys[g] : 0ull;
+    uint32_t cnt = 0;
+    for (int v = sub; valid && v < W; v += tpr) {
+        if (v == w) continue;
+        cnt += v < w ? count_le(keys + v * k, uint32_t(k), x) : count_lt(keys + v * k, uint32_t(k), x);
+    }
+    for (int o = tpr >> 1; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);  // tpr <= 32 lanes
+    const uint32_t r = cnt + uint32_t(j);
+    if (valid && sub == 0 && r < uint32_t(k)) {
+        const ShardRec q = rec[g];
+        idx[r] = q.g;
+        if (sc) sc[r] = q.s;
     }
 }
 
@@ -222,7 +227,11 @@ cudaError_t launch_merge_records(const LaunchCtx& c, const ShardRec* d_rec, int 
             if (e != cudaSuccess) return e;
             attr = size_t(optin);
         }
-        merge_records_kernel<<<W, 1024, smem, c.stream>>>(d_rec, W, int(k), d_idx, d_sc);
+        int tpr = 1;
+        while (tpr < W && tpr < 32) tpr <<= 1;
+        const int per_cta = 1024 / tpr;
+        merge_records_kernel<<<int((tot + per_cta - 1) / per_cta), 1024, smem, c.stream>>>(d_rec, W, int(k), tpr,
+                                                                                          d_idx, d_sc);
         note_launches(1);
         return cudaGetLastError();
     }
