@@ -63,6 +63,19 @@ constexpr uint64_t kFnvP7 = kFnvP6 * kFnvPrime;
 
 // candidate_id's last two words (space.cpp:43-44): unroll (a power of two <= 2^15: two non-zero
 // bytes at most) and vectorize (one byte), from the state after k_tile
+// fnv_small(h, v) (the four bytes of v, then the four zero bytes of the int64 word) with the zero
+// bytes of a k_tile < 2^16 folded into one multiply by P^6
+__device__ __forceinline__ uint64_t fnv_ktile(uint64_t h, uint32_t v) {
+    h = (h ^ (v & 0xffu)) * kFnvPrime;
+    h = (h ^ ((v >> 8) & 0xffu)) * kFnvPrime;
+    if (v >> 16) {
+        h = (h ^ ((v >> 16) & 0xffu)) * kFnvPrime;
+        h = (h ^ (v >> 24)) * kFnvPrime;
+        return h * kFnvPrime4;
+    }
+    return h * kFnvP6;
+}
+
 __device__ __forceinline__ uint64_t fnv_tail(uint64_t h, uint32_t u, uint32_t v) {
     const uint32_t unroll = 1u << u;
     h = (h ^ (unroll & 0xffu)) * kFnvPrime;
@@ -1107,14 +1120,14 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         gmin = min(gmin, gq[j]);
         if (gq[j] == 0xffffffffu) continue;
         const uint32_t i = base + uint32_t(j) * kSRT + tid;
-        pred[i] = p[j];
+        __stcs(pred + i, p[j]);
         atomicAdd(hist + (gq[j] >> segshift), 1u);
         if (ids) {
             const Genome x = genome_unpack(sgen[j * kSRT + tid]);
             const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
             const uint64_t h = bulk ? skh[key] : __ldg(khash + key);
             __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
-                   static_cast<unsigned long long>(fnv_tail(fnv_small(h, sdivk[x.k]), x.u, x.v)));
+                   static_cast<unsigned long long>(fnv_tail(fnv_ktile(h, sdivk[x.k]), x.u, x.v)));
         }
     }
     SR_TRACE(1);
