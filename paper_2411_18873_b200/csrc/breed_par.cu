@@ -52,8 +52,8 @@ constexpr int kWinT = 256;              // threads per window CTA (>= 156: the g
 constexpr int kWc = 2048;               // starts per window item (chunk-local u16 walker ids)
 constexpr int kRing = 2560;             // stream words staged per window CTA (slot p % kRing)
 constexpr int kRingMargin = 256;        // the ring starts this many words behind the chunk's mean path
-constexpr int kCompact = 8;             // live-list compaction period (steps)
-constexpr int kRingLag = 8;             // cp.async groups in flight per thread
+constexpr int kEpoch = 8;               // steps per epoch: claims, merges, ring slide, compaction once per epoch
+static_assert(kQ % kEpoch == 0, "snapshots fall on epoch ends");
 constexpr int kHash = 4096;             // merge hash slots (>= the live positions' span)
 constexpr int kWcap = 16 * kWc;         // window starts per block at most
 constexpr int kEstK = 4;                // consumption samples per offspring
@@ -526,11 +526,10 @@ __device__ __forceinline__ uint32_t fast_words(const BreedConst& K, const PlanHd
 }
 
 // one window item: every start of a chunk walked through its block at once, merged as walks meet.
-// One barrier per step: positions are double-buffered by step parity (pos[t & 1] -> pos[(t+1) & 1]),
-// so the merge check of step t (which reads the winner's new position) never races the next
-// step's moves; the claim words are tagged with the step, so a stale or early claim can only
-// hide a merge (the walks then stay separate, still exact), never fake one.  The live list is
-// compacted every kCompact steps.
+// One barrier round per epoch of kEpoch steps (not per step): inside an epoch each thread moves its
+// own walkers; at the epoch's end the claim words (tagged with the time, so a stale or early claim
+// can only hide a merge -- the walks then stay separate, still exact -- never fake one) merge the
+// walks standing on the same word, and the live list is compacted.
 __global__ void __launch_bounds__(kWinT, 3)
     breed_win_kernel(const uint8_t* __restrict__ gplan, uint32_t plan_pre, const uint64_t* __restrict__ par,
                      const uint64_t* __restrict__ pid, int64_t np, int64_t n, int S, int B, double mut, double mutcro,
@@ -538,13 +537,13 @@ __global__ void __launch_bounds__(kWinT, 3)
                      const BlockWin* __restrict__ win, uint32_t* __restrict__ endpos, uint16_t* __restrict__ gparent,
                      uint16_t* __restrict__ gmtime, uint2* __restrict__ snapidx, uint64_t* __restrict__ pool,
                      unsigned long long pool_cap, int gen_here, int prof, int check, unsigned long long* err) {
-    // dynamic smem: [ring u64[kRing] | claims u32[kHash] | pos u32[2][kWc] | live u16[2][kWc] |
+    // dynamic smem: [ring u64[kRing] | claims u32[kHash] | pos u32[kWc] | live u16[2][kWc] |
     //                parent u16[kWc] | plan prefix (header, tilings, divisors of K, repair tables)]
     extern __shared__ int4 wsm[];
     uint64_t* ring = reinterpret_cast<uint64_t*>(wsm);
     uint32_t* claims = reinterpret_cast<uint32_t*>(ring + kRing);
     uint32_t* pos = claims + kHash;
-    uint16_t* live0 = reinterpret_cast<uint16_t*>(pos + 2 * kWc);
+    uint16_t* live0 = reinterpret_cast<uint16_t*>(pos + kWc);
     uint16_t* live1 = live0 + kWc;
     uint16_t* parent = live1 + kWc;
     uint8_t* splan = reinterpret_cast<uint8_t*>(parent + kWc);
@@ -601,8 +600,7 @@ __global__ void __launch_bounds__(kWinT, 3)
         live0[w] = uint16_t(w);
     }
     // the ring holds words [base_t, base_t + kRing) (slot p % kRing), base_t on the chunk's mean
-    // path; the slide issued at step s lands (is waited for and crosses a barrier) by step
-    // s + kRingLag + 2, so step t reads the ring only for words below base_{t-kRingLag-2} + kRing
+    // path, slid once per epoch (see the epoch loop for when the slid-in words may be read)
     const uint64_t mfix = uint64_t(mean * 4294967296.0);  // words per offspring, 32.32 fixed point
     auto base_at = [&](int s) -> int64_t {
         return (int64_t(lo) + int64_t((mfix * uint64_t(s)) >> 32) - kRingMargin) & ~int64_t(1);
@@ -620,101 +618,119 @@ __global__ void __launch_bounds__(kWinT, 3)
     uint16_t* nxt = live1;
     uint32_t nlive = Wn;
     unsigned long long t_ready = 0, evals = 0, gloads = 0, ck_sb = 0, ck_a = 0, ck_bar = 0, ck_b = 0;
+    const int nep = (nb + kEpoch - 1) / kEpoch;  // epochs (profile averages are per epoch)
     if (prof) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_ready));
-    int64_t q = i0 % np;  // base parent of offspring i (genetic.cpp:160)
-    uint64_t qg = __ldg(par + q), qid = __ldg(pid + q);
-    for (int t = 0; t < nb; ++t, q = (q + 1 == np) ? 0 : q + 1) {
-        const uint64_t cg = qg, cid = qid;
-        {  // the next step's base parent, a step ahead of use
-            const int64_t qn = (q + 1 == np) ? 0 : q + 1;
-            qg = __ldg(par + qn);
-            qid = __ldg(pid + qn);
-        }
-        const int64_t i = i0 + t;
-        const uint32_t tkey = uint32_t(t) << 16;
-        const int64_t vhi = base_at(t > kRingLag + 2 ? t - kRingLag - 2 : 0) + kRing;
-        const uint32_t* pc = pos + (t & 1) * kWc;
-        uint32_t* pn = pos + ((t + 1) & 1) * kWc;
+    // Epochs of kEpoch steps: every walker of a thread advances through the epoch's steps with no
+    // barrier in between (its position is read and written by its owner only); claims, merges,
+    // the ring slide, compaction and snapshots happen once per epoch.  Walkers that coalesced
+    // inside an epoch are merged at its end -- from then on they are the same walk, and gmtime
+    // records the merge as of the epoch's last step (the emit follows merges at steps < tq).
+    __shared__ uint64_t bpar[2][kEpoch], bpid[2][kEpoch];  // base parents of the epoch's steps
+    if (threadIdx.x < kEpoch && int(threadIdx.x) < nb) {
+        const int64_t q = (i0 + threadIdx.x) % np;  // base parent of offspring i (genetic.cpp:160)
+        bpar[0][threadIdx.x] = __ldg(par + q);
+        bpid[0][threadIdx.x] = __ldg(pid + q);
+    }
+    __syncthreads();
+    uint32_t* P0 = pos;  // one buffer: during an epoch only a walker's owner touches its position
+    int f = 0;
+    for (int t = 0; t < nb; t += kEpoch, ++f) {
+        const int te = min(nb, t + kEpoch);
+        // ring words landed and visible: the slide issued at the end of epoch e is waited for at the
+        // end of epoch e + 1 and crosses that epoch's last barrier, so epoch f reads below
+        // base_{(f-1)E} + kRing (the initial fill covers base_0 + kRing)
+        const int64_t vhi = base_at(f >= 2 ? (f - 1) * kEpoch : 0) + kRing;
+        const int64_t fhi = vhi < int64_t(hiw) ? vhi : int64_t(hiw);
         // a contiguous share of the live list per thread (order-preserving compaction below)
         const uint32_t per = (nlive + kWinT - 1) / kWinT;
         const uint32_t a0 = min(nlive, threadIdx.x * per), a1 = min(nlive, a0 + per);
-        const int64_t fhi = vhi < int64_t(hiw) ? vhi : int64_t(hiw);
+        const uint64_t* bp = bpar[f & 1];
+        const uint64_t* bi = bpid[f & 1];
         long long ck0 = prof ? clock64() : 0;
-        StepBase SB;
-        if (a0 < a1) SB = step_base(H, splan, cg, cid);  // threads without walkers skip the step
-        if (prof && a0 < a1) { ck_sb += uint64_t(SB.g & 1) + uint64_t(clock64() - ck0); }
+        for (int st = t; st < te && a0 < a1; ++st) {
+            const StepBase SB = step_base(H, splan, bp[st - t], bi[st - t]);
+            const int64_t i = i0 + st;
+            for (uint32_t a = a0; a < a1; ++a) {
+                const uint32_t w = cur[a];
+                if (parent[w] != w) continue;  // merged at an earlier epoch
+                const uint32_t p0 = P0[w];
+                if (p0 == kGone) continue;
+                uint32_t fw = 0;
+                if (int64_t(p0) >= base && int64_t(p0) + 6 <= fhi) {
+                    const Words6 wv{ring[p0 % kRing], ring[(p0 + 1) % kRing], ring[(p0 + 2) % kRing],
+                                    ring[(p0 + 3) % kRing], ring[(p0 + 4) % kRing], ring[(p0 + 5) % kRing]};
+                    fw = fast_words(K, H, SB, wv);
+                }
+                if (prof) {
+                    ++evals;
+                    if (fw == 0) ++gloads;
+                }
+                if (fw == 0 || check) {
+                    RCursor c{ring, stream, base, vhi, p0, hiw, true};
+                    const Child ch = breed_body(K, H, i, c, p0);
+                    if (fw != 0 && uint64_t(p0) + fw != c.p)  // diagnostic: the fast count disagrees
+                        atomicMin(err, (static_cast<unsigned long long>(i) << 8) | unsigned(ETUNE_ERR_CONSISTENCY));
+                    if (ch.words == kUnknown || ch.words == kIllegal) {
+                        endpos[woff + w] = ch.words == kIllegal ? kFateIllegal : kFateUnknown;
+                        P0[w] = kGone;
+                        continue;
+                    }
+                    fw = uint32_t(c.p - p0);
+                }
+                P0[w] = p0 + fw;
+            }
+        }
+        // claims at the epoch's end: the lowest walker on a word (hash slot, tagged by the time)
+        const uint32_t tkey = uint32_t(te) << 16;
         for (uint32_t a = a0; a < a1; ++a) {
             const uint32_t w = cur[a];
-            if (parent[w] != w) continue;  // merged since the last compaction
-            const uint32_t p0 = pc[w];
-            if (p0 == kGone) {
-                pn[w] = kGone;
-                continue;
-            }
-            uint32_t fw = 0;
-            if (int64_t(p0) >= base && int64_t(p0) + 6 <= fhi) {
-                const Words6 wv{ring[p0 % kRing], ring[(p0 + 1) % kRing], ring[(p0 + 2) % kRing],
-                                ring[(p0 + 3) % kRing], ring[(p0 + 4) % kRing], ring[(p0 + 5) % kRing]};
-                fw = fast_words(K, H, SB, wv);
-            }
-            if (prof) {
-                ++evals;
-                if (fw == 0) ++gloads;
-            }
-            if (fw == 0 || check) {
-                RCursor c{ring, stream, base, vhi, p0, hiw, true};
-                const Child ch = breed_body(K, H, i, c, p0);
-                if (fw != 0 && uint64_t(p0) + fw != c.p)  // diagnostic: the fast count disagrees
-                    atomicMin(err, (static_cast<unsigned long long>(i) << 8) | unsigned(ETUNE_ERR_CONSISTENCY));
-                if (ch.words == kUnknown || ch.words == kIllegal) {
-                    endpos[woff + w] = ch.words == kIllegal ? kFateIllegal : kFateUnknown;
-                    pn[w] = kGone;
-                    continue;
-                }
-                fw = uint32_t(c.p - p0);
-            }
-            const uint32_t p1 = p0 + fw;
-            pn[w] = p1;
-            atomicMax(claims + (p1 & (kHash - 1)), tkey | (0xffffu - w));
+            if (parent[w] != w) continue;
+            const uint32_t p1 = P0[w];
+            if (p1 != kGone) atomicMax(claims + (p1 & (kHash - 1)), tkey | (0xffffu - w));
+        }
+        if (threadIdx.x < kEpoch && te + int(threadIdx.x) < nb) {  // the next epoch's base parents
+            const int64_t q = (i0 + te + threadIdx.x) % np;
+            bpar[(f + 1) & 1][threadIdx.x] = __ldg(par + q);
+            bpid[(f + 1) & 1][threadIdx.x] = __ldg(pid + q);
         }
         long long ck1 = prof ? clock64() : 0;
         __syncthreads();
         long long ck2 = prof ? clock64() : 0;
         if (prof) { ck_a += uint64_t(ck1 - ck0); ck_bar += uint64_t(ck2 - ck1); }
-        // slide the ring along the mean path (the words entering it are read hundreds of steps later)
-        const int64_t nbase = base_at(t + 1);
+        // slide the ring along the mean path (the words entering it are read epochs later)
+        const int64_t nbase = base_at(te);
         if (nbase > base) {
             for (int64_t p = base + kRing + 2 * int64_t(threadIdx.x); p < nbase + kRing; p += 2 * blockDim.x)
                 if (p >= 0 && uint64_t(p) < hiw) cp_async16(ring + uint32_t(p) % kRing, stream + p);
             base = nbase;
         }
         cp_async_commit();
-        cp_async_wait<kRingLag>();
+        cp_async_wait<1>();
         uint32_t keep = 0;
         for (uint32_t a = a0; a < a1; ++a) {
             const uint32_t w = cur[a];
             if (parent[w] != w) continue;
-            const uint32_t p1 = pn[w];
+            const uint32_t p1 = P0[w];
             if (p1 == kGone) continue;
             const uint32_t k = claims[p1 & (kHash - 1)];
             const uint32_t ww = 0xffffu - (k & 0xffffu);
-            // the winner claimed at this step (tag) and stands on the same word: the same walk from here
-            if ((k >> 16) == uint32_t(t) && ww != w && pn[ww] == p1) {
+            // the winner claimed at this time and stands on the same word: the same walk from here
+            if ((k >> 16) == uint32_t(te) && ww != w && P0[ww] == p1) {
                 parent[w] = uint16_t(ww);
                 gparent[woff + w] = uint16_t(ww);
-                gmtime[woff + w] = uint16_t(t);
+                gmtime[woff + w] = uint16_t(te - 1);
                 continue;
             }
             ++keep;
         }
         if (prof) ck_b += uint64_t(clock64() - ck2);
-        const bool snap = ((t + 1) % kQ) == 0 && t + 1 < nb;
-        if (((t + 1) % kCompact) == 0 || snap) {
+        const bool snap = (te % kQ) == 0 && te < nb;
+        {
             uint32_t tot;
             uint32_t o = block_scan_u32(keep, &tot, ws);  // (ends with a barrier)
             for (uint32_t a = a0; a < a1; ++a) {
                 const uint32_t w = cur[a];
-                if (parent[w] != w || pn[w] == kGone) continue;
+                if (parent[w] != w || P0[w] == kGone) continue;
                 nxt[o++] = uint16_t(w);
             }
             __syncthreads();
@@ -722,18 +738,18 @@ __global__ void __launch_bounds__(kWinT, 3)
             cur = nxt;
             nxt = sw;
             nlive = tot;
-            if (snap) {  // snapshot of the live walkers (w ascending) at time t + 1
+            if (snap) {  // snapshot of the live walkers (w ascending) at time te
                 if (threadIdx.x == 0) {
                     const unsigned long long ob = atomicAdd(&hdr->snap_used, (unsigned long long)tot);
                     s_base = (ob + tot <= pool_cap) ? uint32_t(ob) : 0xffffffffu;
-                    snapidx[size_t(item) * nsub + (t + 1) / kQ] = make_uint2(s_base, tot);
+                    snapidx[size_t(item) * nsub + te / kQ] = make_uint2(s_base, tot);
                 }
                 __syncthreads();
                 const uint32_t sb = s_base;
                 if (sb != 0xffffffffu)
                     for (uint32_t a = threadIdx.x; a < tot; a += blockDim.x) {
                         const uint32_t w = cur[a];
-                        pool[sb + a] = ((unsigned long long)w << 32) | pn[w];
+                        pool[sb + a] = ((unsigned long long)w << 32) | P0[w];
                     }
             }
         }
@@ -753,10 +769,10 @@ __global__ void __launch_bounds__(kWinT, 3)
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
             asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
             printf("ITEM %d %d %u %u %llu %llu %llu %llu %llu %u %llu %llu %llu %llu\n", item, b, Wn, smid, t_start, t_ready,
-                   t_end, s_ev, s_gl, nlive, ck_sb / nb, ck_a / nb, ck_bar / nb, ck_b / nb);
+                   t_end, s_ev, s_gl, nlive, ck_sb / nep, ck_a / nep, ck_bar / nep, ck_b / nep);
         }
     }
-    const uint32_t* pf = pos + (nb & 1) * kWc;
+    const uint32_t* pf = pos;  // positions at time nb
     for (uint32_t a = threadIdx.x; a < nlive; a += blockDim.x) {
         const uint32_t w = cur[a];
         if (parent[w] == w && pf[w] != kGone) endpos[woff + w] = pf[w];
@@ -1011,7 +1027,7 @@ cudaError_t launch_breed_par(const LaunchCtx& c, const uint8_t* d_plan, uint32_t
                                                       l.est);
     const size_t cap = words_cap > 0 && words_cap < l.words ? words_cap : l.words;
     breed_plan_kernel<<<1, 1024, 0, c.stream>>>(l.est, B, S, n, uint64_t(cap), sd_mult, l.win, l.hdr);
-    const size_t win_dyn = size_t(kRing) * 8 + size_t(kHash) * 4 + size_t(kWc) * (8 + 4 + 2) + plan_pre;
+    const size_t win_dyn = size_t(kRing) * 8 + size_t(kHash) * 4 + size_t(kWc) * (4 + 4 + 2) + plan_pre;
     static_assert(size_t(kRing) >= 4 * 160 + 312, "the generator's half-blocks live in the ring");
     e = cudaFuncSetAttribute(breed_win_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(win_dyn));
     if (e != cudaSuccess) return e;

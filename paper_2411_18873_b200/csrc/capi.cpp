@@ -1727,9 +1727,9 @@ int64_t breed_par_min() {
     if (const char* e = std::getenv("ETUNE_BREED_PAR_MIN")) return int64_t(std::atoll(e));
     return int64_t(4096);
 }
-double breed_par_sd() {
+double breed_par_sd() {  // P(|Z| > 4) = 6.3e-5 per block: a 2^20 generation walks ~0.03 blocks exactly
     if (const char* e = std::getenv("ETUNE_BREED_PAR_SD")) return std::atof(e);
-    return 5.0;
+    return 4.0;
 }
 size_t breed_par_words() {
     if (const char* e = std::getenv("ETUNE_BREED_PAR_WORDS")) return size_t(std::atoll(e));
