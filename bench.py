@@ -162,7 +162,7 @@ def time_cpu(op, sched, target_s: float, k: int):
 
 class ClockSampler:
     """SM clocks + throttle reasons sampled through NVML during the timed region
-    (a background thread every 5 ms, plus explicit samples at its start and end)."""
+    (a background thread every 1 ms, plus explicit samples at its start and end)."""
 
     REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
                "sw_power_cap": 0x4}
@@ -194,7 +194,7 @@ class ClockSampler:
             pass
 
     def _loop(self):
-        while not self.stop.wait(0.005):
+        while not self.stop.wait(0.001):
             self.sample()
 
     def __enter__(self):
