@@ -52,7 +52,7 @@ constexpr int kWinT = 256;              // threads per window CTA (>= 156: the g
 constexpr int kWc = 2048;               // starts per window item (chunk-local u16 walker ids)
 constexpr int kRing = 2560;             // stream words staged per window CTA (slot p % kRing)
 constexpr int kRingMargin = 256;        // the ring starts this many words behind the chunk's mean path
-constexpr int kEpoch = 8;               // steps per epoch: claims, merges, ring slide, compaction once per epoch
+constexpr int kEpoch = 16;              // steps per epoch: claims, merges, ring slide, compaction once per epoch
 static_assert(kQ % kEpoch == 0, "snapshots fall on epoch ends");
 constexpr int kHash = 4096;             // merge hash slots (>= the live positions' span)
 constexpr int kWcap = 16 * kWc;         // window starts per block at most
