@@ -35,6 +35,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "breed_core.cuh"
 #include "etune_internal.hpp"
@@ -625,11 +626,11 @@ __global__ void __launch_bounds__(kWinT, 3)
     // the ring slide, compaction and snapshots happen once per epoch.  Walkers that coalesced
     // inside an epoch are merged at its end -- from then on they are the same walk, and gmtime
     // records the merge as of the epoch's last step (the emit follows merges at steps < tq).
-    __shared__ uint64_t bpar[2][kEpoch], bpid[2][kEpoch];  // base parents of the epoch's steps
+    __shared__ StepBase sbase[2][kEpoch];  // the epoch's base parents, prepared once per step
     if (threadIdx.x < kEpoch && int(threadIdx.x) < nb) {
         const int64_t q = (i0 + threadIdx.x) % np;  // base parent of offspring i (genetic.cpp:160)
-        bpar[0][threadIdx.x] = __ldg(par + q);
-        bpid[0][threadIdx.x] = __ldg(pid + q);
+        sbase[0][threadIdx.x] = step_base(*reinterpret_cast<const PlanHdr*>(splan), splan, __ldg(par + q),
+                                          __ldg(pid + q));
     }
     __syncthreads();
     uint32_t* P0 = pos;  // one buffer: during an epoch only a walker's owner touches its position
@@ -644,11 +645,10 @@ __global__ void __launch_bounds__(kWinT, 3)
         // a contiguous share of the live list per thread (order-preserving compaction below)
         const uint32_t per = (nlive + kWinT - 1) / kWinT;
         const uint32_t a0 = min(nlive, threadIdx.x * per), a1 = min(nlive, a0 + per);
-        const uint64_t* bp = bpar[f & 1];
-        const uint64_t* bi = bpid[f & 1];
+        const StepBase* sb = sbase[f & 1];
         long long ck0 = prof ? clock64() : 0;
         for (int st = t; st < te && a0 < a1; ++st) {
-            const StepBase SB = step_base(H, splan, bp[st - t], bi[st - t]);
+            const StepBase SB = sb[st - t];
             const int64_t i = i0 + st;
             for (uint32_t a = a0; a < a1; ++a) {
                 const uint32_t w = cur[a];
@@ -657,8 +657,9 @@ __global__ void __launch_bounds__(kWinT, 3)
                 if (p0 == kGone) continue;
                 uint32_t fw = 0;
                 if (int64_t(p0) >= base && int64_t(p0) + 6 <= fhi) {
-                    const Words6 wv{ring[p0 % kRing], ring[(p0 + 1) % kRing], ring[(p0 + 2) % kRing],
-                                    ring[(p0 + 3) % kRing], ring[(p0 + 4) % kRing], ring[(p0 + 5) % kRing]};
+                    const uint32_t r0 = p0 % kRing;  // slots r0 .. r0 + 5, wrapping once at most
+                    auto slot = [&](uint32_t d) { const uint32_t r = r0 + d; return r < kRing ? r : r - kRing; };
+                    const Words6 wv{ring[r0], ring[slot(1)], ring[slot(2)], ring[slot(3)], ring[slot(4)], ring[slot(5)]};
                     fw = fast_words(K, H, SB, wv);
                 }
                 if (prof) {
@@ -690,8 +691,7 @@ __global__ void __launch_bounds__(kWinT, 3)
         }
         if (threadIdx.x < kEpoch && te + int(threadIdx.x) < nb) {  // the next epoch's base parents
             const int64_t q = (i0 + te + threadIdx.x) % np;
-            bpar[(f + 1) & 1][threadIdx.x] = __ldg(par + q);
-            bpid[(f + 1) & 1][threadIdx.x] = __ldg(pid + q);
+            sbase[(f + 1) & 1][threadIdx.x] = step_base(H, splan, __ldg(par + q), __ldg(pid + q));
         }
         long long ck1 = prof ? clock64() : 0;
         __syncthreads();
@@ -1035,6 +1035,11 @@ cudaError_t launch_breed_par(const LaunchCtx& c, const uint8_t* d_plan, uint32_t
     if (e != cudaSuccess) return e;
     const bool split = split_gen & 1;
     const int prof = (split_gen >> 1) & 1;  // diagnostic: per-item timing printed by the device
+    if (prof) {
+        int occ = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, breed_win_kernel, kWinT, win_dyn);
+        std::printf("WIN smem %zu B (plan prefix %u), %d CTAs/SM\n", win_dyn, plan_pre, occ);
+    }
     if (split) breed_gen_kernel<<<1, 256, 0, c.stream>>>(seed, l.stream, l.hdr);
     // grid: every possible item + the generator; CTAs beyond the plan's items exit at once
     breed_win_kernel<<<unsigned(l.items_max + 1), kWinT, win_dyn, c.stream>>>(
