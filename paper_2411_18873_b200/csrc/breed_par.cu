@@ -418,15 +418,40 @@ __device__ __forceinline__ StepBase step_base(const PlanHdr& H, const uint8_t* P
     return B;
 }
 
+// The coin of genetic.cpp:162 (uniform_real_distribution<double>(0,1) * total, exactly as
+// breed_body computes it) is monotone in the word w0, so "u < x" is "w0 < T(x)": the two cuts
+// (mutation, mutation + crossover) are found once per CTA by bisection on w0 and the walkers
+// compare integers.
+__device__ __forceinline__ double coin_u(uint64_t w0, double total) {
+    const double coin = __dmul_rn(__ull2double_rn(w0), 0x1p-64);
+    return __dmul_rn(coin < 1.0 ? coin : 0x1.fffffffffffffp-1, total);
+}
+struct CoinCut {
+    uint64_t t_mc, t_m;  // u < mutcro iff all_mc or w0 < t_mc; u < mut iff all_m or w0 < t_m
+    int all_mc, all_m;
+};
+__device__ void coin_cut(double x, double total, uint64_t* t, int* all) {
+    if (coin_u(~0ull, total) < x) {
+        *all = 1;
+        *t = ~0ull;
+        return;
+    }
+    uint64_t lo = 0, hi = ~0ull;  // coin_u(hi) >= x
+    while (lo < hi) {
+        const uint64_t mid = lo + ((hi - lo) >> 1);
+        if (coin_u(mid, total) >= x) hi = mid;
+        else lo = mid + 1;
+    }
+    *all = 0;
+    *t = lo;
+}
+
 __device__ __forceinline__ uint32_t fast_words(const BreedConst& K, const PlanHdr& H, const StepBase& B,
-                                               const Words6& w) {
-    // uniform_real_distribution<double>(0,1) * total (genetic.cpp:162), exactly as breed_body
-    const double coin = __dmul_rn(__ull2double_rn(w.w0), 0x1p-64);
-    const double u = __dmul_rn(coin < 1.0 ? coin : 0x1.fffffffffffffp-1, K.total);
-    if (!(u < K.mutcro)) return 1u;  // copy
+                                               const CoinCut& C, const Words6& w) {
+    if (!(C.all_mc || w.w0 < C.t_mc)) return 1u;  // copy
     Genome x = genome_unpack(B.g);
     uint32_t s;
-    if (u < K.mut) {  // mutate_knob (genetic.cpp:60-87)
+    if (C.all_m || w.w0 < C.t_m) {  // mutate_knob (genetic.cpp:60-87)
         if (w.w1 * 6ull < 6ull) return 0u;
         const uint32_t knob = uint32_t(__umul64hi(w.w1, 6ull));
         uint32_t m = uint32_t(H.nt[0]), a = x.t0;
@@ -487,7 +512,7 @@ __device__ __forceinline__ uint32_t fast_words(const BreedConst& K, const PlanHd
         if (th2 > tm) { dim = 2; tm = th2; }
         const uint64_t other = dim == 0 ? th1 * th2 : (dim == 1 ? th0 * th2 : th0 * th1);
         if (int64_t(other) > cap) return 0u;  // no tiling fits: {extent,1,1} and another round
-        const int64_t lim = cap / int64_t(other);
+        const int64_t lim = int64_t(uint32_t(cap) / uint32_t(other));  // cap <= 1024, other <= cap here
         const uint8_t* F = K.P + (dim == 0 ? H.off_fit[0] : (dim == 1 ? H.off_fit[1] : H.off_fit[2]));
         const int ntv = reinterpret_cast<const FitHeader*>(F)->ntv;
         const uint32_t* tv = reinterpret_cast<const uint32_t*>(F + sizeof(FitHeader));
@@ -627,12 +652,18 @@ __global__ void __launch_bounds__(kWinT, 3)
     // inside an epoch are merged at its end -- from then on they are the same walk, and gmtime
     // records the merge as of the epoch's last step (the emit follows merges at steps < tq).
     __shared__ StepBase sbase[2][kEpoch];  // the epoch's base parents, prepared once per step
+    __shared__ CoinCut s_cut;
+    if (threadIdx.x == 0) {
+        coin_cut(mutcro, total, &s_cut.t_mc, &s_cut.all_mc);
+        coin_cut(mut, total, &s_cut.t_m, &s_cut.all_m);
+    }
     if (threadIdx.x < kEpoch && int(threadIdx.x) < nb) {
         const int64_t q = (i0 + threadIdx.x) % np;  // base parent of offspring i (genetic.cpp:160)
         sbase[0][threadIdx.x] = step_base(*reinterpret_cast<const PlanHdr*>(splan), splan, __ldg(par + q),
                                           __ldg(pid + q));
     }
     __syncthreads();
+    const CoinCut CC = s_cut;
     uint32_t* P0 = pos;  // one buffer: during an epoch only a walker's owner touches its position
     int f = 0;
     for (int t = 0; t < nb; t += kEpoch, ++f) {
@@ -660,7 +691,7 @@ __global__ void __launch_bounds__(kWinT, 3)
                     const uint32_t r0 = p0 % kRing;  // slots r0 .. r0 + 5, wrapping once at most
                     auto slot = [&](uint32_t d) { const uint32_t r = r0 + d; return r < kRing ? r : r - kRing; };
                     const Words6 wv{ring[r0], ring[slot(1)], ring[slot(2)], ring[slot(3)], ring[slot(4)], ring[slot(5)]};
-                    fw = fast_words(K, H, SB, wv);
+                    fw = fast_words(K, H, SB, CC, wv);
                 }
                 if (prof) {
                     ++evals;
