@@ -1166,7 +1166,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         if (wact) {
 #pragma unroll
             for (int j = 0; j < kSRPer; ++j) {
-                const uint32_t g = j < per ? sgg[j * kSRT + tid] : 0xffffffffu;
+                const uint32_t g = j < per ? gq[j] : 0xffffffffu;  // still in registers
                 const uint32_t sg = g >> segshift;
                 if (g != 0xffffffffu) {
                     if (sg < b0) ml |= 1u << j;
@@ -1215,7 +1215,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             const unsigned bb = __ballot_sync(0xffffffffu, (mb >> j) & 1u);
             const unsigned bl = __ballot_sync(0xffffffffu, (ml >> j) & 1u);
             if ((mb >> j) & 1u)
-                sb0[S.jw[j * 32 + warp] + __popc(bb & lt)] = (uint32_t(j * kSRT + tid) << 19) | (sgg[j * kSRT + tid] & qmask);
+                sb0[S.jw[j * 32 + warp] + __popc(bb & lt)] = (uint32_t(j * kSRT + tid) << 19) | (gq[j] & qmask);
             if ((ml >> j) & 1u) {
                 const uint32_t off = loff + __popc(bl & lt);
                 if (off < uint32_t(kSRListCap)) {
