@@ -485,6 +485,42 @@ def run_ours(args):
         dist.barrier()
     value = world * n / (ms / 1e3)
 
+    # ---- score only (SURVEY §8(d) "scored" = features -> prediction, no keep-the-best): etune_cu_score on the
+    # row table, the same population and outputs, from a CUDA graph like the step
+    score_only = None
+    if world == 1:
+        def sstep(i):
+            b = i % nb
+            forest.score(plan, genomes[b], out=preds[b], ids_out=ids[b])
+
+        for i in range(3):
+            sstep(i)
+        torch.cuda.synchronize()
+        sg2 = None
+        if use_graph:
+            sg2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(sg2, stream=stream):
+                for i in range(args.steps):
+                    sstep(i)
+            sg2.replay()
+            torch.cuda.synchronize()
+        se0, se1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        se0.record(stream)
+        if sg2 is not None:
+            sg2.replay()
+        else:
+            for i in range(args.steps):
+                sstep(i)
+        se1.record(stream)
+        torch.cuda.synchronize()
+        sms = se0.elapsed_time(se1) / args.steps
+        del sg2
+        score_only = {"value": n / (sms / 1e3), "unit": UNIT, "ms_per_step": sms,
+                      "what": "etune_cu_score (row table: genome -> prediction + candidate_id, no selection) over the "
+                              "bench population, the K steps from a CUDA graph",
+                      "roofline": {"bound": "hbm", "achieved": n * ALGO_BYTES / (sms / 1e3) / 1e9, "unit": "GB/s",
+                                   "algorithmic_bytes_per_candidate": ALGO_BYTES}}
+
     # ---- feature mode: etune_cu_features, genome -> 16 f64 features + id; HBM-bound
     feature_mode = None
     if world == 1:
@@ -701,6 +737,10 @@ def run_ours(args):
         "eager_ms_per_step": eager_ms,
         "clocks": clocks,
     }
+    if score_only:
+        score_only["roofline"]["peak"] = hbm
+        score_only["roofline"]["frac"] = score_only["roofline"]["achieved"] / hbm
+        line["score_only"] = score_only
     if feature_mode:
         fr = feature_mode["roofline"]
         fr["peak"] = hbm
