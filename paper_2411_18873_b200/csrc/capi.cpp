@@ -837,10 +837,6 @@ etune_status etune_cu_plan_create(etune_cu_ctx* c, const etune_op_spec* op, cons
             CU(cudaMalloc(&p->d_khk, size_t(nkeys) * size_t(H.ndk) * 8));
             CU(cudaMalloc(&p->d_khash, size_t(nkeys + 2) * 8));  // + padding: whole 16-byte bulk copies
             CU(launch_key_hash(c->lc(), p->d_blob, nkeys, p->d_khk, p->d_khash));
-            if (H.ndk <= 1024 && nkeys * 80 <= (int64_t(64) << 20)) {  // feature mode's per-key records
-                CU(cudaMalloc(&p->d_kfeat, size_t(nkeys) * 80));
-                CU(launch_key_features(c->lc(), p->d_blob, nkeys, p->d_khash, p->d_kfeat));
-            }
         }
     }
     CU(cudaStreamSynchronize(c->stream));
@@ -877,7 +873,6 @@ etune_status etune_cu_plan_destroy(etune_cu_plan* p) {
     cudaStreamSynchronize(c->stream);  // kernels still reading the plan's tables
     cudaFree(p->d_khash);
     cudaFree(p->d_khk);
-    cudaFree(p->d_kfeat);
     cudaFree(p->d_blob);
     delete p;
     ctx_release(c);
@@ -988,11 +983,7 @@ etune_status etune_cu_counters(etune_cu_ctx* c, const etune_cu_plan* p, const ui
 etune_status etune_cu_features(etune_cu_ctx* c, const etune_cu_plan* p, const uint64_t* d_genome, int64_t n,
                                double* d_feat, uint64_t* d_ids) {
     CHECK_PLAN_ARGS(d_feat && d_genome);
-    // ETUNE_FEATURES_TABLE=0 (diagnostic, read per call): the table-lookup kernel even when the records exist
-    const char* ft = std::getenv("ETUNE_FEATURES_TABLE");
-    const bool records = p->d_kfeat && !(ft && ft[0] == '0');
-    if (records) CU(launch_features_key(c->lc(), p->d_blob, p->d_kfeat, d_genome, n, d_feat, d_ids));
-    else CU(launch_features(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_feat, d_ids));
+    CU(launch_features(c->lc(), p->d_blob, p->build.hdr.total, d_genome, n, d_feat, d_ids));
     return ETUNE_OK;
 }
 

@@ -87,7 +87,6 @@ struct etune_cu_plan {
     // (0: the operator's row table would be too large, the form is not offered)
     uint64_t* d_khash = nullptr;  // per key: after the three tilings
     uint64_t* d_khk = nullptr;    // per (key, k_tile index): after k_tile as well
-    double* d_kfeat = nullptr;    // per key: the 9 tiling-dependent features + the FNV state (feature mode)
     int64_t nkeys = 0, kuv_domain = 0, rows_cap = 0;
 };
 

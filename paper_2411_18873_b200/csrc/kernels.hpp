@@ -100,11 +100,6 @@ int64_t rowtab_kuv_domain(const int64_t* divk, int ndk);
 size_t rowtab_scratch_bytes(int nnodes);
 // candidate_id's FNV state per (tiling-triple key, k_tile index) after k_tile (d_khk, nkeys * ndk)
 // and per key after the three tilings (d_khash, nkeys)
-// feature mode on per-key records (plan creation: launch_key_features, nkeys x 10 words)
-cudaError_t launch_key_features(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, const uint64_t* d_khash,
-                                double* d_kfeat);
-cudaError_t launch_features_key(const LaunchCtx& c, const uint8_t* d_plan, const double* d_kfeat,
-                                const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids);
 cudaError_t launch_key_hash(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, uint64_t* d_khk,
                             uint64_t* d_khash);
 // d_clskuv: ndk * 64 u16; d_crep: one u32 per class (<= rowtab_kuv_domain); d_rowpred: rows_cap doubles

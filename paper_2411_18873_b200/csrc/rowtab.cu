@@ -399,110 +399,6 @@ __global__ void key_hash_kernel(const uint8_t* __restrict__ P, int64_t nkeys, ui
     }
 }
 
-// ------------------------------------------------------------ feature mode
-// Per tiling-triple key, the features that depend on the three tilings only (features.cpp:27-45:
-// f1 = f4 int ops, f2 = f5 global loads, f8 levels, f9 per-thread n, f11 grid, f12 block, f13
-// efficiency, f14 active SMs, f15 intensity) and candidate_id's FNV state after the tilings:
-// ten 8-byte words, the reference's values computed once per key by plan_features itself.
-constexpr int kKeyFeatWords = 10;
-__global__ void key_feat_kernel(const uint8_t* __restrict__ P, int64_t nkeys, const uint64_t* __restrict__ khash,
-                                double* __restrict__ out) {
-    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(P);
-    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
-    for (int64_t key = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; key < nkeys;
-         key += int64_t(gridDim.x) * blockDim.x) {
-        Knobs c;
-        c.r[0] = at<TilingRec>(P, H.off_til[0])[uint32_t(key / (int64_t(nt1) * nt2))];
-        c.r[1] = at<TilingRec>(P, H.off_til[1])[uint32_t((key / nt2) % nt1)];
-        c.r[2] = at<TilingRec>(P, H.off_til[2])[uint32_t(key % nt2)];
-        c.k = 0;
-        c.k_tile = at<int64_t>(P, H.off_divk)[0];
-        c.unroll = 1;
-        c.vec = 1;
-        double f[16];
-        plan_features(P, H, c, f);
-        double* o = out + key * kKeyFeatWords;
-        o[0] = f[1];
-        o[1] = f[2];
-        o[2] = f[8];
-        o[3] = f[9];
-        o[4] = f[11];
-        o[5] = f[12];
-        o[6] = f[13];
-        o[7] = f[14];
-        o[8] = f[15];
-        o[9] = __longlong_as_double(static_cast<long long>(khash[key]));
-    }
-}
-
-// Feature mode on the per-key records: genome -> one 80-byte record (5 x 16-byte loads of one
-// L2-resident line pair) + f10 and k_tile from shared memory + f6 / f7 / f0 / f3 -> the 16
-// features (and the id from the record's FNV state); a warp's rows leave through the shared-memory
-// transpose as coalesced 16-byte stores.
-constexpr int kKFT = 256;
-__global__ void __launch_bounds__(kKFT, 4) features_key_kernel(const uint8_t* __restrict__ gplan,
-                                                               const double2* __restrict__ kfeat,
-                                                               const uint64_t* __restrict__ genome, int64_t n,
-                                                               double* __restrict__ feat, uint64_t* __restrict__ ids) {
-    extern __shared__ int4 ksm[];
-    double* ssteps = reinterpret_cast<double*>(ksm);           // [ndk]
-    uint32_t* sdiv = reinterpret_cast<uint32_t*>(ssteps + 1024);  // [ndk]
-    __shared__ double tr[kKFT / 32][32 * 17];
-    const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
-    const int ndk = H.ndk;
-    const uint32_t nt1 = uint32_t(H.nt[1]), nt2 = uint32_t(H.nt[2]);
-    const double f0 = H.f0, f3 = H.f3;
-    for (int i = threadIdx.x; i < ndk; i += kKFT) {
-        ssteps[i] = at<double>(gplan, H.off_steps)[i];
-        sdiv[i] = uint32_t(at<int64_t>(gplan, H.off_divk)[i]);
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double* t = tr[warp];
-    for (int64_t w0 = (blockIdx.x * int64_t(kKFT) + threadIdx.x) & ~int64_t(31); w0 < n;
-         w0 += int64_t(gridDim.x) * kKFT) {
-        const int64_t i = w0 + lane;
-        const int m = int(n - w0 < 32 ? n - w0 : 32);
-        if (i < n) {
-            const Genome x = genome_unpack(__ldcs(genome + i));
-            const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
-            const double2* r = kfeat + size_t(key) * (kKeyFeatWords / 2);
-            const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
-            double* row = t + lane * 17;
-            row[0] = f0;
-            row[1] = a.x;
-            row[2] = a.y;
-            row[3] = f3;
-            row[4] = a.x;
-            row[5] = a.y;
-            row[6] = static_cast<double>(1u << x.v);
-            row[7] = static_cast<double>(1u << x.u);
-            row[8] = b.x;
-            row[9] = b.y;
-            row[10] = ssteps[x.k];
-            row[11] = c.x;
-            row[12] = c.y;
-            row[13] = d.x;
-            row[14] = d.y;
-            row[15] = e.x;
-            if (ids) {
-                const uint64_t h = static_cast<uint64_t>(__double_as_longlong(e.y));
-                __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
-                       static_cast<unsigned long long>(fnv_tail(fnv_ktile(h, sdiv[x.k]), x.u, x.v)));
-            }
-        }
-        __syncwarp();
-        double2* o = reinterpret_cast<double2*>(feat + 16 * w0);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int dd = 2 * (32 * q + lane);
-            const int row = dd >> 4, col = dd & 15;
-            if (row < m) __stcs(o + 32 * q + lane, make_double2(t[row * 17 + col], t[row * 17 + col + 1]));
-        }
-        __syncwarp();
-    }
-}
-
 // ------------------------------------------------------------------- scoring
 constexpr int kRowsT = 512;
 constexpr int kRowsPer = 4;  // candidates per thread per pass (independent gathers in flight)
@@ -1500,28 +1396,6 @@ cudaError_t launch_key_hash(const LaunchCtx& c, const uint8_t* d_plan, int64_t n
     const int64_t want = (nkeys * 64 + 255) / 256;
     const int grid = int(want < int64_t(c.sm_count) * 4 ? want : int64_t(c.sm_count) * 4);
     key_hash_kernel<<<grid, 256, 0, c.stream>>>(d_plan, nkeys, d_khk, d_khash);
-    note_launches(1);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_key_features(const LaunchCtx& c, const uint8_t* d_plan, int64_t nkeys, const uint64_t* d_khash,
-                                double* d_kfeat) {
-    if (nkeys <= 0) return cudaSuccess;
-    const int64_t want = (nkeys + 255) / 256;
-    const int grid = int(want < int64_t(c.sm_count) * 4 ? want : int64_t(c.sm_count) * 4);
-    key_feat_kernel<<<grid, 256, 0, c.stream>>>(d_plan, nkeys, d_khash, d_kfeat);
-    note_launches(1);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_features_key(const LaunchCtx& c, const uint8_t* d_plan, const double* d_kfeat,
-                                const uint64_t* d_genome, int64_t n, double* d_feat, uint64_t* d_ids) {
-    if (n <= 0) return cudaSuccess;
-    const size_t sm = 1024 * 8 + 1024 * 4;  // steps and k_tile words for ndk <= 1024
-    const int64_t want = (n + kKFT - 1) / kKFT;
-    const int64_t cap = int64_t(c.sm_count) * 64;
-    features_key_kernel<<<int(want < cap ? want : cap), kKFT, sm, c.stream>>>(
-        d_plan, reinterpret_cast<const double2*>(d_kfeat), d_genome, n, d_feat, d_ids);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -287,22 +287,3 @@ def test_topk_fast_path_and_fallback(oracle, ctx, capi, kind, n, k):
     idx = capi.topk(ctx, dev(vals), k)
     ctx.synchronize()
     assert (idx.cpu().numpy() == oracle.topk(vals, k)).all()
-
-
-@pytest.mark.parametrize("text", ["conv:1,56,56,64,64,3,1,1", "mm:1,512,3072,768", "mm:1,1024,1024,1024"])
-def test_feature_mode_paths_agree(oracle, ctx, capi, monkeypatch, text):
-    """Feature mode has two kernels: the per-key records (default when the plan holds them) and the
-    table-lookup kernel (ETUNE_FEATURES_TABLE=0, and plans whose records would exceed 64 MB).  On a
-    bred 2^18 population both give the same 16 features and ids bit for bit, and a 20000-candidate
-    slice equals the oracle's features_from_counters."""
-    op = parse_op(text)
-    plan = capi.Plan(ctx, op, num_sms=148)
-    g, _, _ = capi.reproduce(plan, plan.sample_random(1024, 42), 1 << 18, 7)
-    f1, i1 = plan.features(g, with_ids=True)
-    monkeypatch.setenv("ETUNE_FEATURES_TABLE", "0")
-    f0, i0 = plan.features(g, with_ids=True)
-    ctx.synchronize()
-    assert (bits(f1) == bits(f0)).all() and (capi.as_u64(i1) == capi.as_u64(i0)).all()
-    s = plan.decode(g[:20000]).cpu().numpy()
-    assert (bits(f1[:20000]) == oracle.features(op, s, 148).view(np.uint64)).all()
-    assert (capi.as_u64(i1[:20000]) == oracle.ids(op, s)).all()
