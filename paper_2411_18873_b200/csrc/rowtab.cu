@@ -834,6 +834,7 @@ constexpr int kSRLevels = 3;  // radix-select levels over the group index (<= 2^
 constexpr int kSRRep = 8;  // replicas of the appended list: the ranking CTAs read different L2 lines
 struct RowSelWork {
     uint32_t nlist, pad[3];
+    uint32_t gbar[2], gpad[2];           // split grid barriers 1 and 2: arrivals of this call
     uint32_t tot[kSRKeys][32];           // crossing segment: candidates per group offset (a line each)
     uint32_t tiecnt[kSRMaxCtas];
     uint32_t kcnt[kSRKeys][kSRMaxCtas];  // crossing segment: candidates per (group offset, CTA)
@@ -1017,6 +1018,32 @@ __device__ __forceinline__ void sr_append_block(RowSelWork* W, uint32_t* ws, uin
         }
 }
 
+// Split grid barrier (the grid is co-resident: cooperative launch) on a per-barrier arrival
+// counter.  arrive: the CTA's writes are ordered before its arrival (bar.sync, then a cumulative
+// fence by the arriving thread); wait: spin with acquire loads until every CTA arrived.  Work
+// placed between the two fills the barrier's release latency -- here, the candidate ids.  The
+// counters return to zero between calls: barrier 2's in phase A of the next call (its arrivals
+// come after barrier 1), barrier 1's by CTA 0 once barrier 2 (or the radix path's first
+// barrier) has passed -- every CTA is past barrier 1 by then.
+__device__ __forceinline__ void gbar_arrive(uint32_t* bar) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicAdd(bar, 1u);
+    }
+}
+__device__ __forceinline__ void gbar_wait(const uint32_t* bar) {
+    if (threadIdx.x == 0) {
+        uint32_t v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= gridDim.x) break;
+            __nanosleep(32);
+        }
+    }
+    __syncthreads();
+}
+
 struct SRStatic {
     uint32_t ws[5 * 33];
     uint32_t part[kSRT];
@@ -1109,7 +1136,6 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         gq[j] = uint32_t(__double_as_longlong(r.y));
     }
     SR_TRACE(14);
-    if (bulk) mbar_wait(&S.mbar[kSRPer], 0);
     // ---- A2: outputs, histogram, g kept in shared memory; the thread's lowest g
     uint32_t gmin = 0xffffffffu;
 #pragma unroll
@@ -1122,14 +1148,22 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         const uint32_t i = base + uint32_t(j) * kSRT + tid;
         __stcs(pred + i, p[j]);
         atomicAdd(hist + (gq[j] >> segshift), 1u);
-        if (ids) {
-            const Genome x = genome_unpack(sgen[j * kSRT + tid]);
+    }
+    // candidate ids of the thread's candidates [j0, j1): computed inside the barriers' release
+    // latency (they are outputs only; nothing in the kernel reads them)
+    auto write_ids = [&](int j0, int j1) {
+        if (!ids) return;
+        if (bulk) mbar_wait(&S.mbar[kSRPer], 0);
+        for (int j = j0; j < j1; ++j) {
+            const uint64_t g = sgen[j * kSRT + tid];
+            if (g == ~0ull) continue;
+            const Genome x = genome_unpack(g);
             const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
             const uint64_t h = bulk ? skh[key] : __ldg(khash + key);
-            __stcs(reinterpret_cast<unsigned long long*>(ids) + i,
+            __stcs(reinterpret_cast<unsigned long long*>(ids) + (base + uint32_t(j) * kSRT + tid),
                    static_cast<unsigned long long>(fnv_tail(fnv_ktile(h, sdivk[x.k]), x.u, x.v)));
         }
-    }
+    };
     SR_TRACE(1);
     __syncthreads();
     // flush: segment i = r * T + t (a warp's atomics hit one line)
@@ -1141,9 +1175,20 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     // the per-group totals of the crossing segment are added after barrier 1 and read after
     // barrier 2: the previous call's are cleared here
     if (blockIdx.x == 0 && tid < kSRKeys) W->tot[tid][0] = 0u;
+    if (blockIdx.x == 0 && tid == 0) W->gbar[1] = 0u;  // the previous call's barrier 2; this call's arrive after barrier 1
     SR_TRACE(2);
-    if (only_a) return;  // diagnostic: phase A alone (profilers cannot split a cooperative kernel)
-    cg::this_grid().sync();
+    if (only_a) {  // diagnostic: phase A alone (profilers cannot split a cooperative kernel)
+        write_ids(0, per);
+        return;
+    }
+    const bool exact_path = segshift <= 6 && !force_radix;  // grid-uniform
+    // ids of j < 4 inside barrier 1, of j >= 4 (R0's second half: untouched until after barrier 2)
+    // inside barrier 2; the radix path writes them all at barrier 1
+    static_assert(kSRR0 / 2 == 4 * kSRT * 8, "genomes of j >= 4 live in R0's second half");
+    const int jsplit = exact_path ? min(per, 4) : per;
+    gbar_arrive(&W->gbar[0]);
+    write_ids(0, jsplit);
+    gbar_wait(&W->gbar[0]);
     SR_TRACE(3);
     // ---- B: the segment b0 of the k-th candidate (every CTA: one 16-byte load per thread)
     const uint32_t kk = uint32_t(k);
@@ -1151,10 +1196,13 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const uint32_t b0 = S.bin, before0 = S.before;
     SR_TRACE(7);
     if (trace && tid == 0) trace[blockIdx.x * kSRTraceSlots + 15] = S.cnt;
-    unsigned long long* xk = reinterpret_cast<unsigned long long*>(dsm);  // ranked list (R0, 32 KB)
-    uint32_t* sb0 = reinterpret_cast<uint32_t*>(dsm + kSRR0 / 2);         // b0's candidates (R0, 32 KB)
+    // R0 after phase A: b0's candidates in the first half (the genomes of j < 4 there are done with
+    // at barrier 1), the ranked list in the second (written after barrier 2, whose release latency
+    // computes the ids of j >= 4 from the genomes still there)
+    uint32_t* sb0 = reinterpret_cast<uint32_t*>(dsm);                              // R0, 32 KB
+    unsigned long long* xk = reinterpret_cast<unsigned long long*>(dsm + kSRR0 / 2);  // R0, 32 KB
     auto gkey = [&](int j) { return (uint64_t(sgg[j * kSRT + tid]) << 32) | uint64_t(base + uint32_t(j) * kSRT + tid); };
-    if (segshift <= 6 && !force_radix) {  // grid-uniform
+    if (exact_path) {
         const uint32_t nq = 1u << segshift, qmask = nq - 1u;
         const unsigned lt = (1u << lane) - 1u;
         // ---- C: the candidates below b0 -> the list (fewer than k); b0's candidates compacted in
@@ -1269,8 +1317,11 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             if (r) atomicAdd(&W->tot[tid][0], r);
         }
         SR_TRACE(4);
-        cg::this_grid().sync();
+        gbar_arrive(&W->gbar[1]);
+        write_ids(jsplit, per);
+        gbar_wait(&W->gbar[1]);
         SR_TRACE(5);
+        if (blockIdx.x == 0 && tid == 0) W->gbar[0] = 0u;  // every CTA is past barrier 1
         // nothing reads the list length or the level-0 counts after the barrier: reset them here
         if (blockIdx.x == 0 && tid == 0) W->nlist = 0u;
         for (int i = blockIdx.x * kSRT + tid; i < nseg; i += gridDim.x * kSRT) W->lvl[0][i] = 0u;
@@ -1350,6 +1401,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     if (tid == 0) W->tiecnt[blockIdx.x] = cta_ties;
     cg::this_grid().sync();
     SR_TRACE(5);
+    if (blockIdx.x == 0 && tid == 0) W->gbar[0] = 0u;  // every CTA is past barrier 1
     if (blockIdx.x == 0 && tid == 0) W->nlist = 0u;
     for (int i = blockIdx.x * kSRT + tid; i < nbc; i += gridDim.x * kSRT) W->lvl[L][i] = 0u;
     // ---- D2: output positions without a sort.  A tie's position is below + its rank among the ties
