@@ -10,6 +10,7 @@
 #include <cmath>
 #include <limits>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -1562,6 +1563,10 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
     CU(cudaEventRecord(c->ev_done[0], c->stream));
     CU(cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
     CU(cudaStreamWaitEvent(c->d2h, c->ev_done[0], 0));
+    // ETUNE_E2E_TRACE=1 (diagnostic): host time spent narrowing rows and waiting for staging, per call
+    static const bool e2e_trace = std::getenv("ETUNE_E2E_TRACE") != nullptr;
+    double e2e_pack_us = 0.0, e2e_wait_us = 0.0;
+    const auto e2e_t0 = std::chrono::steady_clock::now();
     char* io = static_cast<char*>(c->io);
     char* pin = static_cast<char*>(c->hpin);
     for (int64_t lo = 0, i = 0; lo < n; lo += chunk, ++i) {
@@ -1576,8 +1581,14 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         const bool raw = pinned && raw_every > 0 && i % raw_every == 0 && n > chunk;
         int fb = 8;
         if (!raw) {
+            const auto tw0 = std::chrono::steady_clock::now();
             if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));  // pinned buffer b read by chunk i-2's H2D
+            const auto tw1 = std::chrono::steady_clock::now();
             fb = pack_rows(c, h_sched + lo, m, h_rows);
+            if (e2e_trace) {
+                e2e_wait_us += std::chrono::duration<double, std::micro>(tw1 - tw0).count();
+                e2e_pack_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw1).count();
+            }
         }
         if (i >= 2) CU(cudaStreamWaitEvent(c->h2d, c->ev_out[b], 0));  // buffer b drained by chunk i-2's D2H
         CU(cudaMemcpyAsync(d_rows, raw ? static_cast<const void*>(h_sched + lo) : h_rows,
@@ -1617,7 +1628,13 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
             if (etune_status st = drain(b)) return st;
     CU(cudaEventRecord(c->ev_out[0], c->d2h));
     CU(cudaStreamWaitEvent(c->stream, c->ev_out[0], 0));
-    return etune_cu_synchronize(c, first_bad);
+    const etune_status fin = etune_cu_synchronize(c, first_bad);
+    if (e2e_trace)
+        std::fprintf(stderr, "e2e n=%lld: total %.0f us, narrowing %.0f us, staging waits %.0f us, pool %d threads\n",
+                     (long long)n,
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - e2e_t0).count(),
+                     e2e_pack_us, e2e_wait_us, c->pool->size());
+    return fin;
 }
 
 }  // namespace
