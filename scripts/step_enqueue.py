@@ -23,6 +23,7 @@ ap.add_argument("--n", type=int, default=1 << 20)
 ap.add_argument("--k", type=int, default=1024)
 ap.add_argument("--iters", type=int, default=200)
 ap.add_argument("--bufs", type=int, default=16)
+ap.add_argument("--no-ids", action="store_true", help="score without candidate ids")
 a = ap.parse_args()
 g = np.load(os.path.join(ROOT, "tests", "golden", "golden_reference.npz"))
 k = f"{a.model}/model/"
@@ -38,7 +39,7 @@ gen, _, _ = capi.reproduce(plan, par, a.n, 7)
 nb = a.bufs
 bufs = [gen.clone() for _ in range(nb)]
 preds = [torch.empty(a.n, dtype=torch.float64, device="cuda") for _ in range(nb)]
-idss = [torch.empty(a.n, dtype=torch.int64, device="cuda") for _ in range(nb)]
+idss = [None if a.no_ids else torch.empty(a.n, dtype=torch.int64, device="cuda") for _ in range(nb)]
 idx = torch.empty(a.k, dtype=torch.int64, device="cuda")
 fo = capi.Forest.from_flat(ctx, fl)
 fo.compile(plan)
