@@ -786,13 +786,16 @@ __global__ void rowtab_pack_kernel(const RowTabMeta* __restrict__ meta, const do
 // order inside a CTA is (j, t) order.  Every candidate's g stays in shared memory across the
 // grid barriers (nothing is re-read from HBM, and no per-candidate global atomic: copies of one
 // parent share a row and would serialise in L2).
-//   A   score: the CTA's genomes arrive by bulk copies (TMA) into shared memory, one mbarrier per
-//       1024; genome -> row -> {prediction, g} (one 16-byte gather, all of a thread's gathers in
-//       flight together) -> prediction + id (per-key FNV state staged in shared memory by another
-//       bulk copy) out; a shared-memory histogram of g by segment (G / 4096 groups each) flushed
-//       with one atomic per non-empty segment, plus 64 super-segment sums.
-//   B   (every CTA, after barrier 1) the segment b0 of the k-th candidate: super-segment sums,
-//       then the 64 segments of the crossing super-segment -- two 256-byte reads, no hot 16 KB.
+//   A   score: the thread's genomes are loaded first (coalesced, all in flight) and kept in shared
+//       memory; genome -> row -> {prediction, g} (one 16-byte gather, all of a thread's gathers in
+//       flight together) -> prediction out; a shared-memory histogram of g by segment (G / 4096
+//       groups each) flushed with one atomic per non-empty segment (a warp's atomics on one line).
+//   ids The candidate ids (per-key FNV state staged in shared memory by one bulk copy, then the
+//       k_tile / unroll / vectorize bytes) are outputs only: they are computed between the arrive
+//       and the wait of the split grid barriers, filling their release latency (j < 4 at barrier
+//       1, j >= 4 at barrier 2).
+//   B   (every CTA, after barrier 1) the segment b0 of the k-th candidate: one 16-byte load of the
+//       counts per thread and a block scan.
 //   C   (segments of <= 64 groups: G <= 2^18) the candidates below b0 (fewer than k) are appended
 //       to a list; the CTA's candidates in b0 are compacted in index order and given their order
 //       among the CTA's candidates of the same group (a stable multi-split); the CTA publishes
