@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <mutex>
 #include <vector>
 
 #include "etune_internal.hpp"
@@ -1607,25 +1608,25 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
     PL.ndk = ndk;
     PL.off_divk = off_divk;
     PL.khash_smem = khash_smem;
-    static int optin = 0, sms = 0;
-    if (!optin) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     // one CTA per SM: candidates per thread so that the grid covers n
     int64_t gmax = std::min<int64_t>(int64_t(c.sm_count), kSRMaxCtas);
     const int64_t per = (n + gmax * kSRT - 1) / (gmax * kSRT);
     if (per > kSRPer) return cudaErrorNotSupported;  // beyond the grid: the bucketed selection
     const size_t sm = sm_fixed + size_t(per) * kSRT * 4;
     if (sm + sizeof(SRStatic) + 1024 > size_t(optin)) return cudaErrorNotSupported;  // tables too large
-    static size_t attr_sm = 0;
-    if (sm > attr_sm) {
-        const cudaError_t e = cudaFuncSetAttribute(score_select_rows_kernel,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-        if (e != cudaSuccess) return e;
-        attr_sm = sm;
+    {  // the kernel's dynamic-smem ceiling only grows (contexts on several host threads share it)
+        static std::mutex mu;
+        static size_t attr_sm = 0;
+        std::lock_guard<std::mutex> lock(mu);
+        if (sm > attr_sm) {
+            const cudaError_t e = cudaFuncSetAttribute(score_select_rows_kernel,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            if (e != cudaSuccess) return e;
+            attr_sm = sm;
+        }
     }
     const int64_t grid = (n + per * kSRT - 1) / (per * kSRT);
     int per_i = int(per);
