@@ -1058,6 +1058,7 @@ struct SRStatic {
     uint32_t jw[kSRPer * 32];             // b0's candidates per (j, warp), then their offsets
     uint32_t lw[32];                      // candidates below b0 per warp, then their offsets
     uint32_t bin, before, cnt, base, mc;
+    uint32_t fb, fl;                      // phase C fast path: b0 / below-b0 candidates of the CTA
     __align__(8) uint64_t mbar[kSRPer + 2];
 };
 
@@ -1112,6 +1113,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         reinterpret_cast<uint4*>(hist)[tid] = make_uint4(0, 0, 0, 0);
         if (tid < kSRPer * 32) S.jw[tid] = 0u;  // phase C: only warps holding candidates at or below b0 write
         if (tid < 32) S.lw[tid] = 0u;
+        if (tid == 0) S.fb = S.fl = 0u;
     }
     const uint32_t groups = uint32_t(M.groups);
     const int gbits = groups > 1 ? 32 - __clz(int(groups - 1)) : 0;
@@ -1225,6 +1227,61 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
                     else if (sg == b0) mb |= 1u << j;
                 }
             }
+        }
+        // fast path (the usual case: nothing below b0, at most 32 of the CTA's candidates in it):
+        // unordered append to shared memory, then one warp sorts them by index, multi-splits them by
+        // group and publishes the counts -- one block barrier instead of the ordered compaction's four
+        if (mb) {
+            const uint32_t nb = __popc(mb);
+            uint32_t slot = atomicAdd(&S.fb, nb);
+#pragma unroll
+            for (int j = 0; j < kSRPer; ++j)
+                if (((mb >> j) & 1u) && slot < 8192u) sb0[slot++] = (uint32_t(j * kSRT + tid) << 19) | (gq[j] & qmask);
+        }
+        if (ml) atomicAdd(&S.fl, __popc(ml));
+        if (tid < kSRKeys) S.run[tid] = 0u;
+        __syncthreads();
+        const bool fast = S.fl == 0u && S.fb <= 64u;  // block-uniform
+        uint32_t mc = S.fb;  // b0's candidates in sb0 (the ordered compaction recounts them)
+        if (fast && warp == 0) {
+            const uint32_t fbn = S.fb;  // lane l holds entries l and l + 32 (index in the high bits)
+            uint32_t e0 = lane < int(fbn) ? sb0[lane] : 0xffffffffu;
+            uint32_t e1 = lane + 32 < int(fbn) ? sb0[lane + 32] : 0xffffffffu;
+            for (int kb = 2; kb <= 64; kb <<= 1)  // bitonic sort of the 64, ascending
+                for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+                    if (jb == 32) {  // partners in the same lane (kb == 64: ascending)
+                        const uint32_t lo = min(e0, e1), hi = max(e0, e1);
+                        e0 = lo;
+                        e1 = hi;
+                    } else {
+                        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, e0, jb);
+                        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, e1, jb);
+                        const bool lowside = (lane & jb) == 0;
+                        const bool up0 = (lane & kb) == 0, up1 = ((lane + 32) & kb) == 0;
+                        e0 = (lowside == up0) ? min(e0, o0) : max(e0, o0);
+                        e1 = (lowside == up1) ? min(e1, o1) : max(e1, o1);
+                    }
+                }
+            // stable multi-split of the sorted 64: order among the same group offset
+            const bool v0 = lane < int(fbn), v1 = lane + 32 < int(fbn);
+            const uint32_t q0 = v0 ? (e0 & 63u) : 64u, q1 = v1 ? (e1 & 63u) : 65u;
+            const unsigned p0 = __match_any_sync(0xffffffffu, q0), l0 = p0 & lt;
+            const unsigned p1 = __match_any_sync(0xffffffffu, q1), l1 = p1 & lt;
+            if (v0 && l0 == 0) S.run[q0] = __popc(p0);
+            __syncwarp();
+            const uint32_t c0 = v1 ? S.run[q1] : 0u;  // the first half's count of e1's group
+            __syncwarp();
+            if (v0) sb0[lane] = e0 | (uint32_t(__popc(l0)) << 6);
+            if (v1) sb0[lane + 32] = e1 | ((c0 + uint32_t(__popc(l1))) << 6);
+            if (v1 && l1 == 0) S.run[q1] = c0 + __popc(p1);
+            __syncwarp();
+            for (int qq = lane; qq < int(nq); qq += 32) {
+                const uint32_t r = S.run[qq];
+                W->kcnt[qq][blockIdx.x] = r;
+                if (r) atomicAdd(&W->tot[qq][0], r);
+            }
+        }
+        if (wact && !fast) {
 #pragma unroll
             for (int j = 0; j < kSRPer; ++j) {
                 const unsigned bb = __ballot_sync(0xffffffffu, (mb >> j) & 1u);
@@ -1233,6 +1290,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
                 lw += __popc(bl);
             }
         }
+        if (!fast) {  // block-uniform: the ordered compaction
         if (wact && lane == 0) S.lw[warp] = lw;
         if (tid < kSRKeys) S.run[tid] = 0u;
         __syncthreads();
@@ -1259,7 +1317,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             }
         }
         __syncthreads();
-        const uint32_t mc = S.mc;
+        mc = S.mc;
         uint32_t loff = S.base + S.lw[warp];
 #pragma unroll
         for (int j = 0; j < kSRPer; ++j) {
@@ -1320,6 +1378,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             W->kcnt[tid][blockIdx.x] = r;
             if (r) atomicAdd(&W->tot[tid][0], r);
         }
+        }  // ordered compaction
         SR_TRACE(4);
         gbar_arrive(&W->gbar[1]);
         write_ids(jsplit, per);
