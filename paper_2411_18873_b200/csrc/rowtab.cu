@@ -1121,7 +1121,6 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const int nseg = int((groups + (1u << segshift) - 1) >> segshift);
     const uint32_t nkc = uint32_t(M.nkc);
     __syncthreads();
-    SR_TRACE(13);
     const uint16_t* scls = reinterpret_cast<const uint16_t*>(scls32);
     // ---- A1: every gather of the thread in flight together; the genomes go to shared memory
     double p[kSRPer];
@@ -1160,14 +1159,20 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     auto write_ids = [&](int j0, int j1) {
         if (!ids) return;
         if (bulk) mbar_wait(&S.mbar[kSRPer], 0);
-        for (int j = j0; j < j1; ++j) {
+        const bool full = int64_t(base) + int64_t(per) * kSRT <= n;  // block-uniform: no absent candidate
+        auto one = [&](int j, const uint64_t* kh) {
             const uint64_t g = sgen[j * kSRT + tid];
-            if (g == ~0ull) continue;
-            const Genome x = genome_unpack(g);
+            const Genome x = genome_unpack(full || g != ~0ull ? g : 0ull);  // an absent candidate reads key 0
             const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
-            const uint64_t h = bulk ? skh[key] : __ldg(khash + key);
-            __stcs(reinterpret_cast<unsigned long long*>(ids) + (base + uint32_t(j) * kSRT + tid),
-                   static_cast<unsigned long long>(fnv_tail(fnv_ktile(h, sdivk[x.k]), x.u, x.v)));
+            const uint64_t id = fnv_tail(fnv_ktile(kh[key], sdivk[x.k]), x.u, x.v);
+            if (full || g != ~0ull)
+                __stcs(reinterpret_cast<unsigned long long*>(ids) + (base + uint32_t(j) * kSRT + tid),
+                       static_cast<unsigned long long>(id));
+        };
+        if (bulk) {
+            for (int j = j0; j < j1; ++j) one(j, skh);
+        } else {
+            for (int j = j0; j < j1; ++j) one(j, khash);
         }
     };
     SR_TRACE(1);
@@ -1194,6 +1199,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const int jsplit = exact_path ? min(per, 4) : per;
     gbar_arrive(&W->gbar[0]);
     write_ids(0, jsplit);
+    SR_TRACE(13);
     gbar_wait(&W->gbar[0]);
     SR_TRACE(3);
     // ---- B: the segment b0 of the k-th candidate (every CTA: one 16-byte load per thread)
@@ -1734,7 +1740,7 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
                      (unsigned long long)h[size_t(want_trace - 1) * kSRMaxCtas * S + 15]);
         static const char* names[S] = {"start", "A done", "flushed", "sync1", "appended", "sync2",
                                        "ranked", "crossed", "staged", "counted", "L-append", "compact",
-                                       "msplit", "prologue", "A1 issued", "count"};
+                                       "msplit", "ids1 done", "A1 issued", "count"};
         std::fprintf(stderr, "rowsel trace n=%lld grid=%lld per=%d over %d calls (us from the first CTA start):\n",
                      (long long)n, (long long)grid, per_i, want_trace);
         for (int s = 0; s < 15; ++s) {
