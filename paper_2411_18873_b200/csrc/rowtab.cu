@@ -814,6 +814,7 @@ constexpr int kSRPer = 8;
 constexpr int kSRMaxCtas = 1024;
 constexpr int kSRMaxSeg = 4096;    // segment histogram bins (shared memory)
 constexpr int kSRKeys = 64;        // groups per segment the exact crossing path (C/D) handles
+constexpr int kSRIdsA = 0, kSRIdsB = 4;  // ids: j < A in phase A, A <= j < B at barrier 1, the rest at barrier 2
 constexpr int kSRListCap = 8192;   // appended records (radix path: < k; crossing path: < k)
 static_assert(kSRListCap >= kSelMaxK, "the tie path appends at most k records");
 // dynamic shared memory: [R0: genome staging, later the ranked list + the CTA's crossing-segment
@@ -1075,7 +1076,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const RowTabMeta* __restrict__ meta, const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash,
     const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, double* __restrict__ pred,
     uint64_t* __restrict__ ids, int64_t* __restrict__ out, RowSelWork* __restrict__ W,
-    unsigned long long* __restrict__ trace, int only_a, int force_radix) {
+    unsigned long long* __restrict__ trace, int only_a, int force_radix, int ids_a, int ids_b) {
     namespace cg = cooperative_groups;
     SR_TRACE(0);
     extern __shared__ int4 dsm4[];
@@ -1141,19 +1142,6 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         gq[j] = uint32_t(__double_as_longlong(r.y));
     }
     SR_TRACE(14);
-    // ---- A2: outputs, histogram, g kept in shared memory; the thread's lowest g
-    uint32_t gmin = 0xffffffffu;
-#pragma unroll
-    for (int j = 0; j < kSRPer; ++j) {
-        if (j >= per) break;
-        if (sgen[j * kSRT + tid] == ~0ull) gq[j] = 0xffffffffu;  // no candidate
-        sgg[j * kSRT + tid] = gq[j];
-        gmin = min(gmin, gq[j]);
-        if (gq[j] == 0xffffffffu) continue;
-        const uint32_t i = base + uint32_t(j) * kSRT + tid;
-        __stcs(pred + i, p[j]);
-        atomicAdd(hist + (gq[j] >> segshift), 1u);
-    }
     // candidate ids of the thread's candidates [j0, j1): computed inside the barriers' release
     // latency (they are outputs only; nothing in the kernel reads them)
     auto write_ids = [&](int j0, int j1) {
@@ -1175,6 +1163,20 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             for (int j = j0; j < j1; ++j) one(j, khash);
         }
     };
+    // ---- A2: outputs, histogram, g kept in shared memory; the thread's lowest g
+    uint32_t gmin = 0xffffffffu;
+#pragma unroll
+    for (int j = 0; j < kSRPer; ++j) {
+        if (j >= per) break;
+        if (sgen[j * kSRT + tid] == ~0ull) gq[j] = 0xffffffffu;  // no candidate
+        sgg[j * kSRT + tid] = gq[j];
+        gmin = min(gmin, gq[j]);
+        if (gq[j] == 0xffffffffu) continue;
+        const uint32_t i = base + uint32_t(j) * kSRT + tid;
+        __stcs(pred + i, p[j]);
+        atomicAdd(hist + (gq[j] >> segshift), 1u);
+        if (j < ids_a) write_ids(j, j + 1);  // these ids overlap phase A's memory stalls
+    }
     SR_TRACE(1);
     __syncthreads();
     // flush: segment i = r * T + t (a warp's atomics hit one line)
@@ -1189,16 +1191,16 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     if (blockIdx.x == 0 && tid == 0) W->gbar[1] = 0u;  // the previous call's barrier 2; this call's arrive after barrier 1
     SR_TRACE(2);
     if (only_a) {  // diagnostic: phase A alone (profilers cannot split a cooperative kernel)
-        write_ids(0, per);
+        write_ids(min(per, ids_a), per);
         return;
     }
     const bool exact_path = segshift <= 6 && !force_radix;  // grid-uniform
     // ids of j < 4 inside barrier 1, of j >= 4 (R0's second half: untouched until after barrier 2)
     // inside barrier 2; the radix path writes them all at barrier 1
     static_assert(kSRR0 / 2 == 4 * kSRT * 8, "genomes of j >= 4 live in R0's second half");
-    const int jsplit = exact_path ? min(per, 4) : per;
+    const int ja = min(per, ids_a), jsplit = exact_path ? max(ja, min(per, ids_b)) : per;
     gbar_arrive(&W->gbar[0]);
-    write_ids(0, jsplit);
+    write_ids(ja, jsplit);
     SR_TRACE(13);
     gbar_wait(&W->gbar[0]);
     SR_TRACE(3);
@@ -1714,10 +1716,17 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
     // ETUNE_ROWSEL_RADIX=1 (diagnostic, read every call): the radix-select path for any group count
     const char* fr = std::getenv("ETUNE_ROWSEL_RADIX");
     int force_radix = (fr && fr[0] == '1') ? 1 : 0;
+    // which candidates' ids are computed where: j < ids_a inside phase A, ids_a <= j < ids_b inside barrier
+    // 1's release, the rest inside barrier 2's (ETUNE_ROWSEL_IDS="a,b", diagnostic; b >= 4: R0 layout)
+    int ids_a = kSRIdsA, ids_b = kSRIdsB;
+    if (const char* e = std::getenv("ETUNE_ROWSEL_IDS")) {
+        if (std::sscanf(e, "%d,%d", &ids_a, &ids_b) != 2) ids_a = kSRIdsA, ids_b = kSRIdsB;
+        if (ids_b < 4) ids_b = 4;
+    }
     void* args[] = {(void*)&d_plan,   (void*)&PL,       (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowrec,
                     (void*)&d_khash,  (void*)&d_genome, (void*)&n,    (void*)&k,        (void*)&per_i,
                     (void*)&d_pred,   (void*)&d_ids,    (void*)&d_idx,  (void*)&W,        (void*)&tr,
-                    (void*)&oa,       (void*)&force_radix};
+                    (void*)&oa,       (void*)&force_radix, (void*)&ids_a, (void*)&ids_b};
     note_launches(1);
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(score_select_rows_kernel),
                                                       dim3(unsigned(grid)), dim3(kSRT), args, sm, c.stream);
