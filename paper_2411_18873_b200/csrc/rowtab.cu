@@ -814,7 +814,8 @@ constexpr int kSRPer = 8;
 constexpr int kSRMaxCtas = 1024;
 constexpr int kSRMaxSeg = 4096;    // segment histogram bins (shared memory)
 constexpr int kSRKeys = 64;        // groups per segment the exact crossing path (C/D) handles
-constexpr int kSRIdsA = 0, kSRIdsB = 4;  // ids: j < A in phase A, A <= j < B at barrier 1, the rest at barrier 2
+constexpr int kSRIdsA = 0, kSRIdsB = 4, kSRIdsC = 8;  // ids: j < A in phase A, [A, B) at barrier 1, [B, C) at
+                                                      // barrier 2, the rest in phase D's round trip
 constexpr int kSRListCap = 8192;   // appended records (radix path: < k; crossing path: < k)
 static_assert(kSRListCap >= kSelMaxK, "the tie path appends at most k records");
 // dynamic shared memory: [R0: genome staging, later the ranked list + the CTA's crossing-segment
@@ -1076,7 +1077,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const RowTabMeta* __restrict__ meta, const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash,
     const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, double* __restrict__ pred,
     uint64_t* __restrict__ ids, int64_t* __restrict__ out, RowSelWork* __restrict__ W,
-    unsigned long long* __restrict__ trace, int only_a, int force_radix, int ids_a, int ids_b) {
+    unsigned long long* __restrict__ trace, int only_a, int force_radix, int ids_a, int ids_b, int ids_c) {
     namespace cg = cooperative_groups;
     SR_TRACE(0);
     extern __shared__ int4 dsm4[];
@@ -1199,6 +1200,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     // inside barrier 2; the radix path writes them all at barrier 1
     static_assert(kSRR0 / 2 == 4 * kSRT * 8, "genomes of j >= 4 live in R0's second half");
     const int ja = min(per, ids_a), jsplit = exact_path ? max(ja, min(per, ids_b)) : per;
+    const int jsplit2 = exact_path ? max(jsplit, min(per, ids_c)) : per;  // the rest in phase D's round trip
     gbar_arrive(&W->gbar[0]);
     write_ids(ja, jsplit);
     SR_TRACE(13);
@@ -1389,17 +1391,31 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         }  // ordered compaction
         SR_TRACE(4);
         gbar_arrive(&W->gbar[1]);
-        write_ids(jsplit, per);
+        write_ids(jsplit, jsplit2);
         gbar_wait(&W->gbar[1]);
         SR_TRACE(5);
         if (blockIdx.x == 0 && tid == 0) W->gbar[0] = 0u;  // every CTA is past barrier 1
         // nothing reads the list length or the level-0 counts after the barrier: reset them here
         if (blockIdx.x == 0 && tid == 0) W->nlist = 0u;
         for (int i = blockIdx.x * kSRT + tid; i < nseg; i += gridDim.x * kSRT) W->lvl[0][i] = 0u;
-        // ---- D: b0's per-group totals (warp 0) and, per group the CTA holds, the CTAs before it
+        // ---- D: b0's per-group totals (warp 0) and, per group the CTA holds, the CTAs before it.
+        //      The loads go out first; the last candidates' ids fill their round trip.
+        constexpr int kPre = 5;  // CTAs before this one per lane and group: the grid is <= 160 here
+        uint32_t t0 = 0, t1 = 0, pa[kPre], pb[kPre];
+        const int qa = warp, qb = warp + 32;
+        const bool ha = qa < int(nq) && S.run[qa] != 0u, hb = qb < int(nq) && S.run[qb] != 0u;  // warp-uniform
         if (warp == 0) {
-            const uint32_t t0 = lane < int(nq) ? __ldcg(&W->tot[lane][0]) : 0u;
-            const uint32_t t1 = lane + 32 < int(nq) ? __ldcg(&W->tot[lane + 32][0]) : 0u;
+            t0 = lane < int(nq) ? __ldcg(&W->tot[lane][0]) : 0u;
+            t1 = lane + 32 < int(nq) ? __ldcg(&W->tot[lane + 32][0]) : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kPre; ++i) {
+            const uint32_t c = uint32_t(lane + 32 * i);
+            pa[i] = (ha && c < blockIdx.x) ? __ldcg(&W->kcnt[qa][c]) : 0u;
+            pb[i] = (hb && c < blockIdx.x) ? __ldcg(&W->kcnt[qb][c]) : 0u;
+        }
+        write_ids(jsplit2, per);
+        if (warp == 0) {
             uint32_t inc = t0;
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
@@ -1414,12 +1430,25 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
             S.ktot[lane] = inc - t0;
             S.ktot[lane + 32] = all0 + inc1 - t1;
         }
-        for (int q = warp; q < int(nq); q += kSRT / 32) {
-            if (S.run[q] == 0u) continue;  // warp-uniform
-            uint32_t s = 0;
-            for (uint32_t c = lane; c < blockIdx.x; c += 32) s += __ldcg(&W->kcnt[q][c]);
-            for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0) S.kpre[q] = s;
+        if (ha || hb) {
+            uint32_t sa = 0, sbb = 0;
+#pragma unroll
+            for (int i = 0; i < kPre; ++i) {
+                sa += pa[i];
+                sbb += pb[i];
+            }
+            for (uint32_t c = lane + 32 * kPre; c < blockIdx.x; c += 32) {  // grids beyond 160 CTAs
+                if (ha) sa += __ldcg(&W->kcnt[qa][c]);
+                if (hb) sbb += __ldcg(&W->kcnt[qb][c]);
+            }
+            for (int o = 16; o; o >>= 1) {
+                sa += __shfl_xor_sync(0xffffffffu, sa, o);
+                sbb += __shfl_xor_sync(0xffffffffu, sbb, o);
+            }
+            if (lane == 0) {
+                if (ha) S.kpre[qa] = sa;
+                if (hb) S.kpre[qb] = sbb;
+            }
         }
         __syncthreads();
         for (uint32_t pidx = tid; pidx < mc; pidx += kSRT) {
@@ -1718,15 +1747,15 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
     int force_radix = (fr && fr[0] == '1') ? 1 : 0;
     // which candidates' ids are computed where: j < ids_a inside phase A, ids_a <= j < ids_b inside barrier
     // 1's release, the rest inside barrier 2's (ETUNE_ROWSEL_IDS="a,b", diagnostic; b >= 4: R0 layout)
-    int ids_a = kSRIdsA, ids_b = kSRIdsB;
+    int ids_a = kSRIdsA, ids_b = kSRIdsB, ids_c = kSRIdsC;
     if (const char* e = std::getenv("ETUNE_ROWSEL_IDS")) {
-        if (std::sscanf(e, "%d,%d", &ids_a, &ids_b) != 2) ids_a = kSRIdsA, ids_b = kSRIdsB;
+        if (std::sscanf(e, "%d,%d,%d", &ids_a, &ids_b, &ids_c) != 3) ids_a = kSRIdsA, ids_b = kSRIdsB, ids_c = kSRIdsC;
         if (ids_b < 4) ids_b = 4;
     }
     void* args[] = {(void*)&d_plan,   (void*)&PL,       (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowrec,
                     (void*)&d_khash,  (void*)&d_genome, (void*)&n,    (void*)&k,        (void*)&per_i,
                     (void*)&d_pred,   (void*)&d_ids,    (void*)&d_idx,  (void*)&W,        (void*)&tr,
-                    (void*)&oa,       (void*)&force_radix, (void*)&ids_a, (void*)&ids_b};
+                    (void*)&oa,       (void*)&force_radix, (void*)&ids_a, (void*)&ids_b, (void*)&ids_c};
     note_launches(1);
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(score_select_rows_kernel),
                                                       dim3(unsigned(grid)), dim3(kSRT), args, sm, c.stream);
