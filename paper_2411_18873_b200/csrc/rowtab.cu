@@ -830,7 +830,7 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // diagnostic (ETUNE_ROWSEL_TRACE): per-CTA globaltimer stamps, kSRTraceSlots slots per CTA
-constexpr int kSRTraceSlots = 16;  // slot 15 holds the crossing segment's count, not a time
+constexpr int kSRTraceSlots = 18;  // slot 15 holds the crossing segment's count, slot 16 the SM id: not times
 #define SR_TRACE(slot) \
     do { \
         if (trace && threadIdx.x == 0) trace[blockIdx.x * kSRTraceSlots + (slot)] = globaltimer(); \
@@ -1050,6 +1050,25 @@ __device__ __forceinline__ void gbar_wait(const uint32_t* bar) {
     __syncthreads();
 }
 
+// row-record gather with a selectable cache policy (diagnostic ETUNE_ROWSEL_GMODE): 0 ld.global.nc (L1
+// allocating), 1 ld.global.cg (L2 only; the default), 2 .nc.L1::no_allocate, 3 .nc.L1::evict_first.
+// The table (1.5 MB for C2) does not fit L1 and ~7 K gathers per SM are in flight at once: bypassing L1
+// measured 1.5 us per step faster than the L1-allocating load (profiles/r02z_gather_policy.txt).
+__device__ __forceinline__ double2 ld_row(const RowRec* p, int mode) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 r;
+    if (mode == 1) return __ldcg(q);
+    if (mode == 2) {
+        asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(q));
+        return r;
+    }
+    if (mode == 3) {
+        asm("ld.global.nc.L1::evict_first.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(q));
+        return r;
+    }
+    return __ldg(q);
+}
+
 struct SRStatic {
     uint32_t ws[5 * 33];
     uint32_t part[kSRT];
@@ -1077,7 +1096,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const RowTabMeta* __restrict__ meta, const RowRec* __restrict__ rowrec, const uint64_t* __restrict__ khash,
     const uint64_t* __restrict__ genome, int64_t n, int64_t k, int per, double* __restrict__ pred,
     uint64_t* __restrict__ ids, int64_t* __restrict__ out, RowSelWork* __restrict__ W,
-    unsigned long long* __restrict__ trace, int only_a, int force_radix, int ids_a, int ids_b, int ids_c) {
+    unsigned long long* __restrict__ trace, int only_a, int force_radix, int ids_a, int ids_b, int ids_c, int gmode) {
     namespace cg = cooperative_groups;
     SR_TRACE(0);
     extern __shared__ int4 dsm4[];
@@ -1123,6 +1142,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     const int nseg = int((groups + (1u << segshift) - 1) >> segshift);
     const uint32_t nkc = uint32_t(M.nkc);
     __syncthreads();
+    SR_TRACE(17);
     const uint16_t* scls = reinterpret_cast<const uint16_t*>(scls32);
     // ---- A1: every gather of the thread in flight together; the genomes go to shared memory
     double p[kSRPer];
@@ -1138,7 +1158,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
         // unconditional gather (an absent candidate reads row 0): a select on the loaded value here
         // would wait for it and serialise the thread's gathers
-        const double2 r = __ldg(reinterpret_cast<const double2*>(rowrec) + (key * nkc + kc));
+        const double2 r = ld_row(rowrec + (key * nkc + kc), gmode);
         p[j] = r.x;
         gq[j] = uint32_t(__double_as_longlong(r.y));
     }
@@ -1211,7 +1231,12 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     sr_cross(W->lvl[0], kk, S.ws, &S.bin, &S.before, &S.cnt);
     const uint32_t b0 = S.bin, before0 = S.before;
     SR_TRACE(7);
-    if (trace && tid == 0) trace[blockIdx.x * kSRTraceSlots + 15] = S.cnt;
+    if (trace && tid == 0) {
+        trace[blockIdx.x * kSRTraceSlots + 15] = S.cnt;
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        trace[blockIdx.x * kSRTraceSlots + 16] = smid;
+    }
     // R0 after phase A: b0's candidates in the first half (the genomes of j < 4 there are done with
     // at barrier 1), the ranked list in the second (written after barrier 2, whose release latency
     // computes the ids of j >= 4 from the genomes still there)
@@ -1752,10 +1777,12 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
         if (std::sscanf(e, "%d,%d,%d", &ids_a, &ids_b, &ids_c) != 3) ids_a = kSRIdsA, ids_b = kSRIdsB, ids_c = kSRIdsC;
         if (ids_b < 4) ids_b = 4;
     }
+    const char* gm = std::getenv("ETUNE_ROWSEL_GMODE");  // diagnostic, read every call
+    int gmode = gm ? std::atoi(gm) : 1;
     void* args[] = {(void*)&d_plan,   (void*)&PL,       (void*)&d_clskuv, (void*)&d_meta, (void*)&d_rowrec,
                     (void*)&d_khash,  (void*)&d_genome, (void*)&n,    (void*)&k,        (void*)&per_i,
                     (void*)&d_pred,   (void*)&d_ids,    (void*)&d_idx,  (void*)&W,        (void*)&tr,
-                    (void*)&oa,       (void*)&force_radix, (void*)&ids_a, (void*)&ids_b, (void*)&ids_c};
+                    (void*)&oa,       (void*)&force_radix, (void*)&ids_a, (void*)&ids_b, (void*)&ids_c, (void*)&gmode};
     note_launches(1);
     const cudaError_t e = cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(score_select_rows_kernel),
                                                       dim3(unsigned(grid)), dim3(kSRT), args, sm, c.stream);
@@ -1771,21 +1798,40 @@ cudaError_t launch_score_select_rows(const LaunchCtx& c, const uint8_t* d_plan, 
             unsigned long long t0 = ~0ull;
             for (int b = 0; b < int(grid); ++b) t0 = std::min(t0, t[b * S]);
             for (int b = 0; b < int(grid); ++b)
-                for (int s = 0; s < 15; ++s)
-                    if (t[b * S + s] >= t0) v[s].push_back(double(t[b * S + s] - t0) * 1e-3);
+                for (int s = 0; s < S; ++s)
+                    if (s != 15 && s != 16 && t[b * S + s] >= t0) v[s].push_back(double(t[b * S + s] - t0) * 1e-3);
         }
         std::fprintf(stderr, "rowsel: candidates in the crossing segment of the last call: %llu\n",
                      (unsigned long long)h[size_t(want_trace - 1) * kSRMaxCtas * S + 15]);
         static const char* names[S] = {"start", "A done", "flushed", "sync1", "appended", "sync2",
                                        "ranked", "crossed", "staged", "counted", "L-append", "compact",
-                                       "msplit", "ids1 done", "A1 issued", "count"};
+                                       "msplit", "ids1 done", "A1 issued", "count", "smid", "prologue"};
         std::fprintf(stderr, "rowsel trace n=%lld grid=%lld per=%d over %d calls (us from the first CTA start):\n",
                      (long long)n, (long long)grid, per_i, want_trace);
-        for (int s = 0; s < 15; ++s) {
+        for (int s = 0; s < S; ++s) {
             if (v[s].empty()) continue;
             std::sort(v[s].begin(), v[s].end());
             std::fprintf(stderr, "  %-9s min %7.2f  p50 %7.2f  p90 %7.2f  max %7.2f\n", names[s], v[s].front(),
                          v[s][v[s].size() / 2], v[s][v[s].size() * 9 / 10], v[s].back());
+        }
+        // the same stamps per SM-id bucket of 16 (mean over the CTAs and calls): is a part of the chip slower?
+        for (int s : {14, 1, 13}) {
+            double sum[16] = {}, cnt[16] = {};
+            for (int call = 0; call < want_trace; ++call) {
+                const unsigned long long* t = h.data() + size_t(call) * kSRMaxCtas * S;
+                unsigned long long t0 = ~0ull;
+                for (int b = 0; b < int(grid); ++b) t0 = std::min(t0, t[b * S]);
+                for (int b = 0; b < int(grid); ++b) {
+                    if (t[b * S + s] < t0) continue;
+                    const int q = int(t[b * S + 16] / 16) & 15;
+                    sum[q] += double(t[b * S + s] - t0) * 1e-3;
+                    cnt[q] += 1;
+                }
+            }
+            std::fprintf(stderr, "  %-9s by smid/16:", names[s]);
+            for (int q = 0; q < 16; ++q)
+                if (cnt[q] > 0) std::fprintf(stderr, " %5.2f", sum[q] / cnt[q]);
+            std::fprintf(stderr, "\n");
         }
         cudaMemset(trace, 0, h.size() * 8);
     }
