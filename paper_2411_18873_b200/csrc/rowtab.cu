@@ -15,7 +15,7 @@
 //                          value's count of thresholds it does not fall below, the
 //                          distinct attained count triples over the legal (k, u, v)
 //                          -> Kuv class table [k][u][v] and one representative per class
-//   rowtab_build_kernel    one thread per row: the representative genome's features from
+//   rowtab_build_kernel    four lanes per row: the representative genome's features from
 //                          the plan tables, the reference tree walk over the forest, the
 //                          row's prediction (+ the lowest / highest order key for the
 //                          fused selection's buckets)
@@ -264,6 +264,10 @@ __global__ void __launch_bounds__(kClsT, 1) rowtab_classes_kernel(const uint8_t*
 }
 
 constexpr int kBuildT = 256;
+// compact walk: L lanes per row (4 by default), tree t on lane t % L; the lanes' leaf values are added
+// in tree order through shuffles, so the sum is the reference's sequential one (bit-identical), while
+// a row's dependent node-load chain is L times shorter and the rows spread evenly over the SMs
+constexpr int kBuildFS = 17;  // feature-vector stride in doubles (16 + 1: the lanes' reads spread over the banks)
 
 __device__ __forceinline__ uint64_t order_key(double p) {
     const uint64_t b = static_cast<uint64_t>(__double_as_longlong(p));
@@ -280,12 +284,13 @@ struct CNode {
 };
 static_assert(sizeof(CNode) == 16, "CNode layout");
 
-// One thread per row: features of the row's representative genome, then RegressionTree::eval
-// summed in tree order (energy_model.cpp:36-44, 245-249) -- the same comparisons, the same leaf
-// doubles and the same DADD order as walk_forest / the reference.  COMPACT: nodes staged as CNode
-// and features in shared memory ([16][kBuildT], one LDS per visited node); else the GNode walk
-// over global memory (forests of >= 65536 nodes or too large for shared memory).
-template <bool COMPACT>
+// Per row: features of the row's representative genome, then RegressionTree::eval summed in tree
+// order (energy_model.cpp:36-44, 245-249) -- the same comparisons, the same leaf doubles and the
+// same DADD order as walk_forest / the reference.  COMPACT: nodes staged as CNode and the row's
+// features in shared memory (one LDS per visited node), L lanes per row walking the trees
+// round-robin; else one thread per row and the GNode walk over global memory (forests of >= 65536
+// nodes or too large for shared memory).
+template <bool COMPACT, int L>
 __global__ void __launch_bounds__(kBuildT) rowtab_build_kernel(const uint8_t* __restrict__ P,
                                                                const uint8_t* __restrict__ Q, int nnodes,
                                                                RowTabMeta* __restrict__ meta,
@@ -322,7 +327,7 @@ __global__ void __launch_bounds__(kBuildT) rowtab_build_kernel(const uint8_t* __
     const int64_t rows = int64_t(H.nt[0]) * nt1 * nt2 * nkc;
     const double base = QH.base, lr = QH.lr;
     uint64_t lo = ~0ull, hi = 0ull;
-    for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rows; r += int64_t(gridDim.x) * blockDim.x) {
+    auto row_knobs = [&](int64_t r) {
         const uint32_t key = uint32_t(r / nkc), kc = uint32_t(r - int64_t(key) * nkc);
         const uint32_t t2 = key % nt2, q = key / nt2, t1 = q % nt1, t0 = q / nt1;
         const uint32_t rep = __ldg(crep + kc);
@@ -334,31 +339,64 @@ __global__ void __launch_bounds__(kBuildT) rowtab_build_kernel(const uint8_t* __
         c.k_tile = divk[c.k];
         c.unroll = 1u << ((rep >> 2) & 15u);
         c.vec = 1u << (rep & 3u);
-        double f[16];
-        plan_features(P, H, c, f);
-        double p;
-        if (COMPACT) {
+        return c;
+    };
+    if (COMPACT) {
+        const int l = threadIdx.x & (L - 1), g = threadIdx.x / L;
+        const int lead = (threadIdx.x & 31) & ~(L - 1);  // the group's lane 0 within the warp
+        double* myf = fs + g * kBuildFS;
+        const int64_t step = int64_t(gridDim.x) * (kBuildT / L);
+        const int64_t iters = (rows + step - 1) / step;  // warp-uniform trip count (shuffles below)
+        for (int64_t it = 0; it < iters; ++it) {
+            const int64_t r = it * step + int64_t(blockIdx.x) * (kBuildT / L) + g;
+            const bool valid = r < rows;
+            if (valid) {  // every lane computes the features, lane l stores those with j % L == l
+                double f[16];
+                plan_features(P, H, row_knobs(r), f);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) fs[j * kBuildT + threadIdx.x] = f[j];
-            const double* myf = fs + threadIdx.x;
-            double sum = 0.0;
-            for (int t = 0; t < ntrees; ++t) {
-                CNode nd = sn[sroots[t]];
-                while (nd.feature >= 0) {
-                    const double v = myf[nd.feature * kBuildT];
-                    nd = sn[v < nd.tv ? (nd.lr & 0xffffu) : (nd.lr >> 16)];
-                }
-                sum = __dadd_rn(sum, nd.tv);
+                for (int j = 0; j < 16; ++j)
+                    if ((j & (L - 1)) == l) myf[j] = f[j];
             }
-            const double s = __dadd_rn(base, __dmul_rn(lr, sum));
-            p = (1e-6 < s) ? s : 1e-6;
-        } else {
-            p = walk_forest(QH, groots, gnodes, f);
+            __syncwarp();
+            double sum = 0.0;
+            for (int tb = 0; tb < ntrees; tb += L) {
+                const int t = tb + l;
+                double v = 0.0;
+                if (valid && t < ntrees) {
+                    CNode nd = sn[sroots[t]];
+                    while (nd.feature >= 0) {
+                        const double x = myf[nd.feature];
+                        nd = sn[x < nd.tv ? (nd.lr & 0xffffu) : (nd.lr >> 16)];
+                    }
+                    v = nd.tv;
+                }
+#pragma unroll
+                for (int q = 0; q < L; ++q) {  // trees tb .. tb + L - 1, in order
+                    const double w = __shfl_sync(0xffffffffu, v, lead + q);
+                    if (tb + q < ntrees) sum = __dadd_rn(sum, w);
+                }
+            }
+            __syncwarp();  // the next row's features overwrite myf
+            if (valid && l == 0) {
+                const double s = __dadd_rn(base, __dmul_rn(lr, sum));
+                const double p = (1e-6 < s) ? s : 1e-6;
+                rowpred[r] = p;
+                const uint64_t o = order_key(p);
+                lo = o < lo ? o : lo;
+                hi = o > hi ? o : hi;
+            }
         }
-        rowpred[r] = p;
-        const uint64_t o = order_key(p);
-        lo = o < lo ? o : lo;
-        hi = o > hi ? o : hi;
+    } else {
+        for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < rows;
+             r += int64_t(gridDim.x) * blockDim.x) {
+            double f[16];
+            plan_features(P, H, row_knobs(r), f);
+            const double p = walk_forest(QH, groots, gnodes, f);
+            rowpred[r] = p;
+            const uint64_t o = order_key(p);
+            lo = o < lo ? o : lo;
+            hi = o > hi ? o : hi;
+        }
     }
     for (int s = 16; s > 0; s >>= 1) {
         const uint64_t a = __shfl_xor_sync(0xffffffffu, lo, s), b = __shfl_xor_sync(0xffffffffu, hi, s);
@@ -1599,25 +1637,38 @@ cudaError_t launch_rowtab_compile(const LaunchCtx& c, const uint8_t* d_plan, uin
     {  // the tree count is in the predict blob's header (host mirror not needed: bound by nnodes)
         ntrees = nnodes;  // roots region sized for the worst case (one node per tree)
     }
-    const size_t sm_c = ((node_bytes + size_t(ntrees) * 4 + 15) / 16) * 16 + size_t(16) * kBuildT * 8;
+    // ETUNE_BUILD_LANES (diagnostic): lanes per row of the compact walk, 1 / 2 / 4 / 8 (default 4)
+    static const int lanes = [] {
+        const char* ev = std::getenv("ETUNE_BUILD_LANES");
+        const int v = ev ? std::atoi(ev) : 4;
+        return v == 1 || v == 2 || v == 8 ? v : 4;
+    }();
+    const int rows_cta = kBuildT / lanes;
+    const size_t sm_c = ((node_bytes + size_t(ntrees) * 4 + 15) / 16) * 16 + size_t(kBuildFS) * rows_cta * 8;
     const bool compact = nnodes < 65536 && sm_c <= size_t(optin);
     int per_sm = 0;
-    const int64_t want = (rows_cap + kBuildT - 1) / kBuildT;
+    int64_t want = (rows_cap + kBuildT - 1) / kBuildT;
     if (compact) {
-        e = cudaFuncSetAttribute(rowtab_build_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_c));
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rowtab_build_kernel<true>, kBuildT, sm_c);
-        if (e != cudaSuccess) return e;
-        if (per_sm < 1) return cudaErrorInvalidConfiguration;
-        const int64_t cap = int64_t(c.sm_count) * per_sm;
-        e = launch_pdl(rowtab_build_kernel<true>, dim3(int(want < cap ? (want > 0 ? want : 1) : cap)), dim3(kBuildT),
-                       sm_c, c.stream, d_plan, d_pred, nnodes, d_meta, static_cast<const uint32_t*>(d_crep),
-                       d_rowpred);
+        want = (rows_cap + rows_cta - 1) / rows_cta;
+        auto go = [&](auto kern) {
+            cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm_c));
+            if (e2 != cudaSuccess) return e2;
+            e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBuildT, sm_c);
+            if (e2 != cudaSuccess) return e2;
+            if (per_sm < 1) return cudaErrorInvalidConfiguration;
+            const int64_t cap = int64_t(c.sm_count) * per_sm;
+            return launch_pdl(kern, dim3(int(want < cap ? (want > 0 ? want : 1) : cap)), dim3(kBuildT), sm_c, c.stream,
+                              d_plan, d_pred, nnodes, d_meta, static_cast<const uint32_t*>(d_crep), d_rowpred);
+        };
+        e = lanes == 1 ? go(rowtab_build_kernel<true, 1>)
+            : lanes == 2 ? go(rowtab_build_kernel<true, 2>)
+            : lanes == 8 ? go(rowtab_build_kernel<true, 8>)
+                         : go(rowtab_build_kernel<true, 4>);
     } else {
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rowtab_build_kernel<false>, kBuildT, 0);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, rowtab_build_kernel<false, 1>, kBuildT, 0);
         if (e != cudaSuccess) return e;
         const int64_t cap = int64_t(c.sm_count) * (per_sm > 0 ? per_sm : 1);
-        e = launch_pdl(rowtab_build_kernel<false>, dim3(int(want < cap ? (want > 0 ? want : 1) : cap)), dim3(kBuildT),
+        e = launch_pdl(rowtab_build_kernel<false, 1>, dim3(int(want < cap ? (want > 0 ? want : 1) : cap)), dim3(kBuildT),
                        0, c.stream, d_plan, d_pred, nnodes, d_meta, static_cast<const uint32_t*>(d_crep), d_rowpred);
     }
     note_launches(2);
