@@ -645,16 +645,18 @@ def run_ours(args):
             return dt
 
         def h2d_bytes(pinned_rows):
-            # the host pool narrows each 2^17-row chunk to the smallest field width holding it (u16 here);
+            # the host pool narrows each chunk (2^17 rows) to the smallest field width holding it (u16 here);
             # with a pinned caller buffer every 4th chunk is copied raw (96 B/row) instead
             fb = 2 if (sched.min() >= 0 and sched.max() < 1 << 16) else 4 if sched.max() < 1 << 32 else 8
             chunk, raw_every = 1 << int(os.environ.get("ETUNE_E2E_CHUNK_LOG2", "17")), \
                 int(os.environ.get("ETUNE_E2E_RAW_EVERY", "4"))
-            tot = 0
-            for i, lo in enumerate(range(0, n, chunk)):
-                mm = min(chunk, n - lo)
-                raw = pinned_rows and raw_every > 0 and i % raw_every == 0 and n > chunk
+            tot, lo, i = 0, 0, 0
+            while lo < n:  # the library's chunk schedule: full chunks, the final one a quarter chunk
+                rem, q = n - lo, chunk // 4
+                mm = rem if rem <= q else rem - q if rem <= chunk + q else chunk
+                raw = pinned_rows and raw_every > 0 and i % raw_every == 0 and mm == chunk
                 tot += mm * 12 * (8 if raw else fb)
+                lo, i = lo + mm, i + 1
             return tot
 
         reps = max(5, args.steps // 4)

@@ -215,7 +215,10 @@ int host_threads() {
 
 // Packs m rows into pinned `dst` with the narrowest field width that holds them (2, 4 or
 // 8 bytes), split over the host pool.  Returns the field width.
-int pack_rows(etune_cu_ctx* c, const etune_schedule* src, int64_t m, void* dst) {
+// extra_tasks / extra (optional): more pool tasks run in the same dispatch as the narrowing (the
+// previous chunks' outputs copied out of staging), exactly once
+int pack_rows(etune_cu_ctx* c, const etune_schedule* src, int64_t m, void* dst, int extra_tasks = 0,
+              const std::function<void(int)>* extra = nullptr) {
     const int tasks = std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m / 2048));
     auto range = [&](int t, int64_t* a, int64_t* b) {  // even row boundaries: 24 fields = 3 AVX-512 words
         *a = (m * t / tasks) & ~int64_t(1);
@@ -223,7 +226,8 @@ int pack_rows(etune_cu_ctx* c, const etune_schedule* src, int64_t m, void* dst) 
     };
     std::vector<char> ok(size_t(tasks), 1);
     const bool simd = have_avx512() && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
-    c->pool->run(tasks, [&](int t) {
+    c->pool->run(tasks + (extra ? extra_tasks : 0), [&](int t) {
+        if (t >= tasks) return (*extra)(t - tasks);
         int64_t a, b;
         range(t, &a, &b);
         ok[size_t(t)] = simd ? narrow_u16_avx512(reinterpret_cast<const int64_t*>(src), static_cast<uint16_t*>(dst),
@@ -1544,20 +1548,32 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         c->hout_bytes = 2 * size_t(cap) * 16;
     }
     int64_t pend_lo[2] = {-1, -1}, pend_m[2] = {0, 0};  // staged chunk waiting in hout buffer b
-    auto drain = [&](int b) -> etune_status {
-        if (pend_lo[b] < 0) return ETUNE_OK;
-        CU(cudaEventSynchronize(c->ev_out[b]));
+    auto out_tasks = [&](int b) {
+        return int(std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, pend_m[b] / 4096)));
+    };
+    auto out_copy = [&](int b, int t, int tasks) {  // part t of staging buffer b's outputs to the caller's arrays
         const double* sp = reinterpret_cast<const double*>(static_cast<char*>(c->hout) + size_t(b) * size_t(cap) * 16);
         const uint64_t* si = reinterpret_cast<const uint64_t*>(sp + cap);
         const int64_t lo2 = pend_lo[b], m2 = pend_m[b];
-        const int tasks = int(std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m2 / 4096)));
-        c->pool->run(tasks, [&](int t) {
-            const int64_t a = m2 * t / tasks, e = m2 * (t + 1) / tasks;
-            if (h_pred) std::memcpy(h_pred + lo2 + a, sp + a, size_t(e - a) * 8);
-            if (h_ids) std::memcpy(h_ids + lo2 + a, si + a, size_t(e - a) * 8);
-        });
+        const int64_t a = m2 * t / tasks, e = m2 * (t + 1) / tasks;
+        if (h_pred) std::memcpy(h_pred + lo2 + a, sp + a, size_t(e - a) * 8);
+        if (h_ids) std::memcpy(h_ids + lo2 + a, si + a, size_t(e - a) * 8);
+    };
+    auto drain = [&](int b) -> etune_status {
+        if (pend_lo[b] < 0) return ETUNE_OK;
+        CU(cudaEventSynchronize(c->ev_out[b]));
+        const int tasks = out_tasks(b);
+        c->pool->run(tasks, [&](int t) { out_copy(b, t, tasks); });
         pend_lo[b] = -1;
         return ETUNE_OK;
+    };
+    // chunk sizes: full chunks, then the last full chunk split so that the final one is a quarter chunk
+    // (the tail after the last narrowing -- its copy in, scoring, copy out -- shrinks with it)
+    auto chunk_at = [&](int64_t rem) -> int64_t {
+        const int64_t q = chunk / 4;
+        if (rem <= q) return rem;
+        if (rem <= chunk + q) return rem - q;
+        return chunk;
     };
     // the caller's earlier work on the ctx stream happens-before this call's copies
     CU(cudaEventRecord(c->ev_done[0], c->stream));
@@ -1569,7 +1585,8 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
     const auto e2e_t0 = std::chrono::steady_clock::now();
     char* io = static_cast<char*>(c->io);
     char* pin = static_cast<char*>(c->hpin);
-    for (int64_t lo = 0, i = 0; lo < n; lo += chunk, ++i) {
+    for (int64_t lo = 0, i = 0, m = 0; lo < n; lo += m, ++i) {
+        m = chunk_at(n - lo);
         const int b = int(i & 1);
         char* base = io + size_t(b) * size_t(cap) * per;
         void* d_rows = base;
@@ -1577,14 +1594,22 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         auto* d_pred = d_all ? d_all + lo : reinterpret_cast<double*>(base + size_t(cap) * (sizeof(etune_schedule) + 8));
         auto* d_ids = reinterpret_cast<uint64_t*>(base + size_t(cap) * (sizeof(etune_schedule) + 16));
         void* h_rows = pin + size_t(b) * size_t(cap) * sizeof(etune_schedule);
-        const int64_t m = (n - lo) < chunk ? (n - lo) : chunk;
-        const bool raw = pinned && raw_every > 0 && i % raw_every == 0 && n > chunk;
+        const bool raw = pinned && raw_every > 0 && i % raw_every == 0 && m == chunk;  // full chunks only
         int fb = 8;
         if (!raw) {
             const auto tw0 = std::chrono::steady_clock::now();
             if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));  // pinned buffer b read by chunk i-2's H2D
             const auto tw1 = std::chrono::steady_clock::now();
-            fb = pack_rows(c, h_sched + lo, m, h_rows);
+            // chunk i-2's outputs leave staging buffer b in the same pool dispatch when their D2H has
+            // landed (else after this chunk's launches, below)
+            int xt = 0;
+            std::function<void(int)> xf;
+            if (stage_out && pend_lo[b] >= 0 && cudaEventQuery(c->ev_out[b]) == cudaSuccess) {
+                xt = out_tasks(b);
+                xf = [&out_copy, b, xt](int t) { out_copy(b, t, xt); };
+            }
+            fb = pack_rows(c, h_sched + lo, m, h_rows, xt, xt ? &xf : nullptr);
+            if (xt) pend_lo[b] = -1;
             if (e2e_trace) {
                 e2e_wait_us += std::chrono::duration<double, std::micro>(tw1 - tw0).count();
                 e2e_pack_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw1).count();

@@ -23,6 +23,8 @@ ctx = capi.Context(0)
 plan = capi.Plan(ctx, parse_op("conv:1,56,56,64,64,3,1,1"))
 gen, _, _ = capi.reproduce(plan, plan.sample_random(1024, 42), 1 << 20, 7)
 sched = plan.decode(gen).cpu().numpy()
+if os.environ.get("E2E_PINNED") == "1":  # the caller's rows in pinned memory (raw DMA chunks)
+    sched = torch.from_numpy(sched).pin_memory().numpy()
 fo = capi.Forest.from_flat(ctx, fl)
 idx = np.zeros(1024, np.int64)
 pred = np.zeros(len(sched))
