@@ -1088,8 +1088,9 @@ __device__ __forceinline__ void gbar_wait(const uint32_t* bar) {
     __syncthreads();
 }
 
-// row-record gather with a selectable cache policy (diagnostic ETUNE_ROWSEL_GMODE): 0 ld.global.nc (L1
-// allocating), 1 ld.global.cg (L2 only; the default), 2 .nc.L1::no_allocate, 3 .nc.L1::evict_first.
+// row-record gather with a selectable cache policy (diagnostic ETUNE_ROWSEL_GMODE, low 4 bits): 0
+// ld.global.nc (L1 allocating), 1 ld.global.cg (L2 only; the default), 2 .nc.L1::no_allocate,
+// 3 .nc.L1::evict_first; + 16: no in-thread row dedup (every candidate gathers its record).
 // The table (1.5 MB for C2) does not fit L1 and ~7 K gathers per SM are in flight at once: bypassing L1
 // measured 1.5 us per step faster than the L1-allocating load (profiles/r02z_gather_policy.txt).
 __device__ __forceinline__ double2 ld_row(const RowRec* p, int mode) {
@@ -1183,8 +1184,15 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     SR_TRACE(17);
     const uint16_t* scls = reinterpret_cast<const uint16_t*>(scls32);
     // ---- A1: every gather of the thread in flight together; the genomes go to shared memory
+    // A thread's candidates j share their base parent (i % P), so bred populations repeat rows inside a
+    // thread (C2 bench population: 5.7 distinct genomes per 7): a candidate whose row an earlier one of
+    // the thread already gathers is not gathered again; A2 copies the earlier candidate's record
+    // (dsrc: 3 bits per j, the source candidate or j itself).  Absent candidates gather nothing.
     double p[kSRPer];
     uint32_t gq[kSRPer];
+    uint32_t rw[kSRPer];
+    uint32_t dsrc = 0u;
+    const bool dedup = !(gmode & 16);
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j) {
         if (j >= per) break;
@@ -1194,11 +1202,21 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         const Genome x = genome_unpack(v ? g : 0ull);
         const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
         const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
-        // unconditional gather (an absent candidate reads row 0): a select on the loaded value here
-        // would wait for it and serialise the thread's gathers
-        const double2 r = ld_row(rowrec + (key * nkc + kc), gmode);
-        p[j] = r.x;
-        gq[j] = uint32_t(__double_as_longlong(r.y));
+        rw[j] = v ? key * nkc + kc : 0xffffffffu;
+        uint32_t src = uint32_t(j);
+#pragma unroll
+        for (int q = j - 1; q >= 0; --q)
+            if (dedup && rw[q] == rw[j]) src = uint32_t(q);  // the earliest match
+        dsrc |= src << (3 * j);
+        // the gather's predicate is known before it issues: no select on a loaded value serialises the
+        // thread's gathers
+        p[j] = 0.0;
+        gq[j] = 0u;
+        if (v && src == uint32_t(j)) {
+            const double2 r = ld_row(rowrec + rw[j], gmode & 15);
+            p[j] = r.x;
+            gq[j] = uint32_t(__double_as_longlong(r.y));
+        }
     }
     SR_TRACE(14);
     // candidate ids of the thread's candidates [j0, j1): computed inside the barriers' release
@@ -1227,6 +1245,15 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j) {
         if (j >= per) break;
+        {
+            const uint32_t src = (dsrc >> (3 * j)) & 7u;  // a repeated row: the earlier candidate's record
+#pragma unroll
+            for (int q = 0; q < j; ++q)
+                if (src == uint32_t(q)) {
+                    p[j] = p[q];
+                    gq[j] = gq[q];
+                }
+        }
         if (sgen[j * kSRT + tid] == ~0ull) gq[j] = 0xffffffffu;  // no candidate
         sgg[j * kSRT + tid] = gq[j];
         gmin = min(gmin, gq[j]);
