@@ -449,7 +449,7 @@ __global__ void __launch_bounds__(kRowsT) score_rows_kernel(const uint8_t* __res
                                                             const uint64_t* __restrict__ khk,
                                                             const uint64_t* __restrict__ genome, int64_t n,
                                                             double* __restrict__ pred, uint64_t* __restrict__ ids,
-                                                            const SelHist sel_in) {
+                                                            const SelHist sel_in, int nodedup) {
     extern __shared__ uint32_t rsm[];  // Kuv class table [ndk][16][4] (u16 pairs), then k_tile low words [ndk]
     __shared__ uint32_t shist[kSelBins];
     const PlanHdr& H = *reinterpret_cast<const PlanHdr*>(gplan);
@@ -480,18 +480,34 @@ __global__ void __launch_bounds__(kRowsT) score_rows_kernel(const uint8_t* __res
         uint32_t key[kRowsPer];
         double p[kRowsPer];
         uint64_t h[kRowsPer];
+        // a thread's candidates are `stride` apart and share their base parent when P divides it: an
+        // equal genome earlier in the pass gathers for it (3 bits per j: the source candidate or j)
+        uint32_t dsrc = 0u;
 #pragma unroll
         for (int j = 0; j < kRowsPer; ++j) {
             const Genome x = genome_unpack(g[j]);
             key[j] = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
             const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);  // in bounds for any genome
-            p[j] = base + j * stride < n ? __ldg(rowpred + (size_t(key[j]) * nkc + kc)) : 0.0;
-            h[j] = (ids && base + j * stride < n) ? __ldg(khk + (size_t(key[j]) * ndk + x.k)) : 0ull;
+            uint32_t src = uint32_t(j);
+#pragma unroll
+            for (int q = j - 1; q >= 0; --q)
+                if (!nodedup && g[q] == g[j]) src = uint32_t(q);
+            dsrc |= src << (3 * j);
+            const bool own = src == uint32_t(j) && base + j * stride < n;
+            p[j] = own ? __ldg(rowpred + (size_t(key[j]) * nkc + kc)) : 0.0;
+            h[j] = (ids && own) ? __ldg(khk + (size_t(key[j]) * ndk + x.k)) : 0ull;
         }
 #pragma unroll
         for (int j = 0; j < kRowsPer; ++j) {
             const int64_t i = base + j * stride;
             if (i >= n) break;
+            const uint32_t src = (dsrc >> (3 * j)) & 7u;
+#pragma unroll
+            for (int q = 0; q < j; ++q)
+                if (src == uint32_t(q)) {
+                    p[j] = p[q];
+                    h[j] = h[q];
+                }
             pred[i] = p[j];  // plain store: stays in L2 for the selection filter that re-reads it
             if (sel.hist) atomicAdd(&shist[sel_bin(p[j], sel)], 1u);
             if (ids) {
@@ -1720,8 +1736,10 @@ cudaError_t launch_score_rows(const LaunchCtx& c, const uint8_t* d_plan, int ndk
     const int64_t want = (n + int64_t(kRowsT) * kRowsPer - 1) / (int64_t(kRowsT) * kRowsPer);
     const int64_t cap = int64_t(c.sm_count) * per_sm;
     const int grid = int(want < cap ? want : cap);
+    const char* nd = std::getenv("ETUNE_ROWS_NODEDUP");  // diagnostic, read every call
+    const int nodedup = nd && nd[0] == '1' ? 1 : 0;
     e = launch_pdl(score_rows_kernel, dim3(grid), dim3(kRowsT), sm, c.stream, d_plan, d_clskuv, d_meta, d_rowpred,
-                   d_khash, d_genome, n, d_pred, d_ids, sel);
+                   d_khash, d_genome, n, d_pred, d_ids, sel, nodedup);
     note_launches(1);
     return e;
 }
