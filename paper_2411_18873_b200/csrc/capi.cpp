@@ -213,41 +213,73 @@ int host_threads() {
     return n;
 }
 
-// Packs m rows into pinned `dst` with the narrowest field width that holds them (2, 4 or
-// 8 bytes), split over the host pool.  Returns the field width.
-// extra_tasks / extra (optional): more pool tasks run in the same dispatch as the narrowing (the
-// previous chunks' outputs copied out of staging), exactly once
-int pack_rows(etune_cu_ctx* c, const etune_schedule* src, int64_t m, void* dst, int extra_tasks = 0,
-              const std::function<void(int)>* extra = nullptr) {
-    const int tasks = std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m / 2048));
-    auto range = [&](int t, int64_t* a, int64_t* b) {  // even row boundaries: 24 fields = 3 AVX-512 words
+// Packs m rows into pinned `dst` with the narrowest field width that holds them (2, 4 or 8 bytes),
+// split over the host pool.  start() hands the u16 pass to the workers and returns (the caller issues
+// CUDA work meanwhile); finish() joins it, runs the wider fallbacks if a field did not fit, and returns
+// the field width.  `extra` (optional): more pool tasks in the same dispatch (a previous chunk's
+// outputs copied out of staging), run exactly once.  A job must not move while it runs.
+struct PackJob {
+    etune_cu_ctx* c = nullptr;
+    const etune_schedule* src = nullptr;
+    int64_t m = 0;
+    void* dst = nullptr;
+    int tasks = 0, extra_tasks = 0;
+    bool simd = false;
+    bool active = false;
+    std::vector<char> ok;
+    std::function<void(int)> extra, fn;
+
+    PackJob() = default;
+    PackJob(const PackJob&) = delete;
+    PackJob& operator=(const PackJob&) = delete;
+    ~PackJob() {  // an early return while the workers still run this job: wait for them
+        if (active) c->pool->join();
+    }
+
+    void range(int t, int64_t* a, int64_t* b) const {  // even row boundaries: 24 fields = 3 AVX-512 words
         *a = (m * t / tasks) & ~int64_t(1);
         *b = t + 1 == tasks ? m : (m * (t + 1) / tasks) & ~int64_t(1);
-    };
-    std::vector<char> ok(size_t(tasks), 1);
-    const bool simd = have_avx512() && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
-    c->pool->run(tasks + (extra ? extra_tasks : 0), [&](int t) {
-        if (t >= tasks) return (*extra)(t - tasks);
-        int64_t a, b;
-        range(t, &a, &b);
-        ok[size_t(t)] = simd ? narrow_u16_avx512(reinterpret_cast<const int64_t*>(src), static_cast<uint16_t*>(dst),
-                                                 12 * a, 12 * b)
-                             : narrow_rows(src, static_cast<uint16_t*>(dst), a, b);
-    });
-    if (std::all_of(ok.begin(), ok.end(), [](char x) { return x != 0; })) return 2;
-    c->pool->run(tasks, [&](int t) {
-        int64_t a, b;
-        range(t, &a, &b);
-        ok[size_t(t)] = narrow_rows(src, static_cast<uint32_t*>(dst), a, b);
-    });
-    if (std::all_of(ok.begin(), ok.end(), [](char x) { return x != 0; })) return 4;
-    c->pool->run(tasks, [&](int t) {
-        int64_t a, b;
-        range(t, &a, &b);
-        std::memcpy(static_cast<etune_schedule*>(dst) + a, src + a, size_t(b - a) * sizeof(etune_schedule));
-    });
-    return 8;
-}
+    }
+    void start(etune_cu_ctx* c_, const etune_schedule* s, int64_t m_, void* d, int xt, std::function<void(int)> xf) {
+        c = c_;
+        src = s;
+        m = m_;
+        dst = d;
+        tasks = int(std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m / 2048)));
+        extra_tasks = xt;
+        extra = std::move(xf);
+        ok.assign(size_t(tasks), 1);
+        simd = have_avx512() && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+        fn = [this](int t) {
+            if (t >= tasks) return extra(t - tasks);
+            int64_t a, b;
+            range(t, &a, &b);
+            ok[size_t(t)] = simd ? narrow_u16_avx512(reinterpret_cast<const int64_t*>(src), static_cast<uint16_t*>(dst),
+                                                     12 * a, 12 * b)
+                                 : narrow_rows(src, static_cast<uint16_t*>(dst), a, b);
+        };
+        c->pool->start(tasks + (extra ? extra_tasks : 0), fn);
+        active = true;
+    }
+    int finish() {
+        c->pool->join();
+        active = false;
+        auto all_ok = [&] { return std::all_of(ok.begin(), ok.end(), [](char x) { return x != 0; }); };
+        if (all_ok()) return 2;
+        c->pool->run(tasks, [&](int t) {
+            int64_t a, b;
+            range(t, &a, &b);
+            ok[size_t(t)] = narrow_rows(src, static_cast<uint32_t*>(dst), a, b);
+        });
+        if (all_ok()) return 4;
+        c->pool->run(tasks, [&](int t) {
+            int64_t a, b;
+            range(t, &a, &b);
+            std::memcpy(static_cast<etune_schedule*>(dst) + a, src + a, size_t(b - a) * sizeof(etune_schedule));
+        });
+        return 8;
+    }
+};
 
 etune_status ensure_io(etune_cu_ctx* c, size_t bytes) {
     if (c->io_bytes >= bytes) return ETUNE_OK;
@@ -1548,73 +1580,93 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         c->hout_bytes = 2 * size_t(cap) * 16;
     }
     int64_t pend_lo[2] = {-1, -1}, pend_m[2] = {0, 0};  // staged chunk waiting in hout buffer b
-    auto out_tasks = [&](int b) {
-        return int(std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, pend_m[b] / 4096)));
+    auto out_tasks = [&](int64_t m2) {
+        return int(std::min<int64_t>(int64_t(c->pool->size()) * 2, std::max<int64_t>(1, m2 / 4096)));
     };
-    auto out_copy = [&](int b, int t, int tasks) {  // part t of staging buffer b's outputs to the caller's arrays
+    // part t of staging buffer b's outputs (rows [lo2, lo2 + m2) of the call) to the caller's arrays
+    auto out_copy = [=](int b, int64_t lo2, int64_t m2, int t, int tasks) {
         const double* sp = reinterpret_cast<const double*>(static_cast<char*>(c->hout) + size_t(b) * size_t(cap) * 16);
         const uint64_t* si = reinterpret_cast<const uint64_t*>(sp + cap);
-        const int64_t lo2 = pend_lo[b], m2 = pend_m[b];
         const int64_t a = m2 * t / tasks, e = m2 * (t + 1) / tasks;
         if (h_pred) std::memcpy(h_pred + lo2 + a, sp + a, size_t(e - a) * 8);
         if (h_ids) std::memcpy(h_ids + lo2 + a, si + a, size_t(e - a) * 8);
     };
-    auto drain = [&](int b) -> etune_status {
+    auto drain = [&](int b) -> etune_status {  // (the pool must be idle)
         if (pend_lo[b] < 0) return ETUNE_OK;
         CU(cudaEventSynchronize(c->ev_out[b]));
-        const int tasks = out_tasks(b);
-        c->pool->run(tasks, [&](int t) { out_copy(b, t, tasks); });
+        const int64_t lo2 = pend_lo[b], m2 = pend_m[b];
+        const int tasks = out_tasks(m2);
+        c->pool->run(tasks, [&](int t) { out_copy(b, lo2, m2, t, tasks); });
         pend_lo[b] = -1;
         return ETUNE_OK;
     };
     // chunk sizes: full chunks, then the last full chunk split so that the final one is a quarter chunk
     // (the tail after the last narrowing -- its copy in, scoring, copy out -- shrinks with it)
-    auto chunk_at = [&](int64_t rem) -> int64_t {
-        const int64_t q = chunk / 4;
-        if (rem <= q) return rem;
-        if (rem <= chunk + q) return rem - q;
-        return chunk;
-    };
+    std::vector<std::pair<int64_t, int64_t>> chunks;  // (first row, rows)
+    for (int64_t lo = 0, m = 0; lo < n; lo += m) {
+        const int64_t rem = n - lo, q = chunk / 4;
+        m = rem <= q ? rem : rem <= chunk + q ? rem - q : chunk;
+        chunks.emplace_back(lo, m);
+    }
+    const int nch = int(chunks.size());
+    auto is_raw = [&](int i) { return pinned && raw_every > 0 && i % raw_every == 0 && chunks[size_t(i)].second == chunk; };
     // the caller's earlier work on the ctx stream happens-before this call's copies
     CU(cudaEventRecord(c->ev_done[0], c->stream));
     CU(cudaStreamWaitEvent(c->h2d, c->ev_done[0], 0));
     CU(cudaStreamWaitEvent(c->d2h, c->ev_done[0], 0));
-    // ETUNE_E2E_TRACE=1 (diagnostic): host time spent narrowing rows and waiting for staging, per call
+    // ETUNE_E2E_TRACE=1 (diagnostic): host time spent joining the narrowing and waiting for staging, per call
     static const bool e2e_trace = std::getenv("ETUNE_E2E_TRACE") != nullptr;
     double e2e_pack_us = 0.0, e2e_wait_us = 0.0;
     const auto e2e_t0 = std::chrono::steady_clock::now();
     char* io = static_cast<char*>(c->io);
     char* pin = static_cast<char*>(c->hpin);
-    for (int64_t lo = 0, i = 0, m = 0; lo < n; lo += m, ++i) {
-        m = chunk_at(n - lo);
-        const int b = int(i & 1);
+    PackJob jobs[2];
+    // Chunk i's narrowing starts on the pool workers before chunk i-1's CUDA work is issued by this
+    // thread (which then joins it), so the launches and copies of one chunk overlap the next one's
+    // narrowing.  Its staging buffer i & 1 was read by chunk i-2's H2D; chunk i-2's outputs, still in
+    // output staging buffer i & 1, leave it in the same dispatch when their D2H has landed.
+    auto begin = [&](int i) -> etune_status {
+        if (is_raw(i)) return ETUNE_OK;
+        const int b = i & 1;
+        const auto tw0 = std::chrono::steady_clock::now();
+        if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));
+        if (e2e_trace) e2e_wait_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw0).count();
+        int xt = 0;
+        std::function<void(int)> xf;
+        if (stage_out && pend_lo[b] >= 0 && cudaEventQuery(c->ev_out[b]) == cudaSuccess) {
+            const int64_t lo2 = pend_lo[b], m2 = pend_m[b];
+            xt = out_tasks(m2);
+            xf = [out_copy, b, lo2, m2, xt](int t) { out_copy(b, lo2, m2, t, xt); };
+            pend_lo[b] = -1;
+        }
+        jobs[b].start(c, h_sched + chunks[size_t(i)].first, chunks[size_t(i)].second,
+                      pin + size_t(b) * size_t(cap) * sizeof(etune_schedule), xt, std::move(xf));
+        return ETUNE_OK;
+    };
+    if (etune_status st = begin(0)) return st;
+    for (int i = 0; i < nch; ++i) {
+        const int64_t lo = chunks[size_t(i)].first, m = chunks[size_t(i)].second;
+        const int b = i & 1;
         char* base = io + size_t(b) * size_t(cap) * per;
         void* d_rows = base;
         auto* d_gen = reinterpret_cast<uint64_t*>(base + size_t(cap) * sizeof(etune_schedule));
         auto* d_pred = d_all ? d_all + lo : reinterpret_cast<double*>(base + size_t(cap) * (sizeof(etune_schedule) + 8));
         auto* d_ids = reinterpret_cast<uint64_t*>(base + size_t(cap) * (sizeof(etune_schedule) + 16));
         void* h_rows = pin + size_t(b) * size_t(cap) * sizeof(etune_schedule);
-        const bool raw = pinned && raw_every > 0 && i % raw_every == 0 && m == chunk;  // full chunks only
+        const bool raw = is_raw(i);
         int fb = 8;
         if (!raw) {
-            const auto tw0 = std::chrono::steady_clock::now();
-            if (i >= 2) CU(cudaEventSynchronize(c->ev_in[b]));  // pinned buffer b read by chunk i-2's H2D
             const auto tw1 = std::chrono::steady_clock::now();
-            // chunk i-2's outputs leave staging buffer b in the same pool dispatch when their D2H has
-            // landed (else after this chunk's launches, below)
-            int xt = 0;
-            std::function<void(int)> xf;
-            if (stage_out && pend_lo[b] >= 0 && cudaEventQuery(c->ev_out[b]) == cudaSuccess) {
-                xt = out_tasks(b);
-                xf = [&out_copy, b, xt](int t) { out_copy(b, t, xt); };
-            }
-            fb = pack_rows(c, h_sched + lo, m, h_rows, xt, xt ? &xf : nullptr);
-            if (xt) pend_lo[b] = -1;
-            if (e2e_trace) {
-                e2e_wait_us += std::chrono::duration<double, std::micro>(tw1 - tw0).count();
+            fb = jobs[b].finish();
+            if (e2e_trace)
                 e2e_pack_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - tw1).count();
-            }
         }
+        // chunk i-2's outputs still in output staging buffer b (not copied out with a narrowing): now,
+        // while the pool is idle
+        if (stage_out)
+            if (etune_status st = drain(b)) return st;
+        if (i + 1 < nch)
+            if (etune_status st = begin(i + 1)) return st;
         if (i >= 2) CU(cudaStreamWaitEvent(c->h2d, c->ev_out[b], 0));  // buffer b drained by chunk i-2's D2H
         CU(cudaMemcpyAsync(d_rows, raw ? static_cast<const void*>(h_sched + lo) : h_rows,
                            size_t(m) * 12 * size_t(fb), cudaMemcpyHostToDevice, c->h2d));
@@ -1626,7 +1678,6 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
         CU(cudaEventRecord(c->ev_done[b], c->stream));
         CU(cudaStreamWaitEvent(c->d2h, c->ev_done[b], 0));
         if (stage_out) {
-            if (etune_status st = drain(b)) return st;  // chunk i-2's outputs out of staging buffer b
             double* sp = reinterpret_cast<double*>(static_cast<char*>(c->hout) + size_t(b) * size_t(cap) * 16);
             if (h_pred) CU(cudaMemcpyAsync(sp, d_pred, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
             if (h_ids) CU(cudaMemcpyAsync(sp + cap, d_ids, size_t(m) * 8, cudaMemcpyDeviceToHost, c->d2h));
@@ -1655,7 +1706,7 @@ etune_status host_pipeline(etune_cu_ctx* c, const etune_cu_plan* p, etune_cu_for
     CU(cudaStreamWaitEvent(c->stream, c->ev_out[0], 0));
     const etune_status fin = etune_cu_synchronize(c, first_bad);
     if (e2e_trace)
-        std::fprintf(stderr, "e2e n=%lld: total %.0f us, narrowing %.0f us, staging waits %.0f us, pool %d threads\n",
+        std::fprintf(stderr, "e2e n=%lld: total %.0f us, narrowing joins %.0f us, staging waits %.0f us, pool %d threads\n",
                      (long long)n,
                      std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - e2e_t0).count(),
                      e2e_pack_us, e2e_wait_us, c->pool->size());

@@ -44,7 +44,17 @@ public:
     // fn(task) for task in [0, tasks), on the workers and the calling thread; returns
     // when every task has finished.  One run at a time (the ctx is single-threaded).
     void run(int tasks, const std::function<void(int)>& fn) {
-        if (tasks <= 0) return;
+        start(tasks, fn);
+        join();
+    }
+    // run() in two halves: the workers begin at once, the caller may do other work (CUDA launches)
+    // before it joins; fn must stay alive until join() returns.
+    void start(int tasks, const std::function<void(int)>& fn) {
+        if (tasks <= 0) {
+            fn_ = nullptr;
+            left_.store(0);
+            return;
+        }
         {
             std::lock_guard<std::mutex> g(mu_);
             fn_ = &fn;
@@ -54,7 +64,9 @@ public:
             gen_.fetch_add(1, std::memory_order_release);  // publishes fn_ / tasks_ to spinning workers
         }
         if (sleepers_.load() > 0) cv_.notify_all();
-        work();
+    }
+    void join() {
+        if (fn_) work();
         while (left_.load(std::memory_order_acquire) != 0) ETUNE_POOL_PAUSE();
         fn_ = nullptr;
     }
