@@ -1207,7 +1207,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
     double p[kSRPer];
     uint32_t gq[kSRPer];
     uint32_t rw[kSRPer];
-    uint32_t dsrc = 0u;
+    uint32_t dsrc = 0u, absent = 0u;  // absent: bit j set when candidate j does not exist
     const bool dedup = !(gmode & 16);
 #pragma unroll
     for (int j = 0; j < kSRPer; ++j) {
@@ -1219,6 +1219,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
         const uint32_t key = (x.t0 * nt1 + x.t1) * nt2 + x.t2;
         const uint32_t kc = min(uint32_t(scls[(x.k * 16u + x.u) * 4u + x.v]), nkc - 1u);
         rw[j] = v ? key * nkc + kc : 0xffffffffu;
+        absent |= v ? 0u : 1u << j;
         uint32_t src = uint32_t(j);
 #pragma unroll
         for (int q = j - 1; q >= 0; --q)
@@ -1270,7 +1271,7 @@ __global__ void __launch_bounds__(kSRT, 1) score_select_rows_kernel(
                     gq[j] = gq[q];
                 }
         }
-        if (sgen[j * kSRT + tid] == ~0ull) gq[j] = 0xffffffffu;  // no candidate
+        if ((absent >> j) & 1u) gq[j] = 0xffffffffu;  // no candidate
         sgg[j * kSRT + tid] = gq[j];
         gmin = min(gmin, gq[j]);
         if (gq[j] == 0xffffffffu) continue;
